@@ -1,0 +1,197 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes wrapper around the plain C++ oracle (oracle/sz3_oracle.cpp).
+
+The oracle is the single-threaded CPU definition of SZ3's block-regression predictor with
+linear-scaling quantisation (Lemma 1, prediction P:156, quantiser P:406-409,
+App. A loop P:980-992, value-range eb P:833).  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this package.  It shares
+no code with ``paper_2111_02925_b200`` and never imports it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sz3_oracle.cpp")
+_LIB_PATH = os.path.join(_HERE, "liboracle_sz3.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, EINVAL, EUNSUPPORTED, ERANGE, EBADRANGE, EOVERFLOW = 0, -1, -2, -3, -5, -6
+BLOCK = 6
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with g++ (-O2, no FP contraction)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+               "-o", tmp, _SRC]
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "elem_near_ties", "elem_div_mismatch", "coef_near_ties", "coef_tie_blocks",
+        "radius_outliers", "verify_outliers", "nonfinite_outliers", "zero_predictor_blocks")]
+
+    def as_dict(self) -> dict:
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            P, U64, U32, I32, D = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_double
+            lib.orc_value_range.argtypes = [I32, U64, P, P]
+            lib.orc_compress.argtypes = [I32, P, U64, U32, U32, I32, D, P, P, P, P, P, P, P, P, U64, P, P, P, P, P]
+            lib.orc_decompress.argtypes = [I32, P, U64, U32, U32, D, P, P, P, P, U64, P]
+            lib.orc_block_beta.argtypes = [P, I32, I32, I32, P, P]
+            lib.orc_block_beta.restype = None
+            lib.orc_coef_codes.argtypes = [P, D, U32, P, P]
+            lib.orc_predict.argtypes = [P, I32, I32, I32]
+            lib.orc_predict.restype = D
+            lib.orc_quantize_element.argtypes = [I32, D, D, D, U32, P, P]
+            lib.orc_num_blocks.argtypes = [P, U32]
+            lib.orc_num_blocks.restype = U64
+            _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dtype_id(dt) -> int:
+    dt = np.dtype(dt)
+    if dt == np.float32:
+        return 0
+    if dt == np.float64:
+        return 1
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+def num_blocks(dims, B: int = BLOCK) -> int:
+    d = np.ascontiguousarray(dims, dtype=np.uint64)
+    return int(_load().orc_num_blocks(_ptr(d), B))
+
+
+def value_range(x: np.ndarray) -> tuple[float, float]:
+    x = np.ascontiguousarray(x)
+    out = np.zeros(2, np.float64)
+    rc = _load().orc_value_range(_dtype_id(x.dtype), x.size, _ptr(x), _ptr(out))
+    if rc != OK:
+        raise ValueError(f"orc_value_range rc={rc}")
+    return float(out[0]), float(out[1])
+
+
+@dataclass
+class Compressed:
+    dims: tuple
+    dtype: np.dtype
+    radius: int
+    eb_abs: float
+    codes: np.ndarray          # uint16, same shape as the field
+    coef_codes: np.ndarray     # int32 [NB, 4]
+    coef_raw: np.ndarray       # float64 [NB, 4]  unquantised beta
+    block_exempt: np.ndarray   # uint8 [NB] coefficient near-tie blocks
+    outlier_idx: np.ndarray    # uint64 global linear index, emission order (block-major)
+    outlier_val: np.ndarray    # T
+    hist: np.ndarray           # int64 [2R]
+    counters: dict = field(default_factory=dict)
+    dim0_offset: int = 0
+    xprime: np.ndarray | None = None   # compress-time reconstruction (T), same shape as the field
+
+
+def compress(x: np.ndarray, eb: float, eb_mode: str = "rel", radius: int = 32768,
+             dim0_offset: int = 0, value_range_override: tuple | None = None,
+             B: int = BLOCK) -> Compressed:
+    """Oracle O1-O11 over a 3D field (1D/2D are embedded with leading extents 1, DESIGN G18)."""
+    x = np.ascontiguousarray(x)
+    shape = (1,) * (3 - x.ndim) + tuple(x.shape)
+    dims = np.array(shape, np.uint64)
+    N = int(np.prod(shape))
+    nb = num_blocks(dims, B)
+    codes = np.empty(shape, np.uint16)
+    coef = np.empty((nb, 4), np.int32)
+    coef_raw = np.empty((nb, 4), np.float64)
+    exempt = np.empty(nb, np.uint8)
+    cap = N
+    oidx = np.empty(cap, np.uint64)
+    oval = np.empty(cap, x.dtype)
+    nout = np.zeros(1, np.uint64)
+    hist = np.empty(2 * radius, np.int64)
+    eb_abs = np.zeros(1, np.float64)
+    xprime = np.empty(shape, x.dtype)
+    cnt = Counters()
+    rng = None if value_range_override is None else np.array(value_range_override, np.float64)
+    mode = {"abs": 0, "rel": 1}[eb_mode]
+    rc = _load().orc_compress(_dtype_id(x.dtype), _ptr(dims), dim0_offset, B, radius, mode, float(eb),
+                              _ptr(rng), _ptr(x), _ptr(codes), _ptr(coef), _ptr(coef_raw), _ptr(exempt),
+                              _ptr(oidx), _ptr(oval), cap, _ptr(nout), _ptr(hist), _ptr(eb_abs),
+                              ctypes.byref(cnt), _ptr(xprime))
+    if rc != OK:
+        raise ValueError(f"orc_compress rc={rc}")
+    n = int(nout[0])
+    return Compressed(tuple(int(s) for s in shape), x.dtype, radius, float(eb_abs[0]), codes, coef, coef_raw,
+                      exempt, oidx[:n].copy(), oval[:n].copy(), hist, cnt.as_dict(), dim0_offset, xprime)
+
+
+def decompress(c: Compressed | None = None, *, dims=None, dtype=None, radius=None, eb_abs=None, codes=None,
+               coef_codes=None, outlier_idx=None, outlier_val=None, dim0_offset=0, B: int = BLOCK) -> np.ndarray:
+    if c is not None:
+        dims, dtype, radius, eb_abs = c.dims, c.dtype, c.radius, c.eb_abs
+        codes, coef_codes, outlier_idx, outlier_val, dim0_offset = (
+            c.codes, c.coef_codes, c.outlier_idx, c.outlier_val, c.dim0_offset)
+    d = np.array(dims, np.uint64)
+    out = np.empty(tuple(int(s) for s in dims), dtype)
+    codes = np.ascontiguousarray(codes, np.uint16)
+    coef_codes = np.ascontiguousarray(coef_codes, np.int32)
+    oidx = np.ascontiguousarray(outlier_idx, np.uint64)
+    oval = np.ascontiguousarray(outlier_val, dtype)
+    rc = _load().orc_decompress(_dtype_id(dtype), _ptr(d), dim0_offset, B, radius, float(eb_abs), _ptr(codes),
+                                _ptr(coef_codes), _ptr(oidx), _ptr(oval), oidx.size, _ptr(out))
+    if rc != OK:
+        raise ValueError(f"orc_decompress rc={rc}")
+    return out
+
+
+def block_beta(f: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """O4 + O5 on one dense block; returns (V0,Vx,Vy,Vz), (b0,b1,b2,b3)."""
+    f = np.ascontiguousarray(f, np.float64)
+    assert f.ndim == 3
+    V = np.zeros(4)
+    beta = np.zeros(4)
+    _load().orc_block_beta(_ptr(f), f.shape[0], f.shape[1], f.shape[2], _ptr(V), _ptr(beta))
+    return V, beta
+
+
+def coef_codes(beta, eb_abs: float, B: int = BLOCK):
+    b = np.ascontiguousarray(beta, np.float64)
+    c = np.zeros(4, np.int32)
+    bh = np.zeros(4)
+    zero = _load().orc_coef_codes(_ptr(b), float(eb_abs), B, _ptr(c), _ptr(bh))
+    return c, bh, bool(zero)
+
+
+def predict(bhat, i: int, j: int, k: int) -> float:
+    b = np.ascontiguousarray(bhat, np.float64)
+    return float(_load().orc_predict(_ptr(b), i, j, k))
+
+
+def quantize_element(x: float, p: float, eb_abs: float, radius: int = 32768, dtype=np.float64):
+    """O8-O10 for one element; returns (code, x', kind) with kind 0 ok / 1 radius / 2 verify / 3 non-finite."""
+    code = ctypes.c_uint16(0)
+    xp = ctypes.c_double(0)
+    kind = _load().orc_quantize_element(_dtype_id(dtype), float(x), float(p), float(eb_abs), radius,
+                                        ctypes.byref(code), ctypes.byref(xp))
+    return int(code.value), float(xp.value), int(kind)

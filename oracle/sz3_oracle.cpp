@@ -1,0 +1,445 @@
+// =====================================================================================
+//  oracle/sz3_oracle.cpp -- TEST INFRASTRUCTURE ONLY (not part of the product path).
+//
+//  A plain, slow, single-threaded CPU definition of SZ3's block-wise linear-regression
+//  predictor with linear-scaling quantisation, written from PAPER.md (arxiv 2111.02925):
+//    * Lemma 1 / Eq. (thm1sol)  P:46-67   closed-form regression coefficients
+//    * "Prediction"             P:156     f^(r)_ijk = b0 + i b1 + j b2 + k b3, residual,
+//                                         linear-scaling quantisation
+//    * Quantizer instances      P:406-409 equal bins of width 2*eb, out-of-range residuals
+//                                         are "unpredictable" and stored separately
+//    * quantize / recover       P:400-404, App. A
+//    * block-then-element loop  App. A, Alg. 1
+//    * value-range-relative eb
+//  Readings of silent / garbled passages (coefficient bins, tie rule, verify step, ...) are the
+//  ones listed in DESIGN.md section "Readings" (G1..G18) and in oracle/DEFINITION.md.
+//
+//  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+//  load this library. It shares no code, header, table or constant with
+//  paper_2111_02925_b200/ (the CUDA path), and neither side includes the other.
+//
+//  Build: g++ -O2 -std=c++17 -ffp-contract=off -fno-fast-math -shared -fPIC
+//  (-ffp-contract=off: no multiply-add contraction except where std::fma is written out.)
+// =====================================================================================
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+
+extern "C" {
+
+// Status codes (same meaning as include/sz3g.h, restated here on purpose: no shared header).
+enum { ORC_OK = 0, ORC_EINVAL = -1, ORC_EUNSUPPORTED = -2, ORC_ERANGE = -3, ORC_EBADRANGE = -5,
+       ORC_EOVERFLOW = -6 };
+
+// Counters reported next to the outputs (SURVEY 8(c) "Reported counters").
+struct orc_counters {
+  uint64_t elem_near_ties;      // (i)  frac((x-p)/(2eb)) within 1e-9 of 1/2 (true division)
+  uint64_t elem_div_mismatch;   // (ii) rint((x-p)/(2eb)) != rint((x-p)*fl(1/(2eb)))
+  uint64_t coef_near_ties;      // (iii) coefficients whose beta/w lies in the tie window
+  uint64_t coef_tie_blocks;     //       blocks holding at least one such coefficient
+  uint64_t radius_outliers;     // |t| >= R or |rint(t)| >= R (finite t)
+  uint64_t verify_outliers;     // failed the O9 verify step
+  uint64_t nonfinite_outliers;  // t not finite (NaN / Inf input)
+  uint64_t zero_predictor_blocks; // O6 fallback: non-finite or int32-overflowing coefficient
+};
+
+}  // extern "C"
+
+namespace {
+
+// ---------------------------------------------------------------- element type helpers
+template <typename T> struct dtype_of;
+template <> struct dtype_of<float> { static constexpr int id = 0; };
+template <> struct dtype_of<double> { static constexpr int id = 1; };
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- O1 / O2: error bound
+// O1: ABS -> eb_abs = eb; REL (value range) -> eb_abs = eb * (hi - lo).
+// O2: twoeb = 2 eb_abs, inv2eb = 1/twoeb, w0 = eb_abs/2, ws = eb_abs/(2B)  (DESIGN G1, G5).
+struct Bounds {
+  double eb_abs, twoeb, inv2eb, w0, ws;
+};
+
+inline bool make_bounds(int eb_mode, double eb, double lo, double hi, uint32_t B, Bounds* out) {
+  double eb_abs;
+  if (eb_mode == 0) {
+    eb_abs = eb;
+  } else {
+    double range = hi - lo;
+    eb_abs = eb * range;
+  }
+  if (!std::isfinite(eb_abs) || !(eb_abs > 0.0)) return false;
+  out->eb_abs = eb_abs;
+  out->twoeb = 2.0 * eb_abs;
+  out->inv2eb = 1.0 / out->twoeb;
+  out->w0 = eb_abs / 2.0;
+  out->ws = eb_abs / (2.0 * (double)B);
+  return true;
+}
+
+// ---------------------------------------------------------------- O4: block moments
+// V0 = sum f, Vx = sum i f, Vy = sum j f, Vz = sum k f  (Lemma 1), sequential loops
+// i -> j -> k with k fastest, f = (double) x.
+template <typename T>
+void block_moments(const T* x, uint64_t n1, uint64_t n2, uint64_t i0, uint64_t j0, uint64_t k0,
+                   int m0, int m1, int m2, double V[4]) {
+  double V0 = 0.0, Vx = 0.0, Vy = 0.0, Vz = 0.0;
+  for (int i = 0; i < m0; i++)
+    for (int j = 0; j < m1; j++)
+      for (int k = 0; k < m2; k++) {
+        double f = (double)x[((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k)];
+        V0 += f;
+        Vx += (double)i * f;
+        Vy += (double)j * f;
+        Vz += (double)k * f;
+      }
+  V[0] = V0; V[1] = Vx; V[2] = Vy; V[3] = Vz;
+}
+
+// ---------------------------------------------------------------- O5: Lemma 1
+// beta_d = 6 / (n1 n2 n3 (n_d + 1)) * (2 V_d / (n_d - 1) - V0)
+// beta_0 = V0 / (n1 n2 n3) - ((n1-1)/2 b1 + (n2-1)/2 b2 + (n3-1)/2 b3)
+// Extent-1 axis: slope 0 (DESIGN G2; the Lemma divides by n_d - 1).
+void lemma_beta(const double V[4], int m0, int m1, int m2, double beta[4]) {
+  const int m[3] = {m0, m1, m2};
+  const double Nb = (double)m0 * (double)m1 * (double)m2;
+  for (int d = 0; d < 3; d++) {
+    if (m[d] > 1) {
+      double scale = 6.0 / (Nb * (double)(m[d] + 1));
+      double inner = 2.0 * V[d + 1] / (double)(m[d] - 1) - V[0];
+      beta[d + 1] = scale * inner;
+    } else {
+      beta[d + 1] = 0.0;
+    }
+  }
+  beta[0] = V[0] / Nb - ((double)(m0 - 1) / 2.0 * beta[1] + (double)(m1 - 1) / 2.0 * beta[2] +
+                         (double)(m2 - 1) / 2.0 * beta[3]);
+}
+
+// ---------------------------------------------------------------- O6: coefficient codes
+// Independent per-block linear quantisation (DESIGN G1): c0 = rint(b0/w0), c_d = rint(b_d/ws),
+// ties to even; non-finite or |c| > 2^31-1 -> all four codes 0 ("zero predictor").
+// Returns true if the zero predictor was used.
+bool coef_codes(const double beta[4], const Bounds& bd, int32_t c[4], double bhat[4]) {
+  double r[4];
+  bool bad = false;
+  for (int d = 0; d < 4; d++) {
+    double w = (d == 0) ? bd.w0 : bd.ws;
+    r[d] = std::nearbyint(beta[d] / w);
+    if (!std::isfinite(r[d]) || std::fabs(r[d]) > 2147483647.0) bad = true;
+  }
+  for (int d = 0; d < 4; d++) c[d] = bad ? 0 : (int32_t)r[d];
+  bhat[0] = (double)c[0] * bd.w0;
+  for (int d = 1; d < 4; d++) bhat[d] = (double)c[d] * bd.ws;
+  return bad;
+}
+
+// ---------------------------------------------------------------- O7: prediction
+// p = b0 + i b1 + j b2 + k b3 evaluated as fma(b1, i, fma(b2, j, fma(b3, k, b0)))
+// (DESIGN G12: fixed order, explicit fused multiply-adds).
+inline double predict(const double bh[4], int i, int j, int k) {
+  return std::fma(bh[1], (double)i, std::fma(bh[2], (double)j, std::fma(bh[3], (double)k, bh[0])));
+}
+
+// ---------------------------------------------------------------- O8-O10: one element
+// t = (x - p) * inv2eb; outlier if !(|t| < R); q = rint(t); outlier if |q| >= R;
+// x' = (T)(p + twoeb*q) (mul then add, no FMA); outlier if |x' - x| > eb_abs; code = R + q.
+// kind: 0 predictable, 1 radius, 2 verify, 3 non-finite.
+template <typename T>
+inline int quantize_element(T xv, double p, const Bounds& bd, uint32_t R, uint16_t* code,
+                            T* xprime) {
+  const double xd = (double)xv;
+  const double t = (xd - p) * bd.inv2eb;
+  if (!(std::fabs(t) < (double)R)) {
+    *code = 0; *xprime = xv;
+    return std::isfinite(t) ? 1 : 3;
+  }
+  const double q = std::nearbyint(t);
+  if (std::fabs(q) >= (double)R) {
+    *code = 0; *xprime = xv;
+    return 1;
+  }
+  const double prod = bd.twoeb * q;
+  const double y = p + prod;
+  const T xp = (T)y;
+  if (std::fabs((double)xp - xd) > bd.eb_abs) {
+    *code = 0; *xprime = xv;
+    return 2;
+  }
+  *code = (uint16_t)((int64_t)R + (int64_t)q);
+  *xprime = xp;
+  return 0;
+}
+
+inline bool near_half(double u, double window) {
+  double fl = std::floor(u);
+  return std::fabs(u - fl - 0.5) <= window;
+}
+
+// ---------------------------------------------------------------- whole-field compression
+template <typename T>
+int compress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R,
+                  int eb_mode, double eb, const double* range, const T* x, uint16_t* codes,
+                  int32_t* coef, double* coef_raw, uint8_t* block_exempt, uint64_t* out_idx,
+                  T* out_val, uint64_t cap, uint64_t* n_out, int64_t* hist, double* eb_abs_out,
+                  orc_counters* cnt, T* xprime) {
+  const uint64_t n0 = dims[0], n1 = dims[1], n2 = dims[2];
+  const uint64_t N = n0 * n1 * n2;
+  double lo = 0.0, hi = 0.0;
+  if (eb_mode == 1) {
+    if (range) {
+      lo = range[0]; hi = range[1];
+    } else {
+      // a0 / O1: value range over the (local) field, as T widened to fp64.
+      lo = hi = (double)x[0];
+      for (uint64_t e = 0; e < N; e++) {
+        double v = (double)x[e];
+        if (std::isnan(v)) { lo = hi = v; break; }
+        if (v < lo) lo = v;
+        if (v > hi) hi = v;
+      }
+    }
+  }
+  Bounds bd;
+  if (!make_bounds(eb_mode, eb, lo, hi, B, &bd)) return ORC_EBADRANGE;
+  if (eb_abs_out) *eb_abs_out = bd.eb_abs;
+
+  orc_counters c{};
+  uint64_t nout = 0;
+  const uint64_t NB0 = ceil_div(n0, B), NB1 = ceil_div(n1, B), NB2 = ceil_div(n2, B);
+  if (hist) std::memset(hist, 0, sizeof(int64_t) * 2 * (size_t)R);
+
+  // O3: blocks in row-major block order; edge blocks clipped (DESIGN G3).
+  for (uint64_t a = 0; a < NB0; a++)
+    for (uint64_t b = 0; b < NB1; b++)
+      for (uint64_t cc = 0; cc < NB2; cc++) {
+        const uint64_t bid = (a * NB1 + b) * NB2 + cc;
+        const uint64_t i0 = a * B, j0 = b * B, k0 = cc * B;
+        const int m0 = (int)std::min<uint64_t>(B, n0 - i0);
+        const int m1 = (int)std::min<uint64_t>(B, n1 - j0);
+        const int m2 = (int)std::min<uint64_t>(B, n2 - k0);
+        double V[4], beta[4], bhat[4];
+        int32_t cd[4];
+        block_moments(x, n1, n2, i0, j0, k0, m0, m1, m2, V);
+        lemma_beta(V, m0, m1, m2, beta);
+        if (coef_codes(beta, bd, cd, bhat)) c.zero_predictor_blocks++;
+        for (int d = 0; d < 4; d++) {
+          coef[4 * bid + d] = cd[d];
+          if (coef_raw) coef_raw[4 * bid + d] = beta[d];
+        }
+        // (iii) coefficient tie window: the GPU may sum moments in another order, so its beta
+        // can differ by the parity tolerance 1e-12 * max(|beta|, mean|f|); a code can then
+        // differ only if beta/w lies within that distance (or 1e-9) of a half-integer.
+        double absum = 0.0;
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++)
+              absum += std::fabs((double)x[((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k)]);
+        const double scale = absum / ((double)m0 * m1 * m2);
+        bool tie_block = false;
+        for (int d = 0; d < 4; d++) {
+          const double w = (d == 0) ? bd.w0 : bd.ws;
+          const double u = beta[d] / w;
+          if (!std::isfinite(u)) continue;
+          const double win = std::max(1e-9, 1e-12 * std::max(std::fabs(beta[d]), scale) / w);
+          if (near_half(u, win)) { c.coef_near_ties++; tie_block = true; }
+        }
+        if (tie_block) c.coef_tie_blocks++;
+        if (block_exempt) block_exempt[bid] = tie_block ? 1 : 0;
+
+        // Alg. 1: for every element of the block, predict then quantize.
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++) {
+              const uint64_t e = ((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k);
+              const double p = predict(bhat, i, j, k);
+              // counters (i), (ii): pre-rounding residual / (2 eb) by true division
+              const double tdiv = ((double)x[e] - p) / bd.twoeb;
+              const double tmul = ((double)x[e] - p) * bd.inv2eb;
+              if (std::isfinite(tdiv) && std::fabs(tmul) < (double)R) {
+                if (near_half(tdiv, 1e-9)) c.elem_near_ties++;
+                if (std::nearbyint(tdiv) != std::nearbyint(tmul)) c.elem_div_mismatch++;
+              }
+              uint16_t code;
+              T xp;
+              const int kind = quantize_element<T>(x[e], p, bd, R, &code, &xp);
+              codes[e] = code;
+              if (xprime) xprime[e] = xp;
+              if (kind != 0) {
+                if (kind == 1) c.radius_outliers++;
+                else if (kind == 2) c.verify_outliers++;
+                else c.nonfinite_outliers++;
+                if (nout < cap) {
+                  out_idx[nout] = e + dim0_offset * n1 * n2;
+                  out_val[nout] = x[e];
+                }
+                nout++;
+              }
+              if (hist) hist[code]++;  // O11 (bin 0 counts outliers)
+            }
+      }
+  if (n_out) *n_out = nout;
+  if (cnt) *cnt = c;
+  return nout > cap ? ORC_EOVERFLOW : ORC_OK;
+}
+
+// ---------------------------------------------------------------- decompression
+// recover: recompute O6-O7 from the codes, x' = (T)(p + twoeb*(c - R)) for c != 0
+// (same ops as O9), x' = stored value for c == 0 ("stored separately").
+template <typename T>
+int decompress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R,
+                    double eb_abs, const uint16_t* codes, const int32_t* coef,
+                    const uint64_t* out_idx, const T* out_val, uint64_t n_out, T* xo) {
+  Bounds bd;
+  if (!make_bounds(0, eb_abs, 0, 0, B, &bd)) return ORC_EINVAL;
+  const uint64_t n0 = dims[0], n1 = dims[1], n2 = dims[2];
+  const uint64_t NB0 = ceil_div(n0, B), NB1 = ceil_div(n1, B), NB2 = ceil_div(n2, B);
+  for (uint64_t a = 0; a < NB0; a++)
+    for (uint64_t b = 0; b < NB1; b++)
+      for (uint64_t cc = 0; cc < NB2; cc++) {
+        const uint64_t bid = (a * NB1 + b) * NB2 + cc;
+        const uint64_t i0 = a * B, j0 = b * B, k0 = cc * B;
+        const int m0 = (int)std::min<uint64_t>(B, n0 - i0);
+        const int m1 = (int)std::min<uint64_t>(B, n1 - j0);
+        const int m2 = (int)std::min<uint64_t>(B, n2 - k0);
+        double bhat[4];
+        bhat[0] = (double)coef[4 * bid] * bd.w0;
+        for (int d = 1; d < 4; d++) bhat[d] = (double)coef[4 * bid + d] * bd.ws;
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++) {
+              const uint64_t e = ((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k);
+              const uint16_t code = codes[e];
+              if (code == 0) { xo[e] = (T)0; continue; }
+              const double p = predict(bhat, i, j, k);
+              const double q = (double)((int64_t)code - (int64_t)R);
+              const double prod = bd.twoeb * q;
+              const double y = p + prod;
+              xo[e] = (T)y;
+            }
+      }
+  const uint64_t base = dim0_offset * n1 * n2;
+  for (uint64_t m = 0; m < n_out; m++) {
+    const uint64_t e = out_idx[m] - base;
+    if (out_idx[m] < base || e >= n0 * n1 * n2) return ORC_EINVAL;
+    xo[e] = out_val[m];
+  }
+  return ORC_OK;
+}
+
+bool check_dims(const uint64_t* dims, uint32_t B, uint32_t R) {
+  if (!dims || dims[0] == 0 || dims[1] == 0 || dims[2] == 0) return false;
+  if (B < 1 || R < 1 || R > 32768) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+// a0: value range [lo, hi] of an n-element T array (NaN anywhere -> both NaN).
+int orc_value_range(int dtype, uint64_t n, const void* x, double out[2]) {
+  if (!x || n == 0) return ORC_EINVAL;
+  double lo, hi;
+  if (dtype == 0) {
+    const float* f = (const float*)x;
+    lo = hi = f[0];
+    for (uint64_t e = 0; e < n; e++) {
+      double v = f[e];
+      if (std::isnan(v)) { lo = hi = v; break; }
+      lo = std::min(lo, v); hi = std::max(hi, v);
+    }
+  } else if (dtype == 1) {
+    const double* f = (const double*)x;
+    lo = hi = f[0];
+    for (uint64_t e = 0; e < n; e++) {
+      double v = f[e];
+      if (std::isnan(v)) { lo = hi = v; break; }
+      lo = std::min(lo, v); hi = std::max(hi, v);
+    }
+  } else {
+    return ORC_EUNSUPPORTED;
+  }
+  out[0] = lo; out[1] = hi;
+  return ORC_OK;
+}
+
+int orc_compress(int dtype, const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R,
+                 int eb_mode, double eb, const double* range, const void* x, uint16_t* codes,
+                 int32_t* coef, double* coef_raw, uint8_t* block_exempt, uint64_t* out_idx,
+                 void* out_val, uint64_t cap, uint64_t* n_out, int64_t* hist, double* eb_abs_out,
+                 orc_counters* cnt, void* xprime /* nullable: compress-time x' (T) */) {
+  if (!check_dims(dims, B, R)) return (R < 1 || R > 32768) ? ORC_ERANGE : ORC_EINVAL;
+  if (!x || !codes || !coef || (cap > 0 && (!out_idx || !out_val))) return ORC_EINVAL;
+  if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != 0 && eb_mode != 1)) return ORC_EINVAL;
+  if (dtype == 0)
+    return compress_impl<float>(dims, dim0_offset, B, R, eb_mode, eb, range, (const float*)x,
+                                codes, coef, coef_raw, block_exempt, out_idx, (float*)out_val, cap,
+                                n_out, hist, eb_abs_out, cnt, (float*)xprime);
+  if (dtype == 1)
+    return compress_impl<double>(dims, dim0_offset, B, R, eb_mode, eb, range, (const double*)x,
+                                 codes, coef, coef_raw, block_exempt, out_idx, (double*)out_val,
+                                 cap, n_out, hist, eb_abs_out, cnt, (double*)xprime);
+  return ORC_EUNSUPPORTED;
+}
+
+int orc_decompress(int dtype, const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R,
+                   double eb_abs, const uint16_t* codes, const int32_t* coef,
+                   const uint64_t* out_idx, const void* out_val, uint64_t n_out, void* x_out) {
+  if (!check_dims(dims, B, R)) return (R < 1 || R > 32768) ? ORC_ERANGE : ORC_EINVAL;
+  if (!codes || !coef || !x_out || (n_out > 0 && (!out_idx || !out_val))) return ORC_EINVAL;
+  if (dtype == 0)
+    return decompress_impl<float>(dims, dim0_offset, B, R, eb_abs, codes, coef, out_idx,
+                                  (const float*)out_val, n_out, (float*)x_out);
+  if (dtype == 1)
+    return decompress_impl<double>(dims, dim0_offset, B, R, eb_abs, codes, coef, out_idx,
+                                   (const double*)out_val, n_out, (double*)x_out);
+  return ORC_EUNSUPPORTED;
+}
+
+// ----- block / element level entry points (used by the pins in tests/test_oracle_pins.py)
+
+// O4 + O5 on one dense m0 x m1 x m2 block of fp64 values (row-major, k fastest).
+void orc_block_beta(const double* f, int m0, int m1, int m2, double V_out[4], double beta[4]) {
+  double V[4];
+  block_moments<double>(f, (uint64_t)m1, (uint64_t)m2, 0, 0, 0, m0, m1, m2, V);
+  lemma_beta(V, m0, m1, m2, beta);
+  if (V_out) for (int d = 0; d < 4; d++) V_out[d] = V[d];
+}
+
+// O6 on given raw coefficients; returns 1 if the zero predictor was chosen.
+int orc_coef_codes(const double beta[4], double eb_abs, uint32_t B, int32_t c[4], double bhat[4]) {
+  Bounds bd;
+  if (!make_bounds(0, eb_abs, 0, 0, B, &bd)) return -1;
+  return coef_codes(beta, bd, c, bhat) ? 1 : 0;
+}
+
+// O7.
+double orc_predict(const double bhat[4], int i, int j, int k) { return predict(bhat, i, j, k); }
+
+// O8-O10 for one element of dtype (value passed widened to fp64; for f32 it must be an f32
+// value). Returns the outlier kind (0 predictable, 1 radius, 2 verify, 3 non-finite).
+int orc_quantize_element(int dtype, double x, double p, double eb_abs, uint32_t R, uint16_t* code,
+                         double* xprime) {
+  Bounds bd;
+  if (!make_bounds(0, eb_abs, 0, 0, 6, &bd)) return -1;
+  if (dtype == 0) {
+    float xp;
+    int k = quantize_element<float>((float)x, p, bd, R, code, &xp);
+    *xprime = xp;
+    return k;
+  }
+  double xp;
+  int k = quantize_element<double>(x, p, bd, R, code, &xp);
+  *xprime = xp;
+  return k;
+}
+
+uint64_t orc_num_blocks(const uint64_t dims[3], uint32_t B) {
+  return ceil_div(dims[0], B) * ceil_div(dims[1], B) * ceil_div(dims[2], B);
+}
+
+}  // extern "C"
