@@ -1,0 +1,134 @@
+/* =====================================================================================
+ * sz3g.h -- C ABI of the B200 (sm_100a) block-regression compressor hot path.
+ *
+ * Implements, on device, SZ3's block-wise linear-regression predictor with linear-scaling
+ * quantisation (arxiv 2111.02925, PAPER.md):
+ *   - Lemma 1 / Eq. (thm1sol) closed-form coefficients ............ P:46-67
+ *   - prediction f_ijk = b0 + i b1 + j b2 + k b3, residual,
+ *     linear-scaling quantisation ................................. P:156
+ *   - bins of width 2*eb, out-of-range residuals stored separately
+ *   - quantize / recover ........................................... P:400-404, App. A
+ *   - block-then-element iteration ................................. App. A
+ *   - error bound normalised to the value range .................... P:833
+ * The exact arithmetic (operation order, rounding, the readings of passages the paper leaves
+ * silent) is oracle/DEFINITION.md O1-O11 + D; DESIGN.md lists the readings G1-G18.
+ *
+ * Conventions for every call:
+ *   - Data pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless a parameter
+ *     says "host".  The caller owns every buffer; the library never allocates or frees device
+ *     memory and keeps no state between calls (re-entrant on different streams).
+ *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream) and returns
+ *     before it completes.  Host-side argument errors are returned synchronously (SZ3G_E*);
+ *     device-side conditions are written to a caller-provided device status word.
+ *   - Grids are row-major, contiguous, slowest dimension first: element (i,j,k) lives at
+ *     ((i*n1 + j)*n2 + k).  1D / 2D fields are passed as 3D with leading extents 1.
+ *   - Blocks are B x B x B (B = block_size = 6), edge blocks clipped (never padded); block id
+ *     (a*NB1 + b)*NB2 + c with NB_d = ceil(n_d / B).
+ * ===================================================================================== */
+#ifndef SZ3G_H
+#define SZ3G_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sz3g_stream_t; /* == cudaStream_t */
+
+/* ---- return codes (host side, synchronous) */
+#define SZ3G_OK            0
+#define SZ3G_EINVAL       (-1) /* null pointer, a zero extent, eb <= 0 or not finite, bad enum   */
+#define SZ3G_EUNSUPPORTED (-2) /* dtype / block_size / ndim not supported by the device path     */
+#define SZ3G_ERANGE       (-3) /* radius outside [1, 32768] (codes must fit uint16)             */
+#define SZ3G_ECUDA        (-4) /* a CUDA launch / driver call failed (see sz3g_last_cuda_error) */
+
+/* ---- device status bits (written with atomicOr into *d_status; caller zeroes it first) */
+#define SZ3G_STATUS_OUTLIER_OVERFLOW 0x1u /* *d_outlier_count > outlier_cap: retry, larger cap */
+#define SZ3G_STATUS_BAD_RANGE        0x2u /* eb_abs not finite or <= 0 (REL: max-min <= 0/NaN) */
+
+typedef enum { SZ3G_F32 = 0, SZ3G_F64 = 1 } sz3g_dtype;
+/* ABS: eb is absolute.  REL: eb_abs = eb * (max - min) over the (global) field. */
+typedef enum { SZ3G_EB_ABS = 0, SZ3G_EB_REL_RANGE = 1 } sz3g_eb_mode;
+
+/* flags for sz3g_params.flags */
+#define SZ3G_FLAG_FORCE_GENERIC 0x1u /* use the plain coalesced-load kernels even where the
+                                        TMA/mbarrier pipeline applies (parity testing)        */
+
+typedef struct {
+  sz3g_dtype dtype;
+  int        ndim;          /* 1..3 (informational; dims are always 3D, leading extents 1)    */
+  uint64_t   dims[3];       /* local extents n0, n1, n2 (slowest first), all >= 1             */
+  uint64_t   dim0_offset;   /* global index of this slab's first dim-0 plane (a multiple of B
+                               when the field is sharded; 0 if not).  Only outlier indices
+                               depend on it: they are global linear indices.                 */
+} sz3g_grid;
+
+typedef struct {
+  uint32_t     block_size;  /* B; must be 6 (the tile shape of the device kernels)            */
+  uint32_t     radius;      /* R in [1, 32768]: codes R+q for |q| < R, 0 = outlier; 2R bins  */
+  sz3g_eb_mode eb_mode;
+  double       eb;          /* > 0, finite; absolute or value-range relative                 */
+  uint32_t     flags;       /* SZ3G_FLAG_*                                                    */
+} sz3g_params;
+
+/* a0 -- value range (needed for REL eb).
+ * x: prod(dims) elements of grid->dtype.  d_minmax: device double[2] <- {min, max}, the
+ * extrema widened to fp64.  If x holds a NaN, at least one of the two is NaN.  3 launches. */
+int sz3g_value_range(const sz3g_grid* grid, const void* x, double* d_minmax, sz3g_stream_t stream);
+
+/* a1-a7 -- compression (one fused kernel; 1 launch).
+ *   x            in   prod(dims) T, row-major.
+ *   d_minmax     in   device double[2] {min, max}; required iff eb_mode == REL (pass the GLOBAL
+ *                     range when the field is sharded, so every slab uses the same eb).
+ *   codes        out  prod(dims) uint16, same layout as x: R+q, or 0 for an outlier.
+ *   coef_codes   out  4 x nblocks int32, [block][c0,c1,c2,c3]; b0 bin = eb/2, slopes eb/(2B).
+ *   coef_raw     out  nullable; 4 x nblocks double, unquantised beta (parity checks only).
+ *   outlier_idx  out  up to outlier_cap uint64 GLOBAL linear indices (dim0_offset applied),
+ *   outlier_val  out  and their original values (T), in no particular order.
+ *   d_outlier_count in/out device uint64 (caller zeroes it): incremented by the true number of
+ *                     outliers; entries beyond outlier_cap are dropped and status bit 0 set.
+ *   hist         in/out nullable; 2R int64 bins ACCUMULATED (+=): hist[code] counts codes,
+ *                     hist[0] = outliers (P:418 frequency table).  Zero it for a fresh count.
+ *   d_eb_abs     out  nullable; device double <- the absolute eb actually used.
+ *   d_status     in/out device int32, SZ3G_STATUS_* bits or-ed in.
+ * Host errors: EINVAL, EUNSUPPORTED (dtype, block_size != 6), ERANGE (radius), ECUDA.      */
+int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, const void* x,
+                             const double* d_minmax, uint16_t* codes, int32_t* coef_codes,
+                             double* coef_raw, uint64_t* outlier_idx, void* outlier_val,
+                             uint64_t outlier_cap, unsigned long long* d_outlier_count,
+                             int64_t* hist, double* d_eb_abs, int32_t* d_status,
+                             sz3g_stream_t stream);
+
+/* a8 -- decompression (recover): x_out = (T)(p + 2 eb (c - R)) for c != 0, then the
+ * stored outlier values are scattered to their indices (2 launches, stream-ordered).
+ * params->eb_mode must be SZ3G_EB_ABS with params->eb = the eb_abs used at compression.
+ * outlier_idx are global indices (grid->dim0_offset is subtracted).  n_outliers is a HOST
+ * count (<= the capacity used at compression).  Bit-identical to the compress-time x'.     */
+int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
+                               const uint16_t* codes, const int32_t* coef_codes,
+                               const uint64_t* outlier_idx, const void* outlier_val,
+                               uint64_t n_outliers, void* x_out, sz3g_stream_t stream);
+
+/* a7 standalone -- histogram of n uint16 codes into 2R int64 bins, ACCUMULATED (+=).  Codes
+ * >= 2R are ignored.  1 launch. */
+int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* hist,
+                   sz3g_stream_t stream);
+
+/* number of regression blocks of a grid: prod ceil(n_d / block_size) (0 on bad input) */
+uint64_t sz3g_num_blocks(const sz3g_grid* grid, uint32_t block_size);
+
+/* 1 if the TMA/mbarrier pipelined kernels apply to this grid (alignment permitting), else 0 */
+int sz3g_uses_tma(const sz3g_grid* grid, int decompress);
+
+/* total device kernels this process has launched through the library (for launch counting) */
+uint64_t sz3g_launch_count(void);
+
+const char* sz3g_strerror(int code);
+const char* sz3g_last_cuda_error(void);
+const char* sz3g_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SZ3G_H */

@@ -1,0 +1,766 @@
+// libsz3g -- C ABI (include/sz3g.h) + sm_100a kernels of the block-regression compressor path.
+//
+// Kernels (DESIGN.md §5 lists each with its roofline):
+//   k_range_init / k_value_range / k_range_final   a0: min/max via ordered-u64 atomics
+//   k_compress_tma<T,W,S>      a1-a7 fused, persistent; 1 TMA producer warp + W consumer warps,
+//                              S-stage mbarrier ring of 6x6x96 tiles, codes staged in smem and
+//                              written back by TMA store, smem histogram window
+//   k_compress_plain<T>        same arithmetic, predicated coalesced global loads (any shape)
+//   k_decompress_tma<T,W,S>    a8: TMA-loaded code tiles -> x' tiles -> TMA store
+//   k_decompress_plain<T>      a8 for any shape
+//   k_outlier_scatter<T>       a8: x[idx] = val
+//   k_histogram                a7 standalone (smem window + global atomics)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <type_traits>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/sz3g.h"
+#include "ptx.cuh"
+#include "tile.cuh"
+
+using namespace sz3g;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+thread_local char g_cuda_err[256] = "";
+
+// ---------------------------------------------------------------------------------- a0
+__device__ __forceinline__ unsigned long long ord_key(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_to_double(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+__global__ void k_range_init(unsigned long long* keys) {
+  keys[0] = ~0ull;  // running min key
+  keys[1] = 0ull;   // running max key
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_value_range(const T* __restrict__ x, uint64_t n, unsigned long long* keys) {
+  T lo = x[0], hi = x[0];
+  bool nan = false;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int VEC = 16 / sizeof(T);
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  uint64_t done = 0;
+  if (aligned) {
+    using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    const V* xv = reinterpret_cast<const V*>(x);
+    const uint64_t nv = n / VEC;
+    uint64_t v = tid;
+    for (; v + 3 * nth < nv; v += 4 * nth) {
+      V a[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) a[u] = __ldcs(xv + v + u * nth);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const T* e = reinterpret_cast<const T*>(&a[u]);
+#pragma unroll
+        for (int c = 0; c < VEC; c++) {
+          nan |= (e[c] != e[c]);
+          lo = e[c] < lo ? e[c] : lo;
+          hi = e[c] > hi ? e[c] : hi;
+        }
+      }
+    }
+    for (; v < nv; v += nth) {
+      V a = __ldcs(xv + v);
+      const T* e = reinterpret_cast<const T*>(&a);
+#pragma unroll
+      for (int c = 0; c < VEC; c++) {
+        nan |= (e[c] != e[c]);
+        lo = e[c] < lo ? e[c] : lo;
+        hi = e[c] > hi ? e[c] : hi;
+      }
+    }
+    done = nv * VEC;
+  }
+  for (uint64_t e = done + tid; e < n; e += nth) {
+    const T v = x[e];
+    nan |= (v != v);
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+  double dlo = (double)lo, dhi = (double)hi;
+  if (dlo != dlo) dlo = dhi;  // x[0] NaN: min/max by comparisons never replace it
+  if (dhi != dhi) dhi = dlo;
+  unsigned long long klo = ord_key(dlo), khi = ord_key(dhi);
+  if (nan) khi = ord_key(__longlong_as_double(0x7ff8000000000000ll));  // max key = +NaN
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    klo = min(klo, __shfl_xor_sync(0xffffffffu, klo, o));
+    khi = max(khi, __shfl_xor_sync(0xffffffffu, khi, o));
+  }
+  __shared__ unsigned long long s_lo[8], s_hi[8];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { s_lo[w] = klo; s_hi[w] = khi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); i++) { klo = min(klo, s_lo[i]); khi = max(khi, s_hi[i]); }
+    atomicMin(&keys[0], klo);
+    atomicMax(&keys[1], khi);
+  }
+}
+
+__global__ void k_range_final(unsigned long long* keys) {
+  double* d = reinterpret_cast<double*>(keys);
+  const double lo = key_to_double(keys[0]), hi = key_to_double(keys[1]);
+  d[0] = lo;
+  d[1] = hi;
+}
+
+// ---------------------------------------------------------------------------------- shared parts
+struct KArgs {
+  Geo g;
+  uint32_t R;
+  int eb_mode;
+  double eb;
+  const double* d_minmax;
+  double* d_eb_abs;
+  int32_t* d_status;
+};
+
+__device__ __forceinline__ void hist_init(HistSmem& hs, uint32_t* win, uint32_t* zero, uint32_t R) {
+  hs.win = win;
+  hs.zero = zero;
+  hs.dummy = zero + 1;  // 32 sink slots follow the zero-bin counter
+  hs.nwin = min(2u * R, (uint32_t)HWIN);
+  hs.lo = (2u * R <= (uint32_t)HWIN) ? 0u : R - HWIN / 2;
+  for (uint32_t b = threadIdx.x; b < hs.nwin; b += blockDim.x) win[b] = 0u;
+  if (threadIdx.x == 0) *zero = 0u;
+}
+
+__device__ __forceinline__ void hist_flush(const HistSmem& hs, unsigned long long* hist) {
+  for (uint32_t b = threadIdx.x; b < hs.nwin; b += blockDim.x) {
+    const uint32_t v = hs.win[b];
+    if (v) atomicAdd(&hist[hs.lo + b], (unsigned long long)v);
+  }
+  if (threadIdx.x == 0 && *hs.zero) atomicAdd(&hist[0], (unsigned long long)*hs.zero);
+}
+
+// CTA prologue: O1/O2 constants into smem; returns false (and sets the status bit) on a bad range
+__device__ __forceinline__ bool cta_consts(const KArgs& a, Consts* s_k, int* s_ok) {
+  if (threadIdx.x == 0) {
+    Consts K;
+    const bool ok = make_consts(a.eb_mode, a.eb, a.d_minmax, K);
+    *s_ok = ok;
+    if (ok) *s_k = K;
+    if (blockIdx.x == 0) {
+      if (!ok && a.d_status) atomicOr(a.d_status, (int)SZ3G_STATUS_BAD_RANGE);
+      if (a.d_eb_abs) *a.d_eb_abs = ok ? K.eb_abs : __longlong_as_double(0x7ff8000000000000ll);
+    }
+  }
+  __syncthreads();
+  return *s_ok != 0;
+}
+
+__device__ __forceinline__ void overflow_check(const KArgs& a, const unsigned long long* ocount, uint64_t cap) {
+  // the last CTA to finish cannot know it is last without scratch; every CTA checks (cheap, 1 thread)
+  if (threadIdx.x == 0) {
+    if (*(volatile const unsigned long long*)ocount > cap) atomicOr(a.d_status, (int)SZ3G_STATUS_OUTLIER_OVERFLOW);
+  }
+}
+
+template <typename T, bool IN_SMEM, bool HIST>
+__device__ __forceinline__ void compress_tile_dispatch(const T* xs, uint64_t si, uint64_t sj, uint16_t* cs, uint64_t ci,
+                                                       uint64_t cj, const TileCoord tc, const Geo& g, const Consts& K,
+                                                       uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
+  if (tile_full(tc, g)) compress_tile<T, IN_SMEM, HIST, true>(xs, si, sj, cs, ci, cj, tc, g, K, R, o, hs);
+  else compress_tile<T, IN_SMEM, HIST, false>(xs, si, sj, cs, ci, cj, tc, g, K, R, o, hs);
+}
+
+// copy a staged 6x6x96 code tile to the global code array (fallback when no TMA store applies:
+// n2 * 2 bytes is not a multiple of 16).  Rows are 96 codes; 32-bit stores when n2 is even.
+__device__ __forceinline__ void store_code_rows(const uint16_t* __restrict__ cbuf, uint16_t* __restrict__ codes,
+                                                const TileCoord tc, const Geo& g) {
+  const int lane = threadIdx.x & 31;
+  const int m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
+  const int m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
+  const int kval = (int)umin64(TK, g.n2 - (uint64_t)tc.c * TK);
+  const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+  const bool even = (g.n2 & 1) == 0 && (reinterpret_cast<uintptr_t>(codes) & 3) == 0;
+  for (int i = 0; i < m0; i++)
+    for (int j = 0; j < m1; j++) {
+      const uint16_t* src = cbuf + (i * BS + j) * TK;
+      uint16_t* dst = codes + off + ((uint64_t)i * g.n1 + j) * g.n2;
+      if (even) {
+        for (int w = lane; 2 * w < kval; w += 32) {
+          if (2 * w + 1 < kval) reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(src)[w];
+          else dst[2 * w] = src[2 * w];
+        }
+      } else {
+        for (int k = lane; k < kval; k += 32) dst[k] = src[k];
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------------- compress, plain
+template <typename T, bool HIST>
+__global__ void __launch_bounds__(128) k_compress_plain(const T* __restrict__ x, KArgs a, CompressOut<T> o) {
+  __shared__ uint32_t s_win[HWIN];
+  __shared__ uint32_t s_zero[33];
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  HistSmem hs;
+  hist_init(hs, s_win, s_zero, a.R);
+  if (!cta_consts(a, &s_k, &s_ok)) return;
+  const Consts K = s_k;
+  const Geo& g = a.g;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < g.ntiles; t += warps) {
+    const TileCoord tc = decode_tile(t, g);
+    const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+    compress_tile_dispatch<T, false, HIST>(x + off, g.n1 * g.n2, g.n2, o.codes + off, g.n1 * g.n2, g.n2, tc, g, K, a.R, o, hs);
+  }
+  __syncthreads();
+  if (HIST) hist_flush(hs, o.hist);
+  overflow_check(a, o.ocount, o.cap);
+}
+
+// ---------------------------------------------------------------------------------- compress, TMA
+template <typename T, int W, int S>
+struct CompressSmem {
+  static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr size_t code_bytes = sizeof(uint16_t) * TILE_ELEMS;
+  static constexpr size_t off_codes = S * stage_bytes;
+  static constexpr size_t off_hist = off_codes + W * code_bytes;
+  static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (HWIN + 36);
+  static constexpr size_t off_k = off_bar + 2 * S * sizeof(uint64_t);
+  static constexpr size_t total = off_k + sizeof(Consts) + 16;
+};
+
+template <typename T, int W, int S, bool HIST>
+__global__ void __launch_bounds__((W + 1) * 32, 1)
+    k_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, int codes_tma,
+                   KArgs a, CompressOut<T> o) {
+  using L = CompressSmem<T, W, S>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  T* stages = reinterpret_cast<T*>(smem);
+  uint16_t* cbuf = reinterpret_cast<uint16_t*>(smem + L::off_codes);
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(smem + L::off_hist);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* empty = full + S;
+  Consts* s_k = reinterpret_cast<Consts*>(smem + L::off_k);
+  int* s_ok = reinterpret_cast<int*>(smem + L::off_k + sizeof(Consts));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  HistSmem hs;
+  hist_init(hs, s_win, s_win + HWIN, a.R);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (!cta_consts(a, s_k, s_ok)) return;
+  const Geo& g = a.g;
+  const uint64_t G = gridDim.x;
+  if (warp == W) {
+    // ---------------- producer: one elected lane streams tiles into the ring
+    if (lane == 0) {
+      ptx::prefetch_tensormap(&tm_x);
+      uint32_t n = 0;
+      for (uint64_t t = blockIdx.x; t < g.ntiles; t += G, n++) {
+        const uint32_t s = n % S, ph = (n / S) & 1u;
+        ptx::mbar_wait(&empty[s], ph ^ 1u);
+        const TileCoord tc = decode_tile(t, g);
+        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L::stage_bytes);
+        ptx::tma_load_3d(stages + (size_t)s * TILE_ELEMS, &tm_x, &full[s], (int)(tc.c * TK), (int)(tc.b * BS),
+                         (int)(tc.a * BS));
+      }
+    }
+  } else {
+    // ---------------- consumers: warp w takes the CTA's tiles w, w+W, ...
+    const Consts K = *s_k;
+    uint16_t* mycodes = cbuf + (size_t)warp * TILE_ELEMS;
+    uint32_t n = warp;
+    for (uint64_t t = blockIdx.x + (uint64_t)warp * G; t < g.ntiles; t += (uint64_t)W * G, n += W) {
+      const uint32_t s = n % S, ph = (n / S) & 1u;
+      const TileCoord tc = decode_tile(t, g);
+      if (codes_tma) {
+        if (lane == 0) ptx::bulk_wait_read0();  // previous TMA store finished reading mycodes
+        __syncwarp();
+      }
+      ptx::mbar_wait(&full[s], ph);
+      const T* xs = stages + (size_t)s * TILE_ELEMS;
+      compress_tile_dispatch<T, true, HIST>(xs, BS * TK, TK, mycodes, BS * TK, TK, tc, g, K, a.R, o, hs);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+      if (codes_tma) {
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_3d(&tm_c, mycodes, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+          ptx::bulk_commit();
+        }
+      } else {
+        store_code_rows(mycodes, o.codes, tc, g);
+        __syncwarp();
+      }
+    }
+    if (codes_tma && lane == 0) ptx::bulk_wait0();
+  }
+  __syncthreads();
+  if (HIST) hist_flush(hs, o.hist);
+  overflow_check(a, o.ocount, o.cap);
+}
+
+// ---------------------------------------------------------------------------------- decompress
+template <typename T>
+__global__ void __launch_bounds__(128) k_decompress_plain(const uint16_t* __restrict__ codes,
+                                                          const int32_t* __restrict__ coef, T* __restrict__ xo,
+                                                          KArgs a) {
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  if (!cta_consts(a, &s_k, &s_ok)) return;
+  const Consts K = s_k;
+  const Geo& g = a.g;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < g.ntiles; t += warps) {
+    const TileCoord tc = decode_tile(t, g);
+    const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+    decompress_tile<T, false, false>(codes + off, g.n1 * g.n2, g.n2, xo + off, g.n1 * g.n2, g.n2, tc, g, K, a.R,
+                                     coef);
+  }
+}
+
+template <typename T, int W, int S>
+struct DecompressSmem {
+  static constexpr size_t stage_bytes = sizeof(uint16_t) * TILE_ELEMS;
+  static constexpr size_t out_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr size_t off_out = S * stage_bytes;
+  static constexpr size_t off_bar = off_out + W * out_bytes;
+  static constexpr size_t off_k = off_bar + 2 * S * sizeof(uint64_t);
+  static constexpr size_t total = off_k + sizeof(Consts) + 16;
+};
+
+template <typename T, int W, int S>
+__global__ void __launch_bounds__((W + 1) * 32, 1)
+    k_decompress_tma(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_x,
+                     const int32_t* __restrict__ coef, KArgs a) {
+  using L = DecompressSmem<T, W, S>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t* stages = reinterpret_cast<uint16_t*>(smem);
+  T* obuf = reinterpret_cast<T*>(smem + L::off_out);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* empty = full + S;
+  Consts* s_k = reinterpret_cast<Consts*>(smem + L::off_k);
+  int* s_ok = reinterpret_cast<int*>(smem + L::off_k + sizeof(Consts));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (!cta_consts(a, s_k, s_ok)) return;
+  const Geo& g = a.g;
+  const uint64_t G = gridDim.x;
+  if (warp == W) {
+    if (lane == 0) {
+      ptx::prefetch_tensormap(&tm_c);
+      uint32_t n = 0;
+      for (uint64_t t = blockIdx.x; t < g.ntiles; t += G, n++) {
+        const uint32_t s = n % S, ph = (n / S) & 1u;
+        ptx::mbar_wait(&empty[s], ph ^ 1u);
+        const TileCoord tc = decode_tile(t, g);
+        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L::stage_bytes);
+        ptx::tma_load_3d(stages + (size_t)s * TILE_ELEMS, &tm_c, &full[s], (int)(tc.c * TK), (int)(tc.b * BS),
+                         (int)(tc.a * BS));
+      }
+    }
+  } else {
+    const Consts K = *s_k;
+    T* myout = obuf + (size_t)warp * TILE_ELEMS;
+    uint32_t n = warp;
+    for (uint64_t t = blockIdx.x + (uint64_t)warp * G; t < g.ntiles; t += (uint64_t)W * G, n += W) {
+      const uint32_t s = n % S, ph = (n / S) & 1u;
+      const TileCoord tc = decode_tile(t, g);
+      if (lane == 0) ptx::bulk_wait_read0();
+      __syncwarp();
+      ptx::mbar_wait(&full[s], ph);
+      decompress_tile<T, true, true>(stages + (size_t)s * TILE_ELEMS, BS * TK, TK, myout, BS * TK, TK, tc, g, K,
+                                     a.R, coef);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(&tm_x, myout, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+        ptx::bulk_commit();
+      }
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+}
+
+template <typename T>
+__global__ void k_outlier_scatter(const uint64_t* __restrict__ idx, const T* __restrict__ val, uint64_t n,
+                                  uint64_t base, uint64_t N, T* __restrict__ xo) {
+  for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < n; m += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = idx[m] - base;
+    if (idx[m] >= base && e < N) xo[e] = val[m];
+  }
+}
+
+// ---------------------------------------------------------------------------------- histogram
+__global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ codes, uint64_t n, uint32_t R,
+                                                   unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t s_win[HWIN];
+  __shared__ uint32_t s_zero[33];
+  HistSmem hs;
+  hist_init(hs, s_win, s_zero, R);
+  __syncthreads();
+  const uint32_t nb = 2u * R;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
+  auto add = [&](uint32_t c) {
+    if (c >= nb) return;
+    const uint32_t w = c - hs.lo;
+    if (w < hs.nwin) atomicAdd(&s_win[w], 1u);
+    else atomicAdd(&hist[c], 1ull);
+  };
+  uint64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(codes) & 15) == 0) {
+    const uint4* cv = reinterpret_cast<const uint4*>(codes);
+    const uint64_t nv = n / 8;
+    for (uint64_t v = tid; v < nv; v += nth) {
+      const uint4 q = __ldcs(cv + v);
+      const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        add(w4[u] & 0xffffu);
+        add(w4[u] >> 16);
+      }
+    }
+    done = nv * 8;
+  }
+  for (uint64_t e = done + tid; e < n; e += nth) add(codes[e]);
+  __syncthreads();
+  hist_flush(hs, hist);
+}
+
+// ---------------------------------------------------------------------------------- host helpers
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+inline bool hist_ptr_nonnull(const int64_t* h) { return h != nullptr; }
+
+int cuda_fail(cudaError_t e) {
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return SZ3G_ECUDA;
+}
+
+int check_launch(int nlaunch) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches.fetch_add((uint64_t)nlaunch, std::memory_order_relaxed);
+  return SZ3G_OK;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 3D tensor map over a row-major (n0, n1, n2) array, box {96, 6, 6}
+bool make_map(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, const Geo& g) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {g.n2, g.n1, g.n0};
+  const cuuint64_t strides[2] = {g.n2 * esize, g.n1 * g.n2 * esize};
+  const cuuint32_t box[3] = {(cuuint32_t)TK, (cuuint32_t)BS, (cuuint32_t)BS};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool map_ok(const void* ptr, size_t esize, const Geo& g) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0) return false;
+  if ((g.n2 * esize) % 16 != 0) return false;
+  if (g.n0 > (1ull << 31) || g.n1 > (1ull << 31) || g.n2 > (1ull << 31)) return false;
+  if (g.n1 * g.n2 * esize >= (1ull << 40)) return false;
+  return encode_fn() != nullptr;
+}
+
+int validate_grid(const sz3g_grid* grid) {
+  if (!grid) return SZ3G_EINVAL;
+  if (grid->dtype != SZ3G_F32 && grid->dtype != SZ3G_F64) return SZ3G_EUNSUPPORTED;
+  if (grid->ndim < 1 || grid->ndim > 3) return SZ3G_EUNSUPPORTED;
+  if (grid->dims[0] == 0 || grid->dims[1] == 0 || grid->dims[2] == 0) return SZ3G_EINVAL;
+  return SZ3G_OK;
+}
+
+int validate_params(const sz3g_params* p) {
+  if (!p) return SZ3G_EINVAL;
+  if (p->block_size != BS) return SZ3G_EUNSUPPORTED;
+  if (p->radius < 1 || p->radius > 32768) return SZ3G_ERANGE;
+  if (p->eb_mode != SZ3G_EB_ABS && p->eb_mode != SZ3G_EB_REL_RANGE) return SZ3G_EINVAL;
+  if (!(p->eb > 0.0) || !(p->eb < 1e308)) return SZ3G_EINVAL;
+  return SZ3G_OK;
+}
+
+Geo make_geo(const sz3g_grid* grid) {
+  Geo g;
+  g.n0 = grid->dims[0];
+  g.n1 = grid->dims[1];
+  g.n2 = grid->dims[2];
+  g.NB0 = (uint32_t)((g.n0 + BS - 1) / BS);
+  g.NB1 = (uint32_t)((g.n1 + BS - 1) / BS);
+  g.NB2 = (uint32_t)((g.n2 + BS - 1) / BS);
+  g.NT2 = (g.NB2 + 15) / 16;
+  g.ntiles = (uint64_t)g.NB0 * g.NB1 * g.NT2;
+  g.gofs = grid->dim0_offset * g.n1 * g.n2;
+  return g;
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// tuned configurations: (consumer warps, ring stages); smem fits the 227 KiB per-CTA limit
+constexpr int CW32 = 8, CS32 = 10;   // f32 compress: 10 x 13.5 KiB stages + 8 x 6.75 KiB codes + 32 KiB hist
+constexpr int CW64 = 4, CS64 = 6;    // f64 compress: 6 x 27 KiB + 4 x 6.75 KiB + 32 KiB
+constexpr int DW32 = 8, DS32 = 12;   // f32 decompress: 12 x 6.75 KiB + 8 x 13.5 KiB
+constexpr int DW64 = 6, DS64 = 8;    // f64 decompress: 8 x 6.75 KiB + 6 x 27 KiB
+
+template <typename T, int W, int S, bool HIST>
+int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
+                        const CompressOut<T>& co, cudaStream_t st) {
+  using L = CompressSmem<T, W, S>;
+  static_assert(L::total <= 232448, "smem");
+  CUtensorMap mx, mc;
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
+  memset(&mc, 0, sizeof(mc));
+  if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) codes_tma = false;
+  auto kern = k_compress_tma<T, W, S, HIST>;
+  cudaError_t e = set_smem(kern, L::total);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
+  kern<<<(unsigned)grid, (W + 1) * 32, L::total, st>>>(mx, mc, codes_tma ? 1 : 0, ka, co);
+  return check_launch(1);
+}
+
+template <typename T, int W, int S>
+int launch_decompress_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, void* xo, const KArgs& ka,
+                          cudaStream_t st) {
+  using L = DecompressSmem<T, W, S>;
+  static_assert(L::total <= 232448, "smem");
+  CUtensorMap mc, mx;
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) return SZ3G_ECUDA;
+  if (!make_map(&mx, dt, sizeof(T), xo, g)) return SZ3G_ECUDA;
+  auto kern = k_decompress_tma<T, W, S>;
+  cudaError_t e = set_smem(kern, L::total);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
+  kern<<<(unsigned)grid, (W + 1) * 32, L::total, st>>>(mc, mx, coef, ka);
+  return check_launch(1);
+}
+
+}  // namespace
+
+// ====================================================================================== C ABI
+extern "C" {
+
+int sz3g_value_range(const sz3g_grid* grid, const void* x, double* d_minmax, sz3g_stream_t stream) {
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  if (!x || !d_minmax) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t n = grid->dims[0] * grid->dims[1] * grid->dims[2];
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(d_minmax);
+  k_range_init<<<1, 1, 0, st>>>(keys);
+  const uint64_t want = (n + 255) / 256;
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sm_count() * 8));
+  if (grid->dtype == SZ3G_F32) k_value_range<float><<<blocks, 256, 0, st>>>((const float*)x, n, keys);
+  else k_value_range<double><<<blocks, 256, 0, st>>>((const double*)x, n, keys);
+  k_range_final<<<1, 1, 0, st>>>(keys);
+  return check_launch(3);
+}
+
+int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, const void* x,
+                             const double* d_minmax, uint16_t* codes, int32_t* coef_codes, double* coef_raw,
+                             uint64_t* outlier_idx, void* outlier_val, uint64_t outlier_cap,
+                             unsigned long long* d_outlier_count, int64_t* hist, double* d_eb_abs,
+                             int32_t* d_status, sz3g_stream_t stream) {
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  rc = validate_params(params);
+  if (rc) return rc;
+  if (!x || !codes || !coef_codes || !d_outlier_count || !d_status) return SZ3G_EINVAL;
+  if (outlier_cap > 0 && (!outlier_idx || !outlier_val)) return SZ3G_EINVAL;
+  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(coef_codes) & 15) || (coef_raw && (reinterpret_cast<uintptr_t>(coef_raw) & 15)))
+    return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Geo g = make_geo(grid);
+  KArgs ka;
+  ka.g = g;
+  ka.R = params->radius;
+  ka.eb_mode = (int)params->eb_mode;
+  ka.eb = params->eb;
+  ka.d_minmax = d_minmax;
+  ka.d_eb_abs = d_eb_abs;
+  ka.d_status = d_status;
+  const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
+  const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
+  const bool tma = !generic && map_ok(x, es, g);
+  const bool codes_tma = tma && map_ok(codes, 2, g);
+  const bool use_hist = hist_ptr_nonnull(hist);
+  if (grid->dtype == SZ3G_F32) {
+    CompressOut<float> co{codes, coef_codes, coef_raw, outlier_idx, (float*)outlier_val, outlier_cap,
+                          d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
+    if (tma) return use_hist ? launch_compress_tma<float, CW32, CS32, true>(g, x, codes, codes_tma, ka, co, st)
+                         : launch_compress_tma<float, CW32, CS32, false>(g, x, codes, codes_tma, ka, co, st);
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
+    if (use_hist) k_compress_plain<float, true><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
+    else k_compress_plain<float, false><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
+  } else {
+    CompressOut<double> co{codes, coef_codes, coef_raw, outlier_idx, (double*)outlier_val, outlier_cap,
+                           d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
+    if (tma) return use_hist ? launch_compress_tma<double, CW64, CS64, true>(g, x, codes, codes_tma, ka, co, st)
+                         : launch_compress_tma<double, CW64, CS64, false>(g, x, codes, codes_tma, ka, co, st);
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
+    if (use_hist) k_compress_plain<double, true><<<blocks, 128, 0, st>>>((const double*)x, ka, co);
+    else k_compress_plain<double, false><<<blocks, 128, 0, st>>>((const double*)x, ka, co);
+  }
+  return check_launch(1);
+}
+
+int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params, const uint16_t* codes,
+                               const int32_t* coef_codes, const uint64_t* outlier_idx, const void* outlier_val,
+                               uint64_t n_outliers, void* x_out, sz3g_stream_t stream) {
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  rc = validate_params(params);
+  if (rc) return rc;
+  if (params->eb_mode != SZ3G_EB_ABS) return SZ3G_EINVAL;
+  if (!codes || !coef_codes || !x_out) return SZ3G_EINVAL;
+  if (n_outliers > 0 && (!outlier_idx || !outlier_val)) return SZ3G_EINVAL;
+  if (reinterpret_cast<uintptr_t>(coef_codes) & 15) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Geo g = make_geo(grid);
+  KArgs ka;
+  memset(&ka, 0, sizeof(ka));
+  ka.g = g;
+  ka.R = params->radius;
+  ka.eb_mode = 0;
+  ka.eb = params->eb;
+  int32_t* dummy_status = nullptr;  // decompress never reports: eb validated on the host
+  ka.d_status = dummy_status;
+  const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
+  const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
+  const bool tma = !generic && map_ok(codes, 2, g) && map_ok(x_out, es, g);
+  const uint64_t N = g.n0 * g.n1 * g.n2;
+  int launched = 0;
+  if (grid->dtype == SZ3G_F32) {
+    if (tma) {
+      rc = launch_decompress_tma<float, DW32, DS32>(g, codes, coef_codes, x_out, ka, st);
+      if (rc) return rc;
+    } else {
+      const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
+      k_decompress_plain<float><<<blocks, 128, 0, st>>>(codes, coef_codes, (float*)x_out, ka);
+      launched++;
+    }
+    if (n_outliers) {
+      const unsigned b = (unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096);
+      k_outlier_scatter<float><<<b, 256, 0, st>>>(outlier_idx, (const float*)outlier_val, n_outliers, g.gofs, N,
+                                                  (float*)x_out);
+      launched++;
+    }
+  } else {
+    if (tma) {
+      rc = launch_decompress_tma<double, DW64, DS64>(g, codes, coef_codes, x_out, ka, st);
+      if (rc) return rc;
+    } else {
+      const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
+      k_decompress_plain<double><<<blocks, 128, 0, st>>>(codes, coef_codes, (double*)x_out, ka);
+      launched++;
+    }
+    if (n_outliers) {
+      const unsigned b = (unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096);
+      k_outlier_scatter<double><<<b, 256, 0, st>>>(outlier_idx, (const double*)outlier_val, n_outliers, g.gofs, N,
+                                                   (double*)x_out);
+      launched++;
+    }
+  }
+  return check_launch(launched);
+}
+
+int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* hist, sz3g_stream_t stream) {
+  if (!hist || (n > 0 && !codes)) return SZ3G_EINVAL;
+  if (radius < 1 || radius > 32768) return SZ3G_ERANGE;
+  if (n == 0) return SZ3G_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, sm_count() * 2));
+  k_histogram<<<blocks, 512, 0, st>>>(codes, n, radius, reinterpret_cast<unsigned long long*>(hist));
+  return check_launch(1);
+}
+
+uint64_t sz3g_num_blocks(const sz3g_grid* grid, uint32_t block_size) {
+  if (!grid || block_size == 0) return 0;
+  uint64_t nb = 1;
+  for (int d = 0; d < 3; d++) nb *= (grid->dims[d] + block_size - 1) / block_size;
+  return nb;
+}
+
+int sz3g_uses_tma(const sz3g_grid* grid, int decompress) {
+  if (validate_grid(grid)) return 0;
+  const Geo g = make_geo(grid);
+  const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
+  const bool xin = (g.n2 * es) % 16 == 0;
+  const bool cod = (g.n2 * 2) % 16 == 0;
+  if (encode_fn() == nullptr) return 0;
+  return decompress ? (xin && cod) : xin;
+}
+
+uint64_t sz3g_launch_count(void) { return g_launches.load(); }
+
+const char* sz3g_strerror(int code) {
+  switch (code) {
+    case SZ3G_OK: return "ok";
+    case SZ3G_EINVAL: return "invalid argument";
+    case SZ3G_EUNSUPPORTED: return "unsupported dtype/block size/ndim";
+    case SZ3G_ERANGE: return "radius out of range [1, 32768]";
+    case SZ3G_ECUDA: return "CUDA error";
+    default: return "unknown error";
+  }
+}
+
+const char* sz3g_last_cuda_error(void) { return g_cuda_err; }
+const char* sz3g_version(void) { return "sz3g 0.1 (sm_100a)"; }
+
+}  // extern "C"

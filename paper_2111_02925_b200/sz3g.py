@@ -1,0 +1,293 @@
+"""Python binding of libsz3g (include/sz3g.h): argument marshalling only.
+
+Every step of the path runs in the library's sm_100a kernels; PyTorch only provides device memory,
+streams and (in ``dist.py``) process groups.  There is no CPU fallback: if the library is missing or
+no CUDA device is present, the calls raise.
+
+Names follow the C ABI: ``value_range``, ``regression_compress``, ``regression_decompress``,
+``histogram``, ``num_blocks``.  ``compress`` / ``decompress`` are the one-call conveniences on top.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+from . import build as _build
+
+SZ3G_F32, SZ3G_F64 = 0, 1
+SZ3G_EB_ABS, SZ3G_EB_REL_RANGE = 0, 1
+FLAG_FORCE_GENERIC = 0x1
+STATUS_OUTLIER_OVERFLOW, STATUS_BAD_RANGE = 0x1, 0x2
+BLOCK = 6
+_ERR = {0: "ok", -1: "EINVAL", -2: "EUNSUPPORTED", -3: "ERANGE", -4: "ECUDA"}
+
+
+class SZ3GError(RuntimeError):
+    pass
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int), ("ndim", ctypes.c_int), ("dims", ctypes.c_uint64 * 3),
+                ("dim0_offset", ctypes.c_uint64)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("block_size", ctypes.c_uint32), ("radius", ctypes.c_uint32), ("eb_mode", ctypes.c_int),
+                ("eb", ctypes.c_double), ("flags", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(allow_build: bool = False):
+    """Load libsz3g.so (built in-tree by ``__graft_entry__.build()``); raise loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.LIB):
+        if allow_build:
+            _build.build()
+        else:
+            raise SZ3GError(f"libsz3g.so not built ({_build.LIB}); run `python -m paper_2111_02925_b200.build`")
+    lib = ctypes.CDLL(_build.LIB)
+    P, U64, U32, I32, D = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_double
+    GP, PP = ctypes.POINTER(Grid), ctypes.POINTER(Params)
+    lib.sz3g_value_range.argtypes = [GP, P, P, P]
+    lib.sz3g_regression_compress.argtypes = [GP, PP, P, P, P, P, P, P, P, U64, P, P, P, P, P]
+    lib.sz3g_regression_decompress.argtypes = [GP, PP, P, P, P, P, U64, P, P]
+    lib.sz3g_histogram.argtypes = [P, U64, U32, P, P]
+    lib.sz3g_num_blocks.argtypes = [GP, U32]
+    lib.sz3g_num_blocks.restype = U64
+    lib.sz3g_uses_tma.argtypes = [GP, I32]
+    lib.sz3g_launch_count.restype = U64
+    for f in ("sz3g_strerror",):
+        getattr(lib, f).argtypes = [I32]
+        getattr(lib, f).restype = ctypes.c_char_p
+    lib.sz3g_last_cuda_error.restype = ctypes.c_char_p
+    lib.sz3g_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regression_decompress", "sz3g_histogram",
+                    "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_strerror",
+                    "sz3g_last_cuda_error", "sz3g_version")
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        extra = ""
+        if rc == -4:
+            extra = ": " + load().sz3g_last_cuda_error().decode()
+        raise SZ3GError(f"{what} failed: {_ERR.get(rc, rc)}{extra}")
+
+
+def _dtype_id(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return SZ3G_F32
+    if dt == torch.float64:
+        return SZ3G_F64
+    raise SZ3GError(f"unsupported dtype {dt}")
+
+
+def _shape3(shape) -> tuple:
+    shape = tuple(int(s) for s in shape)
+    if not 1 <= len(shape) <= 3:
+        raise SZ3GError("fields are 1D, 2D or 3D")
+    return (1,) * (3 - len(shape)) + shape
+
+
+def make_grid(shape, dtype: torch.dtype, dim0_offset: int = 0) -> Grid:
+    s3 = _shape3(shape)
+    return Grid(_dtype_id(dtype), len(tuple(shape)), (ctypes.c_uint64 * 3)(*s3), dim0_offset)
+
+
+def make_params(eb: float, eb_mode: str = "rel", radius: int = 32768, flags: int = 0) -> Params:
+    mode = {"abs": SZ3G_EB_ABS, "rel": SZ3G_EB_REL_RANGE}[eb_mode]
+    return Params(BLOCK, radius, mode, float(eb), flags)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise SZ3GError("tensors passed to libsz3g must be contiguous CUDA tensors")
+
+
+def num_blocks(shape) -> int:
+    g = make_grid(shape, torch.float32)
+    return int(load().sz3g_num_blocks(ctypes.byref(g), BLOCK))
+
+
+def uses_tma(shape, dtype: torch.dtype, decompress: bool = False) -> bool:
+    g = make_grid(shape, dtype)
+    return bool(load().sz3g_uses_tma(ctypes.byref(g), int(decompress)))
+
+
+def launch_count() -> int:
+    return int(load().sz3g_launch_count())
+
+
+# ------------------------------------------------------------------------------------------- a0
+def value_range(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Device double[2] {min, max} of x (sz3g_value_range)."""
+    _require_cuda(x)
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=x.device)
+    g = make_grid(x.shape, x.dtype)
+    _check(load().sz3g_value_range(ctypes.byref(g), _ptr(x), _ptr(out), _stream(stream)), "sz3g_value_range")
+    return out
+
+
+# ------------------------------------------------------------------------------------------- a1-a7
+@dataclass
+class Compressed:
+    shape: tuple
+    dtype: torch.dtype
+    radius: int
+    dim0_offset: int
+    codes: torch.Tensor           # uint16, field shape
+    coef_codes: torch.Tensor      # int32 [NB, 4]
+    coef_raw: torch.Tensor | None  # float64 [NB, 4]
+    outlier_idx: torch.Tensor     # int64 (uint64 bits) [cap]
+    outlier_val: torch.Tensor     # T [cap]
+    outlier_count: torch.Tensor   # int64 [1] (device)
+    hist: torch.Tensor | None     # int64 [2R]
+    eb_abs_dev: torch.Tensor      # float64 [1] (device)
+    status: torch.Tensor          # int32 [1] (device)
+    n_outliers: int | None = None
+    eb_abs: float | None = None
+
+    def finalize(self) -> "Compressed":
+        """Synchronise on the results, raise on device status bits, fill n_outliers / eb_abs."""
+        st = int(self.status.item())
+        cnt = int(self.outlier_count.item())
+        if st & STATUS_BAD_RANGE:
+            raise SZ3GError("bad value range: eb_abs is not finite or <= 0")
+        if st & STATUS_OUTLIER_OVERFLOW:
+            raise SZ3GError(f"outlier capacity {self.outlier_idx.numel()} exceeded ({cnt} outliers)")
+        self.n_outliers = cnt
+        self.eb_abs = float(self.eb_abs_dev.item())
+        return self
+
+
+class CompressBuffers:
+    """Preallocated device outputs for repeated compression of one shape (no allocation per call)."""
+
+    def __init__(self, shape, dtype: torch.dtype, radius: int = 32768, outlier_cap: int | None = None,
+                 device=None, coef_raw: bool = False, hist: bool = True):
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        N = 1
+        for s in shape:
+            N *= int(s)
+        nb = num_blocks(shape)
+        cap = outlier_cap if outlier_cap is not None else max(4096, N // 64)
+        self.shape, self.dtype, self.radius = tuple(shape), dtype, radius
+        self.codes = torch.empty(tuple(shape), dtype=torch.uint16, device=device)
+        self.coef_codes = torch.empty((nb, 4), dtype=torch.int32, device=device)
+        self.coef_raw = torch.empty((nb, 4), dtype=torch.float64, device=device) if coef_raw else None
+        self.outlier_idx = torch.empty(cap, dtype=torch.int64, device=device)
+        self.outlier_val = torch.empty(cap, dtype=dtype, device=device)
+        self.outlier_count = torch.zeros(1, dtype=torch.int64, device=device)
+        self.hist = torch.zeros(2 * radius, dtype=torch.int64, device=device) if hist else None
+        self.eb_abs = torch.zeros(1, dtype=torch.float64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.minmax = torch.zeros(2, dtype=torch.float64, device=device)
+
+    def reset(self):
+        """Zero the accumulating outputs (outlier counter, histogram, status)."""
+        self.outlier_count.zero_()
+        self.status.zero_()
+        if self.hist is not None:
+            self.hist.zero_()
+
+
+def regression_compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768,
+                        d_minmax: torch.Tensor | None = None, bufs: CompressBuffers | None = None,
+                        outlier_cap: int | None = None, coef_raw: bool = False, hist: bool = True,
+                        dim0_offset: int = 0, flags: int = 0, stream=None, reset: bool = True) -> Compressed:
+    """sz3g_regression_compress.  Asynchronous: call ``.finalize()`` on the result to sync and check.
+
+    In REL mode ``d_minmax`` (device double[2]) is the global value range; when omitted it is computed
+    here with ``value_range`` (unsharded use).  ``bufs`` reuses preallocated outputs; with
+    ``reset=False`` the histogram / outlier counter / status are NOT zeroed first (caller did it).
+    """
+    _require_cuda(x)
+    if bufs is None:
+        bufs = CompressBuffers(x.shape, x.dtype, radius, outlier_cap, x.device, coef_raw, hist)
+    elif reset:
+        bufs.reset()
+    if bufs is not None and bufs.radius != radius:
+        raise SZ3GError("buffer radius mismatch")
+    if bufs is not None and reset is True and bufs.hist is not None and hist is False:
+        pass
+    if eb_mode == "rel" and d_minmax is None:
+        d_minmax = value_range(x, bufs.minmax, stream)
+    g = make_grid(x.shape, x.dtype, dim0_offset)
+    p = make_params(eb, eb_mode, radius, flags)
+    rc = load().sz3g_regression_compress(
+        ctypes.byref(g), ctypes.byref(p), _ptr(x), _ptr(d_minmax), _ptr(bufs.codes), _ptr(bufs.coef_codes),
+        _ptr(bufs.coef_raw), _ptr(bufs.outlier_idx), _ptr(bufs.outlier_val), bufs.outlier_idx.numel(),
+        _ptr(bufs.outlier_count), _ptr(bufs.hist if hist else None), _ptr(bufs.eb_abs), _ptr(bufs.status),
+        _stream(stream))
+    _check(rc, "sz3g_regression_compress")
+    return Compressed(tuple(x.shape), x.dtype, radius, dim0_offset, bufs.codes, bufs.coef_codes, bufs.coef_raw,
+                      bufs.outlier_idx, bufs.outlier_val, bufs.outlier_count, bufs.hist if hist else None,
+                      bufs.eb_abs, bufs.status)
+
+
+def regression_decompress(codes: torch.Tensor, coef_codes: torch.Tensor, outlier_idx: torch.Tensor,
+                          outlier_val: torch.Tensor, n_outliers: int, eb_abs: float, radius: int = 32768,
+                          dtype: torch.dtype = torch.float32, dim0_offset: int = 0, out: torch.Tensor | None = None,
+                          flags: int = 0, stream=None) -> torch.Tensor:
+    """sz3g_regression_decompress (recover) + outlier scatter."""
+    _require_cuda(codes, coef_codes, outlier_idx, outlier_val, out)
+    if out is None:
+        out = torch.empty(codes.shape, dtype=dtype, device=codes.device)
+    g = make_grid(codes.shape, out.dtype, dim0_offset)
+    p = make_params(eb_abs, "abs", radius, flags)
+    rc = load().sz3g_regression_decompress(ctypes.byref(g), ctypes.byref(p), _ptr(codes), _ptr(coef_codes),
+                                           _ptr(outlier_idx), _ptr(outlier_val), int(n_outliers), _ptr(out),
+                                           _stream(stream))
+    _check(rc, "sz3g_regression_decompress")
+    return out
+
+
+def histogram(codes: torch.Tensor, radius: int = 32768, hist: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sz3g_histogram: accumulate the 2R-bin int64 histogram of uint16 codes."""
+    _require_cuda(codes, hist)
+    if hist is None:
+        hist = torch.zeros(2 * radius, dtype=torch.int64, device=codes.device)
+    rc = load().sz3g_histogram(_ptr(codes), codes.numel(), radius, _ptr(hist), _stream(stream))
+    _check(rc, "sz3g_histogram")
+    return hist
+
+
+# ------------------------------------------------------------------------------------------- one-call API
+def compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768, **kw) -> Compressed:
+    """Compress a CUDA field and check the device status (synchronises)."""
+    res = regression_compress(x, eb, eb_mode, radius, **kw)
+    res.finalize()
+    return res
+
+
+def decompress(res: Compressed, out: torch.Tensor | None = None, flags: int = 0) -> torch.Tensor:
+    if res.n_outliers is None:
+        res.finalize()
+    return regression_decompress(res.codes, res.coef_codes, res.outlier_idx, res.outlier_val, res.n_outliers,
+                                 res.eb_abs, res.radius, res.dtype, res.dim0_offset, out, flags)

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element, on the same
+seeded input bytes.  Rules in tests/parity_util.py.  Needs a B200 (marked gpu)."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from tests.parity_util import compare  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+GEN = 0x1  # FLAG_FORCE_GENERIC
+
+
+def sz():
+    from paper_2111_02925_b200 import sz3g
+    sz3g.load()
+    return sz3g
+
+
+def run_gpu(x: torch.Tensor, eb, mode, R, flags=0, dim0_offset=0, d_minmax=None, cap=None):
+    s = sz()
+    res = s.regression_compress(x, eb, mode, R, d_minmax=d_minmax, coef_raw=True, flags=flags,
+                                dim0_offset=dim0_offset, outlier_cap=cap if cap is not None else x.numel())
+    res.finalize()
+    xo = s.decompress(res, flags=flags)
+    torch.cuda.synchronize()
+    n = res.n_outliers
+    gpu = dict(codes=res.codes.cpu().numpy(), coef_codes=res.coef_codes.cpu().numpy(),
+               coef_raw=res.coef_raw.cpu().numpy(),
+               outlier_idx=res.outlier_idx[:n].cpu().numpy().view(np.uint64),
+               outlier_val=res.outlier_val[:n].cpu().numpy(),
+               hist=res.hist.cpu().numpy(), eb_abs=res.eb_abs)
+    return gpu, xo.cpu().numpy(), res
+
+
+def check(xh: np.ndarray, eb, mode, R, flags=0, rng_override=None):
+    x = torch.from_numpy(np.ascontiguousarray(xh)).cuda()
+    gpu, xdec, res = run_gpu(x, eb, mode, R, flags)
+    orc = oracle.compress(xh, eb, mode, radius=R, value_range_override=rng_override)
+    dec_of_gpu = oracle.decompress(dims=orc.dims, dtype=xh.dtype, radius=R, eb_abs=orc.eb_abs, codes=gpu["codes"],
+                                   coef_codes=gpu["coef_codes"], outlier_idx=gpu["outlier_idx"],
+                                   outlier_val=gpu["outlier_val"])
+    rep = compare(xh, gpu, orc, xdec_gpu=xdec, xdec_orc_of_gpu=dec_of_gpu)
+    return rep
+
+
+# ----------------------------------------------------------------------------- fuzz (both kernel paths)
+def fuzz_case(t):
+    rng = np.random.default_rng(1000 + t)
+    shapes = [(13, 17, 96), (7, 11, 200), (20, 6, 64), (1, 1, 500), (3, 40, 8), (12, 12, 12), (40, 1, 36),
+              (6, 6, 97), (9, 5, 104), (1, 37, 1)]
+    dims = shapes[t % len(shapes)] if t < 20 else tuple(int(v) for v in rng.integers(1, 41, size=3))
+    dtype = [np.float32, np.float64][t % 2]
+    mode = ["abs", "rel"][(t // 2) % 2]
+    R = [32768, 4, 64, 1, 32768][(t // 4) % 5]
+    kind = t % 4
+    if kind == 0:
+        f = rng.normal(size=dims)
+    elif kind == 1:
+        f = np.cumsum(np.cumsum(rng.normal(size=dims), axis=-1), axis=0)
+    elif kind == 2:
+        f = np.exp(2 * rng.normal(size=dims))
+    else:
+        f = rng.uniform(-1e4, 1e4, size=dims)
+    eb = float(rng.choice([1e-1, 1e-3, 1e-5]))
+    if mode == "abs":
+        eb *= float(np.ptp(f) + 1e-3)
+    return f.astype(dtype), eb, mode, R
+
+
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+@pytest.mark.parametrize("t", list(range(40)))
+def test_fuzz_parity(t, flags):
+    f, eb, mode, R = fuzz_case(t)
+    if mode == "rel" and np.ptp(f) == 0:
+        pytest.skip("constant field")
+    check(f, eb, mode, R, flags)
+
+
+# ----------------------------------------------------------------------------- configs at full size
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_config_full_size(name):
+    from synth import config_by_name, make_field
+    cfg = config_by_name(name)
+    x = make_field(cfg, device="cuda")
+    xh = x.cpu().numpy()
+    rep = check(xh, cfg.eb, cfg.eb_mode, cfg.radius)
+    print(name, rep)
+    # blocks exempt as coefficient near-ties: the window width is set by the 1e-12 beta tolerance, so
+    # expect ~ 8 * window * NB of them (a few per 10^5 blocks on c4); none may be a real mismatch beyond
+    nb = oracle.num_blocks(xh.shape)
+    assert rep["exempt_blocks"] <= max(4, nb // 10000)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_config_plain_path(name):
+    from synth import config_by_name, make_field
+    cfg = config_by_name(name)
+    xh = make_field(cfg, device="cuda").cpu().numpy()
+    check(xh, cfg.eb, cfg.eb_mode, cfg.radius, GEN)
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled_slabs():
+    """Config 5 (16 GiB) on the GPU in the bench's launch configuration; the oracle recomputes three
+    block-aligned slabs (with the global value range) and every property that holds at any size is
+    checked on the full output."""
+    from synth import config_by_name, make_field
+    cfg = config_by_name("c5")
+    s = sz()
+    x = make_field(cfg, device="cuda")
+    res = s.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, coef_raw=False)
+    res.finalize()
+    mm = res.eb_abs
+    lo, hi = (float(v) for v in s.value_range(x).cpu())
+    assert mm == cfg.eb * (hi - lo)
+    n = res.n_outliers
+    N = x.numel()
+    assert int(res.hist.sum()) == N and int(res.hist[0]) == n
+    # decompress and check the bound everywhere, chunked
+    xo = s.decompress(res)
+    for a in range(0, x.shape[0], 64):
+        err = (xo[a:a + 64].double() - x[a:a + 64].double()).abs().max().item()
+        assert err <= res.eb_abs
+    n0, n1, n2 = x.shape
+    NB1, NB2 = math.ceil(n1 / 6), math.ceil(n2 / 6)
+    oidx = res.outlier_idx[:n].cpu().numpy().view(np.uint64)
+    oval = res.outlier_val[:n].cpu().numpy()
+    for a0, rows in [(0, 12), (510, 6), (1020, 4)]:
+        xs = x[a0:a0 + rows].cpu().numpy()
+        orc = oracle.compress(xs, cfg.eb, "rel", radius=cfg.radius, dim0_offset=a0, value_range_override=(lo, hi))
+        assert orc.eb_abs == res.eb_abs
+        b0, b1 = (a0 // 6) * NB1 * NB2, ((a0 + rows + 5) // 6) * NB1 * NB2
+        gc = res.coef_codes[b0:b1].cpu().numpy()
+        ex = orc.block_exempt.astype(bool)
+        assert np.array_equal(gc[~ex], orc.coef_codes[~ex])
+        codes = res.codes[a0:a0 + rows].cpu().numpy()
+        if not ex.any():
+            assert np.array_equal(codes, orc.codes)
+            sel = (oidx >= a0 * n1 * n2) & (oidx < (a0 + rows) * n1 * n2)
+            order = np.argsort(oidx[sel])
+            assert np.array_equal(oidx[sel][order], np.sort(orc.outlier_idx))
+            assert np.array_equal(oval[sel][order], orc.outlier_val[np.argsort(orc.outlier_idx)])
+            xd = xo[a0:a0 + rows].cpu().numpy()
+            assert np.array_equal(xd.view(np.uint8), orc.xprime.view(np.uint8))
+
+
+# ----------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+def test_degenerate_extents(flags):
+    rng = np.random.default_rng(5)
+    for dims in [(1, 1, 1), (1, 1, 7), (1, 7, 1), (7, 1, 1), (1, 6, 96), (6, 1, 100), (2, 2, 2)]:
+        f = rng.normal(size=dims).astype(np.float32)
+        check(f, 0.01, "abs", 32768, flags)
+
+
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+def test_nonfinite_inputs(flags):
+    f = np.linspace(-3, 3, 13 * 14 * 96, dtype=np.float32).reshape(13, 14, 96)
+    f[1, 2, 3] = np.nan
+    f[12, 13, 95] = np.inf
+    f[6, 6, 50] = -np.inf
+    rep = check(f, 1e-3, "abs", 32768, flags)
+    assert rep["counters"]["nonfinite_outliers"] == 3
+    x = torch.from_numpy(f).cuda()
+    with pytest.raises(Exception):
+        sz().compress(x, 1e-3, "rel")   # bad range (status bit 1)
+
+
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+def test_checkerboard_ties_and_linear_field(flags):
+    dims = (12, 18, 96)
+    i, j, k = np.meshgrid(*[np.arange(n) for n in dims], indexing="ij")
+    f = ((-1.0) ** (i + j + k)).astype(np.float32)
+    rep = check(f, 1.0, "abs", 32768, flags)
+    assert rep["counters"]["elem_near_ties"] == f.size
+    g = (0.5 + 0.25 * i - 0.125 * j + 0.0625 * k).astype(np.float32)
+    x = torch.from_numpy(g).cuda()
+    res = sz().compress(x, 1e-2, "rel")
+    assert bool((res.codes.long() == 32768).all())
+
+
+def test_outlier_overflow_and_small_radius():
+    rng = np.random.default_rng(3)
+    f = rng.normal(size=(24, 24, 96)).astype(np.float32)
+    x = torch.from_numpy(f).cuda()
+    with pytest.raises(Exception, match="capacity"):
+        sz().compress(x, 1e-4, "rel", radius=4, outlier_cap=10)
+    rep = check(f, 1e-3, "rel", 4)
+    assert rep["outliers"] > 1000
+
+
+def test_invalid_arguments():
+    s = sz()
+    x = torch.zeros((0, 4, 4), device="cuda")
+    with pytest.raises(Exception):
+        s.compress(x, 1e-3, "abs")
+    y = torch.ones((6, 6, 6), device="cuda")
+    with pytest.raises(Exception):
+        s.compress(y, -1.0, "abs")
+    with pytest.raises(Exception):
+        s.compress(y, 1e-3, "abs", radius=40000)
+
+
+def test_value_range_and_histogram_standalone():
+    s = sz()
+    rng = np.random.default_rng(0)
+    for dt in (np.float32, np.float64):
+        f = rng.normal(size=(37, 11, 7)).astype(dt)
+        mm = s.value_range(torch.from_numpy(f).cuda()).cpu().numpy()
+        assert mm[0] == f.min() and mm[1] == f.max()
+    for R in (1, 4, 100, 32768):
+        codes = rng.integers(0, 2 * R, size=1_000_003).astype(np.uint16)
+        h = s.histogram(torch.from_numpy(codes).cuda(), R).cpu().numpy()
+        assert np.array_equal(h, np.bincount(codes, minlength=2 * R))
+
+
+def test_gpu_slab_invariance():
+    """Block-aligned slabs with dim0_offset and the global range reproduce the whole-field output."""
+    s = sz()
+    from synth import make_field
+    x = make_field("c2", device="cuda", shape=(48, 64, 96))
+    whole = s.compress(x, 1e-4, "rel", coef_raw=False)
+    mm = s.value_range(x)
+    codes, hist = [], torch.zeros_like(whole.hist)
+    for a, b in [(0, 12), (12, 30), (30, 48)]:
+        part = s.regression_compress(x[a:b].contiguous(), 1e-4, "rel", d_minmax=mm, dim0_offset=a)
+        part.finalize()
+        codes.append(part.codes.clone())
+        hist += part.hist
+    assert torch.equal(torch.cat(codes), whole.codes)
+    assert torch.equal(hist, whole.hist)
