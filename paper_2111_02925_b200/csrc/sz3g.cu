@@ -18,6 +18,7 @@
 #include <type_traits>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -131,14 +132,18 @@ struct KArgs {
   const double* d_minmax;
   double* d_eb_abs;
   int32_t* d_status;
+  double uround;  // fast-verify roundoff constant of T
+  uint32_t pf;    // L2 prefetch distance of the TMA producers, tiles per CTA
 };
 
 __device__ __forceinline__ void hist_init(HistSmem& hs, uint32_t* win, uint32_t* zero, uint32_t R) {
   hs.win = win;
   hs.zero = zero;
   hs.dummy = zero + 1;  // 32 sink slots follow the zero-bin counter
-  hs.nwin = min(2u * R, (uint32_t)HWIN);
-  hs.lo = (2u * R <= (uint32_t)HWIN) ? 0u : R - HWIN / 2;
+  // window of codes counted in shared memory: [lo, lo + nwin), lo >= 1 so code 0 (outliers) is
+  // always outside it and goes through the zero counter
+  hs.lo = (2u * R - 1u <= (uint32_t)HWIN) ? 1u : R - HWIN / 2;
+  hs.nwin = min(2u * R - 1u, (uint32_t)HWIN);
   for (uint32_t b = threadIdx.x; b < hs.nwin; b += blockDim.x) win[b] = 0u;
   if (threadIdx.x == 0) *zero = 0u;
 }
@@ -155,7 +160,7 @@ __device__ __forceinline__ void hist_flush(const HistSmem& hs, unsigned long lon
 __device__ __forceinline__ bool cta_consts(const KArgs& a, Consts* s_k, int* s_ok) {
   if (threadIdx.x == 0) {
     Consts K;
-    const bool ok = make_consts(a.eb_mode, a.eb, a.d_minmax, K);
+    const bool ok = make_consts(a.eb_mode, a.eb, a.d_minmax, a.uround, K);
     *s_ok = ok;
     if (ok) *s_k = K;
     if (blockIdx.x == 0) {
@@ -231,30 +236,52 @@ __global__ void __launch_bounds__(128) k_compress_plain(const T* __restrict__ x,
 }
 
 // ---------------------------------------------------------------------------------- compress, TMA
-template <typename T, int W, int S>
+// Persistent, one CTA per SM.  Warp NG*G is the producer (one elected lane streams 6x6x96 tiles with
+// TMA).  The other NG*G warps form NG groups of G warps; a group takes one tile at a time (group g:
+// the CTA's tiles g, g+NG, ...), each warp owning P = 6/G i-planes.  Every group has a private
+// D-deep mbarrier ring (stage s = g*D + slot): a stage has exactly one consumer, which visits it in
+// order, so a waiter can never be two phases ahead of the barrier (a ring shared round-robin by
+// independent consumers lets a fast consumer's parity wait match the *previous* phase).
+// Sharing a stage across a group keeps ~4 warps per scheduler resident (the fp64/convert stream of
+// one warp issues well below 1 IPC) within the 227 KiB of shared memory.
+//   per tile: wait full -> partial moments -> exchange (named barrier B1) -> coefficients ->
+//   quantise own planes into the group's code buffer -> rare path -> B2 -> warp 0: release the
+//   stage, TMA-store the code tile (or copy rows when no TMA store applies).
+template <typename T, int G, int NG, int D>
 struct CompressSmem {
+  static constexpr int P = BS / G;
+  static constexpr int S = NG * D;
   static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
   static constexpr size_t code_bytes = sizeof(uint16_t) * TILE_ELEMS;
   static constexpr size_t off_codes = S * stage_bytes;
-  static constexpr size_t off_hist = off_codes + W * code_bytes;
+  static constexpr size_t off_exch = off_codes + NG * code_bytes;
+  static constexpr size_t off_hist = off_exch + (size_t)NG * G * 4 * 32 * sizeof(double);
   static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (HWIN + 36);
   static constexpr size_t off_k = off_bar + 2 * S * sizeof(uint64_t);
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
 };
 
-template <typename T, int W, int S, bool HIST>
-__global__ void __launch_bounds__((W + 1) * 32, 1)
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename T, int G, int NG, int D, bool HIST>
+__global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     k_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, int codes_tma,
                    KArgs a, CompressOut<T> o) {
-  using L = CompressSmem<T, W, S>;
+  using L_ = CompressSmem<T, G, NG, D>;
+  constexpr int P = L_::P;
+  constexpr int S = L_::S;
+  static_assert(BS % G == 0, "G must divide 6");
   extern __shared__ __align__(128) uint8_t smem[];
   T* stages = reinterpret_cast<T*>(smem);
-  uint16_t* cbuf = reinterpret_cast<uint16_t*>(smem + L::off_codes);
-  uint32_t* s_win = reinterpret_cast<uint32_t*>(smem + L::off_hist);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint16_t* cbuf = reinterpret_cast<uint16_t*>(smem + L_::off_codes);
+  double* exch = reinterpret_cast<double*>(smem + L_::off_exch);
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(smem + L_::off_hist);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
   uint64_t* empty = full + S;
-  Consts* s_k = reinterpret_cast<Consts*>(smem + L::off_k);
-  int* s_ok = reinterpret_cast<int*>(smem + L::off_k + sizeof(Consts));
+  Consts* s_k = reinterpret_cast<Consts*>(smem + L_::off_k);
+  int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   HistSmem hs;
   hist_init(hs, s_win, s_win + HWIN, a.R);
@@ -267,51 +294,81 @@ __global__ void __launch_bounds__((W + 1) * 32, 1)
   }
   if (!cta_consts(a, s_k, s_ok)) return;
   const Geo& g = a.g;
-  const uint64_t G = gridDim.x;
-  if (warp == W) {
-    // ---------------- producer: one elected lane streams tiles into the ring
+  const uint64_t Gr = gridDim.x;
+  if (warp == NG * G) {
+    // ---------------- producer
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_x);
-      uint32_t n = 0;
-      for (uint64_t t = blockIdx.x; t < g.ntiles; t += G, n++) {
-        const uint32_t s = n % S, ph = (n / S) & 1u;
-        ptx::mbar_wait(&empty[s], ph ^ 1u);
+      for (uint64_t p = 0, t = blockIdx.x; p < a.pf && t < g.ntiles; p++, t += Gr) {
         const TileCoord tc = decode_tile(t, g);
-        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L::stage_bytes);
+        ptx::tma_prefetch_3d(&tm_x, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+      }
+      uint32_t n = 0;
+      for (uint64_t t = blockIdx.x; t < g.ntiles; t += Gr, n++) {
+        const uint64_t tp = t + (uint64_t)a.pf * Gr;
+        if (a.pf && tp < g.ntiles) {
+          const TileCoord tq = decode_tile(tp, g);
+          ptx::tma_prefetch_3d(&tm_x, (int)(tq.c * TK), (int)(tq.b * BS), (int)(tq.a * BS));
+        }
+        const uint32_t k = n / NG, s = (n % NG) * D + k % D, ph = (k / D) & 1u;
+        ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
+        const TileCoord tc = decode_tile(t, g);
+        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L_::stage_bytes);
         ptx::tma_load_3d(stages + (size_t)s * TILE_ELEMS, &tm_x, &full[s], (int)(tc.c * TK), (int)(tc.b * BS),
                          (int)(tc.a * BS));
       }
     }
   } else {
-    // ---------------- consumers: warp w takes the CTA's tiles w, w+W, ...
+    // ---------------- consumer groups
+    const int grp = warp / G, wg = warp - grp * G, i0 = wg * P;
+    const int bar_id = 1 + grp;
     const Consts K = *s_k;
-    uint16_t* mycodes = cbuf + (size_t)warp * TILE_ELEMS;
-    uint32_t n = warp;
-    for (uint64_t t = blockIdx.x + (uint64_t)warp * G; t < g.ntiles; t += (uint64_t)W * G, n += W) {
-      const uint32_t s = n % S, ph = (n / S) & 1u;
+    uint16_t* mycodes = cbuf + (size_t)grp * TILE_ELEMS;
+    double* myexch = exch + (size_t)grp * G * 4 * 32;
+    uint32_t k = 0;
+    for (uint64_t t = blockIdx.x + (uint64_t)grp * Gr; t < g.ntiles; t += (uint64_t)NG * Gr, k++) {
+      const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
       const TileCoord tc = decode_tile(t, g);
-      if (codes_tma) {
-        if (lane == 0) ptx::bulk_wait_read0();  // previous TMA store finished reading mycodes
-        __syncwarp();
-      }
+      const LaneGeom L = lane_geom(tc, g);
+      const bool full_tile = tile_full(tc, g);
+      if (codes_tma && wg == 0 && lane == 0) ptx::bulk_wait_read0();  // previous store done reading mycodes
       ptx::mbar_wait(&full[s], ph);
       const T* xs = stages + (size_t)s * TILE_ELEMS;
-      compress_tile_dispatch<T, true, HIST>(xs, BS * TK, TK, mycodes, BS * TK, TK, tc, g, K, a.R, o, hs);
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[s]);
-      if (codes_tma) {
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          ptx::tma_store_3d(&tm_c, mycodes, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
-          ptx::bulk_commit();
+      double V[4];
+      moments_partial<T, true, P>(xs, BS * TK, TK, i0, L, V);
+#pragma unroll
+      for (int d = 0; d < 4; d++) myexch[(wg * 4 + d) * 32 + lane] = V[d];
+      named_bar_sync(bar_id, G * 32);  // B1
+#pragma unroll
+      for (int d = 0; d < 4; d++) {
+        double acc = myexch[d * 32 + lane];
+#pragma unroll
+        for (int w = 1; w < G; w++) acc += myexch[(w * 4 + d) * 32 + lane];
+        V[d] = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+      }
+      double beta[4], bh[4];
+      int32_t cc[4];
+      block_coefs(V, L, K, beta, cc, bh);
+      if (wg == 0) write_coefs(o, tc, g, L, cc, beta);
+      uint32_t umax;
+      if (full_tile) umax = quantize_planes<T, true, HIST, true, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, i0, L, bh, K, a.R, hs);
+      else umax = quantize_planes<T, true, HIST, false, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, i0, L, bh, K, a.R, hs);
+      rare_path<T, HIST, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, i0, L, umax, tc, g, o, hs);
+      if (codes_tma) ptx::fence_proxy_async_smem();
+      named_bar_sync(bar_id, G * 32);  // B2: codes complete, stage no longer read
+      if (wg == 0) {
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        if (codes_tma) {
+          if (lane == 0) {
+            ptx::tma_store_3d(&tm_c, mycodes, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+            ptx::bulk_commit();
+          }
+        } else {
+          store_code_rows(mycodes, o.codes, tc, g);
         }
-      } else {
-        store_code_rows(mycodes, o.codes, tc, g);
-        __syncwarp();
       }
     }
-    if (codes_tma && lane == 0) ptx::bulk_wait0();
+    if (codes_tma && wg == 0 && lane == 0) ptx::bulk_wait0();
   }
   __syncthreads();
   if (HIST) hist_flush(hs, o.hist);
@@ -337,8 +394,9 @@ __global__ void __launch_bounds__(128) k_decompress_plain(const uint16_t* __rest
   }
 }
 
-template <typename T, int W, int S>
+template <typename T, int W, int D>
 struct DecompressSmem {
+  static constexpr int S = W * D;
   static constexpr size_t stage_bytes = sizeof(uint16_t) * TILE_ELEMS;
   static constexpr size_t out_bytes = sizeof(T) * TILE_ELEMS;
   static constexpr size_t off_out = S * stage_bytes;
@@ -347,11 +405,13 @@ struct DecompressSmem {
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
 };
 
-template <typename T, int W, int S>
+// Same producer / private-ring structure as k_compress_tma with single-warp consumers.
+template <typename T, int W, int D>
 __global__ void __launch_bounds__((W + 1) * 32, 1)
     k_decompress_tma(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_x,
                      const int32_t* __restrict__ coef, KArgs a) {
-  using L = DecompressSmem<T, W, S>;
+  using L = DecompressSmem<T, W, D>;
+  constexpr int S = L::S;
   extern __shared__ __align__(128) uint8_t smem[];
   uint16_t* stages = reinterpret_cast<uint16_t*>(smem);
   T* obuf = reinterpret_cast<T*>(smem + L::off_out);
@@ -373,10 +433,19 @@ __global__ void __launch_bounds__((W + 1) * 32, 1)
   if (warp == W) {
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_c);
+      for (uint64_t p = 0, t = blockIdx.x; p < a.pf && t < g.ntiles; p++, t += G) {
+        const TileCoord tc = decode_tile(t, g);
+        ptx::tma_prefetch_3d(&tm_c, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+      }
       uint32_t n = 0;
       for (uint64_t t = blockIdx.x; t < g.ntiles; t += G, n++) {
-        const uint32_t s = n % S, ph = (n / S) & 1u;
-        ptx::mbar_wait(&empty[s], ph ^ 1u);
+        const uint64_t tp = t + (uint64_t)a.pf * G;
+        if (a.pf && tp < g.ntiles) {
+          const TileCoord tq = decode_tile(tp, g);
+          ptx::tma_prefetch_3d(&tm_c, (int)(tq.c * TK), (int)(tq.b * BS), (int)(tq.a * BS));
+        }
+        const uint32_t k = n / W, s = (n % W) * D + k % D, ph = (k / D) & 1u;
+        ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
         const TileCoord tc = decode_tile(t, g);
         ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L::stage_bytes);
         ptx::tma_load_3d(stages + (size_t)s * TILE_ELEMS, &tm_c, &full[s], (int)(tc.c * TK), (int)(tc.b * BS),
@@ -386,9 +455,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 1)
   } else {
     const Consts K = *s_k;
     T* myout = obuf + (size_t)warp * TILE_ELEMS;
-    uint32_t n = warp;
-    for (uint64_t t = blockIdx.x + (uint64_t)warp * G; t < g.ntiles; t += (uint64_t)W * G, n += W) {
-      const uint32_t s = n % S, ph = (n / S) & 1u;
+    uint32_t k = 0;
+    for (uint64_t t = blockIdx.x + (uint64_t)warp * G; t < g.ntiles; t += (uint64_t)W * G, k++) {
+      const uint32_t s = warp * D + k % D, ph = (k / D) & 1u;
       const TileCoord tc = decode_tile(t, g);
       if (lane == 0) ptx::bulk_wait_read0();
       __syncwarp();
@@ -431,6 +500,7 @@ __global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ 
     if (c >= nb) return;
     const uint32_t w = c - hs.lo;
     if (w < hs.nwin) atomicAdd(&s_win[w], 1u);
+    else if (c == 0u) atomicAdd(hs.zero, 1u);
     else atomicAdd(&hist[c], 1ull);
   };
   uint64_t done = 0;
@@ -550,39 +620,48 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 }
 
 // tuned configurations: (consumer warps, ring stages); smem fits the 227 KiB per-CTA limit
-constexpr int CW32 = 8, CS32 = 10;   // f32 compress: 10 x 13.5 KiB stages + 8 x 6.75 KiB codes + 32 KiB hist
-constexpr int CW64 = 4, CS64 = 6;    // f64 compress: 6 x 27 KiB + 4 x 6.75 KiB + 32 KiB
-constexpr int DW32 = 8, DS32 = 12;   // f32 decompress: 12 x 6.75 KiB + 8 x 13.5 KiB
-constexpr int DW64 = 6, DS64 = 8;    // f64 decompress: 8 x 6.75 KiB + 6 x 27 KiB
+constexpr int PF_TILES = 16;        // default L2 prefetch distance of the TMA producers (tiles per CTA)
 
-template <typename T, int W, int S, bool HIST>
+uint32_t prefetch_tiles() {  // SZ3G_PF overrides (tuning only)
+  static uint32_t v = [] {
+    const char* e = getenv("SZ3G_PF");
+    return e ? (uint32_t)atoi(e) : (uint32_t)PF_TILES;
+  }();
+  return v;
+}
+constexpr int CG32 = 3, CN32 = 5, CD32 = 2;  // f32 compress: 5 groups x 3 warps + producer = 16 warps; 2 x 13.5 KiB stages per group
+constexpr int CG64 = 6, CN64 = 2, CD64 = 2;  // f64 compress: 2 groups x 6 warps + producer = 13 warps; 2 x 27 KiB stages per group
+constexpr int DW32 = 8, DD32 = 2;   // f32 decompress: 8 warps x 2 x 6.75 KiB code stages + 8 x 13.5 KiB output tiles
+constexpr int DW64 = 5, DD64 = 2;   // f64 decompress: 5 warps x 2 x 6.75 KiB + 5 x 27 KiB
+
+template <typename T, int G, int NG, int D, bool HIST>
 int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
                         const CompressOut<T>& co, cudaStream_t st) {
-  using L = CompressSmem<T, W, S>;
+  using L = CompressSmem<T, G, NG, D>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mx, mc;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
   memset(&mc, 0, sizeof(mc));
   if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) codes_tma = false;
-  auto kern = k_compress_tma<T, W, S, HIST>;
+  auto kern = k_compress_tma<T, G, NG, D, HIST>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
-  kern<<<(unsigned)grid, (W + 1) * 32, L::total, st>>>(mx, mc, codes_tma ? 1 : 0, ka, co);
+  kern<<<(unsigned)grid, (NG * G + 1) * 32, L::total, st>>>(mx, mc, codes_tma ? 1 : 0, ka, co);
   return check_launch(1);
 }
 
-template <typename T, int W, int S>
+template <typename T, int W, int D>
 int launch_decompress_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, void* xo, const KArgs& ka,
                           cudaStream_t st) {
-  using L = DecompressSmem<T, W, S>;
+  using L = DecompressSmem<T, W, D>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mc, mx;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) return SZ3G_ECUDA;
   if (!make_map(&mx, dt, sizeof(T), xo, g)) return SZ3G_ECUDA;
-  auto kern = k_decompress_tma<T, W, S>;
+  auto kern = k_decompress_tma<T, W, D>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
@@ -635,6 +714,8 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
   ka.d_minmax = d_minmax;
   ka.d_eb_abs = d_eb_abs;
   ka.d_status = d_status;
+  ka.pf = prefetch_tiles();
+  ka.uround = grid->dtype == SZ3G_F32 ? (5.9604644775390625e-08 + 1.12e-16) : 2.3e-16;
   const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
   const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
   const bool tma = !generic && map_ok(x, es, g);
@@ -643,16 +724,16 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
   if (grid->dtype == SZ3G_F32) {
     CompressOut<float> co{codes, coef_codes, coef_raw, outlier_idx, (float*)outlier_val, outlier_cap,
                           d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
-    if (tma) return use_hist ? launch_compress_tma<float, CW32, CS32, true>(g, x, codes, codes_tma, ka, co, st)
-                         : launch_compress_tma<float, CW32, CS32, false>(g, x, codes, codes_tma, ka, co, st);
+    if (tma) return use_hist ? launch_compress_tma<float, CG32, CN32, CD32, true>(g, x, codes, codes_tma, ka, co, st)
+                         : launch_compress_tma<float, CG32, CN32, CD32, false>(g, x, codes, codes_tma, ka, co, st);
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
     if (use_hist) k_compress_plain<float, true><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
     else k_compress_plain<float, false><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
   } else {
     CompressOut<double> co{codes, coef_codes, coef_raw, outlier_idx, (double*)outlier_val, outlier_cap,
                            d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
-    if (tma) return use_hist ? launch_compress_tma<double, CW64, CS64, true>(g, x, codes, codes_tma, ka, co, st)
-                         : launch_compress_tma<double, CW64, CS64, false>(g, x, codes, codes_tma, ka, co, st);
+    if (tma) return use_hist ? launch_compress_tma<double, CG64, CN64, CD64, true>(g, x, codes, codes_tma, ka, co, st)
+                         : launch_compress_tma<double, CG64, CN64, CD64, false>(g, x, codes, codes_tma, ka, co, st);
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
     if (use_hist) k_compress_plain<double, true><<<blocks, 128, 0, st>>>((const double*)x, ka, co);
     else k_compress_plain<double, false><<<blocks, 128, 0, st>>>((const double*)x, ka, co);
@@ -679,6 +760,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   ka.R = params->radius;
   ka.eb_mode = 0;
   ka.eb = params->eb;
+  ka.pf = prefetch_tiles();
   int32_t* dummy_status = nullptr;  // decompress never reports: eb validated on the host
   ka.d_status = dummy_status;
   const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
@@ -688,7 +770,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   int launched = 0;
   if (grid->dtype == SZ3G_F32) {
     if (tma) {
-      rc = launch_decompress_tma<float, DW32, DS32>(g, codes, coef_codes, x_out, ka, st);
+      rc = launch_decompress_tma<float, DW32, DD32>(g, codes, coef_codes, x_out, ka, st);
       if (rc) return rc;
     } else {
       const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
@@ -703,7 +785,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
     }
   } else {
     if (tma) {
-      rc = launch_decompress_tma<double, DW64, DS64>(g, codes, coef_codes, x_out, ka, st);
+      rc = launch_decompress_tma<double, DW64, DD64>(g, codes, coef_codes, x_out, ka, st);
       if (rc) return rc;
     } else {
       const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));

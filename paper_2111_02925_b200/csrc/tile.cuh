@@ -30,6 +30,7 @@ constexpr double I2D_MAGIC = 4503599627370496.0;   // 2^52
 
 struct Consts {
   double eb_abs, twoeb, inv2eb, w0, ws, inv_w0, inv_ws;
+  double vc, vthr;  // fast verify: |t - q| + vc*|x| <= vthr  implies  |(T)(p + 2eb q) - x| <= eb
 };
 
 struct Geo {
@@ -40,7 +41,8 @@ struct Geo {
 };
 
 // O1/O2 on device: same operations as the definition (IEEE division for the constants).
-__device__ __forceinline__ bool make_consts(int eb_mode, double eb, const double* d_minmax, Consts& K) {
+// `uround` is the fast-verify roundoff constant of T (2^-24 + 1.12e-16 for f32, 2.3e-16 for f64).
+__device__ __forceinline__ bool make_consts(int eb_mode, double eb, const double* d_minmax, double uround, Consts& K) {
   double eb_abs = eb;
   if (eb_mode == 1) eb_abs = __dmul_rn(eb, __dsub_rn(d_minmax[1], d_minmax[0]));
   if (!(isfinite(eb_abs) && eb_abs > 0.0)) return false;
@@ -51,6 +53,14 @@ __device__ __forceinline__ bool make_consts(int eb_mode, double eb, const double
   K.ws = __ddiv_rn(eb_abs, 2.0 * BS);
   K.inv_w0 = __ddiv_rn(1.0, K.w0);
   K.inv_ws = __ddiv_rn(1.0, K.ws);
+  // Fast verify (O9 without forming x'): for |t| < 32768, q = rint(t), y = fl(p + fl(2eb q)),
+  //   |r/(2eb) - t| <= 3.4e-16 |t|  (r = x - p),   |x - y| <= 2eb (|t - q| + 1.5e-11) + 1.2e-16 |y|,
+  //   |(T)y - y| <= 2^-24 |y| (f32; 0 for f64),  |d| <= |(T)y - x| (1 + 1.2e-16),  |y| <= |x| + 1.01 eb,
+  // hence  |t - q| + c |x| <= 0.5 - 1e-10 - 1.02 c eb  with  c = 1.01 uround / (2 eb)  implies  |d| <= eb.
+  // (t - q is exact: Sterbenz.)  Elements failing the test take the exact O9 path.  For f32 with a
+  // huge eb, (T)y could overflow to inf: the fast test is disabled there.
+  K.vc = 1.01 * uround / K.twoeb;
+  K.vthr = (uround > 1e-12 && eb_abs > 1e30) ? -1.0 : 0.5 - 1e-10 - 1.02 * K.vc * eb_abs;
   return true;
 }
 
@@ -77,12 +87,14 @@ struct TileCoord {
   uint32_t a, b, c;  // block-row index along dim0, dim1; tile index along dim2
 };
 
-__device__ __forceinline__ TileCoord decode_tile(uint64_t t, const Geo& g) {
+// tile index -> coordinates (32-bit: the host guarantees ntiles < 2^32)
+__device__ __forceinline__ TileCoord decode_tile(uint64_t t64, const Geo& g) {
+  const uint32_t t = (uint32_t)t64;
   TileCoord tc;
-  tc.c = (uint32_t)(t % g.NT2);
-  uint64_t r = t / g.NT2;
-  tc.b = (uint32_t)(r % g.NB1);
-  tc.a = (uint32_t)(r / g.NB1);
+  const uint32_t r = t / g.NT2;
+  tc.c = t - r * g.NT2;
+  tc.a = r / g.NB1;
+  tc.b = r - tc.a * g.NB1;
   return tc;
 }
 
@@ -107,229 +119,325 @@ struct HistSmem {
   uint32_t nwin;   // bins actually used (min(2R, HWIN))
 };
 
+
+// ------------------------------------------------------------------------------------------
+// Compress, in pieces.  A tile's input is addressed as xs[i*si + j*sj + k] (k in [0,96)): either a
+// shared-memory stage (si = 576, sj = 96; zero outside the grid) or the global field (IN_SMEM =
+// false: loads predicated on the grid bounds).  Codes go to cs[i*ci + j*cj + k] likewise.  A warp
+// handles the tile's i-planes [i0, i0 + P): P = 6 for one warp per tile, P = 6/G when a group of G
+// warps shares a tile (the partial moments are then summed across the group through shared memory).
+// ------------------------------------------------------------------------------------------
+struct LaneGeom {
+  int h, kcol;        // half of the block (0/1), first tile column of this lane
+  uint32_t kb;        // block index along dim 2
+  int m0, m1, m2;     // block extents (m2 = 0: no block for this lane)
+  bool kv0, kv1, kv2; // validity of the lane's three columns
+  __device__ __forceinline__ bool kv(int kk) const { return kk == 0 ? kv0 : (kk == 1 ? kv1 : kv2); }
+};
+
+__device__ __forceinline__ LaneGeom lane_geom(const TileCoord tc, const Geo& g) {
+  const int lane = threadIdx.x & 31;
+  LaneGeom L;
+  const int bl = lane >> 1;
+  L.h = lane & 1;
+  L.kb = tc.c * 16u + (uint32_t)bl;
+  L.m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
+  L.m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
+  L.m2 = (L.kb < g.NB2) ? (int)umin64(BS, g.n2 - (uint64_t)L.kb * BS) : 0;
+  L.kcol = 6 * bl + 3 * L.h;
+  L.kv0 = 3 * L.h + 0 < L.m2;
+  L.kv1 = 3 * L.h + 1 < L.m2;
+  L.kv2 = 3 * L.h + 2 < L.m2;
+  return L;
+}
+
 // every element of the tile lies inside the grid (warp-uniform)
 __device__ __forceinline__ bool tile_full(const TileCoord tc, const Geo& g) {
   return (uint64_t)(tc.a + 1) * BS <= g.n0 && (uint64_t)(tc.b + 1) * BS <= g.n1 && (uint64_t)(tc.c + 1) * TK <= g.n2;
 }
 
-// ------------------------------------------------------------------------------------------
-// Compress one tile.  `xs` + (si, sj) address the tile's input: element (i,j,k) of the tile at
-// xs[i*si + j*sj + k] (k in [0,96)); it is either a shared-memory stage (si = 576, sj = 96, all
-// 3456 entries valid, zero outside the grid) or the global field itself (IN_SMEM = false: loads
-// are predicated on the grid bounds).  Codes go to `cs` + (ci, cj) likewise (shared staging
-// buffer or the global code array).
-// ------------------------------------------------------------------------------------------
-template <typename T, bool IN_SMEM, bool HIST, bool FULL>
-__device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj,
-                                              uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
-                                              const TileCoord tc, const Geo& g, const Consts& K,
-                                              const uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
-  const int lane = threadIdx.x & 31;
-  const int bl = lane >> 1, h = lane & 1;
-  const uint32_t kb = tc.c * 16u + (uint32_t)bl;          // block index along dim 2
-  const int m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
-  const int m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
-  const int m2 = (kb < g.NB2) ? (int)umin64(BS, g.n2 - (uint64_t)kb * BS) : 0;
-  const int kcol = 6 * bl + 3 * h;                        // first tile column of this lane
-  // validity of the lane's three columns
-  const bool kv0 = 3 * h + 0 < m2, kv1 = 3 * h + 1 < m2, kv2 = 3 * h + 2 < m2;
-
-  // ---------------- O4: moments V0, Vx, Vy, Vz (fp64).  Row sums S = f0+f1+f2 and the lane's
-  // k-weighted sum K = f1 + 2 f2 first, then P_i = sum_j S, Q_i = sum_j j S, Z_i = sum_j K.
+// O4 partial moments of the lane's three columns over i-planes [i0, i0+P) (fp64).  Row sums
+// S = f0+f1+f2 and the lane-local k-weighted sum f1 + 2 f2 first; P_i = sum_j S, Q_i = sum_j j S,
+// Z_i = sum_j (f1 + 2 f2).  Vz includes the lane's column offset 3h inside the block.
+template <typename T, bool IN_SMEM, int P>
+__device__ __forceinline__ void moments_partial(const T* __restrict__ xs, uint64_t si, uint64_t sj, int i0,
+                                                const LaneGeom& L, double V[4]) {
   double V0 = 0.0, Vx = 0.0, Vy = 0.0, Vz = 0.0;
+  double di = (double)i0;
 #pragma unroll 1
-  for (int i = 0; i < BS; i++) {
-    double P = 0.0, Q = 0.0, Z = 0.0;
+  for (int ii = 0; ii < P; ii++, di += 1.0) {
+    const int i = i0 + ii;
+    double Ps = 0.0, Q = 0.0, Z = 0.0;
+    const T* plane = IN_SMEM ? xs + (uint32_t)(i * BS * TK + L.kcol) : xs + (uint64_t)i * si + L.kcol;
 #pragma unroll
     for (int j = 0; j < BS; j++) {
-      const T* row = xs + i * si + j * sj + kcol;
+      const T* row = IN_SMEM ? plane + j * TK : plane + (uint64_t)j * sj;
       double f0, f1, f2;
       if (IN_SMEM) {
         f0 = to_d<T>(row[0]); f1 = to_d<T>(row[1]); f2 = to_d<T>(row[2]);
       } else {
-        const bool rv = (i < m0) && (j < m1);
-        f0 = (rv && kv0) ? to_d<T>(row[0]) : 0.0;
-        f1 = (rv && kv1) ? to_d<T>(row[1]) : 0.0;
-        f2 = (rv && kv2) ? to_d<T>(row[2]) : 0.0;
+        const bool rv = (i < L.m0) && (j < L.m1);
+        f0 = (rv && L.kv0) ? to_d<T>(row[0]) : 0.0;
+        f1 = (rv && L.kv1) ? to_d<T>(row[1]) : 0.0;
+        f2 = (rv && L.kv2) ? to_d<T>(row[2]) : 0.0;
       }
       const double S = (f0 + f1) + f2;
       const double Kw = fma(2.0, f2, f1);
-      P += S;
+      Ps += S;
       Q = fma((double)j, S, Q);
       Z += Kw;
     }
-    V0 += P;
-    Vx = fma((double)i, P, Vx);
+    V0 += Ps;
+    Vx = fma(di, Ps, Vx);
     Vy += Q;
     Vz += Z;
   }
-  Vz = fma(3.0 * h, V0, Vz);
-  V0 += __shfl_xor_sync(0xffffffffu, V0, 1);
-  Vx += __shfl_xor_sync(0xffffffffu, Vx, 1);
-  Vy += __shfl_xor_sync(0xffffffffu, Vy, 1);
-  Vz += __shfl_xor_sync(0xffffffffu, Vz, 1);
+  V[0] = V0;
+  V[1] = Vx;
+  V[2] = Vy;
+  V[3] = fma(3.0 * L.h, V0, Vz);
+}
 
-  // ---------------- O5: Lemma 1; extent-1 axis -> slope 0 (G2)
-  const bool blk_ok = m2 > 0 && m0 > 0 && m1 > 0;
-  double beta[4] = {0.0, 0.0, 0.0, 0.0};
-  if (blk_ok) {
-    const double Nb = (double)(m0 * m1 * m2);
+// O5 (Lemma 1; extent-1 axis -> slope 0, G2) + O6 (codes; bins eb/2, eb/12, G1; zero
+// predictor fallback) from the full block moments; returns the decoded coefficients (bit-exact).
+__device__ __forceinline__ void block_coefs(const double V[4], const LaneGeom& L, const Consts& K, double beta[4],
+                                            int32_t cc[4], double bh[4]) {
+  beta[0] = beta[1] = beta[2] = beta[3] = 0.0;
+  if (L.m2 > 0) {
+    const double Nb = (double)(L.m0 * L.m1 * L.m2);
     const double invNb = __drcp_rn(Nb);
-    const double Vd[3] = {Vx, Vy, Vz};
-    const int md[3] = {m0, m1, m2};
+    const int md[3] = {L.m0, L.m1, L.m2};
 #pragma unroll
     for (int d = 0; d < 3; d++) {
       if (md[d] > 1) {
         const double sc = c_lemma[md[d]][0] * invNb;
-        const double inner = fma(Vd[d], c_lemma[md[d]][1], -V0);
+        const double inner = fma(V[d + 1], c_lemma[md[d]][1], -V[0]);
         beta[d + 1] = sc * inner;
       }
     }
-    beta[0] = V0 * invNb - ((m0 - 1) * 0.5 * beta[1] + (m1 - 1) * 0.5 * beta[2] + (m2 - 1) * 0.5 * beta[3]);
+    beta[0] = V[0] * invNb - ((L.m0 - 1) * 0.5 * beta[1] + (L.m1 - 1) * 0.5 * beta[2] + (L.m2 - 1) * 0.5 * beta[3]);
   }
-  // ---------------- O6: coefficient codes (bins eb/2, eb/12; G1), zero predictor fallback
-  int32_t cc[4];
-  {
-    double r[4];
-    bool bad = false;
+  // rint by the 1.5*2^52 add/sub (exact for |u| < 2^51; larger, Inf or NaN fail the range test)
+  double r[4], sm[4];
+  bool bad = false;
 #pragma unroll
-    for (int d = 0; d < 4; d++) {
-      r[d] = rint(beta[d] * (d == 0 ? K.inv_w0 : K.inv_ws));
-      bad |= !(fabs(r[d]) <= 2147483647.0);
-    }
-#pragma unroll
-    for (int d = 0; d < 4; d++) cc[d] = bad ? 0 : __double2int_rn(r[d]);
+  for (int d = 0; d < 4; d++) {
+    sm[d] = __dadd_rn(beta[d] * (d == 0 ? K.inv_w0 : K.inv_ws), RINT_MAGIC);
+    r[d] = __dsub_rn(sm[d], RINT_MAGIC);
+    bad |= !(fabs(r[d]) <= 2147483647.0);
   }
-  const double bh0 = __dmul_rn((double)cc[0], K.w0);
-  const double bh1 = __dmul_rn((double)cc[1], K.ws);
-  const double bh2 = __dmul_rn((double)cc[2], K.ws);
-  const double bh3 = __dmul_rn((double)cc[3], K.ws);
-  const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + kb;
-  if (blk_ok && h == 0) {
+  // (double)c == r exactly when c is representable, so b^ = c * w needs no int->fp conversion
+#pragma unroll
+  for (int d = 0; d < 4; d++) {
+    cc[d] = bad ? 0 : __double2loint(sm[d]);
+    bh[d] = bad ? 0.0 : __dmul_rn(r[d], d == 0 ? K.w0 : K.ws);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void write_coefs(const CompressOut<T>& o, const TileCoord tc, const Geo& g,
+                                            const LaneGeom& L, const int32_t cc[4], const double beta[4]) {
+  if (L.m2 > 0 && L.h == 0) {
+    const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
     reinterpret_cast<int4*>(o.coef)[bid] = make_int4(cc[0], cc[1], cc[2], cc[3]);
     if (o.coef_raw) {
       reinterpret_cast<double2*>(o.coef_raw)[2 * bid] = make_double2(beta[0], beta[1]);
       reinterpret_cast<double2*>(o.coef_raw)[2 * bid + 1] = make_double2(beta[2], beta[3]);
     }
   }
+}
 
-  // ---------------- O7-O11 per element, branch-free: 18 independent elements per j (3 k-columns x
-  // 6 i-planes) so the fp64 chains interleave.  FULL tiles (every element inside the grid) skip all
-  // validity predicates.  The histogram takes one red.shared per element at the code clamped into
-  // the smem window; codes outside it (and outliers, code 0) are detected from the lane's running
-  // min / max code and corrected by the rare slow path below, which also appends the outliers.
-  //
-  // ok = |q| < R && |x' - x| <= eb is O8-O9 exactly: for |t| < 2^51, q = rint(t) and |t| >= R implies
-  // |rint(t)| >= R (R integer, rint monotone); for |t| >= 2^51, NaN or Inf, |q| < R is false.  The
-  // verify compare uses <=, which agrees with !(> eb) whenever |q| < R (then d is finite or +-Inf).
+// O7-O11 over i-planes [i0, i0+P), branch-free: 3P independent elements per j so the fp64 chains
+// interleave.  FULL tiles (every element inside the grid) skip all validity predicates.  The
+// histogram takes one red.shared per element at the code clamped into the smem window; codes
+// outside it and outliers (code 0) are flagged through the lane's running max of (code - lo) and
+// handled by rare_path().
+//
+// ok = |q| < R && |x' - x| <= eb is O8-O9 exactly: for |t| < 2^51, q = rint(t) and |t| >= R implies
+// |rint(t)| >= R (R integer, rint monotone); for |t| >= 2^51, NaN or Inf, |q| < R is false.  The
+// verify first tries the fast bound of make_consts (no conversion to T); only inconclusive elements
+// form x' = (T)(p + 2eb q) and compare |x' - x| <= eb in fp64 (<= agrees with !(> eb) there).
+template <typename T, bool IN_SMEM, bool HIST, bool FULL, int P>
+__device__ __forceinline__ uint32_t quantize_planes(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+                                                    uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int i0,
+                                                    const LaneGeom& L, const double bh[4], const Consts& K,
+                                                    const uint32_t R, const HistSmem& hs) {
+  const int lane = threadIdx.x & 31;
   const double Rd = (double)R;
-  const uint32_t win_base = (uint32_t)__cvta_generic_to_shared(hs.win) - 4u * hs.lo;  // &win[c - lo] = base + 4c
+  const uint32_t win_base = HIST ? (uint32_t)__cvta_generic_to_shared(hs.win) : 0u;  // &win[c - lo]
   const uint32_t sink = HIST ? (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * lane : 0u;
-  const uint32_t wlo = hs.lo, whi = hs.lo + hs.nwin - 1u;
-  uint32_t cmin = 0xffffffffu, cmax = 0u;
+  const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;   // window [lo, lo + nwin), lo >= 1
+  uint32_t umax = 0u;                                 // max over valid elements of (code - lo), unsigned
+  if (IN_SMEM) {  // shared-memory tiles: compile-time strides -> immediate address offsets
+    si = BS * TK; sj = TK; ci = BS * TK; cj = TK;
+  }
+  double di[P], dk[3];
+#pragma unroll
+  for (int ii = 0; ii < P; ii++) di[ii] = (double)(i0 + ii);
+#pragma unroll
+  for (int kk = 0; kk < 3; kk++) dk[kk] = (double)(3 * L.h + kk);
+  const T* xbase = xs + (IN_SMEM ? (uint32_t)(i0 * BS * TK + L.kcol) : (uint64_t)i0 * si + L.kcol);
+  uint16_t* cbase = cs + (IN_SMEM ? (uint32_t)(i0 * BS * TK + L.kcol) : (uint64_t)i0 * ci + L.kcol);
+  double dj = 0.0;
 #pragma unroll 1
-  for (int jk = 0; jk < 3 * BS; jk++) {
-    const int j = jk / 3, kk = jk - 3 * j;
-    const bool cv = FULL || ((j < m1) && (kk == 0 ? kv0 : (kk == 1 ? kv1 : kv2)));
-    T xv[BS];
+  for (int j = 0; j < BS; j++, dj += 1.0) {
+    const bool jv = FULL || j < L.m1;
+    const T* xrow = xbase + (IN_SMEM ? (uint32_t)(j * TK) : (uint64_t)j * sj);  // + ii*si + kk
+    uint16_t* crow = cbase + (IN_SMEM ? (uint32_t)(j * TK) : (uint64_t)j * cj);
+    T xv[3][P];
 #pragma unroll
-    for (int i = 0; i < BS; i++) {
-      const bool valid = FULL || (cv && i < m0);
-      if (IN_SMEM || FULL) xv[i] = xs[i * si + j * sj + kcol + kk];
-      else xv[i] = valid ? xs[i * si + j * sj + kcol + kk] : T(0);
-    }
-    // O7 hoisted: base = fma(b2, j, fma(b3, k, b0)), p = fma(b1, i, base)
-    const double base = __fma_rn(bh2, (double)j, __fma_rn(bh3, (double)(3 * h + kk), bh0));
-    uint32_t code[BS];
+    for (int kk = 0; kk < 3; kk++)
 #pragma unroll
-    for (int i = 0; i < BS; i++) {
-      const double xd = to_d<T>(xv[i]);
-      const double p = __fma_rn(bh1, (double)i, base);
-      // O8: t = (x - p) * inv2eb ; q = rint(t) (1.5*2^52 trick, ties-to-even)
-      const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
-      const double sm = __dadd_rn(t, RINT_MAGIC);
-      const double q = __dsub_rn(sm, RINT_MAGIC);
-      // O9: x' = (T)(p + twoeb*q), verify |x' - x| <= eb
-      const double y = __dadd_rn(p, __dmul_rn(K.twoeb, q));
-      const double d = __dsub_rn(to_d<T>(from_d<T>(y)), xd);
-      const bool ok = (fabs(q) < Rd) && (fabs(d) <= K.eb_abs);
-      code[i] = ok ? (uint32_t)(__double2loint(sm) + (int)R) : 0u;   // O10
-    }
-#pragma unroll
-    for (int i = 0; i < BS; i++) {
-      const bool valid = FULL || (cv && i < m0);
-      const uint32_t c = code[i];
-      if (valid) cs[i * ci + j * cj + kcol + kk] = (uint16_t)c;
-      if (FULL) {
-        cmin = min(cmin, c);
-        cmax = max(cmax, c);
-      } else if (valid) {
-        cmin = min(cmin, c);
-        cmax = max(cmax, c);
+      for (int ii = 0; ii < P; ii++) {
+        const bool valid = FULL || (jv && L.kv(kk) && (i0 + ii < L.m0));
+        if (IN_SMEM || FULL) xv[kk][ii] = xrow[ii * si + kk];
+        else xv[kk][ii] = valid ? xrow[ii * si + kk] : T(0);
       }
-      if (HIST) {  // O11
-        const uint32_t cw = min(max(c, wlo), whi);
-        red_smem_add(FULL ? win_base + 4u * cw : (valid ? win_base + 4u * cw : sink), FULL ? 1u : (valid ? 1u : 0u));
+    uint32_t code[3][P];
+    bool need = false;   // some element has |q| < R but an inconclusive fast verify -> exact O9 below
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++) {
+      // O7 hoisted: base = fma(b2, j, fma(b3, k, b0)), p = fma(b1, i, base)
+      const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk[kk], bh[0]));
+#pragma unroll
+      for (int ii = 0; ii < P; ii++) {
+        const double xd = to_d<T>(xv[kk][ii]);
+        const double p = __fma_rn(bh[1], di[ii], base);
+        // O8: t = (x - p) * inv2eb ; q = rint(t) (1.5*2^52 trick, ties-to-even)
+        const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+        const double sm = __dadd_rn(t, RINT_MAGIC);
+        const double q = __dsub_rn(sm, RINT_MAGIC);
+        // O9 fast verify (bound in make_consts)
+        const double v = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, q)));
+        const bool qok = fabs(q) < Rd;
+        const bool fast = v <= K.vthr;
+        const uint32_t c = (uint32_t)(__double2loint(sm) + (int)R);
+        code[kk][ii] = (qok && fast) ? c : 0u;   // O10
+        need |= qok && !fast;
       }
     }
+    if (__any_sync(0xffffffffu, need)) {
+      // exact O9 for the inconclusive elements: x' = (T)(p + twoeb*q), outlier if |x' - x| > eb
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk[kk], bh[0]));
+#pragma unroll
+        for (int ii = 0; ii < P; ii++) {
+          const double xd = to_d<T>(xv[kk][ii]);
+          const double p = __fma_rn(bh[1], di[ii], base);
+          const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+          const double sm = __dadd_rn(t, RINT_MAGIC);
+          const double q = __dsub_rn(sm, RINT_MAGIC);
+          const double v = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, q)));
+          if (fabs(q) < Rd && !(v <= K.vthr)) {
+            const double y = __dadd_rn(p, __dmul_rn(K.twoeb, q));
+            const double d = __dsub_rn(to_d<T>(from_d<T>(y)), xd);
+            code[kk][ii] = (fabs(d) <= K.eb_abs) ? (uint32_t)(__double2loint(sm) + (int)R) : 0u;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++)
+#pragma unroll
+      for (int ii = 0; ii < P; ii++) {
+        const bool valid = FULL || (jv && L.kv(kk) && (i0 + ii < L.m0));
+        const uint32_t c = code[kk][ii];
+        if (valid) crow[ii * ci + kk] = (uint16_t)c;
+        const uint32_t uc = c - wlo;                     // code 0 (outlier) wraps to a huge value
+        if (FULL) umax = max(umax, uc);
+        else if (valid) umax = max(umax, uc);
+        if (HIST) {  // O11: counted at the clamped bin; out-of-window codes corrected in rare_path
+          const uint32_t cw = min(uc, wtop);
+          red_smem_add(FULL ? win_base + 4u * cw : (valid ? win_base + 4u * cw : sink), FULL ? 1u : (valid ? 1u : 0u));
+        }
+      }
   }
+  return umax;
+}
 
-  // ---------------- slow path (rare): outliers -> (global index, value), warp-aggregated append;
-  // histogram correction for codes outside the window [wlo, whi] (counted at the clamped bin).
-  const bool has_out = cmin == 0u;
-  const bool has_spill = HIST && (cmin < wlo || cmax > whi);
-  if (__any_sync(0xffffffffu, has_out || has_spill)) {
-    uint32_t nout = 0;
-    if (has_out || has_spill) {
-      for (int j = 0; j < m1; j++)
-        for (int kk = 0; kk < 3; kk++) {
-          if (!(kk == 0 ? kv0 : (kk == 1 ? kv1 : kv2))) continue;
-          for (int i = 0; i < m0; i++) {
-            const uint32_t c = cs[i * ci + j * cj + kcol + kk];
-            nout += (c == 0u) ? 1u : 0u;
-            if (HIST && c != 0u && (c < wlo || c > whi)) {
-              atomicSub(&hs.win[min(max(c, wlo), whi) - wlo], 1u);
-              atomicAdd(&o.hist[c], 1ull);
-            }
+// Rare path (warp-uniform entry): outliers of i-planes [i0, i0+P) -> (global index, value) with a
+// warp-aggregated append; histogram correction for codes outside the window (counted at the top
+// bin): moved to the global histogram / the zero counter.
+template <typename T, bool HIST, int P>
+__device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+                                          const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int i0,
+                                          const LaneGeom& L, uint32_t umax, const TileCoord tc, const Geo& g,
+                                          const CompressOut<T>& o, const HistSmem& hs) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;
+  const bool has_rare = umax > wtop;
+  if (!__any_sync(0xffffffffu, has_rare)) return;
+  const int i1 = min(i0 + P, L.m0);
+  uint32_t nout = 0;
+  if (has_rare) {
+    for (int j = 0; j < L.m1; j++)
+      for (int kk = 0; kk < 3; kk++) {
+        if (!L.kv(kk)) continue;
+        for (int i = i0; i < i1; i++) {
+          const uint32_t c = cs[i * ci + j * cj + L.kcol + kk];
+          nout += (c == 0u) ? 1u : 0u;
+          if (HIST && c != 0u && c - wlo > wtop) {   // counted at the top bin: move to global
+            atomicSub(&hs.win[wtop], 1u);
+            atomicAdd(&o.hist[c], 1ull);
           }
         }
-    }
-    uint32_t incl = nout;
+      }
+  }
+  uint32_t incl = nout;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += v;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total) {
-      unsigned long long basepos = 0;
-      if (lane == 31) {
-        basepos = atomicAdd(o.ocount, (unsigned long long)total);
-        if (HIST && wlo > 0u) {  // outliers were counted at the clamped bin wlo
-          atomicSub(&hs.win[0], total);
-          atomicAdd(hs.zero, total);
-        }
-      }
-      basepos = __shfl_sync(0xffffffffu, basepos, 31);
-      unsigned long long pos = basepos + (incl - nout);
-      if (nout) {
-        const uint64_t gbase =
-            g.gofs + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)kb * BS + 3 * h;
-        for (int j = 0; j < m1; j++)
-          for (int kk = 0; kk < 3; kk++) {
-            if (!(kk == 0 ? kv0 : (kk == 1 ? kv1 : kv2))) continue;
-            for (int i = 0; i < m0; i++) {
-              if (cs[i * ci + j * cj + kcol + kk] != 0) continue;
-              if (pos < o.cap) {
-                o.oidx[pos] = gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk;
-                o.oval[pos] = xs[i * si + j * sj + kcol + kk];
-              }
-              pos++;
-            }
-          }
-      }
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  unsigned long long basepos = 0;
+  if (lane == 31) {
+    basepos = atomicAdd(o.ocount, (unsigned long long)total);
+    if (HIST) {  // outliers were counted at the clamped (top) bin
+      atomicSub(&hs.win[wtop], total);
+      atomicAdd(hs.zero, total);
     }
   }
+  basepos = __shfl_sync(0xffffffffu, basepos, 31);
+  unsigned long long pos = basepos + (incl - nout);
+  if (nout) {
+    const uint64_t gbase =
+        g.gofs + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)L.kb * BS + 3 * L.h;
+    for (int j = 0; j < L.m1; j++)
+      for (int kk = 0; kk < 3; kk++) {
+        if (!L.kv(kk)) continue;
+        for (int i = i0; i < i1; i++) {
+          if (cs[i * ci + j * cj + L.kcol + kk] != 0) continue;
+          if (pos < o.cap) {
+            o.oidx[pos] = gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk;
+            o.oval[pos] = xs[i * si + j * sj + L.kcol + kk];
+          }
+          pos++;
+        }
+      }
+  }
+}
+
+// One warp compresses a whole tile (plain kernel).
+template <typename T, bool IN_SMEM, bool HIST, bool FULL>
+__device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+                                              uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
+                                              const TileCoord tc, const Geo& g, const Consts& K,
+                                              const uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
+  const LaneGeom L = lane_geom(tc, g);
+  double V[4], beta[4], bh[4];
+  int32_t cc[4];
+  moments_partial<T, IN_SMEM, BS>(xs, si, sj, 0, L, V);
+#pragma unroll
+  for (int d = 0; d < 4; d++) V[d] += __shfl_xor_sync(0xffffffffu, V[d], 1);
+  block_coefs(V, L, K, beta, cc, bh);
+  write_coefs(o, tc, g, L, cc, beta);
+  const uint32_t umax = quantize_planes<T, IN_SMEM, HIST, FULL, 2>(xs, si, sj, cs, ci, cj, 0, L, bh, K, R, hs) ;
+  const uint32_t umax2 = quantize_planes<T, IN_SMEM, HIST, FULL, 2>(xs, si, sj, cs, ci, cj, 2, L, bh, K, R, hs);
+  const uint32_t umax3 = quantize_planes<T, IN_SMEM, HIST, FULL, 2>(xs, si, sj, cs, ci, cj, 4, L, bh, K, R, hs);
+  rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, L, max(umax, max(umax2, umax3)), tc, g, o, hs);
 }
 
 // ------------------------------------------------------------------------------------------

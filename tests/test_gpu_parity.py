@@ -236,3 +236,28 @@ def test_gpu_slab_invariance():
         hist += part.hist
     assert torch.equal(torch.cat(codes), whole.codes)
     assert torch.equal(hist, whole.hist)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_repeat_determinism_full_size(name):
+    """Back-to-back launches (the bench's pattern) must give bit-identical outputs every time.
+    Catches pipeline races that a single parity run can miss."""
+    from synth import config_by_name, make_field
+    s = sz()
+    cfg = config_by_name(name)
+    x = make_field(cfg, device="cuda")
+    bufs = s.CompressBuffers(x.shape, x.dtype, cfg.radius, device=x.device, coef_raw=True)
+    ref = s.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, bufs=bufs, coef_raw=True).finalize()
+    codes0, coef0, hist0, raw0 = ref.codes.clone(), ref.coef_codes.clone(), ref.hist.clone(), ref.coef_raw.clone()
+    xo0 = s.decompress(ref).clone()
+    out = torch.empty_like(x)
+    for _ in range(20):
+        r = s.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, bufs=bufs, coef_raw=True)
+        s.regression_decompress(r.codes, r.coef_codes, r.outlier_idx, r.outlier_val, ref.n_outliers, ref.eb_abs,
+                                cfg.radius, x.dtype, out=out)
+    torch.cuda.synchronize()
+    r.finalize()
+    assert torch.equal(r.codes, codes0) and torch.equal(r.coef_codes, coef0) and torch.equal(r.hist, hist0)
+    assert torch.equal(r.coef_raw, raw0)
+    assert torch.equal(out.view(torch.int32 if x.dtype == torch.float32 else torch.int64),
+                       xo0.view(torch.int32 if x.dtype == torch.float32 else torch.int64))
