@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 block-regression compressor hot path (SZ3, arxiv 2111.02925).
+
+Metric (BASELINE.json): regression compress & decompress GB/s per GPU and at N GPUs, % of HBM roofline.
+Workload: config c5 -- 1024 x 2048 x 2048 fp32 (16 GiB) k^-3 Gaussian random field (seed 4), eb = 1e-3 x
+value range, R = 32768, 6^3 blocks, sharded as block-aligned slabs over the N GPUs (strong scaling).
+
+One step = the whole hot path over the field: a0 value range (+ MAX all-reduce of the range when N > 1),
+a1-a7 fused compress (+ SUM all-reduce of the histogram when N > 1), a8 decompress + outlier scatter.
+value = input bytes of the whole field / step time (max over ranks), i.e. round-trip GB/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sz3g|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+
+Prints ONE JSON line on rank 0.  Inputs (16 GiB) are larger than the 126 MB L2, so no flush is needed
+between steps.  `--impl reference` times the CPU oracle (oracle/, the test checker) on a bounded sample
+of the same workload: the only other place bench.py runs oracle/ is the cpu_baseline leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "regression compress & decompress GB/s per GPU and 8-GPU, % of HBM roofline"
+UNIT = "GB/s"
+CONFIG = "c5"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="sz3g", choices=["sz3g", "reference"])
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-planes", type=int, default=24)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------------- helpers
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def profiled_traffic(kernel: str, config: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{config}:{kernel}")
+
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int, period_ms: int = 50):
+        self.index, self.period_ms = index, period_ms
+        self.proc, self.lines, self.thread = None, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, n in REASON_BITS.items():
+                if bits & b:
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def make_slab(cfg, world, rank):
+    """Generate the global field on this GPU (deterministic: seed 4) and keep this rank's slab."""
+    import torch
+    from paper_2111_02925_b200.dist import slab_bounds
+    from synth import make_field
+    full = make_field(cfg, device="cuda")
+    a, b = slab_bounds(cfg.shape[0], world, rank)
+    x = full[a:b].clone()
+    del full
+    torch.cuda.empty_cache()
+    return x, a
+
+
+# ----------------------------------------------------------------------------------------- CPU oracle
+def oracle_round_trip(xs_np, cfg, lo, hi, dim0_offset):
+    import oracle
+    t0 = time.perf_counter()
+    c = oracle.compress(xs_np, cfg.eb, cfg.eb_mode, radius=cfg.radius, dim0_offset=dim0_offset,
+                        value_range_override=(lo, hi))
+    oracle.decompress(c)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (oracle/, plain single-threaded C++) timed on the host, on a
+    bounded sample of the workload (one 6-plane block row of the c5 field, with the global range)."""
+    import numpy as np
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth import config_by_name, make_field
+    cfg = config_by_name(args.config)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    shape = cfg.shape if dev == "cuda" else (48, 256, 256)
+    full = make_field(cfg, device=dev, shape=shape)
+    lo, hi = float(full.min()), float(full.max())
+    a = (shape[0] // 12) * 6
+    xs = full[a:a + 6].cpu().numpy()
+    del full
+    sample_bytes = xs.nbytes
+    import oracle
+    oracle.build()
+    for _ in range(args.warmup):
+        oracle_round_trip(xs, cfg, lo, hi, a)
+    times = [oracle_round_trip(xs, cfg, lo, hi, a) for _ in range(args.steps)]
+    t = sum(times)
+    value = sample_bytes * args.steps / t / 1e9
+    sample = f"planes [{a},{a + 6}) of {cfg.name} {shape} (one block row, {xs.size} elements, global range)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (f32 data)",
+            "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.desc}", "shape": list(shape),
+                                            "eb_rel": cfg.eb, "radius": cfg.radius, "block": 6},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    from paper_2111_02925_b200 import dist as pdist
+    from paper_2111_02925_b200 import sz3g
+    from synth import config_by_name
+
+    world, rank, local = dist_setup(args)
+    cfg = config_by_name(args.config)
+    sz3g.load()
+    x, a0 = make_slab(cfg, world, rank)
+    N_local, N_global = x.numel(), math.prod(cfg.shape)
+    s = x.element_size()
+    NB_local = sz3g.num_blocks(x.shape)
+    cap = max(1 << 20, N_local // 256)
+    bufs = sz3g.CompressBuffers(x.shape, x.dtype, cfg.radius, outlier_cap=cap, device=x.device)
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    ev = {}
+
+    def step(record=None):
+        sz3g.value_range(x, bufs.minmax)
+        pdist.allreduce_range_(bufs.minmax)
+        bufs.reset()
+        if record is not None:
+            record[0].record(stream)
+        sz3g.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=bufs.minmax, bufs=bufs, reset=False,
+                                 dim0_offset=a0)
+        if record is not None:
+            record[1].record(stream)
+        pdist.allreduce_hist_(bufs.hist)
+        if record is not None:
+            record[2].record(stream)
+        sz3g.regression_decompress(bufs.codes, bufs.coef_codes, bufs.outlier_idx, bufs.outlier_val, cap, cfg.eb,
+                                   cfg.radius, x.dtype, dim0_offset=a0, out=out, d_outlier_count=bufs.outlier_count,
+                                   eb_mode=cfg.eb_mode, d_minmax=bufs.minmax)
+        if record is not None:
+            record[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+    recs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = sz3g.launch_count()
+    with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local) as clk:
+        barrier(world)
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(recs[k])
+        t_end.record(stream)
+        barrier(world)
+    launches = sz3g.launch_count() - l0
+    ms_total = max_over_ranks(t_start.elapsed_time(t_end), world)
+    ms_step = ms_total / args.steps
+    comp_ms = sum(r[0].elapsed_time(r[1]) for r in recs) / args.steps
+    dec_ms = sum(r[2].elapsed_time(r[3]) for r in recs) / args.steps
+    comp_ms_max = max_over_ranks(comp_ms, world)
+    dec_ms_max = max_over_ranks(dec_ms, world)
+
+    res = sz3g.Compressed(tuple(x.shape), x.dtype, cfg.radius, a0, bufs.codes, bufs.coef_codes, None, bufs.outlier_idx,
+                          bufs.outlier_val, bufs.outlier_count, bufs.hist, bufs.eb_abs, bufs.status).finalize()
+    n_out = res.n_outliers
+    # algorithmic bytes per launch: compress reads x, writes codes, coefficient codes, outliers
+    comp_bytes = N_local * (s + 2) + NB_local * 16 + n_out * (8 + s)
+    dec_bytes = N_local * (2 + s) + NB_local * 16 + n_out * (8 + s)
+    peaks = measured_peaks()
+    comp_gbs = comp_bytes / (comp_ms * 1e-3) / 1e9
+    value = N_global * s / (ms_step * 1e-3) / 1e9
+
+    # ---------------- end to end through the public API with HOST buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        h_x = torch.empty_like(x, device="cpu").pin_memory()
+        h_x.copy_(x)
+        h_codes = torch.empty_like(bufs.codes, device="cpu").pin_memory()
+        h_coef = torch.empty_like(bufs.coef_codes, device="cpu").pin_memory()
+        h_oidx = torch.empty_like(bufs.outlier_idx, device="cpu").pin_memory()
+        h_oval = torch.empty_like(bufs.outlier_val, device="cpu").pin_memory()
+        h_cnt = torch.empty_like(bufs.outlier_count, device="cpu").pin_memory()
+        h_hist = torch.empty_like(bufs.hist, device="cpu").pin_memory()
+        h_out = torch.empty_like(x, device="cpu").pin_memory()
+        bi = h_x.numel() * s
+        bo = (h_codes.numel() * 2 + h_coef.numel() * 4 + h_oidx.numel() * 8 + h_oval.numel() * s + 8 +
+              h_hist.numel() * 8 + h_out.numel() * s)
+
+        def e2e_step():
+            x.copy_(h_x, non_blocking=True)
+            step()
+            h_codes.copy_(bufs.codes, non_blocking=True)
+            h_coef.copy_(bufs.coef_codes, non_blocking=True)
+            h_cnt.copy_(bufs.outlier_count, non_blocking=True)
+            h_oidx.copy_(bufs.outlier_idx, non_blocking=True)
+            h_oval.copy_(bufs.outlier_val, non_blocking=True)
+            h_hist.copy_(bufs.hist, non_blocking=True)
+            h_out.copy_(out, non_blocking=True)
+
+        e2e_step()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        barrier(world)
+        e_ms = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
+        e2e = {"value": N_global * s / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "ms_per_step": e_ms,
+               "note": "pinned host x -> device; value_range+compress+decompress; codes, coefficient codes, "
+                       "outliers, histogram and x' -> pinned host; one stream, sequential"}
+
+    # ---------------- CPU oracle beside it (rank 0, N = 1 only; bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        lo, hi = (float(v) for v in bufs.minmax.cpu())
+        p = min(args.cpu_sample_planes, x.shape[0] - 504)
+        xs = x[504:504 + p].cpu().numpy()
+        t = oracle_round_trip(xs, cfg, lo, hi, 504)
+        cpu = {"value": xs.nbytes / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"planes [504,{504 + p}) of {cfg.name} ({xs.size} elements, global range), "
+                         f"compress + decompress, one host core, {t:.1f} s"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 data, f64 arithmetic", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "shape": list(cfg.shape), "eb_rel": cfg.eb,
+                       "radius": cfg.radius, "block": 6, "parallelism": f"slabs{world}",
+                       "l2": "inputs (16 GiB) larger than L2; no flush"},
+            "roofline": {"bound": "hbm", "kernel": "k_compress_tma", "achieved": comp_gbs, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": comp_gbs / peaks["hbm_gbs"],
+                         "traffic": profiled_traffic("k_compress_tma", cfg.name), "peak_source": peaks["source"],
+                         "alg_bytes_per_launch": comp_bytes, "ms_per_launch": comp_ms},
+            "compress_gbs": N_global * s / (comp_ms_max * 1e-3) / 1e9,
+            "decompress_gbs": N_global * s / (dec_ms_max * 1e-3) / 1e9,
+            "decompress_roofline": {"achieved": dec_bytes / (dec_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                    "frac": dec_bytes / (dec_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                    "ms_per_launch": dec_ms},
+            "outliers": n_out, "eb_abs": res.eb_abs,
+            "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

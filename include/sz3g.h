@@ -102,13 +102,23 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
 
 /* a8 -- decompression (recover): x_out = (T)(p + 2 eb (c - R)) for c != 0, then the
  * stored outlier values are scattered to their indices (2 launches, stream-ordered).
- * params->eb_mode must be SZ3G_EB_ABS with params->eb = the eb_abs used at compression.
- * outlier_idx are global indices (grid->dim0_offset is subtracted).  n_outliers is a HOST
- * count (<= the capacity used at compression).  Bit-identical to the compress-time x'.     */
+ *   params           the compression parameters: ABS with eb = eb_abs, or REL with the same
+ *                    relative eb and the same d_minmax (eb_abs is recomputed on the device with
+ *                    the same operations, so it is bit-identical to the compress-time value).
+ *   d_minmax         device double[2]; required iff params->eb_mode == REL.
+ *   outlier_idx      global indices (grid->dim0_offset is subtracted), outlier_val their values.
+ *   n_outliers       HOST count of stored outliers, or, when d_outlier_count is non-NULL, the
+ *                    capacity of outlier_idx / outlier_val (an upper bound).
+ *   d_outlier_count  nullable DEVICE uint64: the count written by sz3g_regression_compress;
+ *                    min(*d_outlier_count, n_outliers) entries are scattered.
+ * With d_minmax and d_outlier_count a compress -> decompress sequence needs no host
+ * synchronisation.  The result is bit-identical to the compress-time x'.                     */
 int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
-                               const uint16_t* codes, const int32_t* coef_codes,
-                               const uint64_t* outlier_idx, const void* outlier_val,
-                               uint64_t n_outliers, void* x_out, sz3g_stream_t stream);
+                               const double* d_minmax, const uint16_t* codes,
+                               const int32_t* coef_codes, const uint64_t* outlier_idx,
+                               const void* outlier_val, uint64_t n_outliers,
+                               const unsigned long long* d_outlier_count, void* x_out,
+                               sz3g_stream_t stream);
 
 /* a7 standalone -- histogram of n uint16 codes into 2R int64 bins, ACCUMULATED (+=).  Codes
  * >= 2R are ignored.  1 launch. */

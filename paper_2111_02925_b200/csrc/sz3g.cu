@@ -479,7 +479,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 1)
 
 template <typename T>
 __global__ void k_outlier_scatter(const uint64_t* __restrict__ idx, const T* __restrict__ val, uint64_t n,
-                                  uint64_t base, uint64_t N, T* __restrict__ xo) {
+                                  const unsigned long long* __restrict__ d_n, uint64_t base, uint64_t N,
+                                  T* __restrict__ xo) {
+  if (d_n) n = min((unsigned long long)n, *d_n);
   for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < n; m += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e = idx[m] - base;
     if (idx[m] >= base && e < N) xo[e] = val[m];
@@ -741,14 +743,15 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
   return check_launch(1);
 }
 
-int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params, const uint16_t* codes,
-                               const int32_t* coef_codes, const uint64_t* outlier_idx, const void* outlier_val,
-                               uint64_t n_outliers, void* x_out, sz3g_stream_t stream) {
+int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax,
+                               const uint16_t* codes, const int32_t* coef_codes, const uint64_t* outlier_idx,
+                               const void* outlier_val, uint64_t n_outliers,
+                               const unsigned long long* d_outlier_count, void* x_out, sz3g_stream_t stream) {
   int rc = validate_grid(grid);
   if (rc) return rc;
   rc = validate_params(params);
   if (rc) return rc;
-  if (params->eb_mode != SZ3G_EB_ABS) return SZ3G_EINVAL;
+  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
   if (!codes || !coef_codes || !x_out) return SZ3G_EINVAL;
   if (n_outliers > 0 && (!outlier_idx || !outlier_val)) return SZ3G_EINVAL;
   if (reinterpret_cast<uintptr_t>(coef_codes) & 15) return SZ3G_EINVAL;
@@ -758,8 +761,9 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   memset(&ka, 0, sizeof(ka));
   ka.g = g;
   ka.R = params->radius;
-  ka.eb_mode = 0;
+  ka.eb_mode = (int)params->eb_mode;
   ka.eb = params->eb;
+  ka.d_minmax = d_minmax;
   ka.pf = prefetch_tiles();
   int32_t* dummy_status = nullptr;  // decompress never reports: eb validated on the host
   ka.d_status = dummy_status;
@@ -779,8 +783,8 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
     }
     if (n_outliers) {
       const unsigned b = (unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096);
-      k_outlier_scatter<float><<<b, 256, 0, st>>>(outlier_idx, (const float*)outlier_val, n_outliers, g.gofs, N,
-                                                  (float*)x_out);
+      k_outlier_scatter<float><<<b, 256, 0, st>>>(outlier_idx, (const float*)outlier_val, n_outliers,
+                                                  d_outlier_count, g.gofs, N, (float*)x_out);
       launched++;
     }
   } else {
@@ -794,8 +798,8 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
     }
     if (n_outliers) {
       const unsigned b = (unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096);
-      k_outlier_scatter<double><<<b, 256, 0, st>>>(outlier_idx, (const double*)outlier_val, n_outliers, g.gofs, N,
-                                                   (double*)x_out);
+      k_outlier_scatter<double><<<b, 256, 0, st>>>(outlier_idx, (const double*)outlier_val, n_outliers,
+                                                   d_outlier_count, g.gofs, N, (double*)x_out);
       launched++;
     }
   }

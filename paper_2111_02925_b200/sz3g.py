@@ -61,7 +61,7 @@ def load(allow_build: bool = False):
     GP, PP = ctypes.POINTER(Grid), ctypes.POINTER(Params)
     lib.sz3g_value_range.argtypes = [GP, P, P, P]
     lib.sz3g_regression_compress.argtypes = [GP, PP, P, P, P, P, P, P, P, U64, P, P, P, P, P]
-    lib.sz3g_regression_decompress.argtypes = [GP, PP, P, P, P, P, U64, P, P]
+    lib.sz3g_regression_decompress.argtypes = [GP, PP, P, P, P, P, P, U64, P, P, P]
     lib.sz3g_histogram.argtypes = [P, U64, U32, P, P]
     lib.sz3g_num_blocks.argtypes = [GP, U32]
     lib.sz3g_num_blocks.restype = U64
@@ -252,18 +252,25 @@ def regression_compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius
 
 
 def regression_decompress(codes: torch.Tensor, coef_codes: torch.Tensor, outlier_idx: torch.Tensor,
-                          outlier_val: torch.Tensor, n_outliers: int, eb_abs: float, radius: int = 32768,
+                          outlier_val: torch.Tensor, n_outliers: int, eb: float, radius: int = 32768,
                           dtype: torch.dtype = torch.float32, dim0_offset: int = 0, out: torch.Tensor | None = None,
-                          flags: int = 0, stream=None) -> torch.Tensor:
-    """sz3g_regression_decompress (recover) + outlier scatter."""
-    _require_cuda(codes, coef_codes, outlier_idx, outlier_val, out)
+                          flags: int = 0, stream=None, d_outlier_count: torch.Tensor | None = None,
+                          eb_mode: str = "abs", d_minmax: torch.Tensor | None = None) -> torch.Tensor:
+    """sz3g_regression_decompress (recover) + outlier scatter.
+
+    ``eb_mode="abs"``: ``eb`` is the eb_abs used at compression.  ``eb_mode="rel"``: ``eb`` is the
+    relative bound and ``d_minmax`` the same device range compression used.  With ``d_outlier_count``
+    (the device counter written by compress) ``n_outliers`` is only the capacity.  Neither form needs
+    a host synchronisation.
+    """
+    _require_cuda(codes, coef_codes, outlier_idx, outlier_val, out, d_outlier_count, d_minmax)
     if out is None:
         out = torch.empty(codes.shape, dtype=dtype, device=codes.device)
     g = make_grid(codes.shape, out.dtype, dim0_offset)
-    p = make_params(eb_abs, "abs", radius, flags)
-    rc = load().sz3g_regression_decompress(ctypes.byref(g), ctypes.byref(p), _ptr(codes), _ptr(coef_codes),
-                                           _ptr(outlier_idx), _ptr(outlier_val), int(n_outliers), _ptr(out),
-                                           _stream(stream))
+    p = make_params(eb, eb_mode, radius, flags)
+    rc = load().sz3g_regression_decompress(ctypes.byref(g), ctypes.byref(p), _ptr(d_minmax), _ptr(codes),
+                                           _ptr(coef_codes), _ptr(outlier_idx), _ptr(outlier_val),
+                                           int(n_outliers), _ptr(d_outlier_count), _ptr(out), _stream(stream))
     _check(rc, "sz3g_regression_decompress")
     return out
 
