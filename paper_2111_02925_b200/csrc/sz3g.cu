@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(128) k_compress_plain(const T* __restrict__ x,
 // ---------------------------------------------------------------------------------- compress, TMA
 // Persistent, one CTA per SM.  Warp NG*G is the producer (one elected lane streams 6x6x96 tiles with
 // TMA).  The other NG*G warps form NG groups of G warps; a group takes one tile at a time (group g:
-// the CTA's tiles g, g+NG, ...), each warp owning P = 6/G i-planes.  Every group has a private
+// the CTA's tiles g, g+NG, ...), each warp owning P = 6/G rows j of all six i-planes.  Every group has a private
 // D-deep mbarrier ring (stage s = g*D + slot): a stage has exactly one consumer, which visits it in
 // order, so a waiter can never be two phases ahead of the barrier (a ring shared round-robin by
 // independent consumers lets a fast consumer's parity wait match the *previous* phase).
@@ -263,6 +263,37 @@ struct CompressSmem {
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One warp's share of a group tile (rows j0 .. j0+6/G-1): partial moments of its rows, exchange (B1), coefficients,
+// quantisation of its planes into the group's code buffer, rare path.  FULL tiles fold the block
+// geometry (6x6x6 everywhere) into constants.
+template <typename T, bool HIST, bool FULL, int G>
+__device__ __forceinline__ void group_tile(const T* __restrict__ xs, uint16_t* __restrict__ mycodes, double* myexch,
+                                           int j0, int wg, int bar_id, const TileCoord tc, const Geo& g,
+                                           const Consts& K, uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
+  constexpr int P = BS / G;
+  const int lane = threadIdx.x & 31;
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  double V[4];
+  moments_partial<T, true, P>(xs, BS * TK, TK, j0, L, V);
+#pragma unroll
+  for (int d = 0; d < 4; d++) myexch[(wg * 4 + d) * 32 + lane] = V[d];
+  named_bar_sync(bar_id, G * 32);  // B1
+#pragma unroll
+  for (int d = 0; d < 4; d++) {
+    double acc = myexch[d * 32 + lane];
+#pragma unroll
+    for (int w = 1; w < G; w++) acc += myexch[(w * 4 + d) * 32 + lane];
+    V[d] = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+  }
+  double beta[4], bh[4];
+  int32_t cc[4];
+  block_coefs<FULL>(V, L, K, beta, cc, bh);
+  if (wg == 0) write_coefs(o, tc, g, L, cc, beta);
+  const uint32_t umax =
+      quantize_rows<T, true, HIST, FULL, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, j0, L, bh, K, R, hs);
+  rare_path<T, HIST, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, j0, L, umax, tc, g, o, hs);
 }
 
 template <typename T, int G, int NG, int D, bool HIST>
@@ -320,7 +351,7 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     }
   } else {
     // ---------------- consumer groups
-    const int grp = warp / G, wg = warp - grp * G, i0 = wg * P;
+    const int grp = warp / G, wg = warp - grp * G, j0 = wg * P;
     const int bar_id = 1 + grp;
     const Consts K = *s_k;
     uint16_t* mycodes = cbuf + (size_t)grp * TILE_ELEMS;
@@ -329,31 +360,13 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     for (uint64_t t = blockIdx.x + (uint64_t)grp * Gr; t < g.ntiles; t += (uint64_t)NG * Gr, k++) {
       const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
       const TileCoord tc = decode_tile(t, g);
-      const LaneGeom L = lane_geom(tc, g);
-      const bool full_tile = tile_full(tc, g);
       if (codes_tma && wg == 0 && lane == 0) ptx::bulk_wait_read0();  // previous store done reading mycodes
       ptx::mbar_wait(&full[s], ph);
       const T* xs = stages + (size_t)s * TILE_ELEMS;
-      double V[4];
-      moments_partial<T, true, P>(xs, BS * TK, TK, i0, L, V);
-#pragma unroll
-      for (int d = 0; d < 4; d++) myexch[(wg * 4 + d) * 32 + lane] = V[d];
-      named_bar_sync(bar_id, G * 32);  // B1
-#pragma unroll
-      for (int d = 0; d < 4; d++) {
-        double acc = myexch[d * 32 + lane];
-#pragma unroll
-        for (int w = 1; w < G; w++) acc += myexch[(w * 4 + d) * 32 + lane];
-        V[d] = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
-      }
-      double beta[4], bh[4];
-      int32_t cc[4];
-      block_coefs(V, L, K, beta, cc, bh);
-      if (wg == 0) write_coefs(o, tc, g, L, cc, beta);
-      uint32_t umax;
-      if (full_tile) umax = quantize_planes<T, true, HIST, true, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, i0, L, bh, K, a.R, hs);
-      else umax = quantize_planes<T, true, HIST, false, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, i0, L, bh, K, a.R, hs);
-      rare_path<T, HIST, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, i0, L, umax, tc, g, o, hs);
+      if (tile_full(tc, g))
+        group_tile<T, HIST, true, G>(xs, mycodes, myexch, j0, wg, bar_id, tc, g, K, a.R, o, hs);
+      else
+        group_tile<T, HIST, false, G>(xs, mycodes, myexch, j0, wg, bar_id, tc, g, K, a.R, o, hs);
       if (codes_tma) ptx::fence_proxy_async_smem();
       named_bar_sync(bar_id, G * 32);  // B2: codes complete, stage no longer read
       if (wg == 0) {
@@ -622,7 +635,7 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 }
 
 // tuned configurations: (consumer warps, ring stages); smem fits the 227 KiB per-CTA limit
-constexpr int PF_TILES = 16;        // default L2 prefetch distance of the TMA producers (tiles per CTA)
+constexpr int PF_TILES = 0;         // default L2 prefetch distance (tiles per CTA); 0: prefetched lines were evicted before use (ncu: +47% DRAM reads on c5)
 
 uint32_t prefetch_tiles() {  // SZ3G_PF overrides (tuning only)
   static uint32_t v = [] {

@@ -135,16 +135,23 @@ struct LaneGeom {
   __device__ __forceinline__ bool kv(int kk) const { return kk == 0 ? kv0 : (kk == 1 ? kv1 : kv2); }
 };
 
+// FULL: the tile lies inside the grid, so every block is 6x6x6 (constants fold)
+template <bool FULL = false>
 __device__ __forceinline__ LaneGeom lane_geom(const TileCoord tc, const Geo& g) {
   const int lane = threadIdx.x & 31;
   LaneGeom L;
   const int bl = lane >> 1;
   L.h = lane & 1;
   L.kb = tc.c * 16u + (uint32_t)bl;
+  L.kcol = 6 * bl + 3 * L.h;
+  if (FULL) {
+    L.m0 = L.m1 = L.m2 = BS;
+    L.kv0 = L.kv1 = L.kv2 = true;
+    return L;
+  }
   L.m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
   L.m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
   L.m2 = (L.kb < g.NB2) ? (int)umin64(BS, g.n2 - (uint64_t)L.kb * BS) : 0;
-  L.kcol = 6 * bl + 3 * L.h;
   L.kv0 = 3 * L.h + 0 < L.m2;
   L.kv1 = 3 * L.h + 1 < L.m2;
   L.kv2 = 3 * L.h + 2 < L.m2;
@@ -156,22 +163,22 @@ __device__ __forceinline__ bool tile_full(const TileCoord tc, const Geo& g) {
   return (uint64_t)(tc.a + 1) * BS <= g.n0 && (uint64_t)(tc.b + 1) * BS <= g.n1 && (uint64_t)(tc.c + 1) * TK <= g.n2;
 }
 
-// O4 partial moments of the lane's three columns over i-planes [i0, i0+P) (fp64).  Row sums
-// S = f0+f1+f2 and the lane-local k-weighted sum f1 + 2 f2 first; P_i = sum_j S, Q_i = sum_j j S,
-// Z_i = sum_j (f1 + 2 f2).  Vz includes the lane's column offset 3h inside the block.
-template <typename T, bool IN_SMEM, int P>
-__device__ __forceinline__ void moments_partial(const T* __restrict__ xs, uint64_t si, uint64_t sj, int i0,
+// O4 partial moments of the lane's three columns over rows j in [j0, j0+PJ), all six i-planes (fp64).
+// Row sums S = f0+f1+f2 and the lane-local k-weighted sum f1 + 2 f2 first; per plane i
+// P_i = sum_j S, Q_i = sum_j j S, Z_i = sum_j (f1 + 2 f2); Vz includes the lane's column offset 3h.
+template <typename T, bool IN_SMEM, int PJ>
+__device__ __forceinline__ void moments_partial(const T* __restrict__ xs, uint64_t si, uint64_t sj, int j0,
                                                 const LaneGeom& L, double V[4]) {
   double V0 = 0.0, Vx = 0.0, Vy = 0.0, Vz = 0.0;
-  double di = (double)i0;
+  double di = 0.0;
 #pragma unroll 1
-  for (int ii = 0; ii < P; ii++, di += 1.0) {
-    const int i = i0 + ii;
+  for (int i = 0; i < BS; i++, di += 1.0) {
     double Ps = 0.0, Q = 0.0, Z = 0.0;
-    const T* plane = IN_SMEM ? xs + (uint32_t)(i * BS * TK + L.kcol) : xs + (uint64_t)i * si + L.kcol;
+    const T* plane = IN_SMEM ? xs + (uint32_t)(i * BS * TK + j0 * TK + L.kcol) : xs + (uint64_t)i * si + (uint64_t)j0 * sj + L.kcol;
 #pragma unroll
-    for (int j = 0; j < BS; j++) {
-      const T* row = IN_SMEM ? plane + j * TK : plane + (uint64_t)j * sj;
+    for (int jj = 0; jj < PJ; jj++) {
+      const int j = j0 + jj;
+      const T* row = IN_SMEM ? plane + jj * TK : plane + (uint64_t)jj * sj;
       double f0, f1, f2;
       if (IN_SMEM) {
         f0 = to_d<T>(row[0]); f1 = to_d<T>(row[1]); f2 = to_d<T>(row[2]);
@@ -200,10 +207,17 @@ __device__ __forceinline__ void moments_partial(const T* __restrict__ xs, uint64
 
 // O5 (Lemma 1; extent-1 axis -> slope 0, G2) + O6 (codes; bins eb/2, eb/12, G1; zero
 // predictor fallback) from the full block moments; returns the decoded coefficients (bit-exact).
+template <bool FULL = false>
 __device__ __forceinline__ void block_coefs(const double V[4], const LaneGeom& L, const Consts& K, double beta[4],
                                             int32_t cc[4], double bh[4]) {
   beta[0] = beta[1] = beta[2] = beta[3] = 0.0;
-  if (L.m2 > 0) {
+  if (FULL) {  // 6x6x6 block: Nb = 216, 6/(m+1) = 6/7, 2/(m-1) = 2/5 (same values as the table path)
+    const double invNb = 1.0 / 216.0;
+    const double sc = (6.0 / 7.0) * invNb;
+#pragma unroll
+    for (int d = 0; d < 3; d++) beta[d + 1] = sc * fma(V[d + 1], 0.4, -V[0]);
+    beta[0] = V[0] * invNb - (2.5 * beta[1] + 2.5 * beta[2] + 2.5 * beta[3]);
+  } else if (L.m2 > 0) {
     const double Nb = (double)(L.m0 * L.m1 * L.m2);
     const double invNb = __drcp_rn(Nb);
     const int md[3] = {L.m0, L.m1, L.m2};
@@ -247,23 +261,58 @@ __device__ __forceinline__ void write_coefs(const CompressOut<T>& o, const TileC
   }
 }
 
-// O7-O11 over i-planes [i0, i0+P), branch-free: 3P independent elements per j so the fp64 chains
-// interleave.  FULL tiles (every element inside the grid) skip all validity predicates.  The
+// Exact O7-O10 for one element (the definition, fp64): code, or 0 for an outlier.
+template <typename T>
+__device__ __forceinline__ uint32_t exact_code(T xv, double p, const Consts& K, uint32_t R) {
+  const double xd = to_d<T>(xv);
+  const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+  const double sm = __dadd_rn(t, RINT_MAGIC);
+  const double q = __dsub_rn(sm, RINT_MAGIC);
+  const double y = __dadd_rn(p, __dmul_rn(K.twoeb, q));
+  const double d = __dsub_rn(to_d<T>(from_d<T>(y)), xd);
+  return (fabs(q) < (double)R && fabs(d) <= K.eb_abs) ? (uint32_t)(__double2loint(sm) + (int)R) : 0u;
+}
+
+// Per-block constants of the fp32 fast path (f32 data).
+//   E = |t32 - t| <= k1 |t32| + kS,   k1 = 3.1 u,   kS = 2.03 u S / eb + 1.2e-11 + 1e-44 / eb
+// with u = 2^-24, S = |b0| + 5 (|b1| + |b2| + |b3|) (derivation in DESIGN.md 4).  Accept the fp32
+// result when |t32 - r| + k1 |t32| + c |x| <= vthr - kS (evaluated with one-sided fp32 margins):
+// then t lies within E of t32, strictly inside r's rounding interval, so rint(t) = r, and the fp64
+// fast-verify condition |t - q| + c |x| <= vthr holds, so x' passes O9.
+struct Fast32 {
+  float b0, b1, b2, b3;  // decoded coefficients rounded to fp32
+  float c32, k1, thr;    // fp32 check constants
+};
+
+__device__ __forceinline__ Fast32 fast32_consts(const double bh[4], const Consts& K) {
+  Fast32 F;
+  F.b0 = __double2float_rn(bh[0]);
+  F.b1 = __double2float_rn(bh[1]);
+  F.b2 = __double2float_rn(bh[2]);
+  F.b3 = __double2float_rn(bh[3]);
+  const double u = 5.9604644775390625e-08;
+  const double S = fabs(bh[0]) + 5.0 * (fabs(bh[1]) + fabs(bh[2]) + fabs(bh[3]));
+  const double kS = 2.03 * u * S / K.eb_abs + 1.2e-11 + 1e-44 / K.eb_abs;
+  F.c32 = __double2float_ru(K.vc);
+  F.k1 = __double2float_ru(3.1 * u);
+  const double thr = (K.vthr - kS) * (1.0 - 4.0 * u);
+  F.thr = thr > 0.0 ? __double2float_rd(thr) : -1.0f;
+  return F;
+}
+
+// O7-O11 over rows j in [j0, j0+PJ), all six i-planes: per (j, k) column six independent elements
+// (i = 0..5).  f32 data take the fp32 fast path above (no conversions, full-rate pipe); f64 data
+// the fp64 fast verify of make_consts.  Elements the fast test cannot decide take the exact
+// definition (rare).  FULL tiles (every element inside the grid) skip all validity predicates.  The
 // histogram takes one red.shared per element at the code clamped into the smem window; codes
 // outside it and outliers (code 0) are flagged through the lane's running max of (code - lo) and
 // handled by rare_path().
-//
-// ok = |q| < R && |x' - x| <= eb is O8-O9 exactly: for |t| < 2^51, q = rint(t) and |t| >= R implies
-// |rint(t)| >= R (R integer, rint monotone); for |t| >= 2^51, NaN or Inf, |q| < R is false.  The
-// verify first tries the fast bound of make_consts (no conversion to T); only inconclusive elements
-// form x' = (T)(p + 2eb q) and compare |x' - x| <= eb in fp64 (<= agrees with !(> eb) there).
-template <typename T, bool IN_SMEM, bool HIST, bool FULL, int P>
-__device__ __forceinline__ uint32_t quantize_planes(const T* __restrict__ xs, uint64_t si, uint64_t sj,
-                                                    uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int i0,
-                                                    const LaneGeom& L, const double bh[4], const Consts& K,
-                                                    const uint32_t R, const HistSmem& hs) {
+template <typename T, bool IN_SMEM, bool HIST, bool FULL, int PJ>
+__device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+                                                  uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
+                                                  const LaneGeom& L, const double bh[4], const Consts& K,
+                                                  const uint32_t R, const HistSmem& hs) {
   const int lane = threadIdx.x & 31;
-  const double Rd = (double)R;
   const uint32_t win_base = HIST ? (uint32_t)__cvta_generic_to_shared(hs.win) : 0u;  // &win[c - lo]
   const uint32_t sink = HIST ? (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * lane : 0u;
   const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;   // window [lo, lo + nwin), lo >= 1
@@ -271,110 +320,100 @@ __device__ __forceinline__ uint32_t quantize_planes(const T* __restrict__ xs, ui
   if (IN_SMEM) {  // shared-memory tiles: compile-time strides -> immediate address offsets
     si = BS * TK; sj = TK; ci = BS * TK; cj = TK;
   }
-  double di[P], dk[3];
-#pragma unroll
-  for (int ii = 0; ii < P; ii++) di[ii] = (double)(i0 + ii);
-#pragma unroll
-  for (int kk = 0; kk < 3; kk++) dk[kk] = (double)(3 * L.h + kk);
-  const T* xbase = xs + (IN_SMEM ? (uint32_t)(i0 * BS * TK + L.kcol) : (uint64_t)i0 * si + L.kcol);
-  uint16_t* cbase = cs + (IN_SMEM ? (uint32_t)(i0 * BS * TK + L.kcol) : (uint64_t)i0 * ci + L.kcol);
-  double dj = 0.0;
+  constexpr bool F32 = sizeof(T) == 4;
+  const Fast32 F = fast32_consts(bh, K);
+  const float inv2eb32 = __double2float_rn(K.inv2eb);
+  const float Rf = (float)R;
+  const double Rd = (double)R;
 #pragma unroll 1
-  for (int j = 0; j < BS; j++, dj += 1.0) {
-    const bool jv = FULL || j < L.m1;
-    const T* xrow = xbase + (IN_SMEM ? (uint32_t)(j * TK) : (uint64_t)j * sj);  // + ii*si + kk
-    uint16_t* crow = cbase + (IN_SMEM ? (uint32_t)(j * TK) : (uint64_t)j * cj);
-    T xv[3][P];
+  for (int jk = 0; jk < 3 * PJ; jk++) {
+    const int jj = jk / 3, kk = jk - 3 * jj, j = j0 + jj;
+    const bool cv = FULL || ((j < L.m1) && L.kv(kk));
+    const T* xcol = xs + (IN_SMEM ? (uint32_t)(j * TK + L.kcol + kk) : (uint64_t)j * sj + L.kcol + kk);  // + i*si
+    uint16_t* ccol = cs + (IN_SMEM ? (uint32_t)(j * TK + L.kcol + kk) : (uint64_t)j * cj + L.kcol + kk);
+    T xv[BS];
 #pragma unroll
-    for (int kk = 0; kk < 3; kk++)
+    for (int i = 0; i < BS; i++) {
+      const bool valid = FULL || (cv && i < L.m0);
+      if (IN_SMEM || FULL) xv[i] = xcol[i * si];
+      else xv[i] = valid ? xcol[i * si] : T(0);
+    }
+    const double dj = (double)j, dk = (double)(3 * L.h + kk);
+    uint32_t code[BS];
+    bool need = false;   // some element the fast test cannot decide -> exact definition below
+    if (F32) {
+      // fp32 fast path: p32 = fma(b1, i, fma(b2, j, fma(b3, k, b0))) in fp32; bound in Fast32
+      const float base32 = __fmaf_rn(F.b2, (float)j, __fmaf_rn(F.b3, (float)(3 * L.h + kk), F.b0));
 #pragma unroll
-      for (int ii = 0; ii < P; ii++) {
-        const bool valid = FULL || (jv && L.kv(kk) && (i0 + ii < L.m0));
-        if (IN_SMEM || FULL) xv[kk][ii] = xrow[ii * si + kk];
-        else xv[kk][ii] = valid ? xrow[ii * si + kk] : T(0);
+      for (int i = 0; i < BS; i++) {
+        const float xf = (float)xv[i];
+        const float p32 = __fmaf_rn(F.b1, (float)i, base32);
+        const float t32 = __fmul_rn(__fsub_rn(xf, p32), inv2eb32);
+        const float s32 = __fadd_rn(t32, 12582912.0f);       // 1.5 * 2^23: rint for |t32| < 2^22
+        const float r = __fsub_rn(s32, 12582912.0f);
+        const float e = __fsub_rn(t32, r);                    // exact (Sterbenz)
+        const float v = __fmaf_rn(F.c32, fabsf(xf), __fmaf_rn(F.k1, fabsf(t32), fabsf(e)));
+        const bool ok = (v <= F.thr) && (fabsf(r) < Rf);
+        code[i] = ok ? (uint32_t)(__float_as_int(s32) - 0x4B400000 + (int)R) : 0u;   // O10
+        need |= !ok;
       }
-    uint32_t code[3][P];
-    bool need = false;   // some element has |q| < R but an inconclusive fast verify -> exact O9 below
+    } else {
+      const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk, bh[0]));
 #pragma unroll
-    for (int kk = 0; kk < 3; kk++) {
-      // O7 hoisted: base = fma(b2, j, fma(b3, k, b0)), p = fma(b1, i, base)
-      const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk[kk], bh[0]));
-#pragma unroll
-      for (int ii = 0; ii < P; ii++) {
-        const double xd = to_d<T>(xv[kk][ii]);
-        const double p = __fma_rn(bh[1], di[ii], base);
-        // O8: t = (x - p) * inv2eb ; q = rint(t) (1.5*2^52 trick, ties-to-even)
+      for (int i = 0; i < BS; i++) {
+        const double xd = to_d<T>(xv[i]);
+        const double p = __fma_rn(bh[1], (double)i, base);
         const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
         const double sm = __dadd_rn(t, RINT_MAGIC);
         const double q = __dsub_rn(sm, RINT_MAGIC);
-        // O9 fast verify (bound in make_consts)
-        const double v = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, q)));
-        const bool qok = fabs(q) < Rd;
-        const bool fast = v <= K.vthr;
-        const uint32_t c = (uint32_t)(__double2loint(sm) + (int)R);
-        code[kk][ii] = (qok && fast) ? c : 0u;   // O10
-        need |= qok && !fast;
+        const double v = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, q)));   // fast verify (make_consts)
+        const bool ok = (v <= K.vthr) && (fabs(q) < Rd);
+        code[i] = ok ? (uint32_t)(__double2loint(sm) + (int)R) : 0u;
+        need |= !ok;
       }
     }
     if (__any_sync(0xffffffffu, need)) {
-      // exact O9 for the inconclusive elements: x' = (T)(p + twoeb*q), outlier if |x' - x| > eb
+      const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk, bh[0]));
 #pragma unroll
-      for (int kk = 0; kk < 3; kk++) {
-        const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk[kk], bh[0]));
-#pragma unroll
-        for (int ii = 0; ii < P; ii++) {
-          const double xd = to_d<T>(xv[kk][ii]);
-          const double p = __fma_rn(bh[1], di[ii], base);
-          const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
-          const double sm = __dadd_rn(t, RINT_MAGIC);
-          const double q = __dsub_rn(sm, RINT_MAGIC);
-          const double v = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, q)));
-          if (fabs(q) < Rd && !(v <= K.vthr)) {
-            const double y = __dadd_rn(p, __dmul_rn(K.twoeb, q));
-            const double d = __dsub_rn(to_d<T>(from_d<T>(y)), xd);
-            code[kk][ii] = (fabs(d) <= K.eb_abs) ? (uint32_t)(__double2loint(sm) + (int)R) : 0u;
-          }
-        }
-      }
+      for (int i = 0; i < BS; i++)
+        if (code[i] == 0u) code[i] = exact_code<T>(xv[i], __fma_rn(bh[1], (double)i, base), K, R);
     }
 #pragma unroll
-    for (int kk = 0; kk < 3; kk++)
-#pragma unroll
-      for (int ii = 0; ii < P; ii++) {
-        const bool valid = FULL || (jv && L.kv(kk) && (i0 + ii < L.m0));
-        const uint32_t c = code[kk][ii];
-        if (valid) crow[ii * ci + kk] = (uint16_t)c;
-        const uint32_t uc = c - wlo;                     // code 0 (outlier) wraps to a huge value
-        if (FULL) umax = max(umax, uc);
-        else if (valid) umax = max(umax, uc);
-        if (HIST) {  // O11: counted at the clamped bin; out-of-window codes corrected in rare_path
-          const uint32_t cw = min(uc, wtop);
-          red_smem_add(FULL ? win_base + 4u * cw : (valid ? win_base + 4u * cw : sink), FULL ? 1u : (valid ? 1u : 0u));
-        }
+    for (int i = 0; i < BS; i++) {
+      const bool valid = FULL || (cv && i < L.m0);
+      const uint32_t c = code[i];
+      if (valid) ccol[i * ci] = (uint16_t)c;
+      const uint32_t uc = c - wlo;                     // code 0 (outlier) wraps to a huge value
+      if (FULL) umax = max(umax, uc);
+      else if (valid) umax = max(umax, uc);
+      if (HIST) {  // O11: counted at the clamped bin; out-of-window codes corrected in rare_path
+        const uint32_t cw = min(uc, wtop);
+        red_smem_add(FULL ? win_base + 4u * cw : (valid ? win_base + 4u * cw : sink), FULL ? 1u : (valid ? 1u : 0u));
       }
+    }
   }
   return umax;
 }
 
-// Rare path (warp-uniform entry): outliers of i-planes [i0, i0+P) -> (global index, value) with a
+// Rare path (warp-uniform entry): outliers of rows [j0, j0+PJ) -> (global index, value) with a
 // warp-aggregated append; histogram correction for codes outside the window (counted at the top
 // bin): moved to the global histogram / the zero counter.
-template <typename T, bool HIST, int P>
+template <typename T, bool HIST, int PJ>
 __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si, uint64_t sj,
-                                          const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int i0,
+                                          const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
                                           const LaneGeom& L, uint32_t umax, const TileCoord tc, const Geo& g,
                                           const CompressOut<T>& o, const HistSmem& hs) {
   const int lane = threadIdx.x & 31;
   const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;
   const bool has_rare = umax > wtop;
   if (!__any_sync(0xffffffffu, has_rare)) return;
-  const int i1 = min(i0 + P, L.m0);
+  const int j1 = min(j0 + PJ, L.m1);
   uint32_t nout = 0;
   if (has_rare) {
-    for (int j = 0; j < L.m1; j++)
+    for (int j = j0; j < j1; j++)
       for (int kk = 0; kk < 3; kk++) {
         if (!L.kv(kk)) continue;
-        for (int i = i0; i < i1; i++) {
+        for (int i = 0; i < L.m0; i++) {
           const uint32_t c = cs[i * ci + j * cj + L.kcol + kk];
           nout += (c == 0u) ? 1u : 0u;
           if (HIST && c != 0u && c - wlo > wtop) {   // counted at the top bin: move to global
@@ -405,10 +444,10 @@ __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si,
   if (nout) {
     const uint64_t gbase =
         g.gofs + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)L.kb * BS + 3 * L.h;
-    for (int j = 0; j < L.m1; j++)
+    for (int j = j0; j < j1; j++)
       for (int kk = 0; kk < 3; kk++) {
         if (!L.kv(kk)) continue;
-        for (int i = i0; i < i1; i++) {
+        for (int i = 0; i < L.m0; i++) {
           if (cs[i * ci + j * cj + L.kcol + kk] != 0) continue;
           if (pos < o.cap) {
             o.oidx[pos] = gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk;
@@ -426,18 +465,16 @@ __device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t
                                               uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
                                               const TileCoord tc, const Geo& g, const Consts& K,
                                               const uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
-  const LaneGeom L = lane_geom(tc, g);
+  const LaneGeom L = lane_geom<FULL>(tc, g);
   double V[4], beta[4], bh[4];
   int32_t cc[4];
   moments_partial<T, IN_SMEM, BS>(xs, si, sj, 0, L, V);
 #pragma unroll
   for (int d = 0; d < 4; d++) V[d] += __shfl_xor_sync(0xffffffffu, V[d], 1);
-  block_coefs(V, L, K, beta, cc, bh);
+  block_coefs<FULL>(V, L, K, beta, cc, bh);
   write_coefs(o, tc, g, L, cc, beta);
-  const uint32_t umax = quantize_planes<T, IN_SMEM, HIST, FULL, 2>(xs, si, sj, cs, ci, cj, 0, L, bh, K, R, hs) ;
-  const uint32_t umax2 = quantize_planes<T, IN_SMEM, HIST, FULL, 2>(xs, si, sj, cs, ci, cj, 2, L, bh, K, R, hs);
-  const uint32_t umax3 = quantize_planes<T, IN_SMEM, HIST, FULL, 2>(xs, si, sj, cs, ci, cj, 4, L, bh, K, R, hs);
-  rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, L, max(umax, max(umax2, umax3)), tc, g, o, hs);
+  const uint32_t umax = quantize_rows<T, IN_SMEM, HIST, FULL, BS>(xs, si, sj, cs, ci, cj, 0, L, bh, K, R, hs);
+  rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, L, umax, tc, g, o, hs);
 }
 
 // ------------------------------------------------------------------------------------------
