@@ -261,3 +261,43 @@ def test_repeat_determinism_full_size(name):
     assert torch.equal(r.coef_raw, raw0)
     assert torch.equal(out.view(torch.int32 if x.dtype == torch.float32 else torch.int64),
                        xo0.view(torch.int32 if x.dtype == torch.float32 else torch.int64))
+
+
+# ----------------------------------------------------------------------------- fast-path boundaries
+def adversarial_case(kind):
+    rng = np.random.default_rng(77)
+    dims = (12, 18, 96)
+    i, j, k = np.meshgrid(*[np.arange(n) for n in dims], indexing="ij")
+    if kind == "half_bins":        # linear field + checkerboard of +-3.5 bins: moments unchanged, t = +-3.5 exactly
+        eb = 2.0 ** -6
+        f = 0.25 * i - 0.125 * j + 0.0625 * k + ((-1.0) ** (i + j + k)) * 3.5 * 2 * eb
+        return f.astype(np.float32), eb, "abs", 32768
+    if kind == "near_half":        # half-bins +- a few ulps
+        eb = 2.0 ** -6
+        f = (0.25 * i + (rng.integers(-40, 40, size=dims) + 0.5) * 2 * eb).astype(np.float32)
+        f = np.nextafter(f, np.where(rng.random(dims) < 0.5, np.inf, -np.inf).astype(np.float32))
+        return f.astype(np.float32), eb, "abs", 32768
+    if kind == "offset":           # large offset: the fp32 bound rejects most elements
+        return (1e6 + rng.normal(size=dims) * 0.5).astype(np.float32), 1e-3, "abs", 32768
+    if kind == "float_resolution": # eb below half an f32 ulp of the data: x' rounding fails the verify
+        return (100 + 0.01 * np.sin(0.3 * i + 0.2 * j + 0.1 * k) + 1e-4 * rng.normal(size=dims)).astype(np.float32), \
+            5e-6, "abs", 32768   # ulp(100)/2 < eb < ulp(100)
+    if kind == "denormal":
+        return (rng.normal(size=dims) * 1e-39).astype(np.float32), 1e-41, "abs", 32768
+    if kind == "huge_eb":
+        return (rng.normal(size=dims) * 1e30).astype(np.float32), 1e31, "abs", 16
+    if kind == "wide_range":       # heavy tails, REL eb, small radius
+        return np.exp(4 * rng.normal(size=dims)).astype(np.float32), 1e-4, "rel", 256
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+@pytest.mark.parametrize("kind", ["half_bins", "near_half", "offset", "float_resolution", "denormal", "huge_eb",
+                                  "wide_range"])
+def test_fast_path_boundaries(kind, flags):
+    f, eb, mode, R = adversarial_case(kind)
+    rep = check(f, eb, mode, R, flags)
+    if kind == "half_bins":
+        assert rep["counters"]["elem_near_ties"] == f.size
+    if kind == "float_resolution":
+        assert rep["counters"]["verify_outliers"] > 0
