@@ -134,7 +134,18 @@ struct KArgs {
   int32_t* d_status;
   double uround;  // fast-verify roundoff constant of T
   uint32_t pf;    // L2 prefetch distance of the TMA producers, tiles per CTA
+  uint32_t chunk; // adjacent tiles per CTA chunk of the persistent kernels' schedule (>= 1)
 };
+
+// The persistent kernels' tile sequence of one CTA: chunks of C adjacent tiles, chunks strided over
+// the grid: t(n) = ((n / C) * grid + cta) * C + n % C, increasing in n (stop at t >= ntiles).
+// Adjacent tiles share DRAM write units of the outputs (a 96-wide tile row is 192 B of codes or
+// 384 B of f32): on different SMs at different times the partially written units are evicted and
+// read back (ncu: +31% DRAM reads); chunks keep them on one SM while the grid-wide working set stays
+// a compact band of the field (good DRAM page locality).
+__device__ __forceinline__ uint64_t tile_at(uint64_t n, uint32_t C) {
+  return ((n / C) * gridDim.x + blockIdx.x) * C + n % C;
+}
 
 __device__ __forceinline__ void hist_init(HistSmem& hs, uint32_t* win, uint32_t* zero, uint32_t R) {
   hs.win = win;
@@ -330,16 +341,21 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     // ---------------- producer
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_x);
-      for (uint64_t p = 0, t = blockIdx.x; p < a.pf && t < g.ntiles; p++, t += Gr) {
-        const TileCoord tc = decode_tile(t, g);
+      for (uint64_t p = 0; p < a.pf; p++) {
+        const uint64_t tp = tile_at(p, a.chunk);
+        if (tp >= g.ntiles) break;
+        const TileCoord tc = decode_tile(tp, g);
         ptx::tma_prefetch_3d(&tm_x, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
       }
-      uint32_t n = 0;
-      for (uint64_t t = blockIdx.x; t < g.ntiles; t += Gr, n++) {
-        const uint64_t tp = t + (uint64_t)a.pf * Gr;
-        if (a.pf && tp < g.ntiles) {
-          const TileCoord tq = decode_tile(tp, g);
-          ptx::tma_prefetch_3d(&tm_x, (int)(tq.c * TK), (int)(tq.b * BS), (int)(tq.a * BS));
+      for (uint32_t n = 0;; n++) {
+        const uint64_t t = tile_at(n, a.chunk);
+        if (t >= g.ntiles) break;
+        if (a.pf) {
+          const uint64_t tp = tile_at(n + a.pf, a.chunk);
+          if (tp < g.ntiles) {
+            const TileCoord tq = decode_tile(tp, g);
+            ptx::tma_prefetch_3d(&tm_x, (int)(tq.c * TK), (int)(tq.b * BS), (int)(tq.a * BS));
+          }
         }
         const uint32_t k = n / NG, s = (n % NG) * D + k % D, ph = (k / D) & 1u;
         ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
@@ -357,7 +373,9 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     uint16_t* mycodes = cbuf + (size_t)grp * TILE_ELEMS;
     double* myexch = exch + (size_t)grp * G * 4 * 32;
     uint32_t k = 0;
-    for (uint64_t t = blockIdx.x + (uint64_t)grp * Gr; t < g.ntiles; t += (uint64_t)NG * Gr, k++) {
+    for (uint64_t n = grp;; n += NG, k++) {
+      const uint64_t t = tile_at(n, a.chunk);
+      if (t >= g.ntiles) break;
       const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
       const TileCoord tc = decode_tile(t, g);
       if (codes_tma && wg == 0 && lane == 0) ptx::bulk_wait_read0();  // previous store done reading mycodes
@@ -402,87 +420,107 @@ __global__ void __launch_bounds__(128) k_decompress_plain(const uint16_t* __rest
   for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < g.ntiles; t += warps) {
     const TileCoord tc = decode_tile(t, g);
     const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
-    decompress_tile<T, false, false>(codes + off, g.n1 * g.n2, g.n2, xo + off, g.n1 * g.n2, g.n2, tc, g, K, a.R,
-                                     coef);
+    const LaneGeom L = lane_geom<false>(tc, g);
+    int4 cc = make_int4(0, 0, 0, 0);
+    if (L.m2 > 0) cc = __ldg(reinterpret_cast<const int4*>(coef) + ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb);
+    double bh[4];
+    decode_coefs(cc, K, bh);
+    decompress_rows<T, false, false, false, BS>(codes + off, g.n1 * g.n2, g.n2, xo + off, g.n1 * g.n2, g.n2, 0, L, bh,
+                                                K, a.R);
   }
 }
 
-template <typename T, int W, int D>
+// Persistent, one CTA per SM, same producer / private-ring structure as k_compress_tma.  A stage
+// holds a tile's codes (TMA, 6x6x96 u16) and its <= 16 blocks' coefficient codes (1D bulk copy,
+// 16 B per block).  A group of G warps shares a stage; each warp decodes rows [j0, j0 + 6/G) into
+// its own shared row slab and TMA-stores it (box {96, 6/G, 6}).  The stage is released through an
+// empty barrier with G arrivals, so there is no group barrier at all.
+template <typename T, int G, int NG, int D>
 struct DecompressSmem {
-  static constexpr int S = W * D;
-  static constexpr size_t stage_bytes = sizeof(uint16_t) * TILE_ELEMS;
-  static constexpr size_t out_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr int P = BS / G;
+  static constexpr int S = NG * D;
+  static constexpr size_t code_bytes = sizeof(uint16_t) * TILE_ELEMS;
+  static constexpr size_t stage_bytes = code_bytes + 16 * 16;            // codes + 16 coefficient codes
+  static constexpr size_t slab_bytes = sizeof(T) * BS * P * TK;          // one warp's output rows
   static constexpr size_t off_out = S * stage_bytes;
-  static constexpr size_t off_bar = off_out + W * out_bytes;
+  static constexpr size_t off_bar = off_out + (size_t)NG * G * slab_bytes;
   static constexpr size_t off_k = off_bar + 2 * S * sizeof(uint64_t);
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
 };
 
-// Same producer / private-ring structure as k_compress_tma with single-warp consumers.
-template <typename T, int W, int D>
-__global__ void __launch_bounds__((W + 1) * 32, 1)
+template <typename T, int G, int NG, int D>
+__global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     k_decompress_tma(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_x,
                      const int32_t* __restrict__ coef, KArgs a) {
-  using L = DecompressSmem<T, W, D>;
-  constexpr int S = L::S;
+  using L_ = DecompressSmem<T, G, NG, D>;
+  constexpr int P = L_::P;
+  constexpr int S = L_::S;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint16_t* stages = reinterpret_cast<uint16_t*>(smem);
-  T* obuf = reinterpret_cast<T*>(smem + L::off_out);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint8_t* stages = smem;
+  T* obuf = reinterpret_cast<T*>(smem + L_::off_out);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
   uint64_t* empty = full + S;
-  Consts* s_k = reinterpret_cast<Consts*>(smem + L::off_k);
-  int* s_ok = reinterpret_cast<int*>(smem + L::off_k + sizeof(Consts));
+  Consts* s_k = reinterpret_cast<Consts*>(smem + L_::off_k);
+  int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], G);
     }
     ptx::fence_mbar_init();
   }
   if (!cta_consts(a, s_k, s_ok)) return;
   const Geo& g = a.g;
-  const uint64_t G = gridDim.x;
-  if (warp == W) {
+  const uint64_t Gr = gridDim.x;
+  if (warp == NG * G) {
+    // ---------------- producer
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_c);
-      for (uint64_t p = 0, t = blockIdx.x; p < a.pf && t < g.ntiles; p++, t += G) {
-        const TileCoord tc = decode_tile(t, g);
-        ptx::tma_prefetch_3d(&tm_c, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
-      }
-      uint32_t n = 0;
-      for (uint64_t t = blockIdx.x; t < g.ntiles; t += G, n++) {
-        const uint64_t tp = t + (uint64_t)a.pf * G;
-        if (a.pf && tp < g.ntiles) {
-          const TileCoord tq = decode_tile(tp, g);
-          ptx::tma_prefetch_3d(&tm_c, (int)(tq.c * TK), (int)(tq.b * BS), (int)(tq.a * BS));
-        }
-        const uint32_t k = n / W, s = (n % W) * D + k % D, ph = (k / D) & 1u;
+      for (uint32_t n = 0;; n++) {
+        const uint64_t t = tile_at(n, a.chunk);
+        if (t >= g.ntiles) break;
+        const uint32_t k = n / NG, s = (n % NG) * D + k % D, ph = (k / D) & 1u;
         ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
         const TileCoord tc = decode_tile(t, g);
-        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L::stage_bytes);
-        ptx::tma_load_3d(stages + (size_t)s * TILE_ELEMS, &tm_c, &full[s], (int)(tc.c * TK), (int)(tc.b * BS),
-                         (int)(tc.a * BS));
+        const uint32_t nblk = min(16u, g.NB2 - tc.c * 16u);
+        uint8_t* st = stages + (size_t)s * L_::stage_bytes;
+        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L_::code_bytes + 16u * nblk);
+        ptx::tma_load_3d(st, &tm_c, &full[s], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+        const uint64_t bid0 = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + (uint64_t)tc.c * 16u;
+        ptx::bulk_load(st + L_::code_bytes, coef + 4 * bid0, 16u * nblk, &full[s]);
       }
     }
   } else {
+    // ---------------- consumer groups: warp wg of group grp decodes rows [j0, j0 + P)
+    const int grp = warp / G, wg = warp - grp * G, j0 = wg * P;
     const Consts K = *s_k;
-    T* myout = obuf + (size_t)warp * TILE_ELEMS;
+    T* myout = obuf + (size_t)warp * (BS * P * TK);
     uint32_t k = 0;
-    for (uint64_t t = blockIdx.x + (uint64_t)warp * G; t < g.ntiles; t += (uint64_t)W * G, k++) {
-      const uint32_t s = warp * D + k % D, ph = (k / D) & 1u;
+    for (uint64_t n = grp;; n += NG, k++) {
+      const uint64_t t = tile_at(n, a.chunk);
+      if (t >= g.ntiles) break;
+      const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
       const TileCoord tc = decode_tile(t, g);
-      if (lane == 0) ptx::bulk_wait_read0();
+      if (lane == 0) ptx::bulk_wait_read0();   // my previous slab store finished reading myout
       __syncwarp();
       ptx::mbar_wait(&full[s], ph);
-      decompress_tile<T, true, true>(stages + (size_t)s * TILE_ELEMS, BS * TK, TK, myout, BS * TK, TK, tc, g, K,
-                                     a.R, coef);
+      const uint8_t* st = stages + (size_t)s * L_::stage_bytes;
+      const uint16_t* cst = reinterpret_cast<const uint16_t*>(st);
+      const bool full_tile = tile_full(tc, g);
+      const LaneGeom L = full_tile ? lane_geom<true>(tc, g) : lane_geom<false>(tc, g);
+      int4 cc = make_int4(0, 0, 0, 0);
+      if (L.m2 > 0) cc = reinterpret_cast<const int4*>(st + L_::code_bytes)[lane >> 1];
+      double bh[4];
+      decode_coefs(cc, K, bh);
+      if (full_tile) decompress_rows<T, true, true, true, P>(cst, BS * TK, TK, myout, 0, 0, j0, L, bh, K, a.R);
+      else decompress_rows<T, true, true, false, P>(cst, BS * TK, TK, myout, 0, 0, j0, L, bh, K, a.R);
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);   // this warp no longer reads the stage
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        ptx::tma_store_3d(&tm_x, myout, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+        ptx::tma_store_3d(&tm_x, myout, (int)(tc.c * TK), (int)(tc.b * BS + j0), (int)(tc.a * BS));
         ptx::bulk_commit();
       }
     }
@@ -577,16 +615,21 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 3D tensor map over a row-major (n0, n1, n2) array, box {96, 6, 6}
-bool make_map(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, const Geo& g) {
+// 3D tensor map over a row-major (n0, n1, n2) array, box {96, box_j, 6}.  Store maps use no L2
+// promotion: with 256-B promotion a 384-B (or 192-B) row covers 1.5 promoted blocks and L2 fills the
+// unwritten half from DRAM (ncu: DRAM reads = 1/3 of the bytes written).
+bool make_map(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, const Geo& g, int box_j = BS,
+              bool store = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[3] = {g.n2, g.n1, g.n0};
   const cuuint64_t strides[2] = {g.n2 * esize, g.n1 * g.n2 * esize};
-  const cuuint32_t box[3] = {(cuuint32_t)TK, (cuuint32_t)BS, (cuuint32_t)BS};
+  const cuuint32_t box[3] = {(cuuint32_t)TK, (cuuint32_t)box_j, (cuuint32_t)BS};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_NONE,
+                  store ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -637,6 +680,18 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 // tuned configurations: (consumer warps, ring stages); smem fits the 227 KiB per-CTA limit
 constexpr int PF_TILES = 0;         // default L2 prefetch distance (tiles per CTA); 0: prefetched lines were evicted before use (ncu: +47% DRAM reads on c5)
 
+uint32_t chunk_tiles(bool decompress) {  // SZ3G_CHUNK_C / SZ3G_CHUNK_D override (tuning only)
+  static uint32_t vc = [] {
+    const char* e = getenv("SZ3G_CHUNK_C");
+    return e ? (uint32_t)std::max(1, atoi(e)) : 2u;
+  }();
+  static uint32_t vd = [] {
+    const char* e = getenv("SZ3G_CHUNK_D");
+    return e ? (uint32_t)std::max(1, atoi(e)) : 16u;
+  }();
+  return decompress ? vd : vc;
+}
+
 uint32_t prefetch_tiles() {  // SZ3G_PF overrides (tuning only)
   static uint32_t v = [] {
     const char* e = getenv("SZ3G_PF");
@@ -646,8 +701,8 @@ uint32_t prefetch_tiles() {  // SZ3G_PF overrides (tuning only)
 }
 constexpr int CG32 = 3, CN32 = 5, CD32 = 2;  // f32 compress: 5 groups x 3 warps + producer = 16 warps; 2 x 13.5 KiB stages per group
 constexpr int CG64 = 6, CN64 = 2, CD64 = 2;  // f64 compress: 2 groups x 6 warps + producer = 13 warps; 2 x 27 KiB stages per group
-constexpr int DW32 = 8, DD32 = 2;   // f32 decompress: 8 warps x 2 x 6.75 KiB code stages + 8 x 13.5 KiB output tiles
-constexpr int DW64 = 5, DD64 = 2;   // f64 decompress: 5 warps x 2 x 6.75 KiB + 5 x 27 KiB
+constexpr int DG32 = 3, DN32 = 5, DD32 = 3;  // f32 decompress: 5 groups x 3 warps + producer; 3 x 7 KiB stages per group
+constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 warps + producer
 
 template <typename T, int G, int NG, int D, bool HIST>
 int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
@@ -658,7 +713,7 @@ int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
   memset(&mc, 0, sizeof(mc));
-  if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) codes_tma = false;
+  if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g, BS, true)) codes_tma = false;
   auto kern = k_compress_tma<T, G, NG, D, HIST>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -667,20 +722,20 @@ int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes
   return check_launch(1);
 }
 
-template <typename T, int W, int D>
+template <typename T, int G, int NG, int D>
 int launch_decompress_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, void* xo, const KArgs& ka,
                           cudaStream_t st) {
-  using L = DecompressSmem<T, W, D>;
+  using L = DecompressSmem<T, G, NG, D>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mc, mx;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) return SZ3G_ECUDA;
-  if (!make_map(&mx, dt, sizeof(T), xo, g)) return SZ3G_ECUDA;
-  auto kern = k_decompress_tma<T, W, D>;
+  if (!make_map(&mx, dt, sizeof(T), xo, g, L::P, true)) return SZ3G_ECUDA;
+  auto kern = k_decompress_tma<T, G, NG, D>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
-  kern<<<(unsigned)grid, (W + 1) * 32, L::total, st>>>(mc, mx, coef, ka);
+  kern<<<(unsigned)grid, (NG * G + 1) * 32, L::total, st>>>(mc, mx, coef, ka);
   return check_launch(1);
 }
 
@@ -730,6 +785,7 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
   ka.d_eb_abs = d_eb_abs;
   ka.d_status = d_status;
   ka.pf = prefetch_tiles();
+  ka.chunk = chunk_tiles(false);
   ka.uround = grid->dtype == SZ3G_F32 ? (5.9604644775390625e-08 + 1.12e-16) : 2.3e-16;
   const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
   const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
@@ -778,6 +834,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   ka.eb = params->eb;
   ka.d_minmax = d_minmax;
   ka.pf = prefetch_tiles();
+  ka.chunk = chunk_tiles(true);
   int32_t* dummy_status = nullptr;  // decompress never reports: eb validated on the host
   ka.d_status = dummy_status;
   const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
@@ -787,7 +844,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   int launched = 0;
   if (grid->dtype == SZ3G_F32) {
     if (tma) {
-      rc = launch_decompress_tma<float, DW32, DD32>(g, codes, coef_codes, x_out, ka, st);
+      rc = launch_decompress_tma<float, DG32, DN32, DD32>(g, codes, coef_codes, x_out, ka, st);
       if (rc) return rc;
     } else {
       const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
@@ -802,7 +859,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
     }
   } else {
     if (tma) {
-      rc = launch_decompress_tma<double, DW64, DD64>(g, codes, coef_codes, x_out, ka, st);
+      rc = launch_decompress_tma<double, DG64, DN64, DD64>(g, codes, coef_codes, x_out, ka, st);
       if (rc) return rc;
     } else {
       const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));

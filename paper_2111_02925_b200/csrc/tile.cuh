@@ -478,49 +478,49 @@ __device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t
 }
 
 // ------------------------------------------------------------------------------------------
-// Decompress one tile (recover): x' = (T)(p + twoeb*(c - R)) for c != 0, 0 for c == 0
-// (outlier values are scattered afterwards).  Codes read from cs + (ci, cj) (smem stage or
-// global, predicated), x' written to xo + (oi, oj) (smem staging or global, predicated).
+// Decompress (recover): x' = (T)(p + twoeb*(c - R)) for c != 0, 0 for c == 0 (outlier values
+// are scattered afterwards) over rows j in [j0, j0+PJ), all six i-planes.  Codes are read from
+// cs[i*ci + j*cj + k] (shared stage or global, predicated); x' goes to a shared row slab laid out
+// [i][jj][k] for a TMA store of box {96, PJ, 6} (OUT_SMEM) or straight to global xo[i*oi + j*oj + k].
 // ------------------------------------------------------------------------------------------
-template <typename T, bool IN_SMEM, bool OUT_SMEM>
-__device__ __forceinline__ void decompress_tile(const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
-                                                T* __restrict__ xo, uint64_t oi, uint64_t oj, const TileCoord tc,
-                                                const Geo& g, const Consts& K, const uint32_t R,
-                                                const int32_t* __restrict__ coef) {
-  const int lane = threadIdx.x & 31;
-  const int bl = lane >> 1, h = lane & 1;
-  const uint32_t kb = tc.c * 16u + (uint32_t)bl;
-  const int m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
-  const int m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
-  const int m2 = (kb < g.NB2) ? (int)umin64(BS, g.n2 - (uint64_t)kb * BS) : 0;
-  const int kcol = 6 * bl + 3 * h;
-  int4 cc = make_int4(0, 0, 0, 0);
-  const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + kb;
-  if (m2 > 0) cc = __ldg(reinterpret_cast<const int4*>(coef) + bid);
-  const double bh0 = __dmul_rn((double)cc.x, K.w0);
-  const double bh1 = __dmul_rn((double)cc.y, K.ws);
-  const double bh2 = __dmul_rn((double)cc.z, K.ws);
-  const double bh3 = __dmul_rn((double)cc.w, K.ws);
+__device__ __forceinline__ void decode_coefs(const int4 cc, const Consts& K, double bh[4]) {
+  bh[0] = __dmul_rn((double)cc.x, K.w0);
+  bh[1] = __dmul_rn((double)cc.y, K.ws);
+  bh[2] = __dmul_rn((double)cc.z, K.ws);
+  bh[3] = __dmul_rn((double)cc.w, K.ws);
+}
+
+template <typename T, bool IN_SMEM, bool OUT_SMEM, bool FULL, int PJ>
+__device__ __forceinline__ void decompress_rows(const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
+                                                T* __restrict__ xo, uint64_t oi, uint64_t oj, int j0,
+                                                const LaneGeom& L, const double bh[4], const Consts& K,
+                                                const uint32_t R) {
+  if (IN_SMEM) { ci = BS * TK; cj = TK; }
   const double cR = __dadd_rn(I2D_MAGIC, (double)R);  // exact: 2^52 + R
 #pragma unroll 1
-  for (int j = 0; j < BS; j++) {
+  for (int jk = 0; jk < 3 * PJ; jk++) {
+    const int jj = jk / 3, kk = jk - 3 * jj, j = j0 + jj;
+    const bool cv = FULL || ((j < L.m1) && L.kv(kk));
+    const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * L.h + kk), bh[0]));
+    const uint16_t* ccol = cs + (IN_SMEM ? (uint32_t)(j * TK + L.kcol + kk) : (uint64_t)j * cj + L.kcol + kk);
+    T* ocol = xo + (OUT_SMEM ? (uint32_t)(jj * TK + L.kcol + kk) : (uint64_t)j * oj + L.kcol + kk);
+    uint32_t c[BS];
 #pragma unroll
-    for (int kk = 0; kk < 3; kk++) {
-      const bool kv = (3 * h + kk < m2) && (j < m1);
-      const double base = __fma_rn(bh2, (double)j, __fma_rn(bh3, (double)(3 * h + kk), bh0));
+    for (int i = 0; i < BS; i++) {
+      const bool valid = FULL || (cv && i < L.m0);
+      if (IN_SMEM || FULL) c[i] = ccol[i * ci];
+      else c[i] = valid ? ccol[i * ci] : 0u;
+    }
 #pragma unroll
-      for (int i = 0; i < BS; i++) {
-        const bool valid = kv && (i < m0);
-        uint32_t c;
-        if (IN_SMEM) c = cs[i * ci + j * cj + kcol + kk];
-        else c = valid ? cs[i * ci + j * cj + kcol + kk] : 0u;
-        const double p = __fma_rn(bh1, (double)i, base);
-        // (double)(c - R) exactly, without an int->fp conversion: hi/lo = 2^52 + c, minus 2^52 + R
-        const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)c), cR);
-        const double y = __dadd_rn(p, __dmul_rn(K.twoeb, qd));
-        const T xv = c ? from_d<T>(y) : T(0);
-        if (OUT_SMEM || valid) xo[i * oi + j * oj + kcol + kk] = xv;
-      }
+    for (int i = 0; i < BS; i++) {
+      const bool valid = FULL || (cv && i < L.m0);
+      const double p = __fma_rn(bh[1], (double)i, base);
+      // (double)(c - R) exactly, without an int->fp conversion: hi/lo = 2^52 + c, minus 2^52 + R
+      const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)c[i]), cR);
+      const double y = __dadd_rn(p, __dmul_rn(K.twoeb, qd));
+      const T xv = c[i] ? from_d<T>(y) : T(0);
+      if (OUT_SMEM) ocol[i * (PJ * TK)] = xv;
+      else if (valid) ocol[i * oi] = xv;
     }
   }
 }
