@@ -56,15 +56,20 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
   return ok != 0;
 }
 
+// consumer-side wait: one probe, then probes with a short sleep (a polling warp steals issue slots
+// from the warps that share its scheduler)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait_sleep(bar, parity)) {
+  if (mbar_try_wait(bar, parity)) return;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(64);
   }
 }
 
 // producer-side wait with back-off: a spinning producer lane steals issue slots from the consumer
 // warps that share its SM sub-partition
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait_sleep(bar, parity)) {
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(400);
   }
 }
 

@@ -147,6 +147,26 @@ __device__ __forceinline__ uint64_t tile_at(uint64_t n, uint32_t C) {
   return ((n / C) * gridDim.x + blockIdx.x) * C + n % C;
 }
 
+// The same sequence walked incrementally with a fixed stride in n (no division per tile).
+struct TileWalk {
+  uint64_t chunk;   // n / C
+  uint32_t w;       // n % C
+  uint32_t C, stride_c, stride_w;  // stride in n = stride_c * C + stride_w
+  __device__ __forceinline__ TileWalk(uint32_t n0, uint32_t C_, uint32_t stride) {
+    C = C_;
+    chunk = n0 / C;
+    w = n0 % C;
+    stride_c = stride / C;
+    stride_w = stride % C;
+  }
+  __device__ __forceinline__ uint64_t tile() const { return (chunk * gridDim.x + blockIdx.x) * C + w; }
+  __device__ __forceinline__ void next() {
+    chunk += stride_c;
+    w += stride_w;
+    if (w >= C) { w -= C; chunk++; }
+  }
+};
+
 __device__ __forceinline__ void hist_init(HistSmem& hs, uint32_t* win, uint32_t* zero, uint32_t R) {
   hs.win = win;
   hs.zero = zero;
@@ -247,81 +267,111 @@ __global__ void __launch_bounds__(128) k_compress_plain(const T* __restrict__ x,
 }
 
 // ---------------------------------------------------------------------------------- compress, TMA
-// Persistent, one CTA per SM.  Warp NG*G is the producer (one elected lane streams 6x6x96 tiles with
-// TMA).  The other NG*G warps form NG groups of G warps; a group takes one tile at a time (group g:
-// the CTA's tiles g, g+NG, ...), each warp owning P = 6/G rows j of all six i-planes.  Every group has a private
-// D-deep mbarrier ring (stage s = g*D + slot): a stage has exactly one consumer, which visits it in
-// order, so a waiter can never be two phases ahead of the barrier (a ring shared round-robin by
-// independent consumers lets a fast consumer's parity wait match the *previous* phase).
-// Sharing a stage across a group keeps ~4 warps per scheduler resident (the fp64/convert stream of
-// one warp issues well below 1 IPC) within the 227 KiB of shared memory.
-//   per tile: wait full -> partial moments -> exchange (named barrier B1) -> coefficients ->
-//   quantise own planes into the group's code buffer -> rare path -> B2 -> warp 0: release the
-//   stage, TMA-store the code tile (or copy rows when no TMA store applies).
-template <typename T, int G, int NG, int D>
+// Persistent, one CTA per SM, warp-specialised.  Warp NG*(1+Q) is the producer: one elected lane
+// streams 6x6x96 tiles with TMA.  The rest form NG groups; group g takes the CTA's tiles g, g+NG, ...
+// through a private D-deep ring of stages (a stage has one consumer sequence, so an mbarrier parity
+// wait can never match a stale phase).  Per group:
+//   * 1 moment warp: whole-tile moments (a2), Lemma coefficients (a3), coefficient codes (a4) and the
+//     fp32 fast-path constants, once per tile, into the stage's coefficient slot -> `ready`;
+//   * Q quantise warps: rows [q*P, q*P + P) of all six i-planes (a5-a7) into a private code slab,
+//     TMA-stored as a {96, P, 6} box; each arrives on `empty` (count Q) when done with the stage.
+// No named barriers, no partial-moment exchange, no redundant coefficient work.
+struct CoefSlot {  // per stage: the tile's 16 blocks
+  double bh[16][4];
+  Fast32 f[16];
+};
+
+template <typename T, int NG, int Q, int D>
 struct CompressSmem {
-  static constexpr int P = BS / G;
+  static constexpr int P = BS / Q;
   static constexpr int S = NG * D;
+  static constexpr int WARPS = NG * (1 + Q) + 1;
   static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
-  static constexpr size_t code_bytes = sizeof(uint16_t) * TILE_ELEMS;
-  static constexpr size_t off_codes = S * stage_bytes;
-  static constexpr size_t off_exch = off_codes + NG * code_bytes;
-  static constexpr size_t off_hist = off_exch + (size_t)NG * G * 4 * 32 * sizeof(double);
+  static constexpr size_t slab_bytes = sizeof(uint16_t) * BS * P * TK;
+  static constexpr size_t off_slab = S * stage_bytes;
+  static constexpr size_t off_slot = off_slab + (size_t)NG * Q * slab_bytes;
+  static constexpr size_t off_hist = off_slot + S * sizeof(CoefSlot);
   static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (HWIN + 36);
-  static constexpr size_t off_k = off_bar + 2 * S * sizeof(uint64_t);
+  static constexpr size_t off_k = off_bar + 3 * S * sizeof(uint64_t);
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
 };
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// One warp's share of a group tile (rows j0 .. j0+6/G-1): partial moments of its rows, exchange (B1), coefficients,
-// quantisation of its planes into the group's code buffer, rare path.  FULL tiles fold the block
-// geometry (6x6x6 everywhere) into constants.
-template <typename T, bool HIST, bool FULL, int G>
-__device__ __forceinline__ void group_tile(const T* __restrict__ xs, uint16_t* __restrict__ mycodes, double* myexch,
-                                           int j0, int wg, int bar_id, const TileCoord tc, const Geo& g,
-                                           const Consts& K, uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
-  constexpr int P = BS / G;
+// copy a quantise warp's code slab (rows j0 .. j0+P-1, layout [i][jj][k]) to the global code array
+// (fallback when no TMA store applies: n2 * 2 bytes is not a multiple of 16)
+template <int P>
+__device__ __forceinline__ void store_code_slab(const uint16_t* __restrict__ slab, uint16_t* __restrict__ codes,
+                                                const TileCoord tc, const Geo& g, int j0) {
   const int lane = threadIdx.x & 31;
-  const LaneGeom L = lane_geom<FULL>(tc, g);
-  double V[4];
-  moments_partial<T, true, P>(xs, BS * TK, TK, j0, L, V);
-#pragma unroll
-  for (int d = 0; d < 4; d++) myexch[(wg * 4 + d) * 32 + lane] = V[d];
-  named_bar_sync(bar_id, G * 32);  // B1
-#pragma unroll
-  for (int d = 0; d < 4; d++) {
-    double acc = myexch[d * 32 + lane];
-#pragma unroll
-    for (int w = 1; w < G; w++) acc += myexch[(w * 4 + d) * 32 + lane];
-    V[d] = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
-  }
-  double beta[4], bh[4];
-  int32_t cc[4];
-  block_coefs<FULL>(V, L, K, beta, cc, bh);
-  if (wg == 0) write_coefs(o, tc, g, L, cc, beta);
-  const uint32_t umax =
-      quantize_rows<T, true, HIST, FULL, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, j0, L, bh, K, R, hs);
-  rare_path<T, HIST, P>(xs, BS * TK, TK, mycodes, BS * TK, TK, j0, L, umax, tc, g, o, hs);
+  const int m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
+  const int m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
+  const int kval = (int)umin64(TK, g.n2 - (uint64_t)tc.c * TK);
+  const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+  const bool even = (g.n2 & 1) == 0 && (reinterpret_cast<uintptr_t>(codes) & 3) == 0;
+  for (int i = 0; i < m0; i++)
+    for (int jj = 0; jj < P && j0 + jj < m1; jj++) {
+      const uint16_t* src = slab + (i * P + jj) * TK;
+      uint16_t* dst = codes + off + ((uint64_t)i * g.n1 + j0 + jj) * g.n2;
+      if (even) {
+        for (int w = lane; 2 * w < kval; w += 32) {
+          if (2 * w + 1 < kval) reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(src)[w];
+          else dst[2 * w] = src[2 * w];
+        }
+      } else {
+        for (int k = lane; k < kval; k += 32) dst[k] = src[k];
+      }
+    }
 }
 
-template <typename T, int G, int NG, int D, bool HIST>
-__global__ void __launch_bounds__((NG * G + 1) * 32, 1)
+template <typename T, bool FULL>
+__device__ __forceinline__ void moment_warp_tile(const T* __restrict__ xs, CoefSlot* slot, const TileCoord tc,
+                                                 const Geo& g, const Consts& K, const CompressOut<T>& o) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  double V[4], beta[4], bh[4];
+  int32_t cc[4];
+  moments_partial<T, true, BS>(xs, BS * TK, TK, 0, L, V);
+#pragma unroll
+  for (int d = 0; d < 4; d++) V[d] += __shfl_xor_sync(0xffffffffu, V[d], 1);
+  block_coefs<FULL>(V, L, K, beta, cc, bh);
+  write_coefs(o, tc, g, L, cc, beta);
+  if (L.h == 0) {
+    const int bl = (threadIdx.x & 31) >> 1;
+#pragma unroll
+    for (int d = 0; d < 4; d++) slot->bh[bl][d] = bh[d];
+    slot->f[bl] = fast32_consts(bh, K);
+  }
+}
+
+template <typename T, bool HIST, bool FULL, int P>
+__device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const CoefSlot* slot, uint16_t* slab,
+                                                int j0, const TileCoord tc, const Geo& g, const Consts& K,
+                                                uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int bl = (threadIdx.x & 31) >> 1;
+  double bh[4];
+#pragma unroll
+  for (int d = 0; d < 4; d++) bh[d] = slot->bh[bl][d];
+  const Fast32 F = slot->f[bl];
+  const uint32_t umax =
+      quantize_rows<T, true, HIST, FULL, P, true>(xs, BS * TK, TK, slab, 0, 0, j0, L, bh, F, K, R, hs);
+  rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, umax, tc, g, o, hs);
+}
+
+template <typename T, int NG, int Q, int D, bool HIST>
+__global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
     k_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, int codes_tma,
                    KArgs a, CompressOut<T> o) {
-  using L_ = CompressSmem<T, G, NG, D>;
+  using L_ = CompressSmem<T, NG, Q, D>;
   constexpr int P = L_::P;
   constexpr int S = L_::S;
-  static_assert(BS % G == 0, "G must divide 6");
+  static_assert(BS % Q == 0, "Q must divide 6");
   extern __shared__ __align__(128) uint8_t smem[];
   T* stages = reinterpret_cast<T*>(smem);
-  uint16_t* cbuf = reinterpret_cast<uint16_t*>(smem + L_::off_codes);
-  double* exch = reinterpret_cast<double*>(smem + L_::off_exch);
+  uint16_t* slabs = reinterpret_cast<uint16_t*>(smem + L_::off_slab);
+  CoefSlot* slots = reinterpret_cast<CoefSlot*>(smem + L_::off_slot);
   uint32_t* s_win = reinterpret_cast<uint32_t*>(smem + L_::off_hist);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
-  uint64_t* empty = full + S;
+  uint64_t* ready = full + S;
+  uint64_t* empty = ready + S;
   Consts* s_k = reinterpret_cast<Consts*>(smem + L_::off_k);
   int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -330,34 +380,38 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&ready[s], 1);
+      ptx::mbar_init(&empty[s], Q);
     }
     ptx::fence_mbar_init();
   }
   if (!cta_consts(a, s_k, s_ok)) return;
   const Geo& g = a.g;
-  const uint64_t Gr = gridDim.x;
-  if (warp == NG * G) {
+  if (warp == NG * (1 + Q)) {
     // ---------------- producer
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_x);
-      for (uint64_t p = 0; p < a.pf; p++) {
-        const uint64_t tp = tile_at(p, a.chunk);
-        if (tp >= g.ntiles) break;
-        const TileCoord tc = decode_tile(tp, g);
+      TileWalk tw(0, a.chunk, 1), tp(0, a.chunk, 1);
+      for (uint32_t p = 0; p < a.pf; p++, tp.next()) {   // L2 prefetch runs a.pf tiles ahead of the loads
+        const uint64_t t = tp.tile();
+        if (t >= g.ntiles) break;
+        const TileCoord tc = decode_tile(t, g);
         ptx::tma_prefetch_3d(&tm_x, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
       }
-      for (uint32_t n = 0;; n++) {
-        const uint64_t t = tile_at(n, a.chunk);
+      uint32_t gq = 0, k = 0;   // n = k * NG + gq
+      for (;; tw.next()) {
+        const uint64_t t = tw.tile();
         if (t >= g.ntiles) break;
         if (a.pf) {
-          const uint64_t tp = tile_at(n + a.pf, a.chunk);
-          if (tp < g.ntiles) {
-            const TileCoord tq = decode_tile(tp, g);
-            ptx::tma_prefetch_3d(&tm_x, (int)(tq.c * TK), (int)(tq.b * BS), (int)(tq.a * BS));
+          const uint64_t tq = tp.tile();
+          if (tq < g.ntiles) {
+            const TileCoord tc = decode_tile(tq, g);
+            ptx::tma_prefetch_3d(&tm_x, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
           }
+          tp.next();
         }
-        const uint32_t k = n / NG, s = (n % NG) * D + k % D, ph = (k / D) & 1u;
+        const uint32_t s = gq * D + k % D, ph = (k / D) & 1u;
+        if (++gq == NG) { gq = 0; k++; }
         ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
         const TileCoord tc = decode_tile(t, g);
         ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L_::stage_bytes);
@@ -366,40 +420,55 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
       }
     }
   } else {
-    // ---------------- consumer groups
-    const int grp = warp / G, wg = warp - grp * G, j0 = wg * P;
-    const int bar_id = 1 + grp;
+    const int grp = warp / (1 + Q), role = warp - grp * (1 + Q);   // role 0: moment warp, 1..Q: quantise
     const Consts K = *s_k;
-    uint16_t* mycodes = cbuf + (size_t)grp * TILE_ELEMS;
-    double* myexch = exch + (size_t)grp * G * 4 * 32;
     uint32_t k = 0;
-    for (uint64_t n = grp;; n += NG, k++) {
-      const uint64_t t = tile_at(n, a.chunk);
-      if (t >= g.ntiles) break;
-      const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
-      const TileCoord tc = decode_tile(t, g);
-      if (codes_tma && wg == 0 && lane == 0) ptx::bulk_wait_read0();  // previous store done reading mycodes
-      ptx::mbar_wait(&full[s], ph);
-      const T* xs = stages + (size_t)s * TILE_ELEMS;
-      if (tile_full(tc, g))
-        group_tile<T, HIST, true, G>(xs, mycodes, myexch, j0, wg, bar_id, tc, g, K, a.R, o, hs);
-      else
-        group_tile<T, HIST, false, G>(xs, mycodes, myexch, j0, wg, bar_id, tc, g, K, a.R, o, hs);
-      if (codes_tma) ptx::fence_proxy_async_smem();
-      named_bar_sync(bar_id, G * 32);  // B2: codes complete, stage no longer read
-      if (wg == 0) {
+    if (role == 0) {
+      // ---------------- moment warp
+      for (TileWalk tw(grp, a.chunk, NG);; tw.next(), k++) {
+        const uint64_t t = tw.tile();
+        if (t >= g.ntiles) break;
+        const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
+        const TileCoord tc = decode_tile(t, g);
+        ptx::mbar_wait(&full[s], ph);
+        const T* xs = stages + (size_t)s * TILE_ELEMS;
+        if (tile_full(tc, g)) moment_warp_tile<T, true>(xs, &slots[s], tc, g, K, o);
+        else moment_warp_tile<T, false>(xs, &slots[s], tc, g, K, o);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&ready[s]);
+      }
+    } else {
+      // ---------------- quantise warp q: rows [j0, j0 + P)
+      const int q = role - 1, j0 = q * P;
+      uint16_t* slab = slabs + (size_t)(grp * Q + q) * (BS * P * TK);
+      for (TileWalk tw(grp, a.chunk, NG);; tw.next(), k++) {
+        const uint64_t t = tw.tile();
+        if (t >= g.ntiles) break;
+        const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
+        const TileCoord tc = decode_tile(t, g);
+        if (codes_tma && lane == 0) ptx::bulk_wait_read0();   // previous slab store finished reading
+        __syncwarp();
+        ptx::mbar_wait(&full[s], ph);
+        ptx::mbar_wait(&ready[s], ph);
+        const T* xs = stages + (size_t)s * TILE_ELEMS;
+        if (tile_full(tc, g)) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
+        else quant_warp_tile<T, HIST, false, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
+        __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&empty[s]);
         if (codes_tma) {
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_3d(&tm_c, mycodes, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+            ptx::tma_store_3d(&tm_c, slab, (int)(tc.c * TK), (int)(tc.b * BS + j0), (int)(tc.a * BS));
             ptx::bulk_commit();
           }
         } else {
-          store_code_rows(mycodes, o.codes, tc, g);
+          store_code_slab<P>(slab, o.codes, tc, g, j0);
+          __syncwarp();
         }
       }
+      if (codes_tma && lane == 0) ptx::bulk_wait0();
     }
-    if (codes_tma && wg == 0 && lane == 0) ptx::bulk_wait0();
   }
   __syncthreads();
   if (HIST) hist_flush(hs, o.hist);
@@ -477,10 +546,13 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     // ---------------- producer
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_c);
-      for (uint32_t n = 0;; n++) {
-        const uint64_t t = tile_at(n, a.chunk);
+      TileWalk tw(0, a.chunk, 1);
+      uint32_t gq = 0, k = 0;
+      for (;; tw.next()) {
+        const uint64_t t = tw.tile();
         if (t >= g.ntiles) break;
-        const uint32_t k = n / NG, s = (n % NG) * D + k % D, ph = (k / D) & 1u;
+        const uint32_t s = gq * D + k % D, ph = (k / D) & 1u;
+        if (++gq == NG) { gq = 0; k++; }
         ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
         const TileCoord tc = decode_tile(t, g);
         const uint32_t nblk = min(16u, g.NB2 - tc.c * 16u);
@@ -497,8 +569,8 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     const Consts K = *s_k;
     T* myout = obuf + (size_t)warp * (BS * P * TK);
     uint32_t k = 0;
-    for (uint64_t n = grp;; n += NG, k++) {
-      const uint64_t t = tile_at(n, a.chunk);
+    for (TileWalk tw(grp, a.chunk, NG);; tw.next(), k++) {
+      const uint64_t t = tw.tile();
       if (t >= g.ntiles) break;
       const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
       const TileCoord tc = decode_tile(t, g);
@@ -669,6 +741,9 @@ Geo make_geo(const sz3g_grid* grid) {
   g.NT2 = (g.NB2 + 15) / 16;
   g.ntiles = (uint64_t)g.NB0 * g.NB1 * g.NT2;
   g.gofs = grid->dim0_offset * g.n1 * g.n2;
+  const bool small = g.ntiles < (1ull << 21);
+  g.mNT2 = (small && g.NT2 < (1u << 19)) ? ((1ull << 40) / g.NT2 + 1) : 0;
+  g.mNB1 = (small && g.NB1 < (1u << 19)) ? ((1ull << 40) / g.NB1 + 1) : 0;
   return g;
 }
 
@@ -692,6 +767,14 @@ uint32_t chunk_tiles(bool decompress) {  // SZ3G_CHUNK_C / SZ3G_CHUNK_D override
   return decompress ? vd : vc;
 }
 
+int compress_cfg() {  // SZ3G_CCFG selects a compress kernel shape (tuning only)
+  static int v = [] {
+    const char* e = getenv("SZ3G_CCFG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 uint32_t prefetch_tiles() {  // SZ3G_PF overrides (tuning only)
   static uint32_t v = [] {
     const char* e = getenv("SZ3G_PF");
@@ -699,26 +782,26 @@ uint32_t prefetch_tiles() {  // SZ3G_PF overrides (tuning only)
   }();
   return v;
 }
-constexpr int CG32 = 3, CN32 = 5, CD32 = 2;  // f32 compress: 5 groups x 3 warps + producer = 16 warps; 2 x 13.5 KiB stages per group
-constexpr int CG64 = 6, CN64 = 2, CD64 = 2;  // f64 compress: 2 groups x 6 warps + producer = 13 warps; 2 x 27 KiB stages per group
+constexpr int CN32 = 5, CQ32 = 2, CD32 = 2;  // f32 compress: 5 groups x (1 moment + 2 quantise warps) + producer = 16 warps
+constexpr int CN64 = 3, CQ64 = 3, CD64 = 2;  // f64 compress: 3 groups x (1 + 3) warps + producer = 13 warps
 constexpr int DG32 = 3, DN32 = 5, DD32 = 3;  // f32 decompress: 5 groups x 3 warps + producer; 3 x 7 KiB stages per group
 constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 warps + producer
 
-template <typename T, int G, int NG, int D, bool HIST>
+template <typename T, int NG, int Q, int D, bool HIST>
 int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
                         const CompressOut<T>& co, cudaStream_t st) {
-  using L = CompressSmem<T, G, NG, D>;
+  using L = CompressSmem<T, NG, Q, D>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mx, mc;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
   memset(&mc, 0, sizeof(mc));
-  if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g, BS, true)) codes_tma = false;
-  auto kern = k_compress_tma<T, G, NG, D, HIST>;
+  if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g, L::P, true)) codes_tma = false;
+  auto kern = k_compress_tma<T, NG, Q, D, HIST>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
-  kern<<<(unsigned)grid, (NG * G + 1) * 32, L::total, st>>>(mx, mc, codes_tma ? 1 : 0, ka, co);
+  kern<<<(unsigned)grid, L::WARPS * 32, L::total, st>>>(mx, mc, codes_tma ? 1 : 0, ka, co);
   return check_launch(1);
 }
 
@@ -795,16 +878,23 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
   if (grid->dtype == SZ3G_F32) {
     CompressOut<float> co{codes, coef_codes, coef_raw, outlier_idx, (float*)outlier_val, outlier_cap,
                           d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
-    if (tma) return use_hist ? launch_compress_tma<float, CG32, CN32, CD32, true>(g, x, codes, codes_tma, ka, co, st)
-                         : launch_compress_tma<float, CG32, CN32, CD32, false>(g, x, codes, codes_tma, ka, co, st);
+    if (tma) {
+      const int cfg = compress_cfg();
+      if (cfg == 1) return use_hist ? launch_compress_tma<float, 3, 3, 3, true>(g, x, codes, codes_tma, ka, co, st)
+                                    : launch_compress_tma<float, 3, 3, 3, false>(g, x, codes, codes_tma, ka, co, st);
+      if (cfg == 2) return use_hist ? launch_compress_tma<float, 4, 2, 2, true>(g, x, codes, codes_tma, ka, co, st)
+                                    : launch_compress_tma<float, 4, 2, 2, false>(g, x, codes, codes_tma, ka, co, st);
+      return use_hist ? launch_compress_tma<float, CN32, CQ32, CD32, true>(g, x, codes, codes_tma, ka, co, st)
+                      : launch_compress_tma<float, CN32, CQ32, CD32, false>(g, x, codes, codes_tma, ka, co, st);
+    }
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
     if (use_hist) k_compress_plain<float, true><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
     else k_compress_plain<float, false><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
   } else {
     CompressOut<double> co{codes, coef_codes, coef_raw, outlier_idx, (double*)outlier_val, outlier_cap,
                            d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
-    if (tma) return use_hist ? launch_compress_tma<double, CG64, CN64, CD64, true>(g, x, codes, codes_tma, ka, co, st)
-                         : launch_compress_tma<double, CG64, CN64, CD64, false>(g, x, codes, codes_tma, ka, co, st);
+    if (tma) return use_hist ? launch_compress_tma<double, CN64, CQ64, CD64, true>(g, x, codes, codes_tma, ka, co, st)
+                         : launch_compress_tma<double, CN64, CQ64, CD64, false>(g, x, codes, codes_tma, ka, co, st);
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
     if (use_hist) k_compress_plain<double, true><<<blocks, 128, 0, st>>>((const double*)x, ka, co);
     else k_compress_plain<double, false><<<blocks, 128, 0, st>>>((const double*)x, ka, co);

@@ -31,6 +31,8 @@ constexpr double I2D_MAGIC = 4503599627370496.0;   // 2^52
 struct Consts {
   double eb_abs, twoeb, inv2eb, w0, ws, inv_w0, inv_ws;
   double vc, vthr;  // fast verify: |t - q| + vc*|x| <= vthr  implies  |(T)(p + 2eb q) - x| <= eb
+  double kS_mul, kS_add;  // fp32 fast path: kS = kS_mul * S + kS_add (see fast32_consts)
+  float inv2eb32, c32, k1;
 };
 
 struct Geo {
@@ -38,6 +40,7 @@ struct Geo {
   uint32_t NB0, NB1, NB2, NT2;   // blocks per dim; NT2 = tiles along dim 2 = ceil(NB2/16)
   uint64_t ntiles;
   uint64_t gofs;                 // dim0_offset * n1 * n2 (outlier indices are global)
+  uint64_t mNT2, mNB1;           // floor(2^40 / d) + 1: x / d = (x * m) >> 40 exactly for x, d < 2^19
 };
 
 // O1/O2 on device: same operations as the definition (IEEE division for the constants).
@@ -61,6 +64,14 @@ __device__ __forceinline__ bool make_consts(int eb_mode, double eb, const double
   // huge eb, (T)y could overflow to inf: the fast test is disabled there.
   K.vc = 1.01 * uround / K.twoeb;
   K.vthr = (uround > 1e-12 && eb_abs > 1e30) ? -1.0 : 0.5 - 1e-10 - 1.02 * K.vc * eb_abs;
+  // fp32 fast path constants (f32 data; see fast32_consts): kS = 2.03 u S / eb + 1.2e-11 + 1e-44 / eb,
+  // evaluated as kS_mul * S + kS_add with the multipliers rounded up
+  const double u = 5.9604644775390625e-08;
+  K.kS_mul = __ddiv_ru(2.03 * u, eb_abs) * (1.0 + 1e-15);
+  K.kS_add = 1.2e-11 + __ddiv_ru(1e-44, eb_abs) * (1.0 + 1e-15);
+  K.inv2eb32 = __double2float_rn(K.inv2eb);
+  K.c32 = __double2float_ru(K.vc);
+  K.k1 = __double2float_ru(3.1 * u);
   return true;
 }
 
@@ -87,13 +98,19 @@ struct TileCoord {
   uint32_t a, b, c;  // block-row index along dim0, dim1; tile index along dim2
 };
 
-// tile index -> coordinates (32-bit: the host guarantees ntiles < 2^32)
+// tile index -> coordinates.  Multiply-shift division: with m = floor(2^40/d) + 1, (x*m) >> 40 =
+// floor(x/d) for x < 2^21 and d < 2^19 (the error x(m - 2^40/d)/2^40 < 2^-19 < 1/d); the host falls
+// back to plain division (m = 0) outside that range.
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint32_t d, uint64_t m) {
+  return m ? (uint32_t)(((uint64_t)x * m) >> 40) : x / d;
+}
+
 __device__ __forceinline__ TileCoord decode_tile(uint64_t t64, const Geo& g) {
   const uint32_t t = (uint32_t)t64;
   TileCoord tc;
-  const uint32_t r = t / g.NT2;
+  const uint32_t r = fdiv(t, g.NT2, g.mNT2);
   tc.c = t - r * g.NT2;
-  tc.a = r / g.NB1;
+  tc.a = fdiv(r, g.NB1, g.mNB1);
   tc.b = r - tc.a * g.NB1;
   return tc;
 }
@@ -275,13 +292,16 @@ __device__ __forceinline__ uint32_t exact_code(T xv, double p, const Consts& K, 
 
 // Per-block constants of the fp32 fast path (f32 data).
 //   E = |t32 - t| <= k1 |t32| + kS,   k1 = 3.1 u,   kS = 2.03 u S / eb + 1.2e-11 + 1e-44 / eb
-// with u = 2^-24, S = |b0| + 5 (|b1| + |b2| + |b3|) (derivation in DESIGN.md 4).  Accept the fp32
-// result when |t32 - r| + k1 |t32| + c |x| <= vthr - kS (evaluated with one-sided fp32 margins):
+// with u = 2^-24, S = |b0| + 5 (|b1| + |b2| + |b3|) (derivation in DESIGN.md 4).  The fp64 fast-verify
+// term c |x| is bounded per block too: |x| <= |p| + 2eb |t| (1 + 1e-6) and |p| <= S (i, j, k <= 5), so
+// c |x| <= c S + 2 eb c |t32| (1 + 1e-6) + c 2 eb E.  Accept the fp32 result when
+//   |t32 - r| + (k1 + 2.01 eb c) |t32| <= vthr - kS - c S - 2.01 eb c kS  (one-sided fp32 margins):
 // then t lies within E of t32, strictly inside r's rounding interval, so rint(t) = r, and the fp64
 // fast-verify condition |t - q| + c |x| <= vthr holds, so x' passes O9.
 struct Fast32 {
   float b0, b1, b2, b3;  // decoded coefficients rounded to fp32
-  float c32, k1, thr;    // fp32 check constants
+  float k1, thr;         // |e| + k1 |t32| <= thr
+  float pad0, pad1;
 };
 
 __device__ __forceinline__ Fast32 fast32_consts(const double bh[4], const Consts& K) {
@@ -291,12 +311,13 @@ __device__ __forceinline__ Fast32 fast32_consts(const double bh[4], const Consts
   F.b2 = __double2float_rn(bh[2]);
   F.b3 = __double2float_rn(bh[3]);
   const double u = 5.9604644775390625e-08;
-  const double S = fabs(bh[0]) + 5.0 * (fabs(bh[1]) + fabs(bh[2]) + fabs(bh[3]));
-  const double kS = 2.03 * u * S / K.eb_abs + 1.2e-11 + 1e-44 / K.eb_abs;
-  F.c32 = __double2float_ru(K.vc);
-  F.k1 = __double2float_ru(3.1 * u);
-  const double thr = (K.vthr - kS) * (1.0 - 4.0 * u);
+  const double S = (fabs(bh[0]) + 5.0 * (fabs(bh[1]) + fabs(bh[2]) + fabs(bh[3]))) * (1.0 + 1e-15);
+  const double kS = __fma_ru(K.kS_mul, S, K.kS_add);             // >= 2.03 u S / eb + ...
+  const double c2e = 2.01 * K.eb_abs * K.vc;                       // 2 eb c with margin
+  F.k1 = __double2float_ru((3.1 * u + c2e) * (1.0 + 1e-12));
+  const double thr = (K.vthr - kS - K.vc * S * (1.0 + 1e-12) - c2e * kS) * (1.0 - 4.0 * u);
   F.thr = thr > 0.0 ? __double2float_rd(thr) : -1.0f;
+  F.pad0 = F.pad1 = 0.0f;
   return F;
 }
 
@@ -307,30 +328,35 @@ __device__ __forceinline__ Fast32 fast32_consts(const double bh[4], const Consts
 // histogram takes one red.shared per element at the code clamped into the smem window; codes
 // outside it and outliers (code 0) are flagged through the lane's running max of (code - lo) and
 // handled by rare_path().
-template <typename T, bool IN_SMEM, bool HIST, bool FULL, int PJ>
+template <typename T, bool IN_SMEM, bool HIST, bool FULL, int PJ, bool SLAB>
 __device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint64_t si, uint64_t sj,
                                                   uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
-                                                  const LaneGeom& L, const double bh[4], const Consts& K,
-                                                  const uint32_t R, const HistSmem& hs) {
+                                                  const LaneGeom& L, const double bh[4], const Fast32& F,
+                                                  const Consts& K, const uint32_t R, const HistSmem& hs) {
   const int lane = threadIdx.x & 31;
   const uint32_t win_base = HIST ? (uint32_t)__cvta_generic_to_shared(hs.win) : 0u;  // &win[c - lo]
   const uint32_t sink = HIST ? (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * lane : 0u;
   const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;   // window [lo, lo + nwin), lo >= 1
   uint32_t umax = 0u;                                 // max over valid elements of (code - lo), unsigned
-  if (IN_SMEM) {  // shared-memory tiles: compile-time strides -> immediate address offsets
-    si = BS * TK; sj = TK; ci = BS * TK; cj = TK;
-  }
+  if (IN_SMEM) { si = BS * TK; sj = TK; }             // shared stage: compile-time strides
+  if (SLAB) { ci = PJ * TK; cj = TK; }                // codes: this warp's slab [i][jj][k]
   constexpr bool F32 = sizeof(T) == 4;
-  const Fast32 F = fast32_consts(bh, K);
-  const float inv2eb32 = __double2float_rn(K.inv2eb);
+  const float inv2eb32 = K.inv2eb32;
   const float Rf = (float)R;
   const double Rd = (double)R;
+  // columns (j, k) visited with incremental pointers and fp32 counters (no per-iteration division)
+  const T* xrow = xs + (IN_SMEM ? (uint32_t)(j0 * TK + L.kcol) : (uint64_t)j0 * sj + L.kcol);
+  uint16_t* crow = cs + (SLAB ? (uint32_t)L.kcol : (uint64_t)j0 * cj + L.kcol);
+  float fj = (float)j0;
 #pragma unroll 1
-  for (int jk = 0; jk < 3 * PJ; jk++) {
-    const int jj = jk / 3, kk = jk - 3 * jj, j = j0 + jj;
+  for (int jj = 0; jj < PJ; jj++, fj += 1.0f) {
+    const int j = j0 + jj;
+    const T* xcol = xrow;
+    uint16_t* ccol = crow;
+    float fk = (float)(3 * L.h);
+#pragma unroll 1
+    for (int kk = 0; kk < 3; kk++, xcol++, ccol++, fk += 1.0f) {
     const bool cv = FULL || ((j < L.m1) && L.kv(kk));
-    const T* xcol = xs + (IN_SMEM ? (uint32_t)(j * TK + L.kcol + kk) : (uint64_t)j * sj + L.kcol + kk);  // + i*si
-    uint16_t* ccol = cs + (IN_SMEM ? (uint32_t)(j * TK + L.kcol + kk) : (uint64_t)j * cj + L.kcol + kk);
     T xv[BS];
 #pragma unroll
     for (int i = 0; i < BS; i++) {
@@ -338,27 +364,25 @@ __device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint
       if (IN_SMEM || FULL) xv[i] = xcol[i * si];
       else xv[i] = valid ? xcol[i * si] : T(0);
     }
-    const double dj = (double)j, dk = (double)(3 * L.h + kk);
     uint32_t code[BS];
     bool need = false;   // some element the fast test cannot decide -> exact definition below
     if (F32) {
       // fp32 fast path: p32 = fma(b1, i, fma(b2, j, fma(b3, k, b0))) in fp32; bound in Fast32
-      const float base32 = __fmaf_rn(F.b2, (float)j, __fmaf_rn(F.b3, (float)(3 * L.h + kk), F.b0));
+      const float base32 = __fmaf_rn(F.b2, fj, __fmaf_rn(F.b3, fk, F.b0));
 #pragma unroll
       for (int i = 0; i < BS; i++) {
-        const float xf = (float)xv[i];
-        const float p32 = __fmaf_rn(F.b1, (float)i, base32);
-        const float t32 = __fmul_rn(__fsub_rn(xf, p32), inv2eb32);
+        const float p32 = i == 0 ? base32 : __fmaf_rn(F.b1, (float)i, base32);   // b1 finite: i = 0 exact
+        const float t32 = __fmul_rn(__fsub_rn((float)xv[i], p32), inv2eb32);
         const float s32 = __fadd_rn(t32, 12582912.0f);       // 1.5 * 2^23: rint for |t32| < 2^22
         const float r = __fsub_rn(s32, 12582912.0f);
         const float e = __fsub_rn(t32, r);                    // exact (Sterbenz)
-        const float v = __fmaf_rn(F.c32, fabsf(xf), __fmaf_rn(F.k1, fabsf(t32), fabsf(e)));
+        const float v = __fmaf_rn(F.k1, fabsf(t32), fabsf(e));
         const bool ok = (v <= F.thr) && (fabsf(r) < Rf);
         code[i] = ok ? (uint32_t)(__float_as_int(s32) - 0x4B400000 + (int)R) : 0u;   // O10
         need |= !ok;
       }
     } else {
-      const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk, bh[0]));
+      const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * L.h + kk), bh[0]));
 #pragma unroll
       for (int i = 0; i < BS; i++) {
         const double xd = to_d<T>(xv[i]);
@@ -373,7 +397,7 @@ __device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint
       }
     }
     if (__any_sync(0xffffffffu, need)) {
-      const double base = __fma_rn(bh[2], dj, __fma_rn(bh[3], dk, bh[0]));
+      const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * L.h + kk), bh[0]));
 #pragma unroll
       for (int i = 0; i < BS; i++)
         if (code[i] == 0u) code[i] = exact_code<T>(xv[i], __fma_rn(bh[1], (double)i, base), K, R);
@@ -391,6 +415,9 @@ __device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint
         red_smem_add(FULL ? win_base + 4u * cw : (valid ? win_base + 4u * cw : sink), FULL ? 1u : (valid ? 1u : 0u));
       }
     }
+    }
+    xrow += IN_SMEM ? (uint64_t)TK : sj;
+    crow += cj;
   }
   return umax;
 }
@@ -401,8 +428,8 @@ __device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint
 template <typename T, bool HIST, int PJ>
 __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si, uint64_t sj,
                                           const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
-                                          const LaneGeom& L, uint32_t umax, const TileCoord tc, const Geo& g,
-                                          const CompressOut<T>& o, const HistSmem& hs) {
+                                          int cs_j0, const LaneGeom& L, uint32_t umax, const TileCoord tc,
+                                          const Geo& g, const CompressOut<T>& o, const HistSmem& hs) {
   const int lane = threadIdx.x & 31;
   const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;
   const bool has_rare = umax > wtop;
@@ -414,7 +441,7 @@ __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si,
       for (int kk = 0; kk < 3; kk++) {
         if (!L.kv(kk)) continue;
         for (int i = 0; i < L.m0; i++) {
-          const uint32_t c = cs[i * ci + j * cj + L.kcol + kk];
+          const uint32_t c = cs[i * ci + (j - cs_j0) * cj + L.kcol + kk];
           nout += (c == 0u) ? 1u : 0u;
           if (HIST && c != 0u && c - wlo > wtop) {   // counted at the top bin: move to global
             atomicSub(&hs.win[wtop], 1u);
@@ -448,7 +475,7 @@ __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si,
       for (int kk = 0; kk < 3; kk++) {
         if (!L.kv(kk)) continue;
         for (int i = 0; i < L.m0; i++) {
-          if (cs[i * ci + j * cj + L.kcol + kk] != 0) continue;
+          if (cs[i * ci + (j - cs_j0) * cj + L.kcol + kk] != 0) continue;
           if (pos < o.cap) {
             o.oidx[pos] = gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk;
             o.oval[pos] = xs[i * si + j * sj + L.kcol + kk];
@@ -473,8 +500,10 @@ __device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t
   for (int d = 0; d < 4; d++) V[d] += __shfl_xor_sync(0xffffffffu, V[d], 1);
   block_coefs<FULL>(V, L, K, beta, cc, bh);
   write_coefs(o, tc, g, L, cc, beta);
-  const uint32_t umax = quantize_rows<T, IN_SMEM, HIST, FULL, BS>(xs, si, sj, cs, ci, cj, 0, L, bh, K, R, hs);
-  rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, L, umax, tc, g, o, hs);
+  const Fast32 F = fast32_consts(bh, K);
+  const uint32_t umax =
+      quantize_rows<T, IN_SMEM, HIST, FULL, BS, false>(xs, si, sj, cs, ci, cj, 0, L, bh, F, K, R, hs);
+  rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, 0, L, umax, tc, g, o, hs);
 }
 
 // ------------------------------------------------------------------------------------------
