@@ -175,6 +175,7 @@ __device__ __forceinline__ void hist_init(HistSmem& hs, uint32_t* win, uint32_t*
   // always outside it and goes through the zero counter
   hs.lo = (2u * R - 1u <= (uint32_t)HWIN) ? 1u : R - HWIN / 2;
   hs.nwin = min(2u * R - 1u, (uint32_t)HWIN);
+  hs.W = (2u * R - 1u <= (uint32_t)HWIN) ? R : (uint32_t)HWIN / 2u;
   for (uint32_t b = threadIdx.x; b < hs.nwin; b += blockDim.x) win[b] = 0u;
   if (threadIdx.x == 0) *zero = 0u;
 }
@@ -351,9 +352,9 @@ __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const 
 #pragma unroll
   for (int d = 0; d < 4; d++) bh[d] = slot->bh[bl][d];
   const Fast32 F = slot->f[bl];
-  const uint32_t umax =
-      quantize_rows<T, true, HIST, FULL, P, true>(xs, BS * TK, TK, slab, 0, 0, j0, L, bh, F, K, R, hs);
-  rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, umax, tc, g, o, hs);
+  const bool has_out =
+      quantize_rows<T, true, HIST, FULL, P, true>(xs, BS * TK, TK, slab, 0, 0, j0, L, bh, F, K, R, hs, o.hist);
+  rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, has_out, tc, g, o, hs);
 }
 
 template <typename T, int NG, int Q, int D, bool HIST>

@@ -33,6 +33,7 @@ struct Consts {
   double vc, vthr;  // fast verify: |t - q| + vc*|x| <= vthr  implies  |(T)(p + 2eb q) - x| <= eb
   double kS_mul, kS_add;  // fp32 fast path: kS = kS_mul * S + kS_add (see fast32_consts)
   float inv2eb32, c32, k1;
+  int fast32;             // fl32(1/(2eb)) is a normal fp32 number: the fp32 fast path applies
 };
 
 struct Geo {
@@ -64,14 +65,16 @@ __device__ __forceinline__ bool make_consts(int eb_mode, double eb, const double
   // huge eb, (T)y could overflow to inf: the fast test is disabled there.
   K.vc = 1.01 * uround / K.twoeb;
   K.vthr = (uround > 1e-12 && eb_abs > 1e30) ? -1.0 : 0.5 - 1e-10 - 1.02 * K.vc * eb_abs;
-  // fp32 fast path constants (f32 data; see fast32_consts): kS = 2.03 u S / eb + 1.2e-11 + 1e-44 / eb,
-  // evaluated as kS_mul * S + kS_add with the multipliers rounded up
+  // fp32 fast path constants (f32 data; see fast32_consts): kS = 2.52 u S / eb + 1.2e-11 + 1e-43,
+  // evaluated as kS_mul * S + kS_add with the multiplier rounded up.  The fast path needs
+  // fl32(1/(2eb)) to be a normal fp32 number (relative error <= u): otherwise it is switched off.
   const double u = 5.9604644775390625e-08;
-  K.kS_mul = __ddiv_ru(2.03 * u, eb_abs) * (1.0 + 1e-15);
-  K.kS_add = 1.2e-11 + __ddiv_ru(1e-44, eb_abs) * (1.0 + 1e-15);
+  K.kS_mul = __ddiv_ru(2.52 * u, eb_abs) * (1.0 + 1e-15);
+  K.kS_add = 1.2e-11 + 1e-43;
   K.inv2eb32 = __double2float_rn(K.inv2eb);
+  K.fast32 = (K.inv2eb > 2.4e-38 && K.inv2eb < 8.5e37) ? 1 : 0;
   K.c32 = __double2float_ru(K.vc);
-  K.k1 = __double2float_ru(3.1 * u);
+  K.k1 = __double2float_ru(2.1 * u);
   return true;
 }
 
@@ -134,6 +137,7 @@ struct HistSmem {
   uint32_t* dummy; // 32 per-lane sink slots for non-counted elements
   uint32_t lo;
   uint32_t nwin;   // bins actually used (min(2R, HWIN))
+  uint32_t W;      // fast-path acceptance |q| < W: every accepted code lies in the window
 };
 
 
@@ -290,60 +294,74 @@ __device__ __forceinline__ uint32_t exact_code(T xv, double p, const Consts& K, 
   return (fabs(q) < (double)R && fabs(d) <= K.eb_abs) ? (uint32_t)(__double2loint(sm) + (int)R) : 0u;
 }
 
-// Per-block constants of the fp32 fast path (f32 data).
-//   E = |t32 - t| <= k1 |t32| + kS,   k1 = 3.1 u,   kS = 2.03 u S / eb + 1.2e-11 + 1e-44 / eb
-// with u = 2^-24, S = |b0| + 5 (|b1| + |b2| + |b3|) (derivation in DESIGN.md 4).  The fp64 fast-verify
-// term c |x| is bounded per block too: |x| <= |p| + 2eb |t| (1 + 1e-6) and |p| <= S (i, j, k <= 5), so
-// c |x| <= c S + 2 eb c |t32| (1 + 1e-6) + c 2 eb E.  Accept the fp32 result when
-//   |t32 - r| + (k1 + 2.01 eb c) |t32| <= vthr - kS - c S - 2.01 eb c kS  (one-sided fp32 margins):
+// Per-block constants of the fp32 fast path (f32 data), evaluated in the SCALED domain: with the
+// coefficients a_d = fl32(b^_d * inv2eb) and inv32 = fl32(inv2eb),
+//   P32 = fma32(a1, i, fma32(a2, j, fma32(a3, k, a0))),   t32 = fma32(x, inv32, -P32),
+// r = rint(t32), e = t32 - r (exact).  Against the definition's t = fl64(fl64(x - p) * inv2eb):
+//   |t32 - t| <= E = k1 |t32| + kS,   k1 = 2.1 u,   kS = 2.52 u S / eb + 1.2e-11 + 1e-43
+// with u = 2^-24, S = |b0| + 5 (|b1| + |b2| + |b3|) >= |p| (i, j, k <= 5): the t32 rounding (u |t32|),
+// the rounding of inv32 (u |x| / 2eb <= u S / 2eb + u |t|), four roundings in P32 (4.001 u S / 2eb) and
+// fp32 subnormal absolute errors (<= 2e-44); derivation in DESIGN.md 4.  The fp64 fast-verify term
+// c |x| is bounded per block too: |x| <= S + 2eb |t| (1 + 1e-15) and |t| <= |t32| + E, so
+// c |x| <= c S + c2e (|t32| + E) with c2e = 2.01 eb c.  Accept the fp32 result when
+//   |t32 - r| + (k1 + c2e (1 + k1)) |t32| <= vthr - kS (1 + c2e) - c S   (one-sided fp32 margins):
 // then t lies within E of t32, strictly inside r's rounding interval, so rint(t) = r, and the fp64
 // fast-verify condition |t - q| + c |x| <= vthr holds, so x' passes O9.
 struct Fast32 {
-  float b0, b1, b2, b3;  // decoded coefficients rounded to fp32
+  float a0, a1, a2, a3;  // decoded coefficients scaled by 1/(2eb), rounded to fp32
   float k1, thr;         // |e| + k1 |t32| <= thr
   float pad0, pad1;
 };
 
 __device__ __forceinline__ Fast32 fast32_consts(const double bh[4], const Consts& K) {
   Fast32 F;
-  F.b0 = __double2float_rn(bh[0]);
-  F.b1 = __double2float_rn(bh[1]);
-  F.b2 = __double2float_rn(bh[2]);
-  F.b3 = __double2float_rn(bh[3]);
+  F.a0 = __double2float_rn(__dmul_rn(bh[0], K.inv2eb));
+  F.a1 = __double2float_rn(__dmul_rn(bh[1], K.inv2eb));
+  F.a2 = __double2float_rn(__dmul_rn(bh[2], K.inv2eb));
+  F.a3 = __double2float_rn(__dmul_rn(bh[3], K.inv2eb));
   const double u = 5.9604644775390625e-08;
   const double S = (fabs(bh[0]) + 5.0 * (fabs(bh[1]) + fabs(bh[2]) + fabs(bh[3]))) * (1.0 + 1e-15);
-  const double kS = __fma_ru(K.kS_mul, S, K.kS_add);             // >= 2.03 u S / eb + ...
+  const double kS = __fma_ru(K.kS_mul, S, K.kS_add);             // >= 2.52 u S / eb + ...
   const double c2e = 2.01 * K.eb_abs * K.vc;                       // 2 eb c with margin
-  F.k1 = __double2float_ru((3.1 * u + c2e) * (1.0 + 1e-12));
-  const double thr = (K.vthr - kS - K.vc * S * (1.0 + 1e-12) - c2e * kS) * (1.0 - 4.0 * u);
-  F.thr = thr > 0.0 ? __double2float_rd(thr) : -1.0f;
+  F.k1 = __double2float_ru((2.1 * u + c2e * (1.0 + 2.2 * u)) * (1.0 + 1e-12));
+  const double thr = (K.vthr - kS * (1.0 + c2e) - K.vc * S * (1.0 + 1e-12)) * (1.0 - 4.0 * u);
+  F.thr = (K.fast32 && thr > 0.0) ? __double2float_rd(thr) : -1.0f;
   F.pad0 = F.pad1 = 0.0f;
   return F;
 }
 
 // O7-O11 over rows j in [j0, j0+PJ), all six i-planes: per (j, k) column six independent elements
 // (i = 0..5).  f32 data take the fp32 fast path above (no conversions, full-rate pipe); f64 data
-// the fp64 fast verify of make_consts.  Elements the fast test cannot decide take the exact
-// definition (rare).  FULL tiles (every element inside the grid) skip all validity predicates.  The
-// histogram takes one red.shared per element at the code clamped into the smem window; codes
-// outside it and outliers (code 0) are flagged through the lane's running max of (code - lo) and
-// handled by rare_path().
+// the fp64 fast verify of make_consts.  Both round with a BIASED magic M = 1.5 * 2^(p-1) + R, so the
+// low 16 bits of the rounded sum's bit pattern are the code R + q itself (0x4B400000 and 2^51 are
+// multiples of 2^16) and the histogram address is one multiply-add of that word.  An element is
+// accepted when the fast test certifies it AND |q| < W (W = min(R, HWIN/2): its code lies in the smem
+// window); every other valid element (near a half-integer, radius or verify outlier, out-of-window
+// code, non-finite input, huge offsets) gets code 0 and a per-lane sink as histogram address, and
+// the column then takes the exact definition (rare): exact code, histogram update by atomics, and
+// outliers flagged for rare_path().  FULL tiles skip every validity predicate.  Returns whether this
+// lane produced an outlier.
 template <typename T, bool IN_SMEM, bool HIST, bool FULL, int PJ, bool SLAB>
-__device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint64_t si, uint64_t sj,
-                                                  uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
-                                                  const LaneGeom& L, const double bh[4], const Fast32& F,
-                                                  const Consts& K, const uint32_t R, const HistSmem& hs) {
+__device__ __forceinline__ bool quantize_rows(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+                                              uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
+                                              const LaneGeom& L, const double bh[4], const Fast32& F,
+                                              const Consts& K, const uint32_t R, const HistSmem& hs,
+                                              unsigned long long* __restrict__ ghist) {
   const int lane = threadIdx.x & 31;
-  const uint32_t win_base = HIST ? (uint32_t)__cvta_generic_to_shared(hs.win) : 0u;  // &win[c - lo]
+  constexpr bool F32 = sizeof(T) == 4;
+  const uint32_t win_base = HIST ? (uint32_t)__cvta_generic_to_shared(hs.win) : 0u;
   const uint32_t sink = HIST ? (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * lane : 0u;
-  const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;   // window [lo, lo + nwin), lo >= 1
-  uint32_t umax = 0u;                                 // max over valid elements of (code - lo), unsigned
+  // &win[code - lo] = 4 * word + hb  (32-bit shared addresses, wrap-around arithmetic)
+  const uint32_t hb = win_base - 4u * ((F32 ? 0x4B400000u : 0u) + hs.lo);
+  const uint32_t W = HIST ? hs.W : R;
   if (IN_SMEM) { si = BS * TK; sj = TK; }             // shared stage: compile-time strides
   if (SLAB) { ci = PJ * TK; cj = TK; }                // codes: this warp's slab [i][jj][k]
-  constexpr bool F32 = sizeof(T) == 4;
   const float inv2eb32 = K.inv2eb32;
-  const float Rf = (float)R;
-  const double Rd = (double)R;
+  const float M32 = 12582912.0f + (float)R;           // 1.5 * 2^23 + R (exact)
+  const float Wf = (float)W;
+  const double M64 = RINT_MAGIC + (double)R;          // 1.5 * 2^52 + R (exact)
+  const double Wd = (double)W;
+  bool has_out = false;
   // columns (j, k) visited with incremental pointers and fp32 counters (no per-iteration division)
   const T* xrow = xs + (IN_SMEM ? (uint32_t)(j0 * TK + L.kcol) : (uint64_t)j0 * sj + L.kcol);
   uint16_t* crow = cs + (SLAB ? (uint32_t)L.kcol : (uint64_t)j0 * cj + L.kcol);
@@ -364,90 +382,89 @@ __device__ __forceinline__ uint32_t quantize_rows(const T* __restrict__ xs, uint
       if (IN_SMEM || FULL) xv[i] = xcol[i * si];
       else xv[i] = valid ? xcol[i * si] : T(0);
     }
-    uint32_t code[BS];
-    bool need = false;   // some element the fast test cannot decide -> exact definition below
+    uint32_t code[BS];   // low 16 bits = the code (0: not accepted)
+    uint32_t haddr[BS];
+    bool need = false;   // some valid element the fast test cannot decide -> exact definition below
     if (F32) {
-      // fp32 fast path: p32 = fma(b1, i, fma(b2, j, fma(b3, k, b0))) in fp32; bound in Fast32
-      const float base32 = __fmaf_rn(F.b2, fj, __fmaf_rn(F.b3, fk, F.b0));
+      const float base32 = __fmaf_rn(F.a2, fj, __fmaf_rn(F.a3, fk, F.a0));
 #pragma unroll
       for (int i = 0; i < BS; i++) {
-        const float p32 = i == 0 ? base32 : __fmaf_rn(F.b1, (float)i, base32);   // b1 finite: i = 0 exact
-        const float t32 = __fmul_rn(__fsub_rn((float)xv[i], p32), inv2eb32);
-        const float s32 = __fadd_rn(t32, 12582912.0f);       // 1.5 * 2^23: rint for |t32| < 2^22
-        const float r = __fsub_rn(s32, 12582912.0f);
-        const float e = __fsub_rn(t32, r);                    // exact (Sterbenz)
+        const bool valid = FULL || (cv && i < L.m0);
+        const float P = i == 0 ? base32 : __fmaf_rn(F.a1, (float)i, base32);   // a1 finite: i = 0 exact
+        const float t32 = __fmaf_rn((float)xv[i], inv2eb32, -P);
+        const float s32 = __fadd_rn(t32, M32);
+        const float r = __fsub_rn(s32, M32);
+        const float e = __fsub_rn(t32, r);                    // exact
         const float v = __fmaf_rn(F.k1, fabsf(t32), fabsf(e));
-        const bool ok = (v <= F.thr) && (fabsf(r) < Rf);
-        code[i] = ok ? (uint32_t)(__float_as_int(s32) - 0x4B400000 + (int)R) : 0u;   // O10
-        need |= !ok;
+        const bool ok = (v <= F.thr) && (fabsf(r) < Wf);
+        const uint32_t w = __float_as_uint(s32);
+        code[i] = ok ? w : 0u;
+        haddr[i] = (ok && valid) ? 4u * w + hb : sink;
+        need |= valid && !ok;
       }
     } else {
       const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * L.h + kk), bh[0]));
 #pragma unroll
       for (int i = 0; i < BS; i++) {
+        const bool valid = FULL || (cv && i < L.m0);
         const double xd = to_d<T>(xv[i]);
         const double p = __fma_rn(bh[1], (double)i, base);
         const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
-        const double sm = __dadd_rn(t, RINT_MAGIC);
-        const double q = __dsub_rn(sm, RINT_MAGIC);
+        const double sm = __dadd_rn(t, M64);
+        const double q = __dsub_rn(sm, M64);
         const double v = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, q)));   // fast verify (make_consts)
-        const bool ok = (v <= K.vthr) && (fabs(q) < Rd);
-        code[i] = ok ? (uint32_t)(__double2loint(sm) + (int)R) : 0u;
-        need |= !ok;
+        const bool ok = (v <= K.vthr) && (fabs(q) < Wd);
+        const uint32_t w = (uint32_t)__double2loint(sm);
+        code[i] = ok ? w : 0u;
+        haddr[i] = (ok && valid) ? 4u * w + hb : sink;
+        need |= valid && !ok;
       }
     }
     if (__any_sync(0xffffffffu, need)) {
       const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * L.h + kk), bh[0]));
 #pragma unroll
-      for (int i = 0; i < BS; i++)
-        if (code[i] == 0u) code[i] = exact_code<T>(xv[i], __fma_rn(bh[1], (double)i, base), K, R);
+      for (int i = 0; i < BS; i++) {
+        const bool valid = FULL || (cv && i < L.m0);
+        if (valid && code[i] == 0u) {
+          const uint32_t c = exact_code<T>(xv[i], __fma_rn(bh[1], (double)i, base), K, R);
+          code[i] = c;
+          if (c == 0u) has_out = true;   // counted in bin 0 by rare_path
+          else if (HIST) {
+            if (c - hs.lo < hs.nwin) atomicAdd(&hs.win[c - hs.lo], 1u);
+            else atomicAdd(&ghist[c], 1ull);
+          }
+        }
+      }
     }
 #pragma unroll
     for (int i = 0; i < BS; i++) {
       const bool valid = FULL || (cv && i < L.m0);
-      const uint32_t c = code[i];
-      if (valid) ccol[i * ci] = (uint16_t)c;
-      const uint32_t uc = c - wlo;                     // code 0 (outlier) wraps to a huge value
-      if (FULL) umax = max(umax, uc);
-      else if (valid) umax = max(umax, uc);
-      if (HIST) {  // O11: counted at the clamped bin; out-of-window codes corrected in rare_path
-        const uint32_t cw = min(uc, wtop);
-        red_smem_add(FULL ? win_base + 4u * cw : (valid ? win_base + 4u * cw : sink), FULL ? 1u : (valid ? 1u : 0u));
-      }
+      if (valid) ccol[i * ci] = (uint16_t)code[i];
+      if (HIST) red_smem_add(haddr[i], 1u);   // O11 (sink for elements not counted here)
     }
     }
     xrow += IN_SMEM ? (uint64_t)TK : sj;
     crow += cj;
   }
-  return umax;
+  return has_out;
 }
 
 // Rare path (warp-uniform entry): outliers of rows [j0, j0+PJ) -> (global index, value) with a
-// warp-aggregated append; histogram correction for codes outside the window (counted at the top
-// bin): moved to the global histogram / the zero counter.
+// warp-aggregated append, and their count into bin 0.
 template <typename T, bool HIST, int PJ>
 __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si, uint64_t sj,
                                           const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
-                                          int cs_j0, const LaneGeom& L, uint32_t umax, const TileCoord tc,
+                                          int cs_j0, const LaneGeom& L, bool has_out, const TileCoord tc,
                                           const Geo& g, const CompressOut<T>& o, const HistSmem& hs) {
   const int lane = threadIdx.x & 31;
-  const uint32_t wlo = hs.lo, wtop = hs.nwin - 1u;
-  const bool has_rare = umax > wtop;
-  if (!__any_sync(0xffffffffu, has_rare)) return;
+  if (!__any_sync(0xffffffffu, has_out)) return;
   const int j1 = min(j0 + PJ, L.m1);
   uint32_t nout = 0;
-  if (has_rare) {
+  if (has_out) {
     for (int j = j0; j < j1; j++)
       for (int kk = 0; kk < 3; kk++) {
         if (!L.kv(kk)) continue;
-        for (int i = 0; i < L.m0; i++) {
-          const uint32_t c = cs[i * ci + (j - cs_j0) * cj + L.kcol + kk];
-          nout += (c == 0u) ? 1u : 0u;
-          if (HIST && c != 0u && c - wlo > wtop) {   // counted at the top bin: move to global
-            atomicSub(&hs.win[wtop], 1u);
-            atomicAdd(&o.hist[c], 1ull);
-          }
-        }
+        for (int i = 0; i < L.m0; i++) nout += (cs[i * ci + (j - cs_j0) * cj + L.kcol + kk] == 0u) ? 1u : 0u;
       }
   }
   uint32_t incl = nout;
@@ -457,14 +474,10 @@ __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si,
     if (lane >= off) incl += v;
   }
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-  if (total == 0) return;
   unsigned long long basepos = 0;
   if (lane == 31) {
     basepos = atomicAdd(o.ocount, (unsigned long long)total);
-    if (HIST) {  // outliers were counted at the clamped (top) bin
-      atomicSub(&hs.win[wtop], total);
-      atomicAdd(hs.zero, total);
-    }
+    if (HIST) atomicAdd(hs.zero, total);
   }
   basepos = __shfl_sync(0xffffffffu, basepos, 31);
   unsigned long long pos = basepos + (incl - nout);
@@ -501,9 +514,9 @@ __device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t
   block_coefs<FULL>(V, L, K, beta, cc, bh);
   write_coefs(o, tc, g, L, cc, beta);
   const Fast32 F = fast32_consts(bh, K);
-  const uint32_t umax =
-      quantize_rows<T, IN_SMEM, HIST, FULL, BS, false>(xs, si, sj, cs, ci, cj, 0, L, bh, F, K, R, hs);
-  rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, 0, L, umax, tc, g, o, hs);
+  const bool has_out =
+      quantize_rows<T, IN_SMEM, HIST, FULL, BS, false>(xs, si, sj, cs, ci, cj, 0, L, bh, F, K, R, hs, o.hist);
+  rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, 0, L, has_out, tc, g, o, hs);
 }
 
 // ------------------------------------------------------------------------------------------
