@@ -134,6 +134,12 @@ int sz3g_uses_tma(const sz3g_grid* grid, int decompress);
 /* total device kernels this process has launched through the library (for launch counting) */
 uint64_t sz3g_launch_count(void);
 
+/* Performance tuning only (no call changes a result): set knob `key` ("CHUNK_C", "CHUNK_D", "CCFG",
+ * "PF"; defaults are the measured best, environment SZ3G_<KEY> overrides them) for
+ * launches issued after the call.  Process-global, not thread-safe against concurrent launches.
+ * Returns SZ3G_EINVAL for an unknown key. */
+int sz3g_set_tuning(const char* key, int64_t value);
+
 const char* sz3g_strerror(int code);
 const char* sz3g_last_cuda_error(void);
 const char* sz3g_version(void);

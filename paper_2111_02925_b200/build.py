@@ -23,16 +23,17 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, src: str = SRC, out: str = LIB, defines=()) -> str:
+    """nvcc `src` -> `out` (defaults: the in-tree library; another src/out builds an A/B variant)."""
+    if not force and out == LIB and not needs_build():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, SRC]
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *defines, *(["-Xptxas", "-v"] if verbose else []), "-I", os.path.join(ROOT, "include"),
+           "-o", tmp, src]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -421,7 +421,12 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
       }
     }
   } else {
-    const int grp = warp / (1 + Q), role = warp - grp * (1 + Q);   // role 0: moment warp, 1..Q: quantise
+    // role 0: moment warp, 1..Q: quantise.  Warp w runs on SM sub-partition w % 4.  With 1 + Q = 4 the
+    // role is rotated by the group index, so every sub-partition holds one moment warp and Q quantise
+    // warps; with 1 + Q = 3 and 5 groups the plain order already gives the best split (2/3/3/2
+    // quantise warps, moment warps and the producer on the lighter sub-partitions).
+    const int grp = warp / (1 + Q);
+    const int role = (1 + Q == 4) ? (warp - grp * (1 + Q) + (1 + Q) - grp % (1 + Q)) % (1 + Q) : warp - grp * (1 + Q);
     const Consts K = *s_k;
     uint32_t k = 0;
     if (role == 0) {
@@ -756,33 +761,42 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 // tuned configurations: (consumer warps, ring stages); smem fits the 227 KiB per-CTA limit
 constexpr int PF_TILES = 0;         // default L2 prefetch distance (tiles per CTA); 0: prefetched lines were evicted before use (ncu: +47% DRAM reads on c5)
 
-uint32_t chunk_tiles(bool decompress) {  // SZ3G_CHUNK_C / SZ3G_CHUNK_D override (tuning only)
-  static uint32_t vc = [] {
-    const char* e = getenv("SZ3G_CHUNK_C");
-    return e ? (uint32_t)std::max(1, atoi(e)) : 2u;
-  }();
-  static uint32_t vd = [] {
-    const char* e = getenv("SZ3G_CHUNK_D");
-    return e ? (uint32_t)std::max(1, atoi(e)) : 16u;
-  }();
-  return decompress ? vd : vc;
+// Tuning knobs (kernel shape, schedule and wait policy).  Defaults are the measured best on c5; each
+// can be overridden from the environment (SZ3G_<KEY>) or at run time with sz3g_set_tuning().  None
+// changes a result: only which kernel variant runs and how it is scheduled.
+struct Tuning {
+  const char* key;
+  int64_t value;
+};
+Tuning g_tuning[] = {
+    {"CHUNK_C", 2},   // adjacent tiles per CTA chunk, compress
+    {"CHUNK_D", 16},  // adjacent tiles per CTA chunk, decompress
+    {"CCFG", 0},      // f32 compress kernel shape: 0 = 5 x (1 + 2) warps, 1 = 3 x (1 + 3), 2 = 4 x (1 + 2), 3 = 4 x (1 + 3)
+    {"PF", PF_TILES}, // L2 prefetch distance of the compress producer (tiles)
+};
+std::once_flag g_tuning_env_once;
+
+int64_t* tuning_slot(const char* key) {
+  for (auto& t : g_tuning)
+    if (strcmp(t.key, key) == 0) return &t.value;
+  return nullptr;
 }
 
-int compress_cfg() {  // SZ3G_CCFG selects a compress kernel shape (tuning only)
-  static int v = [] {
-    const char* e = getenv("SZ3G_CCFG");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
+int64_t tuning(const char* key) {
+  std::call_once(g_tuning_env_once, [] {
+    for (auto& t : g_tuning) {
+      char name[32];
+      snprintf(name, sizeof(name), "SZ3G_%s", t.key);
+      if (const char* e = getenv(name)) t.value = atoll(e);
+    }
+  });
+  const int64_t* v = tuning_slot(key);
+  return v ? *v : 0;
 }
 
-uint32_t prefetch_tiles() {  // SZ3G_PF overrides (tuning only)
-  static uint32_t v = [] {
-    const char* e = getenv("SZ3G_PF");
-    return e ? (uint32_t)atoi(e) : (uint32_t)PF_TILES;
-  }();
-  return v;
-}
+uint32_t chunk_tiles(bool decompress) { return (uint32_t)std::max<int64_t>(1, tuning(decompress ? "CHUNK_D" : "CHUNK_C")); }
+int compress_cfg() { return (int)tuning("CCFG"); }
+uint32_t prefetch_tiles() { return (uint32_t)std::max<int64_t>(0, tuning("PF")); }
 constexpr int CN32 = 5, CQ32 = 2, CD32 = 2;  // f32 compress: 5 groups x (1 moment + 2 quantise warps) + producer = 16 warps
 constexpr int CN64 = 3, CQ64 = 3, CD64 = 2;  // f64 compress: 3 groups x (1 + 3) warps + producer = 13 warps
 constexpr int DG32 = 3, DN32 = 5, DD32 = 3;  // f32 decompress: 5 groups x 3 warps + producer; 3 x 7 KiB stages per group
@@ -870,6 +884,7 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
   ka.d_status = d_status;
   ka.pf = prefetch_tiles();
   ka.chunk = chunk_tiles(false);
+
   ka.uround = grid->dtype == SZ3G_F32 ? (5.9604644775390625e-08 + 1.12e-16) : 2.3e-16;
   const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
   const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
@@ -885,6 +900,8 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
                                     : launch_compress_tma<float, 3, 3, 3, false>(g, x, codes, codes_tma, ka, co, st);
       if (cfg == 2) return use_hist ? launch_compress_tma<float, 4, 2, 2, true>(g, x, codes, codes_tma, ka, co, st)
                                     : launch_compress_tma<float, 4, 2, 2, false>(g, x, codes, codes_tma, ka, co, st);
+      if (cfg == 3) return use_hist ? launch_compress_tma<float, 4, 3, 2, true>(g, x, codes, codes_tma, ka, co, st)
+                                    : launch_compress_tma<float, 4, 3, 2, false>(g, x, codes, codes_tma, ka, co, st);
       return use_hist ? launch_compress_tma<float, CN32, CQ32, CD32, true>(g, x, codes, codes_tma, ka, co, st)
                       : launch_compress_tma<float, CN32, CQ32, CD32, false>(g, x, codes, codes_tma, ka, co, st);
     }
@@ -926,6 +943,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   ka.d_minmax = d_minmax;
   ka.pf = prefetch_tiles();
   ka.chunk = chunk_tiles(true);
+
   int32_t* dummy_status = nullptr;  // decompress never reports: eb validated on the host
   ka.d_status = dummy_status;
   const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
@@ -995,6 +1013,15 @@ int sz3g_uses_tma(const sz3g_grid* grid, int decompress) {
 }
 
 uint64_t sz3g_launch_count(void) { return g_launches.load(); }
+
+int sz3g_set_tuning(const char* key, int64_t value) {
+  if (!key) return SZ3G_EINVAL;
+  tuning(key);  // apply the environment first, so an explicit call wins
+  int64_t* v = tuning_slot(key);
+  if (!v) return SZ3G_EINVAL;
+  *v = value;
+  return SZ3G_OK;
+}
 
 const char* sz3g_strerror(int code) {
   switch (code) {

@@ -51,12 +51,13 @@ def load(allow_build: bool = False):
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_build.LIB):
-        if allow_build:
+    path = os.environ.get("SZ3G_LIB", _build.LIB)   # SZ3G_LIB: an alternative build (A/B timing only)
+    if not os.path.exists(path):
+        if allow_build and path == _build.LIB:
             _build.build()
         else:
-            raise SZ3GError(f"libsz3g.so not built ({_build.LIB}); run `python -m paper_2111_02925_b200.build`")
-    lib = ctypes.CDLL(_build.LIB)
+            raise SZ3GError(f"libsz3g.so not built ({path}); run `python -m paper_2111_02925_b200.build`")
+    lib = ctypes.CDLL(path)
     P, U64, U32, I32, D = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_double
     GP, PP = ctypes.POINTER(Grid), ctypes.POINTER(Params)
     lib.sz3g_value_range.argtypes = [GP, P, P, P]
@@ -67,6 +68,8 @@ def load(allow_build: bool = False):
     lib.sz3g_num_blocks.restype = U64
     lib.sz3g_uses_tma.argtypes = [GP, I32]
     lib.sz3g_launch_count.restype = U64
+    if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
+        lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
         getattr(lib, f).argtypes = [I32]
         getattr(lib, f).restype = ctypes.c_char_p
@@ -77,7 +80,7 @@ def load(allow_build: bool = False):
 
 
 EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regression_decompress", "sz3g_histogram",
-                    "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_strerror",
+                    "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
 
@@ -141,6 +144,11 @@ def uses_tma(shape, dtype: torch.dtype, decompress: bool = False) -> bool:
 
 def launch_count() -> int:
     return int(load().sz3g_launch_count())
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Performance knob for later launches (sz3g_set_tuning); never changes a result."""
+    _check(load().sz3g_set_tuning(key.encode(), int(value)), f"set_tuning({key})")
 
 
 # ------------------------------------------------------------------------------------------- a0
