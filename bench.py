@@ -5,8 +5,10 @@ Metric (BASELINE.json): regression compress & decompress GB/s per GPU and at N G
 Workload: config c5 -- 1024 x 2048 x 2048 fp32 (16 GiB) k^-3 Gaussian random field (seed 4), eb = 1e-3 x
 value range, R = 32768, 6^3 blocks, sharded as block-aligned slabs over the N GPUs (strong scaling).
 
-One step = the whole hot path over the field: a0 value range (+ MAX all-reduce of the range when N > 1),
-a1-a7 fused compress (+ SUM all-reduce of the histogram when N > 1), a8 decompress + outlier scatter.
+One step = the whole hot path over the field.  Default (--path two-pass): analyze = a0 value range + a2-a3
+block coefficients in one read of x (+ MAX all-reduce of the range when N > 1), quantize = a4-a7 from those
+coefficients (+ SUM all-reduce of the histogram when N > 1), a8 decompress + outlier scatter.  --path fused:
+value range, then the single-pass a1-a7 kernel.
 value = input bytes of the whole field / step time (max over ranks), i.e. round-trip GB/s.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sz3g|reference]
@@ -46,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-planes", type=int, default=24)
+    ap.add_argument("--path", default="two-pass", choices=["two-pass", "fused"],
+                    help="REL compression: analyze (range + beta) -> quantize, or value_range -> fused compress")
     return ap.parse_args()
 
 
@@ -242,14 +246,28 @@ def main():
 
     ev = {}
 
+    two_pass = args.path == "two-pass"
+    beta = bufs.beta_buffer() if two_pass else None
+
     def step(record=None):
-        sz3g.value_range(x, bufs.minmax)
+        if record is not None:
+            record[4].record(stream)
+        if two_pass:
+            sz3g.regression_analyze(x, bufs.minmax, beta)
+        else:
+            sz3g.value_range(x, bufs.minmax)
+        if record is not None:
+            record[5].record(stream)
         pdist.allreduce_range_(bufs.minmax)
         bufs.reset()
         if record is not None:
             record[0].record(stream)
-        sz3g.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=bufs.minmax, bufs=bufs, reset=False,
-                                 dim0_offset=a0)
+        if two_pass:
+            sz3g.regression_quantize(x, cfg.eb, cfg.eb_mode, cfg.radius, bufs.minmax, beta, bufs=bufs, reset=False,
+                                     dim0_offset=a0)
+        else:
+            sz3g.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=bufs.minmax, bufs=bufs,
+                                     reset=False, dim0_offset=a0)
         if record is not None:
             record[1].record(stream)
         pdist.allreduce_hist_(bufs.hist)
@@ -264,7 +282,7 @@ def main():
     for _ in range(args.warmup):
         step()
     barrier(world)
-    recs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    recs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = sz3g.launch_count()
     with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local) as clk:
@@ -279,6 +297,7 @@ def main():
     ms_step = ms_total / args.steps
     comp_ms = sum(r[0].elapsed_time(r[1]) for r in recs) / args.steps
     dec_ms = sum(r[2].elapsed_time(r[3]) for r in recs) / args.steps
+    ana_ms = sum(r[4].elapsed_time(r[5]) for r in recs) / args.steps
     comp_ms_max = max_over_ranks(comp_ms, world)
     dec_ms_max = max_over_ranks(dec_ms, world)
 
@@ -286,7 +305,9 @@ def main():
                           bufs.outlier_val, bufs.outlier_count, bufs.hist, bufs.eb_abs, bufs.status).finalize()
     n_out = res.n_outliers
     # algorithmic bytes per launch: compress reads x, writes codes, coefficient codes, outliers
-    comp_bytes = N_local * (s + 2) + NB_local * 16 + n_out * (8 + s)
+    # (two-pass quantize also reads the analyze pass's beta, 32 B per block); analyze reads x, writes beta
+    comp_bytes = N_local * (s + 2) + NB_local * 16 + n_out * (8 + s) + (NB_local * 32 if two_pass else 0)
+    ana_bytes = N_local * s + (NB_local * 32 if two_pass else 0)
     dec_bytes = N_local * (2 + s) + NB_local * 16 + n_out * (8 + s)
     peaks = measured_peaks()
     comp_gbs = comp_bytes / (comp_ms * 1e-3) / 1e9
@@ -353,15 +374,22 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "shape": list(cfg.shape), "eb_rel": cfg.eb,
                        "radius": cfg.radius, "block": 6, "parallelism": f"slabs{world}",
                        "l2": "inputs (16 GiB) larger than L2; no flush"},
-            "roofline": {"bound": "hbm", "kernel": "k_compress_tma", "achieved": comp_gbs, "peak": peaks["hbm_gbs"],
+            "roofline": {"bound": "hbm", "kernel": "k_compress_tma" + ("<beta in>" if two_pass else ""),
+                         "achieved": comp_gbs, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": comp_gbs / peaks["hbm_gbs"],
-                         "traffic": profiled_traffic("k_compress_tma", cfg.name), "peak_source": peaks["source"],
+                         "traffic": profiled_traffic("k_compress_tma" + ("_beta" if two_pass else ""), cfg.name),
+                         "peak_source": peaks["source"],
                          "alg_bytes_per_launch": comp_bytes, "ms_per_launch": comp_ms},
             "compress_gbs": N_global * s / (comp_ms_max * 1e-3) / 1e9,
             "decompress_gbs": N_global * s / (dec_ms_max * 1e-3) / 1e9,
             "decompress_roofline": {"achieved": dec_bytes / (dec_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                                     "frac": dec_bytes / (dec_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                                     "ms_per_launch": dec_ms},
+            "analyze_roofline": {"kernel": "k_analyze_tma" if two_pass else "k_value_range",
+                                 "achieved": ana_bytes / (ana_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                 "frac": ana_bytes / (ana_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                 "ms_per_step": ana_ms},
+            "path": args.path,
             "outliers": n_out, "eb_abs": res.eb_abs,
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -100,6 +100,34 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
                              int64_t* hist, double* d_eb_abs, int32_t* d_status,
                              sz3g_stream_t stream);
 
+/* Two-pass compression (REL mode: the value range must be known before any coefficient or
+ * element can be quantised).  Split so that each pass reads x once:
+ *
+ * a0 + a2 + a3 -- sz3g_regression_analyze: ONE read of x yields the value range and the
+ * unquantised Lemma-1 coefficients of every block.
+ *   x         in   prod(dims) T, row-major.
+ *   d_minmax  out  device double[2] <- {min, max} as sz3g_value_range (NaN in max if a block of x
+ *                  holds a NaN or infinities of both signs; either way REL compression then
+ *                  reports SZ3G_STATUS_BAD_RANGE).  When sharded, all-reduce it (MIN, MAX)
+ *                  before sz3g_regression_quantize.
+ *   beta      out  4 x nblocks double, [block][b0,b1,b2,b3], 16-byte aligned: bit-identical to
+ *                  the coef_raw output of sz3g_regression_compress on the same x.
+ * Host errors: EINVAL (null / misaligned beta), EUNSUPPORTED, ECUDA.  3 launches.
+ *
+ * a4-a7 -- sz3g_regression_quantize: compression from that beta.  Arguments and outputs are those
+ * of sz3g_regression_compress (without coef_raw), plus
+ *   beta      in   the analyze output for the same x (16-byte aligned).
+ * Given the same x, params and d_minmax, codes / coef_codes / outliers / hist / d_eb_abs are
+ * bit-identical to sz3g_regression_compress.  1 launch.                                        */
+int sz3g_regression_analyze(const sz3g_grid* grid, const void* x, double* d_minmax, double* beta,
+                            sz3g_stream_t stream);
+int sz3g_regression_quantize(const sz3g_grid* grid, const sz3g_params* params, const void* x,
+                             const double* d_minmax, const double* beta, uint16_t* codes,
+                             int32_t* coef_codes, uint64_t* outlier_idx, void* outlier_val,
+                             uint64_t outlier_cap, unsigned long long* d_outlier_count,
+                             int64_t* hist, double* d_eb_abs, int32_t* d_status,
+                             sz3g_stream_t stream);
+
 /* a8 -- decompression (recover): x_out = (T)(p + 2 eb (c - R)) for c != 0, then the
  * stored outlier values are scattered to their indices (2 launches, stream-ordered).
  *   params           the compression parameters: ABS with eb = eb_abs, or REL with the same

@@ -143,10 +143,6 @@ struct KArgs {
 // 384 B of f32): on different SMs at different times the partially written units are evicted and
 // read back (ncu: +31% DRAM reads); chunks keep them on one SM while the grid-wide working set stays
 // a compact band of the field (good DRAM page locality).
-__device__ __forceinline__ uint64_t tile_at(uint64_t n, uint32_t C) {
-  return ((n / C) * gridDim.x + blockIdx.x) * C + n % C;
-}
-
 // The same sequence walked incrementally with a fixed stride in n (no division per tile).
 struct TileWalk {
   uint64_t chunk;   // n / C
@@ -167,15 +163,16 @@ struct TileWalk {
   }
 };
 
-__device__ __forceinline__ void hist_init(HistSmem& hs, uint32_t* win, uint32_t* zero, uint32_t R) {
+__device__ __forceinline__ void hist_init(HistSmem& hs, uint32_t* win, uint32_t* zero, uint32_t R,
+                                          uint32_t hwin = HWIN) {
   hs.win = win;
   hs.zero = zero;
   hs.dummy = zero + 1;  // 32 sink slots follow the zero-bin counter
   // window of codes counted in shared memory: [lo, lo + nwin), lo >= 1 so code 0 (outliers) is
   // always outside it and goes through the zero counter
-  hs.lo = (2u * R - 1u <= (uint32_t)HWIN) ? 1u : R - HWIN / 2;
-  hs.nwin = min(2u * R - 1u, (uint32_t)HWIN);
-  hs.W = (2u * R - 1u <= (uint32_t)HWIN) ? R : (uint32_t)HWIN / 2u;
+  hs.lo = (2u * R - 1u <= hwin) ? 1u : R - hwin / 2;
+  hs.nwin = min(2u * R - 1u, hwin);
+  hs.W = (2u * R - 1u <= hwin) ? R : hwin / 2u;
   for (uint32_t b = threadIdx.x; b < hs.nwin; b += blockDim.x) win[b] = 0u;
   if (threadIdx.x == 0) *zero = 0u;
 }
@@ -211,41 +208,16 @@ __device__ __forceinline__ void overflow_check(const KArgs& a, const unsigned lo
   }
 }
 
-template <typename T, bool IN_SMEM, bool HIST>
+template <typename T, bool IN_SMEM, bool HIST, bool BETA>
 __device__ __forceinline__ void compress_tile_dispatch(const T* xs, uint64_t si, uint64_t sj, uint16_t* cs, uint64_t ci,
                                                        uint64_t cj, const TileCoord tc, const Geo& g, const Consts& K,
                                                        uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
-  if (tile_full(tc, g)) compress_tile<T, IN_SMEM, HIST, true>(xs, si, sj, cs, ci, cj, tc, g, K, R, o, hs);
-  else compress_tile<T, IN_SMEM, HIST, false>(xs, si, sj, cs, ci, cj, tc, g, K, R, o, hs);
-}
-
-// copy a staged 6x6x96 code tile to the global code array (fallback when no TMA store applies:
-// n2 * 2 bytes is not a multiple of 16).  Rows are 96 codes; 32-bit stores when n2 is even.
-__device__ __forceinline__ void store_code_rows(const uint16_t* __restrict__ cbuf, uint16_t* __restrict__ codes,
-                                                const TileCoord tc, const Geo& g) {
-  const int lane = threadIdx.x & 31;
-  const int m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
-  const int m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
-  const int kval = (int)umin64(TK, g.n2 - (uint64_t)tc.c * TK);
-  const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
-  const bool even = (g.n2 & 1) == 0 && (reinterpret_cast<uintptr_t>(codes) & 3) == 0;
-  for (int i = 0; i < m0; i++)
-    for (int j = 0; j < m1; j++) {
-      const uint16_t* src = cbuf + (i * BS + j) * TK;
-      uint16_t* dst = codes + off + ((uint64_t)i * g.n1 + j) * g.n2;
-      if (even) {
-        for (int w = lane; 2 * w < kval; w += 32) {
-          if (2 * w + 1 < kval) reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(src)[w];
-          else dst[2 * w] = src[2 * w];
-        }
-      } else {
-        for (int k = lane; k < kval; k += 32) dst[k] = src[k];
-      }
-    }
+  if (tile_full(tc, g)) compress_tile<T, IN_SMEM, HIST, true, BETA>(xs, si, sj, cs, ci, cj, tc, g, K, R, o, hs);
+  else compress_tile<T, IN_SMEM, HIST, false, BETA>(xs, si, sj, cs, ci, cj, tc, g, K, R, o, hs);
 }
 
 // ---------------------------------------------------------------------------------- compress, plain
-template <typename T, bool HIST>
+template <typename T, bool HIST, bool BETA>
 __global__ void __launch_bounds__(128) k_compress_plain(const T* __restrict__ x, KArgs a, CompressOut<T> o) {
   __shared__ uint32_t s_win[HWIN];
   __shared__ uint32_t s_zero[33];
@@ -260,11 +232,120 @@ __global__ void __launch_bounds__(128) k_compress_plain(const T* __restrict__ x,
   for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < g.ntiles; t += warps) {
     const TileCoord tc = decode_tile(t, g);
     const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
-    compress_tile_dispatch<T, false, HIST>(x + off, g.n1 * g.n2, g.n2, o.codes + off, g.n1 * g.n2, g.n2, tc, g, K, a.R, o, hs);
+    compress_tile_dispatch<T, false, HIST, BETA>(x + off, g.n1 * g.n2, g.n2, o.codes + off, g.n1 * g.n2, g.n2, tc, g, K, a.R, o, hs);
   }
   __syncthreads();
   if (HIST) hist_flush(hs, o.hist);
   overflow_check(a, o.ocount, o.cap);
+}
+
+// ---------------------------------------------------------------------------------- analyze (two-pass)
+// a0 + a2 + a3 in one read of x: the value range (ordered-u64 keys, as k_value_range) and the
+// unquantised beta of every block.  CTA epilogue: min / max over the CTA's lanes -> global atomics.
+template <typename T>
+__device__ __forceinline__ void range_epilogue(MinMax<T> mm, bool nan, unsigned long long* keys, uint64_t* s_red) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  unsigned long long klo = ord_key((double)mm.lo), khi = ord_key((double)mm.hi);
+  if (__any_sync(0xffffffffu, nan)) khi = ord_key(__longlong_as_double(0x7ff8000000000000ll));  // max key = +NaN
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    klo = min(klo, __shfl_xor_sync(0xffffffffu, klo, o));
+    khi = max(khi, __shfl_xor_sync(0xffffffffu, khi, o));
+  }
+  if (l == 0) { s_red[2 * w] = klo; s_red[2 * w + 1] = khi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); i++) {
+      klo = min(klo, (unsigned long long)s_red[2 * i]);
+      khi = max(khi, (unsigned long long)s_red[2 * i + 1]);
+    }
+    atomicMin(&keys[0], klo);
+    atomicMax(&keys[1], khi);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_analyze_plain(const T* __restrict__ x, KArgs a, double* __restrict__ beta,
+                                                       unsigned long long* keys) {
+  __shared__ uint64_t s_red[8];
+  const Geo& g = a.g;
+  MinMax<T> mm;
+  mm.init();
+  bool nan = false;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < g.ntiles; t += warps) {
+    const TileCoord tc = decode_tile(t, g);
+    const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+    nan |= analyze_tile<T, false, false>(x + off, g.n1 * g.n2, g.n2, tc, g, beta, mm);
+  }
+  range_epilogue(mm, nan, keys, s_red);
+}
+
+// Persistent, one CTA per SM, W warps; each warp owns a private D-stage ring of 6x6x96 tiles and
+// feeds it itself (lane 0 issues the TMA load of tile k + D into the stage tile k has just left), so
+// there is no producer warp and no empty barrier.
+template <typename T, int W, int D>
+struct AnalyzeSmem {
+  static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr size_t off_bar = (size_t)W * D * stage_bytes;
+  static constexpr size_t off_red = off_bar + (size_t)W * D * sizeof(uint64_t);
+  static constexpr size_t total = off_red + 2 * W * sizeof(uint64_t) + 16;
+};
+
+template <typename T, int W, int D>
+__global__ void __launch_bounds__(W * 32, 1)
+    k_analyze_tma(const __grid_constant__ CUtensorMap tm_x, KArgs a, double* __restrict__ beta,
+                  unsigned long long* keys) {
+  using L_ = AnalyzeSmem<T, W, D>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
+  uint64_t* s_red = reinterpret_cast<uint64_t*>(smem + L_::off_red);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W * D; s++) ptx::mbar_init(&full[s], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const Geo& g = a.g;
+  T* ring = reinterpret_cast<T*>(smem) + (size_t)warp * D * TILE_ELEMS;
+  uint64_t* bar = full + warp * D;
+  MinMax<T> mm;
+  mm.init();
+  bool nan = false;
+  TileWalk tw(warp, a.chunk, W), tl(warp, a.chunk, W);   // compute cursor, load cursor
+  if (lane == 0) {
+    ptx::prefetch_tensormap(&tm_x);
+    for (int d = 0; d < D; d++, tl.next()) {
+      const uint64_t t = tl.tile();
+      if (t >= g.ntiles) break;
+      const TileCoord tc = decode_tile(t, g);
+      ptx::mbar_arrive_expect_tx(&bar[d], (uint32_t)L_::stage_bytes);
+      ptx::tma_load_3d(ring + (size_t)d * TILE_ELEMS, &tm_x, &bar[d], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+    }
+  }
+  for (uint32_t k = 0;; k++, tw.next()) {
+    const uint64_t t = tw.tile();
+    if (t >= g.ntiles) break;
+    const uint32_t s = k % D, ph = (k / D) & 1u;
+    const TileCoord tc = decode_tile(t, g);
+    ptx::mbar_wait(&bar[s], ph);
+    const T* xs = ring + (size_t)s * TILE_ELEMS;
+    if (tile_full(tc, g)) nan |= analyze_tile<T, true, true>(xs, BS * TK, TK, tc, g, beta, mm);
+    else nan |= analyze_tile<T, true, false>(xs, BS * TK, TK, tc, g, beta, mm);
+    __syncwarp();
+    if (lane == 0) {   // every lane's reads of the stage are done: refill it with tile k + D
+      const uint64_t t2 = tl.tile();
+      if (t2 < g.ntiles) {
+        const TileCoord tc2 = decode_tile(t2, g);
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive_expect_tx(&bar[s], (uint32_t)L_::stage_bytes);
+        ptx::tma_load_3d(ring + (size_t)s * TILE_ELEMS, &tm_x, &bar[s], (int)(tc2.c * TK), (int)(tc2.b * BS),
+                         (int)(tc2.a * BS));
+      }
+      tl.next();
+    }
+  }
+  range_epilogue(mm, nan, keys, s_red);
 }
 
 // ---------------------------------------------------------------------------------- compress, TMA
@@ -282,17 +363,18 @@ struct CoefSlot {  // per stage: the tile's 16 blocks
   Fast32 f[16];
 };
 
-template <typename T, int NG, int Q, int D>
+template <typename T, int NG, int Q, int D, bool BETA = false, bool SELF = false, int HW = HWIN>
 struct CompressSmem {
   static constexpr int P = BS / Q;
   static constexpr int S = NG * D;
-  static constexpr int WARPS = NG * (1 + Q) + 1;
-  static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr int WARPS = NG * (1 + Q) + (SELF ? 0 : 1);   // SELF: no producer warp
+  static constexpr size_t tile_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr size_t stage_bytes = tile_bytes + (BETA ? 16 * 32 : 0);   // + beta of the tile's 16 blocks
   static constexpr size_t slab_bytes = sizeof(uint16_t) * BS * P * TK;
   static constexpr size_t off_slab = S * stage_bytes;
   static constexpr size_t off_slot = off_slab + (size_t)NG * Q * slab_bytes;
   static constexpr size_t off_hist = off_slot + S * sizeof(CoefSlot);
-  static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (HWIN + 36);
+  static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (HW + 36);
   static constexpr size_t off_k = off_bar + 3 * S * sizeof(uint64_t);
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
 };
@@ -342,6 +424,29 @@ __device__ __forceinline__ void moment_warp_tile(const T* __restrict__ xs, CoefS
   }
 }
 
+// two-pass mode: the role-0 warp quantises the coefficients the analyze pass computed (bulk-copied
+// into the stage behind the tile) instead of computing moments
+template <typename T, bool FULL>
+__device__ __forceinline__ void coef_warp_tile(const double* __restrict__ bstage, CoefSlot* slot, const TileCoord tc,
+                                               const Geo& g, const Consts& K, const CompressOut<T>& o) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int bl = (threadIdx.x & 31) >> 1;
+  double beta[4] = {0.0, 0.0, 0.0, 0.0}, bh[4];
+  int32_t cc[4];
+  if (L.m2 > 0) {
+    const double2 b01 = reinterpret_cast<const double2*>(bstage)[2 * bl];
+    const double2 b23 = reinterpret_cast<const double2*>(bstage)[2 * bl + 1];
+    beta[0] = b01.x; beta[1] = b01.y; beta[2] = b23.x; beta[3] = b23.y;
+  }
+  block_codes(beta, K, cc, bh);
+  write_coefs(o, tc, g, L, cc, beta);
+  if (L.h == 0) {
+#pragma unroll
+    for (int d = 0; d < 4; d++) slot->bh[bl][d] = bh[d];
+    slot->f[bl] = fast32_consts(bh, K);
+  }
+}
+
 template <typename T, bool HIST, bool FULL, int P>
 __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const CoefSlot* slot, uint16_t* slab,
                                                 int j0, const TileCoord tc, const Geo& g, const Consts& K,
@@ -357,16 +462,19 @@ __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const 
   rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, has_out, tc, g, o, hs);
 }
 
-template <typename T, int NG, int Q, int D, bool HIST>
-__global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
+// SELF: no producer warp; the role-0 warp of each group feeds its own group's ring (it issues the
+// load of tile k + D - 1 once the quantise warps have released tile k - 1, right after it has
+// published tile k's coefficients), with an optional L2 prefetch one tile further ahead.
+template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF, int HW>
+__global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW>::WARPS * 32, 1)
     k_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, int codes_tma,
                    KArgs a, CompressOut<T> o) {
-  using L_ = CompressSmem<T, NG, Q, D>;
+  using L_ = CompressSmem<T, NG, Q, D, BETA, SELF, HW>;
   constexpr int P = L_::P;
   constexpr int S = L_::S;
   static_assert(BS % Q == 0, "Q must divide 6");
   extern __shared__ __align__(128) uint8_t smem[];
-  T* stages = reinterpret_cast<T*>(smem);
+  auto stage_x = [&](uint32_t s) { return reinterpret_cast<T*>(smem + (size_t)s * L_::stage_bytes); };
   uint16_t* slabs = reinterpret_cast<uint16_t*>(smem + L_::off_slab);
   CoefSlot* slots = reinterpret_cast<CoefSlot*>(smem + L_::off_slot);
   uint32_t* s_win = reinterpret_cast<uint32_t*>(smem + L_::off_hist);
@@ -377,7 +485,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
   int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   HistSmem hs;
-  hist_init(hs, s_win, s_win + HWIN, a.R);
+  hist_init(hs, s_win, s_win + HW, a.R, HW);
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       ptx::mbar_init(&full[s], 1);
@@ -388,7 +496,22 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
   }
   if (!cta_consts(a, s_k, s_ok)) return;
   const Geo& g = a.g;
-  if (warp == NG * (1 + Q)) {
+  // one TMA load of tile t into stage s (+ the beta of its blocks in two-pass mode)
+  auto issue_load = [&](uint32_t s, uint64_t t) {
+    const TileCoord tc = decode_tile(t, g);
+    if (BETA) {   // the tile and the beta of its <= 16 blocks complete on the same barrier
+      const uint32_t nblk = min(16u, g.NB2 - tc.c * 16u);
+      ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L_::tile_bytes + 32u * nblk);
+      ptx::tma_load_3d(stage_x(s), &tm_x, &full[s], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+      const uint64_t bid0 = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + (uint64_t)tc.c * 16u;
+      ptx::bulk_load(reinterpret_cast<uint8_t*>(stage_x(s)) + L_::tile_bytes, o.beta_in + 4 * bid0, 32u * nblk,
+                     &full[s]);
+    } else {
+      ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L_::stage_bytes);
+      ptx::tma_load_3d(stage_x(s), &tm_x, &full[s], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+    }
+  };
+  if (!SELF && warp == NG * (1 + Q)) {
     // ---------------- producer
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_x);
@@ -414,10 +537,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
         const uint32_t s = gq * D + k % D, ph = (k / D) & 1u;
         if (++gq == NG) { gq = 0; k++; }
         ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
-        const TileCoord tc = decode_tile(t, g);
-        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L_::stage_bytes);
-        ptx::tma_load_3d(stages + (size_t)s * TILE_ELEMS, &tm_x, &full[s], (int)(tc.c * TK), (int)(tc.b * BS),
-                         (int)(tc.a * BS));
+        issue_load(s, t);
       }
     }
   } else {
@@ -430,18 +550,51 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
     const Consts K = *s_k;
     uint32_t k = 0;
     if (role == 0) {
-      // ---------------- moment warp
+      // ---------------- moment warp (SELF: also the loader of its group's ring)
+      TileWalk tl(grp, a.chunk, NG), tp(grp, a.chunk, NG);   // load cursor, L2-prefetch cursor
+      if (SELF && lane == 0) {
+        ptx::prefetch_tensormap(&tm_x);
+        for (int d = 0; d < D - 1; d++, tl.next()) {   // tiles 0 .. D-2 now, tile k + D - 1 in iteration k
+          const uint64_t t = tl.tile();
+          if (t < g.ntiles) issue_load(grp * D + d, t);
+        }
+        for (int d = 0; d < D - 1 + (int)a.pf; d++) tp.next();
+      }
       for (TileWalk tw(grp, a.chunk, NG);; tw.next(), k++) {
         const uint64_t t = tw.tile();
         if (t >= g.ntiles) break;
         const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
         const TileCoord tc = decode_tile(t, g);
         ptx::mbar_wait(&full[s], ph);
-        const T* xs = stages + (size_t)s * TILE_ELEMS;
-        if (tile_full(tc, g)) moment_warp_tile<T, true>(xs, &slots[s], tc, g, K, o);
-        else moment_warp_tile<T, false>(xs, &slots[s], tc, g, K, o);
+        const T* xs = stage_x(s);
+        if (BETA) {
+          const double* bst = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(xs) + L_::tile_bytes);
+          if (tile_full(tc, g)) coef_warp_tile<T, true>(bst, &slots[s], tc, g, K, o);
+          else coef_warp_tile<T, false>(bst, &slots[s], tc, g, K, o);
+        } else {
+          if (tile_full(tc, g)) moment_warp_tile<T, true>(xs, &slots[s], tc, g, K, o);
+          else moment_warp_tile<T, false>(xs, &slots[s], tc, g, K, o);
+        }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&ready[s]);
+        if (SELF && lane == 0) {   // then load tile n = k + D - 1 once the quantise warps release tile n - D
+          const uint32_t n = k + D - 1, sn = grp * D + n % D;
+          const uint64_t tn = tl.tile();
+          if (tn < g.ntiles) {
+            ptx::mbar_wait_backoff(&empty[sn], ((n / D) & 1u) ^ 1u);
+            issue_load(sn, tn);
+          }
+          tl.next();
+          if (a.pf) {
+            const uint64_t tq = tp.tile();
+            if (tq < g.ntiles) {
+              const TileCoord tc = decode_tile(tq, g);
+              ptx::tma_prefetch_3d(&tm_x, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+            }
+            tp.next();
+          }
+        }
+        __syncwarp();
       }
     } else {
       // ---------------- quantise warp q: rows [j0, j0 + P)
@@ -456,7 +609,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D>::WARPS * 32, 1)
         __syncwarp();
         ptx::mbar_wait(&full[s], ph);
         ptx::mbar_wait(&ready[s], ph);
-        const T* xs = stages + (size_t)s * TILE_ELEMS;
+        const T* xs = stage_x(s);
         if (tile_full(tc, g)) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
         else quant_warp_tile<T, HIST, false, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
         __syncwarp();
@@ -547,7 +700,6 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
   }
   if (!cta_consts(a, s_k, s_ok)) return;
   const Geo& g = a.g;
-  const uint64_t Gr = gridDim.x;
   if (warp == NG * G) {
     // ---------------- producer
     if (lane == 0) {
@@ -801,18 +953,20 @@ constexpr int CN32 = 5, CQ32 = 2, CD32 = 2;  // f32 compress: 5 groups x (1 mome
 constexpr int CN64 = 3, CQ64 = 3, CD64 = 2;  // f64 compress: 3 groups x (1 + 3) warps + producer = 13 warps
 constexpr int DG32 = 3, DN32 = 5, DD32 = 3;  // f32 decompress: 5 groups x 3 warps + producer; 3 x 7 KiB stages per group
 constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 warps + producer
+constexpr int AW32 = 8, AD32 = 2;            // f32 analyze: 8 self-fed warps x 2 stages (13.5 KiB)
+constexpr int AW64 = 4, AD64 = 2;            // f64 analyze: 4 warps x 2 stages (27 KiB)
 
-template <typename T, int NG, int Q, int D, bool HIST>
+template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN>
 int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
                         const CompressOut<T>& co, cudaStream_t st) {
-  using L = CompressSmem<T, NG, Q, D>;
+  using L = CompressSmem<T, NG, Q, D, BETA, SELF, HW>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mx, mc;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
   memset(&mc, 0, sizeof(mc));
   if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g, L::P, true)) codes_tma = false;
-  auto kern = k_compress_tma<T, NG, Q, D, HIST>;
+  auto kern = k_compress_tma<T, NG, Q, D, HIST, BETA, SELF, HW>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
@@ -835,6 +989,99 @@ int launch_decompress_tma(const Geo& g, const uint16_t* codes, const int32_t* co
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
   kern<<<(unsigned)grid, (NG * G + 1) * 32, L::total, st>>>(mc, mx, coef, ka);
   return check_launch(1);
+}
+
+template <typename T, bool BETA>
+int compress_launch(const Geo& g, const void* x, uint16_t* codes, bool tma, bool codes_tma, bool use_hist,
+                    const KArgs& ka, const CompressOut<T>& co, cudaStream_t st) {
+  if (tma) {
+    if constexpr (sizeof(T) == 4) {
+      const int cfg = compress_cfg();
+      if (cfg == 3)
+        return use_hist ? launch_compress_tma<T, 4, 3, 2, true, BETA>(g, x, codes, codes_tma, ka, co, st)
+                        : launch_compress_tma<T, 4, 3, 2, false, BETA>(g, x, codes, codes_tma, ka, co, st);
+      if (cfg == 4)   // 4 groups x (1 loader/coefficient warp + 3 quantise warps), no producer warp
+        return use_hist ? launch_compress_tma<T, 4, 3, 2, true, BETA, true>(g, x, codes, codes_tma, ka, co, st)
+                        : launch_compress_tma<T, 4, 3, 2, false, BETA, true>(g, x, codes, codes_tma, ka, co, st);
+      if (cfg == 5)   // as 4 with 3-deep rings (histogram window 4096 bins to fit)
+        return use_hist ? launch_compress_tma<T, 4, 3, 3, true, BETA, true, 4096>(g, x, codes, codes_tma, ka, co, st)
+                        : launch_compress_tma<T, 4, 3, 3, false, BETA, true, 4096>(g, x, codes, codes_tma, ka, co, st);
+      return use_hist ? launch_compress_tma<T, CN32, CQ32, CD32, true, BETA>(g, x, codes, codes_tma, ka, co, st)
+                      : launch_compress_tma<T, CN32, CQ32, CD32, false, BETA>(g, x, codes, codes_tma, ka, co, st);
+    } else {
+      return use_hist ? launch_compress_tma<T, CN64, CQ64, CD64, true, BETA>(g, x, codes, codes_tma, ka, co, st)
+                      : launch_compress_tma<T, CN64, CQ64, CD64, false, BETA>(g, x, codes, codes_tma, ka, co, st);
+    }
+  }
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
+  if (use_hist) k_compress_plain<T, true, BETA><<<blocks, 128, 0, st>>>((const T*)x, ka, co);
+  else k_compress_plain<T, false, BETA><<<blocks, 128, 0, st>>>((const T*)x, ka, co);
+  return check_launch(1);
+}
+
+// sz3g_regression_compress (beta_in == nullptr: moments in the kernel) and sz3g_regression_quantize
+// (beta_in: the analyze pass's coefficients) share validation, constants and dispatch.
+int compress_common(const sz3g_grid* grid, const sz3g_params* params, const void* x, const double* d_minmax,
+                    const double* beta_in, uint16_t* codes, int32_t* coef_codes, double* coef_raw,
+                    uint64_t* outlier_idx, void* outlier_val, uint64_t outlier_cap,
+                    unsigned long long* d_outlier_count, int64_t* hist, double* d_eb_abs, int32_t* d_status,
+                    sz3g_stream_t stream) {
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  rc = validate_params(params);
+  if (rc) return rc;
+  if (!x || !codes || !coef_codes || !d_outlier_count || !d_status) return SZ3G_EINVAL;
+  if (outlier_cap > 0 && (!outlier_idx || !outlier_val)) return SZ3G_EINVAL;
+  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(coef_codes) & 15) || (coef_raw && (reinterpret_cast<uintptr_t>(coef_raw) & 15)))
+    return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Geo g = make_geo(grid);
+  KArgs ka;
+  memset(&ka, 0, sizeof(ka));
+  ka.g = g;
+  ka.R = params->radius;
+  ka.eb_mode = (int)params->eb_mode;
+  ka.eb = params->eb;
+  ka.d_minmax = d_minmax;
+  ka.d_eb_abs = d_eb_abs;
+  ka.d_status = d_status;
+  ka.pf = prefetch_tiles();
+  ka.chunk = chunk_tiles(false);
+  ka.uround = grid->dtype == SZ3G_F32 ? (5.9604644775390625e-08 + 1.12e-16) : 2.3e-16;
+  const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
+  const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
+  const bool tma = !generic && map_ok(x, es, g);
+  const bool codes_tma = tma && map_ok(codes, 2, g);
+  const bool use_hist = hist_ptr_nonnull(hist);
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(hist);
+  if (grid->dtype == SZ3G_F32) {
+    CompressOut<float> co{codes, coef_codes, coef_raw, outlier_idx, (float*)outlier_val, outlier_cap,
+                          d_outlier_count, h, beta_in};
+    return beta_in ? compress_launch<float, true>(g, x, codes, tma, codes_tma, use_hist, ka, co, st)
+                   : compress_launch<float, false>(g, x, codes, tma, codes_tma, use_hist, ka, co, st);
+  }
+  CompressOut<double> co{codes, coef_codes, coef_raw, outlier_idx, (double*)outlier_val, outlier_cap,
+                         d_outlier_count, h, beta_in};
+  return beta_in ? compress_launch<double, true>(g, x, codes, tma, codes_tma, use_hist, ka, co, st)
+                 : compress_launch<double, false>(g, x, codes, tma, codes_tma, use_hist, ka, co, st);
+}
+
+template <typename T, int W, int D>
+int launch_analyze_tma(const Geo& g, const void* x, double* beta, unsigned long long* keys, const KArgs& ka,
+                       cudaStream_t st) {
+  using L = AnalyzeSmem<T, W, D>;
+  static_assert(L::total <= 232448, "smem");
+  CUtensorMap mx;
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
+  auto kern = k_analyze_tma<T, W, D>;
+  cudaError_t e = set_smem(kern, L::total);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
+  kern<<<(unsigned)grid, W * 32, L::total, st>>>(mx, ka, beta, keys);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SZ3G_OK;
 }
 
 }  // namespace
@@ -863,61 +1110,46 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
                              uint64_t* outlier_idx, void* outlier_val, uint64_t outlier_cap,
                              unsigned long long* d_outlier_count, int64_t* hist, double* d_eb_abs,
                              int32_t* d_status, sz3g_stream_t stream) {
+  return compress_common(grid, params, x, d_minmax, nullptr, codes, coef_codes, coef_raw, outlier_idx, outlier_val,
+                         outlier_cap, d_outlier_count, hist, d_eb_abs, d_status, stream);
+}
+
+int sz3g_regression_analyze(const sz3g_grid* grid, const void* x, double* d_minmax, double* beta,
+                            sz3g_stream_t stream) {
   int rc = validate_grid(grid);
   if (rc) return rc;
-  rc = validate_params(params);
-  if (rc) return rc;
-  if (!x || !codes || !coef_codes || !d_outlier_count || !d_status) return SZ3G_EINVAL;
-  if (outlier_cap > 0 && (!outlier_idx || !outlier_val)) return SZ3G_EINVAL;
-  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
-  if ((reinterpret_cast<uintptr_t>(coef_codes) & 15) || (coef_raw && (reinterpret_cast<uintptr_t>(coef_raw) & 15)))
-    return SZ3G_EINVAL;
+  if (!x || !d_minmax || !beta || (reinterpret_cast<uintptr_t>(beta) & 15)) return SZ3G_EINVAL;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const Geo g = make_geo(grid);
   KArgs ka;
+  memset(&ka, 0, sizeof(ka));
   ka.g = g;
-  ka.R = params->radius;
-  ka.eb_mode = (int)params->eb_mode;
-  ka.eb = params->eb;
-  ka.d_minmax = d_minmax;
-  ka.d_eb_abs = d_eb_abs;
-  ka.d_status = d_status;
-  ka.pf = prefetch_tiles();
   ka.chunk = chunk_tiles(false);
-
-  ka.uround = grid->dtype == SZ3G_F32 ? (5.9604644775390625e-08 + 1.12e-16) : 2.3e-16;
-  const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(d_minmax);
+  k_range_init<<<1, 1, 0, st>>>(keys);
   const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
-  const bool tma = !generic && map_ok(x, es, g);
-  const bool codes_tma = tma && map_ok(codes, 2, g);
-  const bool use_hist = hist_ptr_nonnull(hist);
-  if (grid->dtype == SZ3G_F32) {
-    CompressOut<float> co{codes, coef_codes, coef_raw, outlier_idx, (float*)outlier_val, outlier_cap,
-                          d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
-    if (tma) {
-      const int cfg = compress_cfg();
-      if (cfg == 1) return use_hist ? launch_compress_tma<float, 3, 3, 3, true>(g, x, codes, codes_tma, ka, co, st)
-                                    : launch_compress_tma<float, 3, 3, 3, false>(g, x, codes, codes_tma, ka, co, st);
-      if (cfg == 2) return use_hist ? launch_compress_tma<float, 4, 2, 2, true>(g, x, codes, codes_tma, ka, co, st)
-                                    : launch_compress_tma<float, 4, 2, 2, false>(g, x, codes, codes_tma, ka, co, st);
-      if (cfg == 3) return use_hist ? launch_compress_tma<float, 4, 3, 2, true>(g, x, codes, codes_tma, ka, co, st)
-                                    : launch_compress_tma<float, 4, 3, 2, false>(g, x, codes, codes_tma, ka, co, st);
-      return use_hist ? launch_compress_tma<float, CN32, CQ32, CD32, true>(g, x, codes, codes_tma, ka, co, st)
-                      : launch_compress_tma<float, CN32, CQ32, CD32, false>(g, x, codes, codes_tma, ka, co, st);
-    }
-    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
-    if (use_hist) k_compress_plain<float, true><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
-    else k_compress_plain<float, false><<<blocks, 128, 0, st>>>((const float*)x, ka, co);
+  if (map_ok(x, es, g)) {
+    rc = grid->dtype == SZ3G_F32 ? launch_analyze_tma<float, AW32, AD32>(g, x, beta, keys, ka, st)
+                                 : launch_analyze_tma<double, AW64, AD64>(g, x, beta, keys, ka, st);
+    if (rc) return rc;
   } else {
-    CompressOut<double> co{codes, coef_codes, coef_raw, outlier_idx, (double*)outlier_val, outlier_cap,
-                           d_outlier_count, reinterpret_cast<unsigned long long*>(hist)};
-    if (tma) return use_hist ? launch_compress_tma<double, CN64, CQ64, CD64, true>(g, x, codes, codes_tma, ka, co, st)
-                         : launch_compress_tma<double, CN64, CQ64, CD64, false>(g, x, codes, codes_tma, ka, co, st);
-    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 4));
-    if (use_hist) k_compress_plain<double, true><<<blocks, 128, 0, st>>>((const double*)x, ka, co);
-    else k_compress_plain<double, false><<<blocks, 128, 0, st>>>((const double*)x, ka, co);
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
+    if (grid->dtype == SZ3G_F32) k_analyze_plain<float><<<blocks, 128, 0, st>>>((const float*)x, ka, beta, keys);
+    else k_analyze_plain<double><<<blocks, 128, 0, st>>>((const double*)x, ka, beta, keys);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
   }
-  return check_launch(1);
+  k_range_final<<<1, 1, 0, st>>>(keys);
+  return check_launch(2);
+}
+
+int sz3g_regression_quantize(const sz3g_grid* grid, const sz3g_params* params, const void* x,
+                             const double* d_minmax, const double* beta, uint16_t* codes, int32_t* coef_codes,
+                             uint64_t* outlier_idx, void* outlier_val, uint64_t outlier_cap,
+                             unsigned long long* d_outlier_count, int64_t* hist, double* d_eb_abs,
+                             int32_t* d_status, sz3g_stream_t stream) {
+  if (!beta || (reinterpret_cast<uintptr_t>(beta) & 15)) return SZ3G_EINVAL;
+  return compress_common(grid, params, x, d_minmax, beta, codes, coef_codes, nullptr, outlier_idx, outlier_val,
+                         outlier_cap, d_outlier_count, hist, d_eb_abs, d_status, stream);
 }
 
 int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax,

@@ -128,6 +128,7 @@ struct CompressOut {
   uint64_t cap;
   unsigned long long* ocount;
   unsigned long long* hist;     // nullable (int64 bins, accumulated)
+  const double* beta_in;        // two-pass mode: [NB][4] beta from the analyze pass (else nullptr)
 };
 
 // Shared-memory histogram state of one CTA.
@@ -184,12 +185,29 @@ __device__ __forceinline__ bool tile_full(const TileCoord tc, const Geo& g) {
   return (uint64_t)(tc.a + 1) * BS <= g.n0 && (uint64_t)(tc.b + 1) * BS <= g.n1 && (uint64_t)(tc.c + 1) * TK <= g.n2;
 }
 
+// Running min / max of the valid elements a lane has seen (a0 fused into the analyze pass).  NaN
+// never replaces a value (fmin/fmax); the analyze kernel detects NaN from the block sums instead.
+template <typename T>
+struct MinMax {
+  T lo, hi;
+  __device__ __forceinline__ void init() {
+    lo = sizeof(T) == 4 ? (T)__int_as_float(0x7f800000) : (T)__longlong_as_double(0x7ff0000000000000ll);
+    hi = -lo;
+  }
+  __device__ __forceinline__ void add(T v) {
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+};
+
 // O4 partial moments of the lane's three columns over rows j in [j0, j0+PJ), all six i-planes (fp64).
 // Row sums S = f0+f1+f2 and the lane-local k-weighted sum f1 + 2 f2 first; per plane i
 // P_i = sum_j S, Q_i = sum_j j S, Z_i = sum_j (f1 + 2 f2); Vz includes the lane's column offset 3h.
-template <typename T, bool IN_SMEM, int PJ>
+// MM: also fold the valid elements into `mm` (FULL: every element of the tile is valid); the sums do
+// not depend on MM, so beta is bit-identical with and without it.
+template <typename T, bool IN_SMEM, int PJ, bool MM = false, bool FULL = false>
 __device__ __forceinline__ void moments_partial(const T* __restrict__ xs, uint64_t si, uint64_t sj, int j0,
-                                                const LaneGeom& L, double V[4]) {
+                                                const LaneGeom& L, double V[4], MinMax<T>* mm = nullptr) {
   double V0 = 0.0, Vx = 0.0, Vy = 0.0, Vz = 0.0;
   double di = 0.0;
 #pragma unroll 1
@@ -201,13 +219,25 @@ __device__ __forceinline__ void moments_partial(const T* __restrict__ xs, uint64
       const int j = j0 + jj;
       const T* row = IN_SMEM ? plane + jj * TK : plane + (uint64_t)jj * sj;
       double f0, f1, f2;
+      const bool rv = (i < L.m0) && (j < L.m1);
       if (IN_SMEM) {
-        f0 = to_d<T>(row[0]); f1 = to_d<T>(row[1]); f2 = to_d<T>(row[2]);
+        const T v0 = row[0], v1 = row[1], v2 = row[2];
+        if (MM) {
+          if (FULL || (rv && L.kv0)) mm->add(v0);
+          if (FULL || (rv && L.kv1)) mm->add(v1);
+          if (FULL || (rv && L.kv2)) mm->add(v2);
+        }
+        f0 = to_d<T>(v0); f1 = to_d<T>(v1); f2 = to_d<T>(v2);
       } else {
-        const bool rv = (i < L.m0) && (j < L.m1);
-        f0 = (rv && L.kv0) ? to_d<T>(row[0]) : 0.0;
-        f1 = (rv && L.kv1) ? to_d<T>(row[1]) : 0.0;
-        f2 = (rv && L.kv2) ? to_d<T>(row[2]) : 0.0;
+        const T v0 = (rv && L.kv0) ? row[0] : T(0);
+        const T v1 = (rv && L.kv1) ? row[1] : T(0);
+        const T v2 = (rv && L.kv2) ? row[2] : T(0);
+        if (MM) {
+          if (rv && L.kv0) mm->add(v0);
+          if (rv && L.kv1) mm->add(v1);
+          if (rv && L.kv2) mm->add(v2);
+        }
+        f0 = to_d<T>(v0); f1 = to_d<T>(v1); f2 = to_d<T>(v2);
       }
       const double S = (f0 + f1) + f2;
       const double Kw = fma(2.0, f2, f1);
@@ -226,11 +256,11 @@ __device__ __forceinline__ void moments_partial(const T* __restrict__ xs, uint64
   V[3] = fma(3.0 * L.h, V0, Vz);
 }
 
-// O5 (Lemma 1; extent-1 axis -> slope 0, G2) + O6 (codes; bins eb/2, eb/12, G1; zero
-// predictor fallback) from the full block moments; returns the decoded coefficients (bit-exact).
+// O5 (Lemma 1; extent-1 axis -> slope 0, G2) from the full block moments.  The fused
+// compress kernel and the two-pass analyze kernel both call this one function, so their beta are
+// bit-identical.
 template <bool FULL = false>
-__device__ __forceinline__ void block_coefs(const double V[4], const LaneGeom& L, const Consts& K, double beta[4],
-                                            int32_t cc[4], double bh[4]) {
+__device__ __forceinline__ void block_beta(const double V[4], const LaneGeom& L, double beta[4]) {
   beta[0] = beta[1] = beta[2] = beta[3] = 0.0;
   if (FULL) {  // 6x6x6 block: Nb = 216, 6/(m+1) = 6/7, 2/(m-1) = 2/5 (same values as the table path)
     const double invNb = 1.0 / 216.0;
@@ -252,6 +282,11 @@ __device__ __forceinline__ void block_coefs(const double V[4], const LaneGeom& L
     }
     beta[0] = V[0] * invNb - ((L.m0 - 1) * 0.5 * beta[1] + (L.m1 - 1) * 0.5 * beta[2] + (L.m2 - 1) * 0.5 * beta[3]);
   }
+}
+
+// O6 (coefficient codes; bins eb/2, eb/12, G1; zero-predictor fallback): codes and the decoded
+// coefficients (bit-exact).
+__device__ __forceinline__ void block_codes(const double beta[4], const Consts& K, int32_t cc[4], double bh[4]) {
   // rint by the 1.5*2^52 add/sub (exact for |u| < 2^51; larger, Inf or NaN fail the range test)
   double r[4], sm[4];
   bool bad = false;
@@ -267,6 +302,14 @@ __device__ __forceinline__ void block_coefs(const double V[4], const LaneGeom& L
     cc[d] = bad ? 0 : __double2loint(sm[d]);
     bh[d] = bad ? 0.0 : __dmul_rn(r[d], d == 0 ? K.w0 : K.ws);
   }
+}
+
+// O5 + O6
+template <bool FULL = false>
+__device__ __forceinline__ void block_coefs(const double V[4], const LaneGeom& L, const Consts& K, double beta[4],
+                                            int32_t cc[4], double bh[4]) {
+  block_beta<FULL>(V, L, beta);
+  block_codes(beta, K, cc, bh);
 }
 
 template <typename T>
@@ -499,8 +542,9 @@ __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si,
   }
 }
 
-// One warp compresses a whole tile (plain kernel).
-template <typename T, bool IN_SMEM, bool HIST, bool FULL>
+// One warp compresses a whole tile (plain kernel).  BETA: the block coefficients come from the
+// analyze pass (o.beta_in) instead of the moments.
+template <typename T, bool IN_SMEM, bool HIST, bool FULL, bool BETA = false>
 __device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj,
                                               uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
                                               const TileCoord tc, const Geo& g, const Consts& K,
@@ -508,15 +552,46 @@ __device__ __forceinline__ void compress_tile(const T* __restrict__ xs, uint64_t
   const LaneGeom L = lane_geom<FULL>(tc, g);
   double V[4], beta[4], bh[4];
   int32_t cc[4];
-  moments_partial<T, IN_SMEM, BS>(xs, si, sj, 0, L, V);
+  if (BETA) {
+    beta[0] = beta[1] = beta[2] = beta[3] = 0.0;
+    if (L.m2 > 0) {
+      const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
+      const double2 b01 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid);
+      const double2 b23 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid + 1);
+      beta[0] = b01.x; beta[1] = b01.y; beta[2] = b23.x; beta[3] = b23.y;
+    }
+    block_codes(beta, K, cc, bh);
+  } else {
+    moments_partial<T, IN_SMEM, BS>(xs, si, sj, 0, L, V);
 #pragma unroll
-  for (int d = 0; d < 4; d++) V[d] += __shfl_xor_sync(0xffffffffu, V[d], 1);
-  block_coefs<FULL>(V, L, K, beta, cc, bh);
+    for (int d = 0; d < 4; d++) V[d] += __shfl_xor_sync(0xffffffffu, V[d], 1);
+    block_coefs<FULL>(V, L, K, beta, cc, bh);
+  }
   write_coefs(o, tc, g, L, cc, beta);
   const Fast32 F = fast32_consts(bh, K);
   const bool has_out =
       quantize_rows<T, IN_SMEM, HIST, FULL, BS, false>(xs, si, sj, cs, ci, cj, 0, L, bh, F, K, R, hs, o.hist);
   rare_path<T, HIST, BS>(xs, si, sj, cs, ci, cj, 0, 0, L, has_out, tc, g, o, hs);
+}
+
+// One warp analyzes a whole tile (a0 + a2 + a3): moments and min/max of the valid elements, beta of
+// its 16 blocks (same functions, same order as the fused compress path: bit-identical beta).
+// Returns whether a block sum is NaN (a NaN element, or infinities of both signs).
+template <typename T, bool IN_SMEM, bool FULL>
+__device__ __forceinline__ bool analyze_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj, const TileCoord tc,
+                                             const Geo& g, double* __restrict__ beta_out, MinMax<T>& mm) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  double V[4], beta[4];
+  moments_partial<T, IN_SMEM, BS, true, FULL>(xs, si, sj, 0, L, V, &mm);
+#pragma unroll
+  for (int d = 0; d < 4; d++) V[d] += __shfl_xor_sync(0xffffffffu, V[d], 1);
+  block_beta<FULL>(V, L, beta);
+  if (L.m2 > 0 && L.h == 0) {
+    const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
+    reinterpret_cast<double2*>(beta_out)[2 * bid] = make_double2(beta[0], beta[1]);
+    reinterpret_cast<double2*>(beta_out)[2 * bid + 1] = make_double2(beta[2], beta[3]);
+  }
+  return L.m2 > 0 && V[0] != V[0];
 }
 
 // ------------------------------------------------------------------------------------------

@@ -63,6 +63,8 @@ def load(allow_build: bool = False):
     lib.sz3g_value_range.argtypes = [GP, P, P, P]
     lib.sz3g_regression_compress.argtypes = [GP, PP, P, P, P, P, P, P, P, U64, P, P, P, P, P]
     lib.sz3g_regression_decompress.argtypes = [GP, PP, P, P, P, P, P, U64, P, P, P]
+    lib.sz3g_regression_analyze.argtypes = [GP, P, P, P, P]
+    lib.sz3g_regression_quantize.argtypes = [GP, PP, P, P, P, P, P, P, P, U64, P, P, P, P, P]
     lib.sz3g_histogram.argtypes = [P, U64, U32, P, P]
     lib.sz3g_num_blocks.argtypes = [GP, U32]
     lib.sz3g_num_blocks.restype = U64
@@ -80,6 +82,7 @@ def load(allow_build: bool = False):
 
 
 EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regression_decompress", "sz3g_histogram",
+                    "sz3g_regression_analyze", "sz3g_regression_quantize",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -216,6 +219,12 @@ class CompressBuffers:
         self.eb_abs = torch.zeros(1, dtype=torch.float64, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.minmax = torch.zeros(2, dtype=torch.float64, device=device)
+        self.beta = None   # [NB, 4] float64, allocated by the two-pass path (regression_analyze)
+
+    def beta_buffer(self) -> torch.Tensor:
+        if self.beta is None:
+            self.beta = torch.empty_like(self.coef_codes, dtype=torch.float64)
+        return self.beta
 
     def reset(self):
         """Zero the accumulating outputs (outlier counter, histogram, status)."""
@@ -259,6 +268,56 @@ def regression_compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius
                       bufs.eb_abs, bufs.status)
 
 
+def regression_analyze(x: torch.Tensor, minmax: torch.Tensor | None = None, beta: torch.Tensor | None = None,
+                       stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """sz3g_regression_analyze: one read of x -> (device double[2] {min, max}, float64 [NB, 4] beta)."""
+    _require_cuda(x, minmax, beta)
+    if minmax is None:
+        minmax = torch.empty(2, dtype=torch.float64, device=x.device)
+    if beta is None:
+        beta = torch.empty((num_blocks(x.shape), 4), dtype=torch.float64, device=x.device)
+    g = make_grid(x.shape, x.dtype)
+    _check(load().sz3g_regression_analyze(ctypes.byref(g), _ptr(x), _ptr(minmax), _ptr(beta), _stream(stream)),
+           "sz3g_regression_analyze")
+    return minmax, beta
+
+
+def regression_quantize(x: torch.Tensor, eb: float, eb_mode: str, radius: int, d_minmax: torch.Tensor | None,
+                        beta: torch.Tensor, bufs: CompressBuffers | None = None, outlier_cap: int | None = None,
+                        hist: bool = True, dim0_offset: int = 0, flags: int = 0, stream=None,
+                        reset: bool = True) -> Compressed:
+    """sz3g_regression_quantize: compression from the analyze pass's beta (asynchronous, like
+    regression_compress; outputs bit-identical to it).  ``Compressed.coef_raw`` is ``beta``."""
+    _require_cuda(x, d_minmax, beta)
+    if bufs is None:
+        bufs = CompressBuffers(x.shape, x.dtype, radius, outlier_cap, x.device, False, hist)
+    elif reset:
+        bufs.reset()
+    if bufs.radius != radius:
+        raise SZ3GError("buffer radius mismatch")
+    g = make_grid(x.shape, x.dtype, dim0_offset)
+    p = make_params(eb, eb_mode, radius, flags)
+    rc = load().sz3g_regression_quantize(
+        ctypes.byref(g), ctypes.byref(p), _ptr(x), _ptr(d_minmax), _ptr(beta), _ptr(bufs.codes),
+        _ptr(bufs.coef_codes), _ptr(bufs.outlier_idx), _ptr(bufs.outlier_val), bufs.outlier_idx.numel(),
+        _ptr(bufs.outlier_count), _ptr(bufs.hist if hist else None), _ptr(bufs.eb_abs), _ptr(bufs.status),
+        _stream(stream))
+    _check(rc, "sz3g_regression_quantize")
+    return Compressed(tuple(x.shape), x.dtype, radius, dim0_offset, bufs.codes, bufs.coef_codes, beta,
+                      bufs.outlier_idx, bufs.outlier_val, bufs.outlier_count, bufs.hist if hist else None,
+                      bufs.eb_abs, bufs.status)
+
+
+def compress_two_pass(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768,
+                      bufs: CompressBuffers | None = None, outlier_cap: int | None = None, hist: bool = True,
+                      flags: int = 0, stream=None) -> Compressed:
+    """analyze (range + beta, one read) -> quantize (one read): the REL-mode path (asynchronous)."""
+    if bufs is None:
+        bufs = CompressBuffers(x.shape, x.dtype, radius, outlier_cap, x.device, False, hist)
+    minmax, beta = regression_analyze(x, bufs.minmax, bufs.beta_buffer(), stream)
+    return regression_quantize(x, eb, eb_mode, radius, minmax, beta, bufs, hist=hist, flags=flags, stream=stream)
+
+
 def regression_decompress(codes: torch.Tensor, coef_codes: torch.Tensor, outlier_idx: torch.Tensor,
                           outlier_val: torch.Tensor, n_outliers: int, eb: float, radius: int = 32768,
                           dtype: torch.dtype = torch.float32, dim0_offset: int = 0, out: torch.Tensor | None = None,
@@ -294,9 +353,19 @@ def histogram(codes: torch.Tensor, radius: int = 32768, hist: torch.Tensor | Non
 
 
 # ------------------------------------------------------------------------------------------- one-call API
-def compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768, **kw) -> Compressed:
-    """Compress a CUDA field and check the device status (synchronises)."""
-    res = regression_compress(x, eb, eb_mode, radius, **kw)
+def compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768, two_pass: bool | None = None,
+             **kw) -> Compressed:
+    """Compress a CUDA field and check the device status (synchronises).  REL mode without a given
+    range takes the two-pass path (analyze -> quantize, each one read of x); ABS mode or a given
+    ``d_minmax`` the fused single-pass kernel.  Both give bit-identical outputs."""
+    if two_pass is None:
+        two_pass = eb_mode == "rel" and kw.get("d_minmax") is None and not kw.get("dim0_offset")
+    if two_pass:
+        kw.pop("coef_raw", None)
+        kw.pop("d_minmax", None)
+        res = compress_two_pass(x, eb, eb_mode, radius, **kw)
+    else:
+        res = regression_compress(x, eb, eb_mode, radius, **kw)
     res.finalize()
     return res
 

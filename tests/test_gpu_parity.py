@@ -23,10 +23,16 @@ def sz():
     return sz3g
 
 
-def run_gpu(x: torch.Tensor, eb, mode, R, flags=0, dim0_offset=0, d_minmax=None, cap=None):
+def run_gpu(x: torch.Tensor, eb, mode, R, flags=0, dim0_offset=0, d_minmax=None, cap=None, two_pass=False):
     s = sz()
-    res = s.regression_compress(x, eb, mode, R, d_minmax=d_minmax, coef_raw=True, flags=flags,
-                                dim0_offset=dim0_offset, outlier_cap=cap if cap is not None else x.numel())
+    cap = cap if cap is not None else x.numel()
+    if two_pass:   # analyze (range + beta) -> quantize; REL uses the analyze pass's own range
+        minmax, beta = s.regression_analyze(x)
+        res = s.regression_quantize(x, eb, mode, R, d_minmax if d_minmax is not None else minmax, beta,
+                                    outlier_cap=cap, flags=flags, dim0_offset=dim0_offset)
+    else:
+        res = s.regression_compress(x, eb, mode, R, d_minmax=d_minmax, coef_raw=True, flags=flags,
+                                    dim0_offset=dim0_offset, outlier_cap=cap)
     res.finalize()
     xo = s.decompress(res, flags=flags)
     torch.cuda.synchronize()
@@ -39,9 +45,9 @@ def run_gpu(x: torch.Tensor, eb, mode, R, flags=0, dim0_offset=0, d_minmax=None,
     return gpu, xo.cpu().numpy(), res
 
 
-def check(xh: np.ndarray, eb, mode, R, flags=0, rng_override=None):
+def check(xh: np.ndarray, eb, mode, R, flags=0, rng_override=None, two_pass=False):
     x = torch.from_numpy(np.ascontiguousarray(xh)).cuda()
-    gpu, xdec, res = run_gpu(x, eb, mode, R, flags)
+    gpu, xdec, res = run_gpu(x, eb, mode, R, flags, two_pass=two_pass)
     orc = oracle.compress(xh, eb, mode, radius=R, value_range_override=rng_override)
     dec_of_gpu = oracle.decompress(dims=orc.dims, dtype=xh.dtype, radius=R, eb_abs=orc.eb_abs, codes=gpu["codes"],
                                    coef_codes=gpu["coef_codes"], outlier_idx=gpu["outlier_idx"],
@@ -81,6 +87,56 @@ def test_fuzz_parity(t, flags):
     if mode == "rel" and np.ptp(f) == 0:
         pytest.skip("constant field")
     check(f, eb, mode, R, flags)
+
+
+# ----------------------------------------------------------------------------- two-pass (analyze -> quantize)
+def assert_same_outputs(a: dict, b: dict):
+    """Bit-identical compression outputs (outliers compared as sets keyed by index)."""
+    for k in ("codes", "coef_codes", "hist"):
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(a["coef_raw"].view(np.uint64), b["coef_raw"].view(np.uint64)), "beta"
+    assert a["eb_abs"] == b["eb_abs"]
+    oa, ob = np.argsort(a["outlier_idx"]), np.argsort(b["outlier_idx"])
+    assert np.array_equal(a["outlier_idx"][oa], b["outlier_idx"][ob])
+    assert np.array_equal(a["outlier_val"][oa].view(np.uint8), b["outlier_val"][ob].view(np.uint8))
+
+
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+@pytest.mark.parametrize("t", list(range(0, 40, 3)))
+def test_two_pass_matches_fused(t, flags):
+    """analyze + quantize reproduce the fused kernel bit for bit (beta, codes, histogram, outliers),
+    and the analyze pass's range equals sz3g_value_range."""
+    f, eb, mode, R = fuzz_case(t)
+    if mode == "rel" and np.ptp(f) == 0:
+        pytest.skip("constant field")
+    x = torch.from_numpy(np.ascontiguousarray(f)).cuda()
+    fused, xo_f, _ = run_gpu(x, eb, mode, R, flags)
+    two, xo_t, _ = run_gpu(x, eb, mode, R, flags, two_pass=True)
+    assert_same_outputs(fused, two)
+    assert np.array_equal(xo_f.view(np.uint8), xo_t.view(np.uint8))
+    mm, _ = sz().regression_analyze(x)
+    assert torch.equal(mm, sz().value_range(x))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_two_pass_config_parity(name):
+    """The two-pass path against the oracle at full size (the bench's REL path)."""
+    from synth import config_by_name, make_field
+    cfg = config_by_name(name)
+    x = make_field(cfg, device="cuda")
+    rep = check(x.cpu().numpy(), cfg.eb, cfg.eb_mode, cfg.radius, two_pass=True)
+    assert rep["exempt_blocks"] <= max(4, oracle.num_blocks(tuple(x.shape)) // 10000)
+
+
+def test_two_pass_nonfinite_range():
+    s = sz()
+    f = np.linspace(-3, 3, 13 * 14 * 96, dtype=np.float32).reshape(13, 14, 96)
+    f[1, 2, 3] = np.nan
+    x = torch.from_numpy(f).cuda()
+    mm, _ = s.regression_analyze(x)
+    assert math.isnan(float(mm[1]))
+    with pytest.raises(Exception):
+        s.compress(x, 1e-3, "rel", two_pass=True)
 
 
 # ----------------------------------------------------------------------------- configs at full size

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--reps", type=int, default=6)
     ap.add_argument("--setting", default="")
     ap.add_argument("--build", action="store_true")
+    ap.add_argument("--path", default="fused", choices=["fused", "two-pass"])
     ap.add_argument("variants", nargs="+")
     a = ap.parse_args()
     vs = [v.split("=", 1) for v in a.variants]
@@ -56,7 +57,7 @@ def main():
         for n, path in vs:
             env = dict(os.environ, SZ3G_LIB=os.path.join(ROOT, path) if not os.path.isabs(path) else path)
             out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tune.py"), "--config", a.config,
-                                  "--reps", str(a.reps), "--rounds", "1", a.setting or "CHUNK_C=2"],
+                                  "--reps", str(a.reps), "--rounds", "1", "--path", a.path, a.setting or "CHUNK_C=2"],
                                  env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
             if not line:

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--rounds", type=int, default=2, help="passes over the settings (interleaved)")
+    ap.add_argument("--path", default="fused", choices=["fused", "two-pass"])
     ap.add_argument("settings", nargs="+")
     args = ap.parse_args()
     import torch
@@ -36,9 +37,17 @@ def main():
     sz3g.value_range(x, bufs.minmax)
     stream = torch.cuda.current_stream()
 
+    beta = None
+    if args.path == "two-pass":
+        _, beta = sz3g.regression_analyze(x, bufs.minmax, bufs.beta_buffer())
+
     def comp():
         bufs.reset()
-        sz3g.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=bufs.minmax, bufs=bufs, reset=False)
+        if beta is not None:
+            sz3g.regression_quantize(x, cfg.eb, cfg.eb_mode, cfg.radius, bufs.minmax, beta, bufs=bufs, reset=False)
+        else:
+            sz3g.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=bufs.minmax, bufs=bufs,
+                                     reset=False)
 
     def dec():
         sz3g.regression_decompress(bufs.codes, bufs.coef_codes, bufs.outlier_idx, bufs.outlier_val, cap, cfg.eb,
