@@ -65,6 +65,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+#ifndef SZ3G_IDLE_WAIT
+#define SZ3G_IDLE_WAIT 1   // 0: nanosleep(64) polling, 1: hardware-suspended try_wait, >= 2: nanosleep(value)
+#endif
+// wait of a warp that is idle most of the time (its work per stage is small)
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+  if (SZ3G_IDLE_WAIT == 1) {
+    while (!mbar_try_wait_sleep(bar, parity)) {
+    }
+  } else {
+    if (mbar_try_wait(bar, parity)) return;
+    while (!mbar_try_wait(bar, parity)) __nanosleep(SZ3G_IDLE_WAIT == 0 ? 64 : SZ3G_IDLE_WAIT);
+  }
+}
+
 // producer-side wait with back-off: a spinning producer lane steals issue slots from the consumer
 // warps that share its SM sub-partition
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {

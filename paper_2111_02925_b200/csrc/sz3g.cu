@@ -565,7 +565,8 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW>::WAR
         if (t >= g.ntiles) break;
         const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
         const TileCoord tc = decode_tile(t, g);
-        ptx::mbar_wait(&full[s], ph);
+        if (BETA) ptx::mbar_wait_idle(&full[s], ph);   // a mostly idle warp: do not steal issue slots
+        else ptx::mbar_wait(&full[s], ph);
         const T* xs = stage_x(s);
         if (BETA) {
           const double* bst = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(xs) + L_::tile_bytes);
