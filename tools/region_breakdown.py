@@ -5,7 +5,8 @@ rows = list(csv.reader(open(path)))
 hi = [i for i, r in enumerate(rows) if r and r[0] == 'Address'][0]
 name = rows[hi - 1][1] if hi > 0 else ''
 h = rows[hi]
-data = [r for r in rows[hi + 1:] if len(r) == len(h)]
+end = next((i for i in range(hi + 1, len(rows)) if rows[i] and rows[i][0] in ('Kernel Name', 'Address')), len(rows))
+data = [r for r in rows[hi + 1:end] if len(r) == len(h)]   # first kernel block only (ncu may print it twice)
 isrc, iex, iss = h.index('Source'), h.index('Instructions Executed'), h.index('Warp Stall Sampling (All Samples)')
 def n(x):
     try: return int(x)
