@@ -18,6 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sz3_oracle.cpp")
+_SRCS = [_SRC, os.path.join(_HERE, "huffman_oracle.cpp")]
 _LIB_PATH = os.path.join(_HERE, "liboracle_sz3.so")
 _lock = threading.Lock()
 _lib = None
@@ -28,10 +29,10 @@ BLOCK = 6
 
 def build(force: bool = False) -> str:
     """Compile the oracle with g++ (-O2, no FP contraction)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB_PATH) or any(os.path.getmtime(_LIB_PATH) < os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-               "-o", tmp, _SRC]
+               "-o", tmp, *_SRCS]
         subprocess.run(cmd, check=True)
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
@@ -63,6 +64,13 @@ def _load():
             lib.orc_quantize_element.argtypes = [I32, D, D, D, U32, P, P]
             lib.orc_num_blocks.argtypes = [P, U32]
             lib.orc_num_blocks.restype = U64
+            lib.orc_huffman_lengths.argtypes = [P, U32, U32, P]
+            lib.orc_huffman_canonical.argtypes = [P, U32, P]
+            lib.orc_huffman_canonical.restype = None
+            lib.orc_huffman_chunk_offsets.argtypes = [P, U64, U32, P, P]
+            lib.orc_huffman_chunk_offsets.restype = None
+            lib.orc_huffman_encode.argtypes = [P, U64, U32, P, P, P, P]
+            lib.orc_huffman_decode.argtypes = [P, P, U64, U32, P, P, U32, P]
             _lib = lib
     return _lib
 
@@ -195,3 +203,56 @@ def quantize_element(x: float, p: float, eb_abs: float, radius: int = 32768, dty
     kind = _load().orc_quantize_element(_dtype_id(dtype), float(x), float(p), float(eb_abs), radius,
                                         ctypes.byref(code), ctypes.byref(xp))
     return int(code.value), float(xp.value), int(kind)
+
+
+# ------------------------------------------------------------------------------------------- Huffman
+# The encoder stage after the quantiser (DEFINITION.md H1-H5; huffman_oracle.cpp).
+HUFF_MAX_LEN = 24    # G20: length limit of the codebook
+HUFF_CHUNK = 2048    # G21: codes per independently decodable chunk
+
+
+def huffman_lengths(hist: np.ndarray, max_len: int = HUFF_MAX_LEN) -> np.ndarray:
+    """H2: optimal code lengths under max_len by package-merge (uint8 per symbol, 0 = absent)."""
+    h = np.ascontiguousarray(hist, dtype=np.int64)
+    lens = np.zeros(h.size, np.uint8)
+    rc = _load().orc_huffman_lengths(_ptr(h), h.size, max_len, _ptr(lens))
+    if rc != 0:
+        raise ValueError(f"orc_huffman_lengths failed ({rc})")
+    return lens
+
+
+def huffman_canonical(lens: np.ndarray) -> np.ndarray:
+    """H3: canonical codewords (uint32, right-aligned) for the given lengths."""
+    L = np.ascontiguousarray(lens, dtype=np.uint8)
+    codes = np.zeros(L.size, np.uint32)
+    _load().orc_huffman_canonical(_ptr(L), L.size, _ptr(codes))
+    return codes
+
+
+def huffman_encode(q: np.ndarray, lens: np.ndarray, codes: np.ndarray, chunk: int = HUFF_CHUNK):
+    """H4: (chunk word offsets uint64[nchunks + 1], payload uint32[offs[-1]])."""
+    q = np.ascontiguousarray(q, dtype=np.uint16).reshape(-1)
+    lens = np.ascontiguousarray(lens, dtype=np.uint8)
+    codes = np.ascontiguousarray(codes, dtype=np.uint32)
+    nch = -(-q.size // chunk)
+    offs = np.zeros(nch + 1, np.uint64)
+    _load().orc_huffman_chunk_offsets(_ptr(q), q.size, chunk, _ptr(lens), _ptr(offs))
+    words = np.zeros(int(offs[-1]), np.uint32)
+    rc = _load().orc_huffman_encode(_ptr(q), q.size, chunk, _ptr(lens), _ptr(codes), _ptr(offs), _ptr(words))
+    if rc != 0:
+        raise ValueError("a code has no codeword")
+    return offs, words
+
+
+def huffman_decode(words: np.ndarray, offs: np.ndarray, n: int, lens: np.ndarray, codes: np.ndarray,
+                   chunk: int = HUFF_CHUNK) -> np.ndarray:
+    """H5: decode n codes."""
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    offs = np.ascontiguousarray(offs, dtype=np.uint64)
+    lens = np.ascontiguousarray(lens, dtype=np.uint8)
+    codes = np.ascontiguousarray(codes, dtype=np.uint32)
+    q = np.zeros(n, np.uint16)
+    rc = _load().orc_huffman_decode(_ptr(words), _ptr(offs), n, chunk, _ptr(lens), _ptr(codes), lens.size, _ptr(q))
+    if rc != 0:
+        raise ValueError(f"corrupt stream ({rc})")
+    return q
