@@ -46,6 +46,10 @@ typedef struct CUstream_st* sz3g_stream_t; /* == cudaStream_t */
 /* ---- device status bits (written with atomicOr into *d_status; caller zeroes it first) */
 #define SZ3G_STATUS_OUTLIER_OVERFLOW 0x1u /* *d_outlier_count > outlier_cap: retry, larger cap */
 #define SZ3G_STATUS_BAD_RANGE        0x2u /* eb_abs not finite or <= 0 (REL: max-min <= 0/NaN) */
+#define SZ3G_STATUS_BAD_HUFFMAN      0x4u /* codebook: no active symbol, a negative / >= 2^47 count,
+                                             or 2^max_len < active symbols; encode: a code without
+                                             a codeword; decode: a corrupt stream               */
+#define SZ3G_STATUS_PAYLOAD_OVERFLOW 0x8u /* encode: the stream needs more than payload_cap words */
 
 typedef enum { SZ3G_F32 = 0, SZ3G_F64 = 1 } sz3g_dtype;
 /* ABS: eb is absolute.  REL: eb_abs = eb * (max - min) over the (global) field. */
@@ -161,6 +165,47 @@ int sz3g_uses_tma(const sz3g_grid* grid, int decompress);
 
 /* total device kernels this process has launched through the library (for launch counting) */
 uint64_t sz3g_launch_count(void);
+
+/* ---- Encoder stage (NEXT-1): Huffman coding of the quantisation codes.  P:156 "The data size will be
+ * significantly reduced after conducting Huffman encoding on the quantization codes"; P:418 the
+ * Huffman encoder "constructs a Huffman tree based on the frequency of input data using a greedy
+ * algorithm, generates codebook according to the tree, and then compress the data using the
+ * codebook"; encode / decode / save / load, App. A P:948-957.  Definition:
+ * oracle/DEFINITION.md H1-H5 (readings G19-G23 in DESIGN.md).
+ *
+ * sz3g_huffman_codebook -- from the (merged) histogram of sz3g_regression_compress / _quantize:
+ *   hist       in   nsym int64 counts (nsym = 2R, <= 65536; counts in [0, 2^47)).
+ *   max_len    in   maximum code length, 1..24 (the stream format uses 24).
+ *   lengths    out  nsym uint8: optimal code lengths under max_len (package-merge, tie rule H2);
+ *                   0 for symbols with count 0; one active symbol gets length 1.
+ *   codewords  out  nsym uint32: canonical codewords (H3), right-aligned.
+ *   dtable     out  sz3g_huffman_dtable_bytes(nsym) bytes, 16-byte aligned: the decoder's tables.
+ *   scratch    in   sz3g_huffman_scratch_bytes(nsym, max_len) bytes of device memory.
+ *   d_status   in/out SZ3G_STATUS_BAD_HUFFMAN on an empty histogram, a bad count or 2^max_len < n.
+ *   One launch (a single CTA).  Bit-identical to the oracle's lengths and codewords.
+ *
+ * sz3g_huffman_encode -- n codes in chunks of `chunk` (1..2048; the format uses 2048):
+ *   chunk_offsets out nchunks + 1 uint64: word offset of each chunk, then the total word count.
+ *   payload       out the chunks, each packed MSB-first into whole 32-bit words (H4); at most
+ *                     payload_cap_words words are written (SZ3G_STATUS_PAYLOAD_OVERFLOW beyond).
+ *   scratch       in  sz3g_huffman_encode_scratch_bytes(n, chunk) bytes of device memory.
+ *   5 launches (chunk sizes, 3-phase scan, pack).  Codes without a codeword set BAD_HUFFMAN.
+ *
+ * sz3g_huffman_decode -- the inverse: n codes from payload / chunk_offsets with the dtable of the
+ *   same codebook (codes 16-byte aligned); a corrupt stream sets BAD_HUFFMAN.  1 launch.        */
+uint64_t sz3g_huffman_scratch_bytes(uint32_t nsym, uint32_t max_len);
+uint64_t sz3g_huffman_dtable_bytes(uint32_t nsym);
+uint64_t sz3g_huffman_encode_scratch_bytes(uint64_t n, uint32_t chunk);
+int sz3g_huffman_codebook(const int64_t* hist, uint32_t nsym, uint32_t max_len, uint8_t* lengths,
+                          uint32_t* codewords, void* dtable, void* scratch, int32_t* d_status,
+                          sz3g_stream_t stream);
+int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const uint8_t* lengths,
+                        const uint32_t* codewords, uint64_t* chunk_offsets, uint32_t* payload,
+                        uint64_t payload_cap_words, void* scratch, int32_t* d_status,
+                        sz3g_stream_t stream);
+int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, uint64_t n,
+                        uint32_t chunk, const void* dtable, uint32_t max_len, uint16_t* codes,
+                        int32_t* d_status, sz3g_stream_t stream);
 
 /* Performance tuning only (no call changes a result): set knob `key` ("CHUNK_C", "CHUNK_D", "CCFG",
  * "PF"; defaults are the measured best, environment SZ3G_<KEY> overrides them) for

@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "sz3g.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "tile.cuh"), os.path.join(HERE, "csrc", "ptx.cuh"),
+SRCS = [SRC, os.path.join(HERE, "csrc", "huffman.cu")]
+DEPS = [*SRCS, os.path.join(HERE, "csrc", "tile.cuh"), os.path.join(HERE, "csrc", "ptx.cuh"),
         os.path.join(ROOT, "include", "sz3g.h")]
 LIB = os.path.join(HERE, "lib", "libsz3g.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -23,14 +24,15 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, src: str = SRC, out: str = LIB, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, src=None, out: str = LIB, defines=()) -> str:
     """nvcc `src` -> `out` (defaults: the in-tree library; another src/out builds an A/B variant)."""
     if not force and out == LIB and not needs_build():
         return LIB
     os.makedirs(os.path.dirname(out), exist_ok=True)
     tmp = out + f".tmp{os.getpid()}"
+    srcs = SRCS if src is None else ([src] if isinstance(src, str) else list(src))
     cmd = [NVCC, *FLAGS, *defines, *(["-Xptxas", "-v"] if verbose else []), "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, src]
+           "-o", tmp, *srcs]
     subprocess.run(cmd, check=True)
     os.replace(tmp, out)
     return out

@@ -28,6 +28,8 @@
 
 using namespace sz3g;
 
+uint64_t sz3g_huffman_launch_count_internal();   // huffman.cu
+
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
@@ -1245,7 +1247,7 @@ int sz3g_uses_tma(const sz3g_grid* grid, int decompress) {
   return decompress ? (xin && cod) : xin;
 }
 
-uint64_t sz3g_launch_count(void) { return g_launches.load(); }
+uint64_t sz3g_launch_count(void) { return g_launches.load() + sz3g_huffman_launch_count_internal(); }
 
 int sz3g_set_tuning(const char* key, int64_t value) {
   if (!key) return SZ3G_EINVAL;

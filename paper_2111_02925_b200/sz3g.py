@@ -21,6 +21,8 @@ SZ3G_F32, SZ3G_F64 = 0, 1
 SZ3G_EB_ABS, SZ3G_EB_REL_RANGE = 0, 1
 FLAG_FORCE_GENERIC = 0x1
 STATUS_OUTLIER_OVERFLOW, STATUS_BAD_RANGE = 0x1, 0x2
+STATUS_BAD_HUFFMAN = 0x4
+STATUS_PAYLOAD_OVERFLOW = 0x8
 BLOCK = 6
 _ERR = {0: "ok", -1: "EINVAL", -2: "EUNSUPPORTED", -3: "ERANGE", -4: "ECUDA"}
 
@@ -70,6 +72,16 @@ def load(allow_build: bool = False):
     lib.sz3g_num_blocks.restype = U64
     lib.sz3g_uses_tma.argtypes = [GP, I32]
     lib.sz3g_launch_count.restype = U64
+    if hasattr(lib, "sz3g_huffman_codebook"):   # absent only in older A/B builds
+        lib.sz3g_huffman_scratch_bytes.argtypes = [U32, U32]
+        lib.sz3g_huffman_scratch_bytes.restype = U64
+        lib.sz3g_huffman_dtable_bytes.argtypes = [U32]
+        lib.sz3g_huffman_dtable_bytes.restype = U64
+        lib.sz3g_huffman_encode_scratch_bytes.argtypes = [U64, U32]
+        lib.sz3g_huffman_encode_scratch_bytes.restype = U64
+        lib.sz3g_huffman_codebook.argtypes = [P, U32, U32, P, P, P, P, P, P]
+        lib.sz3g_huffman_encode.argtypes = [P, U64, U32, P, P, P, P, U64, P, P, P]
+        lib.sz3g_huffman_decode.argtypes = [P, P, U64, U32, P, U32, P, P, P]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
@@ -82,7 +94,9 @@ def load(allow_build: bool = False):
 
 
 EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regression_decompress", "sz3g_histogram",
-                    "sz3g_regression_analyze", "sz3g_regression_quantize",
+                    "sz3g_regression_analyze", "sz3g_regression_quantize", "sz3g_huffman_scratch_bytes",
+                    "sz3g_huffman_dtable_bytes", "sz3g_huffman_encode_scratch_bytes", "sz3g_huffman_codebook",
+                    "sz3g_huffman_encode", "sz3g_huffman_decode",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -375,3 +389,100 @@ def decompress(res: Compressed, out: torch.Tensor | None = None, flags: int = 0)
         res.finalize()
     return regression_decompress(res.codes, res.coef_codes, res.outlier_idx, res.outlier_val, res.n_outliers,
                                  res.eb_abs, res.radius, res.dtype, res.dim0_offset, out, flags)
+
+
+# ------------------------------------------------------------------------------------------- Huffman
+HUFF_MAX_LEN = 24     # DEFINITION.md H2 / G20
+HUFF_CHUNK = 2048     # H4 / G21
+
+
+@dataclass
+class HuffmanTable:
+    lengths: torch.Tensor     # uint8 [nsym]
+    codewords: torch.Tensor   # int32 (uint32 bits) [nsym]
+    dtable: torch.Tensor      # uint8 [sz3g_huffman_dtable_bytes]
+    max_len: int
+    status: torch.Tensor      # int32 [1]
+
+    def check(self) -> "HuffmanTable":
+        if int(self.status.item()) & STATUS_BAD_HUFFMAN:
+            raise SZ3GError("Huffman codebook: empty histogram, bad count, or too many symbols for max_len")
+        return self
+
+
+def huffman_codebook(hist: torch.Tensor, max_len: int = HUFF_MAX_LEN, stream=None) -> HuffmanTable:
+    """sz3g_huffman_codebook (one CTA on the GPU) from a device int64 histogram (asynchronous)."""
+    _require_cuda(hist)
+    lib = load()
+    nsym = hist.numel()
+    dev = hist.device
+    lens = torch.empty(nsym, dtype=torch.uint8, device=dev)
+    cws = torch.empty(nsym, dtype=torch.int32, device=dev)
+    dtab = torch.empty(int(lib.sz3g_huffman_dtable_bytes(nsym)), dtype=torch.uint8, device=dev)
+    scratch = torch.empty(int(lib.sz3g_huffman_scratch_bytes(nsym, max_len)), dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _check(lib.sz3g_huffman_codebook(_ptr(hist), nsym, max_len, _ptr(lens), _ptr(cws), _ptr(dtab), _ptr(scratch),
+                                     _ptr(status), _stream(stream)), "sz3g_huffman_codebook")
+    t = HuffmanTable(lens, cws, dtab, max_len, status)
+    t._scratch = scratch   # keep alive until the stream has run
+    return t
+
+
+@dataclass
+class HuffmanStream:
+    n: int
+    chunk: int
+    offsets: torch.Tensor     # int64 [nchunks + 1] word offsets
+    payload: torch.Tensor     # int32 (uint32 bits) [capacity]
+    status: torch.Tensor
+
+    def words(self) -> int:
+        return int(self.offsets[-1].item())
+
+    def check(self) -> "HuffmanStream":
+        st = int(self.status.item())
+        if st & STATUS_PAYLOAD_OVERFLOW:
+            raise SZ3GError("Huffman payload capacity exceeded")
+        if st & STATUS_BAD_HUFFMAN:
+            raise SZ3GError("a code has no codeword in the Huffman table")
+        return self
+
+
+def huffman_encode(codes: torch.Tensor, table: HuffmanTable, chunk: int = HUFF_CHUNK,
+                   payload: torch.Tensor | None = None, offsets: torch.Tensor | None = None,
+                   scratch: torch.Tensor | None = None, stream=None) -> HuffmanStream:
+    """sz3g_huffman_encode of a uint16 code array (asynchronous).  Without ``payload`` the capacity is
+    the worst case (max_len bits per code + one word per chunk)."""
+    _require_cuda(codes, payload, offsets, scratch)
+    lib = load()
+    n = codes.numel()
+    nch = -(-n // chunk)
+    dev = codes.device
+    if offsets is None:
+        offsets = torch.empty(nch + 1, dtype=torch.int64, device=dev)
+    if payload is None:
+        payload = torch.empty(max(1, -(-n * table.max_len // 32) + nch), dtype=torch.int32, device=dev)
+    if scratch is None:
+        scratch = torch.empty(int(lib.sz3g_huffman_encode_scratch_bytes(n, chunk)), dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _check(lib.sz3g_huffman_encode(_ptr(codes), n, chunk, _ptr(table.lengths), _ptr(table.codewords), _ptr(offsets),
+                                   _ptr(payload), payload.numel(), _ptr(scratch), _ptr(status), _stream(stream)),
+           "sz3g_huffman_encode")
+    hs = HuffmanStream(n, chunk, offsets, payload, status)
+    hs._scratch = scratch
+    return hs
+
+
+def huffman_decode(hs: HuffmanStream, table: HuffmanTable, out: torch.Tensor | None = None,
+                   status: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sz3g_huffman_decode -> uint16 codes (asynchronous; a corrupt stream sets STATUS_BAD_HUFFMAN)."""
+    _require_cuda(out, status)
+    lib = load()
+    dev = hs.payload.device
+    if out is None:
+        out = torch.empty(hs.n, dtype=torch.uint16, device=dev)
+    if status is None:
+        status = hs.status
+    _check(lib.sz3g_huffman_decode(_ptr(hs.payload), _ptr(hs.offsets), hs.n, hs.chunk, _ptr(table.dtable),
+                                   table.max_len, _ptr(out), _ptr(status), _stream(stream)), "sz3g_huffman_decode")
+    return out
