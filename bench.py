@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-planes", type=int, default=24)
+    ap.add_argument("--no-huffman", action="store_true", help="skip the encoder-stage (NEXT-1) measurement")
+    ap.add_argument("--huffman-reps", type=int, default=5)
     ap.add_argument("--path", default="two-pass", choices=["two-pass", "fused"],
                     help="REL compression: analyze (range + beta) -> quantize, or value_range -> fused compress")
     return ap.parse_args()
@@ -221,6 +223,61 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------------------- encoder stage
+def huffman_leg(sz3g, bufs, res, N_local, NB_local, s, args, world, peaks, stream):
+    """NEXT-1 measured on this rank's codes with the merged histogram: codebook (1 CTA), encode,
+    decode, timed with CUDA events (median of --huffman-reps), decode checked against the codes."""
+    import torch
+    codes = bufs.codes.view(-1)
+    n = codes.numel()
+    table = sz3g.huffman_codebook(bufs.hist).check()
+    hs = sz3g.huffman_encode(codes, table).check()
+    out = torch.empty_like(codes)
+    sz3g.huffman_decode(hs, table, out=out)
+    torch.cuda.synchronize()
+    if int(hs.status.item()) or not torch.equal(out, codes):
+        raise RuntimeError("Huffman round trip failed")
+    ev = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
+    t_cb, t_en, t_de = [], [], []
+    for _ in range(args.huffman_reps):
+        e = [ev() for _ in range(4)]
+        e[0].record(stream)
+        table = sz3g.huffman_codebook(bufs.hist)
+        e[1].record(stream)
+        sz3g.huffman_encode(codes, table, payload=hs.payload, offsets=hs.offsets, scratch=hs._scratch)
+        e[2].record(stream)
+        sz3g.huffman_decode(hs, table, out=out)
+        e[3].record(stream)
+        torch.cuda.synchronize()
+        t_cb.append(e[0].elapsed_time(e[1]))
+        t_en.append(e[1].elapsed_time(e[2]))
+        t_de.append(e[2].elapsed_time(e[3]))
+    med = lambda v: sorted(v)[len(v) // 2]   # noqa: E731
+    cb_ms = max_over_ranks(med(t_cb), world)
+    en_ms = max_over_ranks(med(t_en), world)
+    de_ms = max_over_ranks(med(t_de), world)
+    words = hs.words()
+    nch = hs.offsets.numel() - 1
+    pay_b = 4 * words
+    # algorithmic bytes (DESIGN.md 5): encode reads the codes once, writes payload + chunk offsets;
+    # decode reads payload + offsets, writes the codes
+    enc_bytes = 2 * n + pay_b + 8 * (nch + 1)
+    dec_bytes = pay_b + 8 * (nch + 1) + 2 * n
+    n_out = res.n_outliers
+    stored = pay_b + 8 * (nch + 1) + 16 * NB_local + (8 + s) * n_out + table.lengths.numel()
+    return {
+        "bits_per_code": 8 * pay_b / n, "payload_bytes": pay_b, "chunk": hs.chunk, "max_len": table.max_len,
+        "compression_ratio": N_local * s / stored,
+        "ratio_note": "input bytes / (payload + chunk offsets + int32 coefficient codes + outliers + code lengths)",
+        "codebook_ms": cb_ms, "encode_ms": en_ms, "decode_ms": de_ms,
+        "encode_gbs_input": N_local * s / (en_ms * 1e-3) / 1e9,
+        "encode_roofline": {"achieved": enc_bytes / (en_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                            "frac": enc_bytes / (en_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], "alg_bytes": enc_bytes},
+        "decode_roofline": {"achieved": dec_bytes / (de_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                            "frac": dec_bytes / (de_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], "alg_bytes": dec_bytes},
+    }
+
+
 # ----------------------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -313,6 +370,11 @@ def main():
     comp_gbs = comp_bytes / (comp_ms * 1e-3) / 1e9
     value = N_global * s / (ms_step * 1e-3) / 1e9
 
+    # ---------------- encoder stage (NEXT-1): codebook from the merged histogram, encode, decode
+    huff = None
+    if not args.no_huffman:
+        huff = huffman_leg(sz3g, bufs, res, N_local, NB_local, s, args, world, peaks, stream)
+
     # ---------------- end to end through the public API with HOST buffers (pinned), copies timed
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
@@ -390,6 +452,7 @@ def main():
                                  "frac": ana_bytes / (ana_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                                  "ms_per_step": ana_ms},
             "path": args.path,
+            "huffman": huff,
             "outliers": n_out, "eb_abs": res.eb_abs,
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -175,16 +175,19 @@ uint64_t sz3g_launch_count(void);
  *
  * sz3g_huffman_codebook -- from the (merged) histogram of sz3g_regression_compress / _quantize:
  *   hist       in   nsym int64 counts (nsym = 2R, <= 65536; counts in [0, 2^47)).
- *   max_len    in   maximum code length, 1..24 (the stream format uses 24).
+ *   max_len    in   maximum code length, 1..16 (the stream format uses 16).
  *   lengths    out  nsym uint8: optimal code lengths under max_len (package-merge, tie rule H2);
  *                   0 for symbols with count 0; one active symbol gets length 1.
- *   codewords  out  nsym uint32: canonical codewords (H3), right-aligned.
+ *   codewords  out  nsym uint32: (length << 24) | canonical codeword (H3, right-aligned in the low
+ *                   16 bits); 0 for absent symbols.  This packed table is what the encoder reads.
  *   dtable     out  sz3g_huffman_dtable_bytes(nsym) bytes, 16-byte aligned: the decoder's tables.
  *   scratch    in   sz3g_huffman_scratch_bytes(nsym, max_len) bytes of device memory.
  *   d_status   in/out SZ3G_STATUS_BAD_HUFFMAN on an empty histogram, a bad count or 2^max_len < n.
  *   One launch (a single CTA).  Bit-identical to the oracle's lengths and codewords.
  *
- * sz3g_huffman_encode -- n codes in chunks of `chunk` (1..2048; the format uses 2048):
+ * sz3g_huffman_encode -- n codes in chunks of `chunk` (1..2048; the format uses 2048), with the
+ *   packed codewords of sz3g_huffman_codebook (nsym entries; a code >= nsym or with length 0 sets
+ *   BAD_HUFFMAN):
  *   chunk_offsets out nchunks + 1 uint64: word offset of each chunk, then the total word count.
  *   payload       out the chunks, each packed MSB-first into whole 32-bit words (H4); at most
  *                     payload_cap_words words are written (SZ3G_STATUS_PAYLOAD_OVERFLOW beyond).
@@ -192,15 +195,16 @@ uint64_t sz3g_launch_count(void);
  *   5 launches (chunk sizes, 3-phase scan, pack).  Codes without a codeword set BAD_HUFFMAN.
  *
  * sz3g_huffman_decode -- the inverse: n codes from payload / chunk_offsets with the dtable of the
- *   same codebook (codes 16-byte aligned); a corrupt stream sets BAD_HUFFMAN.  1 launch.        */
+ *   same codebook (codes and payload 16-byte aligned); a corrupt stream sets BAD_HUFFMAN.
+ *   1 launch.                                                                                  */
 uint64_t sz3g_huffman_scratch_bytes(uint32_t nsym, uint32_t max_len);
 uint64_t sz3g_huffman_dtable_bytes(uint32_t nsym);
 uint64_t sz3g_huffman_encode_scratch_bytes(uint64_t n, uint32_t chunk);
 int sz3g_huffman_codebook(const int64_t* hist, uint32_t nsym, uint32_t max_len, uint8_t* lengths,
                           uint32_t* codewords, void* dtable, void* scratch, int32_t* d_status,
                           sz3g_stream_t stream);
-int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const uint8_t* lengths,
-                        const uint32_t* codewords, uint64_t* chunk_offsets, uint32_t* payload,
+int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const uint32_t* codewords,
+                        uint32_t nsym, uint64_t* chunk_offsets, uint32_t* payload,
                         uint64_t payload_cap_words, void* scratch, int32_t* d_status,
                         sz3g_stream_t stream);
 int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, uint64_t n,

@@ -207,7 +207,7 @@ def quantize_element(x: float, p: float, eb_abs: float, radius: int = 32768, dty
 
 # ------------------------------------------------------------------------------------------- Huffman
 # The encoder stage after the quantiser (DEFINITION.md H1-H5; huffman_oracle.cpp).
-HUFF_MAX_LEN = 24    # G20: length limit of the codebook
+HUFF_MAX_LEN = 16    # G20: length limit of the codebook
 HUFF_CHUNK = 2048    # G21: codes per independently decodable chunk
 
 

@@ -30,8 +30,8 @@ namespace {
 constexpr int HF_THREADS = 512;         // codebook CTA (16 x 512 radix counters = 32 KiB smem)
 constexpr int HF_WARPS = HF_THREADS / 32;
 constexpr int HF_LUT_BITS = 12;         // decoder first-level table
-constexpr int HF_MAXL = 32;             // array bound for per-length tables (max_len <= 24 supported)
-constexpr int HF_MAX_LEN_LIMIT = 24;
+constexpr int HF_MAXL = 32;             // array bound for per-length tables
+constexpr int HF_MAX_LEN_LIMIT = 16;    // format limit (G20): two codes fit in one 32-bit refill
 
 // ------------------------------------------------------------------------------------------------
 // Device table layout (sz3g_huffman_dtable_bytes): lut[4096] u32 ((len << 16) | symbol, 0 = longer
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     if (tid == 0) {
       const uint32_t sym = (uint32_t)(S.keys0[0] & 0xffffu);
       lens[sym] = 1;
-      cws[sym] = 0;
+      cws[sym] = 1u << 24;   // length 1, codeword 0
       dt->first[1] = 0;
       dt->count[1] = 1;
       for (uint32_t i = 0; i < (1u << (HF_LUT_BITS - 1)); i++) dt->lut[i] = (1u << 16) | sym;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
       uint32_t before = s_run[L];
       for (int w = 0; w < wid; w++) before += s_wl[w * 32 + L];
       const uint32_t cw = s_first[L] + before + rank_w;
-      cws[s] = cw;
+      cws[s] = (L << 24) | cw;   // packed: length in the top 8 bits
       if (L <= HF_LUT_BITS) {
         const uint32_t lo = cw << (HF_LUT_BITS - L), cnt = 1u << (HF_LUT_BITS - L);
         for (uint32_t e = 0; e < cnt; e++) dt->lut[lo + e] = (L << 16) | s;
@@ -314,20 +314,37 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
 // ------------------------------------------------------------------------------------------------
 // encode
 __global__ void __launch_bounds__(256) k_huff_chunk_words(const uint16_t* __restrict__ codes, uint64_t n,
-                                                          uint32_t chunk, const uint8_t* __restrict__ lens,
-                                                          uint64_t* __restrict__ words, uint64_t nch,
+                                                          uint32_t chunk, const uint32_t* __restrict__ tab,
+                                                          uint32_t nsym, uint64_t* __restrict__ words, uint64_t nch,
                                                           int32_t* status) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
+  const bool vec = (chunk % 8 == 0) && ((reinterpret_cast<uintptr_t>(codes) & 15) == 0);
   for (uint64_t c = warp; c < nch; c += nw) {
     const uint64_t e0 = c * chunk, e1 = min(n, e0 + chunk);
     uint64_t bits = 0;
     bool miss = false;
-    for (uint64_t e = e0 + lane; e < e1; e += 32) {
-      const uint32_t L = __ldg(lens + codes[e]);
+    auto add = [&](uint32_t q) {
+      const uint32_t L = q < nsym ? (__ldg(tab + q) >> 24) : 0u;
       bits += L;
       miss |= L == 0;
+    };
+    if (vec) {   // 8 codes per 16-byte load (the chunk start is 16-byte aligned)
+      const uint4* g = reinterpret_cast<const uint4*>(codes + e0);
+      const uint32_t m = (uint32_t)(e1 - e0);
+      for (uint32_t i = lane; 8 * i < m; i += 32) {
+        const uint4 u = __ldg(g + i);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        if (8 * i + 8 <= m) {
+#pragma unroll
+          for (int h = 0; h < 8; h++) add((w[h >> 1] >> (16 * (h & 1))) & 0xffffu);
+        } else {
+          for (uint32_t h = 0; 8 * i + h < m; h++) add((w[h >> 1] >> (16 * (h & 1))) & 0xffffu);
+        }
+      }
+    } else {
+      for (uint64_t e = e0 + lane; e < e1; e += 32) add(codes[e]);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
@@ -420,21 +437,52 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_apply(uint64_t* __restrict__ v,
   if (blockIdx.x == 0 && threadIdx.x == 0) v[m] = sums[nb];
 }
 
-// One warp per chunk (chunk <= 32 * 64 codes).  Lane l owns codes [l*per, (l+1)*per) of the chunk.
-constexpr int ENC_WARPS = 4, ENC_PER = 64, ENC_MAX_CHUNK = 32 * ENC_PER;   // 4 x 6 KiB chunk images
+// One warp per chunk (chunk <= 32 * 64 codes).  The chunk's codes are staged in shared memory with
+// coalesced 16-byte loads (uint4 i stored at slot i ^ ((i >> 3) & 7): conflict-free both when the
+// warp writes consecutive uint4 and when lane l reads its own 8 consecutive uint4).  Lane l owns codes
+// [64 l, 64 l + 64) of the chunk: their bit count, a warp scan for the lane's first bit, then the
+// lane packs whole words of the chunk image (its first and last word shared -> atomicOr).  One
+// lookup per code in the packed table (length << 24 | codeword).
+constexpr int ENC_WARPS = 4, ENC_PER = 64, ENC_MAX_CHUNK = 32 * ENC_PER;   // 4 x (4 KiB image + 4 KiB codes)
 constexpr int ENC_WORDS = ENC_MAX_CHUNK * HF_MAX_LEN_LIMIT / 32 + 1;
+__device__ __forceinline__ uint32_t swz(uint32_t i) { return i ^ ((i >> 3) & 7u); }
+
+struct Packer {
+  uint64_t buf;
+  uint32_t nbuf, wi;
+  bool first;
+  __device__ __forceinline__ void put(uint32_t t, uint32_t* img) {
+    const uint32_t L = t >> 24;
+    buf = (buf << L) | (t & 0xffffffu);
+    nbuf += L;
+    if (nbuf >= 32) {
+      const uint32_t word = (uint32_t)(buf >> (nbuf - 32));
+      if (first) atomicOr(&img[wi], word);
+      else img[wi] = word;
+      first = false;
+      wi++;
+      nbuf -= 32;
+    }
+  }
+};
+
 __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* __restrict__ codes, uint64_t n,
-                                                                uint32_t chunk, const uint8_t* __restrict__ lens,
-                                                                const uint32_t* __restrict__ cws,
-                                                                const uint64_t* __restrict__ offs, uint64_t nch,
-                                                                uint32_t* __restrict__ payload, uint64_t cap,
-                                                                int32_t* status) {
+                                                                uint32_t chunk, const uint32_t* __restrict__ tab,
+                                                                uint32_t nsym, const uint64_t* __restrict__ offs,
+                                                                uint64_t nch, uint32_t* __restrict__ payload,
+                                                                uint64_t cap, int32_t* status) {
   __shared__ uint32_t s_img[ENC_WARPS][ENC_WORDS];
+  __shared__ uint4 s_codes[ENC_WARPS][ENC_MAX_CHUNK / 8];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   uint32_t* img = s_img[wl];
+  uint4* sc = s_codes[wl];
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint32_t per = (chunk + 31) / 32;
+  const bool vec = (chunk == ENC_MAX_CHUNK) && ((reinterpret_cast<uintptr_t>(codes) & 15) == 0);
+  const uint32_t per = vec ? ENC_PER : (chunk + 31) / 32;
+  const uint32_t* __restrict__ tb = tab;
+  const uint32_t ns = nsym;
+  auto look = [tb, ns](uint32_t q) -> uint32_t { return q < ns ? __ldg(tb + q) : 0u; };
   for (uint64_t c = gw; c < nch; c += nw) {
     const uint64_t e0 = c * chunk, e1 = min(n, e0 + chunk);
     const uint64_t w0 = offs[c], nwords = offs[c + 1] - w0;
@@ -443,10 +491,33 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
       continue;
     }
     for (uint32_t i = lane; i < nwords; i += 32) img[i] = 0u;
-    __syncwarp();
-    const uint64_t a0 = min(e1, e0 + (uint64_t)lane * per), a1 = min(e1, a0 + per);
+    const uint32_t m = (uint32_t)(e1 - e0);
+    const uint32_t a0 = min(m, (uint32_t)lane * per), a1 = min(m, a0 + per);
+    const bool fullc = vec && m == ENC_MAX_CHUNK;
     uint32_t bits = 0;
-    for (uint64_t e = a0; e < a1; e++) bits += __ldg(lens + codes[e]);
+    if (vec) {
+      const uint4* g = reinterpret_cast<const uint4*>(codes + e0);
+      for (uint32_t i = lane; i < ENC_MAX_CHUNK / 8; i += 32)
+        sc[swz(i)] = 8 * i < m ? __ldg(g + i) : make_uint4(0, 0, 0, 0);
+      __syncwarp();
+    }
+    if (fullc) {
+#pragma unroll 2
+      for (uint32_t v = 0; v < ENC_PER / 8; v++) {
+        const uint4 u = sc[swz(lane * 8 + v)];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int h = 0; h < 8; h++) bits += look((w[h >> 1] >> (16 * (h & 1))) & 0xffffu) >> 24;
+      }
+    } else if (vec) {
+      for (uint32_t e = a0; e < a1; e++) {
+        const uint4 u = sc[swz(e >> 3)];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        bits += look((w[(e & 7) >> 1] >> (16 * (e & 1))) & 0xffffu) >> 24;
+      }
+    } else {
+      for (uint32_t e = a0; e < a1; e++) bits += look(codes[e0 + e]) >> 24;
+    }
     uint32_t incl = bits;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -454,26 +525,31 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
       if (lane >= o) incl += y;
     }
     const uint32_t b0 = incl - bits;   // first bit of this lane inside the chunk
+    __syncwarp();                      // the image is zeroed before any lane writes into it
     // pack: the buffer starts with the (b0 % 32) bits of the previous lane as zeros, so every emitted
     // word is a whole word of the chunk image; the first and the last are shared -> atomicOr
-    uint64_t buf = 0;
-    uint32_t nbuf = b0 & 31u, wi = b0 >> 5;
-    bool first = true;
-    for (uint64_t e = a0; e < a1; e++) {
-      const uint32_t q = codes[e];
-      const uint32_t L = __ldg(lens + q), cw = __ldg(cws + q);
-      buf = (buf << L) | cw;
-      nbuf += L;
-      if (nbuf >= 32) {
-        const uint32_t word = (uint32_t)(buf >> (nbuf - 32));
-        if (first) atomicOr(&img[wi], word);
-        else img[wi] = word;
-        first = false;
-        wi++;
-        nbuf -= 32;
+    Packer pk{0, b0 & 31u, b0 >> 5, true};
+    if (fullc) {
+#pragma unroll 2
+      for (uint32_t v = 0; v < ENC_PER / 8; v++) {
+        const uint4 u = sc[swz(lane * 8 + v)];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        uint32_t t[8];
+#pragma unroll
+        for (int h = 0; h < 8; h++) t[h] = look((w[h >> 1] >> (16 * (h & 1))) & 0xffffu);
+#pragma unroll
+        for (int h = 0; h < 8; h++) pk.put(t[h], img);
       }
+    } else if (vec) {
+      for (uint32_t e = a0; e < a1; e++) {
+        const uint4 u = sc[swz(e >> 3)];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        pk.put(look((w[(e & 7) >> 1] >> (16 * (e & 1))) & 0xffffu), img);
+      }
+    } else {
+      for (uint32_t e = a0; e < a1; e++) pk.put(look(codes[e0 + e]), img);
     }
-    if (nbuf > 0 && bits > 0) atomicOr(&img[wi], (uint32_t)(buf << (32 - nbuf)));
+    if (pk.nbuf > 0 && bits > 0) atomicOr(&img[pk.wi], (uint32_t)(pk.buf << (32 - pk.nbuf)));
     __syncwarp();
     for (uint32_t i = lane; i < nwords; i += 32) payload[w0 + i] = img[i];
     __syncwarp();
@@ -481,79 +557,165 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
 }
 
 // ------------------------------------------------------------------------------------------------
-// decode: one thread per chunk
-__global__ void __launch_bounds__(256) k_huff_decode(const uint32_t* __restrict__ payload,
-                                                     const uint64_t* __restrict__ offs, uint64_t n, uint32_t chunk,
-                                                     const DTab* __restrict__ dt, uint32_t max_len,
-                                                     uint16_t* __restrict__ codes, uint64_t nch, int32_t* status) {
-  __shared__ uint32_t s_lut[1 << HF_LUT_BITS];
-  __shared__ uint32_t s_first[HF_MAXL], s_count[HF_MAXL], s_base[HF_MAXL];
+// decode: one thread per chunk, warp-synchronous staging.  Lane l of a warp decodes chunk
+// (warp base + l), one code per step.  Codes are at most 16 bits, so a round of 32 steps consumes at
+// most 16 payload words per lane: at the start of every round the warp tops up, with coalesced
+// 64-byte loads (half a warp per chunk), the per-lane ring of 32 words in shared memory (rows padded
+// to 33 words: no bank conflicts when every lane reads its own row).  Lanes refill their 64-bit bit
+// window from their ring once per pair of codes (a pair needs <= 32 bits).  Decoded codes go to a
+// per-lane row of 32 codes in shared memory, written out after each round with one coalesced
+// 64-byte store per chunk.  Codes longer than the 12-bit LUT take a branch-free canonical length
+// search (3 compares), guarded by a warp vote.
+constexpr int DEC_WARPS = 8, DEC_ROUND = 32, RING = 32, RING_P = RING + 1, OUT_P = DEC_ROUND / 2 + 1;
+
+struct DecLane {
+  uint64_t win;      // left-aligned bit window (zeros past the end of the chunk)
+  uint32_t avail;    // valid bits in win
+  uint32_t r;        // next word (relative to the chunk start) to append to the window
+  uint32_t filled;   // words [0, filled) of the chunk have been staged into the ring
+  uint32_t nwords;   // words of this chunk
+  uint32_t consumed; // bits decoded (steps before the chunk end)
+};
+
+__device__ __forceinline__ uint32_t dec_one(DecLane& d, const uint32_t* s_lut, const uint32_t* s_ljl,
+                                            const uint32_t* s_first, const uint32_t* s_base,
+                                            const uint16_t* __restrict__ syms, uint32_t maxl, bool& bad,
+                                            bool active) {
+  const uint32_t top = (uint32_t)(d.win >> 48);   // next 16 bits
+  const uint32_t ent = s_lut[top >> (16 - HF_LUT_BITS)];
+  uint32_t L = ent >> 16, sym = ent & 0xffffu;
+  if (__any_sync(0xffffffffu, ent == 0u)) {
+    if (ent == 0u) {   // canonical: the smallest l > 12 whose left-justified limit exceeds top
+      L = HF_LUT_BITS + 1 + (top >= s_ljl[13] ? 1u : 0u) + (top >= s_ljl[14] ? 1u : 0u) + (top >= s_ljl[15] ? 1u : 0u);
+      if (L > maxl || top >= s_ljl[L]) { bad |= active; L = 1; sym = 0; }
+      else sym = syms[s_base[L] + (top >> (16 - L)) - s_first[L]];
+    }
+  }
+  d.win <<= L;
+  d.avail -= L;
+  d.consumed += active ? L : 0u;   // steps past the end of a short chunk do not count
+  return sym;
+}
+
+__device__ __forceinline__ void dec_refill(DecLane& d, const uint32_t* ring) {
+  if (d.avail <= 32) {
+    const uint32_t w = d.r < d.nwords ? ring[d.r % RING] : 0u;
+    d.win |= (uint64_t)w << (32 - d.avail);
+    d.avail += 32;
+    d.r++;
+  }
+}
+
+__global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* __restrict__ payload,
+                                                                const uint64_t* __restrict__ offs, uint64_t n,
+                                                                uint32_t chunk, const DTab* __restrict__ dt,
+                                                                uint32_t max_len, uint16_t* __restrict__ codes,
+                                                                uint64_t nch, int32_t* status) {
+  extern __shared__ __align__(16) uint32_t dsm[];
+  uint32_t* s_lut = dsm;                                  // 4096
+  uint32_t* s_first = s_lut + (1 << HF_LUT_BITS);         // 32
+  uint32_t* s_base = s_first + HF_MAXL;
+  uint32_t* s_ljl = s_base + HF_MAXL;
+  uint32_t* s_ring = s_ljl + HF_MAXL;                     // [DEC_WARPS][32 lanes][RING_P]
+  uint32_t* s_out = s_ring + DEC_WARPS * 32 * RING_P;     // [DEC_WARPS][32 lanes][OUT_P]
   for (int i = threadIdx.x; i < (1 << HF_LUT_BITS); i += blockDim.x) s_lut[i] = dt->lut[i];
   if (threadIdx.x < HF_MAXL) {
-    s_first[threadIdx.x] = dt->first[threadIdx.x];
-    s_count[threadIdx.x] = dt->count[threadIdx.x];
-    s_base[threadIdx.x] = dt->base[threadIdx.x];
+    const uint32_t l = threadIdx.x;
+    s_first[l] = dt->first[l];
+    s_base[l] = dt->base[l];
+    // left-justified (16-bit) limit of length l; lengths above max_len are unreachable
+    s_ljl[l] = (l >= 1 && l <= max_len) ? (uint32_t)(((uint64_t)dt->first[l] + dt->count[l]) << (16 - l))
+                                        : (l > max_len ? 0x10000u : 0u);
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  uint32_t* ring_w = s_ring + wl * 32 * RING_P;
+  uint32_t* ring = ring_w + lane * RING_P;
+  uint32_t* out_w = s_out + wl * 32 * OUT_P;
+  uint32_t* out = out_w + lane * OUT_P;
   const uint16_t* syms = reinterpret_cast<const uint16_t*>(dt + 1);
-  const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (c >= nch) return;
-  const uint64_t e0 = c * chunk, e1 = min(n, e0 + chunk);
-  const uint32_t* p = payload + offs[c];
-  const uint32_t* pend = payload + offs[c + 1];
-  uint64_t win = 0;     // left-aligned bit window (zeros past the end of the chunk)
-  uint32_t avail = 0;
-  uint64_t consumed = 0;
+  const uint64_t cbase = ((uint64_t)blockIdx.x * DEC_WARPS + wl) * 32;
+  if (cbase >= nch) return;
+  const uint64_t c = cbase + lane;
+  const bool live = c < nch;
+  const uint64_t cc = live ? c : nch - 1;
+  const uint64_t e0 = cc * chunk;
+  const uint32_t m = live ? (uint32_t)(min(n, e0 + chunk) - e0) : 0u;
+  const uint64_t w0 = offs[cc];
+  DecLane d;
+  d.nwords = live ? (uint32_t)(offs[cc + 1] - w0) : 0u;
+  d.win = 0;
+  d.avail = 0;
+  d.r = 0;
+  d.filled = 0;
+  d.consumed = 0;
   bool bad = false;
-  uint32_t pack[4];
-  uint32_t npk = 0;
-  const bool vec = ((e0 & 7) == 0);   // 16-byte stores from an 8-code aligned start
-  for (uint64_t e = e0; e < e1; e++) {
-    if (avail <= 32) {
-      const uint32_t w = p < pend ? *p : 0u;
-      if (p < pend) p++;
-      win |= (uint64_t)w << (32 - avail);
-      avail += 32;
-    }
-    const uint32_t top = (uint32_t)(win >> 40);   // 24 bits
-    uint32_t ent = s_lut[top >> (24 - HF_LUT_BITS)];
-    uint32_t L, sym;
-    if (ent) {
-      L = ent >> 16;
-      sym = ent & 0xffffu;
-    } else {
-      sym = 0;
-      L = 0;
-      for (uint32_t l = HF_LUT_BITS + 1; l <= max_len; l++) {
-        const uint32_t code = top >> (24 - l);
-        if (code - s_first[l] < s_count[l]) {
-          sym = syms[s_base[l] + code - s_first[l]];
-          L = l;
-          break;
+  const uint32_t steps = __reduce_max_sync(0xffffffffu, m);
+  const int half = lane >> 4, hl = lane & 15;
+  for (uint32_t e = 0; e < steps; e += DEC_ROUND) {
+    // (1) top up every ring that holds fewer than 16 unread words (the first round: 32, since the
+    // window is primed with 2 words first): 16 words per lane, 2 lanes per pass.  A fill overwrites
+    // words [filled - 32, filled - 16), all consumed since filled < r + 16.
+    for (int pass = 0; pass < (e == 0 ? 2 : 1); pass++) {
+      const bool need = d.filled < d.r + 16 + (e == 0 ? 16u : 0u) && d.filled < d.nwords;
+      if (__any_sync(0xffffffffu, need)) {
+        // pass j serves chunk 2j + half: all 16 loads are issued before any store
+        uint32_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int src = 2 * j + half;
+          const bool nd = __shfl_sync(0xffffffffu, need, src);
+          const uint32_t fl = __shfl_sync(0xffffffffu, d.filled, src);
+          const uint32_t nw = __shfl_sync(0xffffffffu, d.nwords, src);
+          const uint64_t gw = __shfl_sync(0xffffffffu, w0, src);
+          const uint32_t wi = fl + hl;
+          v[j] = (nd && wi < nw) ? __ldg(payload + gw + wi) : 0u;
         }
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int src = 2 * j + half;
+          const bool nd = __shfl_sync(0xffffffffu, need, src);
+          const uint32_t fl = __shfl_sync(0xffffffffu, d.filled, src);
+          if (nd) ring_w[src * RING_P + (fl + hl) % RING] = v[j];
+        }
+        if (need) d.filled += 16;
       }
-      if (L == 0) { bad = true; L = 1; }
+      __syncwarp();
     }
-    win <<= L;
-    avail -= L;
-    consumed += L;
-    if (vec) {
-      const uint32_t slot = npk >> 1;
-      if (npk & 1) pack[slot] |= sym << 16;
-      else pack[slot] = sym;
-      if (++npk == 8) {
-        *reinterpret_cast<uint4*>(codes + e - 7) = make_uint4(pack[0], pack[1], pack[2], pack[3]);
-        npk = 0;
+    if (e == 0) {   // prime the window: 64 bits
+      dec_refill(d, ring);
+      dec_refill(d, ring);
+    }
+    // (2) 32 steps: 16 pairs of codes
+#pragma unroll 4
+    for (int h = 0; h < DEC_ROUND; h += 2) {
+      const uint32_t a = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, e + h < m);
+      const uint32_t b = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, e + h + 1 < m);
+      dec_refill(d, ring);
+      out[h >> 1] = a | (b << 16);
+    }
+    __syncwarp();
+    // (3) write the round's codes: one chunk row (64 B) per half-warp pass
+    for (int j = 0; j < 32; j += 2) {
+      const int src = j + half;
+      const uint32_t mj = __shfl_sync(0xffffffffu, m, src);
+      const uint64_t ej = __shfl_sync(0xffffffffu, e0, src);
+      const uint32_t k = e + 2 * hl;   // first code of this lane's word
+      const uint32_t v = out_w[src * OUT_P + hl];
+      if (k + 1 < mj && ((ej & 1) == 0)) {
+        *reinterpret_cast<uint32_t*>(codes + ej + k) = v;
+      } else {
+        if (k < mj) codes[ej + k] = (uint16_t)v;
+        if (k + 1 < mj) codes[ej + k + 1] = (uint16_t)(v >> 16);
       }
-    } else {
-      codes[e] = (uint16_t)sym;
     }
+    __syncwarp();
   }
-  if (vec) {   // tail (fewer than 8 codes)
-    for (uint32_t k = 0; k < npk; k++) codes[e1 - npk + k] = (uint16_t)(pack[k >> 1] >> (16 * (k & 1)));
-  }
-  // consumed more bits than the chunk holds?
-  if (bad || consumed > (offs[c + 1] - offs[c]) * 32) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
+  if (live && (bad || d.consumed > d.nwords * 32u)) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
+}
+
+size_t dec_smem_bytes() {
+  return 4ull * ((1 << HF_LUT_BITS) + 3 * HF_MAXL + DEC_WARPS * 32 * (RING_P + OUT_P));
 }
 
 std::atomic<uint64_t> g_hf_launches{0};
@@ -599,10 +761,11 @@ int sz3g_huffman_codebook(const int64_t* hist, uint32_t nsym, uint32_t max_len, 
   return hf_check(1);
 }
 
-int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const uint8_t* lengths,
-                        const uint32_t* codewords, uint64_t* chunk_offsets, uint32_t* payload,
-                        uint64_t payload_cap_words, void* scratch, int32_t* d_status, sz3g_stream_t stream) {
-  if ((n > 0 && !codes) || !lengths || !codewords || !chunk_offsets || !d_status) return SZ3G_EINVAL;
+int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const uint32_t* codewords,
+                        uint32_t nsym, uint64_t* chunk_offsets, uint32_t* payload, uint64_t payload_cap_words,
+                        void* scratch, int32_t* d_status, sz3g_stream_t stream) {
+  if ((n > 0 && !codes) || !codewords || !chunk_offsets || !d_status) return SZ3G_EINVAL;
+  if (nsym < 1 || nsym > 65536) return SZ3G_ERANGE;
   if (chunk < 1 || chunk > ENC_MAX_CHUNK) return SZ3G_ERANGE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const uint64_t nch = (n + chunk - 1) / chunk;
@@ -613,14 +776,14 @@ int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const
   if (!payload || !scratch) return SZ3G_EINVAL;
   const int sms = sm_count_hf();
   const unsigned gw = (unsigned)std::min<uint64_t>((nch * 32 + 255) / 256, (uint64_t)sms * 16);
-  k_huff_chunk_words<<<gw, 256, 0, st>>>(codes, n, chunk, lengths, chunk_offsets, nch, d_status);
+  k_huff_chunk_words<<<gw, 256, 0, st>>>(codes, n, chunk, codewords, nsym, chunk_offsets, nch, d_status);
   const uint64_t nb = (nch + SCAN_TILE - 1) / SCAN_TILE;
   uint64_t* sums = reinterpret_cast<uint64_t*>(scratch);
   k_scan_sums<<<(unsigned)nb, SCAN_T, 0, st>>>(chunk_offsets, nch, sums);
   k_scan_top<<<1, SCAN_T, 0, st>>>(sums, nb);
   k_scan_apply<<<(unsigned)nb, SCAN_T, 0, st>>>(chunk_offsets, nch, sums, nb);
   const unsigned ge = (unsigned)std::min<uint64_t>((nch + ENC_WARPS - 1) / ENC_WARPS, (uint64_t)sms * 8);
-  k_huff_encode<<<ge, ENC_WARPS * 32, 0, st>>>(codes, n, chunk, lengths, codewords, chunk_offsets, nch, payload,
+  k_huff_encode<<<ge, ENC_WARPS * 32, 0, st>>>(codes, n, chunk, codewords, nsym, chunk_offsets, nch, payload,
                                                payload_cap_words, d_status);
   return hf_check(5);
 }
@@ -634,7 +797,14 @@ int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, 
   if (reinterpret_cast<uintptr_t>(codes) & 15) return SZ3G_EINVAL;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const uint64_t nch = (n + chunk - 1) / chunk;
-  k_huff_decode<<<(unsigned)((nch + 255) / 256), 256, 0, st>>>(payload, chunk_offsets, n, chunk,
+  const size_t smem = dec_smem_bytes();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_huff_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const uint64_t per_cta = 32ull * DEC_WARPS;
+  k_huff_decode<<<(unsigned)((nch + per_cta - 1) / per_cta), DEC_WARPS * 32, smem, st>>>(payload, chunk_offsets, n, chunk,
                                                                reinterpret_cast<const DTab*>(dtable), max_len,
                                                                codes, nch, d_status);
   return hf_check(1);

@@ -80,7 +80,7 @@ def load(allow_build: bool = False):
         lib.sz3g_huffman_encode_scratch_bytes.argtypes = [U64, U32]
         lib.sz3g_huffman_encode_scratch_bytes.restype = U64
         lib.sz3g_huffman_codebook.argtypes = [P, U32, U32, P, P, P, P, P, P]
-        lib.sz3g_huffman_encode.argtypes = [P, U64, U32, P, P, P, P, U64, P, P, P]
+        lib.sz3g_huffman_encode.argtypes = [P, U64, U32, P, U32, P, P, U64, P, P, P]
         lib.sz3g_huffman_decode.argtypes = [P, P, U64, U32, P, U32, P, P, P]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
@@ -392,14 +392,14 @@ def decompress(res: Compressed, out: torch.Tensor | None = None, flags: int = 0)
 
 
 # ------------------------------------------------------------------------------------------- Huffman
-HUFF_MAX_LEN = 24     # DEFINITION.md H2 / G20
+HUFF_MAX_LEN = 16     # DEFINITION.md H2 / G20
 HUFF_CHUNK = 2048     # H4 / G21
 
 
 @dataclass
 class HuffmanTable:
     lengths: torch.Tensor     # uint8 [nsym]
-    codewords: torch.Tensor   # int32 (uint32 bits) [nsym]
+    codewords: torch.Tensor   # int32 (uint32 bits) [nsym]: (length << 24) | canonical codeword
     dtable: torch.Tensor      # uint8 [sz3g_huffman_dtable_bytes]
     max_len: int
     status: torch.Tensor      # int32 [1]
@@ -465,8 +465,9 @@ def huffman_encode(codes: torch.Tensor, table: HuffmanTable, chunk: int = HUFF_C
     if scratch is None:
         scratch = torch.empty(int(lib.sz3g_huffman_encode_scratch_bytes(n, chunk)), dtype=torch.uint8, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    _check(lib.sz3g_huffman_encode(_ptr(codes), n, chunk, _ptr(table.lengths), _ptr(table.codewords), _ptr(offsets),
-                                   _ptr(payload), payload.numel(), _ptr(scratch), _ptr(status), _stream(stream)),
+    _check(lib.sz3g_huffman_encode(_ptr(codes), n, chunk, _ptr(table.codewords), table.codewords.numel(),
+                                   _ptr(offsets), _ptr(payload), payload.numel(), _ptr(scratch), _ptr(status),
+                                   _stream(stream)),
            "sz3g_huffman_encode")
     hs = HuffmanStream(n, chunk, offsets, payload, status)
     hs._scratch = scratch
