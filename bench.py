@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cpu-sample-planes", type=int, default=24)
     ap.add_argument("--no-huffman", action="store_true", help="skip the encoder-stage (NEXT-1) measurement")
     ap.add_argument("--huffman-reps", type=int, default=5)
+    ap.add_argument("--no-truncation", action="store_true", help="skip the SZ3-Truncation (NEXT-2) measurement")
+    ap.add_argument("--trunc-k", type=int, default=2)
     ap.add_argument("--path", default="two-pass", choices=["two-pass", "fused"],
                     help="REL compression: analyze (range + beta) -> quantize, or value_range -> fused compress")
     return ap.parse_args()
@@ -278,6 +280,43 @@ def huffman_leg(sz3g, bufs, res, N_local, NB_local, s, args, world, peaks, strea
     }
 
 
+def truncation_leg(sz3g, x, out, args, world, peaks, stream):
+    """NEXT-2: keep k most-significant bytes per value, timed with CUDA events (median of 5),
+    reconstruction checked against the zero-filled definition on a sample."""
+    import torch
+    k, n, s = args.trunc_k, x.numel(), x.element_size()
+    xf = x.view(-1)
+    b = sz3g.truncation_compress(xf, k)
+    y = out.view(-1)
+    sz3g.truncation_decompress(b, n, k, x.dtype, out=y)
+    torch.cuda.synchronize()
+    mask = -(1 << (8 * (s - k))) if s == 4 else None
+    if s == 4:   # spot check: y == x with the low bytes cleared
+        xi = xf[:1 << 20].view(torch.int32)
+        if not torch.equal(y[:1 << 20].view(torch.int32), xi & mask):
+            raise RuntimeError("truncation round trip failed")
+    tc, td = [], []
+    for _ in range(5):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        sz3g.truncation_compress(xf, k, out=b)
+        e[1].record(stream)
+        sz3g.truncation_decompress(b, n, k, x.dtype, out=y)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        tc.append(e[0].elapsed_time(e[1]))
+        td.append(e[1].elapsed_time(e[2]))
+    c_ms = max_over_ranks(sorted(tc)[2], world)
+    d_ms = max_over_ranks(sorted(td)[2], world)
+    nb = n * (s + k)   # algorithmic bytes of either direction
+    return {"k": k, "compression_ratio": s / k, "compress_ms": c_ms, "decompress_ms": d_ms,
+            "compress_gbs_input": n * s / (c_ms * 1e-3) / 1e9,
+            "compress_roofline": {"achieved": nb / (c_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                  "frac": nb / (c_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "decompress_roofline": {"achieved": nb / (d_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                    "frac": nb / (d_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
+
+
 # ----------------------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -375,6 +414,11 @@ def main():
     if not args.no_huffman:
         huff = huffman_leg(sz3g, bufs, res, N_local, NB_local, s, args, world, peaks, stream)
 
+    # ---------------- SZ3-Truncation (NEXT-2) on the same field
+    trunc = None
+    if not args.no_truncation:
+        trunc = truncation_leg(sz3g, x, out, args, world, peaks, stream)
+
     # ---------------- end to end through the public API with HOST buffers (pinned), copies timed
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
@@ -452,7 +496,7 @@ def main():
                                  "frac": ana_bytes / (ana_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                                  "ms_per_step": ana_ms},
             "path": args.path,
-            "huffman": huff,
+            "huffman": huff, "truncation": trunc,
             "outliers": n_out, "eb_abs": res.eb_abs,
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -211,6 +211,20 @@ int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, 
                         uint32_t chunk, const void* dtable, uint32_t max_len, uint16_t* codes,
                         int32_t* d_status, sz3g_stream_t stream);
 
+/* ---- SZ3-Truncation (NEXT-2): "Given the target bytes k as input parameter, it
+ * keeps k most-significant bytes of each floating-point data while discarding the rest of the bytes";
+ * "it bypasses the other stages".  Definition: oracle/DEFINITION.md T1-T2 (reading G24).
+ *   grid   dtype and extents (n = prod(dims) elements; dim0_offset unused).
+ *   x      prod(dims) T; out / in: n * k bytes, element after element, each element's k
+ *          most-significant bytes of its IEEE-754 pattern, most significant first.
+ *   k      1..4 (f32) or 1..8 (f64), else ERANGE.  Buffers 16-byte aligned, else EINVAL.
+ * Decompression writes the stored bytes as the most significant ones and zeros below.  1 launch
+ * each; k = sizeof(T) is bitwise lossless.                                                      */
+int sz3g_truncation_compress(const sz3g_grid* grid, const void* x, uint32_t k, uint8_t* out,
+                             sz3g_stream_t stream);
+int sz3g_truncation_decompress(const sz3g_grid* grid, const uint8_t* in, uint32_t k, void* x_out,
+                               sz3g_stream_t stream);
+
 /* Performance tuning only (no call changes a result): set knob `key` ("CHUNK_C", "CHUNK_D", "CCFG",
  * "PF"; defaults are the measured best, environment SZ3G_<KEY> overrides them) for
  * launches issued after the call.  Process-global, not thread-safe against concurrent launches.

@@ -18,7 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sz3_oracle.cpp")
-_SRCS = [_SRC, os.path.join(_HERE, "huffman_oracle.cpp")]
+_SRCS = [_SRC, os.path.join(_HERE, "huffman_oracle.cpp"), os.path.join(_HERE, "truncation_oracle.cpp")]
 _LIB_PATH = os.path.join(_HERE, "liboracle_sz3.so")
 _lock = threading.Lock()
 _lib = None
@@ -71,6 +71,8 @@ def _load():
             lib.orc_huffman_chunk_offsets.restype = None
             lib.orc_huffman_encode.argtypes = [P, U64, U32, P, P, P, P]
             lib.orc_huffman_decode.argtypes = [P, P, U64, U32, P, P, U32, P]
+            lib.orc_trunc_compress.argtypes = [I32, U64, P, U32, P]
+            lib.orc_trunc_decompress.argtypes = [I32, U64, P, U32, P]
             _lib = lib
     return _lib
 
@@ -256,3 +258,25 @@ def huffman_decode(words: np.ndarray, offs: np.ndarray, n: int, lens: np.ndarray
     if rc != 0:
         raise ValueError(f"corrupt stream ({rc})")
     return q
+
+
+# ------------------------------------------------------------------------------------------- Truncation
+# SZ3-Truncation (DEFINITION.md T1-T2; truncation_oracle.cpp).
+def trunc_compress(x: np.ndarray, k: int) -> np.ndarray:
+    """T1: the k most-significant bytes of every element, most significant first (uint8[n*k])."""
+    x = np.ascontiguousarray(x).reshape(-1)
+    out = np.zeros(x.size * k, np.uint8)
+    rc = _load().orc_trunc_compress(_dtype_id(x.dtype), x.size, _ptr(x), k, _ptr(out))
+    if rc != 0:
+        raise ValueError(f"orc_trunc_compress failed ({rc})")
+    return out
+
+
+def trunc_decompress(b: np.ndarray, n: int, k: int, dtype) -> np.ndarray:
+    """T2: zero-fill the discarded bytes."""
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    x = np.zeros(n, dtype)
+    rc = _load().orc_trunc_decompress(_dtype_id(dtype), n, _ptr(b), k, _ptr(x))
+    if rc != 0:
+        raise ValueError(f"orc_trunc_decompress failed ({rc})")
+    return x

@@ -28,7 +28,8 @@
 
 using namespace sz3g;
 
-uint64_t sz3g_huffman_launch_count_internal();   // huffman.cu
+uint64_t sz3g_huffman_launch_count_internal();      // huffman.cu
+uint64_t sz3g_truncation_launch_count_internal();   // truncation.cu
 
 namespace {
 
@@ -1247,7 +1248,9 @@ int sz3g_uses_tma(const sz3g_grid* grid, int decompress) {
   return decompress ? (xin && cod) : xin;
 }
 
-uint64_t sz3g_launch_count(void) { return g_launches.load() + sz3g_huffman_launch_count_internal(); }
+uint64_t sz3g_launch_count(void) {
+  return g_launches.load() + sz3g_huffman_launch_count_internal() + sz3g_truncation_launch_count_internal();
+}
 
 int sz3g_set_tuning(const char* key, int64_t value) {
   if (!key) return SZ3G_EINVAL;

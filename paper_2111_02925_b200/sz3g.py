@@ -82,6 +82,9 @@ def load(allow_build: bool = False):
         lib.sz3g_huffman_codebook.argtypes = [P, U32, U32, P, P, P, P, P, P]
         lib.sz3g_huffman_encode.argtypes = [P, U64, U32, P, U32, P, P, U64, P, P, P]
         lib.sz3g_huffman_decode.argtypes = [P, P, U64, U32, P, U32, P, P, P]
+    if hasattr(lib, "sz3g_truncation_compress"):   # absent only in older A/B builds
+        lib.sz3g_truncation_compress.argtypes = [GP, P, U32, P, P]
+        lib.sz3g_truncation_decompress.argtypes = [GP, P, U32, P, P]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
@@ -96,7 +99,8 @@ def load(allow_build: bool = False):
 EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regression_decompress", "sz3g_histogram",
                     "sz3g_regression_analyze", "sz3g_regression_quantize", "sz3g_huffman_scratch_bytes",
                     "sz3g_huffman_dtable_bytes", "sz3g_huffman_encode_scratch_bytes", "sz3g_huffman_codebook",
-                    "sz3g_huffman_encode", "sz3g_huffman_decode",
+                    "sz3g_huffman_encode", "sz3g_huffman_decode", "sz3g_truncation_compress",
+                    "sz3g_truncation_decompress",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -486,4 +490,28 @@ def huffman_decode(hs: HuffmanStream, table: HuffmanTable, out: torch.Tensor | N
         status = hs.status
     _check(lib.sz3g_huffman_decode(_ptr(hs.payload), _ptr(hs.offsets), hs.n, hs.chunk, _ptr(table.dtable),
                                    table.max_len, _ptr(out), _ptr(status), _stream(stream)), "sz3g_huffman_decode")
+    return out
+
+
+# ------------------------------------------------------------------------------------------- Truncation
+def truncation_compress(x: torch.Tensor, k: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sz3g_truncation_compress: the k most-significant bytes of every element (uint8 [n * k])."""
+    _require_cuda(x, out)
+    if out is None:
+        out = torch.empty(x.numel() * k, dtype=torch.uint8, device=x.device)
+    g = make_grid((x.numel(),), x.dtype)
+    _check(load().sz3g_truncation_compress(ctypes.byref(g), _ptr(x), k, _ptr(out), _stream(stream)),
+           "sz3g_truncation_compress")
+    return out
+
+
+def truncation_decompress(b: torch.Tensor, n: int, k: int, dtype: torch.dtype = torch.float32,
+                          out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sz3g_truncation_decompress: zero-fill the discarded bytes."""
+    _require_cuda(b, out)
+    if out is None:
+        out = torch.empty(n, dtype=dtype, device=b.device)
+    g = make_grid((n,), dtype)
+    _check(load().sz3g_truncation_decompress(ctypes.byref(g), _ptr(b), k, _ptr(out), _stream(stream)),
+           "sz3g_truncation_decompress")
     return out
