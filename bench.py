@@ -409,10 +409,20 @@ def main():
     comp_gbs = comp_bytes / (comp_ms * 1e-3) / 1e9
     value = N_global * s / (ms_step * 1e-3) / 1e9
 
+    # ---------------- reconstruction quality (NEXT-3 metrics): bound check, max error, PSNR
+    st = sz3g.error_stats(x, out, res.eb_abs).cpu().tolist()
+    lo, hi = (float(v) for v in bufs.minmax.cpu())
+    quality = {"max_abs_err": st[0], "eb_abs": res.eb_abs, "above_eb": int(st[2]),
+               "psnr_db": sz3g.psnr(hi - lo, st[1] / N_local)}
+    if st[2] != 0 or not st[0] <= res.eb_abs:
+        raise RuntimeError(f"error bound violated: {quality}")
+
     # ---------------- encoder stage (NEXT-1): codebook from the merged histogram, encode, decode
     huff = None
     if not args.no_huffman:
         huff = huffman_leg(sz3g, bufs, res, N_local, NB_local, s, args, world, peaks, stream)
+        quality["bit_rate"] = sz3g.bit_rate(8 * s, huff["compression_ratio"])
+        quality["compression_ratio"] = huff["compression_ratio"]
 
     # ---------------- SZ3-Truncation (NEXT-2) on the same field
     trunc = None
@@ -496,7 +506,7 @@ def main():
                                  "frac": ana_bytes / (ana_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                                  "ms_per_step": ana_ms},
             "path": args.path,
-            "huffman": huff, "truncation": trunc,
+            "quality": quality, "huffman": huff, "truncation": trunc,
             "outliers": n_out, "eb_abs": res.eb_abs,
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -225,6 +225,19 @@ int sz3g_truncation_compress(const sz3g_grid* grid, const void* x, uint32_t k, u
 int sz3g_truncation_decompress(const sz3g_grid* grid, const uint8_t* in, uint32_t k, void* x_out,
                                sz3g_stream_t stream);
 
+/* ---- Distortion metrics of a reconstruction (NEXT-3): "The bit rate equals bits/cr
+ * ... PSNR is inversely proportional to the mean square error of decompress data and original data
+ * in logarithmic scale"; SPEC S:545 PSNR = 20 log10(range) - 10 log10(MSE).
+ * sz3g_error_stats: one read of x and y (same grid) ->
+ *   d_out  device double[3] <- {max |x - y|, sum (x - y)^2, #elements with |x - y| > eb}, fp64;
+ *          elements whose x and y are bitwise identical contribute 0 (preserved NaN / Inf), a NaN
+ *          difference makes the max NaN and counts as above eb.  Deterministic (fixed reduction order).
+ *   scratch sz3g_error_stats_scratch_bytes(n) bytes of device memory.  2 launches.
+ * MSE = sum / n; PSNR and the bit rate (bits / ratio) are formed by the caller.                */
+uint64_t sz3g_error_stats_scratch_bytes(uint64_t n);
+int sz3g_error_stats(const sz3g_grid* grid, const void* x, const void* y, double eb, double* d_out,
+                     void* scratch, sz3g_stream_t stream);
+
 /* Performance tuning only (no call changes a result): set knob `key` ("CHUNK_C", "CHUNK_D", "CCFG",
  * "PF"; defaults are the measured best, environment SZ3G_<KEY> overrides them) for
  * launches issued after the call.  Process-global, not thread-safe against concurrent launches.

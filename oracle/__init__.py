@@ -280,3 +280,31 @@ def trunc_decompress(b: np.ndarray, n: int, k: int, dtype) -> np.ndarray:
     if rc != 0:
         raise ValueError(f"orc_trunc_decompress failed ({rc})")
     return x
+
+
+# ------------------------------------------------------------------------------------------- metrics
+# Distortion metrics (DEFINITION.md M1-M3).
+def error_stats(x: np.ndarray, y: np.ndarray, eb: float = float("inf")) -> tuple[float, float, int]:
+    """M1: (max |x - y|, sum (x - y)^2, #(|x - y| > eb)) in fp64; bitwise-identical pairs contribute 0."""
+    x = np.ascontiguousarray(x).reshape(-1)
+    y = np.ascontiguousarray(y).reshape(-1)
+    if x.size == 0:
+        return 0.0, 0.0, 0
+    same = x.view(np.uint8).reshape(x.size, -1) == y.view(np.uint8).reshape(y.size, -1)
+    diff = np.where(same.all(axis=1), 0.0, x.astype(np.float64) - y.astype(np.float64))
+    ad = np.abs(diff)
+    mx = float(np.nan) if np.isnan(ad).any() else float(ad.max(initial=0.0))
+    return mx, float(np.sum(diff * diff)), int(np.sum((ad > eb) | np.isnan(ad)))
+
+
+def psnr(value_range: float, mse: float) -> float:
+    """M2: 20 log10(range) - 10 log10(MSE); +inf for MSE = 0."""
+    import math
+    if mse == 0:
+        return math.inf
+    return 20.0 * math.log10(value_range) - 10.0 * math.log10(mse)
+
+
+def bit_rate(bits_per_sample: int, ratio: float) -> float:
+    """M3: bits / cr."""
+    return bits_per_sample / ratio

@@ -85,6 +85,10 @@ def load(allow_build: bool = False):
     if hasattr(lib, "sz3g_truncation_compress"):   # absent only in older A/B builds
         lib.sz3g_truncation_compress.argtypes = [GP, P, U32, P, P]
         lib.sz3g_truncation_decompress.argtypes = [GP, P, U32, P, P]
+    if hasattr(lib, "sz3g_error_stats"):   # absent only in older A/B builds
+        lib.sz3g_error_stats_scratch_bytes.argtypes = [U64]
+        lib.sz3g_error_stats_scratch_bytes.restype = U64
+        lib.sz3g_error_stats.argtypes = [GP, P, P, D, P, P, P]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
@@ -100,7 +104,7 @@ EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regres
                     "sz3g_regression_analyze", "sz3g_regression_quantize", "sz3g_huffman_scratch_bytes",
                     "sz3g_huffman_dtable_bytes", "sz3g_huffman_encode_scratch_bytes", "sz3g_huffman_codebook",
                     "sz3g_huffman_encode", "sz3g_huffman_decode", "sz3g_truncation_compress",
-                    "sz3g_truncation_decompress",
+                    "sz3g_truncation_decompress", "sz3g_error_stats_scratch_bytes", "sz3g_error_stats",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -515,3 +519,30 @@ def truncation_decompress(b: torch.Tensor, n: int, k: int, dtype: torch.dtype = 
     _check(load().sz3g_truncation_decompress(ctypes.byref(g), _ptr(b), k, _ptr(out), _stream(stream)),
            "sz3g_truncation_decompress")
     return out
+
+
+# ------------------------------------------------------------------------------------------- metrics
+def error_stats(x: torch.Tensor, y: torch.Tensor, eb: float = float("inf"), stream=None) -> torch.Tensor:
+    """sz3g_error_stats: device double[3] {max |x - y|, sum (x - y)^2, #(|x - y| > eb)} (asynchronous)."""
+    _require_cuda(x, y)
+    if x.shape != y.shape or x.dtype != y.dtype:
+        raise SZ3GError("error_stats: x and y must have the same shape and dtype")
+    lib = load()
+    out = torch.empty(3, dtype=torch.float64, device=x.device)
+    scratch = torch.empty(int(lib.sz3g_error_stats_scratch_bytes(x.numel())), dtype=torch.uint8, device=x.device)
+    g = make_grid((x.numel(),), x.dtype)
+    _check(lib.sz3g_error_stats(ctypes.byref(g), _ptr(x), _ptr(y), float(eb), _ptr(out), _ptr(scratch),
+                                _stream(stream)), "sz3g_error_stats")
+    out._scratch = scratch
+    return out
+
+
+def psnr(value_range: float, mse: float) -> float:
+    """20 log10(range) - 10 log10(MSE); +inf when MSE = 0 ("infinity PSNR")."""
+    import math
+    return math.inf if mse == 0 else 20 * math.log10(value_range) - 10 * math.log10(mse)
+
+
+def bit_rate(bits_per_sample: int, ratio: float) -> float:
+    """bits / cr."""
+    return bits_per_sample / ratio
