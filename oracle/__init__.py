@@ -73,6 +73,9 @@ def _load():
             lib.orc_huffman_decode.argtypes = [P, P, U64, U32, P, P, U32, P]
             lib.orc_trunc_compress.argtypes = [I32, U64, P, U32, P]
             lib.orc_trunc_decompress.argtypes = [I32, U64, P, U32, P]
+            lib.orc_coef_delta_encode.argtypes = [P, U64, P, P, U64]
+            lib.orc_coef_delta_encode.restype = U64
+            lib.orc_coef_delta_decode.argtypes = [P, U64, P, U64, P]
             _lib = lib
     return _lib
 
@@ -308,3 +311,28 @@ def psnr(value_range: float, mse: float) -> float:
 def bit_rate(bits_per_sample: int, ratio: float) -> float:
     """M3: bits / cr (P:525)."""
     return bits_per_sample / ratio
+
+
+# ------------------------------------------------------------------------------------------- coefficient deltas
+# NEXT-3 coefficient-code delta coding (DEFINITION.md C1-C2, truncation_oracle.cpp).
+COEF_ESC = 65535
+
+
+def coef_delta_encode(coef: np.ndarray):
+    """C1: (sym uint16 [4 * nb] channel-major, escapes uint64 in position order)."""
+    c = np.ascontiguousarray(coef, dtype=np.int32).reshape(-1, 4)
+    nb = c.shape[0]
+    sym = np.zeros(4 * nb, np.uint16)
+    esc = np.zeros(4 * nb, np.uint64)
+    ne = _load().orc_coef_delta_encode(_ptr(c), nb, _ptr(sym), _ptr(esc), esc.size)
+    return sym, esc[:ne].copy()
+
+
+def coef_delta_decode(sym: np.ndarray, nb: int, esc: np.ndarray) -> np.ndarray:
+    """C2: back to int32 [nb, 4]."""
+    sym = np.ascontiguousarray(sym, dtype=np.uint16)
+    esc = np.ascontiguousarray(esc, dtype=np.uint64)
+    c = np.zeros((nb, 4), np.int32)
+    if _load().orc_coef_delta_decode(_ptr(sym), nb, _ptr(esc), esc.size, _ptr(c)) != 0:
+        raise ValueError("escapes exhausted")
+    return c

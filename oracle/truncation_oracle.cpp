@@ -42,3 +42,56 @@ int orc_trunc_decompress(int dtype, uint64_t n, const uint8_t* in, uint32_t k, v
 }
 
 }  // extern "C"
+
+// =====================================================================================
+//  Coefficient-code delta coding (NEXT-3; DEFINITION.md C1-C2, reading G25).  The G1 coefficient codes
+//  are independent per block; their storage is reduced by integer differencing along the block order
+//  (per channel), a zigzag map to unsigned values, and an escape for values >= 65535, so that the
+//  symbols fit the Huffman coder of the quantisation codes ("Coefficient Compression" is an
+//  empty heading; S:225-233 codes coefficient deltas).  Plain loops.
+// =====================================================================================
+extern "C" {
+
+// C1: coef[nb][4] (int32) -> sym[4][nb] (uint16, channel-major), escapes in position order.
+// Returns the number of escapes (written up to esc_cap).
+uint64_t orc_coef_delta_encode(const int32_t* coef, uint64_t nb, uint16_t* sym, uint64_t* esc, uint64_t esc_cap) {
+  uint64_t ne = 0;
+  for (int ch = 0; ch < 4; ch++) {
+    int64_t prev = 0;
+    for (uint64_t b = 0; b < nb; b++) {
+      const int64_t v = coef[4 * b + ch];
+      const int64_t d = v - prev;
+      prev = v;
+      const uint64_t z = d >= 0 ? (uint64_t)d * 2 : (uint64_t)(-(d + 1)) * 2 + 1;   // zigzag
+      if (z >= 65535) {
+        sym[ch * nb + b] = 65535;
+        if (ne < esc_cap) esc[ne] = z;
+        ne++;
+      } else {
+        sym[ch * nb + b] = (uint16_t)z;
+      }
+    }
+  }
+  return ne;
+}
+
+// C2: the inverse.  Returns 0, or -1 if the escapes run out.
+int orc_coef_delta_decode(const uint16_t* sym, uint64_t nb, const uint64_t* esc, uint64_t nesc, int32_t* coef) {
+  uint64_t k = 0;
+  for (int ch = 0; ch < 4; ch++) {
+    int64_t acc = 0;
+    for (uint64_t b = 0; b < nb; b++) {
+      uint64_t z = sym[ch * nb + b];
+      if (z == 65535) {
+        if (k >= nesc) return -1;
+        z = esc[k++];
+      }
+      const int64_t d = (z & 1) ? -(int64_t)(z >> 1) - 1 : (int64_t)(z >> 1);
+      acc += d;
+      coef[4 * b + ch] = (int32_t)acc;
+    }
+  }
+  return 0;
+}
+
+}  // extern "C"
