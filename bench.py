@@ -266,11 +266,15 @@ def huffman_leg(sz3g, bufs, res, N_local, NB_local, s, args, world, peaks, strea
     enc_bytes = 2 * n + pay_b + 8 * (nch + 1)
     dec_bytes = pay_b + 8 * (nch + 1) + 2 * n
     n_out = res.n_outliers
-    stored = pay_b + 8 * (nch + 1) + 16 * NB_local + (8 + s) * n_out + table.lengths.numel()
+    cstream = sz3g.encode_coefficients(bufs.coef_codes)
+    coef_b = cstream.nbytes()
+    stored = pay_b + 8 * (nch + 1) + coef_b + (8 + s) * n_out + table.stored_bytes()
     return {
         "bits_per_code": 8 * pay_b / n, "payload_bytes": pay_b, "chunk": hs.chunk, "max_len": table.max_len,
         "compression_ratio": N_local * s / stored,
-        "ratio_note": "input bytes / (payload + chunk offsets + int32 coefficient codes + outliers + code lengths)",
+        "coefficient_bytes": coef_b, "coefficient_bytes_raw": 16 * NB_local,
+        "ratio_note": "input bytes / (payload + chunk offsets + delta+Huffman-coded coefficient codes + outliers + "
+                      "canonical codebook)",
         "codebook_ms": cb_ms, "encode_ms": en_ms, "decode_ms": de_ms,
         "encode_gbs_input": N_local * s / (en_ms * 1e-3) / 1e9,
         "encode_roofline": {"achieved": enc_bytes / (en_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],

@@ -238,6 +238,22 @@ uint64_t sz3g_error_stats_scratch_bytes(uint64_t n);
 int sz3g_error_stats(const sz3g_grid* grid, const void* x, const void* y, double eb, double* d_out,
                      void* scratch, sz3g_stream_t stream);
 
+/* ---- Coefficient-code delta coding (NEXT-3), reading G25 of the empty "Coefficient Compression"
+ * heading; definition oracle/DEFINITION.md C1-C2.
+ * sz3g_coef_delta_encode: coef [nb][4] int32 (sz3g_regression_compress output) ->
+ *   sym      out  4 * nb uint16, channel-major [c][block]: zigzag(coef[b][c] - coef[b-1][c]) clipped
+ *                 to 65535 (escape); Huffman-code them with their own histogram (R = 32768 bins).
+ *   escapes  out  the full zigzag values of the escaped positions, in position order (up to esc_cap).
+ *   d_nesc   out  device uint64: the number of escapes.
+ *   scratch  in   sz3g_coef_delta_scratch_bytes(nb) bytes.  3 launches.
+ * sz3g_coef_delta_decode: the inverse (running sums per channel); too few escapes set
+ *   SZ3G_STATUS_BAD_HUFFMAN in *d_status.  5 launches.                                          */
+uint64_t sz3g_coef_delta_scratch_bytes(uint64_t nb);
+int sz3g_coef_delta_encode(const int32_t* coef, uint64_t nb, uint16_t* sym, uint64_t* escapes,
+                           uint64_t esc_cap, uint64_t* d_nesc, void* scratch, sz3g_stream_t stream);
+int sz3g_coef_delta_decode(const uint16_t* sym, uint64_t nb, const uint64_t* escapes, uint64_t nesc,
+                           int32_t* coef, void* scratch, int32_t* d_status, sz3g_stream_t stream);
+
 /* Performance tuning only (no call changes a result): set knob `key` ("CHUNK_C", "CHUNK_D", "CCFG",
  * "PF"; defaults are the measured best, environment SZ3G_<KEY> overrides them) for
  * launches issued after the call.  Process-global, not thread-safe against concurrent launches.

@@ -31,6 +31,7 @@ using namespace sz3g;
 uint64_t sz3g_huffman_launch_count_internal();      // huffman.cu
 uint64_t sz3g_truncation_launch_count_internal();   // truncation.cu
 uint64_t sz3g_metrics_launch_count_internal();      // metrics.cu
+uint64_t sz3g_coefcode_launch_count_internal();     // coefcode.cu
 
 namespace {
 
@@ -1251,7 +1252,7 @@ int sz3g_uses_tma(const sz3g_grid* grid, int decompress) {
 
 uint64_t sz3g_launch_count(void) {
   return g_launches.load() + sz3g_huffman_launch_count_internal() + sz3g_truncation_launch_count_internal() +
-         sz3g_metrics_launch_count_internal();
+         sz3g_metrics_launch_count_internal() + sz3g_coefcode_launch_count_internal();
 }
 
 int sz3g_set_tuning(const char* key, int64_t value) {

@@ -89,6 +89,11 @@ def load(allow_build: bool = False):
         lib.sz3g_error_stats_scratch_bytes.argtypes = [U64]
         lib.sz3g_error_stats_scratch_bytes.restype = U64
         lib.sz3g_error_stats.argtypes = [GP, P, P, D, P, P, P]
+    if hasattr(lib, "sz3g_coef_delta_encode"):   # absent only in older A/B builds
+        lib.sz3g_coef_delta_scratch_bytes.argtypes = [U64]
+        lib.sz3g_coef_delta_scratch_bytes.restype = U64
+        lib.sz3g_coef_delta_encode.argtypes = [P, U64, P, P, U64, P, P, P]
+        lib.sz3g_coef_delta_decode.argtypes = [P, U64, P, U64, P, P, P, P]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
@@ -105,6 +110,7 @@ EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regres
                     "sz3g_huffman_dtable_bytes", "sz3g_huffman_encode_scratch_bytes", "sz3g_huffman_codebook",
                     "sz3g_huffman_encode", "sz3g_huffman_decode", "sz3g_truncation_compress",
                     "sz3g_truncation_decompress", "sz3g_error_stats_scratch_bytes", "sz3g_error_stats",
+                    "sz3g_coef_delta_scratch_bytes", "sz3g_coef_delta_encode", "sz3g_coef_delta_decode",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -412,6 +418,11 @@ class HuffmanTable:
     max_len: int
     status: torch.Tensor      # int32 [1]
 
+    def stored_bytes(self) -> int:
+        """A canonical code is rebuilt from its lengths alone (H3): 4 + 3 bytes per active symbol
+        (u32 count, then u16 symbol + u8 length pairs)."""
+        return 4 + 3 * int((self.lengths > 0).sum().item())
+
     def check(self) -> "HuffmanTable":
         if int(self.status.item()) & STATUS_BAD_HUFFMAN:
             raise SZ3GError("Huffman codebook: empty histogram, bad count, or too many symbols for max_len")
@@ -546,3 +557,71 @@ def psnr(value_range: float, mse: float) -> float:
 def bit_rate(bits_per_sample: int, ratio: float) -> float:
     """P:525: bits / cr."""
     return bits_per_sample / ratio
+
+
+# ------------------------------------------------------------------------------------------- coefficient codes
+COEF_ESC = 65535
+
+
+@dataclass
+class CoefStream:
+    nb: int
+    table: HuffmanTable       # codebook of the delta symbols
+    stream: HuffmanStream     # Huffman-coded symbols (4 * nb)
+    escapes: torch.Tensor     # int64 (uint64 bits) [n_escapes]
+
+    def nbytes(self) -> int:
+        return 4 * self.stream.words() + 8 * self.stream.offsets.numel() + 8 * self.escapes.numel() + \
+            self.table.stored_bytes()
+
+
+def coef_delta_encode(coef_codes: torch.Tensor, stream=None):
+    """sz3g_coef_delta_encode -> (sym uint16 [4 nb], escapes int64 [n], device count) (asynchronous)."""
+    _require_cuda(coef_codes)
+    lib = load()
+    nb = coef_codes.numel() // 4
+    dev = coef_codes.device
+    sym = torch.empty(4 * nb, dtype=torch.uint16, device=dev)
+    esc = torch.empty(max(1, 4 * nb // 64), dtype=torch.int64, device=dev)
+    nesc = torch.zeros(1, dtype=torch.int64, device=dev)
+    scratch = torch.empty(int(lib.sz3g_coef_delta_scratch_bytes(nb)), dtype=torch.uint8, device=dev)
+    _check(lib.sz3g_coef_delta_encode(_ptr(coef_codes), nb, _ptr(sym), _ptr(esc), esc.numel(), _ptr(nesc),
+                                      _ptr(scratch), _stream(stream)), "sz3g_coef_delta_encode")
+    n = int(nesc.item())
+    if n > esc.numel():   # rare: more escapes than the first guess -> once more with room for all
+        esc = torch.empty(n, dtype=torch.int64, device=dev)
+        _check(lib.sz3g_coef_delta_encode(_ptr(coef_codes), nb, _ptr(sym), _ptr(esc), esc.numel(), _ptr(nesc),
+                                          _ptr(scratch), _stream(stream)), "sz3g_coef_delta_encode")
+    return sym, esc[:n]
+
+
+def coef_delta_decode(sym: torch.Tensor, nb: int, escapes: torch.Tensor, out: torch.Tensor | None = None,
+                      status: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sz3g_coef_delta_decode -> int32 [nb, 4]."""
+    _require_cuda(sym, escapes, out, status)
+    lib = load()
+    dev = sym.device
+    if out is None:
+        out = torch.empty((nb, 4), dtype=torch.int32, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    scratch = torch.empty(int(lib.sz3g_coef_delta_scratch_bytes(nb)), dtype=torch.uint8, device=dev)
+    _check(lib.sz3g_coef_delta_decode(_ptr(sym), nb, _ptr(escapes if escapes.numel() else None), escapes.numel(),
+                                      _ptr(out), _ptr(scratch), _ptr(status), _stream(stream)),
+           "sz3g_coef_delta_decode")
+    out._scratch = scratch
+    return out
+
+
+def encode_coefficients(coef_codes: torch.Tensor, stream=None) -> CoefStream:
+    """Coefficient codes -> delta symbols -> their histogram -> Huffman codebook -> encoded stream."""
+    nb = coef_codes.numel() // 4
+    sym, esc = coef_delta_encode(coef_codes, stream)
+    hist = histogram(sym, 32768, stream=stream)
+    table = huffman_codebook(hist, stream=stream)
+    return CoefStream(nb, table, huffman_encode(sym, table, stream=stream), esc)
+
+
+def decode_coefficients(cs: CoefStream, stream=None) -> torch.Tensor:
+    sym = huffman_decode(cs.stream, cs.table, stream=stream)
+    return coef_delta_decode(sym, cs.nb, cs.escapes, stream=stream)
