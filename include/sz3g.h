@@ -42,6 +42,8 @@ typedef struct CUstream_st* sz3g_stream_t; /* == cudaStream_t */
 #define SZ3G_EUNSUPPORTED (-2) /* dtype / block_size / ndim not supported by the device path     */
 #define SZ3G_ERANGE       (-3) /* radius outside [1, 32768] (codes must fit uint16)             */
 #define SZ3G_ECUDA        (-4) /* a CUDA launch / driver call failed (see sz3g_last_cuda_error) */
+#define SZ3G_ECORRUPT     (-5) /* a compressed stream failed validation (magic, version, length,
+                                  section checksum)                                              */
 
 /* ---- device status bits (written with atomicOr into *d_status; caller zeroes it first) */
 #define SZ3G_STATUS_OUTLIER_OVERFLOW 0x1u /* *d_outlier_count > outlier_cap: retry, larger cap */
@@ -197,7 +199,13 @@ uint64_t sz3g_launch_count(void);
  * sz3g_huffman_decode -- the inverse: n codes from payload / chunk_offsets with the dtable of the
  *   same codebook (codes and payload 16-byte aligned); a corrupt stream sets BAD_HUFFMAN.
  *   1 launch.                                                                                  */
+/* sz3g_huffman_codebook_from_lengths -- the same codewords and dtable from stored lengths alone (a
+ *   canonical code is defined by its lengths, H3): lengths must be <= max_len with Kraft sum <= 1 and
+ *   at least one symbol, else BAD_HUFFMAN.  lengths is read, not written.  1 launch.            */
 uint64_t sz3g_huffman_scratch_bytes(uint32_t nsym, uint32_t max_len);
+int sz3g_huffman_codebook_from_lengths(const uint8_t* lengths, uint32_t nsym, uint32_t max_len,
+                                       uint32_t* codewords, void* dtable, int32_t* d_status,
+                                       sz3g_stream_t stream);
 uint64_t sz3g_huffman_dtable_bytes(uint32_t nsym);
 uint64_t sz3g_huffman_encode_scratch_bytes(uint64_t n, uint32_t chunk);
 int sz3g_huffman_codebook(const int64_t* hist, uint32_t nsym, uint32_t max_len, uint8_t* lengths,
@@ -253,6 +261,44 @@ int sz3g_coef_delta_encode(const int32_t* coef, uint64_t nb, uint16_t* sym, uint
                            uint64_t esc_cap, uint64_t* d_nesc, void* scratch, sz3g_stream_t stream);
 int sz3g_coef_delta_decode(const uint16_t* sym, uint64_t nb, const uint64_t* escapes, uint64_t nesc,
                            int32_t* coef, void* scratch, int32_t* d_status, sz3g_stream_t stream);
+
+/* ---- Self-describing compressed stream (NEXT-3): "magic ..., version u16, ... each inner
+ * section: tag u8, length u64, payload".  HOST code and HOST buffers only.  Layout (little-endian):
+ * "SZ3G" | version u16 (1) | 96-byte header | nsec u32 | nsec x {tag u8 | length u64 | FNV-1a-64 of
+ * the payload u64 | payload}.  Reading checks magic, version, every length and checksum and returns
+ * SZ3G_ECORRUPT (with the failing section's tag in *bad_tag) on any mismatch; the returned sections
+ * point into the input buffer.  Section tags used by the Python layer: SZ3G_SEC_*.             */
+typedef struct {
+  sz3g_dtype   dtype;
+  uint32_t     ndim;
+  uint64_t     dims[3];
+  sz3g_eb_mode eb_mode;
+  double       eb;          /* as given (absolute, or relative to the value range)            */
+  double       eb_abs;      /* the absolute bound used                                         */
+  uint32_t     radius, block_size, chunk, max_len, flags;
+  uint64_t     n_outliers, nblocks;
+} sz3g_stream_header;
+typedef struct {
+  uint32_t    tag;
+  const void* data;         /* host */
+  uint64_t    bytes;
+} sz3g_section;
+enum {
+  SZ3G_SEC_CODE_BOOK = 1,   /* canonical codebook of the element codes: u32 n, n x (u16 sym, u8 len) */
+  SZ3G_SEC_CODE_OFFS = 2,   /* chunk word offsets, u64 x (nchunks + 1)                                */
+  SZ3G_SEC_CODE_DATA = 3,   /* Huffman payload words of the element codes                             */
+  SZ3G_SEC_COEF_BOOK = 4,   /* codebook of the coefficient delta symbols                              */
+  SZ3G_SEC_COEF_OFFS = 5,
+  SZ3G_SEC_COEF_DATA = 6,
+  SZ3G_SEC_COEF_ESC = 7,    /* coefficient escapes, u64 zigzag values in position order               */
+  SZ3G_SEC_OUT_IDX = 8,     /* outlier global indices, u64                                            */
+  SZ3G_SEC_OUT_VAL = 9      /* outlier values, T                                                      */
+};
+uint64_t sz3g_stream_size(const sz3g_section* sections, uint32_t nsec);
+int sz3g_stream_write(const sz3g_stream_header* hdr, const sz3g_section* sections, uint32_t nsec,
+                      void* out, uint64_t cap, uint64_t* written);
+int sz3g_stream_read(const void* in, uint64_t len, sz3g_stream_header* hdr, sz3g_section* sections,
+                     uint32_t sec_cap, uint32_t* nsec, uint32_t* bad_tag);
 
 /* Performance tuning only (no call changes a result): set knob `key` ("CHUNK_C", "CHUNK_D", "CCFG",
  * "PF"; defaults are the measured best, environment SZ3G_<KEY> overrides them) for

@@ -122,10 +122,38 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
   const int tid = threadIdx.x;
   const CbScratch S = cb_carve(scratch, nsym);
   if (tid == 0) { s_bad = 0; s_bits = 0; }
-  for (uint32_t s = tid; s < nsym; s += HF_THREADS) { lens[s] = 0; cws[s] = 0; }
+  const bool from_len = hist == nullptr;   // lengths given (a stored canonical codebook): (F) and (G) only
+  for (uint32_t s = tid; s < nsym; s += HF_THREADS) {
+    if (!from_len) lens[s] = 0;
+    cws[s] = 0;
+  }
   for (uint32_t i = tid; i < (1u << HF_LUT_BITS); i += HF_THREADS) dt->lut[i] = 0;
   if (tid < HF_MAXL) { dt->first[tid] = 0; dt->count[tid] = 0; dt->base[tid] = 0; }
+  if (tid <= HF_MAXL) s_blc[tid] = 0;
   __syncthreads();
+  if (from_len) {
+    // validate: every length <= max_len, at least one symbol, Kraft sum <= 1 (sum 2^(max_len - L) <= 2^max_len)
+    __shared__ unsigned long long s_kraft;
+    if (tid == 0) s_kraft = 0;
+    __syncthreads();
+    unsigned long long kr = 0;
+    for (uint32_t s = tid; s < nsym; s += HF_THREADS) {
+      const uint32_t L = lens[s];
+      if (L > max_len) atomicOr(&s_bad, 1u);
+      else if (L) {
+        kr += 1ull << (max_len - L);
+        atomicAdd(&s_blc[L], 1u);
+      }
+    }
+    atomicAdd(&s_kraft, kr);
+    __syncthreads();
+    uint32_t nact = 0;
+    for (int L = 1; L <= HF_MAXL; L++) nact += s_blc[L];
+    if (s_bad || nact == 0 || s_kraft > (1ull << max_len)) {
+      if (tid == 0) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
+      return;
+    }
+  } else {
 
   // (A) compact active symbols, in symbol order: key = (count << 16) | symbol
   const uint32_t per = (nsym + HF_THREADS - 1) / HF_THREADS;
@@ -251,7 +279,6 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
       m = 2 * (m - c);
     }
   }
-  if (tid <= HF_MAXL) s_blc[tid] = 0;
   __syncthreads();
   // (E) lengths of the sorted leaves: len(i) = #{l : i < c[l]}
   for (uint32_t i = tid; i < n; i += HF_THREADS) {
@@ -260,6 +287,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     lens[(uint32_t)(src[i] & 0xffffu)] = (uint8_t)L;
     atomicAdd(&s_blc[L], 1u);
   }
+  }   // !from_len
   __syncthreads();
   // (F) canonical codewords: first code per length (DEFLATE form of H3), then per-symbol rank
   // among the symbols of its length in symbol order
@@ -746,6 +774,19 @@ uint64_t sz3g_huffman_dtable_bytes(uint32_t nsym) { return dtable_bytes(nsym); }
 uint64_t sz3g_huffman_encode_scratch_bytes(uint64_t n, uint32_t chunk) {
   const uint64_t nch = chunk ? (n + chunk - 1) / chunk : 0;
   return 8 * ((nch + SCAN_TILE - 1) / SCAN_TILE + 2);
+}
+
+int sz3g_huffman_codebook_from_lengths(const uint8_t* lengths, uint32_t nsym, uint32_t max_len,
+                                       uint32_t* codewords, void* dtable, int32_t* d_status,
+                                       sz3g_stream_t stream) {
+  if (!lengths || !codewords || !dtable || !d_status) return SZ3G_EINVAL;
+  if (nsym < 1 || nsym > 65536) return SZ3G_ERANGE;
+  if (max_len < 1 || max_len > HF_MAX_LEN_LIMIT) return SZ3G_ERANGE;
+  if (reinterpret_cast<uintptr_t>(dtable) & 15) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_huff_codebook<<<1, HF_THREADS, 0, st>>>(nullptr, nsym, max_len, const_cast<uint8_t*>(lengths), codewords,
+                                            reinterpret_cast<DTab*>(dtable), nullptr, d_status);
+  return hf_check(1);
 }
 
 int sz3g_huffman_codebook(const int64_t* hist, uint32_t nsym, uint32_t max_len, uint8_t* lengths,

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) k_trunc_compress(const uint8_t* __restric
 #pragma unroll
       for (int t = 0; t < 4; t++) {
         const int word = 4 * q + t;   // 32-bit word index inside the group
-        if (S == 4) v[word] = (W)w4[t];
+        if constexpr (S == 4) v[word] = (W)w4[t];
         else if (word & 1) v[word >> 1] |= (W)w4[t] << 32;
         else v[word >> 1] = (W)w4[t];
       }

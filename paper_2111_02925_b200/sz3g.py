@@ -24,7 +24,7 @@ STATUS_OUTLIER_OVERFLOW, STATUS_BAD_RANGE = 0x1, 0x2
 STATUS_BAD_HUFFMAN = 0x4
 STATUS_PAYLOAD_OVERFLOW = 0x8
 BLOCK = 6
-_ERR = {0: "ok", -1: "EINVAL", -2: "EUNSUPPORTED", -3: "ERANGE", -4: "ECUDA"}
+_ERR = {0: "ok", -1: "EINVAL", -2: "EUNSUPPORTED", -3: "ERANGE", -4: "ECUDA", -5: "ECORRUPT"}
 
 
 class SZ3GError(RuntimeError):
@@ -39,6 +39,22 @@ class Grid(ctypes.Structure):
 class Params(ctypes.Structure):
     _fields_ = [("block_size", ctypes.c_uint32), ("radius", ctypes.c_uint32), ("eb_mode", ctypes.c_int),
                 ("eb", ctypes.c_double), ("flags", ctypes.c_uint32)]
+
+
+class StreamHeader(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int), ("ndim", ctypes.c_uint32), ("dims", ctypes.c_uint64 * 3),
+                ("eb_mode", ctypes.c_int), ("eb", ctypes.c_double), ("eb_abs", ctypes.c_double),
+                ("radius", ctypes.c_uint32), ("block_size", ctypes.c_uint32), ("chunk", ctypes.c_uint32),
+                ("max_len", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("n_outliers", ctypes.c_uint64),
+                ("nblocks", ctypes.c_uint64)]
+
+
+class Section(ctypes.Structure):
+    _fields_ = [("tag", ctypes.c_uint32), ("data", ctypes.c_void_p), ("bytes", ctypes.c_uint64)]
+
+
+SEC_CODE_BOOK, SEC_CODE_OFFS, SEC_CODE_DATA, SEC_COEF_BOOK, SEC_COEF_OFFS, SEC_COEF_DATA, SEC_COEF_ESC, \
+    SEC_OUT_IDX, SEC_OUT_VAL = range(1, 10)
 
 
 _lib = None
@@ -94,6 +110,14 @@ def load(allow_build: bool = False):
         lib.sz3g_coef_delta_scratch_bytes.restype = U64
         lib.sz3g_coef_delta_encode.argtypes = [P, U64, P, P, U64, P, P, P]
         lib.sz3g_coef_delta_decode.argtypes = [P, U64, P, U64, P, P, P, P]
+    if hasattr(lib, "sz3g_stream_write"):   # absent only in older A/B builds
+        lib.sz3g_huffman_codebook_from_lengths.argtypes = [P, U32, U32, P, P, P, P]
+        lib.sz3g_stream_size.argtypes = [ctypes.POINTER(Section), U32]
+        lib.sz3g_stream_size.restype = U64
+        lib.sz3g_stream_write.argtypes = [ctypes.POINTER(StreamHeader), ctypes.POINTER(Section), U32, P, U64,
+                                          ctypes.POINTER(U64)]
+        lib.sz3g_stream_read.argtypes = [P, U64, ctypes.POINTER(StreamHeader), ctypes.POINTER(Section), U32,
+                                         ctypes.POINTER(U32), ctypes.POINTER(U32)]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
@@ -111,6 +135,8 @@ EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regres
                     "sz3g_huffman_encode", "sz3g_huffman_decode", "sz3g_truncation_compress",
                     "sz3g_truncation_decompress", "sz3g_error_stats_scratch_bytes", "sz3g_error_stats",
                     "sz3g_coef_delta_scratch_bytes", "sz3g_coef_delta_encode", "sz3g_coef_delta_decode",
+                    "sz3g_huffman_codebook_from_lengths", "sz3g_stream_size", "sz3g_stream_write",
+                    "sz3g_stream_read",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -625,3 +651,121 @@ def encode_coefficients(coef_codes: torch.Tensor, stream=None) -> CoefStream:
 def decode_coefficients(cs: CoefStream, stream=None) -> torch.Tensor:
     sym = huffman_decode(cs.stream, cs.table, stream=stream)
     return coef_delta_decode(sym, cs.nb, cs.escapes, stream=stream)
+
+
+# ------------------------------------------------------------------------------------------- stream container
+def _book_bytes(lengths: torch.Tensor):
+    """Canonical codebook as stored: u32 n, then n x (u16 symbol, u8 length) (host bytes)."""
+    import numpy as np
+    L = lengths.cpu().numpy()
+    sym = np.flatnonzero(L).astype(np.uint16)
+    rec = np.zeros(sym.size, dtype=[("s", "<u2"), ("l", "u1")])
+    rec["s"], rec["l"] = sym, L[sym]
+    return np.uint32(sym.size).tobytes() + rec.tobytes()
+
+
+def _book_lengths(b: bytes, nsym: int, device) -> torch.Tensor:
+    import numpy as np
+    n = int(np.frombuffer(b[:4], np.uint32)[0])
+    rec = np.frombuffer(b[4:4 + 3 * n], dtype=[("s", "<u2"), ("l", "u1")])
+    L = np.zeros(nsym, np.uint8)
+    L[rec["s"]] = rec["l"]
+    return torch.from_numpy(L).to(device)
+
+
+def to_bytes(res: "Compressed", table: HuffmanTable | None = None, hs: HuffmanStream | None = None,
+             coef: CoefStream | None = None, eb: float | None = None, eb_mode: str = "abs") -> bytes:
+    """Serialise a finalized compression result: Huffman-coded codes, delta+Huffman-coded coefficient
+    codes and the outliers, in the self-describing container (sz3g_stream_write).  Missing stages are
+    run here (codebook from res.hist, encode, coefficient coding)."""
+    if res.n_outliers is None:
+        res.finalize()
+    if table is None:
+        table = huffman_codebook(res.hist).check()
+    if hs is None:
+        hs = huffman_encode(res.codes.view(-1), table).check()
+    if coef is None:
+        coef = encode_coefficients(res.coef_codes)
+    n = res.n_outliers
+    host = [
+        (SEC_CODE_BOOK, _book_bytes(table.lengths)),
+        (SEC_CODE_OFFS, hs.offsets.cpu().numpy().tobytes()),
+        (SEC_CODE_DATA, hs.payload[:hs.words()].cpu().numpy().tobytes()),
+        (SEC_COEF_BOOK, _book_bytes(coef.table.lengths)),
+        (SEC_COEF_OFFS, coef.stream.offsets.cpu().numpy().tobytes()),
+        (SEC_COEF_DATA, coef.stream.payload[:coef.stream.words()].cpu().numpy().tobytes()),
+        (SEC_COEF_ESC, coef.escapes.cpu().numpy().tobytes()),
+        (SEC_OUT_IDX, res.outlier_idx[:n].cpu().numpy().tobytes()),
+        (SEC_OUT_VAL, res.outlier_val[:n].cpu().numpy().tobytes()),
+    ]
+    secs = (Section * len(host))()
+    keep = []
+    for i, (tag, b) in enumerate(host):
+        buf = ctypes.create_string_buffer(b, len(b)) if b else None
+        keep.append(buf)
+        secs[i] = Section(tag, ctypes.cast(buf, ctypes.c_void_p) if buf else None, len(b))
+    s3 = _shape3(res.shape)
+    hdr = StreamHeader(_dtype_id(res.dtype), len(res.shape), (ctypes.c_uint64 * 3)(*s3),
+                       {"abs": SZ3G_EB_ABS, "rel": SZ3G_EB_REL_RANGE}[eb_mode],
+                       float(res.eb_abs if eb is None else eb), float(res.eb_abs), res.radius, BLOCK, hs.chunk,
+                       table.max_len, 0, n, res.coef_codes.shape[0])
+    lib = load()
+    size = int(lib.sz3g_stream_size(secs, len(host)))
+    out = ctypes.create_string_buffer(size)
+    wr = ctypes.c_uint64(0)
+    _check(lib.sz3g_stream_write(ctypes.byref(hdr), secs, len(host), out, size, ctypes.byref(wr)),
+           "sz3g_stream_write")
+    return out.raw[:wr.value]
+
+
+def from_bytes(buf: bytes, device=None) -> torch.Tensor:
+    """Parse and validate a container (sz3g_stream_read), then decode on the GPU: codebooks from their
+    lengths, Huffman decode of codes and coefficient symbols, coefficient deltas, regression
+    decompression and the outlier scatter."""
+    import numpy as np
+    lib = load()
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    hdr = StreamHeader()
+    secs = (Section * 16)()
+    nsec, bad = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    rc = lib.sz3g_stream_read(buf, len(buf), ctypes.byref(hdr), secs, 16, ctypes.byref(nsec), ctypes.byref(bad))
+    if rc != 0:
+        raise SZ3GError(f"corrupt stream (section tag {bad.value})" if rc == -5 else f"sz3g_stream_read: {_ERR.get(rc, rc)}")
+    sec = {secs[i].tag: ctypes.string_at(secs[i].data, secs[i].bytes) if secs[i].bytes else b""
+           for i in range(nsec.value)}
+    dtype = {SZ3G_F32: torch.float32, SZ3G_F64: torch.float64}[hdr.dtype]
+    shape = tuple(int(d) for d in hdr.dims)[3 - hdr.ndim:]
+    N = int(np.prod(shape))
+    R, ml, chunk, nb = hdr.radius, hdr.max_len, hdr.chunk, int(hdr.nblocks)
+
+    def table_from(book: bytes, nsym: int) -> HuffmanTable:
+        L = _book_lengths(book, nsym, device)
+        cws = torch.empty(nsym, dtype=torch.int32, device=device)
+        dt = torch.empty(int(lib.sz3g_huffman_dtable_bytes(nsym)), dtype=torch.uint8, device=device)
+        st = torch.zeros(1, dtype=torch.int32, device=device)
+        _check(lib.sz3g_huffman_codebook_from_lengths(_ptr(L), nsym, ml, _ptr(cws), _ptr(dt), _ptr(st),
+                                                      _stream()), "sz3g_huffman_codebook_from_lengths")
+        return HuffmanTable(L, cws, dt, ml, st).check()
+
+    def stream_from(offs: bytes, data: bytes, n: int) -> HuffmanStream:
+        o = torch.from_numpy(np.frombuffer(offs, np.int64).copy()).to(device)
+        p = torch.from_numpy(np.frombuffer(data, np.int32).copy() if data else np.zeros(1, np.int32)).to(device)
+        return HuffmanStream(n, chunk, o, p, torch.zeros(1, dtype=torch.int32, device=device))
+
+    t_codes = table_from(sec[SEC_CODE_BOOK], 2 * R)
+    hs = stream_from(sec[SEC_CODE_OFFS], sec[SEC_CODE_DATA], N)
+    codes = huffman_decode(hs, t_codes).view(shape)
+    t_coef = table_from(sec[SEC_COEF_BOOK], 65536)
+    cs = stream_from(sec[SEC_COEF_OFFS], sec[SEC_COEF_DATA], 4 * nb)
+    esc = torch.from_numpy(np.frombuffer(sec[SEC_COEF_ESC], np.int64).copy()).to(device)
+    coef = coef_delta_decode(huffman_decode(cs, t_coef), nb, esc)
+    oidx = torch.from_numpy(np.frombuffer(sec[SEC_OUT_IDX], np.int64).copy()).to(device)
+    oval = torch.from_numpy(np.frombuffer(sec[SEC_OUT_VAL], np.float32 if dtype == torch.float32 else np.float64)
+                            .copy()).to(device)
+    out = regression_decompress(codes, coef, oidx if oidx.numel() else torch.zeros(1, dtype=torch.int64, device=device),
+                                oval if oval.numel() else torch.zeros(1, dtype=dtype, device=device),
+                                int(hdr.n_outliers), hdr.eb_abs, R, dtype)
+    torch.cuda.synchronize()
+    if int(hs.status.item()) or int(cs.status.item()):
+        raise SZ3GError("corrupt Huffman stream")
+    return out
