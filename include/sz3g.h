@@ -159,6 +159,12 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
 int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* hist,
                    sz3g_stream_t stream);
 
+/* histogram of n uint16 symbols into nbins (<= 65536) int64 bins, ACCUMULATED; the shared-memory
+ * window is [window_lo, window_lo + 8192) -- place it where the symbols' mass is (e.g. 0 for the
+ * zigzag coefficient deltas); symbols >= nbins are ignored.  1 launch.                           */
+int sz3g_histogram_bins(const uint16_t* codes, uint64_t n, uint32_t nbins, uint32_t window_lo,
+                        int64_t* hist, sz3g_stream_t stream);
+
 /* number of regression blocks of a grid: prod ceil(n_d / block_size) (0 on bad input) */
 uint64_t sz3g_num_blocks(const sz3g_grid* grid, uint32_t block_size);
 

@@ -776,14 +776,22 @@ __global__ void k_outlier_scatter(const uint64_t* __restrict__ idx, const T* __r
 }
 
 // ---------------------------------------------------------------------------------- histogram
-__global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ codes, uint64_t n, uint32_t R,
-                                                   unsigned long long* __restrict__ hist) {
+// nb bins; the shared-memory window covers [lo, lo + nwin) (quantisation codes: centred on R; other
+// symbol streams: wherever their mass is, e.g. 0 for zigzag deltas); other bins use global atomics
+__global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ codes, uint64_t n, uint32_t nb,
+                                                   uint32_t lo, unsigned long long* __restrict__ hist) {
   __shared__ uint32_t s_win[HWIN];
   __shared__ uint32_t s_zero[33];
   HistSmem hs;
-  hist_init(hs, s_win, s_zero, R);
+  hs.win = s_win;
+  hs.zero = s_zero;
+  hs.dummy = s_zero + 1;
+  hs.lo = lo;
+  hs.nwin = lo < nb ? min(nb - lo, (uint32_t)HWIN) : 0u;
+  hs.W = 0;
+  for (uint32_t b = threadIdx.x; b < hs.nwin; b += blockDim.x) s_win[b] = 0u;
+  if (threadIdx.x == 0) *s_zero = 0u;
   __syncthreads();
-  const uint32_t nb = 2u * R;
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
   auto add = [&](uint32_t c) {
     if (c >= nb) return;
@@ -1223,13 +1231,26 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   return check_launch(launched);
 }
 
+int sz3g_histogram_bins(const uint16_t* codes, uint64_t n, uint32_t nbins, uint32_t window_lo, int64_t* hist,
+                        sz3g_stream_t stream) {
+  if (!hist || (n > 0 && !codes)) return SZ3G_EINVAL;
+  if (nbins < 1 || nbins > 65536) return SZ3G_ERANGE;
+  if (n == 0) return SZ3G_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, sm_count() * 2));
+  k_histogram<<<blocks, 512, 0, st>>>(codes, n, nbins, window_lo, reinterpret_cast<unsigned long long*>(hist));
+  return check_launch(1);
+}
+
 int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* hist, sz3g_stream_t stream) {
   if (!hist || (n > 0 && !codes)) return SZ3G_EINVAL;
   if (radius < 1 || radius > 32768) return SZ3G_ERANGE;
   if (n == 0) return SZ3G_OK;
+  // window as in the compress kernel: [1, 2R) when it fits, else centred on R
+  const uint32_t lo = (2u * radius - 1u <= (uint32_t)HWIN) ? 1u : radius - HWIN / 2;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, sm_count() * 2));
-  k_histogram<<<blocks, 512, 0, st>>>(codes, n, radius, reinterpret_cast<unsigned long long*>(hist));
+  k_histogram<<<blocks, 512, 0, st>>>(codes, n, 2u * radius, lo, reinterpret_cast<unsigned long long*>(hist));
   return check_launch(1);
 }
 

@@ -84,6 +84,7 @@ def load(allow_build: bool = False):
     lib.sz3g_regression_analyze.argtypes = [GP, P, P, P, P]
     lib.sz3g_regression_quantize.argtypes = [GP, PP, P, P, P, P, P, P, P, U64, P, P, P, P, P]
     lib.sz3g_histogram.argtypes = [P, U64, U32, P, P]
+    lib.sz3g_histogram_bins.argtypes = [P, U64, U32, U32, P, P]
     lib.sz3g_num_blocks.argtypes = [GP, U32]
     lib.sz3g_num_blocks.restype = U64
     lib.sz3g_uses_tma.argtypes = [GP, I32]
@@ -130,6 +131,7 @@ def load(allow_build: bool = False):
 
 
 EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regression_decompress", "sz3g_histogram",
+                    "sz3g_histogram_bins",
                     "sz3g_regression_analyze", "sz3g_regression_quantize", "sz3g_huffman_scratch_bytes",
                     "sz3g_huffman_dtable_bytes", "sz3g_huffman_encode_scratch_bytes", "sz3g_huffman_codebook",
                     "sz3g_huffman_encode", "sz3g_huffman_decode", "sz3g_truncation_compress",
@@ -406,6 +408,17 @@ def histogram(codes: torch.Tensor, radius: int = 32768, hist: torch.Tensor | Non
     return hist
 
 
+def histogram_bins(codes: torch.Tensor, nbins: int, window_lo: int = 0, hist: torch.Tensor | None = None,
+                   stream=None) -> torch.Tensor:
+    """sz3g_histogram_bins: accumulate an nbins int64 histogram with the smem window at window_lo."""
+    _require_cuda(codes, hist)
+    if hist is None:
+        hist = torch.zeros(nbins, dtype=torch.int64, device=codes.device)
+    _check(load().sz3g_histogram_bins(_ptr(codes), codes.numel(), nbins, window_lo, _ptr(hist), _stream(stream)),
+           "sz3g_histogram_bins")
+    return hist
+
+
 # ------------------------------------------------------------------------------------------- one-call API
 def compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768, two_pass: bool | None = None,
              **kw) -> Compressed:
@@ -643,7 +656,7 @@ def encode_coefficients(coef_codes: torch.Tensor, stream=None) -> CoefStream:
     """Coefficient codes -> delta symbols -> their histogram -> Huffman codebook -> encoded stream."""
     nb = coef_codes.numel() // 4
     sym, esc = coef_delta_encode(coef_codes, stream)
-    hist = histogram(sym, 32768, stream=stream)
+    hist = histogram_bins(sym, 65536, 0, stream=stream)   # zigzag deltas: mass near 0
     table = huffman_codebook(hist, stream=stream)
     return CoefStream(nb, table, huffman_encode(sym, table, stream=stream), esc)
 

@@ -51,3 +51,13 @@ def test_config_coefficients_through_huffman(name):
     raw = res.coef_codes.numel() * 4
     print(name, "coefficient bytes", raw, "->", cs.nbytes(), f"({raw / cs.nbytes():.1f}x)")
     assert cs.nbytes() < raw
+
+
+@pytest.mark.parametrize("lo", [0, 100, 60000])
+def test_histogram_bins_window(lo):
+    rng = np.random.default_rng(lo)
+    sym = np.minimum(rng.geometric(0.05, size=1_000_003) - 1 + (lo // 2), 65535).astype(np.uint16)
+    h = sz().histogram_bins(torch.from_numpy(sym).cuda(), 65536, lo).cpu().numpy()
+    assert np.array_equal(h, np.bincount(sym, minlength=65536))
+    h2 = sz().histogram_bins(torch.from_numpy(sym).cuda(), 300, lo).cpu().numpy()   # symbols >= nbins ignored
+    assert np.array_equal(h2, np.bincount(sym[sym < 300], minlength=300))
