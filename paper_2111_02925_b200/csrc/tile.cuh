@@ -91,6 +91,37 @@ __constant__ double c_lemma[7][2] = {{0, 0},       {3.0, 0.0},       {2.0, 2.0},
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+#ifndef SZ3G_X2
+#define SZ3G_X2 1   // packed fp32x2 arithmetic in the fp32 fast path (FFMA2 / FADD2, sm_100a)
+#endif
+// packed fp32 pairs (sm_100a FFMA2 / FADD2): each lane is the IEEE round-to-nearest result of the
+// scalar operation, so a pair computes exactly what two scalar instructions would
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lane_of(uint64_t v, int h) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return h ? hi : lo;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 // unconditional shared-memory add of a 0/1 register (red.shared, no return value): no branch and no
 // convergence region around it (a predicated +1 is turned into a warp-collective ATOMS.POPC.INC)
 __device__ __forceinline__ void red_smem_add(uint32_t addr, uint32_t v) {
@@ -428,7 +459,31 @@ __device__ __forceinline__ bool quantize_rows(const T* __restrict__ xs, uint64_t
     uint32_t code[BS];   // low 16 bits = the code (0: not accepted)
     uint32_t haddr[BS];
     bool need = false;   // some valid element the fast test cannot decide -> exact definition below
-    if (F32) {
+    if (F32 && SZ3G_X2) {
+      // the same IEEE operations on pairs of elements (i, i+1): packed FFMA2 / FADD2, per-lane rn
+      const float base32 = __fmaf_rn(F.a2, fj, __fmaf_rn(F.a3, fk, F.a0));
+#pragma unroll
+      for (int i = 0; i < BS; i += 2) {
+        const uint64_t x2 = pack2((float)xv[i], (float)xv[i + 1]);
+        const uint64_t nP = fma2(pack2(-F.a1, -F.a1), pack2((float)i, (float)(i + 1)), pack2(-base32, -base32));
+        const uint64_t t2 = fma2(x2, pack2(inv2eb32, inv2eb32), nP);   // -P exact: P(i = 0) = base32
+        const uint64_t s2 = add2(t2, pack2(M32, M32));
+        const uint64_t r2 = sub2(s2, pack2(M32, M32));
+        const uint64_t e2 = sub2(t2, r2);                                // exact
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int ii = i + h;
+          const bool valid = FULL || (cv && ii < L.m0);
+          const float t32 = lane_of(t2, h), e = lane_of(e2, h), r = lane_of(r2, h);
+          const float v = __fmaf_rn(F.k1, fabsf(t32), fabsf(e));
+          const bool ok = (v <= F.thr) && (fabsf(r) < Wf);
+          const uint32_t w = __float_as_uint(lane_of(s2, h));
+          code[ii] = ok ? w : 0u;
+          haddr[ii] = (ok && valid) ? 4u * w + hb : sink;
+          need |= valid && !ok;
+        }
+      }
+    } else if (F32) {
       const float base32 = __fmaf_rn(F.a2, fj, __fmaf_rn(F.a3, fk, F.a0));
 #pragma unroll
       for (int i = 0; i < BS; i++) {
