@@ -614,18 +614,24 @@ class CoefStream:
             self.table.stored_bytes()
 
 
-def coef_delta_encode(coef_codes: torch.Tensor, stream=None):
-    """sz3g_coef_delta_encode -> (sym uint16 [4 nb], escapes int64 [n], device count) (asynchronous)."""
+def coef_delta_encode(coef_codes: torch.Tensor, stream=None, sync: bool = True, esc_cap: int | None = None):
+    """sz3g_coef_delta_encode -> (sym uint16 [4 nb], escapes int64 [n]).  With ``sync=False`` no host
+    synchronisation: returns (sym, escape buffer, device count) and the caller checks the count
+    against the buffer (esc_cap entries, default nb)."""
     _require_cuda(coef_codes)
     lib = load()
     nb = coef_codes.numel() // 4
     dev = coef_codes.device
     sym = torch.empty(4 * nb, dtype=torch.uint16, device=dev)
-    esc = torch.empty(max(1, 4 * nb // 64), dtype=torch.int64, device=dev)
+    esc = torch.empty(max(1, esc_cap if esc_cap is not None else (4 * nb // 64 if sync else nb)), dtype=torch.int64,
+                      device=dev)
     nesc = torch.zeros(1, dtype=torch.int64, device=dev)
     scratch = torch.empty(int(lib.sz3g_coef_delta_scratch_bytes(nb)), dtype=torch.uint8, device=dev)
     _check(lib.sz3g_coef_delta_encode(_ptr(coef_codes), nb, _ptr(sym), _ptr(esc), esc.numel(), _ptr(nesc),
                                       _ptr(scratch), _stream(stream)), "sz3g_coef_delta_encode")
+    if not sync:
+        sym._scratch = scratch
+        return sym, esc, nesc
     n = int(nesc.item())
     if n > esc.numel():   # rare: more escapes than the first guess -> once more with room for all
         esc = torch.empty(n, dtype=torch.int64, device=dev)
@@ -652,13 +658,21 @@ def coef_delta_decode(sym: torch.Tensor, nb: int, escapes: torch.Tensor, out: to
     return out
 
 
-def encode_coefficients(coef_codes: torch.Tensor, stream=None) -> CoefStream:
-    """Coefficient codes -> delta symbols -> their histogram -> Huffman codebook -> encoded stream."""
+def encode_coefficients(coef_codes: torch.Tensor, stream=None, sync: bool = True) -> CoefStream:
+    """Coefficient codes -> delta symbols -> their histogram -> Huffman codebook -> encoded stream.
+    ``sync=False``: no host synchronisation; ``escapes`` is then the whole escape buffer and
+    ``n_escapes`` a device count (the caller trims after its own synchronisation)."""
     nb = coef_codes.numel() // 4
-    sym, esc = coef_delta_encode(coef_codes, stream)
+    if sync:
+        sym, esc = coef_delta_encode(coef_codes, stream)
+        nesc = None
+    else:
+        sym, esc, nesc = coef_delta_encode(coef_codes, stream, sync=False)
     hist = histogram_bins(sym, 65536, 0, stream=stream)   # zigzag deltas: mass near 0
     table = huffman_codebook(hist, stream=stream)
-    return CoefStream(nb, table, huffman_encode(sym, table, stream=stream), esc)
+    cs = CoefStream(nb, table, huffman_encode(sym, table, stream=stream), esc)
+    cs.n_escapes = nesc
+    return cs
 
 
 def decode_coefficients(cs: CoefStream, stream=None) -> torch.Tensor:
