@@ -457,7 +457,8 @@ def main():
         h_x = torch.empty_like(x, device="cpu").pin_memory()
         h_x.copy_(x)
         h_out = torch.empty_like(x, device="cpu").pin_memory()
-        codec = PipelinedCodec(tuple(x.shape), x.dtype, cfg.eb, cfg.eb_mode, cfg.radius, device=x.device)
+        codec = PipelinedCodec(tuple(x.shape), x.dtype, cfg.eb, cfg.eb_mode, cfg.radius, device=x.device,
+                               dim0_offset=a0)
         del x, out
         torch.cuda.empty_cache()
         codec.run([h_x], h_out)                      # warm-up (one field)

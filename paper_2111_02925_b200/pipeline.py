@@ -19,6 +19,7 @@ from dataclasses import dataclass
 
 import torch
 
+from . import dist as pdist
 from . import sz3g
 
 
@@ -45,8 +46,11 @@ class HostResult:
 
 class PipelinedCodec:
     def __init__(self, shape, dtype: torch.dtype, eb: float, eb_mode: str = "rel", radius: int = 32768,
-                 device=None, outlier_cap: int | None = None):
+                 device=None, outlier_cap: int | None = None, dim0_offset: int = 0):
+        """shape / dim0_offset: this rank's block-aligned slab when the field is sharded
+        (torch.distributed initialised): the range and the histogram are then all-reduced."""
         self.shape, self.dtype, self.eb, self.eb_mode, self.radius = tuple(shape), dtype, eb, eb_mode, radius
+        self.dim0_offset = dim0_offset
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
         n = 1
@@ -105,14 +109,17 @@ class PipelinedCodec:
             st.wait_event(self.ev_out[b])                    # field k - 2's outputs have left slot b
             bufs.reset()
             sz3g.regression_analyze(x, bufs.minmax, bufs.beta, stream=st)
+            pdist.allreduce_range_(bufs.minmax)    # sharded: the global range (no-op on one rank)
             sz3g.regression_quantize(x, self.eb, self.eb_mode, self.radius, bufs.minmax, bufs.beta, bufs=bufs,
-                                     reset=False, stream=st)
+                                     reset=False, dim0_offset=self.dim0_offset, stream=st)
+            pdist.allreduce_hist_(bufs.hist)       # sharded: one codebook for every slab
             table = sz3g.huffman_codebook(bufs.hist, stream=st)
             hs = sz3g.huffman_encode(bufs.codes.view(-1), table, payload=self.payload[b], offsets=self.offsets[b],
                                      scratch=self.enc_scratch, stream=st)
             coef = sz3g.encode_coefficients(bufs.coef_codes, stream=st, sync=False)
             sz3g.regression_decompress(bufs.codes, bufs.coef_codes, bufs.outlier_idx, bufs.outlier_val,
-                                       bufs.outlier_idx.numel(), self.eb, self.radius, self.dtype, out=self.out[b],
+                                       bufs.outlier_idx.numel(), self.eb, self.radius, self.dtype,
+                                       dim0_offset=self.dim0_offset, out=self.out[b],
                                        d_outlier_count=bufs.outlier_count, eb_mode=self.eb_mode,
                                        d_minmax=bufs.minmax, stream=st)
             # the sizes the copy-out needs, gathered on this stream into pinned host memory: no
