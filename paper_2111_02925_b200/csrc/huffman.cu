@@ -341,6 +341,8 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
 
 // ------------------------------------------------------------------------------------------------
 // encode
+constexpr uint32_t ENC_MAX_CHUNK_W = 2048;   // the format's chunk (k_huff_chunk_words fast path)
+
 __global__ void __launch_bounds__(256) k_huff_chunk_words(const uint16_t* __restrict__ codes, uint64_t n,
                                                           uint32_t chunk, const uint32_t* __restrict__ tab,
                                                           uint32_t nsym, uint64_t* __restrict__ words, uint64_t nch,
@@ -358,7 +360,19 @@ __global__ void __launch_bounds__(256) k_huff_chunk_words(const uint16_t* __rest
       bits += L;
       miss |= L == 0;
     };
-    if (vec) {   // 8 codes per 16-byte load (the chunk start is 16-byte aligned)
+    if (vec && chunk == ENC_MAX_CHUNK_W && e1 - e0 == ENC_MAX_CHUNK_W) {
+      // full 2048-code chunk: the lane's 8 loads are issued together (one DRAM latency per chunk)
+      const uint4* g = reinterpret_cast<const uint4*>(codes + e0) + lane;
+      uint4 u[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) u[k] = __ldcs(g + 32 * k);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+        for (int h = 0; h < 8; h++) add((w[h >> 1] >> (16 * (h & 1))) & 0xffffu);
+      }
+    } else if (vec) {   // 8 codes per 16-byte load (the chunk start is 16-byte aligned)
       const uint4* g = reinterpret_cast<const uint4*>(codes + e0);
       const uint32_t m = (uint32_t)(e1 - e0);
       for (uint32_t i = lane; 8 * i < m; i += 32) {
@@ -510,7 +524,10 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
   const uint32_t per = vec ? ENC_PER : (chunk + 31) / 32;
   const uint32_t* __restrict__ tb = tab;
   const uint32_t ns = nsym;
-  auto look = [tb, ns](uint32_t q) -> uint32_t { return q < ns ? __ldg(tb + q) : 0u; };
+  // codes >= nsym were flagged BAD_HUFFMAN by k_huff_chunk_words; clamping (instead of a guard) keeps
+  // the lookup branch-free and the table pointer in a register
+  const uint32_t smax = ns - 1;
+  auto look = [tb, smax](uint32_t q) -> uint32_t { return __ldg(tb + min(q, smax)); };
   for (uint64_t c = gw; c < nch; c += nw) {
     const uint64_t e0 = c * chunk, e1 = min(n, e0 + chunk);
     const uint64_t w0 = offs[c], nwords = offs[c + 1] - w0;
