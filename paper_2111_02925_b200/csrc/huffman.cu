@@ -732,12 +732,41 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
       dec_refill(d, ring);
     }
     // (2) 32 steps: 16 pairs of codes
+    if (__all_sync(0xffffffffu, e + DEC_ROUND <= m)) {
+      // every lane decodes 32 real codes this round: no per-code bookkeeping; both codes of a pair go
+      // through the LUT and one warp vote per pair catches codes longer than the LUT -- the pair is then
+      // decoded again, code by code, from the saved window
 #pragma unroll 4
-    for (int h = 0; h < DEC_ROUND; h += 2) {
-      const uint32_t a = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, e + h < m);
-      const uint32_t b = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, e + h + 1 < m);
-      dec_refill(d, ring);
-      out[h >> 1] = a | (b << 16);
+      for (int h = 0; h < DEC_ROUND; h += 2) {
+        const uint64_t win0 = d.win;
+        const uint32_t top1 = (uint32_t)(win0 >> 48);
+        const uint32_t ea = s_lut[top1 >> (16 - HF_LUT_BITS)];
+        const uint32_t La = ea >> 16;
+        const uint64_t win1 = win0 << La;
+        const uint32_t eb = s_lut[(uint32_t)(win1 >> 48) >> (16 - HF_LUT_BITS)];
+        const uint32_t Lb = eb >> 16;
+        uint32_t a, b;
+        if (__any_sync(0xffffffffu, ea == 0u || eb == 0u)) {
+          a = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, true);
+          b = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, true);
+        } else {
+          a = ea & 0xffffu;
+          b = eb & 0xffffu;
+          d.win = win1 << Lb;
+          d.avail -= La + Lb;
+          d.consumed += La + Lb;
+        }
+        dec_refill(d, ring);
+        out[h >> 1] = a | (b << 16);
+      }
+    } else {
+#pragma unroll 4
+      for (int h = 0; h < DEC_ROUND; h += 2) {
+        const uint32_t a = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, e + h < m);
+        const uint32_t b = dec_one(d, s_lut, s_ljl, s_first, s_base, syms, max_len, bad, e + h + 1 < m);
+        dec_refill(d, ring);
+        out[h >> 1] = a | (b << 16);
+      }
     }
     __syncwarp();
     // (3) write the round's codes: one chunk row (64 B) per half-warp pass
