@@ -368,11 +368,13 @@ struct CoefSlot {  // per stage: the tile's 16 blocks
   Fast32 f[16];
 };
 
-template <typename T, int NG, int Q, int D, bool BETA = false, bool SELF = false, int HW = HWIN>
+template <typename T, int NG, int Q, int D, bool BETA = false, bool SELF = false, int HW = HWIN, bool NOR0 = false>
 struct CompressSmem {
   static constexpr int P = BS / Q;
   static constexpr int S = NG * D;
-  static constexpr int WARPS = NG * (1 + Q) + (SELF ? 0 : 1);   // SELF: no producer warp
+  // SELF: no producer warp; NOR0 (two-pass only): no role-0 warp, the quantise warps derive the
+  // coefficient constants from the staged beta themselves
+  static constexpr int WARPS = NG * (NOR0 ? Q : 1 + Q) + (SELF ? 0 : 1);
   static constexpr size_t tile_bytes = sizeof(T) * TILE_ELEMS;
   static constexpr size_t stage_bytes = tile_bytes + (BETA ? 16 * 32 : 0);   // + beta of the tile's 16 blocks
   static constexpr size_t slab_bytes = sizeof(uint16_t) * BS * P * TK;
@@ -452,6 +454,31 @@ __device__ __forceinline__ void coef_warp_tile(const double* __restrict__ bstage
   }
 }
 
+// NOR0 mode: the quantise warp turns the staged beta of its lanes' blocks into the decoded coefficients
+// and fast-path constants itself (the same block_codes / fast32_consts as the role-0 warp); warp q == 0
+// writes the coefficient codes
+template <typename T, bool HIST, bool FULL, int P>
+__device__ __forceinline__ void quant_warp_tile_beta(const T* __restrict__ xs, const double* __restrict__ bstage,
+                                                     uint16_t* slab, int j0, bool write_codes, const TileCoord tc,
+                                                     const Geo& g, const Consts& K, uint32_t R,
+                                                     const CompressOut<T>& o, const HistSmem& hs) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int bl = (threadIdx.x & 31) >> 1;
+  double beta[4] = {0.0, 0.0, 0.0, 0.0}, bh[4];
+  int32_t cc[4];
+  if (L.m2 > 0) {
+    const double2 b01 = reinterpret_cast<const double2*>(bstage)[2 * bl];
+    const double2 b23 = reinterpret_cast<const double2*>(bstage)[2 * bl + 1];
+    beta[0] = b01.x; beta[1] = b01.y; beta[2] = b23.x; beta[3] = b23.y;
+  }
+  block_codes(beta, K, cc, bh);
+  if (write_codes) write_coefs(o, tc, g, L, cc, beta);
+  const Fast32 F = fast32_consts(bh, K);
+  const bool has_out =
+      quantize_rows<T, true, HIST, FULL, P, true>(xs, BS * TK, TK, slab, 0, 0, j0, L, bh, F, K, R, hs, o.hist);
+  rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, has_out, tc, g, o, hs);
+}
+
 template <typename T, bool HIST, bool FULL, int P>
 __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const CoefSlot* slot, uint16_t* slab,
                                                 int j0, const TileCoord tc, const Geo& g, const Consts& K,
@@ -470,11 +497,12 @@ __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const 
 // SELF: no producer warp; the role-0 warp of each group feeds its own group's ring (it issues the
 // load of tile k + D - 1 once the quantise warps have released tile k - 1, right after it has
 // published tile k's coefficients), with an optional L2 prefetch one tile further ahead.
-template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF, int HW>
-__global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW>::WARPS * 32, 1)
+template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF, int HW, bool NOR0>
+__global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0>::WARPS * 32, 1)
     k_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, int codes_tma,
                    KArgs a, CompressOut<T> o) {
-  using L_ = CompressSmem<T, NG, Q, D, BETA, SELF, HW>;
+  static_assert(!NOR0 || (BETA && !SELF), "NOR0 needs the two-pass beta and a producer warp");
+  using L_ = CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0>;
   constexpr int P = L_::P;
   constexpr int S = L_::S;
   static_assert(BS % Q == 0, "Q must divide 6");
@@ -516,7 +544,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW>::WAR
       ptx::tma_load_3d(stage_x(s), &tm_x, &full[s], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
     }
   };
-  if (!SELF && warp == NG * (1 + Q)) {
+  if (!SELF && warp == L_::WARPS - 1) {
     // ---------------- producer
     if (lane == 0) {
       ptx::prefetch_tensormap(&tm_x);
@@ -550,8 +578,10 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW>::WAR
     // role is rotated by the group index, so every sub-partition holds one moment warp and Q quantise
     // warps; with 1 + Q = 3 and 5 groups the plain order already gives the best split (2/3/3/2
     // quantise warps, moment warps and the producer on the lighter sub-partitions).
-    const int grp = warp / (1 + Q);
-    const int role = (1 + Q == 4) ? (warp - grp * (1 + Q) + (1 + Q) - grp % (1 + Q)) % (1 + Q) : warp - grp * (1 + Q);
+    const int grp = NOR0 ? warp / Q : warp / (1 + Q);
+    const int role = NOR0 ? 1 + warp % Q
+                          : (1 + Q == 4) ? (warp - grp * (1 + Q) + (1 + Q) - grp % (1 + Q)) % (1 + Q)
+                                         : warp - grp * (1 + Q);
     const Consts K = *s_k;
     uint32_t k = 0;
     if (role == 0) {
@@ -614,10 +644,16 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW>::WAR
         if (codes_tma && lane == 0) ptx::bulk_wait_read0();   // previous slab store finished reading
         __syncwarp();
         ptx::mbar_wait(&full[s], ph);
-        ptx::mbar_wait(&ready[s], ph);
+        if (!NOR0) ptx::mbar_wait(&ready[s], ph);
         const T* xs = stage_x(s);
-        if (tile_full(tc, g)) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
-        else quant_warp_tile<T, HIST, false, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
+        if (NOR0) {
+          const double* bst = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(xs) + L_::tile_bytes);
+          if (tile_full(tc, g)) quant_warp_tile_beta<T, HIST, true, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+          else quant_warp_tile_beta<T, HIST, false, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+        } else {
+          if (tile_full(tc, g)) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
+          else quant_warp_tile<T, HIST, false, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
+        }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&empty[s]);
         if (codes_tma) {
@@ -937,7 +973,9 @@ struct Tuning {
 Tuning g_tuning[] = {
     {"CHUNK_C", 2},   // adjacent tiles per CTA chunk, compress
     {"CHUNK_D", 16},  // adjacent tiles per CTA chunk, decompress
-    {"CCFG", 0},      // f32 compress kernel shape: 0 = 5 x (1 + 2) warps, 1 = 3 x (1 + 3), 2 = 4 x (1 + 2), 3 = 4 x (1 + 3)
+    {"CCFG", 0},      // f32 compress kernel shape: 0 = default (fused 5 x (1 + 2) + producer; two-pass 5 x 3 quantise
+                      // warps + producer, no role-0), 3 = 4 x (1 + 3), 4/5 = producer-less, 6/7/8 = two-pass
+                      // without role-0 at 5 x 2 / 4 x 3 / 5 x 3
     {"PF", PF_TILES}, // L2 prefetch distance of the compress producer (tiles)
 };
 std::once_flag g_tuning_env_once;
@@ -970,17 +1008,17 @@ constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 war
 constexpr int AW32 = 8, AD32 = 2;            // f32 analyze: 8 self-fed warps x 2 stages (13.5 KiB)
 constexpr int AW64 = 4, AD64 = 2;            // f64 analyze: 4 warps x 2 stages (27 KiB)
 
-template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN>
+template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN, bool NOR0 = false>
 int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
                         const CompressOut<T>& co, cudaStream_t st) {
-  using L = CompressSmem<T, NG, Q, D, BETA, SELF, HW>;
+  using L = CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mx, mc;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
   memset(&mc, 0, sizeof(mc));
   if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g, L::P, true)) codes_tma = false;
-  auto kern = k_compress_tma<T, NG, Q, D, HIST, BETA, SELF, HW>;
+  auto kern = k_compress_tma<T, NG, Q, D, HIST, BETA, SELF, HW, NOR0>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
@@ -1020,6 +1058,21 @@ int compress_launch(const Geo& g, const void* x, uint16_t* codes, bool tma, bool
       if (cfg == 5)   // as 4 with 3-deep rings (histogram window 4096 bins to fit)
         return use_hist ? launch_compress_tma<T, 4, 3, 3, true, BETA, true, 4096>(g, x, codes, codes_tma, ka, co, st)
                         : launch_compress_tma<T, 4, 3, 3, false, BETA, true, 4096>(g, x, codes, codes_tma, ka, co, st);
+      if constexpr (BETA) {
+        if (cfg == 6)   // two-pass: no role-0 warp, 5 groups x 2 quantise warps + producer
+          return use_hist ? launch_compress_tma<T, 5, 2, 2, true, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st)
+                          : launch_compress_tma<T, 5, 2, 2, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
+        if (cfg == 7)   // two-pass: no role-0 warp, 4 groups x 3 quantise warps + producer
+          return use_hist ? launch_compress_tma<T, 4, 3, 2, true, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st)
+                          : launch_compress_tma<T, 4, 3, 2, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
+        if (cfg == 8)   // two-pass: no role-0 warp, 5 groups x 3 quantise warps + producer
+          return use_hist ? launch_compress_tma<T, 5, 3, 2, true, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st)
+                          : launch_compress_tma<T, 5, 3, 2, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
+      }
+      if constexpr (BETA) {   // default two-pass shape: 5 groups x 3 quantise warps, no role-0 warp (A/B best)
+        return use_hist ? launch_compress_tma<T, 5, 3, 2, true, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st)
+                        : launch_compress_tma<T, 5, 3, 2, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
+      }
       return use_hist ? launch_compress_tma<T, CN32, CQ32, CD32, true, BETA>(g, x, codes, codes_tma, ka, co, st)
                       : launch_compress_tma<T, CN32, CQ32, CD32, false, BETA>(g, x, codes, codes_tma, ka, co, st);
     } else {
