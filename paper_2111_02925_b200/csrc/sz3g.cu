@@ -1003,7 +1003,10 @@ int compress_cfg() { return (int)tuning("CCFG"); }
 uint32_t prefetch_tiles() { return (uint32_t)std::max<int64_t>(0, tuning("PF")); }
 constexpr int CN32 = 5, CQ32 = 2, CD32 = 2;  // f32 compress: 5 groups x (1 moment + 2 quantise warps) + producer = 16 warps
 constexpr int CN64 = 3, CQ64 = 3, CD64 = 2;  // f64 compress: 3 groups x (1 + 3) warps + producer = 13 warps
-constexpr int DG32 = 3, DN32 = 5, DD32 = 3;  // f32 decompress: 5 groups x 3 warps + producer; 3 x 7 KiB stages per group
+#ifndef SZ3G_DEC_CFG
+#define SZ3G_DEC_CFG 0   // f32 decompress shape (A/B tuning): 0 = 5 x 3 warps, 3-deep; 1 = 7 x 3 warps, 2-deep
+#endif
+constexpr int DG32 = 3, DN32 = SZ3G_DEC_CFG == 1 ? 7 : 5, DD32 = SZ3G_DEC_CFG == 1 ? 2 : 3;  // f32 decompress: groups of 3 warps + producer
 constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 warps + producer
 constexpr int AW32 = 8, AD32 = 2;            // f32 analyze: 8 self-fed warps x 2 stages (13.5 KiB)
 constexpr int AW64 = 4, AD64 = 2;            // f64 analyze: 4 warps x 2 stages (27 KiB)

@@ -18,8 +18,13 @@
 #pragma once
 #include <cstdint>
 
+#ifndef SZ3G_DEC_UNROLL
+#define SZ3G_DEC_UNROLL 1   // unroll of the decompress column loop (A/B tuning)
+#endif
+
 namespace sz3g {
 
+constexpr int DEC_UNROLL = SZ3G_DEC_UNROLL;
 constexpr int BS = 6;                          // regression block size B (north_star: 6x6x6)
 constexpr int TK = 96;                         // tile extent along dim 2 (16 blocks)
 constexpr int TROWS = BS * BS;                 // rows (i,j) per tile
@@ -669,7 +674,7 @@ __device__ __forceinline__ void decompress_rows(const uint16_t* __restrict__ cs,
                                                 const uint32_t R) {
   if (IN_SMEM) { ci = BS * TK; cj = TK; }
   const double cR = __dadd_rn(I2D_MAGIC, (double)R);  // exact: 2^52 + R
-#pragma unroll 1
+#pragma unroll DEC_UNROLL
   for (int jk = 0; jk < 3 * PJ; jk++) {
     const int jj = jk / 3, kk = jk - 3 * jj, j = j0 + jj;
     const bool cv = FULL || ((j < L.m1) && L.kv(kk));
