@@ -1,8 +1,11 @@
-"""TEST INFRASTRUCTURE ONLY -- ctypes wrapper around the plain C++ oracle (oracle/sz3_oracle.cpp).
+"""TEST INFRASTRUCTURE ONLY -- ctypes wrapper around the plain C++ oracle (oracle/*.cpp).
 
 The oracle is the single-threaded CPU definition of SZ3's block-regression predictor with
-linear-scaling quantisation (Lemma 1, prediction P:156, quantiser P:406-409,
-App. A loop P:980-992, value-range eb P:833).  Only ``tests/``, ``__graft_entry__.smoke()`` and
+linear-scaling quantisation (sz3_oracle.cpp: PAPER.md Lemma 1, prediction P:156, quantiser
+P:406-409, App. A loop P:980-992, value-range eb P:833), of the Huffman encoder stage
+(huffman_oracle.cpp: P:156), of SZ3-Truncation and the coefficient delta coding
+(truncation_oracle.cpp: P:848-850) and of the distortion metrics (below: P:525); the exact
+definitions are oracle/DEFINITION.md (O1-O11, D, H1-H5, T1-T2, C1-C2, M1-M3).  Only ``tests/``, ``__graft_entry__.smoke()`` and
 ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this package.  It shares
 no code with ``paper_2111_02925_b200`` and never imports it.
 """
