@@ -382,9 +382,16 @@ struct CompressSmem {
   static constexpr size_t off_slot = off_slab + (size_t)NG * Q * slab_bytes;
   static constexpr size_t off_hist = off_slot + S * sizeof(CoefSlot);
   static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (HW + 36);
-  static constexpr size_t off_k = off_bar + 3 * S * sizeof(uint64_t);
+  static constexpr size_t off_hdr = off_bar + 3 * S * sizeof(uint64_t);   // producer-written tile headers
+  static constexpr size_t off_k = off_hdr + S * sizeof(uint4);
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
+  static_assert(off_hdr % 16 == 0, "stage headers are read as uint4");
 };
+
+// Stage header written by the producer before it arms the stage's full barrier: the tile's coordinates
+// and its full-tile flag (w = 1), or the end of the group's sequence (w = 2).  The consumers read it
+// after the full wait instead of walking and decoding the tile sequence themselves.
+constexpr uint32_t HDR_FULL = 1u, HDR_END = 2u;
 
 // copy a quantise warp's code slab (rows j0 .. j0+P-1, layout [i][jj][k]) to the global code array
 // (fallback when no TMA store applies: n2 * 2 bytes is not a multiple of 16)
@@ -514,6 +521,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
   uint64_t* ready = full + S;
   uint64_t* empty = ready + S;
+  uint4* hdr = reinterpret_cast<uint4*>(smem + L_::off_hdr);
   Consts* s_k = reinterpret_cast<Consts*>(smem + L_::off_k);
   int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -532,6 +540,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
   // one TMA load of tile t into stage s (+ the beta of its blocks in two-pass mode)
   auto issue_load = [&](uint32_t s, uint64_t t) {
     const TileCoord tc = decode_tile(t, g);
+    if (!SELF) hdr[s] = make_uint4(tc.a, tc.b, tc.c, tile_full(tc, g) ? HDR_FULL : 0u);   // released by the arrive
     if (BETA) {   // the tile and the beta of its <= 16 blocks complete on the same barrier
       const uint32_t nblk = min(16u, g.NB2 - tc.c * 16u);
       ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)L_::tile_bytes + 32u * nblk);
@@ -572,6 +581,13 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
         ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
         issue_load(s, t);
       }
+      for (int e = 0; e < NG; e++) {   // end of sequence: one header per group, no data
+        const uint32_t s = gq * D + k % D, ph = (k / D) & 1u;
+        if (++gq == NG) { gq = 0; k++; }
+        ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
+        hdr[s] = make_uint4(0u, 0u, 0u, HDR_END);
+        ptx::mbar_arrive(&full[s]);
+      }
     }
   } else {
     // role 0: moment warp, 1..Q: quantise.  Warp w runs on SM sub-partition w % 4.  With 1 + Q = 4 the
@@ -596,19 +612,30 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
         for (int d = 0; d < D - 1 + (int)a.pf; d++) tp.next();
       }
       for (TileWalk tw(grp, a.chunk, NG);; tw.next(), k++) {
-        const uint64_t t = tw.tile();
-        if (t >= g.ntiles) break;
         const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
-        const TileCoord tc = decode_tile(t, g);
+        TileCoord tc;
+        bool tfull;
+        if (SELF) {
+          const uint64_t t = tw.tile();
+          if (t >= g.ntiles) break;
+          tc = decode_tile(t, g);
+          tfull = tile_full(tc, g);
+        }
         if (BETA) ptx::mbar_wait_idle(&full[s], ph);   // a mostly idle warp: do not steal issue slots
         else ptx::mbar_wait(&full[s], ph);
+        if (!SELF) {
+          const uint4 h = hdr[s];
+          if (h.w == HDR_END) break;
+          tc = TileCoord{h.x, h.y, h.z};
+          tfull = h.w == HDR_FULL;
+        }
         const T* xs = stage_x(s);
         if (BETA) {
           const double* bst = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(xs) + L_::tile_bytes);
-          if (tile_full(tc, g)) coef_warp_tile<T, true>(bst, &slots[s], tc, g, K, o);
+          if (tfull) coef_warp_tile<T, true>(bst, &slots[s], tc, g, K, o);
           else coef_warp_tile<T, false>(bst, &slots[s], tc, g, K, o);
         } else {
-          if (tile_full(tc, g)) moment_warp_tile<T, true>(xs, &slots[s], tc, g, K, o);
+          if (tfull) moment_warp_tile<T, true>(xs, &slots[s], tc, g, K, o);
           else moment_warp_tile<T, false>(xs, &slots[s], tc, g, K, o);
         }
         __syncwarp();
@@ -637,21 +664,32 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
       const int q = role - 1, j0 = q * P;
       uint16_t* slab = slabs + (size_t)(grp * Q + q) * (BS * P * TK);
       for (TileWalk tw(grp, a.chunk, NG);; tw.next(), k++) {
-        const uint64_t t = tw.tile();
-        if (t >= g.ntiles) break;
         const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
-        const TileCoord tc = decode_tile(t, g);
+        TileCoord tc;
+        bool tfull;
+        if (SELF) {
+          const uint64_t t = tw.tile();
+          if (t >= g.ntiles) break;
+          tc = decode_tile(t, g);
+          tfull = tile_full(tc, g);
+        }
         if (codes_tma && lane == 0) ptx::bulk_wait_read0();   // previous slab store finished reading
         __syncwarp();
         ptx::mbar_wait(&full[s], ph);
+        if (!SELF) {
+          const uint4 h = hdr[s];
+          if (h.w == HDR_END) break;
+          tc = TileCoord{h.x, h.y, h.z};
+          tfull = h.w == HDR_FULL;
+        }
         if (!NOR0) ptx::mbar_wait(&ready[s], ph);
         const T* xs = stage_x(s);
         if (NOR0) {
           const double* bst = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(xs) + L_::tile_bytes);
-          if (tile_full(tc, g)) quant_warp_tile_beta<T, HIST, true, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+          if (tfull) quant_warp_tile_beta<T, HIST, true, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
           else quant_warp_tile_beta<T, HIST, false, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
         } else {
-          if (tile_full(tc, g)) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
+          if (tfull) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
           else quant_warp_tile<T, HIST, false, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
         }
         __syncwarp();

@@ -28,12 +28,13 @@ def build_rev(name: str, rev: str):
         print("built", name, rev, "->", out)
         return
     d = tempfile.mkdtemp()
-    for f in ("paper_2111_02925_b200/csrc/sz3g.cu", "paper_2111_02925_b200/csrc/tile.cuh",
-              "paper_2111_02925_b200/csrc/ptx.cuh", "include/sz3g.h"):
+    files = subprocess.run(["git", "ls-tree", "-r", "--name-only", rev, "paper_2111_02925_b200/csrc", "include"],
+                           cwd=ROOT, capture_output=True, text=True, check=True).stdout.split()
+    for f in files:
         os.makedirs(os.path.join(d, os.path.dirname(f)), exist_ok=True)
         src = subprocess.run(["git", "show", f"{rev}:{f}"], cwd=ROOT, capture_output=True, text=True, check=True).stdout
         open(os.path.join(d, f), "w").write(src)
-    B.build(force=True, src=os.path.join(d, "paper_2111_02925_b200/csrc/sz3g.cu"), out=out)
+    B.build(force=True, src=[os.path.join(d, f) for f in files if f.endswith(".cu")], out=out)
     print("built", name, rev, "->", out)
 
 
