@@ -346,8 +346,8 @@ constexpr uint32_t ENC_MAX_CHUNK_W = 2048;   // the format's chunk (k_huff_chunk
 __global__ void __launch_bounds__(256) k_huff_chunk_words(const uint16_t* __restrict__ codes, uint64_t n,
                                                           uint32_t chunk, const uint32_t* __restrict__ tab,
                                                           uint32_t nsym, uint64_t* __restrict__ words, uint64_t nch,
-                                                          int32_t* status) {
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+                                                          int32_t* status, uint64_t c_begin) {
+  const uint64_t warp = c_begin + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   const bool vec = (chunk % 8 == 0) && ((reinterpret_cast<uintptr_t>(codes) & 15) == 0);
@@ -512,13 +512,13 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
                                                                 uint32_t chunk, const uint32_t* __restrict__ tab,
                                                                 uint32_t nsym, const uint64_t* __restrict__ offs,
                                                                 uint64_t nch, uint32_t* __restrict__ payload,
-                                                                uint64_t cap, int32_t* status) {
+                                                                uint64_t cap, int32_t* status, uint64_t c_begin) {
   __shared__ uint32_t s_img[ENC_WARPS][ENC_WORDS];
   __shared__ uint4 s_codes[ENC_WARPS][ENC_MAX_CHUNK / 8];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   uint32_t* img = s_img[wl];
   uint4* sc = s_codes[wl];
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t gw = c_begin + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const bool vec = (chunk == ENC_MAX_CHUNK) && ((reinterpret_cast<uintptr_t>(codes) & 15) == 0);
   const uint32_t per = vec ? ENC_PER : (chunk + 31) / 32;
@@ -600,6 +600,202 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
     __syncwarp();
   }
 }
+
+// ------------------------------------------------------------------------------------------------
+// Full-chunk fast path (chunk = 2048 codes, 16-byte aligned codes): the bulk of every field.
+//
+// The codes of a field concentrate around the radius (the histogram's mass is near R), so each CTA
+// stages a window of EW_TW table entries centred on nsym / 2 in shared memory and looks codes up there;
+// a group of 8 codes with any code outside the window takes the global table for that group (warp
+// vote).  One warp per chunk, lane l owning codes [64 l, 64 l + 64); the chunk is loaded one chunk
+// ahead into registers with coalesced 16-byte loads and restaged through shared memory.
+//
+// k_huff_chunk_words_full: window entries L + (L == 0) << 20 summed with one add per code (bits in the
+// low 20 bits, missing symbols counted above).
+// k_huff_encode_full: ONE lookup per code.  Each lane packs its 64 codes MSB-first into a private
+// word buffer in shared memory starting at bit 0 (pairs of codes are first joined into one <= 32-bit
+// unit, then appended to a 64-bit accumulator), a warp scan gives its first bit in the chunk, and it
+// copies its private words into the chunk image shifted by (first bit mod 32).  The word a lane shares
+// with the next lane is written by the lower lane, which receives the next lane's head bits by a
+// shuffle: every image word is written exactly once, no atomics, no zeroing.  The image leaves with
+// coalesced stores.
+constexpr int EW_TW = 8192, EW_WARPS = 16, EW_CHUNK = 2048, EW_PRIV = 33;
+constexpr int EW_IMG = ENC_WORDS + 3;   // 1028 words per warp
+
+__device__ __forceinline__ uint32_t ew_lo(uint32_t nsym) { return nsym > EW_TW ? nsym / 2 - EW_TW / 2 : 0u; }
+
+// 8 codes of a uint4 -> idx - lo packed per half word; true if every code is inside the window.  A code
+// below lo borrows from the next half (or wraps the top half), which makes that half >= EW_TW: the
+// window test catches every case (lo <= 65536 - EW_TW - 1).
+__device__ __forceinline__ bool ew_in_window(const uint4 u, uint32_t lo2, uint32_t (&d)[4]) {
+  d[0] = u.x - lo2; d[1] = u.y - lo2; d[2] = u.z - lo2; d[3] = u.w - lo2;
+  constexpr uint32_t oor = ((~(uint32_t)(EW_TW - 1)) & 0xffffu) * 0x10001u;
+  return ((d[0] | d[1] | d[2] | d[3]) & oor) == 0u;
+}
+
+// coalesced: load v of lane l is uint4 v * 32 + l of the chunk
+__device__ __forceinline__ void ew_load_chunk(const uint16_t* __restrict__ codes, uint64_t c, int lane, uint4 (&u)[8]) {
+  const uint4* g = reinterpret_cast<const uint4*>(codes + c * EW_CHUNK) + lane;
+#pragma unroll
+  for (int v = 0; v < 8; v++) u[v] = __ldcs(g + 32 * v);
+}
+
+// stage the loaded chunk in shared memory (uint4 i at slot swz(i)) and read back the lane's own 64
+// consecutive codes (uint4 8 l .. 8 l + 7): conflict-free both ways
+__device__ __forceinline__ void ew_restage(const uint4 (&nx)[8], uint4* st, int lane, uint4 (&u)[8]) {
+#pragma unroll
+  for (int v = 0; v < 8; v++) st[swz(v * 32 + lane)] = nx[v];
+  __syncwarp();
+#pragma unroll
+  for (int v = 0; v < 8; v++) u[v] = st[swz(lane * 8 + v)];
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_chunk_words_full(const uint16_t* __restrict__ codes,
+                                                                            uint64_t nfull,
+                                                                            const uint32_t* __restrict__ tab,
+                                                                            uint32_t nsym,
+                                                                            uint64_t* __restrict__ words,
+                                                                            int32_t* status) {
+  __shared__ uint32_t s_len[EW_TW];
+  const uint32_t lo = ew_lo(nsym), lo2 = lo | (lo << 16);
+  for (uint32_t i = threadIdx.x; i < EW_TW; i += blockDim.x) {
+    const uint32_t L = lo + i < nsym ? __ldg(tab + lo + i) >> 24 : 0u;
+    s_len[i] = L + (L == 0 ? (1u << 20) : 0u);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * EW_WARPS;
+  uint64_t c = (uint64_t)blockIdx.x * EW_WARPS + (threadIdx.x >> 5);
+  uint4 nx[8];
+  if (c < nfull) ew_load_chunk(codes, c, lane, nx);
+  for (; c < nfull; c += nw) {
+    uint4 u[8];   // the sum does not care which lane holds which codes: no restaging
+#pragma unroll
+    for (int v = 0; v < 8; v++) u[v] = nx[v];
+    if (c + nw < nfull) ew_load_chunk(codes, c + nw, lane, nx);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int v = 0; v < 8; v++) {
+      uint32_t d[4];
+      if (__all_sync(0xffffffffu, ew_in_window(u[v], lo2, d))) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc += s_len[d[k] & 0xffffu] + s_len[d[k] >> 16];
+      } else {
+        const uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
+#pragma unroll
+        for (int h = 0; h < 8; h++) {
+          const uint32_t q = (w[h >> 1] >> (16 * (h & 1))) & 0xffffu;
+          const uint32_t L = q < nsym ? __ldg(tab + q) >> 24 : 0u;
+          acc += L + (L == 0 ? (1u << 20) : 0u);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      if (acc >> 20) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
+      words[c] = ((acc & 0xfffffu) + 31) / 32;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uint16_t* __restrict__ codes,
+                                                                       uint64_t nfull,
+                                                                       const uint32_t* __restrict__ tab,
+                                                                       uint32_t nsym,
+                                                                       const uint64_t* __restrict__ offs,
+                                                                       uint32_t* __restrict__ payload, uint64_t cap,
+                                                                       int32_t* status) {
+  extern __shared__ __align__(16) uint32_t esm[];
+  uint32_t* s_tab = esm;                                   // [EW_TW] (L << 16) | codeword
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  uint32_t* priv = esm + EW_TW + wl * (32 * EW_PRIV) + lane * EW_PRIV;
+  uint32_t* img = esm + EW_TW + EW_WARPS * 32 * EW_PRIV + wl * EW_IMG;
+  const uint32_t lo = ew_lo(nsym), lo2 = lo | (lo << 16), smax = nsym - 1;
+  for (uint32_t i = threadIdx.x; i < EW_TW; i += blockDim.x) {
+    const uint32_t t = lo + i < nsym ? __ldg(tab + lo + i) : 0u;
+    s_tab[i] = ((t >> 24) << 16) | (t & 0xffffu);
+  }
+  __syncthreads();
+  const uint64_t nw = (uint64_t)gridDim.x * EW_WARPS;
+  uint64_t c = (uint64_t)blockIdx.x * EW_WARPS + wl;
+  uint4 nx[8];
+  if (c < nfull) ew_load_chunk(codes, c, lane, nx);
+  for (; c < nfull; c += nw) {
+    uint4 u[8];
+    ew_restage(nx, reinterpret_cast<uint4*>(img), lane, u);   // the image is free until step (3)
+    if (c + nw < nfull) ew_load_chunk(codes, c + nw, lane, nx);
+    // (1) pack the lane's 64 codes into its private buffer
+    uint64_t acc = 0;
+    uint32_t nb = 0, wi = 0;
+#pragma unroll
+    for (int v = 0; v < 8; v++) {
+      uint32_t d[4], e[8];
+      if (__all_sync(0xffffffffu, ew_in_window(u[v], lo2, d))) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          e[2 * k] = s_tab[d[k] & 0xffffu];
+          e[2 * k + 1] = s_tab[d[k] >> 16];
+        }
+      } else {
+        const uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
+#pragma unroll
+        for (int h = 0; h < 8; h++) {   // codes >= nsym are flagged by the size pass; clamp like it
+          const uint32_t t = __ldg(tab + min((w[h >> 1] >> (16 * (h & 1))) & 0xffffu, smax));
+          e[h] = ((t >> 24) << 16) | (t & 0xffffu);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint32_t ea = e[2 * k], eb = e[2 * k + 1];
+        const uint32_t lb = eb >> 16;
+        const uint32_t pl = (ea >> 16) + lb;                              // <= 32 bits
+        const uint32_t pv = ((ea & 0xffffu) << lb) | (eb & 0xffffu);
+        acc = (acc << pl) | pv;
+        nb += pl;
+        if (nb >= 32) {
+          nb -= 32;
+          priv[wi++] = (uint32_t)(acc >> nb);
+        }
+      }
+    }
+    const uint32_t bits = 32 * wi + nb;
+    if (nb) priv[wi] = (uint32_t)(acc << (32 - nb));
+    // (2) the lane's first bit in the chunk
+    uint32_t incl = bits;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t b0 = incl - bits, sh = b0 & 31u, base = b0 >> 5;
+    const uint32_t nwp = (bits + 31) >> 5, nout = (sh + bits + 31) >> 5;
+    const uint32_t head = nwp ? priv[0] >> sh : 0u;
+    const uint32_t nhead = __shfl_down_sync(0xffffffffu, head, 1);
+    const bool nshare = lane < 31 && ((incl & 31u) != 0);   // my last word continues in the next lane
+    // (3) shifted copy into the chunk image; the first word, if shared, is the previous lane's
+    uint32_t prev = 0u;
+    for (uint32_t j = 0; j < nout; j++) {
+      const uint32_t cur = j < nwp ? priv[j] : 0u;
+      uint32_t val = (cur >> sh) | (sh ? prev << (32 - sh) : 0u);
+      prev = cur;
+      if (j == nout - 1 && nshare) val |= nhead;
+      if (j > 0 || sh == 0) img[base + j] = val;
+    }
+    __syncwarp();
+    // (4) out
+    const uint64_t w0 = offs[c], nwords = offs[c + 1] - w0;
+    if (offs[c + 1] > cap) {
+      if (lane == 0) atomicOr(status, (int)SZ3G_STATUS_PAYLOAD_OVERFLOW);
+    } else {
+      for (uint32_t i = lane; i < nwords; i += 32) payload[w0 + i] = img[i];
+    }
+    __syncwarp();
+  }
+}
+
+size_t ew_smem_bytes() { return 4ull * (EW_TW + EW_WARPS * (32 * EW_PRIV + EW_IMG)); }
 
 // ------------------------------------------------------------------------------------------------
 // decode: one thread per chunk, warp-synchronous staging.  Lane l of a warp decodes chunk
@@ -862,17 +1058,44 @@ int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const
   }
   if (!payload || !scratch) return SZ3G_EINVAL;
   const int sms = sm_count_hf();
-  const unsigned gw = (unsigned)std::min<uint64_t>((nch * 32 + 255) / 256, (uint64_t)sms * 16);
-  k_huff_chunk_words<<<gw, 256, 0, st>>>(codes, n, chunk, codewords, nsym, chunk_offsets, nch, d_status);
+  // full 2048-code chunks take the windowed fast path, the rest (a ragged last chunk, another chunk
+  // size, unaligned codes) the generic kernels
+  const uint64_t nfull = (chunk == EW_CHUNK && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) ? n / EW_CHUNK : 0;
+  const uint64_t nrest = nch - nfull;
+  const unsigned gf = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nfull + EW_WARPS - 1) / EW_WARPS, (uint64_t)sms));
+  int nl = 0;
+  if (nfull) {
+    k_huff_chunk_words_full<<<gf, EW_WARPS * 32, 0, st>>>(codes, nfull, codewords, nsym, chunk_offsets, d_status);
+    nl++;
+  }
+  if (nrest) {
+    const unsigned gw = (unsigned)std::min<uint64_t>((nrest * 32 + 255) / 256, (uint64_t)sms * 16);
+    k_huff_chunk_words<<<gw, 256, 0, st>>>(codes, n, chunk, codewords, nsym, chunk_offsets, nch, d_status, nfull);
+    nl++;
+  }
   const uint64_t nb = (nch + SCAN_TILE - 1) / SCAN_TILE;
   uint64_t* sums = reinterpret_cast<uint64_t*>(scratch);
   k_scan_sums<<<(unsigned)nb, SCAN_T, 0, st>>>(chunk_offsets, nch, sums);
   k_scan_top<<<1, SCAN_T, 0, st>>>(sums, nb);
   k_scan_apply<<<(unsigned)nb, SCAN_T, 0, st>>>(chunk_offsets, nch, sums, nb);
-  const unsigned ge = (unsigned)std::min<uint64_t>((nch + ENC_WARPS - 1) / ENC_WARPS, (uint64_t)sms * 8);
-  k_huff_encode<<<ge, ENC_WARPS * 32, 0, st>>>(codes, n, chunk, codewords, nsym, chunk_offsets, nch, payload,
-                                               payload_cap_words, d_status);
-  return hf_check(5);
+  if (nfull) {
+    const size_t smem = ew_smem_bytes();
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_huff_encode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_huff_encode_full<<<gf, EW_WARPS * 32, smem, st>>>(codes, nfull, codewords, nsym, chunk_offsets, payload,
+                                                        payload_cap_words, d_status);
+    nl++;
+  }
+  if (nrest) {
+    const unsigned ge = (unsigned)std::min<uint64_t>((nrest + ENC_WARPS - 1) / ENC_WARPS, (uint64_t)sms * 8);
+    k_huff_encode<<<ge, ENC_WARPS * 32, 0, st>>>(codes, n, chunk, codewords, nsym, chunk_offsets, nch, payload,
+                                                 payload_cap_words, d_status, nfull);
+    nl++;
+  }
+  return hf_check(nl + 3);
 }
 
 int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, uint64_t n, uint32_t chunk,
