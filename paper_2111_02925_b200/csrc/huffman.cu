@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
 // with the next lane is written by the lower lane, which receives the next lane's head bits by a
 // shuffle: every image word is written exactly once, no atomics, no zeroing.  The image leaves with
 // coalesced stores.
-constexpr int EW_TW = 8192, EW_WARPS = 16, EW_CHUNK = 2048, EW_PRIV = 33;
+constexpr int EW_TW = 8192, EW_WARPS = 16, EW_CHUNK = 2048, EW_PRIV = 35;   // odd row stride: no conflicts
 constexpr int EW_IMG = ENC_WORDS + 3;   // 1028 words per warp
 
 __device__ __forceinline__ uint32_t ew_lo(uint32_t nsym) { return nsym > EW_TW ? nsym / 2 - EW_TW / 2 : 0u; }
@@ -657,45 +657,56 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_chunk_words_full(cons
                                                                             uint32_t nsym,
                                                                             uint64_t* __restrict__ words,
                                                                             int32_t* status) {
-  __shared__ uint32_t s_len[EW_TW];
+  // byte table (4 symbols per bank word: few bank conflicts for codes concentrated near R): the code
+  // length, or 0x80 for a symbol without a codeword (OR-accumulated into the miss flag)
+  __shared__ uint8_t s_len[EW_TW];
   const uint32_t lo = ew_lo(nsym), lo2 = lo | (lo << 16);
   for (uint32_t i = threadIdx.x; i < EW_TW; i += blockDim.x) {
     const uint32_t L = lo + i < nsym ? __ldg(tab + lo + i) >> 24 : 0u;
-    s_len[i] = L + (L == 0 ? (1u << 20) : 0u);
+    s_len[i] = (uint8_t)(L ? L : 0x80u);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * EW_WARPS;
   uint64_t c = (uint64_t)blockIdx.x * EW_WARPS + (threadIdx.x >> 5);
+  if (c >= nfull) return;
   uint4 nx[8];
-  if (c < nfull) ew_load_chunk(codes, c, lane, nx);
+  ew_load_chunk(codes, c, lane, nx);
   for (; c < nfull; c += nw) {
     uint4 u[8];   // the sum does not care which lane holds which codes: no restaging
 #pragma unroll
     for (int v = 0; v < 8; v++) u[v] = nx[v];
-    if (c + nw < nfull) ew_load_chunk(codes, c + nw, lane, nx);
-    uint32_t acc = 0;
+    // unconditional prefetch (the last iteration reloads its own chunk): a predicated load would be
+    // merged into the live registers and waited for at once
+    ew_load_chunk(codes, c + nw < nfull ? c + nw : c, lane, nx);
+    uint32_t acc = 0, miss = 0;
 #pragma unroll
     for (int v = 0; v < 8; v++) {
       uint32_t d[4];
       if (__all_sync(0xffffffffu, ew_in_window(u[v], lo2, d))) {
 #pragma unroll
-        for (int k = 0; k < 4; k++) acc += s_len[d[k] & 0xffffu] + s_len[d[k] >> 16];
+        for (int k = 0; k < 4; k++) {
+          const uint32_t la = s_len[d[k] & 0xffffu], lb = s_len[d[k] >> 16];
+          acc += la + lb;
+          miss |= la | lb;
+        }
       } else {
         const uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
 #pragma unroll
         for (int h = 0; h < 8; h++) {
           const uint32_t q = (w[h >> 1] >> (16 * (h & 1))) & 0xffffu;
           const uint32_t L = q < nsym ? __ldg(tab + q) >> 24 : 0u;
-          acc += L + (L == 0 ? (1u << 20) : 0u);
+          acc += L;
+          miss |= L ? 0u : 0x80u;
         }
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const bool bad = __any_sync(0xffffffffu, (miss & 0x80u) != 0);
     if (lane == 0) {
-      if (acc >> 20) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
-      words[c] = ((acc & 0xfffffu) + 31) / 32;
+      if (bad) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
+      words[c] = (acc + 31) / 32;
     }
   }
 }
@@ -720,12 +731,21 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
   __syncthreads();
   const uint64_t nw = (uint64_t)gridDim.x * EW_WARPS;
   uint64_t c = (uint64_t)blockIdx.x * EW_WARPS + wl;
+  if (c >= nfull) return;
+  const bool vec_out = (reinterpret_cast<uintptr_t>(payload) & 15) == 0;
   uint4 nx[8];
-  if (c < nfull) ew_load_chunk(codes, c, lane, nx);
+  ew_load_chunk(codes, c, lane, nx);
+  uint64_t nw0 = offs[c], nw1 = offs[c + 1];
   for (; c < nfull; c += nw) {
     uint4 u[8];
     ew_restage(nx, reinterpret_cast<uint4*>(img), lane, u);   // the image is free until step (3)
-    if (c + nw < nfull) ew_load_chunk(codes, c + nw, lane, nx);
+    const uint64_t w0 = nw0, w1 = nw1;
+    {   // unconditional prefetch of the next chunk and its offsets (the last iteration reloads its own)
+      const uint64_t cn = c + nw < nfull ? c + nw : c;
+      ew_load_chunk(codes, cn, lane, nx);
+      nw0 = offs[cn];
+      nw1 = offs[cn + 1];
+    }
     // (1) pack the lane's 64 codes into its private buffer
     uint64_t acc = 0;
     uint32_t nb = 0, wi = 0;
@@ -761,7 +781,8 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
       }
     }
     const uint32_t bits = 32 * wi + nb;
-    if (nb) priv[wi] = (uint32_t)(acc << (32 - nb));
+    priv[wi] = nb ? (uint32_t)(acc << (32 - nb)) : 0u;   // the partial last word, or a zero sentinel
+    priv[wi + 1] = 0u;                                    // (3) reads up to word wi + 1
     // (2) the lane's first bit in the chunk
     uint32_t incl = bits;
 #pragma unroll
@@ -769,27 +790,39 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    const uint32_t b0 = incl - bits, sh = b0 & 31u, base = b0 >> 5;
-    const uint32_t nwp = (bits + 31) >> 5, nout = (sh + bits + 31) >> 5;
-    const uint32_t head = nwp ? priv[0] >> sh : 0u;
-    const uint32_t nhead = __shfl_down_sync(0xffffffffu, head, 1);
+    const uint32_t b0 = incl - bits, sh = b0 & 31u;
+    const uint32_t nout = (sh + bits + 31) >> 5;   // image words this lane's bits touch
+    const uint32_t p0 = priv[0];
+    const uint32_t nhead = __shfl_down_sync(0xffffffffu, p0 >> sh, 1);
     const bool nshare = lane < 31 && ((incl & 31u) != 0);   // my last word continues in the next lane
-    // (3) shifted copy into the chunk image; the first word, if shared, is the previous lane's
-    uint32_t prev = 0u;
-    for (uint32_t j = 0; j < nout; j++) {
-      const uint32_t cur = j < nwp ? priv[j] : 0u;
-      uint32_t val = (cur >> sh) | (sh ? prev << (32 - sh) : 0u);
+    // (3) shifted copy into the image, placed at word (w0 mod 4) so that the copy-out is 16-byte
+    // aligned on both sides.  Word j of the lane's span = (priv[j - 1] : priv[j]) >> sh; a shared first
+    // word (sh != 0) is written by the previous lane, which ORs in this lane's head.
+    const uint32_t a = (uint32_t)(w0 & 3u);
+    uint32_t* dst = img + a + (b0 >> 5);
+    uint32_t j = sh ? 1u : 0u, prev = sh ? p0 : 0u;
+    for (; j + 1 < nout; j++) {
+      const uint32_t cur = priv[j];
+      dst[j] = __funnelshift_r(cur, prev, sh);
       prev = cur;
-      if (j == nout - 1 && nshare) val |= nhead;
-      if (j > 0 || sh == 0) img[base + j] = val;
     }
+    if (j < nout) dst[j] = __funnelshift_r(priv[j], prev, sh) | (nshare ? nhead : 0u);
     __syncwarp();
     // (4) out
-    const uint64_t w0 = offs[c], nwords = offs[c + 1] - w0;
-    if (offs[c + 1] > cap) {
+    const uint32_t nwords = (uint32_t)(w1 - w0);
+    if (w1 > cap) {
       if (lane == 0) atomicOr(status, (int)SZ3G_STATUS_PAYLOAD_OVERFLOW);
     } else {
-      for (uint32_t i = lane; i < nwords; i += 32) payload[w0 + i] = img[i];
+      uint32_t* gout = payload + (w0 - a);    // 16-byte aligned when payload is
+      const uint32_t e_ = a + nwords, v0 = (a + 3) >> 2, v1 = e_ >> 2;
+      if (vec_out && v0 <= v1) {
+        for (uint32_t k = v0 + lane; k < v1; k += 32)
+          reinterpret_cast<uint4*>(gout)[k] = reinterpret_cast<const uint4*>(img)[k];
+        if (lane < 4 * v0 - a) gout[a + lane] = img[a + lane];               // head words
+        if (lane < e_ - 4 * v1) gout[4 * v1 + lane] = img[4 * v1 + lane];    // tail words
+      } else {
+        for (uint32_t i = a + lane; i < e_; i += 32) gout[i] = img[i];
+      }
     }
     __syncwarp();
   }

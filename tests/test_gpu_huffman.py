@@ -150,3 +150,48 @@ def test_config_code_streams(name):
     olens, ocws, offs, words = round_trip(q, hist)
     bits = int((hist * olens.astype(np.int64)).sum())
     print(name, "bits/code", bits / q.size, "words", int(offs[-1]))
+
+
+def test_full_chunk_path_alignments_and_window():
+    """The full-chunk fast path (2048-code chunks, 16-byte aligned codes) against the oracle's stream,
+    written into a 16-byte aligned payload and into one offset by a word (scalar copy-out), from
+    aligned codes and from codes offset by one element (generic kernels); codes spread over 65536
+    symbols so that warps leave the shared table window."""
+    s = sz()
+    rng = np.random.default_rng(11)
+    R = 32768
+    n = 2048 * 37 + 5
+    q = np.clip(np.round(rng.standard_cauchy(n + 1) * 40) + R, 0, 2 * R - 1).astype(np.uint16)
+    q[rng.random(n + 1) < 0.01] = rng.integers(0, 2 * R, size=int((rng.random(n + 1) < 0.01).sum()) or 1)[0]
+    hist = np.bincount(q, minlength=2 * R)
+    t, lens, cws = gpu_table(hist)
+    qd = torch.from_numpy(q).cuda()
+    for view in (qd[:n], qd[1:]):
+        q_np = view.cpu().numpy()
+        offs_o, words_o = oracle.huffman_encode(q_np, lens, cws, 2048)
+        for shift in (0, 1, 2, 3):
+            cap = int(offs_o[-1]) + 8
+            buf = torch.zeros(cap + shift, dtype=torch.int32, device="cuda")
+            hs = s.huffman_encode(view, t, payload=buf[shift:]).check()
+            assert np.array_equal(hs.offsets.cpu().numpy().view(np.uint64), offs_o)
+            got = buf[shift:shift + int(offs_o[-1])].cpu().numpy().view(np.uint32)
+            assert np.array_equal(got, words_o), f"payload (shift {shift})"
+            dec = s.huffman_decode(hs, t)
+            torch.cuda.synchronize()
+            assert np.array_equal(dec.cpu().numpy(), q_np)
+
+
+def test_full_chunk_path_flags_missing_codeword():
+    """A code without a codeword inside full chunks (in the table window, and >= nsym) is flagged."""
+    s = sz()
+    R = 512
+    q = np.full(2048 * 4, R, np.uint16)
+    q[::7] = R + 1
+    hist = np.bincount(q, minlength=2 * R)
+    t, *_ = gpu_table(hist)
+    for bad_code in (R + 5, 2 * R + 3):
+        qb = q.copy()
+        qb[3000] = bad_code
+        hs = s.huffman_encode(torch.from_numpy(qb).cuda(), t)
+        torch.cuda.synchronize()
+        assert int(hs.status.item()) & s.STATUS_BAD_HUFFMAN

@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--setting", default="")
     ap.add_argument("--build", action="store_true")
     ap.add_argument("--path", default="fused", choices=["fused", "two-pass"])
+    ap.add_argument("--tool", default="tune.py", help="tools/<tool> printing tune.py's JSON (e.g. huff_time.py)")
     ap.add_argument("variants", nargs="+")
     a = ap.parse_args()
     vs = [v.split("=", 1) for v in a.variants]
@@ -57,7 +58,7 @@ def main():
     for r in range(a.rounds):
         for n, path in vs:
             env = dict(os.environ, SZ3G_LIB=os.path.join(ROOT, path) if not os.path.isabs(path) else path)
-            out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tune.py"), "--config", a.config,
+            out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", a.tool), "--config", a.config,
                                   "--reps", str(a.reps), "--rounds", "1", "--path", a.path, a.setting or "CHUNK_C=2"],
                                  env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
