@@ -607,20 +607,21 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
 // The codes of a field concentrate around the radius (the histogram's mass is near R), so each CTA
 // stages a window of EW_TW table entries centred on nsym / 2 in shared memory and looks codes up there;
 // a group of 8 codes with any code outside the window takes the global table for that group (warp
-// vote).  One warp per chunk, lane l owning codes [64 l, 64 l + 64); the chunk is loaded one chunk
-// ahead into registers with coalesced 16-byte loads and restaged through shared memory.
+// vote).  One warp per chunk; chunks are loaded one chunk ahead into registers with coalesced 16-byte
+// loads (load v of lane l = uint4 32 v + l of the chunk).
 //
-// k_huff_chunk_words_full: window entries L + (L == 0) << 20 summed with one add per code (bits in the
-// low 20 bits, missing symbols counted above).
-// k_huff_encode_full: ONE lookup per code.  Each lane packs its 64 codes MSB-first into a private
-// word buffer in shared memory starting at bit 0 (pairs of codes are first joined into one <= 32-bit
-// unit, then appended to a 64-bit accumulator), a warp scan gives its first bit in the chunk, and it
-// copies its private words into the chunk image shifted by (first bit mod 32).  The word a lane shares
-// with the next lane is written by the lower lane, which receives the next lane's head bits by a
-// shuffle: every image word is written exactly once, no atomics, no zeroing.  The image leaves with
-// coalesced stores.
-constexpr int EW_TW = 8192, EW_WARPS = 16, EW_CHUNK = 2048, EW_PRIV = 35;   // odd row stride: no conflicts
-constexpr int EW_IMG = ENC_WORDS + 3;   // 1028 words per warp
+// k_huff_chunk_words_full: the bit count of every group of 64 consecutive codes (uint4 8 g .. 8 g + 7
+// of the chunk) from a byte table of lengths -- the 8-lane sums of the coalesced layout -- then the
+// chunk's word count and, per group g, its first bit inside the chunk (u16, `loff`).
+// k_huff_encode_full: lane g owns group g (its 64 codes restaged through shared memory) and its first
+// bit is known from `loff`, so it packs its codes MSB-first straight into the chunk image at their
+// final place: pairs of codes are joined into one <= 32-bit unit and appended to a 64-bit accumulator,
+// every completed word is stored.  A lane that does not start on a word boundary stores its first word
+// with the previous lane's bits as zeros; after a warp barrier the previous lane ORs its partial last
+// word into it.  No atomics, no zeroing.  The image sits at word (w0 mod 4) so that it leaves with 16-byte stores.
+// A chunk holding a code without a codeword is flagged (BAD_HUFFMAN) and gets 0 words.
+constexpr int EW_TW = 8192, EW_WARPS = 16, EW_CHUNK = 2048;
+constexpr int EW_IMG = ENC_WORDS + 3;   // 1028 words per warp (a <= 3 words of alignment + 1025)
 
 __device__ __forceinline__ uint32_t ew_lo(uint32_t nsym) { return nsym > EW_TW ? nsym / 2 - EW_TW / 2 : 0u; }
 
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_chunk_words_full(cons
                                                                             const uint32_t* __restrict__ tab,
                                                                             uint32_t nsym,
                                                                             uint64_t* __restrict__ words,
+                                                                            uint16_t* __restrict__ loff,
                                                                             int32_t* status) {
   // byte table (4 symbols per bank word: few bank conflicts for codes concentrated near R): the code
   // length, or 0x80 for a symbol without a codeword (OR-accumulated into the miss flag)
@@ -673,21 +675,22 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_chunk_words_full(cons
   uint4 nx[8];
   ew_load_chunk(codes, c, lane, nx);
   for (; c < nfull; c += nw) {
-    uint4 u[8];   // the sum does not care which lane holds which codes: no restaging
+    uint4 u[8];
 #pragma unroll
     for (int v = 0; v < 8; v++) u[v] = nx[v];
     // unconditional prefetch (the last iteration reloads its own chunk): a predicated load would be
     // merged into the live registers and waited for at once
     ew_load_chunk(codes, c + nw < nfull ? c + nw : c, lane, nx);
-    uint32_t acc = 0, miss = 0;
+    uint32_t sv[8], miss = 0;   // sv[v]: bits of the lane's uint4 32 v + lane
 #pragma unroll
     for (int v = 0; v < 8; v++) {
       uint32_t d[4];
+      sv[v] = 0;
       if (__all_sync(0xffffffffu, ew_in_window(u[v], lo2, d))) {
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           const uint32_t la = s_len[d[k] & 0xffffu], lb = s_len[d[k] >> 16];
-          acc += la + lb;
+          sv[v] += la + lb;
           miss |= la | lb;
         }
       } else {
@@ -696,17 +699,41 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_chunk_words_full(cons
         for (int h = 0; h < 8; h++) {
           const uint32_t q = (w[h >> 1] >> (16 * (h & 1))) & 0xffffu;
           const uint32_t L = q < nsym ? __ldg(tab + q) >> 24 : 0u;
-          acc += L;
+          sv[v] += L;
           miss |= L ? 0u : 0x80u;
         }
       }
     }
+    // uint4 32 v + l belongs to group 4 v + l / 8, so group 4 v + s is the sum of sv[v] over the 8
+    // lanes of segment s.  Butterfly reduce-scatter inside the segment (7 shuffles): afterwards lane l
+    // holds the sum for v = l & 7, i.e. group 4 (l & 7) + l / 8; one more shuffle gives lane g group g.
+    uint32_t r4[4], r2[2];
+    {
+      const bool hb = (lane >> 2) & 1;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      for (int j = 0; j < 4; j++)
+        r4[j] = (hb ? sv[j + 4] : sv[j]) + __shfl_xor_sync(0xffffffffu, hb ? sv[j] : sv[j + 4], 4);
+    }
+    {
+      const bool hb = (lane >> 1) & 1;
+#pragma unroll
+      for (int j = 0; j < 2; j++)
+        r2[j] = (hb ? r4[j + 2] : r4[j]) + __shfl_xor_sync(0xffffffffu, hb ? r4[j] : r4[j + 2], 2);
+    }
+    const bool hb0 = lane & 1;
+    const uint32_t fin = (hb0 ? r2[1] : r2[0]) + __shfl_xor_sync(0xffffffffu, hb0 ? r2[0] : r2[1], 1);
+    const uint32_t mine = __shfl_sync(0xffffffffu, fin, 8 * (lane & 3) + (lane >> 2));
     const bool bad = __any_sync(0xffffffffu, (miss & 0x80u) != 0);
-    if (lane == 0) {
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    loff[c * 32 + lane] = bad ? (uint16_t)0 : (uint16_t)(incl - mine);
+    if (lane == 31) {
       if (bad) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
-      words[c] = (acc + 31) / 32;
+      words[c] = bad ? 0 : (incl + 31) / 32;
     }
   }
 }
@@ -716,13 +743,13 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
                                                                        const uint32_t* __restrict__ tab,
                                                                        uint32_t nsym,
                                                                        const uint64_t* __restrict__ offs,
+                                                                       const uint16_t* __restrict__ loff,
                                                                        uint32_t* __restrict__ payload, uint64_t cap,
                                                                        int32_t* status) {
   extern __shared__ __align__(16) uint32_t esm[];
   uint32_t* s_tab = esm;                                   // [EW_TW] (L << 16) | codeword
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  uint32_t* priv = esm + EW_TW + wl * (32 * EW_PRIV) + lane * EW_PRIV;
-  uint32_t* img = esm + EW_TW + EW_WARPS * 32 * EW_PRIV + wl * EW_IMG;
+  uint32_t* img = esm + EW_TW + wl * EW_IMG;
   const uint32_t lo = ew_lo(nsym), lo2 = lo | (lo << 16), smax = nsym - 1;
   for (uint32_t i = threadIdx.x; i < EW_TW; i += blockDim.x) {
     const uint32_t t = lo + i < nsym ? __ldg(tab + lo + i) : 0u;
@@ -736,19 +763,25 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
   uint4 nx[8];
   ew_load_chunk(codes, c, lane, nx);
   uint64_t nw0 = offs[c], nw1 = offs[c + 1];
+  uint32_t nb0 = loff[c * 32 + lane];
   for (; c < nfull; c += nw) {
     uint4 u[8];
-    ew_restage(nx, reinterpret_cast<uint4*>(img), lane, u);   // the image is free until step (3)
     const uint64_t w0 = nw0, w1 = nw1;
+    const uint32_t b0 = nb0;
+    const uint32_t a = (uint32_t)(w0 & 3u);
+    ew_restage(nx, reinterpret_cast<uint4*>(img), lane, u);   // the image is free until packing
     {   // unconditional prefetch of the next chunk and its offsets (the last iteration reloads its own)
       const uint64_t cn = c + nw < nfull ? c + nw : c;
       ew_load_chunk(codes, cn, lane, nx);
       nw0 = offs[cn];
       nw1 = offs[cn + 1];
+      nb0 = loff[cn * 32 + lane];
     }
-    // (1) pack the lane's 64 codes into its private buffer
+    // pack: the accumulator starts with (b0 mod 32) zero bits (the previous lane's part of the first word)
+    const uint32_t sh = b0 & 31u;
+    uint32_t* dst = img + a + (b0 >> 5);
     uint64_t acc = 0;
-    uint32_t nb = 0, wi = 0;
+    uint32_t nb = sh, wi = 0;
 #pragma unroll
     for (int v = 0; v < 8; v++) {
       uint32_t d[4], e[8];
@@ -776,39 +809,18 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
         nb += pl;
         if (nb >= 32) {
           nb -= 32;
-          priv[wi++] = (uint32_t)(acc >> nb);
+          dst[wi++] = (uint32_t)(acc >> nb);
         }
       }
     }
-    const uint32_t bits = 32 * wi + nb;
-    priv[wi] = nb ? (uint32_t)(acc << (32 - nb)) : 0u;   // the partial last word, or a zero sentinel
-    priv[wi + 1] = 0u;                                    // (3) reads up to word wi + 1
-    // (2) the lane's first bit in the chunk
-    uint32_t incl = bits;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const uint32_t b0 = incl - bits, sh = b0 & 31u;
-    const uint32_t nout = (sh + bits + 31) >> 5;   // image words this lane's bits touch
-    const uint32_t p0 = priv[0];
-    const uint32_t nhead = __shfl_down_sync(0xffffffffu, p0 >> sh, 1);
-    const bool nshare = lane < 31 && ((incl & 31u) != 0);   // my last word continues in the next lane
-    // (3) shifted copy into the image, placed at word (w0 mod 4) so that the copy-out is 16-byte
-    // aligned on both sides.  Word j of the lane's span = (priv[j - 1] : priv[j]) >> sh; a shared first
-    // word (sh != 0) is written by the previous lane, which ORs in this lane's head.
-    const uint32_t a = (uint32_t)(w0 & 3u);
-    uint32_t* dst = img + a + (b0 >> 5);
-    uint32_t j = sh ? 1u : 0u, prev = sh ? p0 : 0u;
-    for (; j + 1 < nout; j++) {
-      const uint32_t cur = priv[j];
-      dst[j] = __funnelshift_r(cur, prev, sh);
-      prev = cur;
-    }
-    if (j < nout) dst[j] = __funnelshift_r(priv[j], prev, sh) | (nshare ? nhead : 0u);
+    // the partial last word continues in the next lane, which has stored its part there (its first
+    // word, the upper bits zero); lane 31's is the chunk's zero-padded last word
     __syncwarp();
-    // (4) out
+    const uint32_t nhead = (nb && lane < 31) ? dst[wi] : 0u;
+    __syncwarp();
+    if (nb) dst[wi] = (uint32_t)(acc << (32 - nb)) | nhead;
+    __syncwarp();
+    // out
     const uint32_t nwords = (uint32_t)(w1 - w0);
     if (w1 > cap) {
       if (lane == 0) atomicOr(status, (int)SZ3G_STATUS_PAYLOAD_OVERFLOW);
@@ -828,7 +840,8 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
   }
 }
 
-size_t ew_smem_bytes() { return 4ull * (EW_TW + EW_WARPS * (32 * EW_PRIV + EW_IMG)); }
+size_t ew_smem_bytes() { return 4ull * (EW_TW + EW_WARPS * EW_IMG); }
+
 
 // ------------------------------------------------------------------------------------------------
 // decode: one thread per chunk, warp-synchronous staging.  Lane l of a warp decodes chunk
@@ -1039,6 +1052,14 @@ int sm_count_hf() {
 
 }  // namespace
 
+// encode scratch: the scan's block sums, then (256-byte aligned) the first bit of every 64-code group
+// of the full chunks (u16, 32 per chunk)
+uint64_t enc_nfull(uint64_t n, uint32_t chunk) { return chunk == EW_CHUNK ? n / EW_CHUNK : 0; }
+uint64_t enc_loff_offset(uint64_t n, uint32_t chunk) {
+  const uint64_t nch = chunk ? (n + chunk - 1) / chunk : 0;
+  return (8 * ((nch + SCAN_TILE - 1) / SCAN_TILE + 2) + 255) / 256 * 256;
+}
+
 // launches of this translation unit (folded into sz3g_launch_count)
 uint64_t sz3g_huffman_launch_count_internal() { return g_hf_launches.load(); }
 
@@ -1047,8 +1068,7 @@ extern "C" {
 uint64_t sz3g_huffman_scratch_bytes(uint32_t nsym, uint32_t max_len) { return cb_scratch_bytes(nsym, max_len); }
 uint64_t sz3g_huffman_dtable_bytes(uint32_t nsym) { return dtable_bytes(nsym); }
 uint64_t sz3g_huffman_encode_scratch_bytes(uint64_t n, uint32_t chunk) {
-  const uint64_t nch = chunk ? (n + chunk - 1) / chunk : 0;
-  return 8 * ((nch + SCAN_TILE - 1) / SCAN_TILE + 2);
+  return enc_loff_offset(n, chunk) + 64 * enc_nfull(n, chunk);
 }
 
 int sz3g_huffman_codebook_from_lengths(const uint8_t* lengths, uint32_t nsym, uint32_t max_len,
@@ -1093,12 +1113,14 @@ int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const
   const int sms = sm_count_hf();
   // full 2048-code chunks take the windowed fast path, the rest (a ragged last chunk, another chunk
   // size, unaligned codes) the generic kernels
-  const uint64_t nfull = (chunk == EW_CHUNK && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) ? n / EW_CHUNK : 0;
+  const uint64_t nfull = (reinterpret_cast<uintptr_t>(codes) & 15) == 0 ? enc_nfull(n, chunk) : 0;
+  uint16_t* loff = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(scratch) + enc_loff_offset(n, chunk));
   const uint64_t nrest = nch - nfull;
   const unsigned gf = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nfull + EW_WARPS - 1) / EW_WARPS, (uint64_t)sms));
   int nl = 0;
   if (nfull) {
-    k_huff_chunk_words_full<<<gf, EW_WARPS * 32, 0, st>>>(codes, nfull, codewords, nsym, chunk_offsets, d_status);
+    k_huff_chunk_words_full<<<gf, EW_WARPS * 32, 0, st>>>(codes, nfull, codewords, nsym, chunk_offsets, loff,
+                                                          d_status);
     nl++;
   }
   if (nrest) {
@@ -1118,8 +1140,8 @@ int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const
       cudaFuncSetAttribute(k_huff_encode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    k_huff_encode_full<<<gf, EW_WARPS * 32, smem, st>>>(codes, nfull, codewords, nsym, chunk_offsets, payload,
-                                                        payload_cap_words, d_status);
+    k_huff_encode_full<<<gf, EW_WARPS * 32, smem, st>>>(codes, nfull, codewords, nsym, chunk_offsets, loff,
+                                                        payload, payload_cap_words, d_status);
     nl++;
   }
   if (nrest) {
