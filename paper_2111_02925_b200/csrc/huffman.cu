@@ -897,7 +897,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
                                                                 const uint64_t* __restrict__ offs, uint64_t n,
                                                                 uint32_t chunk, const DTab* __restrict__ dt,
                                                                 uint32_t max_len, uint16_t* __restrict__ codes,
-                                                                uint64_t nch, int32_t* status) {
+                                                                uint64_t nch, int32_t* status, uint64_t c_begin) {
   extern __shared__ __align__(16) uint32_t dsm[];
   uint32_t* s_lut = dsm;                                  // 4096
   uint32_t* s_first = s_lut + (1 << HF_LUT_BITS);         // 32
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
   uint32_t* out_w = s_out + wl * 32 * OUT_P;
   uint32_t* out = out_w + lane * OUT_P;
   const uint16_t* syms = reinterpret_cast<const uint16_t*>(dt + 1);
-  const uint64_t cbase = ((uint64_t)blockIdx.x * DEC_WARPS + wl) * 32;
+  const uint64_t cbase = c_begin + ((uint64_t)blockIdx.x * DEC_WARPS + wl) * 32;
   if (cbase >= nch) return;
   const uint64_t c = cbase + lane;
   const bool live = c < nch;
@@ -1033,6 +1033,188 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
 size_t dec_smem_bytes() {
   return 4ull * ((1 << HF_LUT_BITS) + 3 * HF_MAXL + DEC_WARPS * 32 * (RING_P + OUT_P));
 }
+
+// ------------------------------------------------------------------------------------------------
+// Full-chunk decoder (chunk = 2048 codes, 16-byte aligned payload and codes): one chunk per lane, as
+// k_huff_decode, but each lane streams its own payload words through a private ring in
+// shared memory (16 words) filled by cp.async (asynchronous global -> shared copies, zero-filled past
+// the end of the payload) every 8 codes, so no cooperative top-up and no registers waiting on loads.  Per pair of codes: two 12-bit LUT lookups from the 64-bit window and ONE warp vote
+// for codes longer than the LUT (then the pair is decoded code by code with the canonical search).  The
+// window takes one ring word whenever it holds <= 32 bits (predicated).  A round's 32 codes stay in
+// registers and leave through a swizzled shared-memory stage with 16-byte stores (4 lanes per 64-byte
+// chunk row).
+constexpr int DF_WARPS = 8, DF_ROUND = 32, DF_RING = 16, DF_RING_W = 20;   // ring: 16 words, 80-byte row stride
+#ifndef SZ3G_DF_DIRECT
+#define SZ3G_DF_DIRECT 0   // 1: a round's codes leave with the lane's own 16-byte stores (no staging)
+#endif
+#ifndef SZ3G_DF_MINB
+#define SZ3G_DF_MINB 4     // __launch_bounds__ minimum blocks per SM: 4 x 8 warps (smem allows 4)
+#endif
+
+struct DfLane {
+  uint64_t buf;     // left-aligned bit window
+  uint32_t avail;   // valid bits in buf
+  uint32_t rpos;    // next ring word to read (mod DF_RING), counted from the aligned chunk start
+  uint32_t fpos;    // ring words requested so far (16-byte copies of 4 words)
+  uint32_t nref;    // words appended to the window
+};
+
+__device__ __forceinline__ void df_copy16(uint32_t s_dst, const uint32_t* __restrict__ payload, uint64_t p,
+                                          uint64_t lim) {
+  const uint32_t bytes = p >= lim ? 0u : (lim - p >= 4 ? 16u : (uint32_t)(4 * (lim - p)));
+  const uint32_t* src = payload + (p < lim ? p : 0);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s_dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void df_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void df_wait2() { asm volatile("cp.async.wait_group 2;\n" ::: "memory"); }
+
+// top the ring up towards DF_RING = 16 words ahead of the read position (<= K copies of 4 words) and
+// wait for the copies requested before the previous call.  Every quarter round (8 codes, <= 4 words
+// read) calls it with K = 1: with g = requested - read at a call, the next call sees g' >=
+// min(g + 4, 13) - 4 >= min(g, 9), and g starts at 14 (16 words, 2 of them in the primed window); the
+// words requested before the previous call reach >= g_prev - 4 >= 5 >= 4 words past the read position.
+template <int K>
+__device__ __forceinline__ void df_topup(DfLane& d, uint32_t s_ring, const uint32_t* __restrict__ payload,
+                                         uint64_t a0, uint64_t lim) {
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    if (d.fpos + 4 <= d.rpos + DF_RING) {
+      df_copy16(s_ring + 4u * (d.fpos & (DF_RING - 1)), payload, a0 + d.fpos, lim);
+      d.fpos += 4;
+    }
+  }
+  df_commit();
+  df_wait2();
+}
+
+// append one ring word when the window holds <= 32 bits
+__device__ __forceinline__ void df_refill(DfLane& d, const uint32_t* ring) {
+  if (d.avail <= 32) {
+    const uint32_t w = ring[d.rpos & (DF_RING - 1)];
+    d.buf |= (uint64_t)w << (32u - d.avail);
+    d.avail += 32u;
+    d.nref++;
+    d.rpos++;
+  }
+}
+
+// one code, any length (LUT, else the canonical search of k_huff_decode's dec_one)
+__device__ __forceinline__ uint32_t df_code(DfLane& d, const uint32_t* s_lut, const uint32_t* s_ljl,
+                                            const uint32_t* s_first, const uint32_t* s_base,
+                                            const uint16_t* __restrict__ syms, uint32_t maxl, bool& bad) {
+  const uint32_t top = (uint32_t)(d.buf >> 48);
+  const uint32_t ent = s_lut[top >> (16 - HF_LUT_BITS)];
+  uint32_t L = ent >> 16, sym = ent & 0xffffu;
+  if (ent == 0u) {
+    L = HF_LUT_BITS + 1 + (top >= s_ljl[13] ? 1u : 0u) + (top >= s_ljl[14] ? 1u : 0u) + (top >= s_ljl[15] ? 1u : 0u);
+    if (L > maxl || top >= s_ljl[L]) { bad = true; L = 1; sym = 0; }
+    else sym = syms[s_base[L] + (top >> (16 - L)) - s_first[L]];
+  }
+  d.buf <<= L;
+  d.avail -= L;
+  return sym;
+}
+
+__global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_full(const uint32_t* __restrict__ payload,
+                                                                    const uint64_t* __restrict__ offs, uint64_t nch,
+                                                                    uint64_t nfull, const DTab* __restrict__ dt,
+                                                                    uint32_t max_len, uint16_t* __restrict__ codes,
+                                                                    int32_t* status) {
+  extern __shared__ __align__(16) uint32_t dsm[];
+  uint32_t* s_lut = dsm;                                  // 4096
+  uint32_t* s_first = s_lut + (1 << HF_LUT_BITS);         // 32
+  uint32_t* s_base = s_first + HF_MAXL;
+  uint32_t* s_ljl = s_base + HF_MAXL;
+  uint32_t* s_rings = s_ljl + HF_MAXL;                    // [DF_WARPS * 32][DF_RING_W]
+  uint4* s_out = reinterpret_cast<uint4*>(s_rings + DF_WARPS * 32 * DF_RING_W);   // [DF_WARPS][128] uint4
+  for (int i = threadIdx.x; i < (1 << HF_LUT_BITS); i += blockDim.x) s_lut[i] = dt->lut[i];
+  if (threadIdx.x < HF_MAXL) {
+    const uint32_t l = threadIdx.x;
+    s_first[l] = dt->first[l];
+    s_base[l] = dt->base[l];
+    s_ljl[l] = (l >= 1 && l <= max_len) ? (uint32_t)(((uint64_t)dt->first[l] + dt->count[l]) << (16 - l))
+                                        : (l > max_len ? 0x10000u : 0u);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const uint64_t c0 = ((uint64_t)blockIdx.x * DF_WARPS + wl) * 32;
+  if (c0 >= nfull) return;
+  const uint16_t* syms = reinterpret_cast<const uint16_t*>(dt + 1);
+  uint4* so = s_out + wl * 128;
+  const uint32_t* ring = s_rings + threadIdx.x * DF_RING_W;
+  const uint32_t s_ring = (uint32_t)__cvta_generic_to_shared(ring);
+  const bool live = c0 + lane < nfull;
+  const uint64_t c = live ? c0 + lane : nfull - 1;   // a dead lane decodes the last full chunk again, unstored
+  const uint64_t lim = offs[nch];
+  const uint64_t w0 = offs[c], nwc = offs[c + 1] - w0;
+  DfLane d;
+  const uint64_t a0 = w0 & ~3ull;
+  d.rpos = (uint32_t)(w0 & 3u);
+  d.fpos = 0;
+  d.buf = 0;
+  d.avail = 0;
+  d.nref = 0;
+  df_topup<DF_RING / 4>(d, s_ring, payload, a0, lim);   // 16 words
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  df_refill(d, ring);                      // prime 64 bits
+  df_refill(d, ring);
+  bool bad = false;
+  const uint32_t maxl = max_len;
+  for (uint32_t e = 0; e < EW_CHUNK; e += DF_ROUND) {
+    uint32_t o[16];
+#pragma unroll
+    for (int h = 0; h < 16; h++) {
+      if ((h % 4 == 0) && (h || e)) df_topup<1>(d, s_ring, payload, a0, lim);
+      const uint64_t win0 = d.buf;
+      const uint32_t ea = s_lut[(uint32_t)(win0 >> (64 - HF_LUT_BITS))];
+      const uint32_t la = ea >> 16;
+      const uint64_t win1 = win0 << la;
+      const uint32_t eb = s_lut[(uint32_t)(win1 >> (64 - HF_LUT_BITS))];
+      const uint32_t lb = eb >> 16;
+      if (__any_sync(0xffffffffu, ea == 0u || eb == 0u)) {
+        const uint32_t a = df_code(d, s_lut, s_ljl, s_first, s_base, syms, maxl, bad);
+        const uint32_t b = df_code(d, s_lut, s_ljl, s_first, s_base, syms, maxl, bad);
+        o[h] = a | (b << 16);
+      } else {
+        d.buf = win1 << lb;
+        d.avail -= la + lb;
+        o[h] = (ea & 0xffffu) | (eb << 16);
+      }
+      df_refill(d, ring);
+    }
+    if (SZ3G_DF_DIRECT) {
+      if (live) {
+        uint4* dst = reinterpret_cast<uint4*>(codes + c * EW_CHUNK + e);
+#pragma unroll
+        for (int j = 0; j < 4; j++) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+      }
+      continue;
+    }
+    // stage: lane l's 4 uint4 at slots 4 l + j, swizzled (conflict-free both ways)
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint32_t i = 4 * lane + j;
+      so[i ^ ((i >> 3) & 3u)] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const uint32_t i = 32 * t + lane, r = i >> 2, j = i & 3u;
+      const uint4 v = so[i ^ ((i >> 3) & 3u)];
+      if (c0 + r < nfull) reinterpret_cast<uint4*>(codes + (c0 + r) * EW_CHUNK + e)[j] = v;
+    }
+    __syncwarp();
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  const uint64_t consumed = 32ull * d.nref - d.avail;
+  if (live && (bad || consumed > nwc * 32)) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
+}
+
+size_t df_smem_bytes() {
+  return 4ull * ((1 << HF_LUT_BITS) + 3 * HF_MAXL) + 4ull * DF_WARPS * 32 * DF_RING_W +
+         (SZ3G_DF_DIRECT ? 0ull : 16ull * 128 * DF_WARPS);
+}
+
 
 std::atomic<uint64_t> g_hf_launches{0};
 
@@ -1162,17 +1344,35 @@ int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, 
   if (reinterpret_cast<uintptr_t>(codes) & 15) return SZ3G_EINVAL;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const uint64_t nch = (n + chunk - 1) / chunk;
-  const size_t smem = dec_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_huff_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  // full 2048-code chunks of a 16-byte aligned payload: the register-queue decoder; the rest (a
+  // ragged last chunk, another chunk size) the ring decoder
+  const uint64_t nfull = (chunk == EW_CHUNK && (reinterpret_cast<uintptr_t>(payload) & 15) == 0) ? n / EW_CHUNK : 0;
+  int nl = 0;
+  if (nfull) {
+    const size_t smem = df_smem_bytes();
+    static bool attr_f = false;
+    if (!attr_f) {
+      cudaFuncSetAttribute(k_huff_decode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_f = true;
+    }
+    const uint64_t per_cta = 32ull * DF_WARPS;
+    k_huff_decode_full<<<(unsigned)((nfull + per_cta - 1) / per_cta), DF_WARPS * 32, smem, st>>>(
+        payload, chunk_offsets, nch, nfull, reinterpret_cast<const DTab*>(dtable), max_len, codes, d_status);
+    nl++;
   }
-  const uint64_t per_cta = 32ull * DEC_WARPS;
-  k_huff_decode<<<(unsigned)((nch + per_cta - 1) / per_cta), DEC_WARPS * 32, smem, st>>>(payload, chunk_offsets, n, chunk,
-                                                               reinterpret_cast<const DTab*>(dtable), max_len,
-                                                               codes, nch, d_status);
-  return hf_check(1);
+  if (nch > nfull) {
+    const size_t smem = dec_smem_bytes();
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_huff_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const uint64_t per_cta = 32ull * DEC_WARPS;
+    k_huff_decode<<<(unsigned)((nch - nfull + per_cta - 1) / per_cta), DEC_WARPS * 32, smem, st>>>(
+        payload, chunk_offsets, n, chunk, reinterpret_cast<const DTab*>(dtable), max_len, codes, nch, d_status, nfull);
+    nl++;
+  }
+  return hf_check(nl);
 }
 
 }  // extern "C"
