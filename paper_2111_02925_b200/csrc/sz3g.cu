@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(128) k_decompress_plain(const uint16_t* __rest
 // 16 B per block).  A group of G warps shares a stage; each warp decodes rows [j0, j0 + 6/G) into
 // its own shared row slab and TMA-stores it (box {96, 6/G, 6}).  The stage is released through an
 // empty barrier with G arrivals, so there is no group barrier at all.
-template <typename T, int G, int NG, int D>
+template <typename T, int G, int NG, int D, int OB = 1>
 struct DecompressSmem {
   static constexpr int P = BS / G;
   static constexpr int S = NG * D;
@@ -751,16 +751,16 @@ struct DecompressSmem {
   static constexpr size_t stage_bytes = code_bytes + 16 * 16;            // codes + 16 coefficient codes
   static constexpr size_t slab_bytes = sizeof(T) * BS * P * TK;          // one warp's output rows
   static constexpr size_t off_out = S * stage_bytes;
-  static constexpr size_t off_bar = off_out + (size_t)NG * G * slab_bytes;
+  static constexpr size_t off_bar = off_out + (size_t)NG * G * OB * slab_bytes;   // OB slabs per warp
   static constexpr size_t off_k = off_bar + 2 * S * sizeof(uint64_t);
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
 };
 
-template <typename T, int G, int NG, int D>
+template <typename T, int G, int NG, int D, int OB = 1>
 __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     k_decompress_tma(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_x,
                      const int32_t* __restrict__ coef, KArgs a) {
-  using L_ = DecompressSmem<T, G, NG, D>;
+  using L_ = DecompressSmem<T, G, NG, D, OB>;
   constexpr int P = L_::P;
   constexpr int S = L_::S;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -805,14 +805,15 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
     // ---------------- consumer groups: warp wg of group grp decodes rows [j0, j0 + P)
     const int grp = warp / G, wg = warp - grp * G, j0 = wg * P;
     const Consts K = *s_k;
-    T* myout = obuf + (size_t)warp * (BS * P * TK);
+    T* myout0 = obuf + (size_t)warp * OB * (BS * P * TK);
     uint32_t k = 0;
     for (TileWalk tw(grp, a.chunk, NG);; tw.next(), k++) {
       const uint64_t t = tw.tile();
       if (t >= g.ntiles) break;
       const uint32_t s = grp * D + k % D, ph = (k / D) & 1u;
       const TileCoord tc = decode_tile(t, g);
-      if (lane == 0) ptx::bulk_wait_read0();   // my previous slab store finished reading myout
+      T* myout = myout0 + (size_t)(OB > 1 ? k % OB : 0) * (BS * P * TK);
+      if (lane == 0) ptx::bulk_wait_read<OB - 1>();   // the store that last used this slab has read it
       __syncwarp();
       ptx::mbar_wait(&full[s], ph);
       const uint8_t* st = stages + (size_t)s * L_::stage_bytes;
@@ -1042,9 +1043,12 @@ uint32_t prefetch_tiles() { return (uint32_t)std::max<int64_t>(0, tuning("PF"));
 constexpr int CN32 = 5, CQ32 = 2, CD32 = 2;  // f32 compress: 5 groups x (1 moment + 2 quantise warps) + producer = 16 warps
 constexpr int CN64 = 3, CQ64 = 3, CD64 = 2;  // f64 compress: 3 groups x (1 + 3) warps + producer = 13 warps
 #ifndef SZ3G_DEC_CFG
-#define SZ3G_DEC_CFG 0   // f32 decompress shape (A/B tuning): 0 = 5 x 3 warps, 3-deep; 1 = 7 x 3 warps, 2-deep
+#define SZ3G_DEC_CFG 2   // f32 decompress shape (A/B tuning): 0 = 5 x 3 warps, 3-deep; 1 = 7 x 3 warps, 2-deep;
+                         // 2 = 5 x 3, 2-deep, 2 output slabs per warp; 3 = 4 x 3, 3-deep, 2 slabs
 #endif
-constexpr int DG32 = 3, DN32 = SZ3G_DEC_CFG == 1 ? 7 : 5, DD32 = SZ3G_DEC_CFG == 1 ? 2 : 3;  // f32 decompress: groups of 3 warps + producer
+constexpr int DG32 = 3, DN32 = SZ3G_DEC_CFG == 1 ? 7 : (SZ3G_DEC_CFG == 3 ? 4 : 5),
+              DD32 = (SZ3G_DEC_CFG == 1 || SZ3G_DEC_CFG == 2) ? 2 : 3,
+              DOB32 = SZ3G_DEC_CFG >= 2 ? 2 : 1;  // f32 decompress: groups of 3 warps + producer
 constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 warps + producer
 constexpr int AW32 = 8, AD32 = 2;            // f32 analyze: 8 self-fed warps x 2 stages (13.5 KiB)
 constexpr int AW64 = 4, AD64 = 2;            // f64 analyze: 4 warps x 2 stages (27 KiB)
@@ -1067,16 +1071,16 @@ int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes
   return check_launch(1);
 }
 
-template <typename T, int G, int NG, int D>
+template <typename T, int G, int NG, int D, int OB = 1>
 int launch_decompress_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, void* xo, const KArgs& ka,
                           cudaStream_t st) {
-  using L = DecompressSmem<T, G, NG, D>;
+  using L = DecompressSmem<T, G, NG, D, OB>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mc, mx;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) return SZ3G_ECUDA;
   if (!make_map(&mx, dt, sizeof(T), xo, g, L::P, true)) return SZ3G_ECUDA;
-  auto kern = k_decompress_tma<T, G, NG, D>;
+  auto kern = k_decompress_tma<T, G, NG, D, OB>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
@@ -1293,7 +1297,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
   int launched = 0;
   if (grid->dtype == SZ3G_F32) {
     if (tma) {
-      rc = launch_decompress_tma<float, DG32, DN32, DD32>(g, codes, coef_codes, x_out, ka, st);
+      rc = launch_decompress_tma<float, DG32, DN32, DD32, DOB32>(g, codes, coef_codes, x_out, ka, st);
       if (rc) return rc;
     } else {
       const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
