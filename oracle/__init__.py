@@ -5,7 +5,7 @@ linear-scaling quantisation (sz3_oracle.cpp: PAPER.md Lemma 1, predictio
 P:406-409, App. A loop P:980-992, value-range eb P:833), of the Huffman encoder stage
 (huffman_oracle.cpp: P:156), of SZ3-Truncation and the coefficient delta coding
 (truncation_oracle.cpp: P:848-850) and of the distortion metrics (below: P:525); the exact
-definitions are oracle/DEFINITION.md (O1-O11, D, H1-H5, T1-T2, C1-C2, M1-M3).  Only ``tests/``, ``__graft_entry__.smoke()`` and
+definitions are oracle/DEFINITION.md (O1-O11, D, H1-H5, T1-T2, C1-C2, M1-M3, L1-L7: SZ3-LR).  Only ``tests/``, ``__graft_entry__.smoke()`` and
 ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this package.  It shares
 no code with ``paper_2111_02925_b200`` and never imports it.
 """
@@ -79,6 +79,11 @@ def _load():
             lib.orc_coef_delta_encode.argtypes = [P, U64, P, P, U64]
             lib.orc_coef_delta_encode.restype = U64
             lib.orc_coef_delta_decode.argtypes = [P, U64, P, U64, P]
+            lib.orc_lr_compress.argtypes = [I32, P, U64, U32, U32, I32, D, P, P, P, P, P, P, P, P, P, U64, P, P, P,
+                                            P, P]
+            lib.orc_lr_decompress.argtypes = [I32, P, U64, U32, U32, D, P, P, P, P, P, U64, P]
+            lib.orc_lr_delta.argtypes = [P, I32, I32, I32, I32, I32, I32]
+            lib.orc_lr_delta.restype = ctypes.c_int64
             _lib = lib
     return _lib
 
@@ -339,3 +344,72 @@ def coef_delta_decode(sym: np.ndarray, nb: int, esc: np.ndarray) -> np.ndarray:
     if _load().orc_coef_delta_decode(_ptr(sym), nb, _ptr(esc), esc.size, _ptr(c)) != 0:
         raise ValueError("escapes exhausted")
     return c
+
+
+# ------------------------------------------------------------------------------------------- SZ3-LR
+# The composite Lorenzo / regression predictor (DEFINITION.md L1-L7; sz3_oracle.cpp lr_*).
+@dataclass
+class LRCompressed(Compressed):
+    flags: np.ndarray | None = None    # uint8 [NB]: 1 = Lorenzo block, 0 = regression block
+    n_lorenzo: int = 0
+
+
+def lr_compress(x: np.ndarray, eb: float, eb_mode: str = "rel", radius: int = 32768, dim0_offset: int = 0,
+                value_range_override: tuple | None = None, B: int = BLOCK) -> LRCompressed:
+    """L1-L6 over a 3D field (1D/2D embedded with leading extents 1)."""
+    x = np.ascontiguousarray(x)
+    shape = (1,) * (3 - x.ndim) + tuple(x.shape)
+    dims = np.array(shape, np.uint64)
+    N = int(np.prod(shape))
+    nb = num_blocks(dims, B)
+    codes = np.empty(shape, np.uint16)
+    coef = np.empty((nb, 4), np.int32)
+    coef_raw = np.empty((nb, 4), np.float64)
+    exempt = np.empty(nb, np.uint8)
+    flags = np.empty(nb, np.uint8)
+    oidx = np.empty(N, np.uint64)
+    oval = np.empty(N, x.dtype)
+    nout = np.zeros(1, np.uint64)
+    nlor = np.zeros(1, np.uint64)
+    hist = np.empty(2 * radius, np.int64)
+    eb_abs = np.zeros(1, np.float64)
+    xprime = np.empty(shape, x.dtype)
+    rng = None if value_range_override is None else np.array(value_range_override, np.float64)
+    rc = _load().orc_lr_compress(_dtype_id(x.dtype), _ptr(dims), dim0_offset, B, radius, {"abs": 0, "rel": 1}[eb_mode],
+                                 float(eb), _ptr(rng), _ptr(x), _ptr(codes), _ptr(coef), _ptr(coef_raw), _ptr(exempt),
+                                 _ptr(flags), _ptr(oidx), _ptr(oval), N, _ptr(nout), _ptr(hist), _ptr(eb_abs),
+                                 _ptr(xprime), _ptr(nlor))
+    if rc != OK:
+        raise ValueError(f"orc_lr_compress rc={rc}")
+    n = int(nout[0])
+    return LRCompressed(tuple(int(s) for s in shape), x.dtype, radius, float(eb_abs[0]), codes, coef, coef_raw,
+                        exempt, oidx[:n].copy(), oval[:n].copy(), hist, {}, dim0_offset, xprime, flags,
+                        int(nlor[0]))
+
+
+def lr_decompress(c: LRCompressed | None = None, *, dims=None, dtype=None, radius=None, eb_abs=None, codes=None,
+                  coef_codes=None, flags=None, outlier_idx=None, outlier_val=None, dim0_offset=0,
+                  B: int = BLOCK) -> np.ndarray:
+    """L7."""
+    if c is not None:
+        dims, dtype, radius, eb_abs = c.dims, c.dtype, c.radius, c.eb_abs
+        codes, coef_codes, flags, outlier_idx, outlier_val, dim0_offset = (
+            c.codes, c.coef_codes, c.flags, c.outlier_idx, c.outlier_val, c.dim0_offset)
+    d = np.array(dims, np.uint64)
+    out = np.zeros(tuple(int(s) for s in dims), dtype)
+    codes = np.ascontiguousarray(codes, np.uint16)
+    coef_codes = np.ascontiguousarray(coef_codes, np.int32)
+    flags = np.ascontiguousarray(flags, np.uint8)
+    oidx = np.ascontiguousarray(outlier_idx, np.uint64)
+    oval = np.ascontiguousarray(outlier_val, dtype)
+    rc = _load().orc_lr_decompress(_dtype_id(dtype), _ptr(d), dim0_offset, B, radius, float(eb_abs), _ptr(codes),
+                                   _ptr(coef_codes), _ptr(flags), _ptr(oidx), _ptr(oval), oidx.size, _ptr(out))
+    if rc != OK:
+        raise ValueError(f"orc_lr_decompress rc={rc}")
+    return out
+
+
+def lr_delta(q: np.ndarray, i: int, j: int, k: int) -> int:
+    """L2 on one dense block of int64 values."""
+    q = np.ascontiguousarray(q, np.int64)
+    return int(_load().orc_lr_delta(_ptr(q), q.shape[0], q.shape[1], q.shape[2], i, j, k))

@@ -11,6 +11,8 @@
 //    * quantize / recover       P:400-404, App. A
 //    * block-then-element loop  App. A, Alg. 1
 //    * value-range-relative eb
+//    * SZ3-LR (NEXT-4)          P:845  Lorenzo / regression per block ("better result in between
+//                                      based on blockwise error estimation"); DEFINITION.md L1-L7
 //  Readings of silent / garbled passages (coefficient bins, tie rule, verify step, ...) are the
 //  ones listed in DESIGN.md section "Readings" (G1..G18) and in oracle/DEFINITION.md.
 //
@@ -330,6 +332,227 @@ int decompress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, ui
   return ORC_OK;
 }
 
+
+// ---------------------------------------------------------------- SZ3-LR (NEXT-4; DEFINITION.md L1-L7)
+// "a multialgorithm predictor ... a Lorenzo predictor and a regression-based predictor and predicts
+// data using the better result in between based on blockwise error estimation".  The paper's
+// Lorenzo section is empty (P:7); the readings are DESIGN G26-G29: the Lorenzo predictor works on the
+// prequantised values q = rint(x / 2eb) (L1), first order, block-local (L2); a block's choice is the
+// predictor with the smaller sum of |code - R| (outliers count R) over the block (L5).
+
+// L1: q = rint(x * inv2eb) (the O8 product with p = 0); not usable (q = 0) if |x * inv2eb| >= 2^50 or
+// x is not finite.
+template <typename T>
+inline int64_t lr_prequant(T xv, const Bounds& bd, bool* ok) {
+  const double t = (double)xv * bd.inv2eb;
+  if (!(std::fabs(t) < 1125899906842624.0)) { *ok = false; return 0; }
+  *ok = true;
+  return (int64_t)std::nearbyint(t);
+}
+
+// L2: delta(i,j,k) = sum over a,b,c in {0,1} of (-1)^(a+b+c) q(i-a, j-b, k-c), q = 0 outside the block
+// (block extents m1, m2; q laid out [i][j][k] with strides m1*m2, m2).  Unsigned wrap-around keeps
+// garbage streams defined; valid data never comes near 2^63.
+inline int64_t lr_delta(const std::vector<int64_t>& q, int m1, int m2, int i, int j, int k) {
+  uint64_t s = 0;
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2; b++)
+      for (int c = 0; c < 2; c++) {
+        const int ii = i - a, jj = j - b, kk = k - c;
+        if (ii < 0 || jj < 0 || kk < 0) continue;
+        const uint64_t v = (uint64_t)q[((size_t)ii * m1 + jj) * m2 + kk];
+        s = ((a + b + c) & 1) ? s - v : s + v;
+      }
+  return (int64_t)s;
+}
+
+template <typename T>
+int lr_compress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R, int eb_mode,
+                     double eb, const double* range, const T* x, uint16_t* codes, int32_t* coef,
+                     double* coef_raw, uint8_t* block_exempt, uint8_t* flags, uint64_t* out_idx, T* out_val,
+                     uint64_t cap, uint64_t* n_out, int64_t* hist, double* eb_abs_out, T* xprime,
+                     uint64_t* n_lorenzo) {
+  const uint64_t n0 = dims[0], n1 = dims[1], n2 = dims[2];
+  const uint64_t N = n0 * n1 * n2;
+  double lo = 0.0, hi = 0.0;
+  if (eb_mode == 1) {
+    if (range) {
+      lo = range[0]; hi = range[1];
+    } else {
+      lo = hi = (double)x[0];
+      for (uint64_t e = 0; e < N; e++) {
+        double v = (double)x[e];
+        if (std::isnan(v)) { lo = hi = v; break; }
+        if (v < lo) lo = v;
+        if (v > hi) hi = v;
+      }
+    }
+  }
+  Bounds bd;
+  if (!make_bounds(eb_mode, eb, lo, hi, B, &bd)) return ORC_EBADRANGE;
+  if (eb_abs_out) *eb_abs_out = bd.eb_abs;
+  uint64_t nout = 0, nl = 0;
+  const uint64_t NB0 = ceil_div(n0, B), NB1 = ceil_div(n1, B), NB2 = ceil_div(n2, B);
+  if (hist) std::memset(hist, 0, sizeof(int64_t) * 2 * (size_t)R);
+  const size_t BB = (size_t)B * B * B;
+  std::vector<uint16_t> cR(BB), cL(BB);
+  std::vector<T> xR(BB), xL(BB);
+  std::vector<int64_t> q(BB);
+  std::vector<uint8_t> qok(BB);
+  for (uint64_t a = 0; a < NB0; a++)
+    for (uint64_t b = 0; b < NB1; b++)
+      for (uint64_t cc = 0; cc < NB2; cc++) {
+        const uint64_t bid = (a * NB1 + b) * NB2 + cc;
+        const uint64_t i0 = a * B, j0 = b * B, k0 = cc * B;
+        const int m0 = (int)std::min<uint64_t>(B, n0 - i0);
+        const int m1 = (int)std::min<uint64_t>(B, n1 - j0);
+        const int m2 = (int)std::min<uint64_t>(B, n2 - k0);
+        // L4: the regression side is O4-O10 unchanged
+        double V[4], beta[4], bhat[4];
+        int32_t cd[4];
+        block_moments(x, n1, n2, i0, j0, k0, m0, m1, m2, V);
+        lemma_beta(V, m0, m1, m2, beta);
+        coef_codes(beta, bd, cd, bhat);
+        double absum = 0.0;
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++) absum += std::fabs((double)x[((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k)]);
+        const double scale = absum / ((double)m0 * m1 * m2);
+        bool tie_block = false;
+        for (int d = 0; d < 4; d++) {
+          const double w = (d == 0) ? bd.w0 : bd.ws;
+          const double u = beta[d] / w;
+          if (!std::isfinite(u)) continue;
+          const double win = std::max(1e-9, 1e-12 * std::max(std::fabs(beta[d]), scale) / w);
+          if (near_half(u, win)) tie_block = true;
+        }
+        uint64_t costR = 0, costL = 0;
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++) {
+              const size_t l = ((size_t)i * m1 + j) * m2 + k;
+              const uint64_t e = ((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k);
+              quantize_element<T>(x[e], predict(bhat, i, j, k), bd, R, &cR[l], &xR[l]);
+              costR += cR[l] == 0 ? R : (uint64_t)std::llabs((int64_t)cR[l] - (int64_t)R);
+              bool ok;
+              q[l] = lr_prequant<T>(x[e], bd, &ok);
+              qok[l] = ok ? 1 : 0;
+            }
+        // L2 + L3: Lorenzo residual, code, verify
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++) {
+              const size_t l = ((size_t)i * m1 + j) * m2 + k;
+              const uint64_t e = ((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k);
+              cL[l] = 0;
+              xL[l] = x[e];
+              if (qok[l]) {
+                const int64_t d = lr_delta(q, m1, m2, i, j, k);
+                if (d > -(int64_t)R && d < (int64_t)R) {
+                  const T xp = (T)(bd.twoeb * (double)q[l]);
+                  if (std::fabs((double)xp - (double)x[e]) <= bd.eb_abs) {
+                    cL[l] = (uint16_t)((int64_t)R + d);
+                    xL[l] = xp;
+                  }
+                }
+              }
+              costL += cL[l] == 0 ? R : (uint64_t)std::llabs((int64_t)cL[l] - (int64_t)R);
+            }
+        // L5 + L6: the cheaper predictor (ties -> regression)
+        const bool useL = costL < costR;
+        nl += useL ? 1 : 0;
+        if (flags) flags[bid] = useL ? 1 : 0;
+        for (int d = 0; d < 4; d++) {
+          coef[4 * bid + d] = useL ? 0 : cd[d];
+          if (coef_raw) coef_raw[4 * bid + d] = beta[d];
+        }
+        if (block_exempt) block_exempt[bid] = tie_block ? 1 : 0;
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++) {
+              const size_t l = ((size_t)i * m1 + j) * m2 + k;
+              const uint64_t e = ((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k);
+              const uint16_t code = useL ? cL[l] : cR[l];
+              codes[e] = code;
+              if (xprime) xprime[e] = useL ? xL[l] : xR[l];
+              if (code == 0) {
+                if (nout < cap) {
+                  out_idx[nout] = e + dim0_offset * n1 * n2;
+                  out_val[nout] = x[e];
+                }
+                nout++;
+              }
+              if (hist) hist[code]++;
+            }
+      }
+  if (n_out) *n_out = nout;
+  if (n_lorenzo) *n_lorenzo = nl;
+  return nout > cap ? ORC_EOVERFLOW : ORC_OK;
+}
+
+// L7: outliers first (their stored x is the decompressed value and gives q by L1), then per block in
+// (i, j, k) order: regression blocks as O12, Lorenzo blocks q = (code - R) + (q - delta(q)) at (i,j,k)
+// (the seven earlier neighbours), x' = (T)(twoeb * q).
+template <typename T>
+int lr_decompress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R, double eb_abs,
+                       const uint16_t* codes, const int32_t* coef, const uint8_t* flags, const uint64_t* out_idx,
+                       const T* out_val, uint64_t n_out, T* xo) {
+  Bounds bd;
+  if (!make_bounds(0, eb_abs, 0, 0, B, &bd)) return ORC_EINVAL;
+  const uint64_t n0 = dims[0], n1 = dims[1], n2 = dims[2];
+  const uint64_t base = dim0_offset * n1 * n2;
+  for (uint64_t m = 0; m < n_out; m++) {
+    const uint64_t e = out_idx[m] - base;
+    if (out_idx[m] < base || e >= n0 * n1 * n2) return ORC_EINVAL;
+    xo[e] = out_val[m];
+  }
+  const uint64_t NB0 = ceil_div(n0, B), NB1 = ceil_div(n1, B), NB2 = ceil_div(n2, B);
+  std::vector<int64_t> q((size_t)B * B * B);
+  for (uint64_t a = 0; a < NB0; a++)
+    for (uint64_t b = 0; b < NB1; b++)
+      for (uint64_t cc = 0; cc < NB2; cc++) {
+        const uint64_t bid = (a * NB1 + b) * NB2 + cc;
+        const uint64_t i0 = a * B, j0 = b * B, k0 = cc * B;
+        const int m0 = (int)std::min<uint64_t>(B, n0 - i0);
+        const int m1 = (int)std::min<uint64_t>(B, n1 - j0);
+        const int m2 = (int)std::min<uint64_t>(B, n2 - k0);
+        if (!flags[bid]) {
+          double bhat[4];
+          bhat[0] = (double)coef[4 * bid] * bd.w0;
+          for (int d = 1; d < 4; d++) bhat[d] = (double)coef[4 * bid + d] * bd.ws;
+          for (int i = 0; i < m0; i++)
+            for (int j = 0; j < m1; j++)
+              for (int k = 0; k < m2; k++) {
+                const uint64_t e = ((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k);
+                const uint16_t code = codes[e];
+                if (code == 0) continue;   // the stored value, scattered above
+                const double p = predict(bhat, i, j, k);
+                const double qd = (double)((int64_t)code - (int64_t)R);
+                const double prod = bd.twoeb * qd;
+                xo[e] = (T)(p + prod);
+              }
+          continue;
+        }
+        for (int i = 0; i < m0; i++)
+          for (int j = 0; j < m1; j++)
+            for (int k = 0; k < m2; k++) {
+              const size_t l = ((size_t)i * m1 + j) * m2 + k;
+              const uint64_t e = ((i0 + i) * n1 + (j0 + j)) * n2 + (k0 + k);
+              const uint16_t code = codes[e];
+              if (code == 0) {
+                bool ok;
+                q[l] = lr_prequant<T>(xo[e], bd, &ok);
+                continue;
+              }
+              q[l] = 0;   // delta over the earlier neighbours only
+              const uint64_t pred = (uint64_t)0 - (uint64_t)lr_delta(q, m1, m2, i, j, k);
+              q[l] = (int64_t)(pred + (uint64_t)((int64_t)code - (int64_t)R));
+              xo[e] = (T)(bd.twoeb * (double)q[l]);
+            }
+      }
+  return ORC_OK;
+}
+
 bool check_dims(const uint64_t* dims, uint32_t B, uint32_t R) {
   if (!dims || dims[0] == 0 || dims[1] == 0 || dims[2] == 0) return false;
   if (B < 1 || R < 1 || R > 32768) return false;
@@ -436,6 +659,47 @@ int orc_quantize_element(int dtype, double x, double p, double eb_abs, uint32_t 
   int k = quantize_element<double>(x, p, bd, R, code, &xp);
   *xprime = xp;
   return k;
+}
+
+
+// SZ3-LR (NEXT-4): compress -> codes, coefficient codes (0 for Lorenzo blocks), per-block predictor
+// flags (1 = Lorenzo), outliers, histogram; decompress -> x'.
+int orc_lr_compress(int dtype, const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R, int eb_mode,
+                    double eb, const double* range, const void* x, uint16_t* codes, int32_t* coef, double* coef_raw,
+                    uint8_t* block_exempt, uint8_t* flags, uint64_t* out_idx, void* out_val, uint64_t cap,
+                    uint64_t* n_out, int64_t* hist, double* eb_abs_out, void* xprime, uint64_t* n_lorenzo) {
+  if (!check_dims(dims, B, R)) return (R < 1 || R > 32768) ? ORC_ERANGE : ORC_EINVAL;
+  if (!x || !codes || !coef || !flags || (cap > 0 && (!out_idx || !out_val))) return ORC_EINVAL;
+  if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != 0 && eb_mode != 1)) return ORC_EINVAL;
+  if (dtype == 0)
+    return lr_compress_impl<float>(dims, dim0_offset, B, R, eb_mode, eb, range, (const float*)x, codes, coef, coef_raw,
+                                   block_exempt, flags, out_idx, (float*)out_val, cap, n_out, hist, eb_abs_out,
+                                   (float*)xprime, n_lorenzo);
+  if (dtype == 1)
+    return lr_compress_impl<double>(dims, dim0_offset, B, R, eb_mode, eb, range, (const double*)x, codes, coef,
+                                    coef_raw, block_exempt, flags, out_idx, (double*)out_val, cap, n_out, hist,
+                                    eb_abs_out, (double*)xprime, n_lorenzo);
+  return ORC_EUNSUPPORTED;
+}
+
+int orc_lr_decompress(int dtype, const uint64_t dims[3], uint64_t dim0_offset, uint32_t B, uint32_t R, double eb_abs,
+                      const uint16_t* codes, const int32_t* coef, const uint8_t* flags, const uint64_t* out_idx,
+                      const void* out_val, uint64_t n_out, void* x_out) {
+  if (!check_dims(dims, B, R)) return (R < 1 || R > 32768) ? ORC_ERANGE : ORC_EINVAL;
+  if (!codes || !coef || !flags || !x_out || (n_out > 0 && (!out_idx || !out_val))) return ORC_EINVAL;
+  if (dtype == 0)
+    return lr_decompress_impl<float>(dims, dim0_offset, B, R, eb_abs, codes, coef, flags, out_idx,
+                                     (const float*)out_val, n_out, (float*)x_out);
+  if (dtype == 1)
+    return lr_decompress_impl<double>(dims, dim0_offset, B, R, eb_abs, codes, coef, flags, out_idx,
+                                      (const double*)out_val, n_out, (double*)x_out);
+  return ORC_EUNSUPPORTED;
+}
+
+// L2 on one dense block of integers (for the pins)
+int64_t orc_lr_delta(const int64_t* q, int m0, int m1, int m2, int i, int j, int k) {
+  std::vector<int64_t> v(q, q + (size_t)m0 * m1 * m2);
+  return lr_delta(v, m1, m2, i, j, k);
 }
 
 uint64_t orc_num_blocks(const uint64_t dims[3], uint32_t B) {
