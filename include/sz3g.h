@@ -154,6 +154,34 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
                                const unsigned long long* d_outlier_count, void* x_out,
                                sz3g_stream_t stream);
 
+/* NEXT-4 -- SZ3-LR, the composite predictor: "a Lorenzo predictor and a regression-based predictor
+ * and predicts data using the better result in between based on blockwise error estimation".
+ * Definition oracle/DEFINITION.md L1-L7 (readings DESIGN G26-G29): per 6^3 block, the regression
+ * codes (O7-O10, coefficients from sz3g_regression_analyze's beta) and block-local first-order 3D
+ * Lorenzo codes of the prequantised values q = rint(x / 2eb) (code R + delta, decompressed value
+ * (T)(2eb q)); the block keeps the predictor with the smaller sum of |code - R| (outliers count R).
+ *
+ * sz3g_lr_quantize -- compress from the analyze pass (run sz3g_regression_analyze first; it also
+ * gives the REL range).  Arguments as sz3g_regression_quantize, plus
+ *   flags       out  nblocks uint8: 1 = Lorenzo block, 0 = regression block.
+ *   coef_codes  out  as sz3g_regression_quantize for regression blocks; {0,0,0,0} for Lorenzo blocks.
+ *   codes / outliers / hist / d_outlier_count / d_eb_abs / d_status: of the chosen predictor, with
+ *   the same semantics (outlier values are the original x).
+ * Host errors: EINVAL (null or misaligned pointers), EUNSUPPORTED, ERANGE, ECUDA.  1 launch.
+ *
+ * sz3g_lr_decompress -- x' from the codes, coefficient codes, flags and outliers (arguments as
+ * sz3g_regression_decompress plus flags).  The outlier values are scattered into x_out first:
+ * Lorenzo blocks take their q from them (L7).  2 launches (1 without outliers).                 */
+int sz3g_lr_quantize(const sz3g_grid* grid, const sz3g_params* params, const void* x, const double* d_minmax,
+                     const double* beta, uint16_t* codes, int32_t* coef_codes, uint8_t* flags,
+                     uint64_t* outlier_idx, void* outlier_val, uint64_t outlier_cap,
+                     unsigned long long* d_outlier_count, int64_t* hist, double* d_eb_abs, int32_t* d_status,
+                     sz3g_stream_t stream);
+int sz3g_lr_decompress(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax,
+                       const uint16_t* codes, const int32_t* coef_codes, const uint8_t* flags,
+                       const uint64_t* outlier_idx, const void* outlier_val, uint64_t n_outliers,
+                       const unsigned long long* d_outlier_count, void* x_out, sz3g_stream_t stream);
+
 /* a7 standalone -- histogram of n uint16 codes into 2R int64 bins, ACCUMULATED (+=).  Codes
  * >= 2R are ignored.  1 launch. */
 int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* hist,

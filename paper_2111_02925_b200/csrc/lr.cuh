@@ -1,0 +1,353 @@
+// libsz3g -- SZ3-LR (NEXT-4): the composite Lorenzo / regression predictor, "predicts data using the
+// better result in between based on blockwise error estimation".  Definition:
+// oracle/DEFINITION.md L1-L7 (readings DESIGN G26-G29):
+//   L1 q = rint(x * inv2eb) (0 and unusable if |x * inv2eb| >= 2^50 or x is not finite);
+//   L2 delta = block-local first-order 3D Lorenzo residual of q (zero outside the block);
+//   L3 Lorenzo code R + delta if |delta| < R and x' = (T)(twoeb * q) is within eb, else an outlier;
+//   L4 regression codes O7-O10 from the analyze pass's beta;
+//   L5 the block takes the predictor with the smaller sum of |code - R| (outliers count R; ties ->
+//      regression);  L6 flag per block, coefficient codes 0 for Lorenzo blocks;
+//   L7 decompression: outliers scattered first, Lorenzo blocks rebuild q by an exact integer
+//      recurrence, x' = (T)(twoeb * q).
+// Included by sz3g.cu inside its anonymous namespace (KArgs, TileWalk, histogram helpers, rare_path).
+//
+// Compression: one warp per 6x6x96 tile (16 blocks, 2 lanes per block, 3 columns per lane, as every
+// tile routine of this library).  Each lane walks its 108 elements plane by plane, row by row: the
+// regression code by the definition's fp64 arithmetic (exact_code), q by the magic-number rint, and the
+// Lorenzo residual as three differences -- along k within the lane plus one shuffle from the block's
+// other lane, along j against the previous row (registers), along i against the previous plane (6 rows
+// x 3 columns of int64 in registers).  Both codes go to two shared code slabs; after the two lanes of a
+// block have summed their costs the chosen codes are emitted (global store, shared histogram window,
+// outliers through rare_path).  TMA kernel: W self-fed warps per CTA, each with a private 2-stage ring
+// of tiles (as k_analyze_tma).
+
+constexpr double LR_QMAX = 1125899906842624.0;   // 2^50 (L1)
+constexpr int LR_HW = 4096;                       // histogram window (bins) of the LR kernels
+
+// L1 for one element: q as an exact double (|q| < 2^50) and whether it is usable
+__device__ __forceinline__ double lr_prequant(double xd, const Consts& K, bool& ok) {
+  const double t = __dmul_rn(xd, K.inv2eb);
+  ok = fabs(t) < LR_QMAX;
+  const double q = __dsub_rn(__dadd_rn(t, RINT_MAGIC), RINT_MAGIC);   // rint, ties to even (|t| < 2^51)
+  return ok ? q : 0.0;
+}
+
+// the histogram count of one emitted nonzero code: shared window, else global
+__device__ __forceinline__ void lr_hist(const HistSmem& hs, unsigned long long* hist, uint32_t code) {
+  const uint32_t b = code - hs.lo;
+  if (b < hs.nwin) atomicAdd(&hs.win[b], 1u);
+  else atomicAdd(&hist[code], 1ull);
+}
+
+// One warp, one tile.  xs: the tile (shared stage, si = 576, sj = 96, zero outside the grid) or the
+// field (IN_SMEM = false, predicated loads).  sR / sL: the warp's two code slabs [i][j][k] (6 x 6 x 96).
+template <typename T, bool IN_SMEM, bool FULL>
+__device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
+                                                 uint16_t* sL, const TileCoord tc, const Geo& g, const Consts& K,
+                                                 uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
+                                                 const HistSmem& hs) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int h = L.h;
+  double beta[4] = {0.0, 0.0, 0.0, 0.0}, bh[4];
+  int32_t cc[4];
+  const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
+  if (L.m2 > 0) {
+    const double2 b01 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid);
+    const double2 b23 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid + 1);
+    beta[0] = b01.x; beta[1] = b01.y; beta[2] = b23.x; beta[3] = b23.y;
+  }
+  block_codes(beta, K, cc, bh);
+  const double dR = (double)R;
+  uint32_t costR = 0, costL = 0;
+  int64_t pdj[BS][3];   // j-differences of the previous plane, per row
+#pragma unroll
+  for (int j = 0; j < BS; j++) pdj[j][0] = pdj[j][1] = pdj[j][2] = 0;
+  for (int i = 0; i < BS; i++) {
+    int64_t pdk[3] = {0, 0, 0};   // k-differences of the previous row
+#pragma unroll
+    for (int j = 0; j < BS; j++) {
+      int64_t q[3];
+      uint32_t cr[3];
+      bool ok[3], valid[3];
+      double xd[3], qd[3];
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        valid[kk] = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
+        const uint64_t off = (uint64_t)i * si + (uint64_t)j * sj + L.kcol + kk;
+        const T xv = (IN_SMEM || valid[kk]) ? xs[off] : T(0);
+        xd[kk] = to_d<T>(xv);
+        const double p = __fma_rn(bh[1], (double)i, __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0])));
+        cr[kk] = valid[kk] ? exact_code<T>(xv, p, K, R) : R;
+        qd[kk] = lr_prequant(xd[kk], K, ok[kk]);
+        if (!valid[kk]) { ok[kk] = false; qd[kk] = 0.0; }   // outside the block: q = 0
+        q[kk] = (int64_t)__double2ll_rn(qd[kk]);
+      }
+      // L2 as three differences: k (the block's left lane supplies column 3h - 1), j, i
+      int64_t left = __shfl_up_sync(0xffffffffu, q[2], 1);
+      if (h == 0) left = 0;
+      const int64_t dk[3] = {q[0] - left, q[1] - q[0], q[2] - q[1]};
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const int64_t dj = dk[kk] - pdk[kk];
+        const int64_t delta = dj - pdj[j][kk];
+        pdk[kk] = dk[kk];
+        pdj[j][kk] = dj;
+        uint32_t cl = 0;
+        if (ok[kk] && delta > -(int64_t)R && delta < (int64_t)R) {
+          const T xr = from_d<T>(__dmul_rn(K.twoeb, qd[kk]));
+          if (fabs(__dsub_rn(to_d<T>(xr), xd[kk])) <= K.eb_abs) cl = (uint32_t)((int64_t)R + delta);
+        }
+        if (!valid[kk]) cl = R;
+        costR += cr[kk] ? (uint32_t)fabs((double)cr[kk] - dR) : R;
+        costL += cl ? (uint32_t)fabs((double)cl - dR) : R;
+        const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
+        sR[s] = (uint16_t)cr[kk];
+        sL[s] = (uint16_t)cl;
+      }
+    }
+  }
+  // L5: the block's two lanes sum their costs
+  costR += __shfl_xor_sync(0xffffffffu, costR, 1);
+  costL += __shfl_xor_sync(0xffffffffu, costL, 1);
+  const bool useL = costL < costR;
+  if (L.m2 > 0 && h == 0) {
+    reinterpret_cast<int4*>(o.coef)[bid] = useL ? make_int4(0, 0, 0, 0) : make_int4(cc[0], cc[1], cc[2], cc[3]);
+    flags[bid] = useL ? 1 : 0;
+  }
+  // L6: emit the chosen codes (into sR, for rare_path), histogram, codes to global
+  bool has_out = false;
+  const uint64_t gbase = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+  for (int i = 0; i < BS; i++)
+#pragma unroll
+    for (int j = 0; j < BS; j++)
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
+        const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
+        const uint16_t code = useL ? sL[s] : sR[s];
+        sR[s] = valid ? code : (uint16_t)1;   // rare_path scans sR for zeros of valid elements
+        if (!valid) continue;
+        o.codes[gbase + ((uint64_t)i * g.n1 + j) * g.n2 + L.kcol + kk] = code;
+        if (code) {
+          if (o.hist) lr_hist(hs, o.hist, code);
+        } else {
+          has_out = true;
+        }
+      }
+  __syncwarp();
+  if (o.hist) rare_path<T, true, BS>(xs, si, sj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
+  else rare_path<T, false, BS>(xs, si, sj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
+  __syncwarp();
+}
+
+template <typename T, int W, int D>
+struct LrSmem {
+  static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr size_t slab_bytes = 2 * sizeof(uint16_t) * TILE_ELEMS;   // regression + Lorenzo codes
+  static constexpr size_t off_slab = (size_t)W * D * stage_bytes;
+  static constexpr size_t off_hist = off_slab + (size_t)W * slab_bytes;
+  static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (LR_HW + 36);
+  static constexpr size_t off_k = off_bar + (size_t)W * D * sizeof(uint64_t);
+  static constexpr size_t total = off_k + sizeof(Consts) + 16;
+};
+
+// Persistent, W self-fed warps per CTA (each with a private D-stage TMA ring, as k_analyze_tma).
+template <typename T, int W, int D>
+__global__ void __launch_bounds__(W * 32, 1)
+    k_lr_compress_tma(const __grid_constant__ CUtensorMap tm_x, KArgs a, CompressOut<T> o, uint8_t* __restrict__ flags) {
+  using L_ = LrSmem<T, W, D>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
+  Consts* s_k = reinterpret_cast<Consts*>(smem + L_::off_k);
+  int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(smem + L_::off_hist);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  HistSmem hs;
+  hist_init(hs, s_win, s_win + LR_HW, a.R, LR_HW);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W * D; s++) ptx::mbar_init(&full[s], 1);
+    ptx::fence_mbar_init();
+  }
+  if (!cta_consts(a, s_k, s_ok)) return;
+  const Consts K = *s_k;
+  const Geo& g = a.g;
+  T* ring = reinterpret_cast<T*>(smem) + (size_t)warp * D * TILE_ELEMS;
+  uint16_t* sR = reinterpret_cast<uint16_t*>(smem + L_::off_slab + (size_t)warp * L_::slab_bytes);
+  uint16_t* sL = sR + TILE_ELEMS;
+  uint64_t* bar = full + warp * D;
+  TileWalk tw(warp, a.chunk, W), tl(warp, a.chunk, W);
+  if (lane == 0) {
+    ptx::prefetch_tensormap(&tm_x);
+    for (int d = 0; d < D; d++, tl.next()) {
+      const uint64_t t = tl.tile();
+      if (t >= g.ntiles) break;
+      const TileCoord tc = decode_tile(t, g);
+      ptx::mbar_arrive_expect_tx(&bar[d], (uint32_t)L_::stage_bytes);
+      ptx::tma_load_3d(ring + (size_t)d * TILE_ELEMS, &tm_x, &bar[d], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+    }
+  }
+  for (uint32_t k = 0;; k++, tw.next()) {
+    const uint64_t t = tw.tile();
+    if (t >= g.ntiles) break;
+    const uint32_t s = k % D, ph = (k / D) & 1u;
+    const TileCoord tc = decode_tile(t, g);
+    ptx::mbar_wait(&bar[s], ph);
+    const T* xs = ring + (size_t)s * TILE_ELEMS;
+    if (tile_full(tc, g)) lr_compress_tile<T, true, true>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs);
+    else lr_compress_tile<T, true, false>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs);
+    __syncwarp();
+    if (lane == 0) {   // every lane's reads of the stage are done: refill it with tile k + D
+      const uint64_t t2 = tl.tile();
+      if (t2 < g.ntiles) {
+        const TileCoord tc2 = decode_tile(t2, g);
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive_expect_tx(&bar[s], (uint32_t)L_::stage_bytes);
+        ptx::tma_load_3d(ring + (size_t)s * TILE_ELEMS, &tm_x, &bar[s], (int)(tc2.c * TK), (int)(tc2.b * BS),
+                         (int)(tc2.a * BS));
+      }
+      tl.next();
+    }
+  }
+  __syncthreads();
+  if (o.hist) hist_flush(hs, o.hist);
+  overflow_check(a, o.ocount, o.cap);
+}
+
+// Shapes without a TMA map: one warp per tile straight from the field (4 warps per CTA).
+constexpr int LR_PW = 4;
+template <typename T>
+__global__ void __launch_bounds__(LR_PW * 32) k_lr_compress_plain(const T* __restrict__ x, KArgs a, CompressOut<T> o,
+                                                                  uint8_t* __restrict__ flags) {
+  extern __shared__ __align__(16) uint8_t psmem[];
+  uint16_t* slabs = reinterpret_cast<uint16_t*>(psmem);
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(psmem + (size_t)LR_PW * 2 * TILE_ELEMS * sizeof(uint16_t));
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  HistSmem hs;
+  hist_init(hs, s_win, s_win + LR_HW, a.R, LR_HW);
+  if (!cta_consts(a, &s_k, &s_ok)) return;
+  const Consts K = s_k;
+  const Geo& g = a.g;
+  const int warp = threadIdx.x >> 5;
+  uint16_t* sR = slabs + (size_t)warp * 2 * TILE_ELEMS;
+  uint16_t* sL = sR + TILE_ELEMS;
+  const uint64_t warps = (uint64_t)gridDim.x * LR_PW;
+  for (uint64_t t = blockIdx.x * (uint64_t)LR_PW + warp; t < g.ntiles; t += warps) {
+    const TileCoord tc = decode_tile(t, g);
+    const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+    lr_compress_tile<T, false, false>(x + off, g.n1 * g.n2, g.n2, sR, sL, tc, g, K, a.R, o, flags, hs);
+  }
+  __syncthreads();
+  if (o.hist) hist_flush(hs, o.hist);
+  overflow_check(a, o.ocount, o.cap);
+}
+size_t lr_plain_smem() { return (size_t)LR_PW * 2 * TILE_ELEMS * sizeof(uint16_t) + sizeof(uint32_t) * (LR_HW + 36); }
+
+// ---------------------------------------------------------------------------------- LR decompress
+// One warp per tile straight from global memory.  Regression blocks: x' = (T)(p + twoeb (c - R)).
+// Lorenzo blocks: with r(i,j,k) = q(i,j,k) - q(i-1,j,k) - q(i,j-1,k) + q(i-1,j-1,k) (the (i,j)
+// difference), delta = r(k) - r(k-1), so along each row r is a running sum of the residuals, restarted
+// at an outlier (whose q is L1 of its stored value, already scattered into x_out), and
+// q = r + q(i-1,j,k) + q(i,j-1,k) - q(i-1,j-1,k).  The block's right lane takes the left lane's last r
+// by a shuffle: both lanes first run their columns from r = 0, then the right lane adds the left lane's
+// final r to its columns before its first outlier.  Outliers are not written (the scatter did that).
+template <typename T, bool FULL>
+__device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ codes, const int32_t* __restrict__ coef,
+                                                   const uint8_t* __restrict__ flags, T* __restrict__ xo,
+                                                   const TileCoord tc, const Geo& g, const Consts& K, uint32_t R) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int h = L.h;
+  const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
+  int4 cc = make_int4(0, 0, 0, 0);
+  bool lor = false;
+  if (L.m2 > 0) {
+    cc = __ldg(reinterpret_cast<const int4*>(coef) + bid);
+    lor = __ldg(flags + bid) != 0;
+  }
+  double bh[4];
+  decode_coefs(cc, K, bh);
+  const double cR = __dadd_rn(I2D_MAGIC, (double)R);
+  const uint64_t gbase = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK + L.kcol;
+  // P[j] = q of row j of the previous plane; C = q of the previous row of this plane.  Row j needs
+  // P[j] and P[j - 1]; once it is done P[j - 1] is free and takes this plane's row j - 1.
+  int64_t P[BS][3];
+#pragma unroll
+  for (int j = 0; j < BS; j++) P[j][0] = P[j][1] = P[j][2] = 0;
+  for (int i = 0; i < BS; i++) {
+    int64_t C[3] = {0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < BS; j++) {
+      uint32_t c[3];
+      bool valid[3];
+      const uint64_t e0 = gbase + ((uint64_t)i * g.n1 + j) * g.n2;
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        valid[kk] = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
+        c[kk] = valid[kk] ? (uint32_t)codes[e0 + kk] : R;
+      }
+      if (!lor) {   // regression block (O12)
+#pragma unroll
+        for (int kk = 0; kk < 3; kk++) {
+          if (!valid[kk] || c[kk] == 0) continue;
+          const double p = __fma_rn(bh[1], (double)i, __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0])));
+          const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)c[kk]), cR);
+          xo[e0 + kk] = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, qd)));
+        }
+      }
+      // Lorenzo recurrence, run by every lane (the shuffle needs the whole warp; regression lanes compute
+      // throw-away values)
+      int64_t r[3], base[3];
+      bool nocarry[3];
+      int64_t run = 0;
+      bool cut = false;   // from an outlier on, r no longer depends on the left lane
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        base[kk] = P[j][kk] + C[kk] - (j > 0 ? P[j - 1][kk] : 0);
+        if (lor && valid[kk] && c[kk] == 0) {
+          bool ok;
+          const double qd = lr_prequant(to_d<T>(xo[e0 + kk]), K, ok);
+          run = (int64_t)__double2ll_rn(qd) - base[kk];
+          cut = true;
+        } else {
+          run += valid[kk] ? (int64_t)c[kk] - (int64_t)R : 0;
+        }
+        r[kk] = run;
+        nocarry[kk] = cut;
+      }
+      int64_t carry = __shfl_up_sync(0xffffffffu, r[2], 1);
+      if (h == 0) carry = 0;
+      int64_t q[3];
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        q[kk] = valid[kk] ? (nocarry[kk] ? r[kk] : r[kk] + carry) + base[kk] : 0;
+        if (lor && valid[kk] && c[kk] != 0) xo[e0 + kk] = from_d<T>(__dmul_rn(K.twoeb, (double)q[kk]));
+      }
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        if (j > 0) P[j - 1][kk] = C[kk];
+        C[kk] = q[kk];
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++) P[BS - 1][kk] = C[kk];
+  }
+}
+
+constexpr int LR_DW = 4;   // decompress: warps per CTA
+template <typename T>
+__global__ void __launch_bounds__(LR_DW * 32) k_lr_decompress(const uint16_t* __restrict__ codes,
+                                                              const int32_t* __restrict__ coef,
+                                                              const uint8_t* __restrict__ flags, T* __restrict__ xo,
+                                                              KArgs a) {
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  if (!cta_consts(a, &s_k, &s_ok)) return;
+  const Consts K = s_k;
+  const Geo& g = a.g;
+  const uint64_t warps = (uint64_t)gridDim.x * LR_DW;
+  for (uint64_t t = blockIdx.x * (uint64_t)LR_DW + (threadIdx.x >> 5); t < g.ntiles; t += warps) {
+    const TileCoord tc = decode_tile(t, g);
+    if (tile_full(tc, g)) lr_decompress_tile<T, true>(codes, coef, flags, xo, tc, g, K, a.R);
+    else lr_decompress_tile<T, false>(codes, coef, flags, xo, tc, g, K, a.R);
+  }
+}

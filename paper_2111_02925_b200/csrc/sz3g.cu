@@ -1196,6 +1196,39 @@ int launch_analyze_tma(const Geo& g, const void* x, double* beta, unsigned long 
   return SZ3G_OK;
 }
 
+// ---------------------------------------------------------------------------------- SZ3-LR (NEXT-4)
+#include "lr.cuh"
+
+constexpr int LW32 = 5, LD32 = 2;   // f32 LR compress: 5 self-fed warps x 2 stages (+ 2 code slabs each)
+constexpr int LW64 = 3, LD64 = 2;   // f64 LR compress: 3 warps x 2 stages
+
+template <typename T, int W, int D>
+int launch_lr_tma(const Geo& g, const void* x, const KArgs& ka, const CompressOut<T>& co, uint8_t* flags,
+                  cudaStream_t st) {
+  using L = LrSmem<T, W, D>;
+  static_assert(L::total <= 232448, "smem");
+  CUtensorMap mx;
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
+  auto kern = k_lr_compress_tma<T, W, D>;
+  cudaError_t e = set_smem(kern, L::total);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
+  kern<<<(unsigned)grid, W * 32, L::total, st>>>(mx, ka, co, flags);
+  return check_launch(1);
+}
+
+template <typename T>
+int launch_lr_plain(const Geo& g, const void* x, const KArgs& ka, const CompressOut<T>& co, uint8_t* flags,
+                    cudaStream_t st) {
+  auto kern = k_lr_compress_plain<T>;
+  cudaError_t e = set_smem(kern, lr_plain_smem());
+  if (e != cudaSuccess) return cuda_fail(e);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + LR_PW - 1) / LR_PW, sm_count() * 4));
+  kern<<<blocks, LR_PW * 32, lr_plain_smem(), st>>>((const T*)x, ka, co, flags);
+  return check_launch(1);
+}
+
 }  // namespace
 
 // ====================================================================================== C ABI
@@ -1326,6 +1359,86 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
       launched++;
     }
   }
+  return check_launch(launched);
+}
+
+int sz3g_lr_quantize(const sz3g_grid* grid, const sz3g_params* params, const void* x, const double* d_minmax,
+                     const double* beta, uint16_t* codes, int32_t* coef_codes, uint8_t* flags, uint64_t* outlier_idx,
+                     void* outlier_val, uint64_t outlier_cap, unsigned long long* d_outlier_count, int64_t* hist,
+                     double* d_eb_abs, int32_t* d_status, sz3g_stream_t stream) {
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  rc = validate_params(params);
+  if (rc) return rc;
+  if (!x || !codes || !coef_codes || !flags || !beta || !d_outlier_count || !d_status) return SZ3G_EINVAL;
+  if (outlier_cap > 0 && (!outlier_idx || !outlier_val)) return SZ3G_EINVAL;
+  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(coef_codes) & 15) || (reinterpret_cast<uintptr_t>(beta) & 15)) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Geo g = make_geo(grid);
+  KArgs ka;
+  memset(&ka, 0, sizeof(ka));
+  ka.g = g;
+  ka.R = params->radius;
+  ka.eb_mode = (int)params->eb_mode;
+  ka.eb = params->eb;
+  ka.d_minmax = d_minmax;
+  ka.d_eb_abs = d_eb_abs;
+  ka.d_status = d_status;
+  ka.chunk = chunk_tiles(false);
+  ka.uround = grid->dtype == SZ3G_F32 ? (5.9604644775390625e-08 + 1.12e-16) : 2.3e-16;
+  const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
+  const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
+  const bool tma = !generic && map_ok(x, es, g);
+  unsigned long long* h = hist_ptr_nonnull(hist) ? reinterpret_cast<unsigned long long*>(hist) : nullptr;
+  if (grid->dtype == SZ3G_F32) {
+    CompressOut<float> co{codes, coef_codes, nullptr, outlier_idx, (float*)outlier_val, outlier_cap, d_outlier_count,
+                          h, beta};
+    return tma ? launch_lr_tma<float, LW32, LD32>(g, x, ka, co, flags, st) : launch_lr_plain<float>(g, x, ka, co, flags, st);
+  }
+  CompressOut<double> co{codes, coef_codes, nullptr, outlier_idx, (double*)outlier_val, outlier_cap, d_outlier_count,
+                         h, beta};
+  return tma ? launch_lr_tma<double, LW64, LD64>(g, x, ka, co, flags, st) : launch_lr_plain<double>(g, x, ka, co, flags, st);
+}
+
+int sz3g_lr_decompress(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax,
+                       const uint16_t* codes, const int32_t* coef_codes, const uint8_t* flags,
+                       const uint64_t* outlier_idx, const void* outlier_val, uint64_t n_outliers,
+                       const unsigned long long* d_outlier_count, void* x_out, sz3g_stream_t stream) {
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  rc = validate_params(params);
+  if (rc) return rc;
+  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
+  if (!codes || !coef_codes || !flags || !x_out) return SZ3G_EINVAL;
+  if (n_outliers > 0 && (!outlier_idx || !outlier_val)) return SZ3G_EINVAL;
+  if (reinterpret_cast<uintptr_t>(coef_codes) & 15) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Geo g = make_geo(grid);
+  KArgs ka;
+  memset(&ka, 0, sizeof(ka));
+  ka.g = g;
+  ka.R = params->radius;
+  ka.eb_mode = (int)params->eb_mode;
+  ka.eb = params->eb;
+  ka.d_minmax = d_minmax;
+  const uint64_t N = g.n0 * g.n1 * g.n2;
+  int launched = 0;
+  // L7: the outliers first (their stored values give the Lorenzo blocks their q)
+  if (n_outliers) {
+    const unsigned b = (unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096);
+    if (grid->dtype == SZ3G_F32)
+      k_outlier_scatter<float><<<b, 256, 0, st>>>(outlier_idx, (const float*)outlier_val, n_outliers, d_outlier_count,
+                                                  g.gofs, N, (float*)x_out);
+    else
+      k_outlier_scatter<double><<<b, 256, 0, st>>>(outlier_idx, (const double*)outlier_val, n_outliers,
+                                                   d_outlier_count, g.gofs, N, (double*)x_out);
+    launched++;
+  }
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + LR_DW - 1) / LR_DW, sm_count() * 8));
+  if (grid->dtype == SZ3G_F32) k_lr_decompress<float><<<blocks, LR_DW * 32, 0, st>>>(codes, coef_codes, flags, (float*)x_out, ka);
+  else k_lr_decompress<double><<<blocks, LR_DW * 32, 0, st>>>(codes, coef_codes, flags, (double*)x_out, ka);
+  launched++;
   return check_launch(launched);
 }
 

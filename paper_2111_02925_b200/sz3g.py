@@ -119,6 +119,9 @@ def load(allow_build: bool = False):
                                           ctypes.POINTER(U64)]
         lib.sz3g_stream_read.argtypes = [P, U64, ctypes.POINTER(StreamHeader), ctypes.POINTER(Section), U32,
                                          ctypes.POINTER(U32), ctypes.POINTER(U32)]
+    if hasattr(lib, "sz3g_lr_quantize"):   # absent only in older A/B builds
+        lib.sz3g_lr_quantize.argtypes = [GP, PP, P, P, P, P, P, P, P, P, U64, P, P, P, P, P]
+        lib.sz3g_lr_decompress.argtypes = [GP, PP, P, P, P, P, P, P, U64, P, P, P]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
@@ -138,7 +141,7 @@ EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regres
                     "sz3g_truncation_decompress", "sz3g_error_stats_scratch_bytes", "sz3g_error_stats",
                     "sz3g_coef_delta_scratch_bytes", "sz3g_coef_delta_encode", "sz3g_coef_delta_decode",
                     "sz3g_huffman_codebook_from_lengths", "sz3g_stream_size", "sz3g_stream_write",
-                    "sz3g_stream_read",
+                    "sz3g_stream_read", "sz3g_lr_quantize", "sz3g_lr_decompress",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -239,6 +242,7 @@ class Compressed:
     status: torch.Tensor          # int32 [1] (device)
     n_outliers: int | None = None
     eb_abs: float | None = None
+    lr_flags: torch.Tensor | None = None   # SZ3-LR only: uint8 [NB], 1 = Lorenzo block
 
     def finalize(self) -> "Compressed":
         """Synchronise on the results, raise on device status bits, fill n_outliers / eb_abs."""
@@ -276,11 +280,17 @@ class CompressBuffers:
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.minmax = torch.zeros(2, dtype=torch.float64, device=device)
         self.beta = None   # [NB, 4] float64, allocated by the two-pass path (regression_analyze)
+        self.lr_flags = None   # [NB] uint8, allocated by the SZ3-LR path
 
     def beta_buffer(self) -> torch.Tensor:
         if self.beta is None:
             self.beta = torch.empty_like(self.coef_codes, dtype=torch.float64)
         return self.beta
+
+    def flags_buffer(self) -> torch.Tensor:
+        if self.lr_flags is None:
+            self.lr_flags = torch.empty(self.coef_codes.shape[0], dtype=torch.uint8, device=self.coef_codes.device)
+        return self.lr_flags
 
     def reset(self):
         """Zero the accumulating outputs (outlier counter, histogram, status)."""
@@ -398,6 +408,62 @@ def regression_decompress(codes: torch.Tensor, coef_codes: torch.Tensor, outlier
     return out
 
 
+def lr_quantize(x: torch.Tensor, eb: float, eb_mode: str, radius: int, d_minmax: torch.Tensor | None,
+                beta: torch.Tensor, bufs: CompressBuffers | None = None, outlier_cap: int | None = None,
+                hist: bool = True, dim0_offset: int = 0, flags: int = 0, stream=None, reset: bool = True) -> Compressed:
+    """sz3g_lr_quantize (SZ3-LR; DEFINITION.md L1-L6): per block the better of the regression and
+    the prequantised Lorenzo predictor, from the analyze pass's beta (asynchronous).  The result's
+    ``lr_flags`` marks the Lorenzo blocks; Lorenzo blocks' coefficient codes are 0."""
+    _require_cuda(x, d_minmax, beta)
+    if bufs is None:
+        bufs = CompressBuffers(x.shape, x.dtype, radius, outlier_cap, x.device, False, hist)
+    elif reset:
+        bufs.reset()
+    if bufs.radius != radius:
+        raise SZ3GError("buffer radius mismatch")
+    fl = bufs.flags_buffer()
+    g = make_grid(x.shape, x.dtype, dim0_offset)
+    p = make_params(eb, eb_mode, radius, flags)
+    rc = load().sz3g_lr_quantize(
+        ctypes.byref(g), ctypes.byref(p), _ptr(x), _ptr(d_minmax), _ptr(beta), _ptr(bufs.codes),
+        _ptr(bufs.coef_codes), _ptr(fl), _ptr(bufs.outlier_idx), _ptr(bufs.outlier_val), bufs.outlier_idx.numel(),
+        _ptr(bufs.outlier_count), _ptr(bufs.hist if hist else None), _ptr(bufs.eb_abs), _ptr(bufs.status),
+        _stream(stream))
+    _check(rc, "sz3g_lr_quantize")
+    return Compressed(tuple(x.shape), x.dtype, radius, dim0_offset, bufs.codes, bufs.coef_codes, beta,
+                      bufs.outlier_idx, bufs.outlier_val, bufs.outlier_count, bufs.hist if hist else None,
+                      bufs.eb_abs, bufs.status, lr_flags=fl)
+
+
+def lr_compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768,
+                bufs: CompressBuffers | None = None, outlier_cap: int | None = None, hist: bool = True,
+                flags: int = 0, stream=None, finalize: bool = True) -> Compressed:
+    """SZ3-LR compression: analyze (range + beta, one read) -> lr_quantize (one read)."""
+    if bufs is None:
+        bufs = CompressBuffers(x.shape, x.dtype, radius, outlier_cap, x.device, False, hist)
+    minmax, beta = regression_analyze(x, bufs.minmax, bufs.beta_buffer(), stream)
+    res = lr_quantize(x, eb, eb_mode, radius, minmax, beta, bufs, hist=hist, flags=flags, stream=stream)
+    return res.finalize() if finalize else res
+
+
+def lr_decompress(codes: torch.Tensor, coef_codes: torch.Tensor, lr_flags: torch.Tensor, outlier_idx: torch.Tensor,
+                  outlier_val: torch.Tensor, n_outliers: int, eb: float, radius: int = 32768,
+                  dtype: torch.dtype = torch.float32, dim0_offset: int = 0, out: torch.Tensor | None = None,
+                  flags: int = 0, stream=None, d_outlier_count: torch.Tensor | None = None, eb_mode: str = "abs",
+                  d_minmax: torch.Tensor | None = None) -> torch.Tensor:
+    """sz3g_lr_decompress (L7): outlier scatter, then regression / Lorenzo blocks (asynchronous)."""
+    _require_cuda(codes, coef_codes, lr_flags, outlier_idx, outlier_val, out, d_outlier_count, d_minmax)
+    if out is None:
+        out = torch.empty(codes.shape, dtype=dtype, device=codes.device)
+    g = make_grid(codes.shape, out.dtype, dim0_offset)
+    p = make_params(eb, eb_mode, radius, flags)
+    rc = load().sz3g_lr_decompress(ctypes.byref(g), ctypes.byref(p), _ptr(d_minmax), _ptr(codes), _ptr(coef_codes),
+                                   _ptr(lr_flags), _ptr(outlier_idx), _ptr(outlier_val), int(n_outliers),
+                                   _ptr(d_outlier_count), _ptr(out), _stream(stream))
+    _check(rc, "sz3g_lr_decompress")
+    return out
+
+
 def histogram(codes: torch.Tensor, radius: int = 32768, hist: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """sz3g_histogram: accumulate the 2R-bin int64 histogram of uint16 codes."""
     _require_cuda(codes, hist)
@@ -440,6 +506,9 @@ def compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 327
 def decompress(res: Compressed, out: torch.Tensor | None = None, flags: int = 0) -> torch.Tensor:
     if res.n_outliers is None:
         res.finalize()
+    if res.lr_flags is not None:
+        return lr_decompress(res.codes, res.coef_codes, res.lr_flags, res.outlier_idx, res.outlier_val,
+                             res.n_outliers, res.eb_abs, res.radius, res.dtype, res.dim0_offset, out, flags)
     return regression_decompress(res.codes, res.coef_codes, res.outlier_idx, res.outlier_val, res.n_outliers,
                                  res.eb_abs, res.radius, res.dtype, res.dim0_offset, out, flags)
 
