@@ -39,13 +39,20 @@ __device__ __forceinline__ void lr_hist(const HistSmem& hs, unsigned long long* 
   else atomicAdd(&hist[code], 1ull);
 }
 
+template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
+__device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
+                                        const uint16_t* sL, uint32_t costR, uint32_t costL, const int32_t cc[4],
+                                        uint64_t bid, const LaneGeom& L, const TileCoord tc, const Geo& g,
+                                        const CompressOut<T>& o, uint8_t* __restrict__ flags, const HistSmem& hs,
+                                        const CUtensorMap* tm_c);
+
 // One warp, one tile.  xs: the tile (shared stage, si = 576, sj = 96, zero outside the grid) or the
 // field (IN_SMEM = false, predicated loads).  sR / sL: the warp's two code slabs [i][j][k] (6 x 6 x 96).
-template <typename T, bool IN_SMEM, bool FULL>
-__device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
+template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
+__device__ __forceinline__ void lr_compress_tile_exact(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
                                                  uint16_t* sL, const TileCoord tc, const Geo& g, const Consts& K,
                                                  uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
-                                                 const HistSmem& hs) {
+                                                 const HistSmem& hs, const CUtensorMap* tm_c) {
   const LaneGeom L = lane_geom<FULL>(tc, g);
   const int h = L.h;
   double beta[4] = {0.0, 0.0, 0.0, 0.0}, bh[4];
@@ -106,6 +113,21 @@ __device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint6
       }
     }
   }
+  lr_emit<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, costR, costL, cc, bid, L, tc, g, o, flags, hs, tm_c);
+}
+
+// L5 + L6 for one tile whose regression / Lorenzo codes are in the slabs sR / sL: the lanes of
+// Lorenzo blocks copy their codes over sR, then every valid element's final code is read once
+// (histogram, outliers through rare_path) and the tile leaves with one TMA store of sR (TMA_OUT) or
+// element stores.  With TMA_OUT the caller waits for the store's reads before sR is written again.
+template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
+__device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
+                                        const uint16_t* sL, uint32_t costR, uint32_t costL, const int32_t cc[4],
+                                        uint64_t bid, const LaneGeom& L, const TileCoord tc, const Geo& g,
+                                        const CompressOut<T>& o, uint8_t* __restrict__ flags, const HistSmem& hs,
+                                        const CUtensorMap* tm_c) {
+  const int h = L.h;
+  __syncwarp();
   // L5: the block's two lanes sum their costs
   costR += __shfl_xor_sync(0xffffffffu, costR, 1);
   costL += __shfl_xor_sync(0xffffffffu, costL, 1);
@@ -114,20 +136,29 @@ __device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint6
     reinterpret_cast<int4*>(o.coef)[bid] = useL ? make_int4(0, 0, 0, 0) : make_int4(cc[0], cc[1], cc[2], cc[3]);
     flags[bid] = useL ? 1 : 0;
   }
-  // L6: emit the chosen codes (into sR, for rare_path), histogram, codes to global
+  if (useL) {
+#pragma unroll 1
+    for (int i = 0; i < BS; i++)
+#pragma unroll
+      for (int j = 0; j < BS; j++)
+#pragma unroll
+        for (int kk = 0; kk < 3; kk++) {
+          const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
+          sR[s] = sL[s];
+        }
+  }
   bool has_out = false;
   const uint64_t gbase = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+#pragma unroll 1
   for (int i = 0; i < BS; i++)
 #pragma unroll
     for (int j = 0; j < BS; j++)
 #pragma unroll
       for (int kk = 0; kk < 3; kk++) {
         const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
-        const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
-        const uint16_t code = useL ? sL[s] : sR[s];
-        sR[s] = valid ? code : (uint16_t)1;   // rare_path scans sR for zeros of valid elements
         if (!valid) continue;
-        o.codes[gbase + ((uint64_t)i * g.n1 + j) * g.n2 + L.kcol + kk] = code;
+        const uint16_t code = sR[(uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk)];
+        if (!TMA_OUT) o.codes[gbase + ((uint64_t)i * g.n1 + j) * g.n2 + L.kcol + kk] = code;
         if (code) {
           if (o.hist) lr_hist(hs, o.hist, code);
         } else {
@@ -135,9 +166,188 @@ __device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint6
         }
       }
   __syncwarp();
+  if (TMA_OUT) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      ptx::tma_store_3d(tm_c, sR, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+      ptx::bulk_commit();
+    }
+  }
   if (o.hist) rare_path<T, true, BS>(xs, si, sj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
   else rare_path<T, false, BS>(xs, si, sj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
   __syncwarp();
+}
+
+// The fast routine: the tile's (j, k) columns with the six i-planes in registers (as quantize_rows).
+// Regression codes by the library's certified fast test (fp32 scaled domain for f32 data, the fp64
+// fast verify for f64; make_consts / fast32_consts), the exact definition for the rest (warp vote).
+// Lorenzo: L1 + L3's bound check are the SAME test with a zero predictor (q = rint(x inv2eb), x' =
+// (T)(0 + twoeb q) = (T)(twoeb q)), so the zero-coefficient constants certify q and the bound; the
+// |t| < 2^22 guard keeps the fp32 magic rounding exact.  Residuals in int32: usable while every |q| <
+// 2^26 (|delta| < 2^29); a tile with a larger q (or a fallback q beyond that) is redone by
+// lr_compress_tile_exact (returns false).
+template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
+__device__ __forceinline__ bool lr_compress_tile_fast(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
+                                                      uint16_t* sL, const TileCoord tc, const Geo& g, const Consts& K,
+                                                      uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
+                                                      const HistSmem& hs, const CUtensorMap* tm_c) {
+  constexpr bool F32 = sizeof(T) == 4;
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int h = L.h;
+  double beta[4] = {0.0, 0.0, 0.0, 0.0}, bh[4];
+  int32_t cc[4];
+  const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
+  if (L.m2 > 0) {
+    const double2 b01 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid);
+    const double2 b23 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid + 1);
+    beta[0] = b01.x; beta[1] = b01.y; beta[2] = b23.x; beta[3] = b23.y;
+  }
+  block_codes(beta, K, cc, bh);
+  const Fast32 F = fast32_consts(bh, K);
+  const double zero[4] = {0.0, 0.0, 0.0, 0.0};
+  const Fast32 F0 = fast32_consts(zero, K);
+  const float inv2eb32 = K.inv2eb32;
+  const float M32 = 12582912.0f;                 // 1.5 * 2^23
+  const float Rf = (float)R;
+  const int iR = (int)R;
+  if (IN_SMEM) { si = BS * TK; sj = TK; }
+  uint32_t costR = 0, costL = 0;
+  bool big = false;
+  int32_t Dp[3][BS];   // k-differences of the previous row
+#pragma unroll
+  for (int kk = 0; kk < 3; kk++)
+#pragma unroll
+    for (int i = 0; i < BS; i++) Dp[kk][i] = 0;
+#pragma unroll 1
+  for (int j = 0; j < BS; j++) {
+    int32_t q[3][BS];
+    uint32_t cr[3][BS];
+    bool lv[3][BS];   // Lorenzo-usable: q certified (or exact) and x' = (T)(twoeb q) within eb
+    const float fj = (float)j;
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++) {
+      const bool cv = FULL || ((j < L.m1) && L.kv(kk));
+      T xv[BS];
+#pragma unroll
+      for (int i = 0; i < BS; i++) {
+        const bool valid = FULL || (cv && i < L.m0);
+        const uint64_t off = (uint64_t)i * si + (uint64_t)j * sj + L.kcol + kk;
+        xv[i] = (IN_SMEM || FULL || valid) ? xs[off] : T(0);
+      }
+      bool need = false;
+      if (F32) {
+        const float base32 = __fmaf_rn(F.a2, fj, __fmaf_rn(F.a3, (float)(3 * h + kk), F.a0));
+#pragma unroll
+        for (int i = 0; i < BS; i++) {
+          const bool valid = FULL || (cv && i < L.m0);
+          const float x32 = (float)xv[i];
+          // regression (fast32_consts: certified rint and bound)
+          const float P = i == 0 ? base32 : __fmaf_rn(F.a1, (float)i, base32);
+          const float t32 = __fmaf_rn(x32, inv2eb32, -P);
+          const float r = __fsub_rn(__fadd_rn(t32, M32), M32);
+          const float e = __fsub_rn(t32, r);
+          const bool ok = __fmaf_rn(F.k1, fabsf(t32), fabsf(e)) <= F.thr && fabsf(r) < Rf;
+          cr[kk][i] = ok ? (uint32_t)((int)r + iR) : 0u;
+          need |= valid && !ok;
+          // Lorenzo prequantisation (zero predictor)
+          const float tL = __fmul_rn(x32, inv2eb32);
+          const float sLm = __fadd_rn(tL, M32);
+          const float rL = __fsub_rn(sLm, M32);
+          const float eL = __fsub_rn(tL, rL);
+          const bool okL = __fmaf_rn(F0.k1, fabsf(tL), fabsf(eL)) <= F0.thr && fabsf(tL) < 4194304.0f;
+          q[kk][i] = okL ? (int32_t)rL : 0;
+          lv[kk][i] = okL;
+          need |= valid && !okL;
+        }
+      } else {
+        const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0]));
+#pragma unroll
+        for (int i = 0; i < BS; i++) {
+          const bool valid = FULL || (cv && i < L.m0);
+          const double xd = to_d<T>(xv[i]);
+          const double p = __fma_rn(bh[1], (double)i, base);
+          const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+          const double rq = __dsub_rn(__dadd_rn(t, RINT_MAGIC), RINT_MAGIC);
+          const bool ok = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, rq))) <= K.vthr && fabs(rq) < (double)R;
+          cr[kk][i] = ok ? (uint32_t)((int)rq + iR) : 0u;
+          need |= valid && !ok;
+          const double tL = __dmul_rn(xd, K.inv2eb);
+          const double rL = __dsub_rn(__dadd_rn(tL, RINT_MAGIC), RINT_MAGIC);
+          const bool okL = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(tL, rL))) <= K.vthr && fabs(tL) < 67108864.0;
+          q[kk][i] = okL ? (int32_t)rL : 0;
+          lv[kk][i] = okL;
+          need |= valid && !okL;
+        }
+      }
+      if (__any_sync(0xffffffffu, need)) {   // the exact definitions (rare)
+        const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0]));
+#pragma unroll
+        for (int i = 0; i < BS; i++) {
+          const bool valid = FULL || (cv && i < L.m0);
+          if (!valid) continue;
+          if (cr[kk][i] == 0u) cr[kk][i] = exact_code<T>(xv[i], __fma_rn(bh[1], (double)i, base), K, R);
+          if (!lv[kk][i]) {
+            bool okq;
+            const double xd = to_d<T>(xv[i]);
+            const double qd = lr_prequant(xd, K, okq);
+            if (okq && fabs(qd) >= 67108864.0) big = true;   // beyond the int32 residuals: exact routine
+            q[kk][i] = (okq && !big) ? (int32_t)qd : 0;
+            lv[kk][i] = okq && fabs(__dsub_rn(to_d<T>(from_d<T>(__dmul_rn(K.twoeb, qd))), xd)) <= K.eb_abs;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < BS; i++) {
+        const bool valid = FULL || (cv && i < L.m0);
+        if (!valid) { q[kk][i] = 0; lv[kk][i] = false; cr[kk][i] = R; }
+      }
+    }
+    // L2: k-difference (the block's left lane supplies column 3h - 1), j-difference, i-difference
+    int32_t left[BS];
+#pragma unroll
+    for (int i = 0; i < BS; i++) {
+      left[i] = __shfl_up_sync(0xffffffffu, q[2][i], 1);
+      if (h == 0) left[i] = 0;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++) {
+      const bool cv = FULL || ((j < L.m1) && L.kv(kk));
+      int32_t Eprev = 0;
+#pragma unroll
+      for (int i = 0; i < BS; i++) {
+        const bool valid = FULL || (cv && i < L.m0);
+        const int32_t D = q[kk][i] - (kk == 0 ? left[i] : q[kk - 1][i]);
+        const int32_t E = D - Dp[kk][i];
+        Dp[kk][i] = D;
+        const int32_t delta = E - Eprev;
+        Eprev = E;
+        uint32_t cl = (lv[kk][i] && delta > -iR && delta < iR) ? (uint32_t)(delta + iR) : 0u;
+        if (!valid) cl = R;
+        const uint32_t c = cr[kk][i];
+        costR += c ? (uint32_t)abs((int)c - iR) : R;
+        costL += cl ? (uint32_t)abs((int)cl - iR) : R;
+        const uint32_t sidx = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
+        sR[sidx] = (uint16_t)c;
+        sL[sidx] = (uint16_t)cl;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, big)) return false;
+  lr_emit<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, costR, costL, cc, bid, L, tc, g, o, flags, hs, tm_c);
+  return true;
+}
+
+template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
+__device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
+                                                 uint16_t* sL, const TileCoord tc, const Geo& g, const Consts& K,
+                                                 uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
+                                                 const HistSmem& hs, const CUtensorMap* tm_c) {
+#ifndef SZ3G_LR_FAST
+#define SZ3G_LR_FAST 0   // 1: the certified fp32 fast routine first (measured no faster: the kernel is latency-bound)
+#endif
+  if (!SZ3G_LR_FAST || !lr_compress_tile_fast<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, tc, g, K, R, o, flags, hs, tm_c))
+    lr_compress_tile_exact<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, tc, g, K, R, o, flags, hs, tm_c);
 }
 
 template <typename T, int W, int D>
@@ -154,7 +364,8 @@ struct LrSmem {
 // Persistent, W self-fed warps per CTA (each with a private D-stage TMA ring, as k_analyze_tma).
 template <typename T, int W, int D>
 __global__ void __launch_bounds__(W * 32, 1)
-    k_lr_compress_tma(const __grid_constant__ CUtensorMap tm_x, KArgs a, CompressOut<T> o, uint8_t* __restrict__ flags) {
+    k_lr_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, KArgs a,
+                      CompressOut<T> o, uint8_t* __restrict__ flags) {
   using L_ = LrSmem<T, W, D>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
@@ -191,10 +402,12 @@ __global__ void __launch_bounds__(W * 32, 1)
     if (t >= g.ntiles) break;
     const uint32_t s = k % D, ph = (k / D) & 1u;
     const TileCoord tc = decode_tile(t, g);
+    if (lane == 0) ptx::bulk_wait_read0();   // the previous tile's code store has read sR
+    __syncwarp();
     ptx::mbar_wait(&bar[s], ph);
     const T* xs = ring + (size_t)s * TILE_ELEMS;
-    if (tile_full(tc, g)) lr_compress_tile<T, true, true>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs);
-    else lr_compress_tile<T, true, false>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs);
+    if (tile_full(tc, g)) lr_compress_tile<T, true, true, true>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
+    else lr_compress_tile<T, true, false, true>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
     __syncwarp();
     if (lane == 0) {   // every lane's reads of the stage are done: refill it with tile k + D
       const uint64_t t2 = tl.tile();
@@ -208,13 +421,17 @@ __global__ void __launch_bounds__(W * 32, 1)
       tl.next();
     }
   }
+  if (lane == 0) ptx::bulk_wait0();
   __syncthreads();
   if (o.hist) hist_flush(hs, o.hist);
   overflow_check(a, o.ocount, o.cap);
 }
 
 // Shapes without a TMA map: one warp per tile straight from the field (4 warps per CTA).
-constexpr int LR_PW = 4;
+#ifndef SZ3G_LR_PW
+#define SZ3G_LR_PW 4
+#endif
+constexpr int LR_PW = SZ3G_LR_PW;
 template <typename T>
 __global__ void __launch_bounds__(LR_PW * 32) k_lr_compress_plain(const T* __restrict__ x, KArgs a, CompressOut<T> o,
                                                                   uint8_t* __restrict__ flags) {
@@ -235,7 +452,7 @@ __global__ void __launch_bounds__(LR_PW * 32) k_lr_compress_plain(const T* __res
   for (uint64_t t = blockIdx.x * (uint64_t)LR_PW + warp; t < g.ntiles; t += warps) {
     const TileCoord tc = decode_tile(t, g);
     const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
-    lr_compress_tile<T, false, false>(x + off, g.n1 * g.n2, g.n2, sR, sL, tc, g, K, a.R, o, flags, hs);
+    lr_compress_tile<T, false, false, false>(x + off, g.n1 * g.n2, g.n2, sR, sL, tc, g, K, a.R, o, flags, hs, nullptr);
   }
   __syncthreads();
   if (o.hist) hist_flush(hs, o.hist);
@@ -251,10 +468,12 @@ size_t lr_plain_smem() { return (size_t)LR_PW * 2 * TILE_ELEMS * sizeof(uint16_t
 // q = r + q(i-1,j,k) + q(i,j-1,k) - q(i-1,j-1,k).  The block's right lane takes the left lane's last r
 // by a shuffle: both lanes first run their columns from r = 0, then the right lane adds the left lane's
 // final r to its columns before its first outlier.  Outliers are not written (the scatter did that).
-template <typename T, bool FULL>
-__device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ codes, const int32_t* __restrict__ coef,
+template <typename T, bool FULL, bool IN_SMEM>
+__device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
+                                                   const int32_t* __restrict__ coef,
                                                    const uint8_t* __restrict__ flags, T* __restrict__ xo,
                                                    const TileCoord tc, const Geo& g, const Consts& K, uint32_t R) {
+  if (IN_SMEM) { ci = BS * TK; cj = TK; }
   const LaneGeom L = lane_geom<FULL>(tc, g);
   const int h = L.h;
   const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
@@ -280,10 +499,11 @@ __device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ 
       uint32_t c[3];
       bool valid[3];
       const uint64_t e0 = gbase + ((uint64_t)i * g.n1 + j) * g.n2;
+      const uint16_t* crow = cs + (uint64_t)i * ci + (uint64_t)j * cj + L.kcol;
 #pragma unroll
       for (int kk = 0; kk < 3; kk++) {
         valid[kk] = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
-        c[kk] = valid[kk] ? (uint32_t)codes[e0 + kk] : R;
+        c[kk] = valid[kk] ? (uint32_t)crow[kk] : R;
       }
       if (!lor) {   // regression block (O12)
 #pragma unroll
@@ -347,7 +567,72 @@ __global__ void __launch_bounds__(LR_DW * 32) k_lr_decompress(const uint16_t* __
   const uint64_t warps = (uint64_t)gridDim.x * LR_DW;
   for (uint64_t t = blockIdx.x * (uint64_t)LR_DW + (threadIdx.x >> 5); t < g.ntiles; t += warps) {
     const TileCoord tc = decode_tile(t, g);
-    if (tile_full(tc, g)) lr_decompress_tile<T, true>(codes, coef, flags, xo, tc, g, K, a.R);
-    else lr_decompress_tile<T, false>(codes, coef, flags, xo, tc, g, K, a.R);
+    const uint16_t* cs = codes + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+    if (tile_full(tc, g)) lr_decompress_tile<T, true, false>(cs, g.n1 * g.n2, g.n2, coef, flags, xo, tc, g, K, a.R);
+    else lr_decompress_tile<T, false, false>(cs, g.n1 * g.n2, g.n2, coef, flags, xo, tc, g, K, a.R);
+  }
+}
+
+// The code tiles through a private 2-stage TMA ring per warp (self-fed, as k_analyze_tma): the
+// recurrence reads them from shared memory instead of waiting on a global load per row.
+template <int W, int D>
+struct LrDecSmem {
+  static constexpr size_t stage_bytes = sizeof(uint16_t) * TILE_ELEMS;
+  static constexpr size_t off_bar = (size_t)W * D * stage_bytes;
+  static constexpr size_t off_k = off_bar + (size_t)W * D * sizeof(uint64_t);
+  static constexpr size_t total = off_k + sizeof(Consts) + 16;
+};
+
+template <typename T, int W, int D>
+__global__ void __launch_bounds__(W * 32, 1)
+    k_lr_decompress_tma(const __grid_constant__ CUtensorMap tm_c, const int32_t* __restrict__ coef,
+                        const uint8_t* __restrict__ flags, T* __restrict__ xo, KArgs a) {
+  using L_ = LrDecSmem<W, D>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
+  Consts* s_k = reinterpret_cast<Consts*>(smem + L_::off_k);
+  int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W * D; s++) ptx::mbar_init(&full[s], 1);
+    ptx::fence_mbar_init();
+  }
+  if (!cta_consts(a, s_k, s_ok)) return;
+  const Consts K = *s_k;
+  const Geo& g = a.g;
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem) + (size_t)warp * D * TILE_ELEMS;
+  uint64_t* bar = full + warp * D;
+  TileWalk tw(warp, a.chunk, W), tl(warp, a.chunk, W);
+  if (lane == 0) {
+    ptx::prefetch_tensormap(&tm_c);
+    for (int d = 0; d < D; d++, tl.next()) {
+      const uint64_t t = tl.tile();
+      if (t >= g.ntiles) break;
+      const TileCoord tc = decode_tile(t, g);
+      ptx::mbar_arrive_expect_tx(&bar[d], (uint32_t)L_::stage_bytes);
+      ptx::tma_load_3d(ring + (size_t)d * TILE_ELEMS, &tm_c, &bar[d], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+    }
+  }
+  for (uint32_t k = 0;; k++, tw.next()) {
+    const uint64_t t = tw.tile();
+    if (t >= g.ntiles) break;
+    const uint32_t s = k % D, ph = (k / D) & 1u;
+    const TileCoord tc = decode_tile(t, g);
+    ptx::mbar_wait(&bar[s], ph);
+    const uint16_t* cs = ring + (size_t)s * TILE_ELEMS;
+    if (tile_full(tc, g)) lr_decompress_tile<T, true, true>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R);
+    else lr_decompress_tile<T, false, true>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R);
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t t2 = tl.tile();
+      if (t2 < g.ntiles) {
+        const TileCoord tc2 = decode_tile(t2, g);
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive_expect_tx(&bar[s], (uint32_t)L_::stage_bytes);
+        ptx::tma_load_3d(ring + (size_t)s * TILE_ELEMS, &tm_c, &bar[s], (int)(tc2.c * TK), (int)(tc2.b * BS),
+                         (int)(tc2.a * BS));
+      }
+      tl.next();
+    }
   }
 }

@@ -1199,7 +1199,13 @@ int launch_analyze_tma(const Geo& g, const void* x, double* beta, unsigned long 
 // ---------------------------------------------------------------------------------- SZ3-LR (NEXT-4)
 #include "lr.cuh"
 
-constexpr int LW32 = 5, LD32 = 2;   // f32 LR compress: 5 self-fed warps x 2 stages (+ 2 code slabs each)
+#ifndef SZ3G_LR_W
+#define SZ3G_LR_W 7
+#endif
+#ifndef SZ3G_LR_D
+#define SZ3G_LR_D 1
+#endif
+constexpr int LW32 = SZ3G_LR_W, LD32 = SZ3G_LR_D;   // f32 LR compress: 7 self-fed warps x 1 stage (+ 2 code slabs each)
 constexpr int LW64 = 3, LD64 = 2;   // f64 LR compress: 3 warps x 2 stages
 
 template <typename T, int W, int D>
@@ -1207,15 +1213,37 @@ int launch_lr_tma(const Geo& g, const void* x, const KArgs& ka, const CompressOu
                   cudaStream_t st) {
   using L = LrSmem<T, W, D>;
   static_assert(L::total <= 232448, "smem");
-  CUtensorMap mx;
+  CUtensorMap mx, mc;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
+  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, co.codes, g)) return SZ3G_ECUDA;
   auto kern = k_lr_compress_tma<T, W, D>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
-  kern<<<(unsigned)grid, W * 32, L::total, st>>>(mx, ka, co, flags);
+  kern<<<(unsigned)grid, W * 32, L::total, st>>>(mx, mc, ka, co, flags);
   return check_launch(1);
+}
+
+#ifndef SZ3G_LRD_W
+#define SZ3G_LRD_W 4
+#endif
+constexpr int LDW = SZ3G_LRD_W, LDD = 2;   // LR decompress: self-fed warps x code-tile stages
+
+template <typename T, int W, int D>
+int launch_lr_dec_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, const uint8_t* flags, void* xo,
+                      const KArgs& ka, cudaStream_t st) {
+  using L = LrDecSmem<W, D>;
+  static_assert(L::total <= 232448, "smem");
+  CUtensorMap mc;
+  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) return SZ3G_ECUDA;
+  auto kern = k_lr_decompress_tma<T, W, D>;
+  cudaError_t e = set_smem(kern, L::total);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count() * std::max(1, 64 / W));
+  kern<<<(unsigned)grid, W * 32, L::total, st>>>(mc, coef, flags, (T*)xo, ka);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SZ3G_OK;
 }
 
 template <typename T>
@@ -1389,7 +1417,7 @@ int sz3g_lr_quantize(const sz3g_grid* grid, const sz3g_params* params, const voi
   ka.uround = grid->dtype == SZ3G_F32 ? (5.9604644775390625e-08 + 1.12e-16) : 2.3e-16;
   const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
   const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
-  const bool tma = !generic && map_ok(x, es, g);
+  const bool tma = !generic && map_ok(x, es, g) && map_ok(codes, 2, g);
   unsigned long long* h = hist_ptr_nonnull(hist) ? reinterpret_cast<unsigned long long*>(hist) : nullptr;
   if (grid->dtype == SZ3G_F32) {
     CompressOut<float> co{codes, coef_codes, nullptr, outlier_idx, (float*)outlier_val, outlier_cap, d_outlier_count,
@@ -1435,9 +1463,17 @@ int sz3g_lr_decompress(const sz3g_grid* grid, const sz3g_params* params, const d
                                                    d_outlier_count, g.gofs, N, (double*)x_out);
     launched++;
   }
-  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + LR_DW - 1) / LR_DW, sm_count() * 8));
-  if (grid->dtype == SZ3G_F32) k_lr_decompress<float><<<blocks, LR_DW * 32, 0, st>>>(codes, coef_codes, flags, (float*)x_out, ka);
-  else k_lr_decompress<double><<<blocks, LR_DW * 32, 0, st>>>(codes, coef_codes, flags, (double*)x_out, ka);
+  const bool generic = (params->flags & SZ3G_FLAG_FORCE_GENERIC) != 0;
+  if (!generic && map_ok(codes, 2, g)) {
+    ka.chunk = chunk_tiles(true);
+    rc = grid->dtype == SZ3G_F32 ? launch_lr_dec_tma<float, LDW, LDD>(g, codes, coef_codes, flags, x_out, ka, st)
+                                 : launch_lr_dec_tma<double, LDW, LDD>(g, codes, coef_codes, flags, x_out, ka, st);
+    if (rc) return rc;
+  } else {
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + LR_DW - 1) / LR_DW, sm_count() * 8));
+    if (grid->dtype == SZ3G_F32) k_lr_decompress<float><<<blocks, LR_DW * 32, 0, st>>>(codes, coef_codes, flags, (float*)x_out, ka);
+    else k_lr_decompress<double><<<blocks, LR_DW * 32, 0, st>>>(codes, coef_codes, flags, (double*)x_out, ka);
+  }
   launched++;
   return check_launch(launched);
 }
