@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--huffman-reps", type=int, default=5)
     ap.add_argument("--no-truncation", action="store_true", help="skip the SZ3-Truncation (NEXT-2) measurement")
     ap.add_argument("--trunc-k", type=int, default=2)
+    ap.add_argument("--no-lr", action="store_true", help="skip the SZ3-LR (NEXT-4) measurement")
     ap.add_argument("--path", default="two-pass", choices=["two-pass", "fused"],
                     help="REL compression: analyze (range + beta) -> quantize, or value_range -> fused compress")
     return ap.parse_args()
@@ -321,6 +322,58 @@ def truncation_leg(sz3g, x, out, args, world, peaks, stream):
                                     "frac": nb / (d_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
 
 
+def lr_leg(sz3g, x, out, bufs, cfg, a0, N_local, NB_local, s, args, world, peaks, stream):
+    """NEXT-4: SZ3-LR on the same field, from the analyze pass's range and beta (bufs.minmax /
+    bufs.beta of the timed steps): lr_quantize and lr_decompress timed with CUDA events (median of 3),
+    the reconstruction checked against the bound, the codes Huffman-coded for the ratio (not timed)."""
+    import torch
+    ev = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
+    if bufs.beta is None:   # the fused path ran no analyze pass: the range stays the timed steps'
+        sz3g.regression_analyze(x, torch.empty_like(bufs.minmax), bufs.beta_buffer(), stream)
+    tq, td = [], []
+    for _ in range(3):
+        e = [ev() for _ in range(3)]
+        e[0].record(stream)
+        res = sz3g.lr_quantize(x, cfg.eb, cfg.eb_mode, cfg.radius, bufs.minmax, bufs.beta, bufs, dim0_offset=a0,
+                               stream=stream)
+        e[1].record(stream)
+        sz3g.lr_decompress(res.codes, res.coef_codes, res.lr_flags, res.outlier_idx, res.outlier_val,
+                           res.outlier_idx.numel(), cfg.eb, cfg.radius, x.dtype, a0, out, stream=stream,
+                           d_outlier_count=res.outlier_count, eb_mode=cfg.eb_mode, d_minmax=bufs.minmax)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        tq.append(e[0].elapsed_time(e[1]))
+        td.append(e[1].elapsed_time(e[2]))
+    res.finalize()
+    q_ms = max_over_ranks(sorted(tq)[1], world)
+    d_ms = max_over_ranks(sorted(td)[1], world)
+    st = sz3g.error_stats(x, out, res.eb_abs).cpu().tolist()
+    if st[2] != 0 or not st[0] <= res.eb_abs:
+        raise RuntimeError(f"SZ3-LR error bound violated: {st}")
+    n_out = res.n_outliers
+    nl = int(res.lr_flags.sum())
+    table = sz3g.huffman_codebook(res.hist).check()
+    hs = sz3g.huffman_encode(bufs.codes.view(-1), table).check()
+    pay_b = 4 * hs.words()
+    coef_b = sz3g.encode_coefficients(bufs.coef_codes).nbytes()
+    stored = pay_b + 8 * hs.offsets.numel() + coef_b + (NB_local + 7) // 8 + (8 + s) * n_out + table.stored_bytes()
+    # algorithmic bytes (DESIGN.md 5): quantize reads x and beta, writes codes, coefficient codes, flags,
+    # outliers; decompress reads codes, coefficient codes, flags, outliers, writes x'
+    q_bytes = N_local * (s + 2) + NB_local * (32 + 16 + 1) + n_out * (8 + s)
+    d_bytes = N_local * (2 + s) + NB_local * (16 + 1) + n_out * (8 + s)
+    lo, hi = (float(v) for v in bufs.minmax.cpu())
+    return {"lorenzo_blocks": nl, "blocks": NB_local, "lorenzo_fraction": nl / max(1, NB_local),
+            "bits_per_code": 8 * pay_b / N_local, "compression_ratio": N_local * s / stored,
+            "psnr_db": sz3g.psnr(hi - lo, st[1] / N_local), "max_abs_err": st[0], "outliers": n_out,
+            "quantize_ms": q_ms, "decompress_ms": d_ms,
+            "quantize_roofline": {"achieved": q_bytes / (q_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                  "frac": q_bytes / (q_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "decompress_roofline": {"achieved": d_bytes / (d_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                    "frac": d_bytes / (d_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "note": "compression = analyze pass (shared with the regression path) + lr_quantize; ratio counts the "
+                    "predictor flags as a bitmap (1 bit per block)"}
+
+
 # ----------------------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -433,6 +486,11 @@ def main():
     if not args.no_truncation:
         trunc = truncation_leg(sz3g, x, out, args, world, peaks, stream)
 
+    # ---------------- SZ3-LR (NEXT-4) on the same field (reuses bufs: runs after the other legs)
+    lr = None
+    if not args.no_lr:
+        lr = lr_leg(sz3g, x, out, bufs, cfg, a0, N_local, NB_local, s, args, world, peaks, stream)
+
     # ---------------- CPU oracle beside it (rank 0, N = 1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -503,7 +561,7 @@ def main():
                                  "frac": ana_bytes / (ana_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                                  "ms_per_step": ana_ms},
             "path": args.path,
-            "quality": quality, "huffman": huff, "truncation": trunc,
+            "quality": quality, "huffman": huff, "truncation": trunc, "lr": lr,
             "outliers": n_out, "eb_abs": res.eb_abs,
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }
