@@ -179,6 +179,29 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, u
   __syncwarp();
 }
 
+// The exact definitions for one element, out of line (the fast routine's rare fallback)
+struct LrExact {
+  uint32_t cr;   // regression code (O7-O10)
+  int32_t q;     // L1 q (0 if unusable or beyond the int32 residual range)
+  bool lv;       // Lorenzo-usable: q usable and (T)(twoeb q) within eb
+  bool big;      // |q| >= 2^26: the tile needs the int64 routine
+};
+template <typename T>
+__device__ __noinline__ LrExact lr_exact_elem(T xv, double b0, double b1, double b2, double b3, int i, int j, int k,
+                                             const Consts& K, uint32_t R, bool want_cr, bool want_l) {
+  LrExact r{0u, 0, false, false};
+  if (want_cr) r.cr = exact_code<T>(xv, __fma_rn(b1, (double)i, __fma_rn(b2, (double)j, __fma_rn(b3, (double)k, b0))), K, R);
+  if (want_l) {
+    bool okq;
+    const double xd = to_d<T>(xv);
+    const double qd = lr_prequant(xd, K, okq);
+    r.big = okq && fabs(qd) >= 67108864.0;
+    r.q = (okq && !r.big) ? (int32_t)qd : 0;
+    r.lv = okq && fabs(__dsub_rn(to_d<T>(from_d<T>(__dmul_rn(K.twoeb, qd))), xd)) <= K.eb_abs;
+  }
+  return r;
+}
+
 // The fast routine: the tile's (j, k) columns with the six i-planes in registers (as quantize_rows).
 // Regression codes by the library's certified fast test (fp32 scaled domain for f32 data, the fp64
 // fast verify for f64; make_consts / fast32_consts), the exact definition for the rest (warp vote).
@@ -280,20 +303,19 @@ __device__ __forceinline__ bool lr_compress_tile_fast(const T* __restrict__ xs, 
           need |= valid && !okL;
         }
       }
-      if (__any_sync(0xffffffffu, need)) {   // the exact definitions (rare)
-        const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0]));
+      if (__any_sync(0xffffffffu, need)) {   // the exact definitions (rare; out of line: small hot loop)
 #pragma unroll
         for (int i = 0; i < BS; i++) {
           const bool valid = FULL || (cv && i < L.m0);
-          if (!valid) continue;
-          if (cr[kk][i] == 0u) cr[kk][i] = exact_code<T>(xv[i], __fma_rn(bh[1], (double)i, base), K, R);
-          if (!lv[kk][i]) {
-            bool okq;
-            const double xd = to_d<T>(xv[i]);
-            const double qd = lr_prequant(xd, K, okq);
-            if (okq && fabs(qd) >= 67108864.0) big = true;   // beyond the int32 residuals: exact routine
-            q[kk][i] = (okq && !big) ? (int32_t)qd : 0;
-            lv[kk][i] = okq && fabs(__dsub_rn(to_d<T>(from_d<T>(__dmul_rn(K.twoeb, qd))), xd)) <= K.eb_abs;
+          if (valid && (cr[kk][i] == 0u || !lv[kk][i])) {
+            const LrExact ex = lr_exact_elem<T>(xv[i], bh[0], bh[1], bh[2], bh[3], i, j, 3 * h + kk, K, R,
+                                                cr[kk][i] == 0u, !lv[kk][i]);
+            if (cr[kk][i] == 0u) cr[kk][i] = ex.cr;
+            if (!lv[kk][i]) {
+              big |= ex.big;
+              q[kk][i] = ex.q;
+              lv[kk][i] = ex.lv;
+            }
           }
         }
       }
@@ -344,7 +366,7 @@ __device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint6
                                                  uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
                                                  const HistSmem& hs, const CUtensorMap* tm_c) {
 #ifndef SZ3G_LR_FAST
-#define SZ3G_LR_FAST 0   // 1: the certified fp32 fast routine first (measured no faster: the kernel is latency-bound)
+#define SZ3G_LR_FAST 1   // the certified fp32 routine first, the exact one for tiles with |q| >= 2^26
 #endif
   if (!SZ3G_LR_FAST || !lr_compress_tile_fast<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, tc, g, K, R, o, flags, hs, tm_c))
     lr_compress_tile_exact<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, tc, g, K, R, o, flags, hs, tm_c);
