@@ -132,3 +132,17 @@ def test_lr_invalid_arguments():
     rc = lib.sz3g_lr_decompress(ctypes.byref(g), ctypes.byref(p), None, None, None, None, None, None, 0, None, None,
                                 None)
     assert rc == -1
+
+
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_lr_large_q_tiles(dtype, flags):
+    """|x / 2eb| beyond 2^26: those tiles leave the int32 fast routine for the exact int64 one (f64: the
+    Lorenzo codes stay usable; f32: the prequantised grid is coarser than the data, mostly outliers)."""
+    rng = np.random.default_rng(3)
+    shape = (13, 14, 100)
+    i, j, k = np.meshgrid(*(np.arange(n, dtype=np.float64) for n in shape), indexing="ij")
+    x = 1e9 + 1e3 * np.sin(i / 4.0) * np.cos(j / 3.0) + 50.0 * k + rng.uniform(-0.2, 0.2, shape)
+    x[i < 6] -= 1e9          # first block row small: the fast routine, the rest large
+    rep = check_lr(x.astype(dtype), 1.0, "abs", 32768, flags)
+    assert rep["lorenzo_blocks"] > 0
