@@ -32,16 +32,24 @@ __device__ __forceinline__ double lr_prequant(double xd, const Consts& K, bool& 
   return ok ? q : 0.0;
 }
 
-// the histogram count of one emitted nonzero code: shared window, else global
-__device__ __forceinline__ void lr_hist(const HistSmem& hs, unsigned long long* hist, uint32_t code) {
-  const uint32_t b = code - hs.lo;
-  if (b < hs.nwin) atomicAdd(&hs.win[b], 1u);
-  else atomicAdd(&hist[code], 1ull);
-}
+// Where a tile's Lorenzo codes live: a u16 slab, or (TMA kernel) the lane's own element slots of the
+// tile stage, each overwritten once its x has been read (a lane only ever reads its own elements of the
+// stage; outlier values then come from the field in global memory).
+struct LrSlabL {
+  uint16_t* s16;
+  uint32_t* s32;   // non-null: the code of element s is s32[s * w]
+  int w;
+  __device__ __forceinline__ void put(uint32_t s, uint32_t c) const {
+    if (s32) s32[s * w] = c;
+    else s16[s] = (uint16_t)c;
+  }
+  __device__ __forceinline__ uint16_t get(uint32_t s) const { return s32 ? (uint16_t)s32[s * w] : s16[s]; }
+};
 
+// ox / osi / osj: where the outliers' values are read (the stage, or the field when the stage holds codes)
 template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
-__device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
-                                        const uint16_t* sL, uint32_t costR, uint32_t costL, const int32_t cc[4],
+__device__ __forceinline__ void lr_emit(const T* __restrict__ ox, uint64_t osi, uint64_t osj, uint16_t* sR,
+                                        const LrSlabL& sL, uint32_t costR, uint32_t costL, const int32_t cc[4],
                                         uint64_t bid, const LaneGeom& L, const TileCoord tc, const Geo& g,
                                         const CompressOut<T>& o, uint8_t* __restrict__ flags, const HistSmem& hs,
                                         const CUtensorMap* tm_c);
@@ -50,7 +58,7 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, u
 // field (IN_SMEM = false, predicated loads).  sR / sL: the warp's two code slabs [i][j][k] (6 x 6 x 96).
 template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
 __device__ __forceinline__ void lr_compress_tile_exact(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
-                                                 uint16_t* sL, const TileCoord tc, const Geo& g, const Consts& K,
+                                                 const LrSlabL& sL, const TileCoord tc, const Geo& g, const Consts& K,
                                                  uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
                                                  const HistSmem& hs, const CUtensorMap* tm_c) {
   const LaneGeom L = lane_geom<FULL>(tc, g);
@@ -109,7 +117,7 @@ __device__ __forceinline__ void lr_compress_tile_exact(const T* __restrict__ xs,
         costL += cl ? (uint32_t)fabs((double)cl - dR) : R;
         const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
         sR[s] = (uint16_t)cr[kk];
-        sL[s] = (uint16_t)cl;
+        sL.put(s, cl);
       }
     }
   }
@@ -121,8 +129,8 @@ __device__ __forceinline__ void lr_compress_tile_exact(const T* __restrict__ xs,
 // (histogram, outliers through rare_path) and the tile leaves with one TMA store of sR (TMA_OUT) or
 // element stores.  With TMA_OUT the caller waits for the store's reads before sR is written again.
 template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
-__device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
-                                        const uint16_t* sL, uint32_t costR, uint32_t costL, const int32_t cc[4],
+__device__ __forceinline__ void lr_emit(const T* __restrict__ ox, uint64_t osi, uint64_t osj, uint16_t* sR,
+                                        const LrSlabL& sL, uint32_t costR, uint32_t costL, const int32_t cc[4],
                                         uint64_t bid, const LaneGeom& L, const TileCoord tc, const Geo& g,
                                         const CompressOut<T>& o, uint8_t* __restrict__ flags, const HistSmem& hs,
                                         const CUtensorMap* tm_c) {
@@ -144,11 +152,17 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, u
 #pragma unroll
         for (int kk = 0; kk < 3; kk++) {
           const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
-          sR[s] = sL[s];
+          sR[s] = sL.get(s);
         }
   }
   bool has_out = false;
   const uint64_t gbase = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+  // histogram as in quantize_rows: one unconditional shared reduction per element into the window (or
+  // the lane's sink), which the hardware aggregates per address within the warp; codes outside the
+  // window (rare) go to the global bins
+  const uint32_t hb = (uint32_t)__cvta_generic_to_shared(hs.win) - 4u * hs.lo;
+  const uint32_t sink = (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * (threadIdx.x & 31);
+  const bool hist = o.hist != nullptr;
 #pragma unroll 1
   for (int i = 0; i < BS; i++)
 #pragma unroll
@@ -156,14 +170,14 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, u
 #pragma unroll
       for (int kk = 0; kk < 3; kk++) {
         const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
-        if (!valid) continue;
-        const uint16_t code = sR[(uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk)];
-        if (!TMA_OUT) o.codes[gbase + ((uint64_t)i * g.n1 + j) * g.n2 + L.kcol + kk] = code;
-        if (code) {
-          if (o.hist) lr_hist(hs, o.hist, code);
-        } else {
-          has_out = true;
+        const uint32_t code = sR[(uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk)];
+        if (!TMA_OUT && valid) o.codes[gbase + ((uint64_t)i * g.n1 + j) * g.n2 + L.kcol + kk] = (uint16_t)code;
+        const bool inwin = valid && code != 0u && code - hs.lo < hs.nwin;
+        if (hist) {
+          red_smem_add(inwin ? hb + 4u * code : sink, 1u);
+          if (valid && code != 0u && !inwin) atomicAdd(&o.hist[code], 1ull);
         }
+        has_out |= valid && code == 0u;
       }
   __syncwarp();
   if (TMA_OUT) {
@@ -174,8 +188,8 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ xs, uint64_t si, u
       ptx::bulk_commit();
     }
   }
-  if (o.hist) rare_path<T, true, BS>(xs, si, sj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
-  else rare_path<T, false, BS>(xs, si, sj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
+  if (o.hist) rare_path<T, true, BS>(ox, osi, osj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
+  else rare_path<T, false, BS>(ox, osi, osj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
   __syncwarp();
 }
 
@@ -212,7 +226,8 @@ __device__ __noinline__ LrExact lr_exact_elem(T xv, double b0, double b1, double
 // lr_compress_tile_exact (returns false).
 template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
 __device__ __forceinline__ bool lr_compress_tile_fast(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
-                                                      uint16_t* sL, const TileCoord tc, const Geo& g, const Consts& K,
+                                                      const LrSlabL& sL, const T* __restrict__ ox, uint64_t osi,
+                                                      uint64_t osj, const TileCoord tc, const Geo& g, const Consts& K,
                                                       uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
                                                       const HistSmem& hs, const CUtensorMap* tm_c) {
   constexpr bool F32 = sizeof(T) == 4;
@@ -351,31 +366,40 @@ __device__ __forceinline__ bool lr_compress_tile_fast(const T* __restrict__ xs, 
         costL += cl ? (uint32_t)abs((int)cl - iR) : R;
         const uint32_t sidx = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
         sR[sidx] = (uint16_t)c;
-        sL[sidx] = (uint16_t)cl;
+        sL.put(sidx, cl);
       }
     }
   }
   if (__any_sync(0xffffffffu, big)) return false;
-  lr_emit<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, costR, costL, cc, bid, L, tc, g, o, flags, hs, tm_c);
+  lr_emit<T, IN_SMEM, FULL, TMA_OUT>(ox, osi, osj, sR, sL, costR, costL, cc, bid, L, tc, g, o, flags, hs, tm_c);
   return true;
 }
 
+// xs / si / sj: the tile (stage or field); xg: the tile in the field (global strides).  With sL in the
+// stage the exact fallback reads the field (the stage may already hold codes).
 template <typename T, bool IN_SMEM, bool FULL, bool TMA_OUT>
-__device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj, uint16_t* sR,
-                                                 uint16_t* sL, const TileCoord tc, const Geo& g, const Consts& K,
-                                                 uint32_t R, const CompressOut<T>& o, uint8_t* __restrict__ flags,
-                                                 const HistSmem& hs, const CUtensorMap* tm_c) {
+__device__ __forceinline__ void lr_compress_tile(const T* __restrict__ xs, uint64_t si, uint64_t sj, const T* __restrict__ xg,
+                                                 uint16_t* sR, const LrSlabL& sL, const TileCoord tc, const Geo& g,
+                                                 const Consts& K, uint32_t R, const CompressOut<T>& o,
+                                                 uint8_t* __restrict__ flags, const HistSmem& hs, const CUtensorMap* tm_c) {
 #ifndef SZ3G_LR_FAST
 #define SZ3G_LR_FAST 1   // the certified fp32 routine first, the exact one for tiles with |q| >= 2^26
 #endif
-  if (!SZ3G_LR_FAST || !lr_compress_tile_fast<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, tc, g, K, R, o, flags, hs, tm_c))
+  const bool in_stage = sL.s32 != nullptr;
+  if (SZ3G_LR_FAST && lr_compress_tile_fast<T, IN_SMEM, FULL, TMA_OUT>(
+                          xs, si, sj, sR, sL, in_stage ? xg : xs, in_stage ? g.n1 * g.n2 : si, in_stage ? g.n2 : sj,
+                          tc, g, K, R, o, flags, hs, tm_c))
+    return;
+  if (in_stage || !IN_SMEM)
+    lr_compress_tile_exact<T, false, FULL, TMA_OUT>(xg, g.n1 * g.n2, g.n2, sR, sL, tc, g, K, R, o, flags, hs, tm_c);
+  else
     lr_compress_tile_exact<T, IN_SMEM, FULL, TMA_OUT>(xs, si, sj, sR, sL, tc, g, K, R, o, flags, hs, tm_c);
 }
 
 template <typename T, int W, int D>
 struct LrSmem {
   static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
-  static constexpr size_t slab_bytes = 2 * sizeof(uint16_t) * TILE_ELEMS;   // regression + Lorenzo codes
+  static constexpr size_t slab_bytes = sizeof(uint16_t) * TILE_ELEMS;   // regression (then final) codes
   static constexpr size_t off_slab = (size_t)W * D * stage_bytes;
   static constexpr size_t off_hist = off_slab + (size_t)W * slab_bytes;
   static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (LR_HW + 36);
@@ -386,8 +410,8 @@ struct LrSmem {
 // Persistent, W self-fed warps per CTA (each with a private D-stage TMA ring, as k_analyze_tma).
 template <typename T, int W, int D>
 __global__ void __launch_bounds__(W * 32, 1)
-    k_lr_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, KArgs a,
-                      CompressOut<T> o, uint8_t* __restrict__ flags) {
+    k_lr_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c,
+                      const T* __restrict__ x, KArgs a, CompressOut<T> o, uint8_t* __restrict__ flags) {
   using L_ = LrSmem<T, W, D>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
@@ -406,7 +430,6 @@ __global__ void __launch_bounds__(W * 32, 1)
   const Geo& g = a.g;
   T* ring = reinterpret_cast<T*>(smem) + (size_t)warp * D * TILE_ELEMS;
   uint16_t* sR = reinterpret_cast<uint16_t*>(smem + L_::off_slab + (size_t)warp * L_::slab_bytes);
-  uint16_t* sL = sR + TILE_ELEMS;
   uint64_t* bar = full + warp * D;
   TileWalk tw(warp, a.chunk, W), tl(warp, a.chunk, W);
   if (lane == 0) {
@@ -428,8 +451,10 @@ __global__ void __launch_bounds__(W * 32, 1)
     __syncwarp();
     ptx::mbar_wait(&bar[s], ph);
     const T* xs = ring + (size_t)s * TILE_ELEMS;
-    if (tile_full(tc, g)) lr_compress_tile<T, true, true, true>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
-    else lr_compress_tile<T, true, false, true>(xs, BS * TK, TK, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
+    const LrSlabL sL{nullptr, reinterpret_cast<uint32_t*>(ring + (size_t)s * TILE_ELEMS), (int)(sizeof(T) / 4)};
+    const T* xg = x + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+    if (tile_full(tc, g)) lr_compress_tile<T, true, true, true>(xs, BS * TK, TK, xg, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
+    else lr_compress_tile<T, true, false, true>(xs, BS * TK, TK, xg, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
     __syncwarp();
     if (lane == 0) {   // every lane's reads of the stage are done: refill it with tile k + D
       const uint64_t t2 = tl.tile();
@@ -469,12 +494,13 @@ __global__ void __launch_bounds__(LR_PW * 32) k_lr_compress_plain(const T* __res
   const Geo& g = a.g;
   const int warp = threadIdx.x >> 5;
   uint16_t* sR = slabs + (size_t)warp * 2 * TILE_ELEMS;
-  uint16_t* sL = sR + TILE_ELEMS;
+  const LrSlabL sL{sR + TILE_ELEMS, nullptr, 0};
   const uint64_t warps = (uint64_t)gridDim.x * LR_PW;
   for (uint64_t t = blockIdx.x * (uint64_t)LR_PW + warp; t < g.ntiles; t += warps) {
     const TileCoord tc = decode_tile(t, g);
     const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
-    lr_compress_tile<T, false, false, false>(x + off, g.n1 * g.n2, g.n2, sR, sL, tc, g, K, a.R, o, flags, hs, nullptr);
+    lr_compress_tile<T, false, false, false>(x + off, g.n1 * g.n2, g.n2, x + off, sR, sL, tc, g, K, a.R, o, flags, hs,
+                                             nullptr);
   }
   __syncthreads();
   if (o.hist) hist_flush(hs, o.hist);

@@ -1200,13 +1200,13 @@ int launch_analyze_tma(const Geo& g, const void* x, double* beta, unsigned long 
 #include "lr.cuh"
 
 #ifndef SZ3G_LR_W
-#define SZ3G_LR_W 7
+#define SZ3G_LR_W 10
 #endif
 #ifndef SZ3G_LR_D
 #define SZ3G_LR_D 1
 #endif
-constexpr int LW32 = SZ3G_LR_W, LD32 = SZ3G_LR_D;   // f32 LR compress: 7 self-fed warps x 1 stage (+ 2 code slabs each)
-constexpr int LW64 = 3, LD64 = 2;   // f64 LR compress: 3 warps x 2 stages
+constexpr int LW32 = SZ3G_LR_W, LD32 = SZ3G_LR_D;   // f32 LR compress: 10 self-fed warps x 1 stage (+ 1 code slab each)
+constexpr int LW64 = 6, LD64 = 1;   // f64 LR compress: 6 warps x 1 stage
 
 template <typename T, int W, int D>
 int launch_lr_tma(const Geo& g, const void* x, const KArgs& ka, const CompressOut<T>& co, uint8_t* flags,
@@ -1221,7 +1221,7 @@ int launch_lr_tma(const Geo& g, const void* x, const KArgs& ka, const CompressOu
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
-  kern<<<(unsigned)grid, W * 32, L::total, st>>>(mx, mc, ka, co, flags);
+  kern<<<(unsigned)grid, W * 32, L::total, st>>>(mx, mc, (const T*)x, ka, co, flags);
   return check_launch(1);
 }
 
