@@ -32,6 +32,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+NOMINAL_HBM_GBS = 8000.0   # B200 nominal HBM3e bandwidth (north_star's ~8 TB/s): the second denominator of SURVEY 8(d)
 METRIC = "regression compress & decompress GB/s per GPU and 8-GPU, % of HBM roofline"
 UNIT = "GB/s"
 CONFIG = "c5"
@@ -550,15 +551,18 @@ def main():
                          "unit": "GB/s", "frac": comp_gbs / peaks["hbm_gbs"],
                          "traffic": profiled_traffic("k_compress_tma" + ("_beta" if two_pass else ""), cfg.name),
                          "peak_source": peaks["source"],
+                         "frac_nominal": comp_gbs / NOMINAL_HBM_GBS, "peak_nominal": NOMINAL_HBM_GBS,
                          "alg_bytes_per_launch": comp_bytes, "ms_per_launch": comp_ms},
             "compress_gbs": N_global * s / (comp_ms_max * 1e-3) / 1e9,
             "decompress_gbs": N_global * s / (dec_ms_max * 1e-3) / 1e9,
             "decompress_roofline": {"achieved": dec_bytes / (dec_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                                     "frac": dec_bytes / (dec_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                    "frac_nominal": dec_bytes / (dec_ms * 1e-3) / 1e9 / NOMINAL_HBM_GBS,
                                     "ms_per_launch": dec_ms},
             "analyze_roofline": {"kernel": "k_analyze_tma" if two_pass else "k_value_range",
                                  "achieved": ana_bytes / (ana_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                                  "frac": ana_bytes / (ana_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                 "frac_nominal": ana_bytes / (ana_ms * 1e-3) / 1e9 / NOMINAL_HBM_GBS,
                                  "ms_per_step": ana_ms},
             "path": args.path,
             "quality": quality, "huffman": huff, "truncation": trunc, "lr": lr,
