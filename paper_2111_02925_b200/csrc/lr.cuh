@@ -684,3 +684,351 @@ __global__ void __launch_bounds__(W * 32, 1)
     }
   }
 }
+
+// ---------------------------------------------------------------------------------- LR compress, pairs
+// Two warps per tile: warp half HW takes planes [3 HW, 3 HW + 3) and the second half also runs plane 2
+// (q and its j,k-differences only) for its first i-difference, so each lane carries 3 (+1) x 3
+// differences instead of 6 x 3 and the unrolled body holds 9 elements -- the single-warp kernel's
+// 18-element body was ~48 KB of hot code, bound by instruction fetch.  Per tile three pair barriers:
+// slabs free (the previous tile's TMA store has read them), block costs exchanged, codes complete.
+template <typename T, bool FULL>
+__device__ __forceinline__ void lr_half_compute(const T* __restrict__ xs, uint16_t* sR, uint16_t* sL, const LaneGeom& L,
+                                                const double bh[4], const Fast32& F, const Fast32& F0, const Consts& K,
+                                                uint32_t R, uint32_t& costR, uint32_t& costL, bool& big, int HW) {
+  // one code path for both halves (one hot body in the instruction cache): planes P0 .. P0 + 3, codes for
+  // i >= I0; the first half's helper plane is plane -1 (outside the block: q = 0)
+  constexpr bool F32 = sizeof(T) == 4;
+  constexpr int NP = 4;
+  const int I0 = 3 * HW, P0 = 3 * HW - 1;
+  const int h = L.h;
+  const float inv2eb32 = K.inv2eb32;
+  const float M32 = 12582912.0f;                 // 1.5 * 2^23
+  const float Rf = (float)R;
+  const int iR = (int)R;
+  int32_t Dp[3][NP];
+#pragma unroll
+  for (int kk = 0; kk < 3; kk++)
+#pragma unroll
+    for (int ii = 0; ii < NP; ii++) Dp[kk][ii] = 0;
+#pragma unroll 1
+  for (int j = 0; j < BS; j++) {
+    int32_t q[3][NP];
+    uint32_t cr[3][NP];
+    bool lv[3][NP];
+    const float fj = (float)j;
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++) {
+      const bool cv = FULL || ((j < L.m1) && L.kv(kk));
+      T xv[NP];
+#pragma unroll
+      for (int ii = 0; ii < NP; ii++) xv[ii] = (P0 + ii >= 0) ? xs[(P0 + ii) * (BS * TK) + j * TK + L.kcol + kk] : T(0);
+      bool need = false;
+      if (F32) {
+        const float base32 = __fmaf_rn(F.a2, fj, __fmaf_rn(F.a3, (float)(3 * h + kk), F.a0));
+#pragma unroll
+        for (int ii = 0; ii < NP; ii++) {
+          const int i = P0 + ii;
+          const bool valid = i >= 0 && (FULL || (cv && i < L.m0));
+          const float x32 = (float)xv[ii];
+          if (i >= I0) {
+            const float P = i == 0 ? base32 : __fmaf_rn(F.a1, (float)i, base32);
+            const float t32 = __fmaf_rn(x32, inv2eb32, -P);
+            const float r = __fsub_rn(__fadd_rn(t32, M32), M32);
+            const float e = __fsub_rn(t32, r);
+            const bool ok = __fmaf_rn(F.k1, fabsf(t32), fabsf(e)) <= F.thr && fabsf(r) < Rf;
+            cr[kk][ii] = ok ? (uint32_t)((int)r + iR) : 0u;
+            need |= valid && !ok;
+          } else {
+            cr[kk][ii] = R;
+          }
+          const float tL = __fmul_rn(x32, inv2eb32);
+          const float rL = __fsub_rn(__fadd_rn(tL, M32), M32);
+          const float eL = __fsub_rn(tL, rL);
+          const bool okL = __fmaf_rn(F0.k1, fabsf(tL), fabsf(eL)) <= F0.thr && fabsf(tL) < 4194304.0f;
+          q[kk][ii] = okL ? (int32_t)rL : 0;
+          lv[kk][ii] = okL;
+          need |= valid && !okL;
+        }
+      } else {
+        const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0]));
+#pragma unroll
+        for (int ii = 0; ii < NP; ii++) {
+          const int i = P0 + ii;
+          const bool valid = i >= 0 && (FULL || (cv && i < L.m0));
+          const double xd = to_d<T>(xv[ii]);
+          if (i >= I0) {
+            const double p = __fma_rn(bh[1], (double)i, base);
+            const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+            const double rq = __dsub_rn(__dadd_rn(t, RINT_MAGIC), RINT_MAGIC);
+            const bool ok = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(t, rq))) <= K.vthr && fabs(rq) < (double)R;
+            cr[kk][ii] = ok ? (uint32_t)((int)rq + iR) : 0u;
+            need |= valid && !ok;
+          } else {
+            cr[kk][ii] = R;
+          }
+          const double tL = __dmul_rn(xd, K.inv2eb);
+          const double rL = __dsub_rn(__dadd_rn(tL, RINT_MAGIC), RINT_MAGIC);
+          const bool okL = __fma_rn(K.vc, fabs(xd), fabs(__dsub_rn(tL, rL))) <= K.vthr && fabs(tL) < 67108864.0;
+          q[kk][ii] = okL ? (int32_t)rL : 0;
+          lv[kk][ii] = okL;
+          need |= valid && !okL;
+        }
+      }
+      if (__any_sync(0xffffffffu, need)) {   // the exact definitions (rare)
+#pragma unroll
+        for (int ii = 0; ii < NP; ii++) {
+          const int i = P0 + ii;
+          const bool valid = i >= 0 && (FULL || (cv && i < L.m0));
+          const bool wr = i >= I0 && cr[kk][ii] == 0u;
+          if (valid && (wr || !lv[kk][ii])) {
+            const LrExact ex = lr_exact_elem<T>(xv[ii], bh[0], bh[1], bh[2], bh[3], i, j, 3 * h + kk, K, R, wr,
+                                                !lv[kk][ii]);
+            if (wr) cr[kk][ii] = ex.cr;
+            if (!lv[kk][ii]) {
+              big |= ex.big;
+              q[kk][ii] = ex.q;
+              lv[kk][ii] = ex.lv;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int ii = 0; ii < NP; ii++) {
+        const bool valid = P0 + ii >= 0 && (FULL || (cv && P0 + ii < L.m0));
+        if (!valid) { q[kk][ii] = 0; lv[kk][ii] = false; cr[kk][ii] = R; }
+      }
+    }
+    int32_t left[NP];
+#pragma unroll
+    for (int ii = 0; ii < NP; ii++) {
+      left[ii] = __shfl_up_sync(0xffffffffu, q[2][ii], 1);
+      if (h == 0) left[ii] = 0;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++) {
+      const bool cv = FULL || ((j < L.m1) && L.kv(kk));
+      int32_t Eprev = 0;
+#pragma unroll
+      for (int ii = 0; ii < NP; ii++) {
+        const int i = P0 + ii;
+        const int32_t D = q[kk][ii] - (kk == 0 ? left[ii] : q[kk - 1][ii]);
+        const int32_t E = D - Dp[kk][ii];
+        Dp[kk][ii] = D;
+        const int32_t delta = E - Eprev;
+        Eprev = E;
+        if (i < I0) continue;   // the helper plane
+        const bool valid = FULL || (cv && i < L.m0);
+        uint32_t cl = (lv[kk][ii] && delta > -iR && delta < iR) ? (uint32_t)(delta + iR) : 0u;
+        if (!valid) cl = R;
+        const uint32_t c = cr[kk][ii];
+        costR += c ? (uint32_t)abs((int)c - iR) : R;
+        costL += cl ? (uint32_t)abs((int)cl - iR) : R;
+        const uint32_t sidx = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
+        sR[sidx] = (uint16_t)c;
+        sL[sidx] = (uint16_t)cl;
+      }
+    }
+  }
+}
+
+// outliers of planes [i0, i0 + 3) (rare_path over a plane range)
+template <typename T, bool HIST>
+__device__ __forceinline__ void lr_rare_planes(const T* __restrict__ xs, const uint16_t* cs, int i0, const LaneGeom& L,
+                                               bool has_out, const TileCoord tc, const Geo& g, const CompressOut<T>& o,
+                                               const HistSmem& hs) {
+  const int lane = threadIdx.x & 31;
+  if (!__any_sync(0xffffffffu, has_out)) return;
+  const int i1 = min(i0 + 3, L.m0);
+  uint32_t nout = 0;
+  if (has_out) {
+    for (int i = i0; i < i1; i++)
+      for (int j = 0; j < L.m1; j++)
+        for (int kk = 0; kk < 3; kk++)
+          if (L.kv(kk)) nout += (cs[i * (BS * TK) + j * TK + L.kcol + kk] == 0u) ? 1u : 0u;
+  }
+  uint32_t incl = nout;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long basepos = 0;
+  if (lane == 31) {
+    basepos = atomicAdd(o.ocount, (unsigned long long)total);
+    if (HIST) atomicAdd(hs.zero, total);
+  }
+  basepos = __shfl_sync(0xffffffffu, basepos, 31);
+  unsigned long long pos = basepos + (incl - nout);
+  if (nout) {
+    const uint64_t gbase =
+        g.gofs + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)L.kb * BS + 3 * L.h;
+    for (int i = i0; i < i1; i++)
+      for (int j = 0; j < L.m1; j++)
+        for (int kk = 0; kk < 3; kk++) {
+          if (!L.kv(kk) || cs[i * (BS * TK) + j * TK + L.kcol + kk] != 0) continue;
+          if (pos < o.cap) {
+            o.oidx[pos] = gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk;
+            o.oval[pos] = xs[i * (BS * TK) + j * TK + L.kcol + kk];
+          }
+          pos++;
+        }
+  }
+}
+
+template <typename T, int NPAIR>
+struct LrPairSmem {
+  static constexpr size_t stage_bytes = sizeof(T) * TILE_ELEMS;
+  static constexpr size_t slab_bytes = sizeof(uint16_t) * TILE_ELEMS;
+  // + costs + flag, rounded to 128 bytes: every pair's stage is a TMA destination
+  static constexpr size_t pair_bytes = (stage_bytes + 2 * slab_bytes + 2 * 16 * 8 + 16 + 127) / 128 * 128;
+  static constexpr size_t off_hist = (size_t)NPAIR * pair_bytes;
+  static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (LR_HW + 36);
+  static constexpr size_t off_k = off_bar + (size_t)NPAIR * sizeof(uint64_t);
+  static constexpr size_t total = off_k + sizeof(Consts) + 16;
+};
+
+__device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+template <typename T, bool FULL>
+__device__ __forceinline__ void lr_pair_tile(const T* __restrict__ xs, uint16_t* sR, uint16_t* sL, uint2* s_cost,
+                                             int* s_big, int hw, int bar_id, const TileCoord tc, const Geo& g,
+                                             const Consts& K, uint32_t R, const CompressOut<T>& o,
+                                             uint8_t* __restrict__ flags, const HistSmem& hs, const CUtensorMap* tm_c) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int h = L.h, lane = threadIdx.x & 31, bl = lane >> 1;
+  double beta[4] = {0.0, 0.0, 0.0, 0.0}, bh[4];
+  int32_t cc[4];
+  const uint64_t bid = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb;
+  if (L.m2 > 0) {
+    const double2 b01 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid);
+    const double2 b23 = __ldg(reinterpret_cast<const double2*>(o.beta_in) + 2 * bid + 1);
+    beta[0] = b01.x; beta[1] = b01.y; beta[2] = b23.x; beta[3] = b23.y;
+  }
+  block_codes(beta, K, cc, bh);
+  const Fast32 F = fast32_consts(bh, K);
+  const double zero[4] = {0.0, 0.0, 0.0, 0.0};
+  const Fast32 F0 = fast32_consts(zero, K);
+  uint32_t costR = 0, costL = 0;
+  bool big = false;
+  lr_half_compute<T, FULL>(xs, sR, sL, L, bh, F, F0, K, R, costR, costL, big, hw);
+  costR += __shfl_xor_sync(0xffffffffu, costR, 1);
+  costL += __shfl_xor_sync(0xffffffffu, costL, 1);
+  if (h == 0) s_cost[hw * 16 + bl] = make_uint2(costR, costL);
+  if (__any_sync(0xffffffffu, big) && lane == 0) *s_big = 1;
+  pair_bar(bar_id);   // (2) both halves' costs and the big flag
+  if (*s_big) {       // a q beyond the int32 residuals: the whole tile by the int64 routine (first warp)
+    if (hw == 0)
+      lr_compress_tile_exact<T, true, FULL, true>(xs, BS * TK, TK, sR, LrSlabL{sL, nullptr, 0}, tc, g, K, R, o, flags,
+                                                  hs, tm_c);
+    return;
+  }
+  const uint2 c0 = s_cost[bl], c1 = s_cost[16 + bl];
+  const bool useL = c0.y + c1.y < c0.x + c1.x;
+  if (hw == 0 && L.m2 > 0 && h == 0) {
+    reinterpret_cast<int4*>(o.coef)[bid] = useL ? make_int4(0, 0, 0, 0) : make_int4(cc[0], cc[1], cc[2], cc[3]);
+    flags[bid] = useL ? 1 : 0;
+  }
+  const int i0 = 3 * hw;
+  const uint32_t hb = (uint32_t)__cvta_generic_to_shared(hs.win) - 4u * hs.lo;
+  const uint32_t sink = (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * lane;
+  const bool hist = o.hist != nullptr;
+  bool has_out = false;
+#pragma unroll 1
+  for (int i = i0; i < i0 + 3; i++)
+#pragma unroll
+    for (int j = 0; j < BS; j++)
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
+        const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
+        uint32_t code = sR[s];
+        if (useL) {
+          code = sL[s];
+          sR[s] = (uint16_t)code;
+        }
+        const bool inwin = valid && code != 0u && code - hs.lo < hs.nwin;
+        if (hist) {
+          red_smem_add(inwin ? hb + 4u * code : sink, 1u);
+          if (valid && code != 0u && !inwin) atomicAdd(&o.hist[code], 1ull);
+        }
+        has_out |= valid && code == 0u;
+      }
+  __syncwarp();
+  if (hist) lr_rare_planes<T, true>(xs, sR, i0, L, has_out, tc, g, o, hs);
+  else lr_rare_planes<T, false>(xs, sR, i0, L, has_out, tc, g, o, hs);
+  ptx::fence_proxy_async_smem();   // this warp's code writes, before the pair's TMA store
+}
+
+template <typename T, int NPAIR>
+__global__ void __launch_bounds__(NPAIR * 64, 1)
+    k_lr_compress_pair(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, KArgs a,
+                       CompressOut<T> o, uint8_t* __restrict__ flags) {
+  using L_ = LrPairSmem<T, NPAIR>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L_::off_bar);
+  Consts* s_k = reinterpret_cast<Consts*>(smem + L_::off_k);
+  int* s_ok = reinterpret_cast<int*>(smem + L_::off_k + sizeof(Consts));
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(smem + L_::off_hist);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = warp >> 1, hw = warp & 1, bar_id = 1 + p;
+  HistSmem hs;
+  hist_init(hs, s_win, s_win + LR_HW, a.R, LR_HW);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NPAIR; s++) ptx::mbar_init(&full[s], 1);
+    ptx::fence_mbar_init();
+  }
+  if (!cta_consts(a, s_k, s_ok)) return;
+  const Consts K = *s_k;
+  const Geo& g = a.g;
+  uint8_t* pb = smem + (size_t)p * L_::pair_bytes;
+  T* stage = reinterpret_cast<T*>(pb);
+  uint16_t* sR = reinterpret_cast<uint16_t*>(pb + L_::stage_bytes);
+  uint16_t* sL = sR + TILE_ELEMS;
+  uint2* s_cost = reinterpret_cast<uint2*>(pb + L_::stage_bytes + 2 * L_::slab_bytes);
+  int* s_big = reinterpret_cast<int*>(pb + L_::stage_bytes + 2 * L_::slab_bytes + 2 * 16 * 8);
+  const bool loader = hw == 0 && lane == 0;
+  TileWalk tw(p, a.chunk, NPAIR), tl(p, a.chunk, NPAIR);
+  if (loader) {
+    ptx::prefetch_tensormap(&tm_x);
+    const uint64_t t = tl.tile();
+    if (t < g.ntiles) {
+      const TileCoord tc = decode_tile(t, g);
+      ptx::mbar_arrive_expect_tx(&full[p], (uint32_t)L_::stage_bytes);
+      ptx::tma_load_3d(stage, &tm_x, &full[p], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+    }
+    tl.next();
+  }
+  for (uint32_t k = 0;; k++, tw.next()) {
+    const uint64_t t = tw.tile();
+    if (t >= g.ntiles) break;
+    const TileCoord tc = decode_tile(t, g);
+    if (loader) {
+      ptx::bulk_wait_read0();   // the previous tile's code store has read sR
+      *s_big = 0;
+    }
+    pair_bar(bar_id);   // (1) slabs free, flag reset
+    ptx::mbar_wait(&full[p], k & 1u);
+    if (tile_full(tc, g)) lr_pair_tile<T, true>(stage, sR, sL, s_cost, s_big, hw, bar_id, tc, g, K, a.R, o, flags, hs, &tm_c);
+    else lr_pair_tile<T, false>(stage, sR, sL, s_cost, s_big, hw, bar_id, tc, g, K, a.R, o, flags, hs, &tm_c);
+    pair_bar(bar_id);   // (3) the tile's codes complete, the stage no longer read
+    if (loader) {
+      if (!*s_big) {
+        ptx::tma_store_3d(&tm_c, sR, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
+        ptx::bulk_commit();
+      }
+      const uint64_t t2 = tl.tile();
+      if (t2 < g.ntiles) {
+        const TileCoord tc2 = decode_tile(t2, g);
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive_expect_tx(&full[p], (uint32_t)L_::stage_bytes);
+        ptx::tma_load_3d(stage, &tm_x, &full[p], (int)(tc2.c * TK), (int)(tc2.b * BS), (int)(tc2.a * BS));
+      }
+      tl.next();
+    }
+  }
+  if (loader) ptx::bulk_wait0();
+  __syncthreads();
+  if (o.hist) hist_flush(hs, o.hist);
+  overflow_check(a, o.ocount, o.cap);
+}

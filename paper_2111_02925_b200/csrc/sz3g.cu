@@ -1246,6 +1246,28 @@ int launch_lr_dec_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, 
   return SZ3G_OK;
 }
 
+#ifndef SZ3G_LR_PAIR
+#define SZ3G_LR_PAIR 1   // SZ3-LR compress: two warps per tile (k_lr_compress_pair); 0: one warp per tile
+#endif
+constexpr int LP32 = 7, LP64 = 5;   // tile pairs per CTA (f32 / f64)
+
+template <typename T, int NPAIR>
+int launch_lr_pair(const Geo& g, const void* x, const KArgs& ka, const CompressOut<T>& co, uint8_t* flags,
+                   cudaStream_t st) {
+  using L = LrPairSmem<T, NPAIR>;
+  static_assert(L::total <= 232448, "smem");
+  CUtensorMap mx, mc;
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
+  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, co.codes, g)) return SZ3G_ECUDA;
+  auto kern = k_lr_compress_pair<T, NPAIR>;
+  cudaError_t e = set_smem(kern, L::total);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const uint64_t grid = std::min<uint64_t>((g.ntiles + NPAIR - 1) / NPAIR, (uint64_t)sm_count());
+  kern<<<(unsigned)grid, NPAIR * 64, L::total, st>>>(mx, mc, ka, co, flags);
+  return check_launch(1);
+}
+
 template <typename T>
 int launch_lr_plain(const Geo& g, const void* x, const KArgs& ka, const CompressOut<T>& co, uint8_t* flags,
                     cudaStream_t st) {
@@ -1422,10 +1444,12 @@ int sz3g_lr_quantize(const sz3g_grid* grid, const sz3g_params* params, const voi
   if (grid->dtype == SZ3G_F32) {
     CompressOut<float> co{codes, coef_codes, nullptr, outlier_idx, (float*)outlier_val, outlier_cap, d_outlier_count,
                           h, beta};
+    if (tma && SZ3G_LR_PAIR) return launch_lr_pair<float, LP32>(g, x, ka, co, flags, st);
     return tma ? launch_lr_tma<float, LW32, LD32>(g, x, ka, co, flags, st) : launch_lr_plain<float>(g, x, ka, co, flags, st);
   }
   CompressOut<double> co{codes, coef_codes, nullptr, outlier_idx, (double*)outlier_val, outlier_cap, d_outlier_count,
                          h, beta};
+  if (tma && SZ3G_LR_PAIR) return launch_lr_pair<double, LP64>(g, x, ka, co, flags, st);
   return tma ? launch_lr_tma<double, LW64, LD64>(g, x, ka, co, flags, st) : launch_lr_plain<double>(g, x, ka, co, flags, st);
 }
 

@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--flags", type=int, default=int(os.environ.get("LR_FLAGS", "0")))
+ap.add_argument("--no-hist", action="store_true")
 ap.add_argument("rest", nargs="*")
 a, _ = ap.parse_known_args()
 cfg = config_by_name(a.config)
@@ -27,7 +28,7 @@ qs, ds = [], []
 for _ in range(a.reps):
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     e0.record()
-    sz3g.lr_quantize(x, cfg.eb, cfg.eb_mode, cfg.radius, minmax, beta, bufs, flags=a.flags)
+    sz3g.lr_quantize(x, cfg.eb, cfg.eb_mode, cfg.radius, minmax, beta, bufs, flags=a.flags, hist=not a.no_hist)
     e1.record()
     sz3g.lr_decompress(res.codes, res.coef_codes, res.lr_flags, res.outlier_idx, res.outlier_val,
                        res.outlier_idx.numel(), cfg.eb, cfg.radius, x.dtype, out=out, d_outlier_count=res.outlier_count,
