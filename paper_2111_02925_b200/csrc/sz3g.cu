@@ -1050,7 +1050,13 @@ constexpr int DG32 = 3, DN32 = SZ3G_DEC_CFG == 1 ? 7 : (SZ3G_DEC_CFG == 3 ? 4 : 
               DD32 = (SZ3G_DEC_CFG == 1 || SZ3G_DEC_CFG == 2) ? 2 : 3,
               DOB32 = SZ3G_DEC_CFG >= 2 ? 2 : 1;  // f32 decompress: groups of 3 warps + producer
 constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 warps + producer
-constexpr int AW32 = 8, AD32 = 2;            // f32 analyze: 8 self-fed warps x 2 stages (13.5 KiB)
+#ifndef SZ3G_AW
+#define SZ3G_AW 12
+#endif
+#ifndef SZ3G_AD
+#define SZ3G_AD 1
+#endif
+constexpr int AW32 = SZ3G_AW, AD32 = SZ3G_AD;   // f32 analyze: 12 self-fed warps x 1 stage (13.5 KiB each)
 constexpr int AW64 = 4, AD64 = 2;            // f64 analyze: 4 warps x 2 stages (27 KiB)
 
 template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN, bool NOR0 = false>
