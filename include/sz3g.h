@@ -326,8 +326,11 @@ enum {
   SZ3G_SEC_COEF_DATA = 6,
   SZ3G_SEC_COEF_ESC = 7,    /* coefficient escapes, u64 zigzag values in position order               */
   SZ3G_SEC_OUT_IDX = 8,     /* outlier global indices, u64                                            */
-  SZ3G_SEC_OUT_VAL = 9      /* outlier values, T                                                      */
+  SZ3G_SEC_OUT_VAL = 9,     /* outlier values, T                                                      */
+  SZ3G_SEC_LR_FLAGS = 10    /* SZ3-LR predictor flags, one bit per block (LSB first; 1 = Lorenzo);
+                               present iff header.flags has SZ3G_STREAM_LR                            */
 };
+#define SZ3G_STREAM_LR 0x1u   /* sz3g_stream_header.flags: an SZ3-LR stream (decompress with sz3g_lr_decompress) */
 uint64_t sz3g_stream_size(const sz3g_section* sections, uint32_t nsec);
 int sz3g_stream_write(const sz3g_stream_header* hdr, const sz3g_section* sections, uint32_t nsec,
                       void* out, uint64_t cap, uint64_t* written);

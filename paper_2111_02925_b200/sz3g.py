@@ -54,7 +54,8 @@ class Section(ctypes.Structure):
 
 
 SEC_CODE_BOOK, SEC_CODE_OFFS, SEC_CODE_DATA, SEC_COEF_BOOK, SEC_COEF_OFFS, SEC_COEF_DATA, SEC_COEF_ESC, \
-    SEC_OUT_IDX, SEC_OUT_VAL = range(1, 10)
+    SEC_OUT_IDX, SEC_OUT_VAL, SEC_LR_FLAGS = range(1, 11)
+STREAM_LR = 0x1   # sz3g_stream_header.flags: SZ3-LR stream
 
 
 _lib = None
@@ -794,6 +795,9 @@ def to_bytes(res: "Compressed", table: HuffmanTable | None = None, hs: HuffmanSt
         (SEC_OUT_IDX, res.outlier_idx[:n].cpu().numpy().tobytes()),
         (SEC_OUT_VAL, res.outlier_val[:n].cpu().numpy().tobytes()),
     ]
+    if res.lr_flags is not None:   # SZ3-LR: the per-block predictor flags as a bitmap
+        import numpy as np
+        host.append((SEC_LR_FLAGS, np.packbits(res.lr_flags.cpu().numpy(), bitorder="little").tobytes()))
     secs = (Section * len(host))()
     keep = []
     for i, (tag, b) in enumerate(host):
@@ -804,7 +808,7 @@ def to_bytes(res: "Compressed", table: HuffmanTable | None = None, hs: HuffmanSt
     hdr = StreamHeader(_dtype_id(res.dtype), len(res.shape), (ctypes.c_uint64 * 3)(*s3),
                        {"abs": SZ3G_EB_ABS, "rel": SZ3G_EB_REL_RANGE}[eb_mode],
                        float(res.eb_abs if eb is None else eb), float(res.eb_abs), res.radius, BLOCK, hs.chunk,
-                       table.max_len, 0, n, res.coef_codes.shape[0])
+                       table.max_len, STREAM_LR if res.lr_flags is not None else 0, n, res.coef_codes.shape[0])
     lib = load()
     size = int(lib.sz3g_stream_size(secs, len(host)))
     out = ctypes.create_string_buffer(size)
@@ -858,9 +862,18 @@ def from_bytes(buf: bytes, device=None) -> torch.Tensor:
     oidx = torch.from_numpy(np.frombuffer(sec[SEC_OUT_IDX], np.int64).copy()).to(device)
     oval = torch.from_numpy(np.frombuffer(sec[SEC_OUT_VAL], np.float32 if dtype == torch.float32 else np.float64)
                             .copy()).to(device)
-    out = regression_decompress(codes, coef, oidx if oidx.numel() else torch.zeros(1, dtype=torch.int64, device=device),
-                                oval if oval.numel() else torch.zeros(1, dtype=dtype, device=device),
-                                int(hdr.n_outliers), hdr.eb_abs, R, dtype)
+    oidx = oidx if oidx.numel() else torch.zeros(1, dtype=torch.int64, device=device)
+    oval = oval if oval.numel() else torch.zeros(1, dtype=dtype, device=device)
+    if hdr.flags & STREAM_LR:
+        if SEC_LR_FLAGS not in sec:
+            raise SZ3GError("corrupt stream: SZ3-LR stream without its flags section")
+        bits = np.unpackbits(np.frombuffer(sec[SEC_LR_FLAGS], np.uint8), bitorder="little")[:nb]
+        if bits.size != nb:
+            raise SZ3GError("corrupt stream: short SZ3-LR flags section")
+        fl = torch.from_numpy(bits.astype(np.uint8)).to(device)
+        out = lr_decompress(codes, coef, fl, oidx, oval, int(hdr.n_outliers), hdr.eb_abs, R, dtype)
+    else:
+        out = regression_decompress(codes, coef, oidx, oval, int(hdr.n_outliers), hdr.eb_abs, R, dtype)
     torch.cuda.synchronize()
     if int(hs.status.item()) or int(cs.status.item()):
         raise SZ3GError("corrupt Huffman stream")

@@ -47,3 +47,21 @@ def test_outliers_and_corruption():
     b[len(b) // 2] ^= 1
     with pytest.raises(Exception, match="corrupt"):
         s.from_bytes(bytes(b))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_lr_bytes_round_trip(name):
+    """SZ3-LR results through the container: the flags travel as a bitmap section, from_bytes takes the
+    LR decompressor, the output equals the direct LR decompression bit for bit."""
+    s = sz()
+    from synth import config_by_name, make_field
+    cfg = config_by_name(name)
+    x = make_field(cfg, device="cuda")
+    res = s.lr_compress(x, cfg.eb, cfg.eb_mode, cfg.radius)
+    assert int(res.lr_flags.sum()) > 0
+    direct = s.decompress(res)
+    b = s.to_bytes(res, eb=cfg.eb, eb_mode=cfg.eb_mode)
+    back = s.from_bytes(b)
+    assert torch.equal(back.view(torch.uint8), direct.view(torch.uint8))
+    err = (back.double() - x.double()).abs().max().item()
+    assert err <= res.eb_abs
