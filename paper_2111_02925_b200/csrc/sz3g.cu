@@ -382,7 +382,7 @@ struct CompressSmem {
   static constexpr size_t off_slot = off_slab + (size_t)NG * Q * slab_bytes;
   static constexpr size_t off_hist = off_slot + S * sizeof(CoefSlot);
   static constexpr size_t off_bar = off_hist + sizeof(uint32_t) * (HW + 36);
-  static constexpr size_t off_hdr = off_bar + 3 * S * sizeof(uint64_t);   // producer-written tile headers
+  static constexpr size_t off_hdr = (off_bar + 3 * S * sizeof(uint64_t) + 15) / 16 * 16;   // producer-written tile headers
   static constexpr size_t off_k = off_hdr + S * sizeof(uint4);
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
   static_assert(off_hdr % 16 == 0, "stage headers are read as uint4");
