@@ -724,30 +724,40 @@ __device__ __forceinline__ void lr_half_compute(const T* __restrict__ xs, uint16
       for (int ii = 0; ii < NP; ii++) xv[ii] = (P0 + ii >= 0) ? xs[(P0 + ii) * (BS * TK) + j * TK + L.kcol + kk] : T(0);
       bool need = false;
       if (F32) {
+        // packed fp32x2 over pairs of planes (FFMA2 / FADD2: each lane the IEEE result of the scalar op)
         const float base32 = __fmaf_rn(F.a2, fj, __fmaf_rn(F.a3, (float)(3 * h + kk), F.a0));
+        const uint64_t inv2 = pack2(inv2eb32, inv2eb32), M2 = pack2(M32, M32);
 #pragma unroll
-        for (int ii = 0; ii < NP; ii++) {
+        for (int ii = 0; ii < NP; ii += 2) {
           const int i = P0 + ii;
-          const bool valid = i >= 0 && (FULL || (cv && i < L.m0));
-          const float x32 = (float)xv[ii];
-          if (i >= I0) {
-            const float P = i == 0 ? base32 : __fmaf_rn(F.a1, (float)i, base32);
-            const float t32 = __fmaf_rn(x32, inv2eb32, -P);
-            const float r = __fsub_rn(__fadd_rn(t32, M32), M32);
-            const float e = __fsub_rn(t32, r);
-            const bool ok = __fmaf_rn(F.k1, fabsf(t32), fabsf(e)) <= F.thr && fabsf(r) < Rf;
-            cr[kk][ii] = ok ? (uint32_t)((int)r + iR) : 0u;
-            need |= valid && !ok;
-          } else {
-            cr[kk][ii] = R;
+          const uint64_t x2 = pack2((float)xv[ii], (float)xv[ii + 1]);
+          // regression: P = fma(a1, i, base) (exactly base at i = 0 for a finite a1), t = fma(x, inv, -P)
+          const uint64_t nP = fma2(pack2(-F.a1, -F.a1), pack2((float)i, (float)(i + 1)), pack2(-base32, -base32));
+          const uint64_t t2 = fma2(x2, inv2, nP);
+          const uint64_t r2 = sub2(add2(t2, M2), M2);
+          const uint64_t e2 = sub2(t2, r2);
+          // Lorenzo prequantisation: t = x * inv (fma with a -0 addend rounds once, like the product)
+          const uint64_t tL2 = fma2(x2, inv2, pack2(-0.0f, -0.0f));
+          const uint64_t rL2 = sub2(add2(tL2, M2), M2);
+          const uint64_t eL2 = sub2(tL2, rL2);
+#pragma unroll
+          for (int hh = 0; hh < 2; hh++) {
+            const int ip = i + hh;
+            const bool valid = ip >= 0 && (FULL || (cv && ip < L.m0));
+            if (ip >= I0) {
+              const float t32 = lane_of(t2, hh), r = lane_of(r2, hh), e = lane_of(e2, hh);
+              const bool ok = __fmaf_rn(F.k1, fabsf(t32), fabsf(e)) <= F.thr && fabsf(r) < Rf;
+              cr[kk][ii + hh] = ok ? (uint32_t)((int)r + iR) : 0u;
+              need |= valid && !ok;
+            } else {
+              cr[kk][ii + hh] = R;
+            }
+            const float tL = lane_of(tL2, hh), rL = lane_of(rL2, hh), eL = lane_of(eL2, hh);
+            const bool okL = __fmaf_rn(F0.k1, fabsf(tL), fabsf(eL)) <= F0.thr && fabsf(tL) < 4194304.0f;
+            q[kk][ii + hh] = okL ? (int32_t)rL : 0;
+            lv[kk][ii + hh] = okL;
+            need |= valid && !okL;
           }
-          const float tL = __fmul_rn(x32, inv2eb32);
-          const float rL = __fsub_rn(__fadd_rn(tL, M32), M32);
-          const float eL = __fsub_rn(tL, rL);
-          const bool okL = __fmaf_rn(F0.k1, fabsf(tL), fabsf(eL)) <= F0.thr && fabsf(tL) < 4194304.0f;
-          q[kk][ii] = okL ? (int32_t)rL : 0;
-          lv[kk][ii] = okL;
-          need |= valid && !okL;
         }
       } else {
         const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0]));
