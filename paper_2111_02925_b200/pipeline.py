@@ -36,19 +36,26 @@ class HostResult:
     outlier_idx: torch.Tensor
     outlier_val: torch.Tensor
     eb_abs: float
+    lr_flags: torch.Tensor | None = None   # SZ3-LR: uint8 [NB] predictor flags (1 = Lorenzo)
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (
             self.payload, self.offsets, self.coef_payload, self.coef_offsets, self.coef_escapes,
             self.outlier_idx, self.outlier_val)) + 4 + 3 * int((self.code_lengths > 0).sum()) + \
-            4 + 3 * int((self.coef_lengths > 0).sum())
+            4 + 3 * int((self.coef_lengths > 0).sum()) + \
+            ((self.lr_flags.numel() + 7) // 8 if self.lr_flags is not None else 0)   # flags as a bitmap
 
 
 class PipelinedCodec:
     def __init__(self, shape, dtype: torch.dtype, eb: float, eb_mode: str = "rel", radius: int = 32768,
-                 device=None, outlier_cap: int | None = None, dim0_offset: int = 0):
+                 device=None, outlier_cap: int | None = None, dim0_offset: int = 0, predictor: str = "regression"):
         """shape / dim0_offset: this rank's block-aligned slab when the field is sharded
-        (torch.distributed initialised): the range and the histogram are then all-reduced."""
+        (torch.distributed initialised): the range and the histogram are then all-reduced.
+        predictor: "regression" (the block regression predictor) or "lr" (SZ3-LR: per block the better of
+        regression and the prequantised Lorenzo predictor)."""
+        if predictor not in ("regression", "lr"):
+            raise ValueError(f"unknown predictor {predictor!r}")
+        self.predictor = predictor
         self.shape, self.dtype, self.eb, self.eb_mode, self.radius = tuple(shape), dtype, eb, eb_mode, radius
         self.dim0_offset = dim0_offset
         dev = device or torch.device("cuda", torch.cuda.current_device())
@@ -63,6 +70,8 @@ class PipelinedCodec:
         self.bufs = [sz3g.CompressBuffers(self.shape, dtype, radius, outlier_cap, dev) for _ in range(2)]
         for b in self.bufs:
             b.beta_buffer()
+            if predictor == "lr":
+                b.flags_buffer()
         nch = -(-n // sz3g.HUFF_CHUNK)
         cap = -(-n * sz3g.HUFF_MAX_LEN // 32) + nch
         self.payload = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(2)]
@@ -91,6 +100,7 @@ class PipelinedCodec:
             torch.empty(max(1, nb), dtype=torch.int64, pin_memory=True),                       # escapes
             torch.empty(ocap, dtype=torch.int64, pin_memory=True),                             # outlier idx
             torch.empty(ocap, dtype=dtype, pin_memory=True),                                   # outlier val
+            torch.empty(max(1, nb), dtype=torch.uint8, pin_memory=True),                       # LR flags
         ]
 
     # ------------------------------------------------------------------ stages
@@ -110,18 +120,26 @@ class PipelinedCodec:
             bufs.reset()
             sz3g.regression_analyze(x, bufs.minmax, bufs.beta, stream=st)
             pdist.allreduce_range_(bufs.minmax)    # sharded: the global range (no-op on one rank)
-            sz3g.regression_quantize(x, self.eb, self.eb_mode, self.radius, bufs.minmax, bufs.beta, bufs=bufs,
-                                     reset=False, dim0_offset=self.dim0_offset, stream=st)
+            quantize = sz3g.lr_quantize if self.predictor == "lr" else sz3g.regression_quantize
+            quantize(x, self.eb, self.eb_mode, self.radius, bufs.minmax, bufs.beta, bufs=bufs, reset=False,
+                     dim0_offset=self.dim0_offset, stream=st)
             pdist.allreduce_hist_(bufs.hist)       # sharded: one codebook for every slab
             table = sz3g.huffman_codebook(bufs.hist, stream=st)
             hs = sz3g.huffman_encode(bufs.codes.view(-1), table, payload=self.payload[b], offsets=self.offsets[b],
                                      scratch=self.enc_scratch, stream=st)
             coef = sz3g.encode_coefficients(bufs.coef_codes, stream=st, sync=False)
-            sz3g.regression_decompress(bufs.codes, bufs.coef_codes, bufs.outlier_idx, bufs.outlier_val,
-                                       bufs.outlier_idx.numel(), self.eb, self.radius, self.dtype,
-                                       dim0_offset=self.dim0_offset, out=self.out[b],
-                                       d_outlier_count=bufs.outlier_count, eb_mode=self.eb_mode,
-                                       d_minmax=bufs.minmax, stream=st)
+            if self.predictor == "lr":
+                sz3g.lr_decompress(bufs.codes, bufs.coef_codes, bufs.lr_flags, bufs.outlier_idx, bufs.outlier_val,
+                                   bufs.outlier_idx.numel(), self.eb, self.radius, self.dtype,
+                                   dim0_offset=self.dim0_offset, out=self.out[b],
+                                   d_outlier_count=bufs.outlier_count, eb_mode=self.eb_mode,
+                                   d_minmax=bufs.minmax, stream=st)
+            else:
+                sz3g.regression_decompress(bufs.codes, bufs.coef_codes, bufs.outlier_idx, bufs.outlier_val,
+                                           bufs.outlier_idx.numel(), self.eb, self.radius, self.dtype,
+                                           dim0_offset=self.dim0_offset, out=self.out[b],
+                                           d_outlier_count=bufs.outlier_count, eb_mode=self.eb_mode,
+                                           d_minmax=bufs.minmax, stream=st)
             # the sizes the copy-out needs, gathered on this stream into pinned host memory: no
             # operation on the legacy default stream (it would wait for every other stream's work)
             sizes = torch.stack([bufs.status.to(torch.int64)[0], bufs.outlier_count[0],
@@ -153,15 +171,17 @@ class PipelinedCodec:
             self.h_offsets.copy_(self.offsets[b], non_blocking=True)
             host_out.copy_(self.out[b], non_blocking=True)
             small = []
-            for h, t in zip(self.h_small, (table.lengths, coef.stream.payload[:cw], coef.stream.offsets,
-                                           coef.table.lengths, coef.escapes[:nesc], bufs.outlier_idx[:n_out],
-                                           bufs.outlier_val[:n_out])):
+            srcs = [table.lengths, coef.stream.payload[:cw], coef.stream.offsets, coef.table.lengths,
+                    coef.escapes[:nesc], bufs.outlier_idx[:n_out], bufs.outlier_val[:n_out]]
+            if self.predictor == "lr":
+                srcs.append(bufs.lr_flags)
+            for h, t in zip(self.h_small, srcs):
                 hv = h[:t.numel()]
                 hv.copy_(t, non_blocking=True)
                 small.append(hv)
             self.ev_out[b].record(self.s_out)
         return HostResult(hp, self.h_offsets, small[0], small[1], small[2], small[3], small[4], small[5], small[6],
-                          eb_abs)
+                          eb_abs, small[7] if self.predictor == "lr" else None)
 
     # ------------------------------------------------------------------ driver
     def run(self, host_fields, host_out: torch.Tensor, on_result=None) -> list:

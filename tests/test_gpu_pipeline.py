@@ -40,3 +40,24 @@ def test_pipeline_matches_direct():
         cs = sz3g.encode_coefficients(res.coef_codes)
         assert torch.equal(cpay, cs.stream.payload[:cs.stream.words()].cpu())
         assert torch.equal(cesc, cs.escapes.cpu()) and torch.equal(clen, cs.table.lengths.cpu())
+
+
+def test_pipeline_lr_matches_direct():
+    """predictor="lr": every field's reconstruction equals decompress(lr_compress(x)) bit for bit, and the
+    flags reach the host."""
+    from paper_2111_02925_b200 import sz3g
+    from paper_2111_02925_b200.pipeline import PipelinedCodec
+    from synth import config_by_name, make_field
+    cfg = config_by_name("c2")
+    fields = [make_field(cfg, device="cuda", shape=(48, 96, 120)) * (1.0 + 0.5 * k) for k in range(3)]
+    hosts = [f.cpu().pin_memory() for f in fields]
+    h_out = torch.empty_like(hosts[0]).pin_memory()
+    codec = PipelinedCodec(tuple(fields[0].shape), fields[0].dtype, cfg.eb, cfg.eb_mode, cfg.radius, predictor="lr")
+    got = {}
+    codec.run(hosts, h_out, on_result=lambda k, r: got.__setitem__(k, (h_out.clone(), r.lr_flags.clone())))
+    for k, x in enumerate(fields):
+        res = sz3g.lr_compress(x, cfg.eb, cfg.eb_mode, cfg.radius)
+        direct = sz3g.decompress(res).cpu()
+        xo, fl = got[k]
+        assert torch.equal(xo.view(torch.int32), direct.view(torch.int32))
+        assert torch.equal(fl, res.lr_flags.cpu()) and int(fl.sum()) > 0
