@@ -146,3 +146,37 @@ def test_lr_large_q_tiles(dtype, flags):
     x[i < 6] -= 1e9          # first block row small: the fast routine, the rest large
     rep = check_lr(x.astype(dtype), 1.0, "abs", 32768, flags)
     assert rep["lorenzo_blocks"] > 0
+
+
+def test_lr_slab_invariance():
+    """Block-aligned slabs (dim0_offset, the global range) reproduce the whole-field SZ3-LR output: codes,
+    flags, coefficient codes, histogram, and outliers with global indices; each slab decompresses to the
+    matching planes of the whole field's reconstruction."""
+    s = sz()
+    from synth import make_field
+    x = make_field("c2", device="cuda", shape=(48, 64, 96))
+    x.view(-1)[12345] = float("inf")      # an outlier in the second slab (global index)
+    x.view(-1)[250000] = 1e30
+    whole = s.lr_compress(x, 1e-4, "abs", 4096, outlier_cap=x.numel())
+    wcodes, wflags, wcoef, whist = (whole.codes.clone(), whole.lr_flags.clone(), whole.coef_codes.clone(),
+                                    whole.hist.clone())
+    widx = set(whole.outlier_idx[:whole.n_outliers].cpu().tolist())
+    xw = s.decompress(whole).clone()
+    codes, flags, coef, idx, hist = [], [], [], set(), torch.zeros_like(whist)
+    for a, b in [(0, 12), (12, 30), (30, 48)]:
+        xs = x[a:b].contiguous()
+        mm, beta = s.regression_analyze(xs)
+        part = s.lr_quantize(xs, 1e-4, "abs", 4096, mm, beta, outlier_cap=xs.numel(), dim0_offset=a)
+        part.finalize()
+        codes.append(part.codes.clone())
+        flags.append(part.lr_flags.clone())
+        coef.append(part.coef_codes.clone())
+        idx |= set(part.outlier_idx[:part.n_outliers].cpu().tolist())
+        hist += part.hist
+        xo = s.lr_decompress(part.codes, part.coef_codes, part.lr_flags, part.outlier_idx, part.outlier_val,
+                             part.n_outliers, part.eb_abs, 4096, xs.dtype, dim0_offset=a)
+        assert torch.equal(xo.view(torch.int32), xw[a:b].view(torch.int32))
+    assert torch.equal(torch.cat(codes), wcodes)
+    assert torch.equal(torch.cat(flags), wflags) and torch.equal(torch.cat(coef), wcoef)
+    assert torch.equal(hist, whist)
+    assert idx == widx and len(widx) >= 2
