@@ -195,3 +195,13 @@ def test_full_chunk_path_flags_missing_codeword():
         hs = s.huffman_encode(torch.from_numpy(qb).cuda(), t)
         torch.cuda.synchronize()
         assert int(hs.status.item()) & s.STATUS_BAD_HUFFMAN
+
+
+@pytest.mark.parametrize("n", [2047, 2048, 2049, 4096, 2048 * 33, 2048 * 33 + 1])
+def test_full_chunk_boundaries(n):
+    """Sizes at and around multiples of the 2048-code chunk: only full chunks (fast kernels alone), one
+    ragged tail (fast + generic), no full chunk (generic alone) -- against the oracle's stream."""
+    rng = np.random.default_rng(n)
+    R = 512
+    q = np.clip(np.round(rng.standard_normal(n) * 20) + R, 1, 2 * R - 1).astype(np.uint16)
+    round_trip(q, np.bincount(q, minlength=2 * R))
