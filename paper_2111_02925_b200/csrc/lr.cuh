@@ -516,8 +516,12 @@ size_t lr_plain_smem() { return (size_t)LR_PW * 2 * TILE_ELEMS * sizeof(uint16_t
 // q = r + q(i-1,j,k) + q(i,j-1,k) - q(i-1,j-1,k).  The block's right lane takes the left lane's last r
 // by a shuffle: both lanes first run their columns from r = 0, then the right lane adds the left lane's
 // final r to its columns before its first outlier.  Outliers are not written (the scatter did that).
-template <typename T, bool FULL, bool IN_SMEM>
-__device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
+// QT: the recurrence's integer type.  Without an outlier a Lorenzo block's q are prefix sums of residuals
+// |delta| < R, so |q| <= 216 R < 2^23 and int32 is exact (a value with a large q is an outlier at the block
+// origin); an outlier brings an arbitrary q (L1 of its stored value): with QT = int32 the routine then
+// reports it and the caller redoes the tile in int64 (the writes are idempotent).
+template <typename T, bool FULL, bool IN_SMEM, typename QT = int64_t>
+__device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
                                                    const int32_t* __restrict__ coef,
                                                    const uint8_t* __restrict__ flags, T* __restrict__ xo,
                                                    const TileCoord tc, const Geo& g, const Consts& K, uint32_t R) {
@@ -537,11 +541,12 @@ __device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ 
   const uint64_t gbase = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK + L.kcol;
   // P[j] = q of row j of the previous plane; C = q of the previous row of this plane.  Row j needs
   // P[j] and P[j - 1]; once it is done P[j - 1] is free and takes this plane's row j - 1.
-  int64_t P[BS][3];
+  QT P[BS][3];
+  bool wide = false;
 #pragma unroll
   for (int j = 0; j < BS; j++) P[j][0] = P[j][1] = P[j][2] = 0;
   for (int i = 0; i < BS; i++) {
-    int64_t C[3] = {0, 0, 0};
+    QT C[3] = {0, 0, 0};
 #pragma unroll
     for (int j = 0; j < BS; j++) {
       uint32_t c[3];
@@ -564,9 +569,9 @@ __device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ 
       }
       // Lorenzo recurrence, run by every lane (the shuffle needs the whole warp; regression lanes compute
       // throw-away values)
-      int64_t r[3], base[3];
+      QT r[3], base[3];
       bool nocarry[3];
-      int64_t run = 0;
+      QT run = 0;
       bool cut = false;   // from an outlier on, r no longer depends on the left lane
 #pragma unroll
       for (int kk = 0; kk < 3; kk++) {
@@ -574,17 +579,18 @@ __device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ 
         if (lor && valid[kk] && c[kk] == 0) {
           bool ok;
           const double qd = lr_prequant(to_d<T>(xo[e0 + kk]), K, ok);
-          run = (int64_t)__double2ll_rn(qd) - base[kk];
+          run = (QT)__double2ll_rn(qd) - base[kk];
           cut = true;
+          if (sizeof(QT) < 8) wide = true;
         } else {
-          run += valid[kk] ? (int64_t)c[kk] - (int64_t)R : 0;
+          run += valid[kk] ? (QT)c[kk] - (QT)R : (QT)0;
         }
         r[kk] = run;
         nocarry[kk] = cut;
       }
-      int64_t carry = __shfl_up_sync(0xffffffffu, r[2], 1);
+      QT carry = __shfl_up_sync(0xffffffffu, r[2], 1);
       if (h == 0) carry = 0;
-      int64_t q[3];
+      QT q[3];
 #pragma unroll
       for (int kk = 0; kk < 3; kk++) {
         q[kk] = valid[kk] ? (nocarry[kk] ? r[kk] : r[kk] + carry) + base[kk] : 0;
@@ -599,6 +605,7 @@ __device__ __forceinline__ void lr_decompress_tile(const uint16_t* __restrict__ 
 #pragma unroll
     for (int kk = 0; kk < 3; kk++) P[BS - 1][kk] = C[kk];
   }
+  return wide;
 }
 
 constexpr int LR_DW = 4;   // decompress: warps per CTA
@@ -668,8 +675,12 @@ __global__ void __launch_bounds__(W * 32, 1)
     const TileCoord tc = decode_tile(t, g);
     ptx::mbar_wait(&bar[s], ph);
     const uint16_t* cs = ring + (size_t)s * TILE_ELEMS;
-    if (tile_full(tc, g)) lr_decompress_tile<T, true, true>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R);
-    else lr_decompress_tile<T, false, true>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R);
+    if (tile_full(tc, g)) {
+      if (__any_sync(0xffffffffu, lr_decompress_tile<T, true, true, int32_t>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R)))
+        lr_decompress_tile<T, true, true, int64_t>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R);
+    } else {
+      lr_decompress_tile<T, false, true, int64_t>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R);
+    }
     __syncwarp();
     if (lane == 0) {
       const uint64_t t2 = tl.tile();
