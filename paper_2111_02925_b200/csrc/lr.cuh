@@ -520,6 +520,16 @@ size_t lr_plain_smem() { return (size_t)LR_PW * 2 * TILE_ELEMS * sizeof(uint16_t
 // |delta| < R, so |q| <= 216 R < 2^23 and int32 is exact (a value with a large q is an outlier at the block
 // origin); an outlier brings an arbitrary q (L1 of its stored value): with QT = int32 the routine then
 // reports it and the caller redoes the tile in int64 (the writes are idempotent).
+#ifndef SZ3G_LRD_JU
+#define SZ3G_LRD_JU 1
+#endif
+constexpr int LRD_JU = SZ3G_LRD_JU;   // unroll of the regression phase's row loop (A/B tuning)
+#ifndef SZ3G_LRD_COAL
+#define SZ3G_LRD_COAL 1
+#endif
+#ifndef SZ3G_LRD_SPLIT
+#define SZ3G_LRD_SPLIT 1
+#endif
 template <typename T, bool FULL, bool IN_SMEM, typename QT = int64_t>
 __device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
                                                    const int32_t* __restrict__ coef,
@@ -539,6 +549,68 @@ __device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ 
   decode_coefs(cc, K, bh);
   const double cR = __dadd_rn(I2D_MAGIC, (double)R);
   const uint64_t gbase = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK + L.kcol;
+#if SZ3G_LRD_SPLIT
+  // Regression blocks first (O12), row by row with the six planes' chains independent; the Lorenzo
+  // recurrence below then runs only in tiles that hold a Lorenzo block.  A full tile is walked with the
+  // lanes across the row (columns lane, lane + 32, lane + 64, each with its own block's coefficients), so
+  // every store instruction writes 128 contiguous bytes.
+  if (FULL && IN_SMEM && SZ3G_LRD_COAL) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t brow = ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + (uint64_t)tc.c * 16u;
+    double b1[3], b2[3], bk[3];
+    bool reg[3];
+#pragma unroll
+    for (int m = 0; m < 3; m++) {
+      const int k = lane + 32 * m;
+      const int4 c4 = __ldg(reinterpret_cast<const int4*>(coef) + brow + k / BS);
+      reg[m] = __ldg(flags + brow + k / BS) == 0;
+      double bb[4];
+      decode_coefs(c4, K, bb);
+      b1[m] = bb[1];
+      b2[m] = bb[2];
+      bk[m] = __fma_rn(bb[3], (double)(k % BS), bb[0]);
+    }
+    const uint64_t rbase = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK + lane;
+#pragma unroll LRD_JU
+    for (int j = 0; j < BS; j++) {
+#pragma unroll
+      for (int m = 0; m < 3; m++) {
+        const double base = __fma_rn(b2[m], (double)j, bk[m]);
+        uint32_t c[BS];
+#pragma unroll
+        for (int i = 0; i < BS; i++) c[i] = cs[(i * BS + j) * TK + lane + 32 * m];
+#pragma unroll
+        for (int i = 0; i < BS; i++) {
+          if (!reg[m] || c[i] == 0) continue;
+          const double p = __fma_rn(b1[m], (double)i, base);
+          const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)c[i]), cR);
+          xo[rbase + ((uint64_t)i * g.n1 + j) * g.n2 + 32 * m] = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, qd)));
+        }
+      }
+    }
+  } else if (!lor) {
+#pragma unroll LRD_JU
+    for (int j = 0; j < BS; j++) {
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const bool cv = FULL || (j < L.m1 && L.kv(kk));
+        const double base = __fma_rn(bh[2], (double)j, __fma_rn(bh[3], (double)(3 * h + kk), bh[0]));
+        const uint16_t* ccol = cs + (uint64_t)j * cj + L.kcol + kk;
+        uint32_t c[BS];
+#pragma unroll
+        for (int i = 0; i < BS; i++) c[i] = (FULL || (cv && i < L.m0)) ? (uint32_t)ccol[(uint64_t)i * ci] : 0u;
+#pragma unroll
+        for (int i = 0; i < BS; i++) {
+          if (c[i] == 0) continue;
+          const double p = __fma_rn(bh[1], (double)i, base);
+          const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)c[i]), cR);
+          xo[gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk] = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, qd)));
+        }
+      }
+    }
+  }
+  if (!__any_sync(0xffffffffu, lor)) return false;
+#endif
   // P[j] = q of row j of the previous plane; C = q of the previous row of this plane.  Row j needs
   // P[j] and P[j - 1]; once it is done P[j - 1] is free and takes this plane's row j - 1.
   QT P[BS][3];
@@ -558,7 +630,7 @@ __device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ 
         valid[kk] = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
         c[kk] = valid[kk] ? (uint32_t)crow[kk] : R;
       }
-      if (!lor) {   // regression block (O12)
+      if (!SZ3G_LRD_SPLIT && !lor) {   // regression block (O12)
 #pragma unroll
         for (int kk = 0; kk < 3; kk++) {
           if (!valid[kk] || c[kk] == 0) continue;

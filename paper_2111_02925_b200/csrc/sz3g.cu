@@ -1234,7 +1234,10 @@ int launch_lr_tma(const Geo& g, const void* x, const KArgs& ka, const CompressOu
 #ifndef SZ3G_LRD_W
 #define SZ3G_LRD_W 4
 #endif
-constexpr int LDW = SZ3G_LRD_W, LDD = 2;   // LR decompress: self-fed warps x code-tile stages
+#ifndef SZ3G_LRD_D
+#define SZ3G_LRD_D 2
+#endif
+constexpr int LDW = SZ3G_LRD_W, LDD = SZ3G_LRD_D;   // LR decompress: self-fed warps x code-tile stages
 
 template <typename T, int W, int D>
 int launch_lr_dec_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, const uint8_t* flags, void* xo,
