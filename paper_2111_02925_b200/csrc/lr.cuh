@@ -710,8 +710,11 @@ struct LrDecSmem {
   static constexpr size_t total = off_k + sizeof(Consts) + 16;
 };
 
+#ifndef SZ3G_LRD_MINB
+#define SZ3G_LRD_MINB 4   // 128 registers: 4 CTAs (16 warps) per SM (A/B: 1 -> 7.57 ms, 4 -> 6.61 ms on c5)
+#endif
 template <typename T, int W, int D>
-__global__ void __launch_bounds__(W * 32, 1)
+__global__ void __launch_bounds__(W * 32, SZ3G_LRD_MINB)
     k_lr_decompress_tma(const __grid_constant__ CUtensorMap tm_c, const int32_t* __restrict__ coef,
                         const uint8_t* __restrict__ flags, T* __restrict__ xo, KArgs a) {
   using L_ = LrDecSmem<W, D>;
@@ -911,11 +914,13 @@ __device__ __forceinline__ void lr_half_compute(const T* __restrict__ xs, uint16
         Eprev = E;
         if (i < I0) continue;   // the helper plane
         const bool valid = FULL || (cv && i < L.m0);
-        uint32_t cl = (lv[kk][ii] && delta > -iR && delta < iR) ? (uint32_t)(delta + iR) : 0u;
+        // |delta| < R <=> delta + R - 1 in [0, 2R - 1) (|delta| < 2^25: no wrap)
+        uint32_t cl = (lv[kk][ii] && (uint32_t)(delta + iR - 1) < 2u * R - 1u) ? (uint32_t)(delta + iR) : 0u;
         if (!valid) cl = R;
         const uint32_t c = cr[kk][ii];
-        costR += c ? (uint32_t)abs((int)c - iR) : R;
-        costL += cl ? (uint32_t)abs((int)cl - iR) : R;
+        // an outlier (code 0) costs R = |0 - R|
+        costR += (uint32_t)abs((int)c - iR);
+        costL += (uint32_t)abs((int)cl - iR);
         const uint32_t sidx = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
         sR[sidx] = (uint16_t)c;
         sL[sidx] = (uint16_t)cl;
