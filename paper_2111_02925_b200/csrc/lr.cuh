@@ -1032,6 +1032,20 @@ __device__ __forceinline__ void lr_pair_tile(const T* __restrict__ xs, uint16_t*
   const uint32_t sink = (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * lane;
   const bool hist = o.hist != nullptr;
   bool has_out = false;
+  if (__any_sync(0xffffffffu, useL)) {   // the Lorenzo blocks' codes into the stored slab
+    if (useL) {
+#pragma unroll 1
+      for (int i = i0; i < i0 + 3; i++)
+#pragma unroll
+        for (int j = 0; j < BS; j++)
+#pragma unroll
+          for (int kk = 0; kk < 3; kk++) {
+            const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
+            sR[s] = sL[s];
+          }
+    }
+    __syncwarp();
+  }
 #pragma unroll 1
   for (int i = i0; i < i0 + 3; i++)
 #pragma unroll
@@ -1040,11 +1054,7 @@ __device__ __forceinline__ void lr_pair_tile(const T* __restrict__ xs, uint16_t*
       for (int kk = 0; kk < 3; kk++) {
         const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
         const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
-        uint32_t code = sR[s];
-        if (useL) {
-          code = sL[s];
-          sR[s] = (uint16_t)code;
-        }
+        const uint32_t code = sR[s];
         const bool inwin = valid && code != 0u && code - hs.lo < hs.nwin;
         if (hist) {
           red_smem_add(inwin ? hb + 4u * code : sink, 1u);
