@@ -988,6 +988,43 @@ struct LrPairSmem {
 
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
+// Histogram of a half's codes (planes [i0, i0 + 3)); returns whether the lane holds an outlier.  The window
+// starts at lo >= 1, so code 0 is never in it; codes outside the window (and the outliers) are rare and
+// handled in a second walk, keeping the hot loop free of branches.
+template <bool HIST, bool FULL>
+__device__ __forceinline__ bool lr_pair_hist(const uint16_t* sR, int i0, const LaneGeom& L, const HistSmem& hs,
+                                             unsigned long long* ghist, uint32_t hb, uint32_t sink) {
+  bool rare = false;
+#pragma unroll 1
+  for (int i = i0; i < i0 + 3; i++)
+#pragma unroll
+    for (int j = 0; j < BS; j++)
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
+        const uint32_t code = sR[i * (BS * TK) + j * TK + L.kcol + kk];
+        if (HIST) {
+          const bool inwin = valid && code - hs.lo < hs.nwin;
+          red_smem_add(inwin ? hb + 4u * code : sink, 1u);
+          rare |= valid && !inwin;
+        } else {
+          rare |= valid && code == 0u;
+        }
+      }
+  if (!HIST || !rare) return rare;
+  bool has_out = false;
+  for (int i = i0; i < i0 + 3; i++)
+    for (int j = 0; j < BS; j++)
+      for (int kk = 0; kk < 3; kk++) {
+        const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
+        const uint32_t code = sR[i * (BS * TK) + j * TK + L.kcol + kk];
+        if (!valid) continue;
+        if (code == 0u) has_out = true;
+        else if (code - hs.lo >= hs.nwin) atomicAdd(&ghist[code], 1ull);
+      }
+  return has_out;
+}
+
 template <typename T, bool FULL>
 __device__ __forceinline__ void lr_pair_tile(const T* __restrict__ xs, uint16_t* sR, uint16_t* sL, uint2* s_cost,
                                              int* s_big, int hw, int bar_id, const TileCoord tc, const Geo& g,
@@ -1046,22 +1083,8 @@ __device__ __forceinline__ void lr_pair_tile(const T* __restrict__ xs, uint16_t*
     }
     __syncwarp();
   }
-#pragma unroll 1
-  for (int i = i0; i < i0 + 3; i++)
-#pragma unroll
-    for (int j = 0; j < BS; j++)
-#pragma unroll
-      for (int kk = 0; kk < 3; kk++) {
-        const bool valid = FULL || (i < L.m0 && j < L.m1 && L.kv(kk));
-        const uint32_t s = (uint32_t)(i * (BS * TK) + j * TK + L.kcol + kk);
-        const uint32_t code = sR[s];
-        const bool inwin = valid && code != 0u && code - hs.lo < hs.nwin;
-        if (hist) {
-          red_smem_add(inwin ? hb + 4u * code : sink, 1u);
-          if (valid && code != 0u && !inwin) atomicAdd(&o.hist[code], 1ull);
-        }
-        has_out |= valid && code == 0u;
-      }
+  if (hist) has_out = lr_pair_hist<true, FULL>(sR, i0, L, hs, o.hist, hb, sink);
+  else has_out = lr_pair_hist<false, FULL>(sR, i0, L, hs, o.hist, hb, sink);
   __syncwarp();
   if (hist) lr_rare_planes<T, true>(xs, sR, i0, L, has_out, tc, g, o, hs);
   else lr_rare_planes<T, false>(xs, sR, i0, L, has_out, tc, g, o, hs);
