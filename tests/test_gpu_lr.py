@@ -180,3 +180,24 @@ def test_lr_slab_invariance():
     assert torch.equal(torch.cat(flags), wflags) and torch.equal(torch.cat(coef), wcoef)
     assert torch.equal(hist, whist)
     assert idx == widx and len(widx) >= 2
+
+
+@pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
+@pytest.mark.parametrize("R", [32768, 3000])
+def test_lr_codes_outside_histogram_window(R, flags):
+    """Residuals spread over thousands of bins: many codes fall outside the kernels' 4096-bin shared
+    histogram window (global atomics in the second walk), with a curved region where Lorenzo wins; at
+    R = 3000 the wide residuals are also radius outliers."""
+    rng = np.random.default_rng(11)
+    shape = (18, 24, 200)
+    i, j, k = np.meshgrid(*(np.arange(n, dtype=np.float64) for n in shape), indexing="ij")
+    eb = 1e-3
+    noisy = rng.uniform(-1.0, 1.0, shape) * 6000 * 2 * eb
+    curved = 40.0 * np.sin(i / 2.0) * np.cos(k / 3.0) + 0.5 * j * j
+    x = np.where(j < 12, noisy, curved).astype(np.float32)
+    rep = check_lr(x, eb, "abs", R, flags)
+    assert 0 < rep["lorenzo_blocks"] < rep["blocks"]
+    res = sz().lr_compress(torch.from_numpy(x).cuda(), eb, "abs", R, outlier_cap=x.size, flags=flags)
+    codes = res.codes.cpu().numpy().astype(np.int64)
+    inside = (codes >= R - 2048) & (codes < R + 2048)
+    assert (codes != 0).sum() > 0 and (~inside & (codes != 0)).sum() > 1000
