@@ -649,11 +649,15 @@ __device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ 
       for (int kk = 0; kk < 3; kk++) {
         base[kk] = P[j][kk] + C[kk] - (j > 0 ? P[j - 1][kk] : 0);
         if (lor && valid[kk] && c[kk] == 0) {
-          bool ok;
-          const double qd = lr_prequant(to_d<T>(xo[e0 + kk]), K, ok);
-          run = (QT)__double2ll_rn(qd) - base[kk];
+          if (sizeof(QT) < 8) {   // the int64 redo recomputes the tile: no need for this q here
+            wide = true;
+            run = 0;
+          } else {
+            bool ok;
+            const double qd = lr_prequant(to_d<T>(xo[e0 + kk]), K, ok);
+            run = (QT)__double2ll_rn(qd) - base[kk];
+          }
           cut = true;
-          if (sizeof(QT) < 8) wide = true;
         } else {
           run += valid[kk] ? (QT)c[kk] - (QT)R : (QT)0;
         }
