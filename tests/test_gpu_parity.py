@@ -162,51 +162,6 @@ def test_config_plain_path(name):
     check(xh, cfg.eb, cfg.eb_mode, cfg.radius, GEN)
 
 
-@pytest.mark.slow
-def test_c5_full_size_sampled_slabs():
-    """Config 5 (16 GiB) on the GPU in the bench's launch configuration; the oracle recomputes three
-    block-aligned slabs (with the global value range) and every property that holds at any size is
-    checked on the full output."""
-    from synth import config_by_name, make_field
-    cfg = config_by_name("c5")
-    s = sz()
-    x = make_field(cfg, device="cuda")
-    res = s.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, coef_raw=False)
-    res.finalize()
-    mm = res.eb_abs
-    lo, hi = (float(v) for v in s.value_range(x).cpu())
-    assert mm == cfg.eb * (hi - lo)
-    n = res.n_outliers
-    N = x.numel()
-    assert int(res.hist.sum()) == N and int(res.hist[0]) == n
-    # decompress and check the bound everywhere, chunked
-    xo = s.decompress(res)
-    for a in range(0, x.shape[0], 64):
-        err = (xo[a:a + 64].double() - x[a:a + 64].double()).abs().max().item()
-        assert err <= res.eb_abs
-    n0, n1, n2 = x.shape
-    NB1, NB2 = math.ceil(n1 / 6), math.ceil(n2 / 6)
-    oidx = res.outlier_idx[:n].cpu().numpy().view(np.uint64)
-    oval = res.outlier_val[:n].cpu().numpy()
-    for a0, rows in [(0, 12), (510, 6), (1020, 4)]:
-        xs = x[a0:a0 + rows].cpu().numpy()
-        orc = oracle.compress(xs, cfg.eb, "rel", radius=cfg.radius, dim0_offset=a0, value_range_override=(lo, hi))
-        assert orc.eb_abs == res.eb_abs
-        b0, b1 = (a0 // 6) * NB1 * NB2, ((a0 + rows + 5) // 6) * NB1 * NB2
-        gc = res.coef_codes[b0:b1].cpu().numpy()
-        ex = orc.block_exempt.astype(bool)
-        assert np.array_equal(gc[~ex], orc.coef_codes[~ex])
-        codes = res.codes[a0:a0 + rows].cpu().numpy()
-        if not ex.any():
-            assert np.array_equal(codes, orc.codes)
-            sel = (oidx >= a0 * n1 * n2) & (oidx < (a0 + rows) * n1 * n2)
-            order = np.argsort(oidx[sel])
-            assert np.array_equal(oidx[sel][order], np.sort(orc.outlier_idx))
-            assert np.array_equal(oval[sel][order], orc.outlier_val[np.argsort(orc.outlier_idx)])
-            xd = xo[a0:a0 + rows].cpu().numpy()
-            assert np.array_equal(xd.view(np.uint8), orc.xprime.view(np.uint8))
-
-
 # ----------------------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("flags", [0, GEN], ids=["tma", "plain"])
 def test_degenerate_extents(flags):
