@@ -5,18 +5,22 @@ Metric (BASELINE.json): regression compress & decompress GB/s per GPU and at N G
 Workload: config c5 -- 1024 x 2048 x 2048 fp32 (16 GiB) k^-3 Gaussian random field (seed 4), eb = 1e-3 x
 value range, R = 32768, 6^3 blocks, sharded as block-aligned slabs over the N GPUs (strong scaling).
 
-One step = the whole hot path over the field.  Default (--path two-pass): analyze = a0 value range + a2-a3
-block coefficients in one read of x (+ MAX all-reduce of the range when N > 1), quantize = a4-a7 from those
-coefficients (+ SUM all-reduce of the histogram when N > 1), a8 decompress + outlier scatter.  --path fused:
-value range, then the single-pass a1-a7 kernel.
+One step = the whole hot path over the field, ``RoundTrip.step`` (paper_2111_02925_b200/roundtrip.py, the
+object tests/test_gpu_c5.py checks against the oracle).  Default (--path two-pass): analyze = a0 value
+range + a2-a3 block coefficients in one read of x (+ MAX all-reduce of the range when N > 1), quantize =
+a4-a7 from those coefficients (+ SUM all-reduce of the histogram when N > 1), a8 decompress + outlier
+scatter.  --path fused: value range, then the single-pass a1-a7 kernel.
 value = input bytes of the whole field / step time (max over ranks), i.e. round-trip GB/s.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sz3g|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+  torchrun --nproc-per-node 2 bench.py --gpus 2 --dist-backend gloo --shape 96,2048,2048 ...
+                                                            (multi-rank rehearsal on ONE GPU, gloo)
 
-Prints ONE JSON line on rank 0.  Inputs (16 GiB) are larger than the 126 MB L2, so no flush is needed
-between steps.  `--impl reference` times the CPU oracle (oracle/, the test checker) on a bounded sample
-of the same workload: the only other place bench.py runs oracle/ is the cpu_baseline leg.
+Prints ONE JSON line on rank 0.  c5's inputs (16 GiB) are larger than the 126 MB L2, so no flush is
+needed between its steps; the per-config legs (`configs`) flush L2 before every step.  `--impl
+reference` times the CPU oracle (oracle/, the test checker) on a bounded sample of the same workload:
+the only other place bench.py runs oracle/ is the cpu_baseline leg.
 """
 from __future__ import annotations
 
@@ -56,6 +60,14 @@ def parse():
     ap.add_argument("--no-lr", action="store_true", help="skip the SZ3-LR (NEXT-4) measurement")
     ap.add_argument("--path", default="two-pass", choices=["two-pass", "fused"],
                     help="REL compression: analyze (range + beta) -> quantize, or value_range -> fused compress")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend at N > 1 (gloo: rehearse the multi-rank path on one GPU)")
+    ap.add_argument("--shape", default=None, help="n0,n1,n2: the config's recipe at another shape (rehearsals)")
+    ap.add_argument("--configs", default="c2,c3,c4,c5r16,c3r4",
+                    help="per-config legs after the main line (N = 1 only): config names, cNrR = config N at "
+                         "radius R (stress variant); '' for none")
+    ap.add_argument("--config-steps", type=int, default=10)
+    ap.add_argument("--no-ties", action="store_true", help="skip the reported-counter pass (sz3g_tie_counts)")
     return ap.parse_args()
 
 
@@ -136,17 +148,21 @@ class ClockSampler:
 
 
 def dist_setup(args):
+    """One process per GPU.  NCCL by default; gloo (CUDA tensors staged through the host) rehearses the
+    same code path with every rank on one GPU (device = LOCAL_RANK mod the visible GPUs)."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    return world, rank, local
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, dev
 
 
 def max_over_ranks(v: float, world: int) -> float:
@@ -159,6 +175,52 @@ def max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(v: int, world: int) -> int:
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())
+
+
+def host_cpu() -> dict:
+    """Host CPU of this box (the cpu_baseline's machine): model name and logical cores."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def entropy_bits(hist) -> float:
+    """Shannon entropy (bits per code) of the merged code histogram (zeroth-order, P:418's Huffman input)."""
+    import numpy as np
+    h = hist.cpu().numpy().astype(np.float64)
+    n = h.sum()
+    p = h[h > 0] / n
+    return float(-(p * np.log2(p)).sum())
+
+
+# The paper's own CPU numbers (BASELINE.md §1): context only -- other hardware, whole pipelines
+PAPER_CONTEXT = {
+    "hardware": "Bebop (ANL): 2x Intel Xeon E5-2695v4 Broadwell, 36 cores/node, 128 GB DDR4 (P:522); "
+                "thread count not stated",
+    "sz3_truncation_compress_gbs": 1.0,
+    "second_best_compress_gbs": 0.25,
+    "sz3_interp_compress_gbs": "> 0.1",
+    "source": "P:891 (SZ3-Truncation 1 GB/s, 4x the second best = SZ2.1 / SZ3-LR-s, both containing the "
+              "regression predictor; SZ3-Interp > 100 MB/s); the paper has no number for the regression "
+              "path alone and no GPU results (P:900)",
+}
+
+
 def barrier(world):
     import torch
     import torch.distributed as dist
@@ -167,17 +229,23 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
-def make_slab(cfg, world, rank):
-    """Generate the global field on this GPU (deterministic: seed 4) and keep this rank's slab."""
+def make_slab(cfg, world, rank, shape):
+    """Generate the global field (deterministic: the config's seed) and keep only this rank's
+    block-aligned slab on its GPU (the generator needs the whole spectrum; the rest is freed)."""
     import torch
     from paper_2111_02925_b200.dist import slab_bounds
     from synth import make_field
-    full = make_field(cfg, device="cuda")
-    a, b = slab_bounds(cfg.shape[0], world, rank)
+    full = make_field(cfg, device="cuda", shape=shape)
+    a, b = slab_bounds(shape[0], world, rank)
     x = full[a:b].clone()
     del full
     torch.cuda.empty_cache()
     return x, a
+
+
+def flush_l2(buf):
+    """Evict L2 (126 MB) by writing a buffer twice its size (SURVEY 8(d) "Flush L2")."""
+    buf.fill_(1)
 
 
 # ----------------------------------------------------------------------------------------- CPU oracle
@@ -222,7 +290,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (f32 data)",
             "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.desc}", "shape": list(shape),
                                             "eb_rel": cfg.eb, "radius": cfg.radius, "block": 6},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             **host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -375,6 +444,73 @@ def lr_leg(sz3g, x, out, bufs, cfg, a0, N_local, NB_local, s, args, world, peaks
                     "predictor flags as a bitmap (1 bit per block)"}
 
 
+# ----------------------------------------------------------------------------------------- per-config legs
+def alg_bytes(N, NB, s, n_out):
+    """SURVEY 8(d) algorithmic bytes per launch of each kernel: the quantise kernel reads
+    x and writes codes, coefficient codes (16 B / block) and outliers (index + value); the analyze
+    kernel reads x (its 32 B / block of beta is the two-pass split's own traffic, reported apart);
+    decompress reads codes, coefficient codes and outliers and writes x'."""
+    return {"quantize": N * (s + 2) + 16 * NB + n_out * (8 + s), "analyze": N * s,
+            "decompress": N * (2 + s) + 16 * NB + n_out * (8 + s), "beta": 32 * NB}
+
+
+def roof(bytes_, ms, peak):
+    gbs = bytes_ / (ms * 1e-3) / 1e9
+    return {"achieved": gbs, "frac": gbs / peak, "frac_nominal": gbs / NOMINAL_HBM_GBS, "ms_per_launch": ms,
+            "alg_bytes": bytes_}
+
+
+def config_leg(sz3g, spec, peaks, steps, warmup, flush_buf, x=None):
+    """One per-config measurement: `spec` = config name, or cNrR = config N at radius R (labelled
+    stress variant, SURVEY 8(d) point 3).  The same RoundTrip step as the main line (two-pass), L2
+    flushed before every step, per-kernel CUDA events, §8(d) bytes, bound checked, counters reported."""
+    import torch
+    from paper_2111_02925_b200.roundtrip import RoundTrip, bench_outlier_cap
+    from synth import config_by_name, make_field
+    name, R = (spec.split("r")[0], int(spec.split("r")[1])) if "r" in spec else (spec, None)
+    cfg = config_by_name(name)
+    R = R or cfg.radius
+    if x is None:
+        x = make_field(cfg, device="cuda")
+    N, s = x.numel(), x.element_size()
+    NB = sz3g.num_blocks(x.shape)
+    cap = bench_outlier_cap(N) if R >= 1024 else N
+    rt = RoundTrip(x, cfg.eb, cfg.eb_mode, R, outlier_cap=cap)
+    stream = rt.stream
+    for _ in range(warmup):
+        rt.step()
+    recs = []
+    for _ in range(steps):
+        flush_l2(flush_buf)
+        r = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        rt.step(r)
+        recs.append(r)
+    torch.cuda.synchronize()
+    res = rt.result()
+    ana = sum(r[4].elapsed_time(r[5]) for r in recs) / steps
+    qua = sum(r[0].elapsed_time(r[1]) for r in recs) / steps
+    dec = sum(r[2].elapsed_time(r[3]) for r in recs) / steps
+    step = sum(r[4].elapsed_time(r[3]) for r in recs) / steps
+    b = alg_bytes(N, NB, s, res.n_outliers)
+    st = sz3g.error_stats(x, rt.out, res.eb_abs).cpu().tolist()
+    if st[2] != 0 or not st[0] <= res.eb_abs:
+        raise RuntimeError(f"{spec}: error bound violated {st}")
+    ties = sz3g.tie_counts(x, cfg.eb, cfg.eb_mode, R, rt.bufs.minmax, res.coef_codes, rt.beta).cpu().tolist()
+    out = {"shape": list(x.shape), "dtype": str(x.dtype).replace("torch.", ""), "eb_rel": cfg.eb, "radius": R,
+           "stress_variant": R != cfg.radius, "outliers": res.n_outliers, "outlier_frac": res.n_outliers / N,
+           "entropy_bits": entropy_bits(res.hist), "max_abs_err": st[0], "eb_abs": res.eb_abs,
+           "ties": dict(zip(sz3g.TIE_COUNTER_NAMES, ties)),
+           "compress_gbs": N * s / ((ana + qua) * 1e-3) / 1e9, "decompress_gbs": N * s / (dec * 1e-3) / 1e9,
+           "round_trip_gbs": N * s / (step * 1e-3) / 1e9, "ms_per_step": step,
+           "quantize_roofline": roof(b["quantize"], qua, peaks["hbm_gbs"]),
+           "analyze_roofline": roof(b["analyze"], ana, peaks["hbm_gbs"]),
+           "decompress_roofline": roof(b["decompress"], dec, peaks["hbm_gbs"]),
+           "l2": "flushed (2x L2 write) before every step", "steps": steps, "warmup": warmup}
+    del rt
+    torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -382,98 +518,74 @@ def main():
         run_reference(args)
         return
     import torch
-    from paper_2111_02925_b200 import dist as pdist
     from paper_2111_02925_b200 import sz3g
+    from paper_2111_02925_b200.roundtrip import RoundTrip
     from synth import config_by_name
 
-    world, rank, local = dist_setup(args)
+    world, rank, dev = dist_setup(args)
     cfg = config_by_name(args.config)
+    shape = tuple(int(v) for v in args.shape.split(",")) if args.shape else tuple(cfg.shape)
     sz3g.load()
-    x, a0 = make_slab(cfg, world, rank)
-    N_local, N_global = x.numel(), math.prod(cfg.shape)
+    x, a0 = make_slab(cfg, world, rank, shape)
+    N_local, N_global = x.numel(), math.prod(shape)
     s = x.element_size()
     NB_local = sz3g.num_blocks(x.shape)
-    cap = max(1 << 20, N_local // 256)
-    bufs = sz3g.CompressBuffers(x.shape, x.dtype, cfg.radius, outlier_cap=cap, device=x.device)
-    out = torch.empty_like(x)
-    stream = torch.cuda.current_stream()
-
-    ev = {}
-
     two_pass = args.path == "two-pass"
-    beta = bufs.beta_buffer() if two_pass else None
+    rt = RoundTrip(x, cfg.eb, cfg.eb_mode, cfg.radius, dim0_offset=a0, path=args.path)
+    bufs, out, stream = rt.bufs, rt.out, rt.stream
 
-    def step(record=None):
-        if record is not None:
-            record[4].record(stream)
-        if two_pass:
-            sz3g.regression_analyze(x, bufs.minmax, beta)
-        else:
-            sz3g.value_range(x, bufs.minmax)
-        if record is not None:
-            record[5].record(stream)
-        pdist.allreduce_range_(bufs.minmax)
-        bufs.reset()
-        if record is not None:
-            record[0].record(stream)
-        if two_pass:
-            sz3g.regression_quantize(x, cfg.eb, cfg.eb_mode, cfg.radius, bufs.minmax, beta, bufs=bufs, reset=False,
-                                     dim0_offset=a0)
-        else:
-            sz3g.regression_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=bufs.minmax, bufs=bufs,
-                                     reset=False, dim0_offset=a0)
-        if record is not None:
-            record[1].record(stream)
-        pdist.allreduce_hist_(bufs.hist)
-        if record is not None:
-            record[2].record(stream)
-        sz3g.regression_decompress(bufs.codes, bufs.coef_codes, bufs.outlier_idx, bufs.outlier_val, cap, cfg.eb,
-                                   cfg.radius, x.dtype, dim0_offset=a0, out=out, d_outlier_count=bufs.outlier_count,
-                                   eb_mode=cfg.eb_mode, d_minmax=bufs.minmax)
-        if record is not None:
-            record[3].record(stream)
-
-    for _ in range(args.warmup):
-        step()
+    for _ in range(max(3, args.warmup)):
+        rt.step()
     barrier(world)
     recs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = sz3g.launch_count()
-    with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local) as clk:
+    with ClockSampler(dev) as clk:
         barrier(world)
         t_start.record(stream)
         for k in range(args.steps):
-            step(recs[k])
+            rt.step(recs[k])
         t_end.record(stream)
         barrier(world)
-    launches = sz3g.launch_count() - l0
+    launches = sum_over_ranks(sz3g.launch_count() - l0, world)
     ms_total = max_over_ranks(t_start.elapsed_time(t_end), world)
     ms_step = ms_total / args.steps
-    comp_ms = sum(r[0].elapsed_time(r[1]) for r in recs) / args.steps
-    dec_ms = sum(r[2].elapsed_time(r[3]) for r in recs) / args.steps
-    ana_ms = sum(r[4].elapsed_time(r[5]) for r in recs) / args.steps
-    comp_ms_max = max_over_ranks(comp_ms, world)
-    dec_ms_max = max_over_ranks(dec_ms, world)
+    # per-kernel times: mean over the timed steps on this rank, then the max over ranks
+    comp_ms = max_over_ranks(sum(r[0].elapsed_time(r[1]) for r in recs) / args.steps, world)
+    dec_ms = max_over_ranks(sum(r[2].elapsed_time(r[3]) for r in recs) / args.steps, world)
+    ana_ms = max_over_ranks(sum(r[4].elapsed_time(r[5]) for r in recs) / args.steps, world)
+    hist_ar_ms = max_over_ranks(sum(r[1].elapsed_time(r[2]) for r in recs) / args.steps, world)
 
-    res = sz3g.Compressed(tuple(x.shape), x.dtype, cfg.radius, a0, bufs.codes, bufs.coef_codes, None, bufs.outlier_idx,
-                          bufs.outlier_val, bufs.outlier_count, bufs.hist, bufs.eb_abs, bufs.status).finalize()
-    n_out = res.n_outliers
-    # algorithmic bytes per launch: compress reads x, writes codes, coefficient codes, outliers
-    # (two-pass quantize also reads the analyze pass's beta, 32 B per block); analyze reads x, writes beta
-    comp_bytes = N_local * (s + 2) + NB_local * 16 + n_out * (8 + s) + (NB_local * 32 if two_pass else 0)
-    ana_bytes = N_local * s + (NB_local * 32 if two_pass else 0)
-    dec_bytes = N_local * (2 + s) + NB_local * 16 + n_out * (8 + s)
+    res = rt.result()
+    n_out_local = res.n_outliers
+    n_out = sum_over_ranks(n_out_local, world)
     peaks = measured_peaks()
-    comp_gbs = comp_bytes / (comp_ms * 1e-3) / 1e9
+    # algorithmic bytes, per rank; the roofline rows use the max-over-ranks times with
+    # the largest rank's bytes (rank 0 holds the largest slab: slab_bounds gives the extra block rows
+    # to the first ranks)
+    b = alg_bytes(N_local, NB_local, s, n_out_local)
+    b = {k: max_over_ranks(float(v), world) for k, v in b.items()}
     value = N_global * s / (ms_step * 1e-3) / 1e9
+    step_bytes = b["analyze"] + b["quantize"] + b["decompress"]
 
     # ---------------- reconstruction quality (NEXT-3 metrics): bound check, max error, PSNR
     st = sz3g.error_stats(x, out, res.eb_abs).cpu().tolist()
     lo, hi = (float(v) for v in bufs.minmax.cpu())
-    quality = {"max_abs_err": st[0], "eb_abs": res.eb_abs, "above_eb": int(st[2]),
-               "psnr_db": sz3g.psnr(hi - lo, st[1] / N_local)}
-    if st[2] != 0 or not st[0] <= res.eb_abs:
+    quality = {"max_abs_err": max_over_ranks(st[0], world), "eb_abs": res.eb_abs,
+               "above_eb": sum_over_ranks(int(st[2]), world),
+               "psnr_db": sz3g.psnr(hi - lo, (st[1] if world == 1 else _sum_f(st[1], world)) / N_global),
+               "entropy_bits": entropy_bits(bufs.hist)}
+    if quality["above_eb"] != 0 or not quality["max_abs_err"] <= res.eb_abs:
         raise RuntimeError(f"error bound violated: {quality}")
+
+    # ---------------- reported counters (north_star parity rule): near-ties etc. on the whole field
+    ties = None
+    if not args.no_ties:
+        cnt = sz3g.tie_counts(x, cfg.eb, cfg.eb_mode, cfg.radius, bufs.minmax, bufs.coef_codes, rt.beta)
+        ties = {k: sum_over_ranks(int(v), world) for k, v in zip(sz3g.TIE_COUNTER_NAMES, cnt.cpu().tolist())}
+        ties["note"] = ("(i) elements within 1e-9 of a half-integer (t by true division), (ii) rint(division) != "
+                        "rint(reciprocal product), (iii) coefficients in the parity tie window, blocks holding one; "
+                        "sz3g_tie_counts, equal to the oracle's counters on c1-c4 (tests/test_gpu_ties.py)")
 
     # ---------------- encoder stage (NEXT-1): codebook from the merged histogram, encode, decode
     huff = None
@@ -495,13 +607,23 @@ def main():
     # ---------------- CPU oracle beside it (rank 0, N = 1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        lo, hi = (float(v) for v in bufs.minmax.cpu())
-        p = min(args.cpu_sample_planes, x.shape[0] - 504)
-        xs = x[504:504 + p].cpu().numpy()
-        t = oracle_round_trip(xs, cfg, lo, hi, 504)
+        pa = min(504, max(0, (x.shape[0] // 2 // 6) * 6))
+        p = min(args.cpu_sample_planes, x.shape[0] - pa)
+        xs = x[pa:pa + p].cpu().numpy()
+        t = oracle_round_trip(xs, cfg, lo, hi, pa)
         cpu = {"value": xs.nbytes / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"planes [504,{504 + p}) of {cfg.name} ({xs.size} elements, global range), "
-                         f"compress + decompress, one host core, {t:.1f} s"}
+               "sample": f"planes [{pa},{pa + p}) of {cfg.name} ({xs.size} elements, global range), "
+                         f"compress + decompress, one host core, {t:.1f} s", **host_cpu()}
+
+    # ---------------- per-config legs on the same GPU (N = 1): stress variants of this field first
+    legs = {}
+    specs = [v for v in args.configs.split(",") if v] if world == 1 else []
+    eb_abs_used = res.eb_abs
+    del rt, bufs, res, out
+    torch.cuda.empty_cache()
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if specs else None
+    for spec in [v for v in specs if v.split("r")[0] == cfg.name and shape == tuple(cfg.shape)]:
+        legs[spec] = config_leg(sz3g, spec, peaks, args.config_steps, 3, flush_buf, x=x)
 
     # ---------------- end to end through the public API with HOST buffers (pinned), copies timed:
     # paper_2111_02925_b200.pipeline.PipelinedCodec round-trips a sequence of fields from pinned host
@@ -511,68 +633,89 @@ def main():
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
         from paper_2111_02925_b200.pipeline import PipelinedCodec
-        del bufs
-        torch.cuda.empty_cache()
         h_x = torch.empty_like(x, device="cpu").pin_memory()
         h_x.copy_(x)
         h_out = torch.empty_like(x, device="cpu").pin_memory()
         codec = PipelinedCodec(tuple(x.shape), x.dtype, cfg.eb, cfg.eb_mode, cfg.radius, device=x.device,
                                dim0_offset=a0)
-        del x, out
+        del x
         torch.cuda.empty_cache()
-        codec.run([h_x], h_out)                      # warm-up (one field)
+        codec.run([h_x, h_x], h_out)                 # warm-up: both slots (their pinned payload buffers)
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(codec.s_in)
-        results = codec.run([h_x] * args.e2e_steps, h_out)
+        sizes = codec.run([h_x] * args.e2e_steps, h_out)
         e1.record(codec.s_out)
         barrier(world)
         e1.synchronize()
         e_ms = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
-        bi = h_x.numel() * s
-        bo = int(sum(r.nbytes() for r in results) / len(results)) + h_out.numel() * s
+        bi = sum_over_ranks(h_x.numel() * s, world)
+        bo = sum_over_ranks(int(sum(sizes) / len(sizes)) + h_out.numel() * s, world)
         e2e = {"value": N_global * s / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": bi,
                "d2h_bytes_per_step": bo, "ms_per_step": e_ms, "fields": args.e2e_steps,
                "note": "PipelinedCodec: pinned host field -> device, analyze + quantise + Huffman (codes, "
                        "coefficients) + decompress, compressed stream + x' -> pinned host; copies of consecutive "
                        "fields overlapped (3 streams, double-buffered)"}
+        del codec, h_x, h_out
+    else:
+        del x
+    torch.cuda.empty_cache()
+
+    for spec in specs:
+        if spec not in legs:
+            legs[spec] = config_leg(sz3g, spec, peaks, args.config_steps, 3, flush_buf)
 
     if rank == 0:
         clocks = clk.summary()
+        qroof = roof(b["quantize"], comp_ms, peaks["hbm_gbs"])
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 data, f64 arithmetic", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.desc}", "shape": list(cfg.shape), "eb_rel": cfg.eb,
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "shape": list(shape), "eb_rel": cfg.eb,
                        "radius": cfg.radius, "block": 6, "parallelism": f"slabs{world}",
-                       "l2": "inputs (16 GiB) larger than L2; no flush"},
+                       "dist_backend": args.dist_backend if world > 1 else None,
+                       "l2": "inputs (16 GiB) larger than L2; no flush" if N_global * s > (1 << 30)
+                       else "input smaller than 1 GiB: NOT flushed between steps (rehearsal shape)"},
             "roofline": {"bound": "hbm", "kernel": "k_compress_tma" + ("<beta in>" if two_pass else ""),
-                         "achieved": comp_gbs, "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": comp_gbs / peaks["hbm_gbs"],
+                         "achieved": qroof["achieved"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": qroof["frac"],
                          "traffic": profiled_traffic("k_compress_tma" + ("_beta" if two_pass else ""), cfg.name),
-                         "peak_source": peaks["source"],
-                         "frac_nominal": comp_gbs / NOMINAL_HBM_GBS, "peak_nominal": NOMINAL_HBM_GBS,
-                         "alg_bytes_per_launch": comp_bytes, "ms_per_launch": comp_ms},
-            "compress_gbs": N_global * s / (comp_ms_max * 1e-3) / 1e9,
-            "decompress_gbs": N_global * s / (dec_ms_max * 1e-3) / 1e9,
-            "decompress_roofline": {"achieved": dec_bytes / (dec_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
-                                    "frac": dec_bytes / (dec_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                                    "frac_nominal": dec_bytes / (dec_ms * 1e-3) / 1e9 / NOMINAL_HBM_GBS,
-                                    "ms_per_launch": dec_ms},
+                         "peak_source": peaks["source"], "frac_nominal": qroof["frac_nominal"],
+                         "peak_nominal": NOMINAL_HBM_GBS, "alg_bytes_per_launch": b["quantize"],
+                         "bytes_rule": "SURVEY 8(d): N (s + 2) + 16 NB + outliers (8 + s)",
+                         "beta_reread_bytes": b["beta"] if two_pass else 0,
+                         "frac_incl_beta_reread": (b["quantize"] + (b["beta"] if two_pass else 0)) /
+                         (comp_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "ms_per_launch": comp_ms, "ranks": "max over ranks"},
+            "step_roofline": {"alg_bytes": step_bytes, "frac": step_bytes / (ms_step * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                              "frac_nominal": step_bytes / (ms_step * 1e-3) / 1e9 / NOMINAL_HBM_GBS,
+                              "note": "analyze (N s) + quantize + decompress algorithmic bytes / step time"},
+            "compress_gbs": N_global * s / ((ana_ms + comp_ms) * 1e-3) / 1e9,
+            "compress_note": "input bytes / (analyze + quantise) time: REL compression needs both passes (P:833)",
+            "decompress_gbs": N_global * s / (dec_ms * 1e-3) / 1e9,
+            "decompress_roofline": roof(b["decompress"], dec_ms, peaks["hbm_gbs"]),
             "analyze_roofline": {"kernel": "k_analyze_tma" if two_pass else "k_value_range",
-                                 "achieved": ana_bytes / (ana_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
-                                 "frac": ana_bytes / (ana_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                                 "frac_nominal": ana_bytes / (ana_ms * 1e-3) / 1e9 / NOMINAL_HBM_GBS,
-                                 "ms_per_step": ana_ms},
+                                 **roof(b["analyze"], ana_ms, peaks["hbm_gbs"])},
+            "hist_allreduce_ms": hist_ar_ms if world > 1 else 0.0,
             "path": args.path,
-            "quality": quality, "huffman": huff, "truncation": trunc, "lr": lr,
-            "outliers": n_out, "eb_abs": res.eb_abs,
+            "quality": quality, "ties": ties, "huffman": huff, "truncation": trunc, "lr": lr,
+            "configs": legs or None, "outliers": n_out, "eb_abs": eb_abs_used,
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+            "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def _sum_f(v: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 if __name__ == "__main__":

@@ -193,6 +193,24 @@ int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* 
 int sz3g_histogram_bins(const uint16_t* codes, uint64_t n, uint32_t nbins, uint32_t window_lo,
                         int64_t* hist, sz3g_stream_t stream);
 
+/* Reported counters (north_star parity rule: near-ties "are counted, and the count is reported";
+ * SURVEY 8(c) "Reported counters"), a diagnostic pass over x after compression, ACCUMULATED (+=)
+ * into device uint64 d_counts[4]:
+ *   [0] (i)   elements whose pre-rounding residual / (2 eb) -- by TRUE division, t = (x - p) / 2eb --
+ *             lies within 1e-9 of a half-integer;
+ *   [1] (ii)  elements where rint(t by division) != rint((x - p) * fl(1 / 2eb)) (the definition's t,
+ *             DESIGN G5); [0] and [1] count elements with a finite quotient and |t| < R only;
+ *   [2] (iii) coefficients whose beta / w lies within max(1e-9, 1e-12 max(|beta|, mean |f|) / w)
+ *             of a half-integer (w = eb/2 intercept, eb/12 slopes), the parity tie window;
+ *   [3]       blocks holding at least one such coefficient.
+ * p is the O7 prediction from coef_codes (the stored coefficients), eb_abs from params / d_minmax as
+ * in compression.  beta (4 x nblocks double, the analyze pass's or coef_raw) is nullable: then [2]
+ * and [3] are not touched.  Sums and counts follow the definition's loop order, so for the same
+ * codes and beta they equal the oracle's counters exactly.  Not on the timed path.  1 launch. */
+int sz3g_tie_counts(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax, const void* x,
+                    const int32_t* coef_codes, const double* beta, unsigned long long* d_counts,
+                    sz3g_stream_t stream);
+
 /* number of regression blocks of a grid: prod ceil(n_d / block_size) (0 on bad input) */
 uint64_t sz3g_num_blocks(const sz3g_grid* grid, uint32_t block_size);
 
@@ -311,6 +329,7 @@ typedef struct {
   double       eb_abs;      /* the absolute bound used                                         */
   uint32_t     radius, block_size, chunk, max_len, flags;
   uint64_t     n_outliers, nblocks;
+  uint64_t     dim0_offset; /* global plane offset of the slab (outlier indices are global); 0 unsharded */
 } sz3g_stream_header;
 typedef struct {
   uint32_t    tag;
@@ -336,6 +355,21 @@ int sz3g_stream_write(const sz3g_stream_header* hdr, const sz3g_section* section
                       void* out, uint64_t cap, uint64_t* written);
 int sz3g_stream_read(const void* in, uint64_t len, sz3g_stream_header* hdr, sz3g_section* sections,
                      uint32_t sec_cap, uint32_t* nsec, uint32_t* bad_tag);
+/* Consistency of a parsed compressed-field stream (sections as returned by sz3g_stream_read) BEFORE
+ * anything is launched on it: the checksums only catch accidental damage, this catches a stream that is
+ * internally inconsistent (and would make a decoder read past a buffer).  Checks: dtype, 1 <= ndim <= 3
+ * with leading extents 1, block_size 6, radius in [1, 32768], 1 <= max_len <= 16, chunk >= 1, eb_abs
+ * finite and > 0, nblocks == sz3g_num_blocks(dims); every required section present once (LR_FLAGS iff
+ * the LR flag); OUT_IDX = 8 n_outliers and OUT_VAL = sizeof(T) n_outliers bytes, every outlier index in
+ * the slab [dim0_offset n1 n2, (dim0_offset + n0) n1 n2); CODE_OFFS / COEF_OFFS hold exactly
+ * ceil(n / chunk) + 1 u64 offsets (n = N codes, 4 nblocks coefficient symbols), starting at 0,
+ * non-decreasing, each chunk at most ceil(chunk max_len / 32) words, ending at the payload's word count
+ * (CODE_DATA / COEF_DATA a whole number of u32 words); codebooks u32 m then m (u16 symbol < 2R (65536
+ * for the coefficients), u8 length in 1..max_len) records, symbols strictly increasing; COEF_ESC a
+ * whole number of u64; LR_FLAGS ceil(nblocks / 8) bytes.  Returns SZ3G_OK, SZ3G_EINVAL (null
+ * arguments) or SZ3G_ECORRUPT with the offending section's tag (0 = the header) in *bad_tag. */
+int sz3g_stream_validate(const sz3g_stream_header* hdr, const sz3g_section* sections, uint32_t nsec,
+                         uint32_t* bad_tag);
 
 /* Performance tuning only (no call changes a result): set knob `key` ("CHUNK_C", "CHUNK_D", "CCFG",
  * "PF"; defaults are the measured best, environment SZ3G_<KEY> overrides them) for

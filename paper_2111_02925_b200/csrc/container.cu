@@ -8,6 +8,7 @@
 // Layout (little-endian):
 //   "SZ3G" | version u16 = 1 | header (sz3g_stream_header, fixed 96-byte encoding below) |
 //   nsec u32 | nsec x { tag u8 | length u64 | fnv1a64 u64 | payload[length] }
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 
@@ -56,6 +57,7 @@ void encode_header(const sz3g_stream_header* h, uint8_t* o) {
   put<uint32_t>(p, h->flags);
   put<uint64_t>(p, h->n_outliers);
   put<uint64_t>(p, h->nblocks);
+  put<uint64_t>(p, h->dim0_offset);   // bytes 80..87 (zero in streams written before this field existed)
   while (p < o + kHeaderBytes) put<uint8_t>(p, 0);
 }
 
@@ -75,11 +77,119 @@ void decode_header(const uint8_t* i, sz3g_stream_header* h) {
   h->flags = get<uint32_t>(p);
   h->n_outliers = get<uint64_t>(p);
   h->nblocks = get<uint64_t>(p);
+  h->dim0_offset = get<uint64_t>(p);
+}
+
+const sz3g_section* find(const sz3g_section* s, uint32_t n, uint32_t tag, int* count) {
+  const sz3g_section* f = nullptr;
+  *count = 0;
+  for (uint32_t i = 0; i < n; i++)
+    if (s[i].tag == tag) {
+      f = &s[i];
+      (*count)++;
+    }
+  return f;
+}
+
+uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// canonical codebook record list: u32 m, m x (u16 symbol, u8 length), symbols increasing
+bool book_ok(const sz3g_section* b, uint32_t nsym, uint32_t max_len) {
+  if (b->bytes < 4) return false;
+  const uint8_t* p = static_cast<const uint8_t*>(b->data);
+  uint32_t m;
+  std::memcpy(&m, p, 4);
+  if (m > nsym || b->bytes != 4 + 3ull * m) return false;
+  int64_t prev = -1;
+  for (uint32_t r = 0; r < m; r++) {
+    uint16_t sym;
+    std::memcpy(&sym, p + 4 + 3ull * r, 2);
+    const uint8_t len = p[4 + 3ull * r + 2];
+    if (sym >= nsym || (int64_t)sym <= prev || len < 1 || len > max_len) return false;
+    prev = sym;
+  }
+  return true;
+}
+
+// chunk offsets of a Huffman stream of n symbols against its payload section
+bool offsets_ok(const sz3g_section* o, const sz3g_section* d, uint64_t n, uint32_t chunk, uint32_t max_len) {
+  const uint64_t nch = cdiv(n, chunk);
+  if (o->bytes != 8 * (nch + 1) || d->bytes % 4) return false;
+  const uint8_t* p = static_cast<const uint8_t*>(o->data);
+  const uint64_t max_words = cdiv((uint64_t)chunk * max_len, 32);
+  uint64_t prev;
+  std::memcpy(&prev, p, 8);
+  if (prev != 0) return false;
+  for (uint64_t c = 1; c <= nch; c++) {
+    uint64_t v;
+    std::memcpy(&v, p + 8 * c, 8);
+    if (v < prev || v - prev > max_words) return false;
+    prev = v;
+  }
+  return prev == d->bytes / 4;
 }
 
 }  // namespace
 
 extern "C" {
+
+int sz3g_stream_validate(const sz3g_stream_header* h, const sz3g_section* s, uint32_t n, uint32_t* bad_tag) {
+  if (!h || (n && !s)) return SZ3G_EINVAL;
+  uint32_t dummy;
+  uint32_t* bad = bad_tag ? bad_tag : &dummy;
+  *bad = 0;
+  if ((h->dtype != SZ3G_F32 && h->dtype != SZ3G_F64) || h->ndim < 1 || h->ndim > 3 || h->block_size != 6 ||
+      h->radius < 1 || h->radius > 32768 || h->max_len < 1 || h->max_len > 16 || h->chunk < 1 ||
+      !std::isfinite(h->eb_abs) || !(h->eb_abs > 0))
+    return SZ3G_ECORRUPT;
+  uint64_t N = 1;
+  for (int d = 0; d < 3; d++) {
+    if (h->dims[d] == 0 || (d < 3 - (int)h->ndim && h->dims[d] != 1)) return SZ3G_ECORRUPT;
+    if (h->dims[d] > (UINT64_MAX / N)) return SZ3G_ECORRUPT;
+    N *= h->dims[d];
+  }
+  const uint64_t nb = cdiv(h->dims[0], 6) * cdiv(h->dims[1], 6) * cdiv(h->dims[2], 6);
+  if (h->nblocks != nb) return SZ3G_ECORRUPT;
+  const bool lr = (h->flags & SZ3G_STREAM_LR) != 0;
+  const sz3g_section* sec[SZ3G_SEC_LR_FLAGS + 1] = {};
+  for (uint32_t tag = SZ3G_SEC_CODE_BOOK; tag <= SZ3G_SEC_LR_FLAGS; tag++) {
+    int cnt;
+    sec[tag] = find(s, n, tag, &cnt);
+    const bool want = tag != SZ3G_SEC_LR_FLAGS || lr;
+    if ((want && cnt != 1) || (!want && cnt != 0)) {
+      *bad = tag;
+      return SZ3G_ECORRUPT;
+    }
+  }
+  const uint64_t vs = h->dtype == SZ3G_F32 ? 4 : 8;
+  if (sec[SZ3G_SEC_OUT_IDX]->bytes != 8 * h->n_outliers) { *bad = SZ3G_SEC_OUT_IDX; return SZ3G_ECORRUPT; }
+  if (sec[SZ3G_SEC_OUT_VAL]->bytes != vs * h->n_outliers) { *bad = SZ3G_SEC_OUT_VAL; return SZ3G_ECORRUPT; }
+  {
+    const uint64_t plane = h->dims[1] * h->dims[2];
+    const uint64_t lo = h->dim0_offset * plane, hi = lo + N;
+    if (h->dim0_offset > UINT64_MAX / plane || hi < lo) return SZ3G_ECORRUPT;
+    const uint8_t* p = static_cast<const uint8_t*>(sec[SZ3G_SEC_OUT_IDX]->data);
+    for (uint64_t e = 0; e < h->n_outliers; e++) {
+      uint64_t v;
+      std::memcpy(&v, p + 8 * e, 8);
+      if (v < lo || v >= hi) { *bad = SZ3G_SEC_OUT_IDX; return SZ3G_ECORRUPT; }
+    }
+  }
+  if (!book_ok(sec[SZ3G_SEC_CODE_BOOK], 2 * h->radius, h->max_len)) { *bad = SZ3G_SEC_CODE_BOOK; return SZ3G_ECORRUPT; }
+  if (!book_ok(sec[SZ3G_SEC_COEF_BOOK], 65536, h->max_len)) { *bad = SZ3G_SEC_COEF_BOOK; return SZ3G_ECORRUPT; }
+  if (!offsets_ok(sec[SZ3G_SEC_CODE_OFFS], sec[SZ3G_SEC_CODE_DATA], N, h->chunk, h->max_len)) {
+    *bad = SZ3G_SEC_CODE_OFFS;
+    return SZ3G_ECORRUPT;
+  }
+  if (!offsets_ok(sec[SZ3G_SEC_COEF_OFFS], sec[SZ3G_SEC_COEF_DATA], 4 * nb, h->chunk, h->max_len)) {
+    *bad = SZ3G_SEC_COEF_OFFS;
+    return SZ3G_ECORRUPT;
+  }
+  if (sec[SZ3G_SEC_COEF_ESC]->bytes % 8) { *bad = SZ3G_SEC_COEF_ESC; return SZ3G_ECORRUPT; }
+  if (lr && sec[SZ3G_SEC_LR_FLAGS]->bytes != cdiv(nb, 8)) { *bad = SZ3G_SEC_LR_FLAGS; return SZ3G_ECORRUPT; }
+  return SZ3G_OK;
+}
+
 
 uint64_t sz3g_stream_size(const sz3g_section* sections, uint32_t nsec) {
   uint64_t n = 4 + 2 + kHeaderBytes + 4;

@@ -1317,11 +1317,10 @@ int sz3g_huffman_encode(const uint16_t* codes, uint64_t n, uint32_t chunk, const
   k_scan_apply<<<(unsigned)nb, SCAN_T, 0, st>>>(chunk_offsets, nch, sums, nb);
   if (nfull) {
     const size_t smem = ew_smem_bytes();
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_huff_encode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    // per launch: the attribute is per device, and a cached flag would skip it on a second GPU
+    if (cudaFuncSetAttribute(k_huff_encode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return hf_check(nl + 3);
     k_huff_encode_full<<<gf, EW_WARPS * 32, smem, st>>>(codes, nfull, codewords, nsym, chunk_offsets, loff,
                                                         payload, payload_cap_words, d_status);
     nl++;
@@ -1350,11 +1349,9 @@ int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, 
   int nl = 0;
   if (nfull) {
     const size_t smem = df_smem_bytes();
-    static bool attr_f = false;
-    if (!attr_f) {
-      cudaFuncSetAttribute(k_huff_decode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr_f = true;
-    }
+    if (cudaFuncSetAttribute(k_huff_decode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return hf_check(nl);
     const uint64_t per_cta = 32ull * DF_WARPS;
     k_huff_decode_full<<<(unsigned)((nfull + per_cta - 1) / per_cta), DF_WARPS * 32, smem, st>>>(
         payload, chunk_offsets, nch, nfull, reinterpret_cast<const DTab*>(dtable), max_len, codes, d_status);
@@ -1362,11 +1359,8 @@ int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, 
   }
   if (nch > nfull) {
     const size_t smem = dec_smem_bytes();
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_huff_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    if (cudaFuncSetAttribute(k_huff_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return hf_check(nl);
     const uint64_t per_cta = 32ull * DEC_WARPS;
     k_huff_decode<<<(unsigned)((nch - nfull + per_cta - 1) / per_cta), DEC_WARPS * 32, smem, st>>>(
         payload, chunk_offsets, n, chunk, reinterpret_cast<const DTab*>(dtable), max_len, codes, nch, d_status, nfull);

@@ -895,6 +895,85 @@ __global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ 
   hist_flush(hs, hist);
 }
 
+// ---------------------------------------------------------------------------------- reported counters
+// The parity rule's counters (north_star: near-ties "are counted, and the count is reported"; SURVEY
+// 8(c) "Reported counters" (i)-(iii)), a diagnostic pass after compression: one thread per block,
+// sequential i -> j -> k loops over the block as in the definition (so sum |f| and every count are
+// exactly the oracle's for the same coefficient codes and beta).  Consecutive threads take adjacent
+// blocks along dim 2, so a warp's loads of one (i, j, k) cover 32 x 6 contiguous elements.
+__device__ __forceinline__ bool near_half_d(double u, double window) {
+  const double fl = floor(u);
+  return fabs(__dsub_rn(__dsub_rn(u, fl), 0.5)) <= window;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_tie_counts(const T* __restrict__ x, const int32_t* __restrict__ coef,
+                                                    const double* __restrict__ beta, KArgs a,
+                                                    unsigned long long* __restrict__ counts) {
+  Consts K;
+  const bool ok = make_consts(a.eb_mode, a.eb, a.d_minmax, 0.0, K);
+  const Geo& g = a.g;
+  const uint64_t nb = (uint64_t)g.NB0 * g.NB1 * g.NB2;
+  unsigned long long c_i = 0, c_ii = 0, c_iii = 0, c_blk = 0;
+  const double R = (double)a.R;
+  for (uint64_t bid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ok && bid < nb;
+       bid += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = bid % g.NB2, ab = bid / g.NB2, b = ab % g.NB1, a0 = ab / g.NB1;
+    const uint64_t i0 = a0 * BS, j0 = b * BS, k0 = c * BS;
+    const int m0 = (int)umin64(BS, g.n0 - i0), m1 = (int)umin64(BS, g.n1 - j0), m2 = (int)umin64(BS, g.n2 - k0);
+    const int4 cc = reinterpret_cast<const int4*>(coef)[bid];
+    // O6 decoded coefficients: b^ = c * w (the integer c is exact as a double)
+    const double bh0 = __dmul_rn((double)cc.x, K.w0), bh1 = __dmul_rn((double)cc.y, K.ws);
+    const double bh2 = __dmul_rn((double)cc.z, K.ws), bh3 = __dmul_rn((double)cc.w, K.ws);
+    double absum = 0.0;
+    for (int i = 0; i < m0; i++)
+      for (int j = 0; j < m1; j++)
+        for (int k = 0; k < m2; k++) {
+          const double xd = to_d<T>(x[((i0 + i) * g.n1 + (j0 + j)) * g.n2 + (k0 + k)]);
+          absum = __dadd_rn(absum, fabs(xd));
+          // O7
+          const double p = __fma_rn(bh1, (double)i, __fma_rn(bh2, (double)j, __fma_rn(bh3, (double)k, bh0)));
+          const double r = __dsub_rn(xd, p);
+          const double tdiv = __ddiv_rn(r, K.twoeb);
+          const double tmul = __dmul_rn(r, K.inv2eb);
+          if (isfinite(tdiv) && fabs(tmul) < R) {
+            c_i += near_half_d(tdiv, 1e-9) ? 1 : 0;
+            c_ii += (rint(tdiv) != rint(tmul)) ? 1 : 0;
+          }
+        }
+    if (beta) {
+      const double scale = __ddiv_rn(absum, (double)m0 * (double)m1 * (double)m2);
+      bool tie = false;
+#pragma unroll
+      for (int d = 0; d < 4; d++) {
+        const double w = d == 0 ? K.w0 : K.ws;
+        const double bd = beta[4 * bid + d];
+        const double u = __ddiv_rn(bd, w);
+        if (!isfinite(u)) continue;
+        const double win = fmax(1e-9, __ddiv_rn(__dmul_rn(1e-12, fmax(fabs(bd), scale)), w));
+        if (near_half_d(u, win)) {
+          c_iii++;
+          tie = true;
+        }
+      }
+      c_blk += tie ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    c_i += __shfl_xor_sync(0xffffffffu, c_i, o);
+    c_ii += __shfl_xor_sync(0xffffffffu, c_ii, o);
+    c_iii += __shfl_xor_sync(0xffffffffu, c_iii, o);
+    c_blk += __shfl_xor_sync(0xffffffffu, c_blk, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (c_i | c_ii | c_iii | c_blk)) {
+    atomicAdd(&counts[0], c_i);
+    atomicAdd(&counts[1], c_ii);
+    atomicAdd(&counts[2], c_iii);
+    atomicAdd(&counts[3], c_blk);
+  }
+}
+
 // ---------------------------------------------------------------------------------- host helpers
 int sm_count() {
   int dev = 0, sms = 148;
@@ -1531,6 +1610,30 @@ int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, sm_count() * 2));
   k_histogram<<<blocks, 512, 0, st>>>(codes, n, 2u * radius, lo, reinterpret_cast<unsigned long long*>(hist));
+  return check_launch(1);
+}
+
+int sz3g_tie_counts(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax, const void* x,
+                    const int32_t* coef_codes, const double* beta, unsigned long long* d_counts,
+                    sz3g_stream_t stream) {
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  rc = validate_params(params);
+  if (rc) return rc;
+  if (!x || !coef_codes || !d_counts || (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax)) return SZ3G_EINVAL;
+  if (reinterpret_cast<uintptr_t>(coef_codes) & 15) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  KArgs ka;
+  memset(&ka, 0, sizeof(ka));
+  ka.g = make_geo(grid);
+  ka.R = params->radius;
+  ka.eb_mode = (int)params->eb_mode;
+  ka.eb = params->eb;
+  ka.d_minmax = d_minmax;
+  const uint64_t nb = (uint64_t)ka.g.NB0 * ka.g.NB1 * ka.g.NB2;
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, sm_count() * 16));
+  if (grid->dtype == SZ3G_F32) k_tie_counts<float><<<blocks, 256, 0, st>>>((const float*)x, coef_codes, beta, ka, d_counts);
+  else k_tie_counts<double><<<blocks, 256, 0, st>>>((const double*)x, coef_codes, beta, ka, d_counts);
   return check_launch(1);
 }
 

@@ -25,7 +25,8 @@ from . import sz3g
 
 @dataclass
 class HostResult:
-    """Compressed field in pinned host memory (views valid until the next use of the slot)."""
+    """Compressed field in pinned host memory.  Each of the two slots has its own pinned buffers, so a
+    result stays valid until its slot is reused two fields later (consume it in ``on_result``)."""
     payload: torch.Tensor        # int32 [words]
     offsets: torch.Tensor        # int64 [nchunks + 1]
     code_lengths: torch.Tensor   # uint8 [2R]
@@ -84,15 +85,18 @@ class PipelinedCodec:
         self.ev_out = [torch.cuda.Event() for _ in range(2)]
         self.ev_xfree = [torch.cuda.Event() for _ in range(2)]
         self.state = [None, None]
-        self.h_payload = torch.empty(cap, dtype=torch.int32, pin_memory=True)
-        self.h_sizes = [torch.zeros(7, dtype=torch.int64, pin_memory=True) for _ in range(2)]
-        self.h_offsets = torch.empty(nch + 1, dtype=torch.int64, pin_memory=True)
-        # pinned host buffers of the small sections, sized for their maxima (no allocation per field:
-        # a pinned allocation can synchronise the device)
+        # pinned host buffers PER SLOT (a slot's result is not overwritten by the other slot's field).
+        # The payload buffer grows on demand to the payload actually produced (a pinned allocation can
+        # synchronise the device, so it happens at most a few times, on the first fields).
+        self.h_payload = [None, None]
+        self.h_sizes = [torch.zeros(9, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self.h_offsets = [torch.empty(nch + 1, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        # pinned host buffers of the small sections, sized for their maxima (no allocation per field)
         nb = self.bufs[0].coef_codes.shape[0]
+        self.nb = nb
         cnch = -(-4 * nb // sz3g.HUFF_CHUNK)
         ocap = self.bufs[0].outlier_idx.numel()
-        self.h_small = [
+        self.h_small = [[
             torch.empty(2 * radius, dtype=torch.uint8, pin_memory=True),                       # code lengths
             torch.empty(-(-4 * nb * sz3g.HUFF_MAX_LEN // 32) + cnch, dtype=torch.int32, pin_memory=True),
             torch.empty(cnch + 1, dtype=torch.int64, pin_memory=True),                         # coef offsets
@@ -101,7 +105,7 @@ class PipelinedCodec:
             torch.empty(ocap, dtype=torch.int64, pin_memory=True),                             # outlier idx
             torch.empty(ocap, dtype=dtype, pin_memory=True),                                   # outlier val
             torch.empty(max(1, nb), dtype=torch.uint8, pin_memory=True),                       # LR flags
-        ]
+        ] for _ in range(2)]
 
     # ------------------------------------------------------------------ stages
     def _copy_in(self, k: int, host_x: torch.Tensor):
@@ -144,18 +148,19 @@ class PipelinedCodec:
             # operation on the legacy default stream (it would wait for every other stream's work)
             sizes = torch.stack([bufs.status.to(torch.int64)[0], bufs.outlier_count[0],
                                  bufs.eb_abs.view(torch.int64)[0], self.offsets[b][-1], coef.stream.offsets[-1],
-                                 coef.n_escapes[0], table.status.to(torch.int64)[0] | hs.status.to(torch.int64)[0]])
+                                 coef.n_escapes[0], table.status.to(torch.int64)[0] | hs.status.to(torch.int64)[0],
+                                 (table.lengths > 0).sum(), (coef.table.lengths > 0).sum()])
             self.h_sizes[b].copy_(sizes, non_blocking=True)
             self.ev_xfree[b].record(st)
             self.ev_comp[b].record(st)
         self.state[b] = (table, hs, coef)
 
-    def _copy_out(self, k: int, host_out: torch.Tensor) -> HostResult:
+    def _copy_out(self, k: int, host_out: torch.Tensor) -> tuple[HostResult, int]:
         b = k % 2
         bufs = self.bufs[b]
         table, hs, coef = self.state[b]
         self.ev_comp[b].synchronize()                        # sizes of the variable-length sections
-        status, n_out, eb_bits, words, cw, nesc, hstat = (int(v) for v in self.h_sizes[b].tolist())
+        status, n_out, eb_bits, words, cw, nesc, hstat, nact, ncact = (int(v) for v in self.h_sizes[b].tolist())
         if status & sz3g.STATUS_BAD_RANGE:
             raise sz3g.SZ3GError("bad value range")
         if status & sz3g.STATUS_OUTLIER_OVERFLOW:
@@ -164,30 +169,41 @@ class PipelinedCodec:
             raise sz3g.SZ3GError("Huffman stage failed (status or escape capacity)")
         import struct
         eb_abs = struct.unpack("<d", struct.pack("<q", eb_bits))[0]
+        # the slot's pinned buffers were last read by field k - 2's consumer (on_result ran before
+        # this call); the payload buffer grows if this field's payload is larger
+        if self.h_payload[b] is None or self.h_payload[b].numel() < words:
+            self.s_out.synchronize()
+            self.h_payload[b] = torch.empty(max(1, words + words // 4), dtype=torch.int32, pin_memory=True)
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_comp[b])
-            hp = self.h_payload[:words]
+            hp = self.h_payload[b][:words]
             hp.copy_(self.payload[b][:words], non_blocking=True)
-            self.h_offsets.copy_(self.offsets[b], non_blocking=True)
+            self.h_offsets[b].copy_(self.offsets[b], non_blocking=True)
             host_out.copy_(self.out[b], non_blocking=True)
             small = []
             srcs = [table.lengths, coef.stream.payload[:cw], coef.stream.offsets, coef.table.lengths,
                     coef.escapes[:nesc], bufs.outlier_idx[:n_out], bufs.outlier_val[:n_out]]
             if self.predictor == "lr":
                 srcs.append(bufs.lr_flags)
-            for h, t in zip(self.h_small, srcs):
+            for h, t in zip(self.h_small[b], srcs):
                 hv = h[:t.numel()]
                 hv.copy_(t, non_blocking=True)
                 small.append(hv)
             self.ev_out[b].record(self.s_out)
-        return HostResult(hp, self.h_offsets, small[0], small[1], small[2], small[3], small[4], small[5], small[6],
-                          eb_abs, small[7] if self.predictor == "lr" else None)
+        # compressed bytes of this field, from the device-side sizes (no read of the pinned data):
+        # the same sum as HostResult.nbytes()
+        es = torch.empty((), dtype=self.dtype).element_size()
+        nbytes = 4 * words + 8 * self.offsets[b].numel() + 4 * cw + 8 * coef.stream.offsets.numel() + 8 * nesc + \
+            (8 + es) * n_out + 4 + 3 * nact + 4 + 3 * ncact + ((self.nb + 7) // 8 if self.predictor == "lr" else 0)
+        return HostResult(hp, self.h_offsets[b], small[0], small[1], small[2], small[3], small[4], small[5], small[6],
+                          eb_abs, small[7] if self.predictor == "lr" else None), nbytes
 
     # ------------------------------------------------------------------ driver
-    def run(self, host_fields, host_out: torch.Tensor, on_result=None) -> list:
+    def run(self, host_fields, host_out: torch.Tensor, on_result=None) -> list[int]:
         """Round trip every field of `host_fields` (pinned host tensors of the codec's shape); every
-        reconstruction is written to `host_out` (pinned), in order.  Returns the host results' sizes
-        (the payload buffers are reused: consume them in `on_result(k, HostResult)`)."""
+        reconstruction is written to `host_out` (pinned), in order.  Returns each field's compressed
+        size in bytes.  The compressed sections live in per-slot pinned buffers that are reused two
+        fields later: consume them in `on_result(k, HostResult)` (called once field k is on the host)."""
         sizes = []
         nf = len(host_fields)
         for k in range(nf + 1):
@@ -195,10 +211,10 @@ class PipelinedCodec:
                 self._copy_in(k, host_fields[k])
                 self._compute(k)
             if k >= 1:
-                r = self._copy_out(k - 1, host_out)
+                r, nbytes = self._copy_out(k - 1, host_out)
                 if on_result is not None:
                     self.s_out.synchronize()
                     on_result(k - 1, r)
-                sizes.append(r)
+                sizes.append(nbytes)
         self.s_out.synchronize()
         return sizes

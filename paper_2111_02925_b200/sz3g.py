@@ -46,7 +46,7 @@ class StreamHeader(ctypes.Structure):
                 ("eb_mode", ctypes.c_int), ("eb", ctypes.c_double), ("eb_abs", ctypes.c_double),
                 ("radius", ctypes.c_uint32), ("block_size", ctypes.c_uint32), ("chunk", ctypes.c_uint32),
                 ("max_len", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("n_outliers", ctypes.c_uint64),
-                ("nblocks", ctypes.c_uint64)]
+                ("nblocks", ctypes.c_uint64), ("dim0_offset", ctypes.c_uint64)]
 
 
 class Section(ctypes.Structure):
@@ -123,6 +123,11 @@ def load(allow_build: bool = False):
     if hasattr(lib, "sz3g_lr_quantize"):   # absent only in older A/B builds
         lib.sz3g_lr_quantize.argtypes = [GP, PP, P, P, P, P, P, P, P, P, U64, P, P, P, P, P]
         lib.sz3g_lr_decompress.argtypes = [GP, PP, P, P, P, P, P, P, U64, P, P, P]
+    if hasattr(lib, "sz3g_tie_counts"):   # absent only in older A/B builds
+        lib.sz3g_tie_counts.argtypes = [GP, PP, P, P, P, P, P, P]
+    if hasattr(lib, "sz3g_stream_validate"):
+        lib.sz3g_stream_validate.argtypes = [ctypes.POINTER(StreamHeader), ctypes.POINTER(Section), U32,
+                                             ctypes.POINTER(U32)]
     if hasattr(lib, "sz3g_set_tuning"):   # absent only in older A/B builds
         lib.sz3g_set_tuning.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     for f in ("sz3g_strerror",):
@@ -142,7 +147,7 @@ EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regres
                     "sz3g_truncation_decompress", "sz3g_error_stats_scratch_bytes", "sz3g_error_stats",
                     "sz3g_coef_delta_scratch_bytes", "sz3g_coef_delta_encode", "sz3g_coef_delta_decode",
                     "sz3g_huffman_codebook_from_lengths", "sz3g_stream_size", "sz3g_stream_write",
-                    "sz3g_stream_read", "sz3g_lr_quantize", "sz3g_lr_decompress",
+                    "sz3g_stream_read", "sz3g_stream_validate", "sz3g_tie_counts", "sz3g_lr_quantize", "sz3g_lr_decompress",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -486,6 +491,25 @@ def histogram_bins(codes: torch.Tensor, nbins: int, window_lo: int = 0, hist: to
     return hist
 
 
+TIE_COUNTER_NAMES = ("elem_near_ties", "elem_div_mismatch", "coef_near_ties", "coef_tie_blocks")
+
+
+def tie_counts(x: torch.Tensor, eb: float, eb_mode: str, radius: int, d_minmax: torch.Tensor | None,
+               coef_codes: torch.Tensor, beta: torch.Tensor | None = None, counts: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """sz3g_tie_counts: the parity rule's reported counters (i) element near-ties, (ii) division /
+    reciprocal rounding mismatches, (iii) coefficient near-ties and their blocks, ACCUMULATED into a
+    device int64 [4] (asynchronous).  ``beta`` None skips (iii)."""
+    _require_cuda(x, d_minmax, coef_codes, beta, counts)
+    if counts is None:
+        counts = torch.zeros(4, dtype=torch.int64, device=x.device)
+    g = make_grid(x.shape, x.dtype)
+    p = make_params(eb, eb_mode, radius)
+    _check(load().sz3g_tie_counts(ctypes.byref(g), ctypes.byref(p), _ptr(d_minmax), _ptr(x), _ptr(coef_codes),
+                                  _ptr(beta), _ptr(counts), _stream(stream)), "sz3g_tie_counts")
+    return counts
+
+
 # ------------------------------------------------------------------------------------------- one-call API
 def compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768, two_pass: bool | None = None,
              **kw) -> Compressed:
@@ -808,7 +832,8 @@ def to_bytes(res: "Compressed", table: HuffmanTable | None = None, hs: HuffmanSt
     hdr = StreamHeader(_dtype_id(res.dtype), len(res.shape), (ctypes.c_uint64 * 3)(*s3),
                        {"abs": SZ3G_EB_ABS, "rel": SZ3G_EB_REL_RANGE}[eb_mode],
                        float(res.eb_abs if eb is None else eb), float(res.eb_abs), res.radius, BLOCK, hs.chunk,
-                       table.max_len, STREAM_LR if res.lr_flags is not None else 0, n, res.coef_codes.shape[0])
+                       table.max_len, STREAM_LR if res.lr_flags is not None else 0, n, res.coef_codes.shape[0],
+                       int(res.dim0_offset))
     lib = load()
     size = int(lib.sz3g_stream_size(secs, len(host)))
     out = ctypes.create_string_buffer(size)
@@ -831,6 +856,10 @@ def from_bytes(buf: bytes, device=None) -> torch.Tensor:
     rc = lib.sz3g_stream_read(buf, len(buf), ctypes.byref(hdr), secs, 16, ctypes.byref(nsec), ctypes.byref(bad))
     if rc != 0:
         raise SZ3GError(f"corrupt stream (section tag {bad.value})" if rc == -5 else f"sz3g_stream_read: {_ERR.get(rc, rc)}")
+    # header / section consistency BEFORE anything is launched (sizes, offsets, codebooks, indices)
+    rc = lib.sz3g_stream_validate(ctypes.byref(hdr), secs, nsec.value, ctypes.byref(bad))
+    if rc != 0:
+        raise SZ3GError(f"corrupt stream: inconsistent {'header' if bad.value == 0 else f'section {bad.value}'}")
     sec = {secs[i].tag: ctypes.string_at(secs[i].data, secs[i].bytes) if secs[i].bytes else b""
            for i in range(nsec.value)}
     dtype = {SZ3G_F32: torch.float32, SZ3G_F64: torch.float64}[hdr.dtype]
@@ -858,7 +887,8 @@ def from_bytes(buf: bytes, device=None) -> torch.Tensor:
     t_coef = table_from(sec[SEC_COEF_BOOK], 65536)
     cs = stream_from(sec[SEC_COEF_OFFS], sec[SEC_COEF_DATA], 4 * nb)
     esc = torch.from_numpy(np.frombuffer(sec[SEC_COEF_ESC], np.int64).copy()).to(device)
-    coef = coef_delta_decode(huffman_decode(cs, t_coef), nb, esc)
+    coef_status = torch.zeros(1, dtype=torch.int32, device=device)
+    coef = coef_delta_decode(huffman_decode(cs, t_coef), nb, esc, status=coef_status)
     oidx = torch.from_numpy(np.frombuffer(sec[SEC_OUT_IDX], np.int64).copy()).to(device)
     oval = torch.from_numpy(np.frombuffer(sec[SEC_OUT_VAL], np.float32 if dtype == torch.float32 else np.float64)
                             .copy()).to(device)
@@ -871,10 +901,14 @@ def from_bytes(buf: bytes, device=None) -> torch.Tensor:
         if bits.size != nb:
             raise SZ3GError("corrupt stream: short SZ3-LR flags section")
         fl = torch.from_numpy(bits.astype(np.uint8)).to(device)
-        out = lr_decompress(codes, coef, fl, oidx, oval, int(hdr.n_outliers), hdr.eb_abs, R, dtype)
+        out = lr_decompress(codes, coef, fl, oidx, oval, int(hdr.n_outliers), hdr.eb_abs, R, dtype,
+                            dim0_offset=int(hdr.dim0_offset))
     else:
-        out = regression_decompress(codes, coef, oidx, oval, int(hdr.n_outliers), hdr.eb_abs, R, dtype)
+        out = regression_decompress(codes, coef, oidx, oval, int(hdr.n_outliers), hdr.eb_abs, R, dtype,
+                                    dim0_offset=int(hdr.dim0_offset))
     torch.cuda.synchronize()
     if int(hs.status.item()) or int(cs.status.item()):
         raise SZ3GError("corrupt Huffman stream")
+    if int(coef_status.item()):
+        raise SZ3GError("corrupt coefficient stream (escape list)")
     return out

@@ -61,3 +61,28 @@ def test_pipeline_lr_matches_direct():
         xo, fl = got[k]
         assert torch.equal(xo.view(torch.int32), direct.view(torch.int32))
         assert torch.equal(fl, res.lr_flags.cpu()) and int(fl.sum()) > 0
+
+
+def test_pipeline_slots_do_not_alias_and_sizes():
+    """The two slots own separate pinned buffers (r1: HostResults of consecutive fields aliased): when
+    field k + 1 is on the host, field k's result is still intact; run() returns each field's
+    compressed size, equal to HostResult.nbytes()."""
+    from paper_2111_02925_b200.pipeline import PipelinedCodec
+    from synth import config_by_name, make_field
+    cfg = config_by_name("c2")
+    fields = [make_field(cfg, device="cuda", shape=(48, 96, 120)) * (1.0 + 0.5 * k) for k in range(4)]
+    hosts = [f.cpu().pin_memory() for f in fields]
+    h_out = torch.empty_like(hosts[0]).pin_memory()
+    codec = PipelinedCodec(tuple(fields[0].shape), fields[0].dtype, cfg.eb, cfg.eb_mode, cfg.radius)
+    live, snap, nb = {}, {}, {}
+
+    def on(k, r):
+        live[k], snap[k], nb[k] = r, (r.payload.clone(), r.code_lengths.clone(), r.outlier_idx.clone()), r.nbytes()
+        if k >= 1:   # the previous field's result is untouched by this one
+            p, lens, oi = snap[k - 1]
+            assert live[k - 1].payload.data_ptr() != r.payload.data_ptr()
+            assert torch.equal(live[k - 1].payload, p) and torch.equal(live[k - 1].code_lengths, lens)
+            assert torch.equal(live[k - 1].outlier_idx, oi)
+
+    sizes = codec.run(hosts, h_out, on_result=on)
+    assert sizes == [nb[k] for k in range(4)]

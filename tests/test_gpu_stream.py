@@ -65,3 +65,20 @@ def test_lr_bytes_round_trip(name):
     assert torch.equal(back.view(torch.uint8), direct.view(torch.uint8))
     err = (back.double() - x.double()).abs().max().item()
     assert err <= res.eb_abs
+
+
+def test_bytes_round_trip_slab_with_dim0_offset():
+    """A sharded slab (dim0_offset != 0, so its outlier indices are global) through the container: the
+    offset travels in the header and from_bytes scatters every outlier to its place."""
+    s = sz()
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal((24, 30, 100)).astype(np.float32)
+    x = torch.from_numpy(f).cuda()
+    mm = torch.tensor([-8.0, 8.0], dtype=torch.float64, device="cuda")   # a "global" range
+    res = s.regression_compress(x, 1e-3, "rel", radius=64, d_minmax=mm, dim0_offset=600,
+                                outlier_cap=x.numel()).finalize()
+    assert res.n_outliers > 100
+    direct = s.decompress(res)
+    assert ((direct.double() - x.double()).abs().max().item()) <= res.eb_abs
+    back = s.from_bytes(s.to_bytes(res, eb=1e-3, eb_mode="rel"))
+    assert torch.equal(back.view(torch.int32), direct.view(torch.int32))

@@ -426,3 +426,18 @@ def test_nonfinite_inputs_zero_predictor_and_outliers():
     assert np.all(np.abs(xr[ok].astype(np.float64) - f[ok]) <= res.eb_abs)
     with pytest.raises(ValueError):
         oracle.compress(f, 1e-3, "rel")   # REL with a non-finite range is a bad range (G14)
+
+
+@pytest.mark.parametrize("delta,flagged", [(2.0 ** -43, True), (5e-7, False), (0.0, True), (-2.0 ** -43, True)])
+def test_coefficient_tie_window_bounds(delta, flagged):
+    """The parity tie window (SURVEY 8(c) clarification 1): a constant 6^3 block of value
+    c has beta0 = c (P:57 with zero slopes) and, at ABS eb = 1, w0 = eb / 2 = 0.5, so beta0 / w0 =
+    2c.  c = 1.25 + delta puts it 2 delta from the half-integer 2.5: 2^-42 (~2.3e-13) lies inside the
+    1e-9 window and must exempt the block; 1e-6 lies outside and must not.  (c = 1.25 + 2^-43 and all
+    partial sums of the moments are exact doubles.)"""
+    f = np.full((6, 6, 6), 1.25 + delta, dtype=np.float64)
+    c = oracle.compress(f, 1.0, "abs", radius=32768)
+    assert abs(c.coef_raw.reshape(-1)[0] / 0.5 - 2.5) == pytest.approx(abs(2 * delta), rel=1e-6, abs=1e-15)
+    assert bool(c.block_exempt[0]) is flagged
+    assert c.counters["coef_tie_blocks"] == int(flagged)
+    assert c.counters["coef_near_ties"] == int(flagged)
