@@ -12,6 +12,7 @@ SRCS = [SRC, os.path.join(HERE, "csrc", "huffman.cu"), os.path.join(HERE, "csrc"
         os.path.join(HERE, "csrc", "metrics.cu"), os.path.join(HERE, "csrc", "coefcode.cu"),
         os.path.join(HERE, "csrc", "container.cu")]
 DEPS = [*SRCS, os.path.join(HERE, "csrc", "tile.cuh"), os.path.join(HERE, "csrc", "ptx.cuh"),
+        os.path.join(HERE, "csrc", "lr.cuh"),
         os.path.join(ROOT, "include", "sz3g.h")]
 LIB = os.path.join(HERE, "lib", "libsz3g.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -38,6 +39,17 @@ def build(force: bool = False, verbose: bool = False, src=None, out: str = LIB, 
     subprocess.run(cmd, check=True)
     os.replace(tmp, out)
     return out
+
+
+CHAOS_LIB = os.path.join(HERE, "lib", "chaos", "libsz3g.so")
+
+
+def chaos_lib(force: bool = False) -> str:
+    """The race-detection build: -DSZ3G_CHAOS=2000 (random 0..2 us delays at every pipeline hand-off,
+    csrc/ptx.cuh).  Test infrastructure only; the product loads LIB."""
+    if force or not os.path.exists(CHAOS_LIB) or any(os.path.getmtime(d) > os.path.getmtime(CHAOS_LIB) for d in DEPS):
+        build(force=True, out=CHAOS_LIB, defines=["-DSZ3G_CHAOS=2000"])
+    return CHAOS_LIB
 
 
 if __name__ == "__main__":

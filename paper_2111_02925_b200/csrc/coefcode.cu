@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "../../include/sz3g.h"
+#include "ptx.cuh"
 
 namespace {
 
@@ -37,14 +38,14 @@ __device__ V block_scan_excl(V v, V& excl, V* s_w) {
     if (lane >= o) x += y;
   }
   if (lane == 31) s_w[w] = x;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   V before = 0, total = 0;
   for (int i = 0; i < CC_T / 32; i++) {
     if (i < w) before += s_w[i];
     total += s_w[i];
   }
   excl = before + x - v;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   return total;
 }
 
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(CC_T) k_cc_scan(uint64_t* __restrict__ v, uint
   __shared__ uint64_t s_w[CC_T / 32];
   __shared__ uint64_t s_carry;
   if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   for (uint64_t b = 0; b < n; b += CC_T) {
     const uint64_t i = b + threadIdx.x;
     const uint64_t x = i < n ? v[i] : 0;
@@ -91,9 +92,9 @@ __global__ void __launch_bounds__(CC_T) k_cc_scan(uint64_t* __restrict__ v, uint
     const uint64_t tot = block_scan_excl<uint64_t>(x, ex, s_w);
     const uint64_t c = s_carry;
     if (i < n) v[i] = c + ex;
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     if (threadIdx.x == 0) s_carry = c + tot;
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
   }
   if (threadIdx.x == 0) {
     v[n] = s_carry;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(CC_T) k_cc_scan_seg(uint64_t* __restrict__ v, 
   __shared__ uint64_t s_carry;
   for (int ch = 0; ch < 4; ch++) {
     if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     uint64_t* w = v + (uint64_t)ch * tpc;
     for (uint64_t b = 0; b < tpc; b += CC_T) {
       const uint64_t i = b + threadIdx.x;
@@ -207,9 +208,9 @@ __global__ void __launch_bounds__(CC_T) k_cc_scan_seg(uint64_t* __restrict__ v, 
       const uint64_t tot = block_scan_excl<uint64_t>(x, ex, s_w);
       const uint64_t c = s_carry;
       if (i < tpc) w[i] = c + ex;
-      __syncthreads();
+      SZ3G_SYNCTHREADS();
       if (threadIdx.x == 0) s_carry = c + tot;
-      __syncthreads();
+      SZ3G_SYNCTHREADS();
     }
   }
 }

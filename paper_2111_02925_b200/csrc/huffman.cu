@@ -24,6 +24,7 @@
 #include <cstdio>
 
 #include "../../include/sz3g.h"
+#include "ptx.cuh"
 
 namespace {
 
@@ -77,7 +78,7 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& excl
     if (lane >= o) x += y;
   }
   if (lane == 31) s_warp[w] = x;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (w == 0) {
     uint32_t t = lane < HF_WARPS ? s_warp[lane] : 0u;
 #pragma unroll
@@ -87,11 +88,11 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& excl
     }
     s_warp[lane] = t;   // inclusive totals per warp
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const uint32_t before = w ? s_warp[w - 1] : 0u;
   excl = before + x - v;
   const uint32_t total = s_warp[HF_WARPS - 1];
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   return total;
 }
 
@@ -130,12 +131,12 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
   for (uint32_t i = tid; i < (1u << HF_LUT_BITS); i += HF_THREADS) dt->lut[i] = 0;
   if (tid < HF_MAXL) { dt->first[tid] = 0; dt->count[tid] = 0; dt->base[tid] = 0; }
   if (tid <= HF_MAXL) s_blc[tid] = 0;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (from_len) {
     // validate: every length <= max_len, at least one symbol, Kraft sum <= 1 (sum 2^(max_len - L) <= 2^max_len)
     __shared__ unsigned long long s_kraft;
     if (tid == 0) s_kraft = 0;
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     unsigned long long kr = 0;
     for (uint32_t s = tid; s < nsym; s += HF_THREADS) {
       const uint32_t L = lens[s];
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
       }
     }
     atomicAdd(&s_kraft, kr);
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     uint32_t nact = 0;
     for (int L = 1; L <= HF_MAXL; L++) nact += s_blc[L];
     if (s_bad || nact == 0 || s_kraft > (1ull << max_len)) {
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     const uint32_t hb = kmax ? 64u - (uint32_t)__clzll((long long)kmax) : 0u;
     atomicMax(&s_bits, hb);
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const bool bad = s_bad || n == 0 || (max_len < 32 && (1ull << max_len) < n);
   if (bad) {
     if (tid == 0) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     for (uint32_t i = i0; i < i1; i++) cnt[(src[i] >> sh) & 15u]++;
 #pragma unroll
     for (int d = 0; d < 16; d++) s_cnt[d * HF_THREADS + tid] = cnt[d];
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     // exclusive scan over (digit, thread) in digit-major order: thread t owns entries [16t, 16t + 16)
     uint32_t loc[16], sum = 0;
 #pragma unroll
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     block_excl_scan(sum, s_warp, base);
 #pragma unroll
     for (int e = 0; e < 16; e++) s_cnt[16 * tid + e] = base + loc[e];
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     uint32_t off[16];
 #pragma unroll
     for (int d = 0; d < 16; d++) off[d] = s_cnt[d * HF_THREADS + tid];
@@ -231,14 +232,14 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
       for (int e = 0; e < 16; e++) if (e == (int)d) o = off[e]++;
       dst[o] = k;
     }
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     uint64_t* t = src; src = dst; dst = t;
   }
   // sorted keys in src; leaf weights in listA (level max_len list)
   uint64_t* leaves = dst;   // reuse the other sort buffer for the leaf weights
   for (uint32_t i = tid; i < n; i += HF_THREADS) leaves[i] = src[i] >> 16;
   for (uint32_t i = tid; i < n; i += HF_THREADS) S.listA[i] = leaves[i];
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
 
   // (C) package-merge: list[l] = merge(leaves, packages of list[l + 1]), l = max_len - 1 .. 1
   uint64_t* A = S.listA;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     const uint32_t np = lenA / 2;
     if (tid == 0) s_np[l] = np;
     for (uint32_t j = tid; j < np; j += HF_THREADS) pk[j] = A[2 * j] + A[2 * j + 1];
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     const uint32_t tot = n + np;
     const uint32_t oper = (tot + HF_THREADS - 1) / HF_THREADS;
     const uint32_t k0 = min(tot, tid * oper), k1 = min(tot, k0 + oper);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
         else B[k] = pk[b++];
       }
     }
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     uint64_t* t = A; A = B; B = t;
     lenA = tot;
     if (l == 1) break;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
       m = 2 * (m - c);
     }
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   // (E) lengths of the sorted leaves: len(i) = #{l : i < c[l]}
   for (uint32_t i = tid; i < n; i += HF_THREADS) {
     uint32_t L = 0;
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     atomicAdd(&s_blc[L], 1u);
   }
   }   // !from_len
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   // (F) canonical codewords: first code per length (DEFLATE form of H3), then per-symbol rank
   // among the symbols of its length in symbol order
   if (tid == 0) {
@@ -303,11 +304,11 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
       if (L > HF_LUT_BITS) cum += s_blc[L];
     }
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   uint32_t* s_run = s_cnt;            // running count per length over earlier rounds
   uint32_t* s_wl = s_cnt + 64;        // [HF_WARPS][32 lengths] counts of the current round
   for (int i = tid; i < 64 + HF_WARPS * 32; i += HF_THREADS) s_cnt[i] = 0;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const int lane = tid & 31, wid = tid >> 5;
   uint16_t* syms = reinterpret_cast<uint16_t*>(dt + 1);
   for (uint32_t r0 = 0; r0 < nsym; r0 += HF_THREADS) {
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
     const uint32_t peers = __match_any_sync(0xffffffffu, L);
     const uint32_t rank_w = __popc(peers & ((1u << lane) - 1u));
     if (lane == 31 - __clz(peers)) s_wl[wid * 32 + L] = __popc(peers);   // the group's highest lane
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     if (L > 0) {
       uint32_t before = s_run[L];
       for (int w = 0; w < wid; w++) before += s_wl[w * 32 + L];
@@ -329,13 +330,13 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
         syms[dt->base[L] + (cw - s_first[L])] = (uint16_t)s;
       }
     }
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     if (tid < 32) {   // fold this round's per-warp counts into the running counts, clear them
       uint32_t add = 0;
       for (int w = 0; w < HF_WARPS; w++) { add += s_wl[w * 32 + tid]; s_wl[w * 32 + tid] = 0; }
       s_run[tid] += add;
     }
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
   }
 }
 
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_sums(const uint64_t* __restrict
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (threadIdx.x == 0) {
     uint64_t t = 0;
     for (int w = 0; w < SCAN_T / 32; w++) t += s[w];
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_top(uint64_t* __restrict__ sums
   __shared__ uint64_t s_w[SCAN_T / 32];
   __shared__ uint64_t s_carry;
   if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (uint64_t b = 0; b < nb; b += SCAN_T) {
     const uint64_t i = b + threadIdx.x;
@@ -434,14 +435,14 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_top(uint64_t* __restrict__ sums
       if (lane >= o) x += y;
     }
     if (lane == 31) s_w[w] = x;
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     uint64_t before = 0;
     for (int k = 0; k < w; k++) before += s_w[k];
     const uint64_t carry = s_carry;
     if (i < nb) sums[i] = carry + before + x - v;
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
     if (threadIdx.x == SCAN_T - 1) s_carry = carry + before + x;
-    __syncthreads();
+    SZ3G_SYNCTHREADS();
   }
   if (threadIdx.x == 0) sums[nb] = s_carry;
 }
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_apply(uint64_t* __restrict__ v,
     if (lane >= o) x += y;
   }
   if (lane == 31) s_w[w] = x;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   uint64_t before = sums[blockIdx.x];
   for (int k = 0; k < w; k++) before += s_w[k];
   before += x - sum;
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
       const uint4* g = reinterpret_cast<const uint4*>(codes + e0);
       for (uint32_t i = lane; i < ENC_MAX_CHUNK / 8; i += 32)
         sc[swz(i)] = 8 * i < m ? __ldg(g + i) : make_uint4(0, 0, 0, 0);
-      __syncwarp();
+      SZ3G_SYNCWARP();
     }
     if (fullc) {
 #pragma unroll 2
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
       if (lane >= o) incl += y;
     }
     const uint32_t b0 = incl - bits;   // first bit of this lane inside the chunk
-    __syncwarp();                      // the image is zeroed before any lane writes into it
+    SZ3G_SYNCWARP();                      // the image is zeroed before any lane writes into it
     // pack: the buffer starts with the (b0 % 32) bits of the previous lane as zeros, so every emitted
     // word is a whole word of the chunk image; the first and the last are shared -> atomicOr
     Packer pk{0, b0 & 31u, b0 >> 5, true};
@@ -595,9 +596,9 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_huff_encode(const uint16_t* 
       for (uint32_t e = a0; e < a1; e++) pk.put(look(codes[e0 + e]), img);
     }
     if (pk.nbuf > 0 && bits > 0) atomicOr(&img[pk.wi], (uint32_t)(pk.buf << (32 - pk.nbuf)));
-    __syncwarp();
+    SZ3G_SYNCWARP();
     for (uint32_t i = lane; i < nwords; i += 32) payload[w0 + i] = img[i];
-    __syncwarp();
+    SZ3G_SYNCWARP();
   }
 }
 
@@ -646,10 +647,10 @@ __device__ __forceinline__ void ew_load_chunk(const uint16_t* __restrict__ codes
 __device__ __forceinline__ void ew_restage(const uint4 (&nx)[8], uint4* st, int lane, uint4 (&u)[8]) {
 #pragma unroll
   for (int v = 0; v < 8; v++) st[swz(v * 32 + lane)] = nx[v];
-  __syncwarp();
+  SZ3G_SYNCWARP();
 #pragma unroll
   for (int v = 0; v < 8; v++) u[v] = st[swz(lane * 8 + v)];
-  __syncwarp();
+  SZ3G_SYNCWARP();
 }
 
 __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_chunk_words_full(const uint16_t* __restrict__ codes,
@@ -667,7 +668,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_chunk_words_full(cons
     const uint32_t L = lo + i < nsym ? __ldg(tab + lo + i) >> 24 : 0u;
     s_len[i] = (uint8_t)(L ? L : 0x80u);
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const int lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * EW_WARPS;
   uint64_t c = (uint64_t)blockIdx.x * EW_WARPS + (threadIdx.x >> 5);
@@ -755,7 +756,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
     const uint32_t t = lo + i < nsym ? __ldg(tab + lo + i) : 0u;
     s_tab[i] = ((t >> 24) << 16) | (t & 0xffffu);
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const uint64_t nw = (uint64_t)gridDim.x * EW_WARPS;
   uint64_t c = (uint64_t)blockIdx.x * EW_WARPS + wl;
   if (c >= nfull) return;
@@ -815,11 +816,11 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
     }
     // the partial last word continues in the next lane, which has stored its part there (its first
     // word, the upper bits zero); lane 31's is the chunk's zero-padded last word
-    __syncwarp();
+    SZ3G_SYNCWARP();
     const uint32_t nhead = (nb && lane < 31) ? dst[wi] : 0u;
-    __syncwarp();
+    SZ3G_SYNCWARP();
     if (nb) dst[wi] = (uint32_t)(acc << (32 - nb)) | nhead;
-    __syncwarp();
+    SZ3G_SYNCWARP();
     // out
     const uint32_t nwords = (uint32_t)(w1 - w0);
     if (w1 > cap) {
@@ -836,7 +837,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32, 1) k_huff_encode_full(const uin
         for (uint32_t i = a + lane; i < e_; i += 32) gout[i] = img[i];
       }
     }
-    __syncwarp();
+    SZ3G_SYNCWARP();
   }
 }
 
@@ -914,7 +915,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
     s_ljl[l] = (l >= 1 && l <= max_len) ? (uint32_t)(((uint64_t)dt->first[l] + dt->count[l]) << (16 - l))
                                         : (l > max_len ? 0x10000u : 0u);
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   uint32_t* ring_w = s_ring + wl * 32 * RING_P;
   uint32_t* ring = ring_w + lane * RING_P;
@@ -967,7 +968,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
         }
         if (need) d.filled += 16;
       }
-      __syncwarp();
+      SZ3G_SYNCWARP();
     }
     if (e == 0) {   // prime the window: 64 bits
       dec_refill(d, ring);
@@ -1010,7 +1011,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
         out[h >> 1] = a | (b << 16);
       }
     }
-    __syncwarp();
+    SZ3G_SYNCWARP();
     // (3) write the round's codes: one chunk row (64 B) per half-warp pass
     for (int j = 0; j < 32; j += 2) {
       const int src = j + half;
@@ -1025,7 +1026,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_huff_decode(const uint32_t* 
         if (k + 1 < mj) codes[ej + k + 1] = (uint16_t)(v >> 16);
       }
     }
-    __syncwarp();
+    SZ3G_SYNCWARP();
   }
   if (live && (bad || d.consumed > d.nwords * 32u)) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
 }
@@ -1066,7 +1067,10 @@ __device__ __forceinline__ void df_copy16(uint32_t s_dst, const uint32_t* __rest
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s_dst), "l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void df_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void df_wait2() { asm volatile("cp.async.wait_group 2;\n" ::: "memory"); }
+__device__ __forceinline__ void df_wait2() {
+  asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+  sz3g::ptx::chaos_delay();
+}
 
 // top the ring up towards DF_RING = 16 words ahead of the read position (<= K copies of 4 words) and
 // wait for the copies requested before the previous call.  Every quarter round (8 codes, <= 4 words
@@ -1135,7 +1139,7 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
     s_ljl[l] = (l >= 1 && l <= max_len) ? (uint32_t)(((uint64_t)dt->first[l] + dt->count[l]) << (16 - l))
                                         : (l > max_len ? 0x10000u : 0u);
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const uint64_t c0 = ((uint64_t)blockIdx.x * DF_WARPS + wl) * 32;
   if (c0 >= nfull) return;
@@ -1196,14 +1200,14 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
       const uint32_t i = 4 * lane + j;
       so[i ^ ((i >> 3) & 3u)] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
     }
-    __syncwarp();
+    SZ3G_SYNCWARP();
 #pragma unroll
     for (int t = 0; t < 4; t++) {
       const uint32_t i = 32 * t + lane, r = i >> 2, j = i & 3u;
       const uint4 v = so[i ^ ((i >> 3) & 3u)];
       if (c0 + r < nfull) reinterpret_cast<uint4*>(codes + (c0 + r) * EW_CHUNK + e)[j] = v;
     }
-    __syncwarp();
+    SZ3G_SYNCWARP();
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   const uint64_t consumed = 32ull * d.nref - d.avail;

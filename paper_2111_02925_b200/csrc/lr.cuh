@@ -135,7 +135,7 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ ox, uint64_t osi, 
                                         const CompressOut<T>& o, uint8_t* __restrict__ flags, const HistSmem& hs,
                                         const CUtensorMap* tm_c) {
   const int h = L.h;
-  __syncwarp();
+  SZ3G_SYNCWARP();
   // L5: the block's two lanes sum their costs
   costR += __shfl_xor_sync(0xffffffffu, costR, 1);
   costL += __shfl_xor_sync(0xffffffffu, costL, 1);
@@ -179,10 +179,10 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ ox, uint64_t osi, 
         }
         has_out |= valid && code == 0u;
       }
-  __syncwarp();
+  SZ3G_SYNCWARP();
   if (TMA_OUT) {
     ptx::fence_proxy_async_smem();
-    __syncwarp();
+    SZ3G_SYNCWARP();
     if ((threadIdx.x & 31) == 0) {
       ptx::tma_store_3d(tm_c, sR, (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
       ptx::bulk_commit();
@@ -190,7 +190,7 @@ __device__ __forceinline__ void lr_emit(const T* __restrict__ ox, uint64_t osi, 
   }
   if (o.hist) rare_path<T, true, BS>(ox, osi, osj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
   else rare_path<T, false, BS>(ox, osi, osj, sR, BS * TK, TK, 0, 0, L, has_out, tc, g, o, hs);
-  __syncwarp();
+  SZ3G_SYNCWARP();
 }
 
 // The exact definitions for one element, out of line (the fast routine's rare fallback)
@@ -448,14 +448,14 @@ __global__ void __launch_bounds__(W * 32, 1)
     const uint32_t s = k % D, ph = (k / D) & 1u;
     const TileCoord tc = decode_tile(t, g);
     if (lane == 0) ptx::bulk_wait_read0();   // the previous tile's code store has read sR
-    __syncwarp();
+    SZ3G_SYNCWARP();
     ptx::mbar_wait(&bar[s], ph);
     const T* xs = ring + (size_t)s * TILE_ELEMS;
     const LrSlabL sL{nullptr, reinterpret_cast<uint32_t*>(ring + (size_t)s * TILE_ELEMS), (int)(sizeof(T) / 4)};
     const T* xg = x + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
     if (tile_full(tc, g)) lr_compress_tile<T, true, true, true>(xs, BS * TK, TK, xg, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
     else lr_compress_tile<T, true, false, true>(xs, BS * TK, TK, xg, sR, sL, tc, g, K, a.R, o, flags, hs, &tm_c);
-    __syncwarp();
+    SZ3G_SYNCWARP();
     if (lane == 0) {   // every lane's reads of the stage are done: refill it with tile k + D
       const uint64_t t2 = tl.tile();
       if (t2 < g.ntiles) {
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     }
   }
   if (lane == 0) ptx::bulk_wait0();
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (o.hist) hist_flush(hs, o.hist);
   overflow_check(a, o.ocount, o.cap);
 }
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(LR_PW * 32) k_lr_compress_plain(const T* __res
     lr_compress_tile<T, false, false, false>(x + off, g.n1 * g.n2, g.n2, x + off, sR, sL, tc, g, K, a.R, o, flags, hs,
                                              nullptr);
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (o.hist) hist_flush(hs, o.hist);
   overflow_check(a, o.ocount, o.cap);
 }
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(W * 32, SZ3G_LRD_MINB)
     } else {
       lr_decompress_tile<T, false, true, int64_t>(cs, 0, 0, coef, flags, xo, tc, g, K, a.R);
     }
-    __syncwarp();
+    SZ3G_SYNCWARP();
     if (lane == 0) {
       const uint64_t t2 = tl.tile();
       if (t2 < g.ntiles) {
@@ -1085,11 +1085,11 @@ __device__ __forceinline__ void lr_pair_tile(const T* __restrict__ xs, uint16_t*
             sR[s] = sL[s];
           }
     }
-    __syncwarp();
+    SZ3G_SYNCWARP();
   }
   if (hist) has_out = lr_pair_hist<true, FULL>(sR, i0, L, hs, o.hist, hb, sink);
   else has_out = lr_pair_hist<false, FULL>(sR, i0, L, hs, o.hist, hb, sink);
-  __syncwarp();
+  SZ3G_SYNCWARP();
   if (hist) lr_rare_planes<T, true>(xs, sR, i0, L, has_out, tc, g, o, hs);
   else lr_rare_planes<T, false>(xs, sR, i0, L, has_out, tc, g, o, hs);
   ptx::fence_proxy_async_smem();   // this warp's code writes, before the pair's TMA store
@@ -1163,7 +1163,7 @@ __global__ void __launch_bounds__(NPAIR * 64, 1)
     }
   }
   if (loader) ptx::bulk_wait0();
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (o.hist) hist_flush(hs, o.hist);
   overflow_check(a, o.ocount, o.cap);
 }

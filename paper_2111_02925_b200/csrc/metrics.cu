@@ -13,6 +13,7 @@
 #include <cstdint>
 
 #include "../../include/sz3g.h"
+#include "ptx.cuh"
 
 namespace {
 
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(ME_T) k_error_partials(const T* __restrict__ x
   }
   const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) { s[0][w] = mx; s[1][w] = sq; s[2][w] = cnt; }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (threadIdx.x == 0) {
     for (int i = 1; i < ME_T / 32; i++) {
       mx = (s[0][i] > mx || s[0][i] != s[0][i]) ? s[0][i] : mx;

@@ -174,5 +174,19 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// warp / CTA barriers with the chaos delay in front (a no-op in the normal build): a lane or warp
+// that reaches the barrier late exposes a read of data that the barrier does not order
+__device__ __forceinline__ void chaos_syncwarp() {
+  chaos_delay();
+  __syncwarp();
+}
+__device__ __forceinline__ void chaos_syncthreads() {
+  chaos_delay();
+  __syncthreads();
+}
+
 }  // namespace ptx
 }  // namespace sz3g
+
+#define SZ3G_SYNCWARP() ::sz3g::ptx::chaos_syncwarp()
+#define SZ3G_SYNCTHREADS() ::sz3g::ptx::chaos_syncthreads()

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_value_range(const T* __restrict__ x, ui
   __shared__ unsigned long long s_lo[8], s_hi[8];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) { s_lo[w] = klo; s_hi[w] = khi; }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (threadIdx.x == 0) {
     for (int i = 1; i < (int)(blockDim.x >> 5); i++) { klo = min(klo, s_lo[i]); khi = max(khi, s_hi[i]); }
     atomicMin(&keys[0], klo);
@@ -202,7 +202,7 @@ __device__ __forceinline__ bool cta_consts(const KArgs& a, Consts* s_k, int* s_o
       if (a.d_eb_abs) *a.d_eb_abs = ok ? K.eb_abs : __longlong_as_double(0x7ff8000000000000ll);
     }
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   return *s_ok != 0;
 }
 
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(128) k_compress_plain(const T* __restrict__ x,
     const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
     compress_tile_dispatch<T, false, HIST, BETA>(x + off, g.n1 * g.n2, g.n2, o.codes + off, g.n1 * g.n2, g.n2, tc, g, K, a.R, o, hs);
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (HIST) hist_flush(hs, o.hist);
   overflow_check(a, o.ocount, o.cap);
 }
@@ -258,7 +258,7 @@ __device__ __forceinline__ void range_epilogue(MinMax<T> mm, bool nan, unsigned 
     khi = max(khi, __shfl_xor_sync(0xffffffffu, khi, o));
   }
   if (l == 0) { s_red[2 * w] = klo; s_red[2 * w + 1] = khi; }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (threadIdx.x == 0) {
     for (int i = 1; i < (int)(blockDim.x >> 5); i++) {
       klo = min(klo, (unsigned long long)s_red[2 * i]);
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     for (int s = 0; s < W * D; s++) ptx::mbar_init(&full[s], 1);
     ptx::fence_mbar_init();
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const Geo& g = a.g;
   T* ring = reinterpret_cast<T*>(smem) + (size_t)warp * D * TILE_ELEMS;
   uint64_t* bar = full + warp * D;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     const T* xs = ring + (size_t)s * TILE_ELEMS;
     if (tile_full(tc, g)) nan |= analyze_tile<T, true, true>(xs, BS * TK, TK, tc, g, beta, mm);
     else nan |= analyze_tile<T, true, false>(xs, BS * TK, TK, tc, g, beta, mm);
-    __syncwarp();
+    SZ3G_SYNCWARP();
     if (lane == 0) {   // every lane's reads of the stage are done: refill it with tile k + D
       const uint64_t t2 = tl.tile();
       if (t2 < g.ntiles) {
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
           if (tfull) moment_warp_tile<T, true>(xs, &slots[s], tc, g, K, o);
           else moment_warp_tile<T, false>(xs, &slots[s], tc, g, K, o);
         }
-        __syncwarp();
+        SZ3G_SYNCWARP();
         if (lane == 0) ptx::mbar_arrive(&ready[s]);
         if (SELF && lane == 0) {   // then load tile n = k + D - 1 once the quantise warps release tile n - D
           const uint32_t n = k + D - 1, sn = grp * D + n % D;
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
             tp.next();
           }
         }
-        __syncwarp();
+        SZ3G_SYNCWARP();
       }
     } else {
       // ---------------- quantise warp q: rows [j0, j0 + P)
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
           tfull = tile_full(tc, g);
         }
         if (codes_tma && lane == 0) ptx::bulk_wait_read0();   // previous slab store finished reading
-        __syncwarp();
+        SZ3G_SYNCWARP();
         ptx::mbar_wait(&full[s], ph);
         if (!SELF) {
           const uint4 h = hdr[s];
@@ -692,24 +692,24 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
           if (tfull) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
           else quant_warp_tile<T, HIST, false, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
         }
-        __syncwarp();
+        SZ3G_SYNCWARP();
         if (lane == 0) ptx::mbar_arrive(&empty[s]);
         if (codes_tma) {
           ptx::fence_proxy_async_smem();
-          __syncwarp();
+          SZ3G_SYNCWARP();
           if (lane == 0) {
             ptx::tma_store_3d(&tm_c, slab, (int)(tc.c * TK), (int)(tc.b * BS + j0), (int)(tc.a * BS));
             ptx::bulk_commit();
           }
         } else {
           store_code_slab<P>(slab, o.codes, tc, g, j0);
-          __syncwarp();
+          SZ3G_SYNCWARP();
         }
       }
       if (codes_tma && lane == 0) ptx::bulk_wait0();
     }
   }
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   if (HIST) hist_flush(hs, o.hist);
   overflow_check(a, o.ocount, o.cap);
 }
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
       const TileCoord tc = decode_tile(t, g);
       T* myout = myout0 + (size_t)(OB > 1 ? k % OB : 0) * (BS * P * TK);
       if (lane == 0) ptx::bulk_wait_read<OB - 1>();   // the store that last used this slab has read it
-      __syncwarp();
+      SZ3G_SYNCWARP();
       ptx::mbar_wait(&full[s], ph);
       const uint8_t* st = stages + (size_t)s * L_::stage_bytes;
       const uint16_t* cst = reinterpret_cast<const uint16_t*>(st);
@@ -826,10 +826,10 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
       decode_coefs(cc, K, bh);
       if (full_tile) decompress_rows<T, true, true, true, P>(cst, BS * TK, TK, myout, 0, 0, j0, L, bh, K, a.R);
       else decompress_rows<T, true, true, false, P>(cst, BS * TK, TK, myout, 0, 0, j0, L, bh, K, a.R);
-      __syncwarp();
+      SZ3G_SYNCWARP();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);   // this warp no longer reads the stage
       ptx::fence_proxy_async_smem();
-      __syncwarp();
+      SZ3G_SYNCWARP();
       if (lane == 0) {
         ptx::tma_store_3d(&tm_x, myout, (int)(tc.c * TK), (int)(tc.b * BS + j0), (int)(tc.a * BS));
         ptx::bulk_commit();
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ 
   hs.W = 0;
   for (uint32_t b = threadIdx.x; b < hs.nwin; b += blockDim.x) s_win[b] = 0u;
   if (threadIdx.x == 0) *s_zero = 0u;
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
   auto add = [&](uint32_t c) {
     if (c >= nb) return;
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ 
     done = nv * 8;
   }
   for (uint64_t e = done + tid; e < n; e += nth) add(codes[e]);
-  __syncthreads();
+  SZ3G_SYNCTHREADS();
   hist_flush(hs, hist);
 }
 

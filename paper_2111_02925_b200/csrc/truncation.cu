@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "../../include/sz3g.h"
+#include "ptx.cuh"
 
 namespace {
 
@@ -140,14 +141,14 @@ __global__ void __launch_bounds__(256) k_trunc_decompress(const uint8_t* __restr
         const int i = lane * S + q;
         st[i ^ ((i >> 3) & 3)] = q4[q];
       }
-      __syncwarp();
+      SZ3G_SYNCWARP();
       uint4* dst = reinterpret_cast<uint4*>(x + gb * 16 * S);
 #pragma unroll
       for (int q = 0; q < S; q++) {
         const int i = q * 32 + lane;
         __stcs(dst + i, st[i ^ ((i >> 3) & 3)]);
       }
-      __syncwarp();
+      SZ3G_SYNCWARP();
     } else if (g < ng) {
       uint4* dst = reinterpret_cast<uint4*>(x + g * 16 * S);
 #pragma unroll
