@@ -68,6 +68,8 @@ def parse():
                          "radius R (stress variant); '' for none")
     ap.add_argument("--config-steps", type=int, default=10)
     ap.add_argument("--no-ties", action="store_true", help="skip the reported-counter pass (sz3g_tie_counts)")
+    ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step from CUDA graphs (auto: at N = 1; NCCL collectives can be captured, gloo not)")
     return ap.parse_args()
 
 
@@ -475,7 +477,7 @@ def config_leg(sz3g, spec, peaks, steps, warmup, flush_buf, x=None):
     N, s = x.numel(), x.element_size()
     NB = sz3g.num_blocks(x.shape)
     cap = bench_outlier_cap(N) if R >= 1024 else N
-    rt = RoundTrip(x, cfg.eb, cfg.eb_mode, R, outlier_cap=cap)
+    rt = RoundTrip(x, cfg.eb, cfg.eb_mode, R, outlier_cap=cap).capture()   # CUDA graphs: no host gaps
     stream = rt.stream
     for _ in range(warmup):
         rt.step()
@@ -505,7 +507,8 @@ def config_leg(sz3g, spec, peaks, steps, warmup, flush_buf, x=None):
            "quantize_roofline": roof(b["quantize"], qua, peaks["hbm_gbs"]),
            "analyze_roofline": roof(b["analyze"], ana, peaks["hbm_gbs"]),
            "decompress_roofline": roof(b["decompress"], dec, peaks["hbm_gbs"]),
-           "l2": "flushed (2x L2 write) before every step", "steps": steps, "warmup": warmup}
+           "l2": "flushed (2x L2 write) before every step", "steps": steps, "warmup": warmup,
+           "launch": "each segment of the step replayed from a CUDA graph (RoundTrip.capture)"}
     del rt
     torch.cuda.empty_cache()
     return out
@@ -532,6 +535,9 @@ def main():
     NB_local = sz3g.num_blocks(x.shape)
     two_pass = args.path == "two-pass"
     rt = RoundTrip(x, cfg.eb, cfg.eb_mode, cfg.radius, dim0_offset=a0, path=args.path)
+    graphs = args.graphs == "on" or (args.graphs == "auto" and world == 1)
+    if graphs:
+        rt.capture()          # each segment of the step replayed from a CUDA graph (no host gaps)
     bufs, out, stream = rt.bufs, rt.out, rt.stream
 
     for _ in range(max(3, args.warmup)):
@@ -547,7 +553,8 @@ def main():
             rt.step(recs[k])
         t_end.record(stream)
         barrier(world)
-    launches = sum_over_ranks(sz3g.launch_count() - l0, world)
+    launches = sz3g.launch_count() - l0 if not graphs else rt.launches_per_step * args.steps
+    launches = sum_over_ranks(launches, world)
     ms_total = max_over_ranks(t_start.elapsed_time(t_end), world)
     ms_step = ms_total / args.steps
     # per-kernel times: mean over the timed steps on this rank, then the max over ranks
@@ -675,6 +682,7 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "shape": list(shape), "eb_rel": cfg.eb,
                        "radius": cfg.radius, "block": 6, "parallelism": f"slabs{world}",
                        "dist_backend": args.dist_backend if world > 1 else None,
+                       "launch": "CUDA graph per step segment" if graphs else "eager (one host call per kernel)",
                        "l2": "inputs (16 GiB) larger than L2; no flush" if N_global * s > (1 << 30)
                        else "input smaller than 1 GiB: NOT flushed between steps (rehearsal shape)"},
             "roofline": {"bound": "hbm", "kernel": "k_compress_tma" + ("<beta in>" if two_pass else ""),

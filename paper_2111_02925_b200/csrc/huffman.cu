@@ -1053,12 +1053,18 @@ constexpr int DF_WARPS = 8, DF_ROUND = 32, DF_RING = 16, DF_RING_W = 20;   // ri
 #endif
 
 struct DfLane {
-  uint64_t buf;     // left-aligned bit window
-  uint32_t avail;   // valid bits in buf
+  uint32_t hi, lo;  // left-aligned 64-bit bit window (hi = its upper 32 bits)
+  uint32_t avail;   // valid bits in the window
   uint32_t rpos;    // next ring word to read (mod DF_RING), counted from the aligned chunk start
   uint32_t fpos;    // ring words requested so far (16-byte copies of 4 words)
   uint32_t nref;    // words appended to the window
 };
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 
 __device__ __forceinline__ void df_copy16(uint32_t s_dst, const uint32_t* __restrict__ payload, uint64_t p,
                                           uint64_t lim) {
@@ -1091,31 +1097,40 @@ __device__ __forceinline__ void df_topup(DfLane& d, uint32_t s_ring, const uint3
   df_wait2();
 }
 
-// append one ring word when the window holds <= 32 bits
-__device__ __forceinline__ void df_refill(DfLane& d, const uint32_t* ring) {
-  if (d.avail <= 32) {
-    const uint32_t w = ring[d.rpos & (DF_RING - 1)];
-    d.buf |= (uint64_t)w << (32u - d.avail);
-    d.avail += 32u;
-    d.nref++;
-    d.rpos++;
-  }
+// append one ring word when the window holds <= 32 bits (then every valid bit is in hi and lo = 0):
+// branch-free, a 32-bit shared address, clamped funnel shifts (a shift by 32 gives 0)
+__device__ __forceinline__ void df_refill(DfLane& d, uint32_t s_ring) {
+  const bool take = d.avail <= 32u;
+  const uint32_t w = lds32(s_ring + 4u * (d.rpos & (DF_RING - 1)));
+  const uint32_t add_hi = __funnelshift_rc(w, 0u, d.avail);          // w >> avail (0 at avail = 32)
+  const uint32_t new_lo = __funnelshift_lc(0u, w, 32u - d.avail);    // w << (32 - avail) (0 at avail = 0)
+  d.hi = take ? (d.hi | add_hi) : d.hi;
+  d.lo = take ? new_lo : d.lo;
+  d.avail += take ? 32u : 0u;
+  d.nref += take ? 1u : 0u;
+  d.rpos += take ? 1u : 0u;
+}
+
+// shift the window left by L (<= 16) bits
+__device__ __forceinline__ void df_shift(DfLane& d, uint32_t L) {
+  d.hi = __funnelshift_l(d.lo, d.hi, L);
+  d.lo <<= L;
+  d.avail -= L;
 }
 
 // one code, any length (LUT, else the canonical search of k_huff_decode's dec_one)
-__device__ __forceinline__ uint32_t df_code(DfLane& d, const uint32_t* s_lut, const uint32_t* s_ljl,
+__device__ __forceinline__ uint32_t df_code(DfLane& d, uint32_t s_lut, const uint32_t* s_ljl,
                                             const uint32_t* s_first, const uint32_t* s_base,
                                             const uint16_t* __restrict__ syms, uint32_t maxl, bool& bad) {
-  const uint32_t top = (uint32_t)(d.buf >> 48);
-  const uint32_t ent = s_lut[top >> (16 - HF_LUT_BITS)];
+  const uint32_t top = d.hi >> 16;
+  const uint32_t ent = lds32(s_lut + 4u * (top >> (16 - HF_LUT_BITS)));
   uint32_t L = ent >> 16, sym = ent & 0xffffu;
   if (ent == 0u) {
     L = HF_LUT_BITS + 1 + (top >= s_ljl[13] ? 1u : 0u) + (top >= s_ljl[14] ? 1u : 0u) + (top >= s_ljl[15] ? 1u : 0u);
     if (L > maxl || top >= s_ljl[L]) { bad = true; L = 1; sym = 0; }
     else sym = syms[s_base[L] + (top >> (16 - L)) - s_first[L]];
   }
-  d.buf <<= L;
-  d.avail -= L;
+  df_shift(d, L);
   return sym;
 }
 
@@ -1145,8 +1160,9 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
   if (c0 >= nfull) return;
   const uint16_t* syms = reinterpret_cast<const uint16_t*>(dt + 1);
   uint4* so = s_out + wl * 128;
-  const uint32_t* ring = s_rings + threadIdx.x * DF_RING_W;
-  const uint32_t s_ring = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t s_ring = (uint32_t)__cvta_generic_to_shared(s_rings + threadIdx.x * DF_RING_W);
+  // &s_lut[idx] = lut_sh + 4 idx; the index is the window's top 12 bits: (hi >> 20) << 2
+  const uint32_t lut_sh = (uint32_t)__cvta_generic_to_shared(s_lut);
   const bool live = c0 + lane < nfull;
   const uint64_t c = live ? c0 + lane : nfull - 1;   // a dead lane decodes the last full chunk again, unstored
   const uint64_t lim = offs[nch];
@@ -1155,13 +1171,13 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
   const uint64_t a0 = w0 & ~3ull;
   d.rpos = (uint32_t)(w0 & 3u);
   d.fpos = 0;
-  d.buf = 0;
+  d.hi = d.lo = 0;
   d.avail = 0;
   d.nref = 0;
   df_topup<DF_RING / 4>(d, s_ring, payload, a0, lim);   // 16 words
   asm volatile("cp.async.wait_all;\n" ::: "memory");
-  df_refill(d, ring);                      // prime 64 bits
-  df_refill(d, ring);
+  df_refill(d, s_ring);                      // prime 64 bits
+  df_refill(d, s_ring);
   bool bad = false;
   const uint32_t maxl = max_len;
   for (uint32_t e = 0; e < EW_CHUNK; e += DF_ROUND) {
@@ -1169,22 +1185,21 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
 #pragma unroll
     for (int h = 0; h < 16; h++) {
       if ((h % 4 == 0) && (h || e)) df_topup<1>(d, s_ring, payload, a0, lim);
-      const uint64_t win0 = d.buf;
-      const uint32_t ea = s_lut[(uint32_t)(win0 >> (64 - HF_LUT_BITS))];
+      // two codes (<= 32 bits, the window holds > 32): LUT entry (len << 16) | sym, 0 = longer than the LUT
+      const uint32_t ea = lds32(lut_sh + ((d.hi >> (32 - HF_LUT_BITS)) << 2));
       const uint32_t la = ea >> 16;
-      const uint64_t win1 = win0 << la;
-      const uint32_t eb = s_lut[(uint32_t)(win1 >> (64 - HF_LUT_BITS))];
-      const uint32_t lb = eb >> 16;
+      const uint32_t hi1 = __funnelshift_l(d.lo, d.hi, la);
+      const uint32_t eb = lds32(lut_sh + ((hi1 >> (32 - HF_LUT_BITS)) << 2));
       if (__any_sync(0xffffffffu, ea == 0u || eb == 0u)) {
-        const uint32_t a = df_code(d, s_lut, s_ljl, s_first, s_base, syms, maxl, bad);
-        const uint32_t b = df_code(d, s_lut, s_ljl, s_first, s_base, syms, maxl, bad);
+        const uint32_t a = df_code(d, lut_sh, s_ljl, s_first, s_base, syms, maxl, bad);
+        const uint32_t b = df_code(d, lut_sh, s_ljl, s_first, s_base, syms, maxl, bad);
         o[h] = a | (b << 16);
       } else {
-        d.buf = win1 << lb;
-        d.avail -= la + lb;
-        o[h] = (ea & 0xffffu) | (eb << 16);
+        const uint32_t lb = eb >> 16;
+        df_shift(d, la + lb);   // la + lb <= 24
+        o[h] = __byte_perm(ea, eb, 0x5410);   // (ea & 0xffff) | (eb << 16)
       }
-      df_refill(d, ring);
+      df_refill(d, s_ring);
     }
     if (SZ3G_DF_DIRECT) {
       if (live) {

@@ -1120,7 +1120,19 @@ uint32_t chunk_tiles(bool decompress) { return (uint32_t)std::max<int64_t>(1, tu
 int compress_cfg() { return (int)tuning("CCFG"); }
 uint32_t prefetch_tiles() { return (uint32_t)std::max<int64_t>(0, tuning("PF")); }
 constexpr int CN32 = 5, CQ32 = 2, CD32 = 2;  // f32 compress: 5 groups x (1 moment + 2 quantise warps) + producer = 16 warps
-constexpr int CN64 = 3, CQ64 = 3, CD64 = 2;  // f64 compress: 3 groups x (1 + 3) warps + producer = 13 warps
+#ifndef SZ3G_CN64
+#define SZ3G_CN64 3
+#endif
+#ifndef SZ3G_CQ64
+#define SZ3G_CQ64 3
+#endif
+#ifndef SZ3G_CD64
+#define SZ3G_CD64 2
+#endif
+#ifndef SZ3G_CNOR64
+#define SZ3G_CNOR64 1   // two-pass f64: no role-0 warp, the quantise warps derive their coefficients (A/B: 76.1 vs 77.9 us on c4)
+#endif
+constexpr int CN64 = SZ3G_CN64, CQ64 = SZ3G_CQ64, CD64 = SZ3G_CD64;  // f64 compress: 3 groups x (1 + 3) warps + producer
 #ifndef SZ3G_DEC_CFG
 #define SZ3G_DEC_CFG 2   // f32 decompress shape (A/B tuning): 0 = 5 x 3 warps, 3-deep; 1 = 7 x 3 warps, 2-deep;
                          // 2 = 5 x 3, 2-deep, 2 output slabs per warp; 3 = 4 x 3, 3-deep, 2 slabs
@@ -1128,7 +1140,19 @@ constexpr int CN64 = 3, CQ64 = 3, CD64 = 2;  // f64 compress: 3 groups x (1 + 3)
 constexpr int DG32 = 3, DN32 = SZ3G_DEC_CFG == 1 ? 7 : (SZ3G_DEC_CFG == 3 ? 4 : 5),
               DD32 = (SZ3G_DEC_CFG == 1 || SZ3G_DEC_CFG == 2) ? 2 : 3,
               DOB32 = SZ3G_DEC_CFG >= 2 ? 2 : 1;  // f32 decompress: groups of 3 warps + producer
-constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 warps + producer
+#ifndef SZ3G_DG64
+#define SZ3G_DG64 3
+#endif
+#ifndef SZ3G_DN64
+#define SZ3G_DN64 4
+#endif
+#ifndef SZ3G_DD64
+#define SZ3G_DD64 2
+#endif
+#ifndef SZ3G_DOB64
+#define SZ3G_DOB64 1
+#endif
+constexpr int DG64 = SZ3G_DG64, DN64 = SZ3G_DN64, DD64 = SZ3G_DD64, DOB64 = SZ3G_DOB64;  // f64 decompress
 #ifndef SZ3G_AW
 #define SZ3G_AW 12
 #endif
@@ -1136,7 +1160,13 @@ constexpr int DG64 = 3, DN64 = 4, DD64 = 2;  // f64 decompress: 4 groups x 3 war
 #define SZ3G_AD 1
 #endif
 constexpr int AW32 = SZ3G_AW, AD32 = SZ3G_AD;   // f32 analyze: 12 self-fed warps x 1 stage (13.5 KiB each)
-constexpr int AW64 = 4, AD64 = 2;            // f64 analyze: 4 warps x 2 stages (27 KiB)
+#ifndef SZ3G_AW64
+#define SZ3G_AW64 7
+#endif
+#ifndef SZ3G_AD64
+#define SZ3G_AD64 1
+#endif
+constexpr int AW64 = SZ3G_AW64, AD64 = SZ3G_AD64;   // f64 analyze: 7 self-fed warps x 1 stage of 27 KiB (A/B on c4: 71.7 vs 75.8 us for 4 x 2)
 
 template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN, bool NOR0 = false>
 int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
@@ -1206,6 +1236,9 @@ int compress_launch(const Geo& g, const void* x, uint16_t* codes, bool tma, bool
       return use_hist ? launch_compress_tma<T, CN32, CQ32, CD32, true, BETA>(g, x, codes, codes_tma, ka, co, st)
                       : launch_compress_tma<T, CN32, CQ32, CD32, false, BETA>(g, x, codes, codes_tma, ka, co, st);
     } else {
+      if constexpr (BETA && SZ3G_CNOR64 != 0)
+        return use_hist ? launch_compress_tma<T, CN64, CQ64, CD64, true, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st)
+                        : launch_compress_tma<T, CN64, CQ64, CD64, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
       return use_hist ? launch_compress_tma<T, CN64, CQ64, CD64, true, BETA>(g, x, codes, codes_tma, ka, co, st)
                       : launch_compress_tma<T, CN64, CQ64, CD64, false, BETA>(g, x, codes, codes_tma, ka, co, st);
     }
@@ -1483,7 +1516,7 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
     }
   } else {
     if (tma) {
-      rc = launch_decompress_tma<double, DG64, DN64, DD64>(g, codes, coef_codes, x_out, ka, st);
+      rc = launch_decompress_tma<double, DG64, DN64, DD64, DOB64>(g, codes, coef_codes, x_out, ka, st);
       if (rc) return rc;
     } else {
       const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));

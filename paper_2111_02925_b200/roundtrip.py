@@ -40,36 +40,85 @@ class RoundTrip:
         self.beta = self.bufs.beta_buffer() if path == "two-pass" else None
         self.out = torch.empty_like(x)
 
-    def step(self, record=None):
-        """One pass of the whole hot path.  ``record``: 6 CUDA events recorded on the stream at
-        [quantise start, quantise end, decompress start, decompress end, analyze start, analyze end]."""
-        x, b, st = self.x, self.bufs, self.stream
-        ev = (lambda i: record[i].record(st)) if record is not None else (lambda i: None)
-        ev(4)
+    # the step in five segments; every segment launches on the stream it is given
+    def _analyze(self, st):
         if self.path == "two-pass":
-            sz3g.regression_analyze(x, b.minmax, self.beta, stream=st)
+            sz3g.regression_analyze(self.x, self.bufs.minmax, self.beta, stream=st)
         else:
-            sz3g.value_range(x, b.minmax, stream=st)
-        ev(5)
+            sz3g.value_range(self.x, self.bufs.minmax, stream=st)
+
+    def _range_reset(self, st):
         with torch.cuda.stream(st):
-            pdist.allreduce_range_(b.minmax, self.group)
-            b.reset()
-        ev(0)
+            pdist.allreduce_range_(self.bufs.minmax, self.group)
+            self.bufs.reset()
+
+    def _quantize(self, st):
+        x, b = self.x, self.bufs
         if self.path == "two-pass":
             sz3g.regression_quantize(x, self.eb, self.eb_mode, self.radius, b.minmax, self.beta, bufs=b, reset=False,
                                      dim0_offset=self.dim0_offset, stream=st)
         else:
             sz3g.regression_compress(x, self.eb, self.eb_mode, self.radius, d_minmax=b.minmax, bufs=b, reset=False,
                                      dim0_offset=self.dim0_offset, stream=st)
-        ev(1)
+
+    def _hist(self, st):
         with torch.cuda.stream(st):
-            pdist.allreduce_hist_(b.hist, self.group)
-        ev(2)
+            pdist.allreduce_hist_(self.bufs.hist, self.group)
+
+    def _decompress(self, st):
+        b = self.bufs
         sz3g.regression_decompress(b.codes, b.coef_codes, b.outlier_idx, b.outlier_val, self.cap, self.eb,
-                                   self.radius, x.dtype, dim0_offset=self.dim0_offset, out=self.out,
+                                   self.radius, self.x.dtype, dim0_offset=self.dim0_offset, out=self.out,
                                    d_outlier_count=b.outlier_count, eb_mode=self.eb_mode, d_minmax=b.minmax,
                                    stream=st)
-        ev(3)
+
+    SEGMENTS = ("_analyze", "_range_reset", "_quantize", "_hist", "_decompress")
+    # event index recorded after each segment (record[4] before the first): analyze end, quantise
+    # start, quantise end, decompress start, decompress end
+    _AFTER = (5, 0, 1, 2, 3)
+
+    def step(self, record=None):
+        """One pass of the whole hot path.  ``record``: 6 CUDA events recorded on the stream at
+        [quantise start, quantise end, decompress start, decompress end, analyze start, analyze end].
+        After ``capture()`` each segment is replayed from its CUDA graph (no host work per kernel)."""
+        st = self.stream
+        if record is not None:
+            record[4].record(st)
+        graphs = getattr(self, "graphs", None)
+        for name, after in zip(self.SEGMENTS, self._AFTER):
+            if graphs is not None:
+                if graphs[name] is not None:
+                    with torch.cuda.stream(st):
+                        graphs[name].replay()
+            else:
+                getattr(self, name)(st)
+            if record is not None:
+                record[after].record(st)
+
+    def capture(self):
+        """Capture every segment of the step in its own CUDA graph (single process or NCCL; gloo
+        collectives cannot be captured).  Replays launch the same kernels with the same arguments:
+        the buffers are fixed, and the kernels read the range / counters on the device."""
+        if self.group is not None or (torch.distributed.is_initialized() and torch.distributed.get_world_size() > 1
+                                      and torch.distributed.get_backend() != "nccl"):
+            raise RuntimeError("CUDA graph capture needs a single process or NCCL")
+        self.step()                      # warm: lazy attribute / descriptor setup outside the capture
+        torch.cuda.synchronize()
+        graphs = {}
+        l0 = sz3g.launch_count()
+        sharded = torch.distributed.is_initialized() and torch.distributed.get_world_size() > 1
+        for name in self.SEGMENTS:
+            if name == "_hist" and not sharded:   # no collective: nothing to launch
+                graphs[name] = None
+                continue
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                getattr(self, name)(torch.cuda.current_stream())
+            graphs[name] = g
+        torch.cuda.synchronize()
+        self.graphs = graphs
+        self.launches_per_step = sz3g.launch_count() - l0   # library kernels in one replayed step
+        return self
 
     def result(self) -> sz3g.Compressed:
         """The last step's compressed outputs (synchronises; raises on device status bits)."""

@@ -133,3 +133,25 @@ def test_bench_two_ranks_gloo():
     assert d["quality"]["above_eb"] == 0 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["roofline"]["ranks"] == "max over ranks"
     print(json.dumps({k: d[k] for k in ("value", "ms_per_step", "compress_gbs", "decompress_gbs")}))
+
+
+def test_roundtrip_cuda_graph_replay_bit_identical():
+    """RoundTrip.capture(): the step replayed from CUDA graphs (the bench's per-config legs) gives the
+    eager step's outputs bit for bit, replay after replay."""
+    from paper_2111_02925_b200 import sz3g
+    from paper_2111_02925_b200.roundtrip import RoundTrip
+    from synth import make_field
+    sz3g.load()
+    for name, shape, R in (("c3", (60, 96, 200), 8), ("c4", (30, 64, 96), 32768), ("c2", (24, 50, 50), 32768)):
+        x = make_field(name, device="cuda", shape=shape)
+        eager = RoundTrip(x, 1e-3, "rel", R, outlier_cap=x.numel())
+        eager.step()
+        e = eager.result()
+        g = RoundTrip(x, 1e-3, "rel", R, outlier_cap=x.numel()).capture()
+        for _ in range(3):
+            g.out.zero_()
+            g.step()
+            r = g.result()
+            assert torch.equal(r.codes, e.codes) and torch.equal(r.coef_codes, e.coef_codes)
+            assert torch.equal(r.hist, e.hist) and r.n_outliers == e.n_outliers
+            assert torch.equal(g.out.view(torch.uint8), eager.out.view(torch.uint8)), name

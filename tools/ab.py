@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--build", action="store_true")
     ap.add_argument("--path", default="fused", choices=["fused", "two-pass"])
     ap.add_argument("--tool", default="tune.py", help="tools/<tool> printing tune.py's JSON (e.g. huff_time.py)")
+    ap.add_argument("--flush", action="store_true")
+    ap.add_argument("--graphs", action="store_true")
     ap.add_argument("variants", nargs="+")
     a = ap.parse_args()
     vs = [v.split("=", 1) for v in a.variants]
@@ -54,12 +56,14 @@ def main():
         for n, rev in vs:
             build_rev(n, rev)
         return
-    res = {n: ([], []) for n, _ in vs}
+    res = {n: ([], [], []) for n, _ in vs}
     for r in range(a.rounds):
         for n, path in vs:
             env = dict(os.environ, SZ3G_LIB=os.path.join(ROOT, path) if not os.path.isabs(path) else path)
             out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", a.tool), "--config", a.config,
-                                  "--reps", str(a.reps), "--rounds", "1", "--path", a.path, a.setting or "CHUNK_C=2"],
+                                  "--reps", str(a.reps), "--rounds", "1", "--path", a.path,
+                                  *(["--flush"] if a.flush else []), *(["--graphs"] if a.graphs else []),
+                                  a.setting or "CHUNK_C=2"],
                                  env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
             if not line:
@@ -68,12 +72,14 @@ def main():
             d = json.loads(line[-1])
             res[n][0].append(d["compress_ms"][0])
             res[n][1].append(d["decompress_ms"][0])
+            res[n][2].append(d.get("analyze_ms", [0.0])[0])
             print(json.dumps({"round": r, "variant": n, "compress_ms": d["compress_ms"][0],
-                              "decompress_ms": d["decompress_ms"][0]}), flush=True)
-    for n, (c, dd) in res.items():
+                              "decompress_ms": d["decompress_ms"][0], "analyze_ms": res[n][2][-1]}), flush=True)
+    for n, (c, dd, aa) in res.items():
         if c:
             print(json.dumps({"variant": n, "compress_median_ms": statistics.median(c), "compress_min_ms": min(c),
-                              "decompress_median_ms": statistics.median(dd)}))
+                              "decompress_median_ms": statistics.median(dd),
+                              "analyze_median_ms": statistics.median(aa)}))
 
 
 if __name__ == "__main__":

@@ -14,6 +14,7 @@ from synth import make_field, config_by_name
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
 ap.add_argument("--reps", type=int, default=6)
+ap.add_argument("--max-len", type=int, default=16)
 ap.add_argument("rest", nargs="*")
 a, _ = ap.parse_known_args()
 cfg = config_by_name(a.config)
@@ -21,7 +22,7 @@ x = make_field(cfg, device="cuda")
 res = sz3g.compress(x, cfg.eb, cfg.eb_mode, cfg.radius)
 del x
 codes = res.codes.view(-1)
-t = sz3g.huffman_codebook(res.hist)
+t = sz3g.huffman_codebook(res.hist, max_len=a.max_len).check()
 hs = sz3g.huffman_encode(codes, t)
 out = sz3g.huffman_decode(hs, t)
 torch.cuda.synchronize()
@@ -37,4 +38,8 @@ for _ in range(a.reps):
     torch.cuda.synchronize()
     enc.append(e0.elapsed_time(e1))
     dec.append(e1.elapsed_time(e2))
-print(json.dumps({"compress_ms": [statistics.median(enc)], "decompress_ms": [statistics.median(dec)]}))
+lens = t.lengths.cpu().double()
+h = res.hist.cpu().double()
+print(json.dumps({"compress_ms": [statistics.median(enc)], "decompress_ms": [statistics.median(dec)],
+                  "max_len": a.max_len, "bits_per_code": float((lens * h).sum() / h.sum()),
+                  "frac_codes_over_12_bits": float(h[lens > 12].sum() / h.sum())}))

@@ -18,7 +18,7 @@ for f in re.split(r'\n\s+Function : ', txt)[1:]:
         m = re.search(r'BRA\s+(?:\S+\s+)?0x([0-9a-f]+)', l)
         if m:
             tgt = int(m.group(1), 16)
-            if tgt < addr[i] and minlen <= (i - addr.index(tgt)) <= 400:
+            if tgt < addr[i] and minlen <= (i - addr.index(tgt)) <= 4000:
                 j = addr.index(tgt)
                 c = collections.Counter(o.split('.')[0] for o in ops[j:i + 1])
                 print(f'  loop [{j},{i}] len {i - j + 1}:', ' '.join(f'{k}={v}' for k, v in c.most_common(16)))

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--rounds", type=int, default=2, help="passes over the settings (interleaved)")
     ap.add_argument("--path", default="fused", choices=["fused", "two-pass"])
+    ap.add_argument("--flush", action="store_true", help="write 256 MB before every timed launch (evict L2)")
+    ap.add_argument("--graphs", action="store_true", help="replay each timed call from a CUDA graph (no host gaps)")
     ap.add_argument("settings", nargs="+")
     args = ap.parse_args()
     import torch
@@ -54,12 +56,26 @@ def main():
                                    cfg.radius, x.dtype, out=out, d_outlier_count=bufs.outlier_count,
                                    eb_mode=cfg.eb_mode, d_minmax=bufs.minmax)
 
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
+
+    def ana():
+        sz3g.regression_analyze(x, bufs.minmax, bufs.beta_buffer())
+
     def timeit(fn):
         for _ in range(2):
             fn()
+        if args.graphs:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn_ = fn
+                fn_()
+            fn = g.replay
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.reps)]
         for a, b in evs:
             bufs.reset()
+            if flush_buf is not None:
+                flush_buf.fill_(1)
             a.record(stream)
             fn()
             b.record(stream)
@@ -84,11 +100,13 @@ def main():
             if ref_codes is None:
                 ref_codes = h
             td = timeit(dec)
-            res.setdefault(st, []).append((tc, td, h == ref_codes))
+            ta = timeit(ana) if beta is not None else 0.0
+            res.setdefault(st, []).append((tc, td, h == ref_codes, ta))
             # restore defaults for keys not in the next setting: every setting lists its keys explicitly
     for st, v in res.items():
-        print(json.dumps({"setting": st, "compress_ms": [round(a, 4) for a, _, _ in v],
-                          "decompress_ms": [round(b, 4) for _, b, _ in v], "codes_match": all(c for *_, c in v)}))
+        print(json.dumps({"setting": st, "compress_ms": [round(a, 4) for a, _, _, _ in v],
+                          "decompress_ms": [round(b, 4) for _, b, _, _ in v],
+                          "analyze_ms": [round(t, 4) for *_, t in v], "codes_match": all(c for _, _, c, _ in v)}))
 
 
 if __name__ == "__main__":
