@@ -118,7 +118,8 @@ int sz3g_regression_compress(const sz3g_grid* grid, const sz3g_params* params, c
  *                  before sz3g_regression_quantize.
  *   beta      out  4 x nblocks double, [block][b0,b1,b2,b3], 16-byte aligned: bit-identical to
  *                  the coef_raw output of sz3g_regression_compress on the same x.
- * Host errors: EINVAL (null / misaligned beta), EUNSUPPORTED, ECUDA.  3 launches.
+ * Host errors: EINVAL (null / misaligned beta), EUNSUPPORTED, ECUDA.  3 launches (range init, the pass, range final;
+ *           1 cooperative launch when built with -DSZ3G_ANA_COOP=1).
  *
  * a4-a7 -- sz3g_regression_quantize: compression from that beta.  Arguments and outputs are those
  * of sz3g_regression_compress (without coef_raw), plus

@@ -124,9 +124,11 @@ __global__ void __launch_bounds__(HF_THREADS, 1)
   const CbScratch S = cb_carve(scratch, nsym);
   if (tid == 0) { s_bad = 0; s_bits = 0; }
   const bool from_len = hist == nullptr;   // lengths given (a stored canonical codebook): (F) and (G) only
-  for (uint32_t s = tid; s < nsym; s += HF_THREADS) {
+  uint16_t* syms0 = reinterpret_cast<uint16_t*>(dt + 1);   // long-code symbol table: zeroed, so every
+  for (uint32_t s = tid; s < nsym; s += HF_THREADS) {         // byte of the decode table is defined
     if (!from_len) lens[s] = 0;
     cws[s] = 0;
+    syms0[s] = 0;
   }
   for (uint32_t i = tid; i < (1u << HF_LUT_BITS); i += HF_THREADS) dt->lut[i] = 0;
   if (tid < HF_MAXL) { dt->first[tid] = 0; dt->count[tid] = 0; dt->base[tid] = 0; }

@@ -10,6 +10,7 @@
 //   k_decompress_plain<T>      a8 for any shape
 //   k_outlier_scatter<T>       a8: x[idx] = val
 //   k_histogram                a7 standalone (smem window + global atomics)
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -297,7 +298,11 @@ struct AnalyzeSmem {
   static constexpr size_t total = off_red + 2 * W * sizeof(uint64_t) + 16;
 };
 
-template <typename T, int W, int D>
+// COOP (cooperative launch, every CTA resident): the range keys are initialised by CTA 0 and turned
+// into doubles by CTA 0 after grid-wide barriers, instead of by two one-thread kernels before and
+// after (a small field pays ~8 us for those two launches).  The first barrier comes after each warp
+// has issued its first TMA loads, so it overlaps their latency.
+template <typename T, int W, int D, bool COOP = false>
 __global__ void __launch_bounds__(W * 32, 1)
     k_analyze_tma(const __grid_constant__ CUtensorMap tm_x, KArgs a, double* __restrict__ beta,
                   unsigned long long* keys) {
@@ -328,6 +333,13 @@ __global__ void __launch_bounds__(W * 32, 1)
       ptx::tma_load_3d(ring + (size_t)d * TILE_ELEMS, &tm_x, &bar[d], (int)(tc.c * TK), (int)(tc.b * BS), (int)(tc.a * BS));
     }
   }
+  if (COOP) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      keys[0] = ~0ull;  // running min key
+      keys[1] = 0ull;   // running max key
+    }
+    cooperative_groups::this_grid().sync();
+  }
   for (uint32_t k = 0;; k++, tw.next()) {
     const uint64_t t = tw.tile();
     if (t >= g.ntiles) break;
@@ -351,6 +363,15 @@ __global__ void __launch_bounds__(W * 32, 1)
     }
   }
   range_epilogue(mm, nan, keys, s_red);
+  if (COOP) {
+    cooperative_groups::this_grid().sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double* d = reinterpret_cast<double*>(keys);
+      const double lo = key_to_double(keys[0]), hi = key_to_double(keys[1]);
+      d[0] = lo;
+      d[1] = hi;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------- compress, TMA
@@ -1297,6 +1318,11 @@ int compress_common(const sz3g_grid* grid, const sz3g_params* params, const void
                  : compress_launch<double, false>(g, x, codes, tma, codes_tma, use_hist, ka, co, st);
 }
 
+#ifndef SZ3G_ANA_COOP
+#define SZ3G_ANA_COOP 0   // 1: analyze as ONE cooperative launch (range init / final inside, grid.sync); A/B on
+                          // c4 / c3: 75.7 / 120.9 us against 71.7 / 116.7 us for the three launches
+#endif
+
 template <typename T, int W, int D>
 int launch_analyze_tma(const Geo& g, const void* x, double* beta, unsigned long long* keys, const KArgs& ka,
                        cudaStream_t st) {
@@ -1305,12 +1331,26 @@ int launch_analyze_tma(const Geo& g, const void* x, double* beta, unsigned long 
   CUtensorMap mx;
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
+  const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
+  if (SZ3G_ANA_COOP) {
+    // one CTA per SM (launch bounds + shared memory): a grid of <= #SMs CTAs is co-resident
+    auto kern = k_analyze_tma<T, W, D, true>;
+    cudaError_t e = set_smem(kern, L::total);
+    if (e != cudaSuccess) return cuda_fail(e);
+    KArgs kc = ka;
+    void* args[] = {(void*)&mx, (void*)&kc, (void*)&beta, (void*)&keys};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(W * 32), args, L::total, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SZ3G_OK;
+  }
   auto kern = k_analyze_tma<T, W, D>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
-  const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
+  k_range_init<<<1, 1, 0, st>>>(keys);
   kern<<<(unsigned)grid, W * 32, L::total, st>>>(mx, ka, beta, keys);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_range_final<<<1, 1, 0, st>>>(keys);
+  g_launches.fetch_add(3, std::memory_order_relaxed);
   return SZ3G_OK;
 }
 
@@ -1442,20 +1482,19 @@ int sz3g_regression_analyze(const sz3g_grid* grid, const void* x, double* d_minm
   ka.g = g;
   ka.chunk = chunk_tiles(false);
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(d_minmax);
-  k_range_init<<<1, 1, 0, st>>>(keys);
   const size_t es = grid->dtype == SZ3G_F32 ? 4 : 8;
-  if (map_ok(x, es, g)) {
+  if (map_ok(x, es, g)) {   // TMA kernel: its launcher counts its launches (1 cooperative, or 3)
     rc = grid->dtype == SZ3G_F32 ? launch_analyze_tma<float, AW32, AD32>(g, x, beta, keys, ka, st)
                                  : launch_analyze_tma<double, AW64, AD64>(g, x, beta, keys, ka, st);
     if (rc) return rc;
-  } else {
-    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
-    if (grid->dtype == SZ3G_F32) k_analyze_plain<float><<<blocks, 128, 0, st>>>((const float*)x, ka, beta, keys);
-    else k_analyze_plain<double><<<blocks, 128, 0, st>>>((const double*)x, ka, beta, keys);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return check_launch(0);
   }
+  k_range_init<<<1, 1, 0, st>>>(keys);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
+  if (grid->dtype == SZ3G_F32) k_analyze_plain<float><<<blocks, 128, 0, st>>>((const float*)x, ka, beta, keys);
+  else k_analyze_plain<double><<<blocks, 128, 0, st>>>((const double*)x, ka, beta, keys);
   k_range_final<<<1, 1, 0, st>>>(keys);
-  return check_launch(2);
+  return check_launch(3);
 }
 
 int sz3g_regression_quantize(const sz3g_grid* grid, const sz3g_params* params, const void* x,
