@@ -525,6 +525,10 @@ __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const 
 // SELF: no producer warp; the role-0 warp of each group feeds its own group's ring (it issues the
 // load of tile k + D - 1 once the quantise warps have released tile k - 1, right after it has
 // published tile k's coefficients), with an optional L2 prefetch one tile further ahead.
+#ifndef SZ3G_QWAIT
+#define SZ3G_QWAIT 1   // quantise warps' wait for a full stage: 0 = try_wait + nanosleep(64) polling,
+                       // 1 = hardware-suspended try_wait (no polling instructions: less issue, less power)
+#endif
 template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF, int HW, bool NOR0>
 __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0>::WARPS * 32, 1)
     k_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, int codes_tma,
@@ -696,7 +700,8 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
         }
         if (codes_tma && lane == 0) ptx::bulk_wait_read0();   // previous slab store finished reading
         SZ3G_SYNCWARP();
-        ptx::mbar_wait(&full[s], ph);
+        if (SZ3G_QWAIT) ptx::mbar_wait_idle(&full[s], ph);   // hardware-suspended: no polling instructions
+        else ptx::mbar_wait(&full[s], ph);
         if (!SELF) {
           const uint4 h = hdr[s];
           if (h.w == HDR_END) break;

@@ -441,6 +441,18 @@ __device__ __forceinline__ bool quantize_rows(const T* __restrict__ xs, uint64_t
   const double M64 = RINT_MAGIC + (double)R;          // 1.5 * 2^52 + R (exact)
   const double Wd = (double)W;
   bool has_out = false;
+#ifndef SZ3G_IPAIR_REG
+#define SZ3G_IPAIR_REG 1
+#endif
+#if SZ3G_X2
+  // the packed (i, i + 1) plane indices: immediates (re-created in uniform registers for every column,
+  // 6 UMOV per 6 elements) or, with SZ3G_IPAIR_REG, register pairs (a runtime zero, R >> 31 with
+  // R <= 32768, keeps the compiler from folding them back into immediates)
+  const float zf = SZ3G_IPAIR_REG ? (float)(R >> 31) : 0.0f;
+  uint64_t ipair[3];
+#pragma unroll
+  for (int q = 0; q < 3; q++) ipair[q] = pack2(zf + (float)(2 * q), zf + (float)(2 * q + 1));
+#endif
   // columns (j, k) visited with incremental pointers and fp32 counters (no per-iteration division)
   const T* xrow = xs + (IN_SMEM ? (uint32_t)(j0 * TK + L.kcol) : (uint64_t)j0 * sj + L.kcol);
   uint16_t* crow = cs + (SLAB ? (uint32_t)L.kcol : (uint64_t)j0 * cj + L.kcol);
@@ -470,7 +482,7 @@ __device__ __forceinline__ bool quantize_rows(const T* __restrict__ xs, uint64_t
 #pragma unroll
       for (int i = 0; i < BS; i += 2) {
         const uint64_t x2 = pack2((float)xv[i], (float)xv[i + 1]);
-        const uint64_t nP = fma2(pack2(-F.a1, -F.a1), pack2((float)i, (float)(i + 1)), pack2(-base32, -base32));
+        const uint64_t nP = fma2(pack2(-F.a1, -F.a1), ipair[i >> 1], pack2(-base32, -base32));
         const uint64_t t2 = fma2(x2, pack2(inv2eb32, inv2eb32), nP);   // -P exact: P(i = 0) = base32
         const uint64_t s2 = add2(t2, pack2(M32, M32));
         const uint64_t r2 = sub2(s2, pack2(M32, M32));
