@@ -42,4 +42,5 @@ lens = t.lengths.cpu().double()
 h = res.hist.cpu().double()
 print(json.dumps({"compress_ms": [statistics.median(enc)], "decompress_ms": [statistics.median(dec)],
                   "max_len": a.max_len, "bits_per_code": float((lens * h).sum() / h.sum()),
-                  "frac_codes_over_12_bits": float(h[lens > 12].sum() / h.sum())}))
+                  "frac_codes_over_12_bits": float(h[lens > 12].sum() / h.sum()),
+                  "lut2_entries": int(65536 - sum(int((lens == L).sum()) << (16 - L) for L in range(1, 13)))}))
