@@ -5,7 +5,8 @@ linear-scaling quantisation (sz3_oracle.cpp: PAPER.md Lemma 1, predictio
 P:406-409, App. A loop P:980-992, value-range eb P:833), of the Huffman encoder stage
 (huffman_oracle.cpp: P:156), of SZ3-Truncation and the coefficient delta coding
 (truncation_oracle.cpp: P:848-850) and of the distortion metrics (below: P:525); the exact
-definitions are oracle/DEFINITION.md (O1-O11, D, H1-H5, T1-T2, C1-C2, M1-M3, L1-L7: SZ3-LR).  Only ``tests/``, ``__graft_entry__.smoke()`` and
+definitions are oracle/DEFINITION.md (O1-O11, D, H1-H5, T1-T2, C1-C2, M1-M3, L1-L7: SZ3-LR, P:845,
+I1-I6: SZ3-Interp, P:852-853).  Only ``tests/``, ``__graft_entry__.smoke()`` and
 ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this package.  It shares
 no code with ``paper_2111_02925_b200`` and never imports it.
 """
@@ -82,6 +83,12 @@ def _load():
             lib.orc_lr_compress.argtypes = [I32, P, U64, U32, U32, I32, D, P, P, P, P, P, P, P, P, P, U64, P, P, P,
                                             P, P]
             lib.orc_lr_decompress.argtypes = [I32, P, U64, U32, U32, D, P, P, P, P, P, U64, P]
+            lib.orc_interp_compress.argtypes = [I32, P, U64, U32, I32, D, P, P, P, P, P, U64, P, P, P, P, P]
+            lib.orc_interp_decompress.argtypes = [I32, P, U64, U32, D, P, P, P, U64, P]
+            lib.orc_interp_predict.argtypes = [D, D, D, D, I32]
+            lib.orc_interp_predict.restype = D
+            lib.orc_interp_pass_of.argtypes = [P, U64, U64, U64]
+            lib.orc_interp_pass_of.restype = ctypes.c_int64
             lib.orc_lr_delta.argtypes = [P, I32, I32, I32, I32, I32, I32]
             lib.orc_lr_delta.restype = ctypes.c_int64
             _lib = lib
@@ -413,3 +420,74 @@ def lr_delta(q: np.ndarray, i: int, j: int, k: int) -> int:
     """L2 on one dense block of int64 values."""
     q = np.ascontiguousarray(q, np.int64)
     return int(_load().orc_lr_delta(_ptr(q), q.shape[0], q.shape[1], q.shape[2], i, j, k))
+
+
+# SZ3-Interp (P:852-853; DEFINITION.md I1-I6; sz3_oracle.cpp interp_*)
+@dataclass
+class InterpCompressed:
+    dims: tuple
+    dtype: np.dtype
+    radius: int
+    eb_abs: float
+    codes: np.ndarray          # uint16, field shape (the anchor's code is 0)
+    outlier_idx: np.ndarray    # uint64 global indices (the anchor first)
+    outlier_val: np.ndarray
+    hist: np.ndarray
+    counters: dict
+    dim0_offset: int
+    xprime: np.ndarray         # compress-time reconstruction
+
+
+def interp_compress(x: np.ndarray, eb: float, eb_mode: str = "rel", radius: int = 32768, dim0_offset: int = 0,
+                    value_range_override: tuple | None = None) -> InterpCompressed:
+    """I1-I5 over a 3D field (1D/2D embedded with leading extents 1)."""
+    x = np.ascontiguousarray(x)
+    shape = (1,) * (3 - x.ndim) + tuple(x.shape)
+    dims = np.array(shape, np.uint64)
+    N = int(np.prod(shape))
+    codes = np.empty(shape, np.uint16)
+    oidx = np.empty(N, np.uint64)
+    oval = np.empty(N, x.dtype)
+    nout = np.zeros(1, np.uint64)
+    hist = np.empty(2 * radius, np.int64)
+    eb_abs = np.zeros(1, np.float64)
+    xprime = np.empty(shape, x.dtype)
+    cnt = Counters()
+    rng = None if value_range_override is None else np.array(value_range_override, np.float64)
+    rc = _load().orc_interp_compress(_dtype_id(x.dtype), _ptr(dims), dim0_offset, radius, {"abs": 0, "rel": 1}[eb_mode],
+                                     float(eb), _ptr(rng), _ptr(x), _ptr(codes), _ptr(oidx), _ptr(oval), N, _ptr(nout),
+                                     _ptr(hist), _ptr(eb_abs), _ptr(xprime), ctypes.byref(cnt))
+    if rc != OK:
+        raise ValueError(f"orc_interp_compress rc={rc}")
+    n = int(nout[0])
+    return InterpCompressed(tuple(int(s) for s in shape), x.dtype, radius, float(eb_abs[0]), codes, oidx[:n].copy(),
+                            oval[:n].copy(), hist, cnt.as_dict(), dim0_offset, xprime)
+
+
+def interp_decompress(c: InterpCompressed | None = None, *, dims=None, dtype=None, radius=None, eb_abs=None,
+                      codes=None, outlier_idx=None, outlier_val=None, dim0_offset=0) -> np.ndarray:
+    """I6."""
+    if c is not None:
+        dims, dtype, radius, eb_abs = c.dims, c.dtype, c.radius, c.eb_abs
+        codes, outlier_idx, outlier_val, dim0_offset = c.codes, c.outlier_idx, c.outlier_val, c.dim0_offset
+    d = np.array(dims, np.uint64)
+    out = np.zeros(tuple(int(s) for s in dims), dtype)
+    codes = np.ascontiguousarray(codes, np.uint16)
+    oidx = np.ascontiguousarray(outlier_idx, np.uint64)
+    oval = np.ascontiguousarray(outlier_val, dtype)
+    rc = _load().orc_interp_decompress(_dtype_id(dtype), _ptr(d), dim0_offset, radius, float(eb_abs), _ptr(codes),
+                                       _ptr(oidx), _ptr(oval), oidx.size, _ptr(out))
+    if rc != OK:
+        raise ValueError(f"orc_interp_decompress rc={rc}")
+    return out
+
+
+def interp_predict(a: float, b: float, c: float, e: float, method: int) -> float:
+    """I3: method 2 cubic (donors -3s, -s, +s, +3s), 1 linear (-s, +s), 0 copy of -s."""
+    return float(_load().orc_interp_predict(a, b, c, e, method))
+
+
+def interp_pass_of(dims, i0: int, i1: int, i2: int) -> int:
+    """I2: the pass (3 level + axis, level 0 = the largest stride) that predicts index (i0, i1, i2); -1 = anchor."""
+    d = np.array(dims, np.uint64)
+    return int(_load().orc_interp_pass_of(_ptr(d), i0, i1, i2))

@@ -13,6 +13,8 @@
 //    * value-range-relative eb
 //    * SZ3-LR (NEXT-4)          P:845  Lorenzo / regression per block ("better result in between
 //                                      based on blockwise error estimation"); DEFINITION.md L1-L7
+//    * SZ3-Interp (NEXT-4)      P:852-853 "Both linear interpolation and cubic spline interpolation
+//                                      are included", "constant coefficients"; DEFINITION.md I1-I6
 //  Readings of silent / garbled passages (coefficient bins, tie rule, verify step, ...) are the
 //  ones listed in DESIGN.md section "Readings" (G1..G18) and in oracle/DEFINITION.md.
 //
@@ -553,6 +555,162 @@ int lr_decompress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t B,
   return ORC_OK;
 }
 
+// ---------------------------------------------------------------- SZ3-Interp (NEXT-4; DEFINITION.md I1-I6)
+// I2: the level plan.  S = the largest power of two below the largest extent; levels s = S, S/2, .., 1;
+// in a level, one pass per axis d = 0, 1, 2.  Pass (s, d) predicts the indices whose coordinate along
+// d is an odd multiple of s, whose coordinates along the earlier axes are multiples of s and along the
+// later axes multiples of 2s.  Every index but the anchor (0, 0, 0) belongs to exactly one pass.
+inline uint64_t interp_top_stride(const uint64_t dims[3]) {
+  const uint64_t n = std::max(dims[0], std::max(dims[1], dims[2]));
+  uint64_t S = 1;
+  while (2 * S < n) S *= 2;
+  return n > 1 ? S : 0;
+}
+
+// I3: prediction along axis d from the reconstructed donors at -3s, -s, +s, +3s (cubic spline weights
+// (-1, 9, 9, -1)/16 when all four exist, the midpoint when only -s and +s do, else a copy of -s).
+// All in fp64, no contraction: u = b + c, v = a + e, p = (9 u - v) * 0.0625.
+inline double interp_predict(double a, double b, double c, double e, int method) {
+  if (method == 2) {
+    const double u = b + c;
+    const double v = a + e;
+    const double w = 9.0 * u;
+    return (w - v) * 0.0625;
+  }
+  if (method == 1) return (b + c) * 0.5;
+  return b;
+}
+
+// method of a target at coordinate i along an axis of extent n with stride s
+inline int interp_method(uint64_t i, uint64_t n, uint64_t s) {
+  if (i >= 3 * s && i + 3 * s < n) return 2;
+  if (i + s < n) return 1;
+  return 0;
+}
+
+template <typename T>
+int interp_compress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t R, int eb_mode, double eb,
+                         const double* range, const T* x, uint16_t* codes, uint64_t* out_idx, T* out_val,
+                         uint64_t cap, uint64_t* n_out, int64_t* hist, double* eb_abs_out, T* xp, orc_counters* cnt) {
+  const uint64_t n0 = dims[0], n1 = dims[1], n2 = dims[2], N = n0 * n1 * n2;
+  double lo = 0.0, hi = 0.0;
+  if (eb_mode == 1) {   // I1 = O1
+    if (range) {
+      lo = range[0]; hi = range[1];
+    } else {
+      lo = hi = (double)x[0];
+      for (uint64_t e = 0; e < N; e++) {
+        double v = (double)x[e];
+        if (std::isnan(v)) { lo = hi = v; break; }
+        if (v < lo) lo = v;
+        if (v > hi) hi = v;
+      }
+    }
+  }
+  Bounds bd;
+  if (!make_bounds(eb_mode, eb, lo, hi, 6, &bd)) return ORC_EBADRANGE;
+  if (eb_abs_out) *eb_abs_out = bd.eb_abs;
+  orc_counters c{};
+  uint64_t nout = 0;
+  auto outlier = [&](uint64_t e) {
+    if (nout < cap) { out_idx[nout] = e + dim0_offset * n1 * n2; out_val[nout] = x[e]; }
+    nout++;
+  };
+  // I4: the anchor is stored as it is
+  codes[0] = 0;
+  xp[0] = x[0];
+  outlier(0);
+  const uint64_t S = interp_top_stride(dims);
+  const uint64_t st[3] = {n1 * n2, n2, 1};
+  for (uint64_t s = S; s >= 1; s /= 2) {
+    for (int d = 0; d < 3; d++) {
+      uint64_t first[3], step[3];
+      for (int a = 0; a < 3; a++) {
+        first[a] = a == d ? s : 0;
+        step[a] = (a == d || a > d) ? 2 * s : s;
+      }
+      for (uint64_t i0 = first[0]; i0 < n0; i0 += step[0])
+        for (uint64_t i1 = first[1]; i1 < n1; i1 += step[1])
+          for (uint64_t i2 = first[2]; i2 < n2; i2 += step[2]) {
+            const uint64_t e = i0 * st[0] + i1 * st[1] + i2 * st[2];
+            const uint64_t id = d == 0 ? i0 : (d == 1 ? i1 : i2);
+            const int m = interp_method(id, dims[d], s);
+            const uint64_t sd = s * st[d];
+            const double a = m == 2 ? (double)xp[e - 3 * sd] : 0.0;
+            const double b = (double)xp[e - sd];
+            const double cc = m >= 1 ? (double)xp[e + sd] : 0.0;
+            const double ee = m == 2 ? (double)xp[e + 3 * sd] : 0.0;
+            const double p = interp_predict(a, b, cc, ee, m);
+            // I5 = O8-O10 with the interpolated prediction
+            uint16_t code;
+            T xv;
+            const int kind = quantize_element<T>(x[e], p, bd, R, &code, &xv);
+            codes[e] = code;
+            xp[e] = xv;
+            if (kind != 0) {
+              if (kind == 1) c.radius_outliers++;
+              else if (kind == 2) c.verify_outliers++;
+              else c.nonfinite_outliers++;
+              outlier(e);
+            }
+          }
+    }
+    if (s == 1) break;
+  }
+  if (hist) {   // O11
+    std::memset(hist, 0, sizeof(int64_t) * 2 * (size_t)R);
+    for (uint64_t e = 0; e < N; e++) hist[codes[e]]++;
+  }
+  *n_out = nout;
+  if (cnt) *cnt = c;
+  return nout > cap ? ORC_EOVERFLOW : ORC_OK;
+}
+
+// I6: decompression replays the plan on x' (outlier values first, then the passes in order)
+template <typename T>
+int interp_decompress_impl(const uint64_t dims[3], uint64_t dim0_offset, uint32_t R, double eb_abs,
+                           const uint16_t* codes, const uint64_t* out_idx, const T* out_val, uint64_t n_out,
+                           T* xo) {
+  const uint64_t n0 = dims[0], n1 = dims[1], n2 = dims[2], N = n0 * n1 * n2;
+  Bounds bd;
+  if (!make_bounds(0, eb_abs, 0, 0, 6, &bd)) return ORC_EBADRANGE;
+  for (uint64_t e = 0; e < N; e++) xo[e] = T(0);
+  for (uint64_t o = 0; o < n_out; o++) {
+    const uint64_t e = out_idx[o] - dim0_offset * n1 * n2;
+    if (e < N) xo[e] = out_val[o];
+  }
+  const uint64_t S = interp_top_stride(dims);
+  const uint64_t st[3] = {n1 * n2, n2, 1};
+  for (uint64_t s = S; s >= 1; s /= 2) {
+    for (int d = 0; d < 3; d++) {
+      uint64_t first[3], step[3];
+      for (int a = 0; a < 3; a++) {
+        first[a] = a == d ? s : 0;
+        step[a] = (a == d || a > d) ? 2 * s : s;
+      }
+      for (uint64_t i0 = first[0]; i0 < n0; i0 += step[0])
+        for (uint64_t i1 = first[1]; i1 < n1; i1 += step[1])
+          for (uint64_t i2 = first[2]; i2 < n2; i2 += step[2]) {
+            const uint64_t e = i0 * st[0] + i1 * st[1] + i2 * st[2];
+            if (codes[e] == 0) continue;   // outlier: its value is already in place
+            const uint64_t id = d == 0 ? i0 : (d == 1 ? i1 : i2);
+            const int m = interp_method(id, dims[d], s);
+            const uint64_t sd = s * st[d];
+            const double a = m == 2 ? (double)xo[e - 3 * sd] : 0.0;
+            const double b = (double)xo[e - sd];
+            const double cc = m >= 1 ? (double)xo[e + sd] : 0.0;
+            const double ee = m == 2 ? (double)xo[e + 3 * sd] : 0.0;
+            const double p = interp_predict(a, b, cc, ee, m);
+            const double q = (double)((int64_t)codes[e] - (int64_t)R);
+            const double prod = bd.twoeb * q;
+            xo[e] = (T)(p + prod);
+          }
+    }
+    if (s == 1) break;
+  }
+  return ORC_OK;
+}
+
 bool check_dims(const uint64_t* dims, uint32_t B, uint32_t R) {
   if (!dims || dims[0] == 0 || dims[1] == 0 || dims[2] == 0) return false;
   if (B < 1 || R < 1 || R > 32768) return false;
@@ -700,6 +858,62 @@ int orc_lr_decompress(int dtype, const uint64_t dims[3], uint64_t dim0_offset, u
 int64_t orc_lr_delta(const int64_t* q, int m0, int m1, int m2, int i, int j, int k) {
   std::vector<int64_t> v(q, q + (size_t)m0 * m1 * m2);
   return lr_delta(v, m1, m2, i, j, k);
+}
+
+
+// SZ3-Interp (NEXT-4): compress -> codes, outliers (the anchor first), histogram, x'; decompress -> x'.
+int orc_interp_compress(int dtype, const uint64_t dims[3], uint64_t dim0_offset, uint32_t R, int eb_mode, double eb,
+                        const double* range, const void* x, uint16_t* codes, uint64_t* out_idx, void* out_val,
+                        uint64_t cap, uint64_t* n_out, int64_t* hist, double* eb_abs_out, void* xprime,
+                        orc_counters* cnt) {
+  if (!check_dims(dims, 6, R)) return (R < 1 || R > 32768) ? ORC_ERANGE : ORC_EINVAL;
+  if (!x || !codes || !xprime || !n_out || cap < 1 || !out_idx || !out_val) return ORC_EINVAL;
+  if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != 0 && eb_mode != 1)) return ORC_EINVAL;
+  if (dtype == 0)
+    return interp_compress_impl<float>(dims, dim0_offset, R, eb_mode, eb, range, (const float*)x, codes, out_idx,
+                                       (float*)out_val, cap, n_out, hist, eb_abs_out, (float*)xprime, cnt);
+  if (dtype == 1)
+    return interp_compress_impl<double>(dims, dim0_offset, R, eb_mode, eb, range, (const double*)x, codes, out_idx,
+                                        (double*)out_val, cap, n_out, hist, eb_abs_out, (double*)xprime, cnt);
+  return ORC_EUNSUPPORTED;
+}
+
+int orc_interp_decompress(int dtype, const uint64_t dims[3], uint64_t dim0_offset, uint32_t R, double eb_abs,
+                          const uint16_t* codes, const uint64_t* out_idx, const void* out_val, uint64_t n_out,
+                          void* x_out) {
+  if (!check_dims(dims, 6, R)) return (R < 1 || R > 32768) ? ORC_ERANGE : ORC_EINVAL;
+  if (!codes || !x_out || (n_out > 0 && (!out_idx || !out_val))) return ORC_EINVAL;
+  if (dtype == 0)
+    return interp_decompress_impl<float>(dims, dim0_offset, R, eb_abs, codes, out_idx, (const float*)out_val, n_out,
+                                         (float*)x_out);
+  if (dtype == 1)
+    return interp_decompress_impl<double>(dims, dim0_offset, R, eb_abs, codes, out_idx, (const double*)out_val,
+                                          n_out, (double*)x_out);
+  return ORC_EUNSUPPORTED;
+}
+
+// I3 and the I2 pass of one index (for the pins): pass id = 3 * level + axis, level 0 = the top stride;
+// -1 for the anchor
+double orc_interp_predict(double a, double b, double c, double e, int method) {
+  return interp_predict(a, b, c, e, method);
+}
+
+int64_t orc_interp_pass_of(const uint64_t dims[3], uint64_t i0, uint64_t i1, uint64_t i2) {
+  const uint64_t S = interp_top_stride(dims);
+  const uint64_t ii[3] = {i0, i1, i2};
+  int64_t level = 0;
+  for (uint64_t s = S; s >= 1; s /= 2, level++) {
+    for (int d = 0; d < 3; d++) {
+      bool in = ii[d] % (2 * s) == s;
+      for (int a = 0; a < 3 && in; a++) {
+        if (a < d) in = ii[a] % s == 0;
+        if (a > d) in = ii[a] % (2 * s) == 0;
+      }
+      if (in) return 3 * level + d;
+    }
+    if (s == 1) break;
+  }
+  return -1;
 }
 
 uint64_t orc_num_blocks(const uint64_t dims[3], uint32_t B) {
