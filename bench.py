@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-truncation", action="store_true", help="skip the SZ3-Truncation (NEXT-2) measurement")
     ap.add_argument("--trunc-k", type=int, default=2)
     ap.add_argument("--no-lr", action="store_true", help="skip the SZ3-LR (NEXT-4) measurement")
+    ap.add_argument("--no-interp", action="store_true", help="skip the SZ3-Interp (NEXT-4) measurement")
     ap.add_argument("--path", default="two-pass", choices=["two-pass", "fused"],
                     help="REL compression: analyze (range + beta) -> quantize, or value_range -> fused compress")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -446,6 +447,56 @@ def lr_leg(sz3g, x, out, bufs, cfg, a0, N_local, NB_local, s, args, world, peaks
                     "predictor flags as a bitmap (1 bit per block)"}
 
 
+def interp_leg(sz3g, x, out, minmax, cfg, N_local, s, args, world, peaks, stream):
+    """NEXT-4 SZ3-Interp (DEFINITION.md I1-I6) on the same field with the timed steps' range:
+    compress (level passes + histogram) and decompress timed with CUDA events (median of 3), the
+    reconstruction checked against the bound, the codes Huffman-coded for the ratio (not timed).  Level
+    passes cross every slab boundary, so at N > 1 every rank compresses its own slab as a separate field."""
+    import torch
+    ev = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
+    res = sz3g.interp_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=minmax,
+                               outlier_cap=max(1 << 20, N_local // 64), stream=stream)
+    tc, td = [], []
+    for _ in range(3):
+        e = [ev() for _ in range(3)]
+        e[0].record(stream)
+        sz3g.interp_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, d_minmax=minmax, out=res, stream=stream)
+        e[1].record(stream)
+        sz3g.interp_decompress(res.codes, res.outlier_idx, res.outlier_val, res.outlier_idx.numel(), cfg.eb,
+                               cfg.radius, x.dtype, out=out, d_outlier_count=res.outlier_count, eb_mode=cfg.eb_mode,
+                               d_minmax=minmax, stream=stream)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        tc.append(e[0].elapsed_time(e[1]))
+        td.append(e[1].elapsed_time(e[2]))
+    res.finalize()
+    c_ms = max_over_ranks(sorted(tc)[1], world)
+    d_ms = max_over_ranks(sorted(td)[1], world)
+    st = sz3g.error_stats(x, out, res.eb_abs).cpu().tolist()
+    if st[2] != 0 or not st[0] <= res.eb_abs:
+        raise RuntimeError(f"SZ3-Interp error bound violated: {st}")
+    n_out = res.n_outliers
+    table = sz3g.huffman_codebook(res.hist).check()
+    hs = sz3g.huffman_encode(res.codes.view(-1), table).check()
+    pay_b = 4 * hs.words()
+    stored = pay_b + 8 * hs.offsets.numel() + (8 + s) * n_out + table.stored_bytes()
+    # algorithmic bytes (DESIGN.md 5): compress reads x, writes codes and the reconstruction x' (its
+    # working buffer); decompress reads codes, writes x'; the donors' re-reads are the method's own
+    c_bytes = N_local * (s + 2 + s) + n_out * (8 + s)
+    d_bytes = N_local * (2 + s) + n_out * (8 + s)
+    lo, hi = (float(v) for v in minmax.cpu())
+    del res, hs
+    return {"outliers": n_out, "bits_per_code": 8 * pay_b / N_local, "compression_ratio": N_local * s / stored,
+            "psnr_db": sz3g.psnr(hi - lo, st[1] / N_local), "max_abs_err": st[0],
+            "compress_ms": c_ms, "decompress_ms": d_ms,
+            "compress_roofline": {"achieved": c_bytes / (c_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                  "frac": c_bytes / (c_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "decompress_roofline": {"achieved": d_bytes / (d_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                                    "frac": d_bytes / (d_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "note": "level-serial: one launch per pass (3 per level); compression = value range (shared) + passes "
+                    "+ histogram"}
+
+
 # ----------------------------------------------------------------------------------------- per-config legs
 def alg_bytes(N, NB, s, n_out):
     """SURVEY 8(d) algorithmic bytes per launch of each kernel: the quantise kernel reads
@@ -611,6 +662,11 @@ def main():
     if not args.no_lr:
         lr = lr_leg(sz3g, x, out, bufs, cfg, a0, N_local, NB_local, s, args, world, peaks, stream)
 
+    # ---------------- SZ3-Interp (NEXT-4) on the same field
+    interp = None
+    if not args.no_interp:
+        interp = interp_leg(sz3g, x, out, bufs.minmax, cfg, N_local, s, args, world, peaks, stream)
+
     # ---------------- CPU oracle beside it (rank 0, N = 1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -707,7 +763,7 @@ def main():
                                  **roof(b["analyze"], ana_ms, peaks["hbm_gbs"])},
             "hist_allreduce_ms": hist_ar_ms if world > 1 else 0.0,
             "path": args.path,
-            "quality": quality, "ties": ties, "huffman": huff, "truncation": trunc, "lr": lr,
+            "quality": quality, "ties": ties, "huffman": huff, "truncation": trunc, "lr": lr, "interp": interp,
             "configs": legs or None, "outliers": n_out, "eb_abs": eb_abs_used,
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
             "paper_context": PAPER_CONTEXT,

@@ -183,6 +183,33 @@ int sz3g_lr_decompress(const sz3g_grid* grid, const sz3g_params* params, const d
                        const uint64_t* outlier_idx, const void* outlier_val, uint64_t n_outliers,
                        const unsigned long long* d_outlier_count, void* x_out, sz3g_stream_t stream);
 
+/* NEXT-4 -- SZ3-Interp, the multilevel interpolation predictor: "Both linear interpolation and cubic
+ * spline interpolation are included ... SZ3-Interp has constant coefficients and therefore does not have
+ * storage overhead".  Definition oracle/DEFINITION.md I1-I6 (readings DESIGN G30-G33): levels of
+ * stride s = S .. 1 (S the largest power of two below the largest extent), one pass per axis; each
+ * target is predicted from RECONSTRUCTED donors at -3s, -s, +s, +3s along the pass axis (cubic weights
+ * (-1, 9, 9, -1)/16, the midpoint near the far edge, a copy of -s at it) and quantised as O8-O10; the
+ * anchor (0,0,0) is stored as an outlier.  Level-serial: one launch per non-empty pass (<= 3 log2 S).
+ * Not sharded (donors cross any slab boundary): one GPU per field.
+ *
+ * sz3g_interp_compress -- arguments as sz3g_regression_compress (no coefficients), plus
+ *   xprime  out  prod(dims) T: the reconstruction x' (the method's working buffer; equal to what
+ *                sz3g_interp_decompress returns).
+ *   hist    nullable, 2R int64 bins ACCUMULATED (sz3g_histogram over the finished codes).
+ *   outlier_cap >= 1 (the anchor is always stored).
+ * Host errors: EINVAL, EUNSUPPORTED, ERANGE, ECUDA; device status bits as regression.
+ *
+ * sz3g_interp_decompress -- arguments as sz3g_regression_decompress (no coefficients): outlier
+ * values scattered into x_out first, then the passes in plan order.                              */
+int sz3g_interp_compress(const sz3g_grid* grid, const sz3g_params* params, const void* x, const double* d_minmax,
+                         uint16_t* codes, void* xprime, uint64_t* outlier_idx, void* outlier_val,
+                         uint64_t outlier_cap, unsigned long long* d_outlier_count, int64_t* hist,
+                         double* d_eb_abs, int32_t* d_status, sz3g_stream_t stream);
+int sz3g_interp_decompress(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax,
+                           const uint16_t* codes, const uint64_t* outlier_idx, const void* outlier_val,
+                           uint64_t n_outliers, const unsigned long long* d_outlier_count, void* x_out,
+                           sz3g_stream_t stream);
+
 /* a7 standalone -- histogram of n uint16 codes into 2R int64 bins, ACCUMULATED (+=).  Codes
  * >= 2R are ignored.  1 launch. */
 int sz3g_histogram(const uint16_t* codes, uint64_t n, uint32_t radius, int64_t* hist,

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "sz3g.cu")
 SRCS = [SRC, os.path.join(HERE, "csrc", "huffman.cu"), os.path.join(HERE, "csrc", "truncation.cu"),
         os.path.join(HERE, "csrc", "metrics.cu"), os.path.join(HERE, "csrc", "coefcode.cu"),
-        os.path.join(HERE, "csrc", "container.cu")]
+        os.path.join(HERE, "csrc", "container.cu"), os.path.join(HERE, "csrc", "interp.cu")]
 DEPS = [*SRCS, os.path.join(HERE, "csrc", "tile.cuh"), os.path.join(HERE, "csrc", "ptx.cuh"),
         os.path.join(HERE, "csrc", "lr.cuh"),
         os.path.join(ROOT, "include", "sz3g.h")]

@@ -1,0 +1,318 @@
+// libsz3g -- SZ3-Interp (NEXT-4): the multilevel interpolation predictor of PAPER.md P:852-853 ("Both
+// linear interpolation and cubic spline interpolation are included", "constant coefficients"), with
+// linear-scaling quantisation and reconstruction.  Definition: oracle/DEFINITION.md
+// I1-I6; readings G30-G33.
+//
+// The method is level-serial: a pass (s, d) predicts its targets from donors that earlier passes have
+// already RECONSTRUCTED, so passes run in plan order, one launch each, while the targets of one pass are
+// independent of one another (their donors are even multiples of s along d) and run fully in parallel:
+//   k_interp_anchor   the anchor (0,0,0) stored as an outlier; eb_abs / status; x'[0] = x[0]
+//   k_interp_pass<T, DEC>  one thread per target of pass (s, d): donors from x' at -3s, -s, +s, +3s along
+//                     d, cubic / linear / copy (I3), then O8-O10 (compress: code, x', outlier append
+//                     warp-aggregated) or the recovery (decompress: x' for code != 0)
+//   k_interp_scatter  decompress: outlier values into x' before the passes
+//   k_interp_final    outlier-capacity status
+// The histogram (O11) is the standalone sz3g_histogram over the finished codes.  Arithmetic is the
+// definition's, op for op (fp64, explicit __d*_rn, no contraction): bit-exact against the oracle.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/sz3g.h"
+#include "ptx.cuh"
+#include "tile.cuh"
+
+using namespace sz3g;
+
+namespace {
+
+std::atomic<uint64_t> g_ip_launches{0};
+
+struct IpArgs {
+  uint64_t n[3];          // extents
+  uint64_t st[3];         // element strides (n1 n2, n2, 1)
+  uint64_t first[3], step[3], cnt[3];   // the pass's targets along each axis
+  uint64_t s;             // stride of the level
+  int d;                  // axis of the pass
+  uint32_t R;
+  int eb_mode;
+  double eb;
+  const double* d_minmax;
+  double* d_eb_abs;
+  int32_t* d_status;
+  uint64_t gofs;          // dim0_offset * n1 * n2
+  uint64_t cap;
+};
+
+__device__ __forceinline__ bool ip_consts(const IpArgs& a, Consts& K) {
+  return make_consts(a.eb_mode, a.eb, a.d_minmax, 0.0, K);
+}
+
+// I3, op for op: u = b + c, v = a + e, p = (9 u - v) * 0.0625 | (b + c) * 0.5 | b
+__device__ __forceinline__ double ip_predict(double a, double b, double c, double e, int m) {
+  if (m == 2) return __dmul_rn(__dsub_rn(__dmul_rn(9.0, __dadd_rn(b, c)), __dadd_rn(a, e)), 0.0625);
+  if (m == 1) return __dmul_rn(__dadd_rn(b, c), 0.5);
+  return b;
+}
+
+template <typename T>
+__global__ void k_interp_anchor(const T* __restrict__ x, T* __restrict__ xp, uint16_t* __restrict__ codes,
+                                uint64_t* __restrict__ oidx, T* __restrict__ oval,
+                                unsigned long long* __restrict__ ocount, IpArgs a) {
+  Consts K;
+  const bool ok = ip_consts(a, K);
+  if (!ok && a.d_status) atomicOr(a.d_status, (int)SZ3G_STATUS_BAD_RANGE);
+  if (a.d_eb_abs) *a.d_eb_abs = ok ? K.eb_abs : __longlong_as_double(0x7ff8000000000000ll);
+  codes[0] = 0;
+  xp[0] = x[0];
+  const unsigned long long pos = atomicAdd(ocount, 1ull);
+  if (pos < a.cap) {
+    oidx[pos] = a.gofs;
+    oval[pos] = x[0];
+  }
+}
+
+template <typename T, bool DEC>
+__global__ void __launch_bounds__(256) k_interp_pass(const T* __restrict__ x, T* __restrict__ xp,
+                                                     uint16_t* __restrict__ codes, uint64_t* __restrict__ oidx,
+                                                     T* __restrict__ oval, unsigned long long* __restrict__ ocount,
+                                                     IpArgs a) {
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    Consts K;
+    s_ok = ip_consts(a, K);
+    s_k = K;
+  }
+  SZ3G_SYNCTHREADS();
+  if (!s_ok) return;
+  const Consts K = s_k;
+  const uint64_t sd = a.s * a.st[a.d];
+  const uint64_t nd = a.n[a.d];
+  const uint64_t t2 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t t0 = blockIdx.z; t0 < a.cnt[0]; t0 += gridDim.z)
+    for (uint64_t t1 = blockIdx.y; t1 < a.cnt[1]; t1 += gridDim.y) {
+      const bool live = t2 < a.cnt[2];
+      const uint64_t i0 = a.first[0] + t0 * a.step[0], i1 = a.first[1] + t1 * a.step[1];
+      const uint64_t i2 = a.first[2] + (live ? t2 : 0) * a.step[2];
+      const uint64_t e = i0 * a.st[0] + i1 * a.st[1] + i2 * a.st[2];
+      const uint64_t id = a.d == 0 ? i0 : (a.d == 1 ? i1 : i2);
+      const int m = (id >= 3 * a.s && id + 3 * a.s < nd) ? 2 : (id + a.s < nd ? 1 : 0);
+      bool is_out = false;
+      if (live) {
+        const uint16_t cin = DEC ? codes[e] : (uint16_t)1;
+        if (cin != 0) {
+          const double b = to_d<T>(xp[e - sd]);
+          const double c = m >= 1 ? to_d<T>(xp[e + sd]) : 0.0;
+          const double av = m == 2 ? to_d<T>(xp[e - 3 * sd]) : 0.0;
+          const double ev = m == 2 ? to_d<T>(xp[e + 3 * sd]) : 0.0;
+          const double p = ip_predict(av, b, c, ev, m);
+          if (DEC) {
+            // I6: x' = (T)(p + twoeb (code - R)), the product rounded first (no contraction)
+            const double q = (double)((int)cin - (int)a.R);
+            xp[e] = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, q)));
+          } else {
+            // I5 = O8-O10 (the exact definition; magic rint valid for |t| < 2^51, larger |t| or NaN fail
+            // the radius test exactly as in O8)
+            const T xv = x[e];
+            const double xd = to_d<T>(xv);
+            const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+            const double sm = __dadd_rn(t, RINT_MAGIC);
+            const double q = __dsub_rn(sm, RINT_MAGIC);
+            const T y = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, q)));
+            const bool ok = fabs(t) < (double)a.R && fabs(q) < (double)a.R &&
+                            fabs(__dsub_rn(to_d<T>(y), xd)) <= K.eb_abs;
+            codes[e] = ok ? (uint16_t)(__double2loint(sm) + (int)a.R) : (uint16_t)0;
+            xp[e] = ok ? y : xv;
+            is_out = !ok;
+          }
+        }
+      }
+      if (!DEC) {   // warp-aggregated outlier append (warp-uniform loop trip: t0, t1 shared by the block)
+        const uint32_t bal = __ballot_sync(0xffffffffu, is_out);
+        if (bal) {
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(ocount, (unsigned long long)__popc(bal));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (is_out) {
+            const unsigned long long pos = base + __popc(bal & ((1u << lane) - 1u));
+            if (pos < a.cap) {
+              oidx[pos] = a.gofs + e;
+              oval[pos] = x[e];
+            }
+          }
+        }
+      }
+    }
+}
+
+template <typename T>
+__global__ void k_interp_scatter(const uint64_t* __restrict__ idx, const T* __restrict__ val, uint64_t n,
+                                 const unsigned long long* __restrict__ d_n, uint64_t base, uint64_t N,
+                                 T* __restrict__ xo) {
+  const uint64_t cnt = d_n ? min((uint64_t)*d_n, n) : n;
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < cnt; o += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = idx[o] - base;
+    if (e < N) xo[e] = val[o];
+  }
+}
+
+__global__ void k_interp_final(const unsigned long long* ocount, uint64_t cap, int32_t* status) {
+  if (*ocount > cap) atomicOr(status, (int)SZ3G_STATUS_OUTLIER_OVERFLOW);
+}
+
+uint64_t top_stride(const uint64_t n[3]) {
+  const uint64_t m = std::max(n[0], std::max(n[1], n[2]));
+  uint64_t S = 1;
+  while (2 * S < m) S *= 2;
+  return m > 1 ? S : 0;
+}
+
+// I2: the targets of pass (s, d) along each axis
+bool pass_geometry(IpArgs& a, uint64_t s, int d) {
+  a.s = s;
+  a.d = d;
+  for (int ax = 0; ax < 3; ax++) {
+    a.first[ax] = ax == d ? s : 0;
+    a.step[ax] = ax >= d ? 2 * s : s;
+    a.cnt[ax] = a.first[ax] < a.n[ax] ? (a.n[ax] - 1 - a.first[ax]) / a.step[ax] + 1 : 0;
+  }
+  return a.cnt[0] && a.cnt[1] && a.cnt[2];
+}
+
+int ip_validate(const sz3g_grid* g, const sz3g_params* p) {
+  if (!g || !p) return SZ3G_EINVAL;
+  if (g->dtype != SZ3G_F32 && g->dtype != SZ3G_F64) return SZ3G_EUNSUPPORTED;
+  if (g->ndim < 1 || g->ndim > 3) return SZ3G_EUNSUPPORTED;
+  if (!g->dims[0] || !g->dims[1] || !g->dims[2]) return SZ3G_EINVAL;
+  if (p->block_size != 6) return SZ3G_EUNSUPPORTED;
+  if (p->radius < 1 || p->radius > 32768) return SZ3G_ERANGE;
+  if (p->eb_mode != SZ3G_EB_ABS && p->eb_mode != SZ3G_EB_REL_RANGE) return SZ3G_EINVAL;
+  if (!(p->eb > 0.0) || !(p->eb < 1e308)) return SZ3G_EINVAL;
+  return SZ3G_OK;
+}
+
+IpArgs base_args(const sz3g_grid* g, const sz3g_params* p, const double* d_minmax) {
+  IpArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int ax = 0; ax < 3; ax++) a.n[ax] = g->dims[ax];
+  a.st[0] = a.n[1] * a.n[2];
+  a.st[1] = a.n[2];
+  a.st[2] = 1;
+  a.R = p->radius;
+  a.eb_mode = (int)p->eb_mode;
+  a.eb = p->eb;
+  a.d_minmax = d_minmax;
+  a.gofs = g->dim0_offset * a.n[1] * a.n[2];
+  return a;
+}
+
+template <typename T, bool DEC>
+int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* oval, unsigned long long* ocount,
+               cudaStream_t st, int& nl) {
+  const uint64_t S = top_stride(a.n);
+  for (uint64_t s = S; s >= 1; s /= 2) {
+    for (int d = 0; d < 3; d++) {
+      if (!pass_geometry(a, s, d)) continue;
+      const dim3 grid((unsigned)((a.cnt[2] + 255) / 256), (unsigned)std::min<uint64_t>(a.cnt[1], 65535),
+                      (unsigned)std::min<uint64_t>(a.cnt[0], 65535));
+      k_interp_pass<T, DEC><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+      nl++;
+    }
+    if (s == 1) break;
+  }
+  return SZ3G_OK;
+}
+
+int ip_check(int nl) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return SZ3G_ECUDA;
+  g_ip_launches.fetch_add((uint64_t)nl, std::memory_order_relaxed);
+  return SZ3G_OK;
+}
+
+}  // namespace
+
+uint64_t sz3g_interp_launch_count_internal() { return g_ip_launches.load(); }
+
+extern "C" {
+
+int sz3g_interp_compress(const sz3g_grid* grid, const sz3g_params* params, const void* x, const double* d_minmax,
+                         uint16_t* codes, void* xprime, uint64_t* outlier_idx, void* outlier_val, uint64_t outlier_cap,
+                         unsigned long long* d_outlier_count, int64_t* hist, double* d_eb_abs, int32_t* d_status,
+                         sz3g_stream_t stream) {
+  int rc = ip_validate(grid, params);
+  if (rc) return rc;
+  if (!x || !codes || !xprime || !outlier_idx || !outlier_val || outlier_cap < 1 || !d_outlier_count || !d_status)
+    return SZ3G_EINVAL;
+  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  IpArgs a = base_args(grid, params, d_minmax);
+  a.d_eb_abs = d_eb_abs;
+  a.d_status = d_status;
+  a.cap = outlier_cap;
+  int nl = 0;
+  if (grid->dtype == SZ3G_F32) {
+    k_interp_anchor<float><<<1, 1, 0, st>>>((const float*)x, (float*)xprime, codes, outlier_idx, (float*)outlier_val,
+                                            d_outlier_count, a);
+    nl++;
+    a.d_eb_abs = nullptr;
+    a.d_status = nullptr;
+    run_passes<float, false>(a, (const float*)x, (float*)xprime, codes, outlier_idx, (float*)outlier_val,
+                             d_outlier_count, st, nl);
+  } else {
+    k_interp_anchor<double><<<1, 1, 0, st>>>((const double*)x, (double*)xprime, codes, outlier_idx,
+                                             (double*)outlier_val, d_outlier_count, a);
+    nl++;
+    a.d_eb_abs = nullptr;
+    a.d_status = nullptr;
+    run_passes<double, false>(a, (const double*)x, (double*)xprime, codes, outlier_idx, (double*)outlier_val,
+                              d_outlier_count, st, nl);
+  }
+  k_interp_final<<<1, 1, 0, st>>>(d_outlier_count, outlier_cap, d_status);
+  nl++;
+  rc = ip_check(nl);
+  if (rc) return rc;
+  if (hist) {
+    const uint64_t N = grid->dims[0] * grid->dims[1] * grid->dims[2];
+    return sz3g_histogram(codes, N, params->radius, hist, stream);
+  }
+  return SZ3G_OK;
+}
+
+int sz3g_interp_decompress(const sz3g_grid* grid, const sz3g_params* params, const double* d_minmax,
+                           const uint16_t* codes, const uint64_t* outlier_idx, const void* outlier_val,
+                           uint64_t n_outliers, const unsigned long long* d_outlier_count, void* x_out,
+                           sz3g_stream_t stream) {
+  int rc = ip_validate(grid, params);
+  if (rc) return rc;
+  if (!codes || !x_out || (n_outliers > 0 && (!outlier_idx || !outlier_val))) return SZ3G_EINVAL;
+  if (params->eb_mode == SZ3G_EB_REL_RANGE && !d_minmax) return SZ3G_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  IpArgs a = base_args(grid, params, d_minmax);
+  const uint64_t N = a.n[0] * a.n[1] * a.n[2];
+  int nl = 0;
+  uint16_t* cw = const_cast<uint16_t*>(codes);   // read-only in the decompress instantiation
+  if (grid->dtype == SZ3G_F32) {
+    if (n_outliers) {
+      k_interp_scatter<float><<<(unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096), 256, 0, st>>>(
+          outlier_idx, (const float*)outlier_val, n_outliers, d_outlier_count, a.gofs, N, (float*)x_out);
+      nl++;
+    }
+    run_passes<float, true>(a, nullptr, (float*)x_out, cw, nullptr, nullptr, nullptr, st, nl);
+  } else {
+    if (n_outliers) {
+      k_interp_scatter<double><<<(unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096), 256, 0, st>>>(
+          outlier_idx, (const double*)outlier_val, n_outliers, d_outlier_count, a.gofs, N, (double*)x_out);
+      nl++;
+    }
+    run_passes<double, true>(a, nullptr, (double*)x_out, cw, nullptr, nullptr, nullptr, st, nl);
+  }
+  return ip_check(nl);
+}
+
+}  // extern "C"

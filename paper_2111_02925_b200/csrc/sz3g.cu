@@ -33,6 +33,7 @@ uint64_t sz3g_huffman_launch_count_internal();      // huffman.cu
 uint64_t sz3g_truncation_launch_count_internal();   // truncation.cu
 uint64_t sz3g_metrics_launch_count_internal();      // metrics.cu
 uint64_t sz3g_coefcode_launch_count_internal();     // coefcode.cu
+uint64_t sz3g_interp_launch_count_internal();       // interp.cu
 
 namespace {
 
@@ -1733,7 +1734,8 @@ int sz3g_uses_tma(const sz3g_grid* grid, int decompress) {
 
 uint64_t sz3g_launch_count(void) {
   return g_launches.load() + sz3g_huffman_launch_count_internal() + sz3g_truncation_launch_count_internal() +
-         sz3g_metrics_launch_count_internal() + sz3g_coefcode_launch_count_internal();
+         sz3g_metrics_launch_count_internal() + sz3g_coefcode_launch_count_internal() +
+         sz3g_interp_launch_count_internal();
 }
 
 int sz3g_set_tuning(const char* key, int64_t value) {

@@ -123,6 +123,9 @@ def load(allow_build: bool = False):
     if hasattr(lib, "sz3g_lr_quantize"):   # absent only in older A/B builds
         lib.sz3g_lr_quantize.argtypes = [GP, PP, P, P, P, P, P, P, P, P, U64, P, P, P, P, P]
         lib.sz3g_lr_decompress.argtypes = [GP, PP, P, P, P, P, P, P, U64, P, P, P]
+    if hasattr(lib, "sz3g_interp_compress"):   # absent only in older A/B builds
+        lib.sz3g_interp_compress.argtypes = [GP, PP, P, P, P, P, P, P, U64, P, P, P, P, P]
+        lib.sz3g_interp_decompress.argtypes = [GP, PP, P, P, P, P, U64, P, P, P]
     if hasattr(lib, "sz3g_tie_counts"):   # absent only in older A/B builds
         lib.sz3g_tie_counts.argtypes = [GP, PP, P, P, P, P, P, P]
     if hasattr(lib, "sz3g_stream_validate"):
@@ -147,7 +150,8 @@ EXPORTED_SYMBOLS = ("sz3g_value_range", "sz3g_regression_compress", "sz3g_regres
                     "sz3g_truncation_decompress", "sz3g_error_stats_scratch_bytes", "sz3g_error_stats",
                     "sz3g_coef_delta_scratch_bytes", "sz3g_coef_delta_encode", "sz3g_coef_delta_decode",
                     "sz3g_huffman_codebook_from_lengths", "sz3g_stream_size", "sz3g_stream_write",
-                    "sz3g_stream_read", "sz3g_stream_validate", "sz3g_tie_counts", "sz3g_lr_quantize", "sz3g_lr_decompress",
+                    "sz3g_stream_read", "sz3g_stream_validate", "sz3g_tie_counts", "sz3g_interp_compress",
+                    "sz3g_interp_decompress", "sz3g_lr_quantize", "sz3g_lr_decompress",
                     "sz3g_num_blocks", "sz3g_uses_tma", "sz3g_launch_count", "sz3g_set_tuning", "sz3g_strerror",
                     "sz3g_last_cuda_error", "sz3g_version")
 
@@ -489,6 +493,88 @@ def histogram_bins(codes: torch.Tensor, nbins: int, window_lo: int = 0, hist: to
     _check(load().sz3g_histogram_bins(_ptr(codes), codes.numel(), nbins, window_lo, _ptr(hist), _stream(stream)),
            "sz3g_histogram_bins")
     return hist
+
+
+# ------------------------------------------------------------------------------------------- SZ3-Interp
+@dataclass
+class InterpCompressed:
+    """sz3g_interp_compress outputs (device).  ``xprime`` is the compress-time reconstruction."""
+    shape: tuple
+    dtype: torch.dtype
+    radius: int
+    dim0_offset: int
+    codes: torch.Tensor
+    xprime: torch.Tensor
+    outlier_idx: torch.Tensor
+    outlier_val: torch.Tensor
+    outlier_count: torch.Tensor
+    hist: torch.Tensor | None
+    eb_abs_dev: torch.Tensor
+    status: torch.Tensor
+    n_outliers: int | None = None
+    eb_abs: float | None = None
+
+    def finalize(self) -> "InterpCompressed":
+        st = int(self.status.item())
+        cnt = int(self.outlier_count.item())
+        if st & STATUS_BAD_RANGE:
+            raise SZ3GError("bad value range: eb_abs is not finite or <= 0")
+        if st & STATUS_OUTLIER_OVERFLOW:
+            raise SZ3GError(f"outlier capacity {self.outlier_idx.numel()} exceeded ({cnt} outliers)")
+        self.n_outliers = cnt
+        self.eb_abs = float(self.eb_abs_dev.item())
+        return self
+
+
+def interp_compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: int = 32768,
+                    d_minmax: torch.Tensor | None = None, outlier_cap: int | None = None, hist: bool = True,
+                    out: "InterpCompressed | None" = None, stream=None) -> InterpCompressed:
+    """sz3g_interp_compress (SZ3-Interp; DEFINITION.md I1-I5), asynchronous.  REL mode without a
+    given device range computes it with value_range.  ``out`` reuses a previous result's buffers."""
+    _require_cuda(x, d_minmax)
+    dev = x.device
+    if out is None:
+        N = x.numel()
+        cap = outlier_cap if outlier_cap is not None else max(4096, N // 64)
+        out = InterpCompressed(tuple(x.shape), x.dtype, radius, 0, torch.empty(tuple(x.shape), dtype=torch.uint16, device=dev),
+                               torch.empty_like(x), torch.empty(cap, dtype=torch.int64, device=dev),
+                               torch.empty(cap, dtype=x.dtype, device=dev), torch.zeros(1, dtype=torch.int64, device=dev),
+                               torch.zeros(2 * radius, dtype=torch.int64, device=dev) if hist else None,
+                               torch.zeros(1, dtype=torch.float64, device=dev), torch.zeros(1, dtype=torch.int32, device=dev))
+    else:
+        out.outlier_count.zero_()
+        out.status.zero_()
+        if out.hist is not None:
+            out.hist.zero_()
+        out.n_outliers = out.eb_abs = None
+    if eb_mode == "rel" and d_minmax is None:
+        d_minmax = value_range(x, stream=stream)
+    g = make_grid(x.shape, x.dtype)
+    p = make_params(eb, eb_mode, radius)
+    rc = load().sz3g_interp_compress(ctypes.byref(g), ctypes.byref(p), _ptr(x), _ptr(d_minmax), _ptr(out.codes),
+                                     _ptr(out.xprime), _ptr(out.outlier_idx), _ptr(out.outlier_val),
+                                     out.outlier_idx.numel(), _ptr(out.outlier_count), _ptr(out.hist), _ptr(out.eb_abs_dev),
+                                     _ptr(out.status), _stream(stream))
+    _check(rc, "sz3g_interp_compress")
+    out._minmax = d_minmax
+    return out
+
+
+def interp_decompress(codes: torch.Tensor, outlier_idx: torch.Tensor, outlier_val: torch.Tensor, n_outliers: int,
+                      eb: float, radius: int = 32768, dtype: torch.dtype = torch.float32, out: torch.Tensor | None = None,
+                      d_outlier_count: torch.Tensor | None = None, eb_mode: str = "abs",
+                      d_minmax: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sz3g_interp_decompress (I6), asynchronous; arguments as regression_decompress."""
+    _require_cuda(codes, outlier_idx, outlier_val, out, d_outlier_count, d_minmax)
+    if out is None:
+        out = torch.empty(codes.shape, dtype=dtype, device=codes.device)
+    g = make_grid(codes.shape, out.dtype)
+    p = make_params(eb, eb_mode, radius)
+    rc = load().sz3g_interp_decompress(ctypes.byref(g), ctypes.byref(p), _ptr(d_minmax), _ptr(codes), _ptr(outlier_idx),
+                                       _ptr(outlier_val), int(n_outliers), _ptr(d_outlier_count), _ptr(out),
+                                       _stream(stream))
+    _check(rc, "sz3g_interp_decompress")
+    return out
 
 
 TIE_COUNTER_NAMES = ("elem_near_ties", "elem_div_mismatch", "coef_near_ties", "coef_tie_blocks")

@@ -77,6 +77,10 @@ def cases():
                 lr = sz3g.lr_compress(x, 1e-3, "rel", R, outlier_cap=x.numel(), flags=flags)
                 out[f"{tag}/lr"] = h(lr.codes, lr.coef_codes, lr.lr_flags, lr.hist, *outliers(lr))
                 out[f"{tag}/lr_dec"] = h(sz3g.decompress(lr, flags=flags))
+        ir = sz3g.interp_compress(x, 1e-3, "rel", 64, outlier_cap=x.numel()).finalize()
+        out[f"{name}/interp"] = h(ir.codes, ir.xprime, ir.hist, *outliers(ir))
+        out[f"{name}/interp_dec"] = h(sz3g.interp_decompress(ir.codes, ir.outlier_idx, ir.outlier_val, ir.n_outliers,
+                                                             ir.eb_abs, 64, x.dtype))
         out[f"{name}/value_range"] = h(sz3g.value_range(x))
         res = sz3g.compress(x, 1e-3, "rel", 32768)
         out[f"{name}/histogram"] = h(sz3g.histogram(res.codes.view(-1), 32768))
