@@ -150,6 +150,199 @@ __global__ void __launch_bounds__(256) k_interp_pass(const T* __restrict__ x, T*
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Level s = 1 fused (its three passes hold 7/8 of the targets): one CTA per tile of 2 planes (i0 even,
+// i0 + 1) x L1_TJ rows x L1_TK columns, in shared memory with a halo of 2 even coordinates along j and k
+// (the -+1, -+3 donors).  Pass (1,0) targets (i odd, j and k even) are computed over the whole halo box
+// (redundantly with the neighbour tiles: the same inputs, the same IEEE operations, the same x'),
+// pass (1,1) targets (j odd, k even) over the tile's rows and the box's columns, pass (1,2) targets
+// (k odd) over the tile; the (1,0) donors (level >= 2 points of planes i0 - 2 .. i0 + 4) come from x'
+// in global memory, every other donor from the box.  Work is split as one warp per row, lanes along k,
+// so a row's global loads and stores are contiguous.  The tile's x' and codes leave as full rows (the
+// level >= 2 points' values and codes rewritten unchanged), so no write is a partial sector.  Same
+// prediction and quantisation as k_interp_pass, op for op: bit-identical to the per-pass schedule.
+constexpr int L1_TJ = 16, L1_TK = 128, L1_BJ = L1_TJ + 6, L1_BK = L1_TK + 6, L1_WARPS = 16;
+
+template <typename T>
+struct L1Smem {
+  static constexpr size_t box = 2ull * L1_BJ * L1_BK;
+  static constexpr size_t off_x = box * sizeof(T);
+  static constexpr size_t off_c = off_x + box * sizeof(T);
+  static constexpr size_t total = off_c + box * sizeof(uint16_t);
+};
+
+template <typename T, bool DEC>
+__global__ void __launch_bounds__(L1_WARPS * 32) k_interp_l1(const T* __restrict__ x, T* __restrict__ xp,
+                                                             uint16_t* __restrict__ codes, uint64_t* __restrict__ oidx,
+                                                             T* __restrict__ oval, unsigned long long* __restrict__ ocount,
+                                                             IpArgs a) {
+  extern __shared__ __align__(16) uint8_t l1sm[];
+  T* sE = reinterpret_cast<T*>(l1sm);                                   // x' of the box [2][BJ][BK]
+  T* sX = reinterpret_cast<T*>(l1sm + L1Smem<T>::off_x);               // x of the box (compress)
+  uint16_t* sC = reinterpret_cast<uint16_t*>(l1sm + L1Smem<T>::off_c);  // codes of the box
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    Consts K;
+    s_ok = ip_consts(a, K);
+    s_k = K;
+  }
+  const int n0 = (int)a.n[0], n1 = (int)a.n[1], n2 = (int)a.n[2];
+  const int I0 = 2 * (int)blockIdx.z, J0 = L1_TJ * (int)blockIdx.y, K0 = L1_TK * (int)blockIdx.x;
+  const int jb = J0 - 2, kb = K0 - 2;   // box origin (even)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto at = [](int bi, int bj, int bk) { return (bi * L1_BJ + bj) * L1_BK + bk; };
+  auto rowe = [&](int i, int j) { return ((uint64_t)i * (uint64_t)n1 + (uint64_t)j) * (uint64_t)n2; };
+  // (1) load the box, one warp per row: x (compress) or codes (decompress) everywhere, x' at the level >= 2
+  // points (all coordinates even) and, decompressing, at the code-0 targets (their scattered outlier values)
+  for (int r = warp; r < 2 * L1_BJ; r += L1_WARPS) {
+    const int bi = r / L1_BJ, bj = r - bi * L1_BJ, i = I0 + bi, j = jb + bj;
+    if (i >= n0 || j < 0 || j >= n1) continue;
+    const uint64_t re = rowe(i, j);
+    const bool l2row = ((i | j) & 1) == 0;
+    for (int bk = lane; bk < L1_BK; bk += 32) {
+      const int k = kb + bk;
+      if (k < 0 || k >= n2) continue;
+      const uint64_t e = re + (uint64_t)k;
+      const bool l2 = l2row && (k & 1) == 0;
+      const int o = at(bi, bj, bk);
+      uint16_t c = 1;
+      if (DEC || l2) c = codes[e];
+      sC[o] = c;
+      if (!DEC) sX[o] = x[e];
+      if (l2 || (DEC && c == 0)) sE[o] = xp[e];
+    }
+  }
+  SZ3G_SYNCTHREADS();
+  if (!s_ok) return;
+  const Consts K = s_k;
+  // one target at box offset o: quantise (compress) or recover (decompress); returns "own outlier"
+  auto target = [&](int o, double av, double bv, double cv, double ev, int m, bool own) -> bool {
+    const double p = ip_predict(av, bv, cv, ev, m);
+    if (DEC) {
+      const uint16_t c = sC[o];
+      if (c != 0) sE[o] = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)c - (int)a.R))));
+      return false;
+    }
+    const T xv = sX[o];
+    const double xd = to_d<T>(xv);
+    const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+    const double sm = __dadd_rn(t, RINT_MAGIC);
+    const double qd = __dsub_rn(sm, RINT_MAGIC);
+    const T y = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, qd)));
+    const bool ok = fabs(t) < (double)a.R && fabs(qd) < (double)a.R && fabs(__dsub_rn(to_d<T>(y), xd)) <= K.eb_abs;
+    sE[o] = ok ? y : xv;
+    if (own) sC[o] = ok ? (uint16_t)(__double2loint(sm) + (int)a.R) : (uint16_t)0;
+    return own && !ok;
+  };
+  auto append = [&](bool is_out, uint64_t e, int o) {   // warp-aggregated outlier append (all lanes call)
+    if (DEC) return;
+    const uint32_t bal = __ballot_sync(0xffffffffu, is_out);
+    if (!bal) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(ocount, (unsigned long long)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (is_out) {
+      const unsigned long long pos = base + __popc(bal & ((1u << lane) - 1u));
+      if (pos < a.cap) {
+        oidx[pos] = a.gofs + e;
+        oval[pos] = sX[o];
+      }
+    }
+  };
+  const uint64_t p1 = (uint64_t)n1 * n2;
+  // (2) pass (1,0): plane i = I0 + 1, j and k even over the box; donors i -+ 1, -+ 3 (plane I0 from the
+  // box, the others from global x')
+  if (I0 + 1 < n0) {
+    const int i = I0 + 1;
+    const int m = (i >= 3 && i + 3 < n0) ? 2 : (i + 1 < n0 ? 1 : 0);
+    for (int r = warp; r < L1_BJ / 2; r += L1_WARPS) {
+      const int bj = 2 * r, j = jb + bj;
+      const bool rowok = j >= 0 && j < n1;
+      const uint64_t re = rowok ? rowe(i, j) : 0;
+      const bool ownrow = j >= J0 && j < J0 + L1_TJ;
+      for (int h = lane; h < (L1_BK + 1) / 2 + 31 - ((L1_BK + 1) / 2 + 31) % 32; h += 32) {   // warp-uniform trips
+        const int bk = 2 * h, k = kb + bk;
+        const bool live = rowok && h < (L1_BK + 1) / 2 && k >= 0 && k < n2;
+        bool out = false;
+        uint64_t e = 0;
+        const int o = at(1, bj, bk);
+        if (live) {
+          e = re + (uint64_t)k;
+          const double bv = to_d<T>(sE[at(0, bj, bk)]);
+          const double cv = m >= 1 ? to_d<T>(xp[e + p1]) : 0.0;
+          const double av = m == 2 ? to_d<T>(xp[e - 3 * p1]) : 0.0;
+          const double ev = m == 2 ? to_d<T>(xp[e + 3 * p1]) : 0.0;
+          out = target(o, av, bv, cv, ev, m, ownrow && k >= K0 && k < K0 + L1_TK);
+        }
+        append(out, e, o);
+      }
+    }
+  }
+  SZ3G_SYNCTHREADS();
+  // (3) pass (1,1): both planes, j odd in the tile, k even over the box; donors j -+ 1, -+ 3 in the box
+  for (int r = warp; r < 2 * (L1_TJ / 2); r += L1_WARPS) {
+    const int bi = r / (L1_TJ / 2), bj = 3 + 2 * (r % (L1_TJ / 2)), i = I0 + bi, j = jb + bj;
+    const bool rowok = i < n0 && j < n1;
+    const uint64_t re = rowok ? rowe(i, j) : 0;
+    const int m = (j >= 3 && j + 3 < n1) ? 2 : (j + 1 < n1 ? 1 : 0);
+    for (int h = lane; h < (L1_BK + 1) / 2 + 31 - ((L1_BK + 1) / 2 + 31) % 32; h += 32) {
+      const int bk = 2 * h, k = kb + bk;
+      const bool live = rowok && h < (L1_BK + 1) / 2 && k >= 0 && k < n2;
+      bool out = false;
+      uint64_t e = 0;
+      const int o = at(bi, bj, bk);
+      if (live) {
+        e = re + (uint64_t)k;
+        const double bv = to_d<T>(sE[o - L1_BK]);
+        const double cv = m >= 1 ? to_d<T>(sE[o + L1_BK]) : 0.0;
+        const double av = m == 2 ? to_d<T>(sE[o - 3 * L1_BK]) : 0.0;
+        const double ev = m == 2 ? to_d<T>(sE[o + 3 * L1_BK]) : 0.0;
+        out = target(o, av, bv, cv, ev, m, k >= K0 && k < K0 + L1_TK);
+      }
+      append(out, e, o);
+    }
+  }
+  SZ3G_SYNCTHREADS();
+  // (4) pass (1,2): the tile's rows, k odd; donors k -+ 1, -+ 3 in the box
+  for (int r = warp; r < 2 * L1_TJ; r += L1_WARPS) {
+    const int bi = r / L1_TJ, bj = 2 + r % L1_TJ, i = I0 + bi, j = jb + bj;
+    const bool rowok = i < n0 && j < n1;
+    const uint64_t re = rowok ? rowe(i, j) : 0;
+    for (int h = lane; h < L1_TK / 2; h += 32) {
+      const int bk = 3 + 2 * h, k = kb + bk;
+      const bool live = rowok && k < n2;
+      bool out = false;
+      uint64_t e = 0;
+      const int o = at(bi, bj, bk);
+      if (live) {
+        e = re + (uint64_t)k;
+        const int m = (k >= 3 && k + 3 < n2) ? 2 : (k + 1 < n2 ? 1 : 0);
+        const double bv = to_d<T>(sE[o - 1]);
+        const double cv = m >= 1 ? to_d<T>(sE[o + 1]) : 0.0;
+        const double av = m == 2 ? to_d<T>(sE[o - 3]) : 0.0;
+        const double ev = m == 2 ? to_d<T>(sE[o + 3]) : 0.0;
+        out = target(o, av, bv, cv, ev, m, true);
+      }
+      append(out, e, o);
+    }
+  }
+  SZ3G_SYNCTHREADS();
+  // (5) the tile's rows out: x' (and the codes, compressing), level >= 2 points rewritten unchanged
+  for (int r = warp; r < 2 * L1_TJ; r += L1_WARPS) {
+    const int bi = r / L1_TJ, tj = r % L1_TJ, i = I0 + bi, j = J0 + tj;
+    if (i >= n0 || j >= n1) continue;
+    const uint64_t re = rowe(i, j);
+    for (int tk = lane; tk < L1_TK; tk += 32) {
+      const int k = K0 + tk;
+      if (k >= n2) break;
+      const int o = at(bi, tj + 2, tk + 2);
+      xp[re + k] = sE[o];
+      if (!DEC) codes[re + k] = sC[o];
+    }
+  }
+}
+
 template <typename T>
 __global__ void k_interp_scatter(const uint64_t* __restrict__ idx, const T* __restrict__ val, uint64_t n,
                                  const unsigned long long* __restrict__ d_n, uint64_t base, uint64_t N,
@@ -211,11 +404,28 @@ IpArgs base_args(const sz3g_grid* g, const sz3g_params* p, const double* d_minma
   return a;
 }
 
+#ifndef SZ3G_IP_L1
+#define SZ3G_IP_L1 0   // 1: level 1 in the fused tile kernel (bit-exact; c5 46.9 vs 43.8 ms compress for the
+                       // three per-pass launches: 226 instructions per element, issue-bound; kept for A/B)
+#endif
+
 template <typename T, bool DEC>
 int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* oval, unsigned long long* ocount,
                cudaStream_t st, int& nl) {
   const uint64_t S = top_stride(a.n);
   for (uint64_t s = S; s >= 1; s /= 2) {
+    if (s == 1 && SZ3G_IP_L1 && (a.n[0] + 1) / 2 <= 65535 && (a.n[1] + L1_TJ - 1) / L1_TJ <= 65535 &&
+        a.n[0] < (1ull << 31) && a.n[1] < (1ull << 31) && a.n[2] < (1ull << 31)) {
+      const dim3 grid((unsigned)((a.n[2] + L1_TK - 1) / L1_TK), (unsigned)((a.n[1] + L1_TJ - 1) / L1_TJ),
+                      (unsigned)((a.n[0] + 1) / 2));
+      auto kern = k_interp_l1<T, DEC>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L1Smem<T>::total) !=
+          cudaSuccess)
+        return SZ3G_ECUDA;
+      kern<<<grid, L1_WARPS * 32, L1Smem<T>::total, st>>>(x, xp, codes, oidx, oval, ocount, a);
+      nl++;
+      break;
+    }
     for (int d = 0; d < 3; d++) {
       if (!pass_geometry(a, s, d)) continue;
       const dim3 grid((unsigned)((a.cnt[2] + 255) / 256), (unsigned)std::min<uint64_t>(a.cnt[1], 65535),
@@ -262,16 +472,18 @@ int sz3g_interp_compress(const sz3g_grid* grid, const sz3g_params* params, const
     nl++;
     a.d_eb_abs = nullptr;
     a.d_status = nullptr;
-    run_passes<float, false>(a, (const float*)x, (float*)xprime, codes, outlier_idx, (float*)outlier_val,
+    rc = run_passes<float, false>(a, (const float*)x, (float*)xprime, codes, outlier_idx, (float*)outlier_val,
                              d_outlier_count, st, nl);
+    if (rc) return rc;
   } else {
     k_interp_anchor<double><<<1, 1, 0, st>>>((const double*)x, (double*)xprime, codes, outlier_idx,
                                              (double*)outlier_val, d_outlier_count, a);
     nl++;
     a.d_eb_abs = nullptr;
     a.d_status = nullptr;
-    run_passes<double, false>(a, (const double*)x, (double*)xprime, codes, outlier_idx, (double*)outlier_val,
+    rc = run_passes<double, false>(a, (const double*)x, (double*)xprime, codes, outlier_idx, (double*)outlier_val,
                               d_outlier_count, st, nl);
+    if (rc) return rc;
   }
   k_interp_final<<<1, 1, 0, st>>>(d_outlier_count, outlier_cap, d_status);
   nl++;
@@ -303,14 +515,16 @@ int sz3g_interp_decompress(const sz3g_grid* grid, const sz3g_params* params, con
           outlier_idx, (const float*)outlier_val, n_outliers, d_outlier_count, a.gofs, N, (float*)x_out);
       nl++;
     }
-    run_passes<float, true>(a, nullptr, (float*)x_out, cw, nullptr, nullptr, nullptr, st, nl);
+    rc = run_passes<float, true>(a, nullptr, (float*)x_out, cw, nullptr, nullptr, nullptr, st, nl);
+    if (rc) return rc;
   } else {
     if (n_outliers) {
       k_interp_scatter<double><<<(unsigned)std::min<uint64_t>((n_outliers + 255) / 256, 4096), 256, 0, st>>>(
           outlier_idx, (const double*)outlier_val, n_outliers, d_outlier_count, a.gofs, N, (double*)x_out);
       nl++;
     }
-    run_passes<double, true>(a, nullptr, (double*)x_out, cw, nullptr, nullptr, nullptr, st, nl);
+    rc = run_passes<double, true>(a, nullptr, (double*)x_out, cw, nullptr, nullptr, nullptr, st, nl);
+    if (rc) return rc;
   }
   return ip_check(nl);
 }
