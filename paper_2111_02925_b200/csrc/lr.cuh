@@ -530,6 +530,11 @@ constexpr int LRD_JU = SZ3G_LRD_JU;   // unroll of the regression phase's row lo
 #ifndef SZ3G_LRD_SPLIT
 #define SZ3G_LRD_SPLIT 1
 #endif
+#ifndef SZ3G_LRD_COMPACT
+#define SZ3G_LRD_COMPACT 0   // 1: Lorenzo blocks in their own pass over a warp-compacted block list (below;
+                             // bit-exact, measured 8.8 vs 6.5 ms on c5: the tile pass without the recurrence
+                             // still takes 6.4 ms, the separate pass 2.3 ms)
+#endif
 template <typename T, bool FULL, bool IN_SMEM, typename QT = int64_t>
 __device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj,
                                                    const int32_t* __restrict__ coef,
@@ -609,7 +614,7 @@ __device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ 
       }
     }
   }
-  if (!__any_sync(0xffffffffu, lor)) return false;
+  if (SZ3G_LRD_COMPACT || !__any_sync(0xffffffffu, lor)) return false;   // COMPACT: k_lr_lorenzo_blocks
 #endif
   // P[j] = q of row j of the previous plane; C = q of the previous row of this plane.  Row j needs
   // P[j] and P[j - 1]; once it is done P[j - 1] is free and takes this plane's row j - 1.
@@ -682,6 +687,104 @@ __device__ __forceinline__ bool lr_decompress_tile(const uint16_t* __restrict__ 
     for (int kk = 0; kk < 3; kk++) P[BS - 1][kk] = C[kk];
   }
   return wide;
+}
+
+// L7 for the Lorenzo blocks alone (SZ3G_LRD_COMPACT): the tile decompressor writes only the regression
+// blocks, and this pass runs the recurrence for the Lorenzo blocks (5.4% of c5's blocks) instead of in
+// every lane of every tile that holds one (58% of c5's tiles).  A warp scans the flags of 16 consecutive
+// blocks, compacts the Lorenzo ones by ballot and gives each two lanes (columns 0-2 / 3-5, the tile
+// decompressor's lane pairs, so the recurrence and its carry shuffle are the same), reading codes from
+// global memory; int64 throughout.  Outliers: their stored values were scattered first (L7).
+constexpr int LRL_WARPS = 8, LRL_GROUP = 512;
+template <typename T>
+__global__ void __launch_bounds__(LRL_WARPS * 32) k_lr_lorenzo_blocks(const uint16_t* __restrict__ codes,
+                                                                     const uint8_t* __restrict__ flags,
+                                                                     T* __restrict__ xo, KArgs a) {
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  __shared__ uint32_t s_list[LRL_WARPS][LRL_GROUP];   // a warp's compacted Lorenzo blocks (group offsets)
+  if (!cta_consts(a, &s_k, &s_ok)) return;
+  const Consts K = s_k;
+  const Geo& g = a.g;
+  const uint32_t R = a.R;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  uint32_t* list = s_list[wl];
+  const uint64_t nb = (uint64_t)g.NB0 * g.NB1 * g.NB2;
+  const uint64_t ngroups = (nb + LRL_GROUP - 1) / LRL_GROUP;
+  const uint64_t warps = (uint64_t)gridDim.x * LRL_WARPS;
+  for (uint64_t grp = blockIdx.x * (uint64_t)LRL_WARPS + wl; grp < ngroups; grp += warps) {
+    const uint64_t b0 = grp * LRL_GROUP;
+    // compact the group's Lorenzo blocks (ballot per 32 flags)
+    uint32_t nl = 0;
+    for (int q = 0; q < LRL_GROUP; q += 32) {
+      const bool is = b0 + q + lane < nb && flags[b0 + q + lane] != 0;
+      const uint32_t bal = __ballot_sync(0xffffffffu, is);
+      if (is) list[nl + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)(q + lane);
+      nl += __popc(bal);
+    }
+    SZ3G_SYNCWARP();
+    // batches of 16 blocks: lane pair (2 r, 2 r + 1) takes block r of the batch
+    for (uint32_t s0 = 0; s0 < nl; s0 += 16) {
+      const int rnk = lane >> 1, h = lane & 1;
+      const bool act = s0 + rnk < nl;
+      const uint64_t bid = b0 + (act ? list[s0 + rnk] : 0u);
+      const uint64_t bc = bid % g.NB2, bab = bid / g.NB2, bb = bab % g.NB1, ba = bab / g.NB1;
+      const int m0 = (int)umin64(BS, g.n0 - ba * BS), m1 = (int)umin64(BS, g.n1 - bb * BS);
+      const int m2 = (int)umin64(BS, g.n2 - bc * BS);
+      const uint64_t gbase = ((ba * BS) * g.n1 + bb * BS) * g.n2 + bc * BS + 3 * h;
+      int64_t P[BS][3];
+#pragma unroll
+      for (int j = 0; j < BS; j++) P[j][0] = P[j][1] = P[j][2] = 0;
+      for (int i = 0; i < BS; i++) {
+        // the plane's 6 x 3 codes of this lane, loaded together (independent of the recurrence)
+        uint32_t c[BS][3];
+#pragma unroll
+        for (int j = 0; j < BS; j++)
+#pragma unroll
+          for (int kk = 0; kk < 3; kk++) {
+            const bool v = act && i < m0 && j < m1 && 3 * h + kk < m2;
+            c[j][kk] = v ? (uint32_t)codes[gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk] : 0xffffffffu;
+          }
+        int64_t C[3] = {0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < BS; j++) {
+          const uint64_t e0 = gbase + ((uint64_t)i * g.n1 + j) * g.n2;
+          int64_t r[3], base[3];
+          bool nocarry[3];
+          int64_t run = 0;
+          bool cut = false;
+#pragma unroll
+          for (int kk = 0; kk < 3; kk++) {
+            const bool valid = c[j][kk] != 0xffffffffu;
+            base[kk] = P[j][kk] + C[kk] - (j > 0 ? P[j - 1][kk] : 0);
+            if (valid && c[j][kk] == 0) {
+              bool ok;
+              const double qd = lr_prequant(to_d<T>(xo[e0 + kk]), K, ok);
+              run = (int64_t)__double2ll_rn(qd) - base[kk];
+              cut = true;
+            } else {
+              run += valid ? (int64_t)c[j][kk] - (int64_t)R : (int64_t)0;
+            }
+            r[kk] = run;
+            nocarry[kk] = cut;
+          }
+          int64_t carry = __shfl_up_sync(0xffffffffu, r[2], 1);
+          if (h == 0) carry = 0;
+#pragma unroll
+          for (int kk = 0; kk < 3; kk++) {
+            const bool valid = c[j][kk] != 0xffffffffu;
+            const int64_t q = valid ? (nocarry[kk] ? r[kk] : r[kk] + carry) + base[kk] : 0;
+            if (valid && c[j][kk] != 0) xo[e0 + kk] = from_d<T>(__dmul_rn(K.twoeb, (double)q));
+            if (j > 0) P[j - 1][kk] = C[kk];
+            C[kk] = q;
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 3; kk++) P[BS - 1][kk] = C[kk];
+      }
+    }
+    SZ3G_SYNCWARP();
+  }
 }
 
 constexpr int LR_DW = 4;   // decompress: warps per CTA

@@ -1665,6 +1665,14 @@ int sz3g_lr_decompress(const sz3g_grid* grid, const sz3g_params* params, const d
     else k_lr_decompress<double><<<blocks, LR_DW * 32, 0, st>>>(codes, coef_codes, flags, (double*)x_out, ka);
   }
   launched++;
+  if (SZ3G_LRD_COMPACT) {   // the Lorenzo blocks (after the regression blocks: disjoint elements)
+    const uint64_t ngroups = (sz3g_num_blocks(grid, BS) + LRL_GROUP - 1) / LRL_GROUP;
+    const unsigned blocks = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((ngroups + LRL_WARPS - 1) / LRL_WARPS, (uint64_t)sm_count() * 16));
+    if (grid->dtype == SZ3G_F32) k_lr_lorenzo_blocks<float><<<blocks, LRL_WARPS * 32, 0, st>>>(codes, flags, (float*)x_out, ka);
+    else k_lr_lorenzo_blocks<double><<<blocks, LRL_WARPS * 32, 0, st>>>(codes, flags, (double*)x_out, ka);
+    launched++;
+  }
   return check_launch(launched);
 }
 
