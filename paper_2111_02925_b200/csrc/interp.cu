@@ -151,6 +151,106 @@ __global__ void __launch_bounds__(256) k_interp_pass(const T* __restrict__ x, T*
 }
 
 // ------------------------------------------------------------------------------------------------
+// Level s = 1 passes, one thread per PAIR of columns (k even, k + 1) of a row holding targets: the pass's
+// target in the pair is predicted and quantised (or recovered) exactly as in k_interp_pass, and the pair
+// is written back whole -- the other element's x' (and code) rewritten unchanged -- so every store covers
+// full sectors instead of every other element (the stride-2 stores of the per-target kernel doubled the
+// DRAM traffic through partial-sector read-modify-writes).  Pass axis d: 2 -> rows (i, j) all, target
+// k + 1; 1 -> rows (i, j odd), target k; 0 -> rows (i odd, j even), target k.
+template <typename T, bool DEC, int D>
+__global__ void __launch_bounds__(256) k_interp_pairs(const T* __restrict__ x, T* __restrict__ xp,
+                                                      uint16_t* __restrict__ codes, uint64_t* __restrict__ oidx,
+                                                      T* __restrict__ oval, unsigned long long* __restrict__ ocount,
+                                                      IpArgs a) {
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    Consts K;
+    s_ok = ip_consts(a, K);
+    s_k = K;
+  }
+  SZ3G_SYNCTHREADS();
+  if (!s_ok) return;
+  const Consts K = s_k;
+  const uint64_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2];
+  const uint64_t np = (n2 + 1) / 2;                       // pairs per row
+  const uint64_t m = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  // rows of the pass: D = 2: every (i, j); D = 1: (i, j odd); D = 0: (i odd, j even)
+  const uint64_t ni = D == 0 ? n0 / 2 : n0, nj = D == 2 ? n1 : (n1 / 2 + (D == 0 ? n1 % 2 : 0));
+  for (uint64_t rr = blockIdx.y; rr < ni * nj; rr += gridDim.y) {
+    const uint64_t ti = rr / nj, tj = rr - ti * nj;
+    const uint64_t i = D == 0 ? 2 * ti + 1 : ti;
+    const uint64_t j = D == 2 ? tj : (D == 1 ? 2 * tj + 1 : 2 * tj);
+    const bool live = m < np;
+    const uint64_t k0 = 2 * (live ? m : 0);
+    const uint64_t kt = D == 2 ? k0 + 1 : k0;             // the target column
+    const bool has_t = live && kt < n2;
+    const bool has_pair = live && k0 + 1 < n2;
+    const uint64_t re = (i * n1 + j) * n2;
+    const uint64_t e = re + kt;
+    bool is_out = false;
+    T xnew = T(0), xold = T(0);
+    uint16_t cnew = 0;
+    if (has_t) {
+      const uint64_t eo = re + (D == 2 ? k0 : k0 + 1);   // the pair's other element (no target of this pass)
+      const uint64_t id = D == 0 ? i : (D == 1 ? j : kt);
+      const uint64_t nd = D == 0 ? n0 : (D == 1 ? n1 : n2);
+      const uint64_t sd = D == 0 ? n1 * n2 : (D == 1 ? n2 : 1);
+      const int mth = (id >= 3 && id + 3 < nd) ? 2 : (id + 1 < nd ? 1 : 0);
+      const double b = to_d<T>(xp[e - sd]);
+      const double c = mth >= 1 ? to_d<T>(xp[e + sd]) : 0.0;
+      const double av = mth == 2 ? to_d<T>(xp[e - 3 * sd]) : 0.0;
+      const double ev = mth == 2 ? to_d<T>(xp[e + 3 * sd]) : 0.0;
+      const double p = ip_predict(av, b, c, ev, mth);
+      if (has_pair) xold = xp[eo];
+      if (DEC) {
+        const uint16_t cin = codes[e];
+        xnew = cin != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)cin - (int)a.R)))) : xp[e];
+      } else {
+        const T xv = x[e];
+        const double xd = to_d<T>(xv);
+        const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+        const double sm = __dadd_rn(t, RINT_MAGIC);
+        const double q = __dsub_rn(sm, RINT_MAGIC);
+        const T y = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, q)));
+        const bool ok = fabs(t) < (double)a.R && fabs(q) < (double)a.R && fabs(__dsub_rn(to_d<T>(y), xd)) <= K.eb_abs;
+        cnew = ok ? (uint16_t)(__double2loint(sm) + (int)a.R) : (uint16_t)0;
+        xnew = ok ? y : xv;
+        is_out = !ok;
+      }
+    }
+    // the whole pair back (the even column first): both values of a pair are this thread's
+    if (has_t) {
+      if (has_pair) {
+        const T lo = D == 2 ? xold : xnew, hi = D == 2 ? xnew : xold;
+        xp[re + k0] = lo;
+        xp[re + k0 + 1] = hi;
+        if (!DEC) codes[e] = cnew;
+      } else {
+        xp[e] = xnew;
+        if (!DEC) codes[e] = cnew;
+      }
+    }
+    if (!DEC) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, is_out);
+      if (bal) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ocount, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (is_out) {
+          const unsigned long long pos = base + __popc(bal & ((1u << lane) - 1u));
+          if (pos < a.cap) {
+            oidx[pos] = a.gofs + e;
+            oval[pos] = x[e];
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Level s = 1 fused (its three passes hold 7/8 of the targets): one CTA per tile of 2 planes (i0 even,
 // i0 + 1) x L1_TJ rows x L1_TK columns, in shared memory with a halo of 2 even coordinates along j and k
 // (the -+1, -+3 donors).  Pass (1,0) targets (i odd, j and k even) are computed over the whole halo box
@@ -404,6 +504,11 @@ IpArgs base_args(const sz3g_grid* g, const sz3g_params* p, const double* d_minma
   return a;
 }
 
+#ifndef SZ3G_IP_PAIRS
+#define SZ3G_IP_PAIRS 1   // level 1 by the pair kernels: 1 = decompression only (c5: 26.5 vs 33.2 ms), 2 = also
+                          // compression (c5: 58.8 vs 43.8 ms: its stores of x and codes interleave with the
+                          // other warps' donor loads of the same sectors; not understood yet), 0 = never
+#endif
 #ifndef SZ3G_IP_L1
 #define SZ3G_IP_L1 0   // 1: level 1 in the fused tile kernel (bit-exact; c5 46.9 vs 43.8 ms compress for the
                        // three per-pass launches: 226 instructions per element, issue-bound; kept for A/B)
@@ -424,6 +529,19 @@ int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* 
         return SZ3G_ECUDA;
       kern<<<grid, L1_WARPS * 32, L1Smem<T>::total, st>>>(x, xp, codes, oidx, oval, ocount, a);
       nl++;
+      break;
+    }
+    if (s == 1 && SZ3G_IP_PAIRS && (DEC || SZ3G_IP_PAIRS > 1)) {   // level 1: pair kernels (full-sector stores)
+      const uint64_t np = (a.n[2] + 1) / 2;
+      for (int d = 0; d < 3; d++) {
+        if (!pass_geometry(a, s, d)) continue;
+        const uint64_t rows = d == 2 ? a.n[0] * a.n[1] : (d == 1 ? a.n[0] * (a.n[1] / 2) : (a.n[0] / 2) * ((a.n[1] + 1) / 2));
+        const dim3 grid((unsigned)((np + 255) / 256), (unsigned)std::min<uint64_t>(rows, 65535));
+        if (d == 0) k_interp_pairs<T, DEC, 0><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        else if (d == 1) k_interp_pairs<T, DEC, 1><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        else k_interp_pairs<T, DEC, 2><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        nl++;
+      }
       break;
     }
     for (int d = 0; d < 3; d++) {

@@ -508,6 +508,42 @@ __device__ __forceinline__ void quant_warp_tile_beta(const T* __restrict__ xs, c
   rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, has_out, tc, g, o, hs);
 }
 
+// NOR0 with SZ3G_QDERIV1: only the group's first quantise warp turns the staged beta into coefficient codes,
+// decoded coefficients and fast-path constants (into the stage's coefficient slot); the group's Q warps
+// meet at a named barrier and all read the slot -- the derivation runs once per tile instead of Q times.
+template <typename T, bool HIST, bool FULL, int P>
+__device__ __forceinline__ void quant_warp_tile_shared(const T* __restrict__ xs, const double* __restrict__ bstage,
+                                                       CoefSlot* slot, uint16_t* slab, int j0, bool derive, int grp,
+                                                       int nthreads, const TileCoord tc, const Geo& g, const Consts& K,
+                                                       uint32_t R, const CompressOut<T>& o, const HistSmem& hs) {
+  const LaneGeom L = lane_geom<FULL>(tc, g);
+  const int bl = (threadIdx.x & 31) >> 1;
+  if (derive) {
+    double beta[4] = {0.0, 0.0, 0.0, 0.0}, bh[4];
+    int32_t cc[4];
+    if (L.m2 > 0) {
+      const double2 b01 = reinterpret_cast<const double2*>(bstage)[2 * bl];
+      const double2 b23 = reinterpret_cast<const double2*>(bstage)[2 * bl + 1];
+      beta[0] = b01.x; beta[1] = b01.y; beta[2] = b23.x; beta[3] = b23.y;
+    }
+    block_codes(beta, K, cc, bh);
+    write_coefs(o, tc, g, L, cc, beta);
+    if (L.h == 0) {
+#pragma unroll
+      for (int d = 0; d < 4; d++) slot->bh[bl][d] = bh[d];
+      slot->f[bl] = fast32_consts(bh, K);
+    }
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(nthreads) : "memory");
+  double bh[4];
+#pragma unroll
+  for (int d = 0; d < 4; d++) bh[d] = slot->bh[bl][d];
+  const Fast32 F = slot->f[bl];
+  const bool has_out =
+      quantize_rows<T, true, HIST, FULL, P, true>(xs, BS * TK, TK, slab, 0, 0, j0, L, bh, F, K, R, hs, o.hist);
+  rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, has_out, tc, g, o, hs);
+}
+
 template <typename T, bool HIST, bool FULL, int P>
 __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const CoefSlot* slot, uint16_t* slab,
                                                 int j0, const TileCoord tc, const Geo& g, const Consts& K,
@@ -526,6 +562,10 @@ __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const 
 // SELF: no producer warp; the role-0 warp of each group feeds its own group's ring (it issues the
 // load of tile k + D - 1 once the quantise warps have released tile k - 1, right after it has
 // published tile k's coefficients), with an optional L2 prefetch one tile further ahead.
+#ifndef SZ3G_QDERIV1
+#define SZ3G_QDERIV1 0   // 1: NOR0 coefficient constants derived once per group and tile (named barrier);
+                         // bit-exact, sustained A/B 4.95 vs 4.79 ms: the barrier costs more than it saves
+#endif
 #ifndef SZ3G_QWAIT
 #define SZ3G_QWAIT 1   // quantise warps' wait for a full stage: 0 = try_wait + nanosleep(64) polling,
                        // 1 = hardware-suspended try_wait (no polling instructions: less issue, less power)
@@ -713,8 +753,18 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
         const T* xs = stage_x(s);
         if (NOR0) {
           const double* bst = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(xs) + L_::tile_bytes);
-          if (tfull) quant_warp_tile_beta<T, HIST, true, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
-          else quant_warp_tile_beta<T, HIST, false, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+          if (SZ3G_QDERIV1) {
+            if (tfull)
+              quant_warp_tile_shared<T, HIST, true, P>(xs, bst, &slots[s], slab, j0, q == 0, grp, 32 * Q, tc, g, K,
+                                                       a.R, o, hs);
+            else
+              quant_warp_tile_shared<T, HIST, false, P>(xs, bst, &slots[s], slab, j0, q == 0, grp, 32 * Q, tc, g, K,
+                                                        a.R, o, hs);
+          } else if (tfull) {
+            quant_warp_tile_beta<T, HIST, true, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+          } else {
+            quant_warp_tile_beta<T, HIST, false, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+          }
         } else {
           if (tfull) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
           else quant_warp_tile<T, HIST, false, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
