@@ -144,3 +144,63 @@ def test_c5_slab_outlier_indices_above_2_32(c5):
                outlier_val=res.outlier_val[:n].cpu().numpy(), hist=res.hist.cpu().numpy(), eb_abs=res.eb_abs)
     assert int(gpu["outlier_idx"].min()) >= 6000 * 2048 * 2048 > 2 ** 32
     compare(xs, gpu, orc, xdec_gpu=rt.out.cpu().numpy())
+
+
+def test_c5_stress_r16_slab_parity(c5):
+    """The bench's c5 stress leg (R = 16: 38.6% of the elements are radius outliers) on a slab, through
+    the bench's two-pass kernels with the global range, element by element against the oracle: the
+    outlier-heavy rare path at the measured configuration."""
+    from paper_2111_02925_b200.roundtrip import RoundTrip
+    cfg, x, rt0, _ = c5
+    lo, hi = (float(v) for v in rt0.bufs.minmax.cpu())
+    a0, rows = 504, 6
+    xs_d = x[a0:a0 + rows].contiguous()
+    rt = RoundTrip(xs_d, cfg.eb, cfg.eb_mode, 16, dim0_offset=a0, outlier_cap=xs_d.numel())
+    rt.bufs.minmax.copy_(torch.tensor([lo, hi], dtype=torch.float64))
+    from paper_2111_02925_b200 import sz3g
+    b = rt.bufs
+    sz3g.regression_analyze(xs_d, torch.empty_like(b.minmax), rt.beta)      # beta of the slab's blocks
+    b.reset()
+    sz3g.regression_quantize(xs_d, cfg.eb, cfg.eb_mode, 16, b.minmax, rt.beta, bufs=b, reset=False, dim0_offset=a0)
+    sz3g.regression_decompress(b.codes, b.coef_codes, b.outlier_idx, b.outlier_val, rt.cap, cfg.eb, 16, xs_d.dtype,
+                               dim0_offset=a0, out=rt.out, d_outlier_count=b.outlier_count, eb_mode="rel",
+                               d_minmax=b.minmax)
+    res = rt.result()
+    xs = xs_d.cpu().numpy()
+    orc = oracle.compress(xs, cfg.eb, "rel", radius=16, dim0_offset=a0, value_range_override=(lo, hi))
+    n = res.n_outliers
+    assert n == orc.outlier_idx.size and n > 0.3 * xs.size
+    gpu = dict(codes=res.codes.cpu().numpy(), coef_codes=res.coef_codes.cpu().numpy(),
+               coef_raw=res.coef_raw.cpu().numpy(), outlier_idx=res.outlier_idx[:n].cpu().numpy().view(np.uint64),
+               outlier_val=res.outlier_val[:n].cpu().numpy(), hist=res.hist.cpu().numpy(), eb_abs=res.eb_abs)
+    compare(xs, gpu, orc, xdec_gpu=rt.out.cpu().numpy())
+
+
+def test_c5_lr_slab_parity(c5):
+    """SZ3-LR (NEXT-4) as the bench's lr leg runs it -- lr_quantize from the analyze pass's range and beta
+    of the whole field -- on a slab of c5, against the LR oracle on that slab with the global range."""
+    from paper_2111_02925_b200 import sz3g
+    cfg, x, rt0, _ = c5
+    lo, hi = (float(v) for v in rt0.bufs.minmax.cpu())
+    n0, n1, n2 = x.shape
+    NB1, NB2 = math.ceil(n1 / 6), math.ceil(n2 / 6)
+    a0, rows = 1014, 6
+    xs_d = x[a0:a0 + rows].contiguous()
+    b0 = (a0 // 6) * NB1 * NB2
+    beta = rt0.beta[b0:b0 + NB1 * NB2].contiguous()       # the timed step's beta of these blocks
+    res = sz3g.lr_quantize(xs_d, cfg.eb, cfg.eb_mode, cfg.radius, rt0.bufs.minmax, beta,
+                           outlier_cap=xs_d.numel(), dim0_offset=a0).finalize()
+    xo = sz3g.lr_decompress(res.codes, res.coef_codes, res.lr_flags, res.outlier_idx, res.outlier_val,
+                            res.outlier_idx.numel(), cfg.eb, cfg.radius, xs_d.dtype, a0,
+                            d_outlier_count=res.outlier_count, eb_mode=cfg.eb_mode, d_minmax=rt0.bufs.minmax)
+    torch.cuda.synchronize()
+    xs = xs_d.cpu().numpy()
+    orc = oracle.lr_compress(xs, cfg.eb, "rel", radius=cfg.radius, dim0_offset=a0, value_range_override=(lo, hi))
+    n = res.n_outliers
+    gflags = res.lr_flags.cpu().numpy()
+    ex = orc.block_exempt.astype(bool)
+    assert np.array_equal(gflags[~ex], orc.flags[~ex]) and int(gflags.sum()) > 0
+    gpu = dict(codes=res.codes.cpu().numpy(), coef_codes=res.coef_codes.cpu().numpy(),
+               coef_raw=res.coef_raw.cpu().numpy(), outlier_idx=res.outlier_idx[:n].cpu().numpy().view(np.uint64),
+               outlier_val=res.outlier_val[:n].cpu().numpy(), hist=res.hist.cpu().numpy(), eb_abs=res.eb_abs)
+    compare(xs, gpu, orc, xdec_gpu=xo.cpu().numpy())
