@@ -39,6 +39,12 @@ class RoundTrip:
         self.bufs = sz3g.CompressBuffers(x.shape, x.dtype, radius, outlier_cap=self.cap, device=x.device)
         self.beta = self.bufs.beta_buffer() if path == "two-pass" else None
         self.out = torch.empty_like(x)
+        # sharded: the histogram all-reduce (needed by the codebook, not by decompression) runs on a side
+        # stream, overlapped with the decompression; the next step's reset and finish() wait for it
+        self.side = torch.cuda.Stream(x.device)
+        self._ev_q = torch.cuda.Event()
+        self._ev_h = torch.cuda.Event()
+        self._hist_pending = False
 
     # the step in five segments; every segment launches on the stream it is given
     def _analyze(self, st):
@@ -50,6 +56,9 @@ class RoundTrip:
     def _range_reset(self, st):
         with torch.cuda.stream(st):
             pdist.allreduce_range_(self.bufs.minmax, self.group)
+            if self._hist_pending:        # the previous step's histogram all-reduce has finished
+                st.wait_event(self._ev_h)
+                self._hist_pending = False
             self.bufs.reset()
 
     def _quantize(self, st):
@@ -85,7 +94,17 @@ class RoundTrip:
         if record is not None:
             record[4].record(st)
         graphs = getattr(self, "graphs", None)
+        sharded = torch.distributed.is_initialized() and torch.distributed.get_world_size(self.group) > 1
         for name, after in zip(self.SEGMENTS, self._AFTER):
+            if name == "_hist" and graphs is None and sharded:   # overlapped with the decompression
+                self._ev_q.record(st)
+                self.side.wait_event(self._ev_q)
+                self._hist(self.side)
+                self._ev_h.record(self.side)
+                self._hist_pending = True
+                if record is not None:
+                    record[after].record(st)
+                continue
             if graphs is not None:
                 if graphs[name] is not None:
                     with torch.cuda.stream(st):
@@ -120,8 +139,15 @@ class RoundTrip:
         self.launches_per_step = sz3g.launch_count() - l0   # library kernels in one replayed step
         return self
 
+    def finish(self):
+        """Make the stream wait for the last step's histogram all-reduce (part of the step's output)."""
+        if self._hist_pending:
+            self.stream.wait_event(self._ev_h)
+            self._hist_pending = False
+
     def result(self) -> sz3g.Compressed:
         """The last step's compressed outputs (synchronises; raises on device status bits)."""
+        self.finish()
         b = self.bufs
         return sz3g.Compressed(tuple(self.x.shape), self.x.dtype, self.radius, self.dim0_offset, b.codes,
                                b.coef_codes, self.beta, b.outlier_idx, b.outlier_val, b.outlier_count, b.hist,
