@@ -542,6 +542,10 @@ def interp_compress(x: torch.Tensor, eb: float, eb_mode: str = "rel", radius: in
                                torch.zeros(2 * radius, dtype=torch.int64, device=dev) if hist else None,
                                torch.zeros(1, dtype=torch.float64, device=dev), torch.zeros(1, dtype=torch.int32, device=dev))
     else:
+        if out.shape != tuple(x.shape) or out.dtype != x.dtype or out.radius != radius or out.codes.device != dev:
+            raise SZ3GError("interp_compress: `out` was made for another shape, dtype, radius or device")
+        if (out.hist is None) == hist:
+            raise SZ3GError("interp_compress: `out` was made with hist=" + str(out.hist is not None))
         out.outlier_count.zero_()
         out.status.zero_()
         if out.hist is not None:
