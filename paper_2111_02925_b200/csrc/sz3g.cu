@@ -562,6 +562,14 @@ __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const 
 // SELF: no producer warp; the role-0 warp of each group feeds its own group's ring (it issues the
 // load of tile k + D - 1 once the quantise warps have released tile k - 1, right after it has
 // published tile k's coefficients), with an optional L2 prefetch one tile further ahead.
+#ifndef SZ3G_PWAIT
+#define SZ3G_PWAIT 1   // producer's wait for a free stage: 0 = try_wait + nanosleep(400), 1 = hardware suspend
+                       // (sustained A/B: quantise 4.758 vs 4.806 ms)
+#endif
+#ifndef SZ3G_DPWAIT
+#define SZ3G_DPWAIT 0   // the decompressor producer's wait for a free stage (as SZ3G_PWAIT); sustained A/B:
+                        // decompress 4.474 vs 4.454 ms, off
+#endif
 #ifndef SZ3G_QDERIV1
 #define SZ3G_QDERIV1 0   // 1: NOR0 coefficient constants derived once per group and tile (named barrier);
                          // bit-exact, sustained A/B 4.95 vs 4.79 ms: the barrier costs more than it saves
@@ -644,7 +652,8 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
         }
         const uint32_t s = gq * D + k % D, ph = (k / D) & 1u;
         if (++gq == NG) { gq = 0; k++; }
-        ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
+        if (SZ3G_PWAIT) ptx::mbar_wait_idle(&empty[s], ph ^ 1u);   // hardware-suspended: no polling loop
+        else ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
         issue_load(s, t);
       }
       for (int e = 0; e < NG; e++) {   // end of sequence: one header per group, no data
@@ -868,7 +877,8 @@ __global__ void __launch_bounds__((NG * G + 1) * 32, 1)
         if (t >= g.ntiles) break;
         const uint32_t s = gq * D + k % D, ph = (k / D) & 1u;
         if (++gq == NG) { gq = 0; k++; }
-        ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
+        if (SZ3G_DPWAIT) ptx::mbar_wait_idle(&empty[s], ph ^ 1u);
+        else ptx::mbar_wait_backoff(&empty[s], ph ^ 1u);
         const TileCoord tc = decode_tile(t, g);
         const uint32_t nblk = min(16u, g.NB2 - tc.c * 16u);
         uint8_t* st = stages + (size_t)s * L_::stage_bytes;
