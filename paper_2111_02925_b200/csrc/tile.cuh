@@ -25,6 +25,10 @@
 namespace sz3g {
 
 constexpr int DEC_UNROLL = SZ3G_DEC_UNROLL;
+#ifndef SZ3G_QKU
+#define SZ3G_QKU 1   // unroll of the quantise loop over a lane's three columns (A/B)
+#endif
+constexpr int QKU = SZ3G_QKU;
 constexpr int BS = 6;                          // regression block size B (north_star: 6x6x6)
 constexpr int TK = 96;                         // tile extent along dim 2 (16 blocks)
 constexpr int TROWS = BS * BS;                 // rows (i,j) per tile
@@ -463,7 +467,7 @@ __device__ __forceinline__ bool quantize_rows(const T* __restrict__ xs, uint64_t
     const T* xcol = xrow;
     uint16_t* ccol = crow;
     float fk = (float)(3 * L.h);
-#pragma unroll 1
+#pragma unroll QKU
     for (int kk = 0; kk < 3; kk++, xcol++, ccol++, fk += 1.0f) {
     const bool cv = FULL || ((j < L.m1) && L.kv(kk));
     T xv[BS];
