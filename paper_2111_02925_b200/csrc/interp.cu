@@ -263,10 +263,12 @@ __global__ void __launch_bounds__(256) k_interp_pairs(const T* __restrict__ x, T
 // prediction and quantisation as k_interp_pass, op for op: bit-identical to the per-pass schedule.
 constexpr int L1_TJ = 16, L1_TK = 128, L1_BJ = L1_TJ + 6, L1_BK = L1_TK + 6, L1_WARPS = 16;
 
+// box buffers: x' as fp64 (every donor is read up to four times: one conversion when it is written instead
+// of one per read), x as T, codes
 template <typename T>
 struct L1Smem {
   static constexpr size_t box = 2ull * L1_BJ * L1_BK;
-  static constexpr size_t off_x = box * sizeof(T);
+  static constexpr size_t off_x = box * sizeof(double);
   static constexpr size_t off_c = off_x + box * sizeof(T);
   static constexpr size_t total = off_c + box * sizeof(uint16_t);
 };
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(L1_WARPS * 32) k_interp_l1(const T* __restrict
                                                              T* __restrict__ oval, unsigned long long* __restrict__ ocount,
                                                              IpArgs a) {
   extern __shared__ __align__(16) uint8_t l1sm[];
-  T* sE = reinterpret_cast<T*>(l1sm);                                   // x' of the box [2][BJ][BK]
+  double* sE = reinterpret_cast<double*>(l1sm);                         // x' of the box [2][BJ][BK], fp64
   T* sX = reinterpret_cast<T*>(l1sm + L1Smem<T>::off_x);               // x of the box (compress)
   uint16_t* sC = reinterpret_cast<uint16_t*>(l1sm + L1Smem<T>::off_c);  // codes of the box
   __shared__ Consts s_k;
@@ -291,37 +293,41 @@ __global__ void __launch_bounds__(L1_WARPS * 32) k_interp_l1(const T* __restrict
   const int I0 = 2 * (int)blockIdx.z, J0 = L1_TJ * (int)blockIdx.y, K0 = L1_TK * (int)blockIdx.x;
   const int jb = J0 - 2, kb = K0 - 2;   // box origin (even)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto at = [](int bi, int bj, int bk) { return (bi * L1_BJ + bj) * L1_BK + bk; };
-  auto rowe = [&](int i, int j) { return ((uint64_t)i * (uint64_t)n1 + (uint64_t)j) * (uint64_t)n2; };
-  // (1) load the box, one warp per row: x (compress) or codes (decompress) everywhere, x' at the level >= 2
-  // points (all coordinates even) and, decompressing, at the code-0 targets (their scattered outlier values)
+  const int klo = kb < 0 ? -kb : 0, khi = min(L1_BK, n2 - kb);   // valid box columns [klo, khi)
+  // (1) the box, one warp per row (row base pointers, 32-bit column offsets)
   for (int r = warp; r < 2 * L1_BJ; r += L1_WARPS) {
     const int bi = r / L1_BJ, bj = r - bi * L1_BJ, i = I0 + bi, j = jb + bj;
     if (i >= n0 || j < 0 || j >= n1) continue;
-    const uint64_t re = rowe(i, j);
-    const bool l2row = ((i | j) & 1) == 0;
-    for (int bk = lane; bk < L1_BK; bk += 32) {
-      const int k = kb + bk;
-      if (k < 0 || k >= n2) continue;
-      const uint64_t e = re + (uint64_t)k;
-      const bool l2 = l2row && (k & 1) == 0;
-      const int o = at(bi, bj, bk);
-      uint16_t c = 1;
-      if (DEC || l2) c = codes[e];
-      sC[o] = c;
-      if (!DEC) sX[o] = x[e];
-      if (l2 || (DEC && c == 0)) sE[o] = xp[e];
+    const uint64_t re = ((uint64_t)i * (uint64_t)n1 + (uint64_t)j) * (uint64_t)n2 + (uint64_t)(int64_t)kb;
+    const int ro = r * L1_BK;
+    if (DEC) {
+      const uint16_t* cr = codes + re;
+      for (int bk = klo + lane; bk < khi; bk += 32) {
+        const uint16_t c = cr[bk];
+        sC[ro + bk] = c;
+        if (c == 0) sE[ro + bk] = to_d<T>(xp[re + bk]);   // an outlier's scattered value
+      }
+    } else {
+      const T* xr = x + re;
+      for (int bk = klo + lane; bk < khi; bk += 32) sX[ro + bk] = xr[bk];
+    }
+    if (((i | j) & 1) == 0) {   // level >= 2 points (all coordinates even): final x' and codes
+      const int k0 = klo + (klo & 1);
+      for (int bk = k0 + 2 * lane; bk < khi; bk += 64) {
+        sE[ro + bk] = to_d<T>(xp[re + bk]);
+        if (!DEC) sC[ro + bk] = codes[re + bk];
+      }
     }
   }
   SZ3G_SYNCTHREADS();
   if (!s_ok) return;
   const Consts K = s_k;
+  const double Rd = (double)a.R;
   // one target at box offset o: quantise (compress) or recover (decompress); returns "own outlier"
-  auto target = [&](int o, double av, double bv, double cv, double ev, int m, bool own) -> bool {
-    const double p = ip_predict(av, bv, cv, ev, m);
+  auto target = [&](int o, double p, bool own) -> bool {
     if (DEC) {
       const uint16_t c = sC[o];
-      if (c != 0) sE[o] = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)c - (int)a.R))));
+      if (c != 0) sE[o] = to_d<T>(from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)c - (int)a.R)))));
       return false;
     }
     const T xv = sX[o];
@@ -329,9 +335,9 @@ __global__ void __launch_bounds__(L1_WARPS * 32) k_interp_l1(const T* __restrict
     const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
     const double sm = __dadd_rn(t, RINT_MAGIC);
     const double qd = __dsub_rn(sm, RINT_MAGIC);
-    const T y = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, qd)));
-    const bool ok = fabs(t) < (double)a.R && fabs(qd) < (double)a.R && fabs(__dsub_rn(to_d<T>(y), xd)) <= K.eb_abs;
-    sE[o] = ok ? y : xv;
+    const double yd = to_d<T>(from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, qd))));
+    const bool ok = fabs(t) < Rd && fabs(qd) < Rd && fabs(__dsub_rn(yd, xd)) <= K.eb_abs;
+    sE[o] = ok ? yd : xd;
     if (own) sC[o] = ok ? (uint16_t)(__double2loint(sm) + (int)a.R) : (uint16_t)0;
     return own && !ok;
   };
@@ -351,78 +357,81 @@ __global__ void __launch_bounds__(L1_WARPS * 32) k_interp_l1(const T* __restrict
     }
   };
   const uint64_t p1 = (uint64_t)n1 * n2;
-  // (2) pass (1,0): plane i = I0 + 1, j and k even over the box; donors i -+ 1, -+ 3 (plane I0 from the
-  // box, the others from global x')
+  constexpr int NKE = L1_BK / 2;   // even box columns: 0, 2, .., L1_BK - 2
+  // (2) pass (1,0): plane I0 + 1, even rows and columns of the box; donors at i -+ 1 (plane I0 in the box,
+  // plane I0 + 2 in global x'), i -+ 3 (global)
   if (I0 + 1 < n0) {
     const int i = I0 + 1;
     const int m = (i >= 3 && i + 3 < n0) ? 2 : (i + 1 < n0 ? 1 : 0);
     for (int r = warp; r < L1_BJ / 2; r += L1_WARPS) {
       const int bj = 2 * r, j = jb + bj;
       const bool rowok = j >= 0 && j < n1;
-      const uint64_t re = rowok ? rowe(i, j) : 0;
+      const uint64_t re = rowok ? ((uint64_t)i * (uint64_t)n1 + (uint64_t)j) * (uint64_t)n2 + (uint64_t)(int64_t)kb : 0;
+      const int ro = (L1_BJ + bj) * L1_BK, ro0 = bj * L1_BK;
       const bool ownrow = j >= J0 && j < J0 + L1_TJ;
-      for (int h = lane; h < (L1_BK + 1) / 2 + 31 - ((L1_BK + 1) / 2 + 31) % 32; h += 32) {   // warp-uniform trips
-        const int bk = 2 * h, k = kb + bk;
-        const bool live = rowok && h < (L1_BK + 1) / 2 && k >= 0 && k < n2;
+      for (int h0 = 0; h0 < NKE; h0 += 32) {
+        const int bk = 2 * (h0 + lane);
+        const bool live = rowok && h0 + lane < NKE && bk >= klo && bk < khi;
         bool out = false;
         uint64_t e = 0;
-        const int o = at(1, bj, bk);
         if (live) {
-          e = re + (uint64_t)k;
-          const double bv = to_d<T>(sE[at(0, bj, bk)]);
+          e = re + (uint64_t)bk;
+          const double bv = sE[ro0 + bk];
           const double cv = m >= 1 ? to_d<T>(xp[e + p1]) : 0.0;
           const double av = m == 2 ? to_d<T>(xp[e - 3 * p1]) : 0.0;
           const double ev = m == 2 ? to_d<T>(xp[e + 3 * p1]) : 0.0;
-          out = target(o, av, bv, cv, ev, m, ownrow && k >= K0 && k < K0 + L1_TK);
+          out = target(ro + bk, ip_predict(av, bv, cv, ev, m), ownrow && bk >= 2 && bk < 2 + L1_TK);
         }
-        append(out, e, o);
+        append(out, e, ro + bk);
       }
     }
   }
   SZ3G_SYNCTHREADS();
-  // (3) pass (1,1): both planes, j odd in the tile, k even over the box; donors j -+ 1, -+ 3 in the box
-  for (int r = warp; r < 2 * (L1_TJ / 2); r += L1_WARPS) {
+  // (3) pass (1,1): both planes, odd rows of the tile, even columns of the box; donors in the box
+  for (int r = warp; r < L1_TJ; r += L1_WARPS) {   // L1_TJ / 2 odd rows x 2 planes
     const int bi = r / (L1_TJ / 2), bj = 3 + 2 * (r % (L1_TJ / 2)), i = I0 + bi, j = jb + bj;
     const bool rowok = i < n0 && j < n1;
-    const uint64_t re = rowok ? rowe(i, j) : 0;
+    const uint64_t re = rowok ? ((uint64_t)i * (uint64_t)n1 + (uint64_t)j) * (uint64_t)n2 + (uint64_t)(int64_t)kb : 0;
     const int m = (j >= 3 && j + 3 < n1) ? 2 : (j + 1 < n1 ? 1 : 0);
-    for (int h = lane; h < (L1_BK + 1) / 2 + 31 - ((L1_BK + 1) / 2 + 31) % 32; h += 32) {
-      const int bk = 2 * h, k = kb + bk;
-      const bool live = rowok && h < (L1_BK + 1) / 2 && k >= 0 && k < n2;
+    const int ro = (bi * L1_BJ + bj) * L1_BK;
+    for (int h0 = 0; h0 < NKE; h0 += 32) {
+      const int bk = 2 * (h0 + lane);
+      const bool live = rowok && h0 + lane < NKE && bk >= klo && bk < khi;
       bool out = false;
       uint64_t e = 0;
-      const int o = at(bi, bj, bk);
+      const int o = ro + bk;
       if (live) {
-        e = re + (uint64_t)k;
-        const double bv = to_d<T>(sE[o - L1_BK]);
-        const double cv = m >= 1 ? to_d<T>(sE[o + L1_BK]) : 0.0;
-        const double av = m == 2 ? to_d<T>(sE[o - 3 * L1_BK]) : 0.0;
-        const double ev = m == 2 ? to_d<T>(sE[o + 3 * L1_BK]) : 0.0;
-        out = target(o, av, bv, cv, ev, m, k >= K0 && k < K0 + L1_TK);
+        e = re + (uint64_t)bk;
+        const double bv = sE[o - L1_BK];
+        const double cv = m >= 1 ? sE[o + L1_BK] : 0.0;
+        const double av = m == 2 ? sE[o - 3 * L1_BK] : 0.0;
+        const double ev = m == 2 ? sE[o + 3 * L1_BK] : 0.0;
+        out = target(o, ip_predict(av, bv, cv, ev, m), bk >= 2 && bk < 2 + L1_TK);
       }
       append(out, e, o);
     }
   }
   SZ3G_SYNCTHREADS();
-  // (4) pass (1,2): the tile's rows, k odd; donors k -+ 1, -+ 3 in the box
+  // (4) pass (1,2): the tile's rows, odd columns; donors in the box
   for (int r = warp; r < 2 * L1_TJ; r += L1_WARPS) {
     const int bi = r / L1_TJ, bj = 2 + r % L1_TJ, i = I0 + bi, j = jb + bj;
     const bool rowok = i < n0 && j < n1;
-    const uint64_t re = rowok ? rowe(i, j) : 0;
-    for (int h = lane; h < L1_TK / 2; h += 32) {
-      const int bk = 3 + 2 * h, k = kb + bk;
+    const uint64_t re = rowok ? ((uint64_t)i * (uint64_t)n1 + (uint64_t)j) * (uint64_t)n2 + (uint64_t)(int64_t)kb : 0;
+    const int ro = (bi * L1_BJ + bj) * L1_BK;
+    for (int h0 = 0; h0 < L1_TK / 2; h0 += 32) {
+      const int bk = 3 + 2 * (h0 + lane), k = kb + bk;
       const bool live = rowok && k < n2;
       bool out = false;
       uint64_t e = 0;
-      const int o = at(bi, bj, bk);
+      const int o = ro + bk;
       if (live) {
-        e = re + (uint64_t)k;
+        e = re + (uint64_t)bk;
         const int m = (k >= 3 && k + 3 < n2) ? 2 : (k + 1 < n2 ? 1 : 0);
-        const double bv = to_d<T>(sE[o - 1]);
-        const double cv = m >= 1 ? to_d<T>(sE[o + 1]) : 0.0;
-        const double av = m == 2 ? to_d<T>(sE[o - 3]) : 0.0;
-        const double ev = m == 2 ? to_d<T>(sE[o + 3]) : 0.0;
-        out = target(o, av, bv, cv, ev, m, true);
+        const double bv = sE[o - 1];
+        const double cv = m >= 1 ? sE[o + 1] : 0.0;
+        const double av = m == 2 ? sE[o - 3] : 0.0;
+        const double ev = m == 2 ? sE[o + 3] : 0.0;
+        out = target(o, ip_predict(av, bv, cv, ev, m), true);
       }
       append(out, e, o);
     }
@@ -432,13 +441,14 @@ __global__ void __launch_bounds__(L1_WARPS * 32) k_interp_l1(const T* __restrict
   for (int r = warp; r < 2 * L1_TJ; r += L1_WARPS) {
     const int bi = r / L1_TJ, tj = r % L1_TJ, i = I0 + bi, j = J0 + tj;
     if (i >= n0 || j >= n1) continue;
-    const uint64_t re = rowe(i, j);
-    for (int tk = lane; tk < L1_TK; tk += 32) {
-      const int k = K0 + tk;
-      if (k >= n2) break;
-      const int o = at(bi, tj + 2, tk + 2);
-      xp[re + k] = sE[o];
-      if (!DEC) codes[re + k] = sC[o];
+    const uint64_t re = ((uint64_t)i * (uint64_t)n1 + (uint64_t)j) * (uint64_t)n2 + (uint64_t)K0;
+    const int ro = (bi * L1_BJ + tj + 2) * L1_BK + 2;
+    const int kend = min(L1_TK, n2 - K0);
+    T* xr = xp + re;
+    uint16_t* cr = codes + re;
+    for (int tk = lane; tk < kend; tk += 32) {
+      xr[tk] = from_d<T>(sE[ro + tk]);
+      if (!DEC) cr[tk] = sC[ro + tk];
     }
   }
 }
@@ -510,8 +520,9 @@ IpArgs base_args(const sz3g_grid* g, const sz3g_params* p, const double* d_minma
                           // other warps' donor loads of the same sectors; not understood yet), 0 = never
 #endif
 #ifndef SZ3G_IP_L1
-#define SZ3G_IP_L1 0   // 1: level 1 in the fused tile kernel (bit-exact; c5 46.9 vs 43.8 ms compress for the
-                       // three per-pass launches: 226 instructions per element, issue-bound; kept for A/B)
+#define SZ3G_IP_L1 0   // 1: level 1 in the fused tile kernel (bit-exact; c5 compress 52.4 / decompress 42.9 ms against
+                       // 43.7 / 26.5 for the per-pass kernels: the five phases of a tile are serialised by block
+                       // barriers with two CTAs per SM, so their load latencies are not hidden; kept for A/B)
 #endif
 
 template <typename T, bool DEC>
