@@ -528,7 +528,15 @@ def config_leg(sz3g, spec, peaks, steps, warmup, flush_buf, x=None):
     N, s = x.numel(), x.element_size()
     NB = sz3g.num_blocks(x.shape)
     cap = bench_outlier_cap(N) if R >= 1024 else N
-    rt = RoundTrip(x, cfg.eb, cfg.eb_mode, R, outlier_cap=cap).capture()   # CUDA graphs: no host gaps
+    rt = RoundTrip(x, cfg.eb, cfg.eb_mode, R, outlier_cap=cap)
+    launch = "each segment of the step replayed from a CUDA graph (RoundTrip.capture)"
+    try:
+        rt.capture()   # CUDA graphs: no host gaps between the small configs' kernels
+    except Exception as e:
+        print(f"bench: CUDA graph capture failed for {spec} ({e}); eager", file=sys.stderr)
+        torch.cuda.synchronize()
+        rt.graphs = None
+        launch = "eager (graph capture failed)"
     stream = rt.stream
     for _ in range(warmup):
         rt.step()
@@ -558,8 +566,7 @@ def config_leg(sz3g, spec, peaks, steps, warmup, flush_buf, x=None):
            "quantize_roofline": roof(b["quantize"], qua, peaks["hbm_gbs"]),
            "analyze_roofline": roof(b["analyze"], ana, peaks["hbm_gbs"]),
            "decompress_roofline": roof(b["decompress"], dec, peaks["hbm_gbs"]),
-           "l2": "flushed (2x L2 write) before every step", "steps": steps, "warmup": warmup,
-           "launch": "each segment of the step replayed from a CUDA graph (RoundTrip.capture)"}
+           "l2": "flushed (2x L2 write) before every step", "steps": steps, "warmup": warmup, "launch": launch}
     del rt
     torch.cuda.empty_cache()
     return out
@@ -588,7 +595,13 @@ def main():
     rt = RoundTrip(x, cfg.eb, cfg.eb_mode, cfg.radius, dim0_offset=a0, path=args.path)
     graphs = args.graphs == "on" or (args.graphs == "auto" and world == 1)
     if graphs:
-        rt.capture()          # each segment of the step replayed from a CUDA graph (no host gaps)
+        try:
+            rt.capture()      # each segment of the step replayed from a CUDA graph (no host gaps)
+        except Exception as e:   # keep measuring (eagerly) rather than fail the run; say so in the line
+            print(f"bench: CUDA graph capture failed ({e}); timing the eager step", file=sys.stderr)
+            torch.cuda.synchronize()
+            rt.graphs = None
+            graphs = False
     bufs, out, stream = rt.bufs, rt.out, rt.stream
 
     for _ in range(max(3, args.warmup)):
