@@ -378,6 +378,7 @@ enum {
                                present iff header.flags has SZ3G_STREAM_LR                            */
 };
 #define SZ3G_STREAM_LR 0x1u   /* sz3g_stream_header.flags: an SZ3-LR stream (decompress with sz3g_lr_decompress) */
+#define SZ3G_STREAM_INTERP 0x2u   /* an SZ3-Interp stream: nblocks 0, no COEF_* sections (sz3g_interp_decompress) */
 uint64_t sz3g_stream_size(const sz3g_section* sections, uint32_t nsec);
 int sz3g_stream_write(const sz3g_stream_header* hdr, const sz3g_section* sections, uint32_t nsec,
                       void* out, uint64_t cap, uint64_t* written);
@@ -388,7 +389,7 @@ int sz3g_stream_read(const void* in, uint64_t len, sz3g_stream_header* hdr, sz3g
  * internally inconsistent (and would make a decoder read past a buffer).  Checks: dtype, 1 <= ndim <= 3
  * with leading extents 1, block_size 6, radius in [1, 32768], 1 <= max_len <= 16, chunk >= 1, eb_abs
  * finite and > 0, nblocks == sz3g_num_blocks(dims); every required section present once (LR_FLAGS iff
- * the LR flag); OUT_IDX = 8 n_outliers and OUT_VAL = sizeof(T) n_outliers bytes, every outlier index in
+ * the LR flag; no coefficient sections and nblocks 0 with the INTERP flag); OUT_IDX = 8 n_outliers and OUT_VAL = sizeof(T) n_outliers bytes, every outlier index in
  * the slab [dim0_offset n1 n2, (dim0_offset + n0) n1 n2); CODE_OFFS / COEF_OFFS hold exactly
  * ceil(n / chunk) + 1 u64 offsets (n = N codes, 4 nblocks coefficient symbols), starting at 0,
  * non-decreasing, each chunk at most ceil(chunk max_len / 32) words, ending at the payload's word count

@@ -148,14 +148,17 @@ int sz3g_stream_validate(const sz3g_stream_header* h, const sz3g_section* s, uin
     if (h->dims[d] > (UINT64_MAX / N)) return SZ3G_ECORRUPT;
     N *= h->dims[d];
   }
-  const uint64_t nb = cdiv(h->dims[0], 6) * cdiv(h->dims[1], 6) * cdiv(h->dims[2], 6);
+  const bool lr = (h->flags & SZ3G_STREAM_LR) != 0, ip = (h->flags & SZ3G_STREAM_INTERP) != 0;
+  if ((lr && ip) || (h->flags & ~(SZ3G_STREAM_LR | SZ3G_STREAM_INTERP))) return SZ3G_ECORRUPT;
+  // SZ3-Interp has no coefficients: nblocks 0 and no coefficient sections
+  const uint64_t nb = ip ? 0 : cdiv(h->dims[0], 6) * cdiv(h->dims[1], 6) * cdiv(h->dims[2], 6);
   if (h->nblocks != nb) return SZ3G_ECORRUPT;
-  const bool lr = (h->flags & SZ3G_STREAM_LR) != 0;
   const sz3g_section* sec[SZ3G_SEC_LR_FLAGS + 1] = {};
   for (uint32_t tag = SZ3G_SEC_CODE_BOOK; tag <= SZ3G_SEC_LR_FLAGS; tag++) {
     int cnt;
     sec[tag] = find(s, n, tag, &cnt);
-    const bool want = tag != SZ3G_SEC_LR_FLAGS || lr;
+    const bool coef = tag >= SZ3G_SEC_COEF_BOOK && tag <= SZ3G_SEC_COEF_ESC;
+    const bool want = tag == SZ3G_SEC_LR_FLAGS ? lr : !(coef && ip);
     if ((want && cnt != 1) || (!want && cnt != 0)) {
       *bad = tag;
       return SZ3G_ECORRUPT;
@@ -176,16 +179,16 @@ int sz3g_stream_validate(const sz3g_stream_header* h, const sz3g_section* s, uin
     }
   }
   if (!book_ok(sec[SZ3G_SEC_CODE_BOOK], 2 * h->radius, h->max_len)) { *bad = SZ3G_SEC_CODE_BOOK; return SZ3G_ECORRUPT; }
-  if (!book_ok(sec[SZ3G_SEC_COEF_BOOK], 65536, h->max_len)) { *bad = SZ3G_SEC_COEF_BOOK; return SZ3G_ECORRUPT; }
+  if (!ip && !book_ok(sec[SZ3G_SEC_COEF_BOOK], 65536, h->max_len)) { *bad = SZ3G_SEC_COEF_BOOK; return SZ3G_ECORRUPT; }
   if (!offsets_ok(sec[SZ3G_SEC_CODE_OFFS], sec[SZ3G_SEC_CODE_DATA], N, h->chunk, h->max_len)) {
     *bad = SZ3G_SEC_CODE_OFFS;
     return SZ3G_ECORRUPT;
   }
-  if (!offsets_ok(sec[SZ3G_SEC_COEF_OFFS], sec[SZ3G_SEC_COEF_DATA], 4 * nb, h->chunk, h->max_len)) {
+  if (!ip && !offsets_ok(sec[SZ3G_SEC_COEF_OFFS], sec[SZ3G_SEC_COEF_DATA], 4 * nb, h->chunk, h->max_len)) {
     *bad = SZ3G_SEC_COEF_OFFS;
     return SZ3G_ECORRUPT;
   }
-  if (sec[SZ3G_SEC_COEF_ESC]->bytes % 8) { *bad = SZ3G_SEC_COEF_ESC; return SZ3G_ECORRUPT; }
+  if (!ip && sec[SZ3G_SEC_COEF_ESC]->bytes % 8) { *bad = SZ3G_SEC_COEF_ESC; return SZ3G_ECORRUPT; }
   if (lr && sec[SZ3G_SEC_LR_FLAGS]->bytes != cdiv(nb, 8)) { *bad = SZ3G_SEC_LR_FLAGS; return SZ3G_ECORRUPT; }
   return SZ3G_OK;
 }

@@ -43,7 +43,7 @@ class HostResult:
         return sum(t.numel() * t.element_size() for t in (
             self.payload, self.offsets, self.coef_payload, self.coef_offsets, self.coef_escapes,
             self.outlier_idx, self.outlier_val)) + 4 + 3 * int((self.code_lengths > 0).sum()) + \
-            4 + 3 * int((self.coef_lengths > 0).sum()) + \
+            (4 + 3 * int((self.coef_lengths > 0).sum()) if self.coef_lengths.numel() else 0) + \
             ((self.lr_flags.numel() + 7) // 8 if self.lr_flags is not None else 0)   # flags as a bitmap
 
 
@@ -52,10 +52,13 @@ class PipelinedCodec:
                  device=None, outlier_cap: int | None = None, dim0_offset: int = 0, predictor: str = "regression"):
         """shape / dim0_offset: this rank's block-aligned slab when the field is sharded
         (torch.distributed initialised): the range and the histogram are then all-reduced.
-        predictor: "regression" (the block regression predictor) or "lr" (SZ3-LR: per block the better of
-        regression and the prequantised Lorenzo predictor)."""
-        if predictor not in ("regression", "lr"):
+        predictor: "regression" (the block regression predictor), "lr" (SZ3-LR: per block the better of
+        regression and the prequantised Lorenzo predictor) or "interp" (SZ3-Interp, level-serial: not
+        shardable, one process per field)."""
+        if predictor not in ("regression", "lr", "interp"):
             raise ValueError(f"unknown predictor {predictor!r}")
+        if predictor == "interp" and torch.distributed.is_initialized() and torch.distributed.get_world_size() > 1:
+            raise ValueError("SZ3-Interp is not sharded: its donors cross every slab boundary")
         self.predictor = predictor
         self.shape, self.dtype, self.eb, self.eb_mode, self.radius = tuple(shape), dtype, eb, eb_mode, radius
         self.dim0_offset = dim0_offset
@@ -69,6 +72,14 @@ class PipelinedCodec:
         self.x = [torch.empty(self.shape, dtype=dtype, device=dev) for _ in range(2)]
         self.out = [torch.empty(self.shape, dtype=dtype, device=dev) for _ in range(2)]
         self.bufs = [sz3g.CompressBuffers(self.shape, dtype, radius, outlier_cap, dev) for _ in range(2)]
+        # SZ3-Interp: per-slot outputs of sz3g_interp_compress (codes, its reconstruction buffer, outliers,
+        # histogram); the coefficient sections are empty
+        self.ires = [None, None]
+        if predictor == "interp":
+            self.ires = [sz3g.InterpCompressed(self.shape, dtype, radius, 0, bf.codes, torch.empty_like(self.x[0]),
+                                               bf.outlier_idx, bf.outlier_val, bf.outlier_count, bf.hist, bf.eb_abs,
+                                               bf.status) for bf in self.bufs]
+            self._none16 = torch.empty(0, dtype=torch.uint8, device=dev)
         for b in self.bufs:
             b.beta_buffer()
             if predictor == "lr":
@@ -122,6 +133,9 @@ class PipelinedCodec:
             st.wait_event(self.ev_in[b])
             st.wait_event(self.ev_out[b])                    # field k - 2's outputs have left slot b
             bufs.reset()
+            if self.predictor == "interp":
+                self._compute_interp(b, x, bufs, st)
+                return
             sz3g.regression_analyze(x, bufs.minmax, bufs.beta, stream=st)
             pdist.allreduce_range_(bufs.minmax)    # sharded: the global range (no-op on one rank)
             quantize = sz3g.lr_quantize if self.predictor == "lr" else sz3g.regression_quantize
@@ -155,6 +169,27 @@ class PipelinedCodec:
             self.ev_comp[b].record(st)
         self.state[b] = (table, hs, coef)
 
+    def _compute_interp(self, b: int, x: torch.Tensor, bufs, st):
+        """SZ3-Interp for slot b (inside _compute's stream context): range, level passes, codebook, encode,
+        decompression from the codes (the round trip, not the compress-time reconstruction)."""
+        res = self.ires[b]
+        mm = sz3g.value_range(x, bufs.minmax, stream=st) if self.eb_mode == "rel" else None
+        sz3g.interp_compress(x, self.eb, self.eb_mode, self.radius, d_minmax=mm, out=res, stream=st)
+        table = sz3g.huffman_codebook(res.hist, stream=st)
+        hs = sz3g.huffman_encode(res.codes.view(-1), table, payload=self.payload[b], offsets=self.offsets[b],
+                                 scratch=self.enc_scratch, stream=st)
+        sz3g.interp_decompress(res.codes, res.outlier_idx, res.outlier_val, res.outlier_idx.numel(), self.eb,
+                               self.radius, self.dtype, out=self.out[b], d_outlier_count=res.outlier_count,
+                               eb_mode=self.eb_mode, d_minmax=mm, stream=st)
+        z = torch.zeros((), dtype=torch.int64, device=self.dev)
+        sizes = torch.stack([res.status.to(torch.int64)[0], res.outlier_count[0], res.eb_abs_dev.view(torch.int64)[0],
+                             self.offsets[b][-1], z, z, table.status.to(torch.int64)[0] | hs.status.to(torch.int64)[0],
+                             (table.lengths > 0).sum(), z])
+        self.h_sizes[b].copy_(sizes, non_blocking=True)
+        self.ev_xfree[b].record(st)
+        self.ev_comp[b].record(st)
+        self.state[b] = (table, hs, None)
+
     def _copy_out(self, k: int, host_out: torch.Tensor) -> tuple[HostResult, int]:
         b = k % 2
         bufs = self.bufs[b]
@@ -165,7 +200,7 @@ class PipelinedCodec:
             raise sz3g.SZ3GError("bad value range")
         if status & sz3g.STATUS_OUTLIER_OVERFLOW:
             raise sz3g.SZ3GError("outlier capacity exceeded")
-        if hstat or nesc > coef.escapes.numel():
+        if hstat or (coef is not None and nesc > coef.escapes.numel()):
             raise sz3g.SZ3GError("Huffman stage failed (status or escape capacity)")
         import struct
         eb_abs = struct.unpack("<d", struct.pack("<q", eb_bits))[0]
@@ -181,8 +216,12 @@ class PipelinedCodec:
             self.h_offsets[b].copy_(self.offsets[b], non_blocking=True)
             host_out.copy_(self.out[b], non_blocking=True)
             small = []
-            srcs = [table.lengths, coef.stream.payload[:cw], coef.stream.offsets, coef.table.lengths,
-                    coef.escapes[:nesc], bufs.outlier_idx[:n_out], bufs.outlier_val[:n_out]]
+            if coef is None:   # SZ3-Interp: no coefficient sections
+                e = self._none16
+                srcs = [table.lengths, e, e, e, e, bufs.outlier_idx[:n_out], bufs.outlier_val[:n_out]]
+            else:
+                srcs = [table.lengths, coef.stream.payload[:cw], coef.stream.offsets, coef.table.lengths,
+                        coef.escapes[:nesc], bufs.outlier_idx[:n_out], bufs.outlier_val[:n_out]]
             if self.predictor == "lr":
                 srcs.append(bufs.lr_flags)
             for h, t in zip(self.h_small[b], srcs):
@@ -193,8 +232,9 @@ class PipelinedCodec:
         # compressed bytes of this field, from the device-side sizes (no read of the pinned data):
         # the same sum as HostResult.nbytes()
         es = torch.empty((), dtype=self.dtype).element_size()
-        nbytes = 4 * words + 8 * self.offsets[b].numel() + 4 * cw + 8 * coef.stream.offsets.numel() + 8 * nesc + \
-            (8 + es) * n_out + 4 + 3 * nact + 4 + 3 * ncact + ((self.nb + 7) // 8 if self.predictor == "lr" else 0)
+        coef_b = 0 if coef is None else 4 * cw + 8 * coef.stream.offsets.numel() + 8 * nesc + 4 + 3 * ncact
+        nbytes = 4 * words + 8 * self.offsets[b].numel() + coef_b + (8 + es) * n_out + 4 + 3 * nact + \
+            ((self.nb + 7) // 8 if self.predictor == "lr" else 0)
         return HostResult(hp, self.h_offsets[b], small[0], small[1], small[2], small[3], small[4], small[5], small[6],
                           eb_abs, small[7] if self.predictor == "lr" else None), nbytes
 

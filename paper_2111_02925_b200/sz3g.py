@@ -56,6 +56,7 @@ class Section(ctypes.Structure):
 SEC_CODE_BOOK, SEC_CODE_OFFS, SEC_CODE_DATA, SEC_COEF_BOOK, SEC_COEF_OFFS, SEC_COEF_DATA, SEC_COEF_ESC, \
     SEC_OUT_IDX, SEC_OUT_VAL, SEC_LR_FLAGS = range(1, 11)
 STREAM_LR = 0x1   # sz3g_stream_header.flags: SZ3-LR stream
+STREAM_INTERP = 0x2   # SZ3-Interp stream (no coefficient sections)
 
 
 _lib = None
@@ -895,21 +896,27 @@ def to_bytes(res: "Compressed", table: HuffmanTable | None = None, hs: HuffmanSt
         table = huffman_codebook(res.hist).check()
     if hs is None:
         hs = huffman_encode(res.codes.view(-1), table).check()
-    if coef is None:
+    interp = isinstance(res, InterpCompressed)
+    if coef is None and not interp:
         coef = encode_coefficients(res.coef_codes)
     n = res.n_outliers
     host = [
         (SEC_CODE_BOOK, _book_bytes(table.lengths)),
         (SEC_CODE_OFFS, hs.offsets.cpu().numpy().tobytes()),
         (SEC_CODE_DATA, hs.payload[:hs.words()].cpu().numpy().tobytes()),
-        (SEC_COEF_BOOK, _book_bytes(coef.table.lengths)),
-        (SEC_COEF_OFFS, coef.stream.offsets.cpu().numpy().tobytes()),
-        (SEC_COEF_DATA, coef.stream.payload[:coef.stream.words()].cpu().numpy().tobytes()),
-        (SEC_COEF_ESC, coef.escapes.cpu().numpy().tobytes()),
+    ]
+    if not interp:
+        host += [
+            (SEC_COEF_BOOK, _book_bytes(coef.table.lengths)),
+            (SEC_COEF_OFFS, coef.stream.offsets.cpu().numpy().tobytes()),
+            (SEC_COEF_DATA, coef.stream.payload[:coef.stream.words()].cpu().numpy().tobytes()),
+            (SEC_COEF_ESC, coef.escapes.cpu().numpy().tobytes()),
+        ]
+    host += [
         (SEC_OUT_IDX, res.outlier_idx[:n].cpu().numpy().tobytes()),
         (SEC_OUT_VAL, res.outlier_val[:n].cpu().numpy().tobytes()),
     ]
-    if res.lr_flags is not None:   # SZ3-LR: the per-block predictor flags as a bitmap
+    if not interp and res.lr_flags is not None:   # SZ3-LR: the per-block predictor flags as a bitmap
         import numpy as np
         host.append((SEC_LR_FLAGS, np.packbits(res.lr_flags.cpu().numpy(), bitorder="little").tobytes()))
     secs = (Section * len(host))()
@@ -922,8 +929,8 @@ def to_bytes(res: "Compressed", table: HuffmanTable | None = None, hs: HuffmanSt
     hdr = StreamHeader(_dtype_id(res.dtype), len(res.shape), (ctypes.c_uint64 * 3)(*s3),
                        {"abs": SZ3G_EB_ABS, "rel": SZ3G_EB_REL_RANGE}[eb_mode],
                        float(res.eb_abs if eb is None else eb), float(res.eb_abs), res.radius, BLOCK, hs.chunk,
-                       table.max_len, STREAM_LR if res.lr_flags is not None else 0, n, res.coef_codes.shape[0],
-                       int(res.dim0_offset))
+                       table.max_len, STREAM_INTERP if interp else (STREAM_LR if res.lr_flags is not None else 0), n,
+                       0 if interp else res.coef_codes.shape[0], int(res.dim0_offset))
     lib = load()
     size = int(lib.sz3g_stream_size(secs, len(host)))
     out = ctypes.create_string_buffer(size)
@@ -974,6 +981,16 @@ def from_bytes(buf: bytes, device=None) -> torch.Tensor:
     t_codes = table_from(sec[SEC_CODE_BOOK], 2 * R)
     hs = stream_from(sec[SEC_CODE_OFFS], sec[SEC_CODE_DATA], N)
     codes = huffman_decode(hs, t_codes).view(shape)
+    if hdr.flags & STREAM_INTERP:   # SZ3-Interp: no coefficients
+        oidx = torch.from_numpy(np.frombuffer(sec[SEC_OUT_IDX], np.int64).copy()).to(device)
+        oval = torch.from_numpy(np.frombuffer(sec[SEC_OUT_VAL], np.float32 if dtype == torch.float32 else np.float64)
+                                .copy()).to(device)
+        out = interp_decompress(codes, oidx, oval, int(hdr.n_outliers), hdr.eb_abs, R, dtype)
+        out = out.view(shape)
+        torch.cuda.synchronize()
+        if int(hs.status.item()):
+            raise SZ3GError("corrupt Huffman stream")
+        return out
     t_coef = table_from(sec[SEC_COEF_BOOK], 65536)
     cs = stream_from(sec[SEC_COEF_OFFS], sec[SEC_COEF_DATA], 4 * nb)
     esc = torch.from_numpy(np.frombuffer(sec[SEC_COEF_ESC], np.int64).copy()).to(device)

@@ -167,3 +167,31 @@ def test_validate_rejects_inconsistent_stream(case, tag):
             h.ndim = 2
     rc, bad = _mut(f)
     assert rc == -5 and bad == tag, (case, rc, bad)
+
+
+def _valid_interp():
+    """A consistent SZ3-Interp stream: no coefficient sections, nblocks 0."""
+    hdr, secs = _valid()
+    secs = [s for s in secs if s[0] not in (sz3g.SEC_COEF_BOOK, sz3g.SEC_COEF_OFFS, sz3g.SEC_COEF_DATA,
+                                             sz3g.SEC_COEF_ESC)]
+    hdr.flags = sz3g.STREAM_INTERP
+    hdr.nblocks = 0
+    return hdr, secs
+
+
+def test_validate_interp_streams():
+    assert validate(*_valid_interp()) == (0, 0)
+    hdr, secs = _valid_interp()
+    hdr.nblocks = 1                                    # an Interp stream carries no blocks
+    assert validate(hdr, secs)[0] == -5
+    hdr, secs = _valid_interp()
+    hdr.flags = sz3g.STREAM_INTERP | sz3g.STREAM_LR    # exclusive
+    assert validate(hdr, secs)[0] == -5
+    hdr, secs = _valid()
+    hdr.flags = sz3g.STREAM_INTERP                     # coefficient sections present
+    hdr.nblocks = 0
+    rc, bad = validate(hdr, secs)
+    assert rc == -5 and bad == sz3g.SEC_COEF_BOOK
+    hdr, secs = _valid()
+    hdr.flags = 0x8                                    # unknown flag
+    assert validate(hdr, secs)[0] == -5

@@ -86,3 +86,37 @@ def test_pipeline_slots_do_not_alias_and_sizes():
 
     sizes = codec.run(hosts, h_out, on_result=on)
     assert sizes == [nb[k] for k in range(4)]
+
+
+def test_pipeline_interp_matches_direct():
+    """predictor="interp": every field's reconstruction equals interp_decompress(interp_compress(x)) bit
+    for bit, its Huffman payload equals huffman_encode of the same codes, there are no coefficient
+    sections, and run()'s sizes equal HostResult.nbytes()."""
+    from paper_2111_02925_b200 import sz3g
+    from paper_2111_02925_b200.pipeline import PipelinedCodec
+    from synth import config_by_name, make_field
+    cfg = config_by_name("c2")
+    fields = [make_field(cfg, device="cuda", shape=(40, 72, 130)) * (1.0 + 0.5 * k) for k in range(3)]
+    hosts = [f.cpu().pin_memory() for f in fields]
+    h_out = torch.empty_like(hosts[0]).pin_memory()
+    R = 512
+    n = fields[0].numel()
+    codec = PipelinedCodec(tuple(fields[0].shape), fields[0].dtype, cfg.eb, cfg.eb_mode, R, outlier_cap=n,
+                           predictor="interp")
+    got = {}
+    codec.run(hosts, h_out, on_result=lambda k, r: got.__setitem__(
+        k, (h_out.clone(), r.payload.clone(), r.offsets.clone(), r.coef_payload.numel(), r.outlier_idx.numel(),
+            r.nbytes())))
+    for k, x in enumerate(fields):
+        res = sz3g.interp_compress(x, cfg.eb, cfg.eb_mode, R, outlier_cap=n).finalize()
+        direct = sz3g.interp_decompress(res.codes, res.outlier_idx, res.outlier_val, res.n_outliers, res.eb_abs, R,
+                                        x.dtype).cpu()
+        xo, pay, offs, ncp, nout, _ = got[k]
+        assert torch.equal(xo.view(torch.int32), direct.view(torch.int32))
+        table = sz3g.huffman_codebook(res.hist).check()
+        hs = sz3g.huffman_encode(res.codes.view(-1), table).check()
+        assert torch.equal(offs, hs.offsets.cpu()) and torch.equal(pay, hs.payload[:hs.words()].cpu())
+        assert ncp == 0 and nout == res.n_outliers > 0
+    sizes = codec.run(hosts, h_out, on_result=lambda k, r: got.__setitem__(k, r.nbytes()))
+    assert sizes == [got[k] for k in range(3)]
+

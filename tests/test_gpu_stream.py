@@ -82,3 +82,21 @@ def test_bytes_round_trip_slab_with_dim0_offset():
     assert ((direct.double() - x.double()).abs().max().item()) <= res.eb_abs
     back = s.from_bytes(s.to_bytes(res, eb=1e-3, eb_mode="rel"))
     assert torch.equal(back.view(torch.int32), direct.view(torch.int32))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_interp_bytes_round_trip(name):
+    """SZ3-Interp results through the container (no coefficient sections): from_bytes takes the Interp
+    decompressor and returns the direct decompression bit for bit."""
+    s = sz()
+    from synth import config_by_name, make_field
+    cfg = config_by_name(name)
+    x = make_field(cfg, device="cuda")
+    res = s.interp_compress(x, cfg.eb, cfg.eb_mode, cfg.radius, outlier_cap=x.numel()).finalize()
+    direct = s.interp_decompress(res.codes, res.outlier_idx, res.outlier_val, res.n_outliers, res.eb_abs, cfg.radius,
+                                 x.dtype)
+    b = s.to_bytes(res, eb=cfg.eb, eb_mode=cfg.eb_mode)
+    back = s.from_bytes(b)
+    assert back.shape == x.shape and torch.equal(back.view(torch.uint8), direct.view(torch.uint8))
+    assert (back.double() - x.double()).abs().max().item() <= res.eb_abs
+    print(name, "interp stream ratio", round(x.numel() * x.element_size() / len(b), 3))
