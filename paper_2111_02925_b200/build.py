@@ -16,8 +16,8 @@ DEPS = [*SRCS, os.path.join(HERE, "csrc", "tile.cuh"), os.path.join(HERE, "csrc"
         os.path.join(ROOT, "include", "sz3g.h")]
 LIB = os.path.join(HERE, "lib", "libsz3g.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+CFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
+LFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static"]
 
 
 def needs_build() -> bool:
@@ -27,16 +27,38 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
+def _obj_dir(out: str, defines) -> str:
+    tag = "default" if not defines else "d" + format(abs(hash(tuple(defines))) % (1 << 32), "08x")
+    return os.path.join(os.path.dirname(out), "obj", tag)
+
+
 def build(force: bool = False, verbose: bool = False, src=None, out: str = LIB, defines=()) -> str:
-    """nvcc `src` -> `out` (defaults: the in-tree library; another src/out builds an A/B variant)."""
+    """nvcc `src` -> `out` (defaults: the in-tree library; another src/out builds an A/B variant).
+    Each translation unit is compiled to its own object in parallel (a unit is recompiled only when it
+    or a shared header changed, unless `force`), then linked with the static CUDA runtime."""
     if not force and out == LIB and not needs_build():
         return LIB
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    tmp = out + f".tmp{os.getpid()}"
     srcs = SRCS if src is None else ([src] if isinstance(src, str) else list(src))
-    cmd = [NVCC, *FLAGS, *defines, *(["-Xptxas", "-v"] if verbose else []), "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, *srcs]
-    subprocess.run(cmd, check=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+    cflags = [NVCC, *CFLAGS, *defines, *(["-Xptxas", "-v"] if verbose else []), *inc]
+    odir = _obj_dir(out, defines) if src is None else os.path.join(os.path.dirname(out), "obj", "ab")
+    os.makedirs(odir, exist_ok=True)
+    hdr_t = max(os.path.getmtime(d) for d in DEPS if not d.endswith(".cu"))
+    procs, objs = [], []
+    for s in srcs:
+        o = os.path.join(odir, os.path.basename(s)[:-3] + ".o")
+        objs.append(o)
+        if not force and src is None and os.path.exists(o) and os.path.getmtime(o) > max(hdr_t, os.path.getmtime(s)):
+            continue
+        procs.append((s, subprocess.Popen([*cflags, "-c", "-o", o + ".tmp", s])))
+    for s, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, f"nvcc {s}")
+        os.replace(os.path.join(odir, os.path.basename(s)[:-3] + ".o.tmp"),
+                   os.path.join(odir, os.path.basename(s)[:-3] + ".o"))
+    tmp = out + f".tmp{os.getpid()}"
+    subprocess.run([NVCC, *LFLAGS, "-o", tmp, *objs], check=True)
     os.replace(tmp, out)
     return out
 
