@@ -1054,12 +1054,16 @@ constexpr int DF_WARPS = 8, DF_ROUND = 32, DF_RING = 16, DF_RING_W = 20;   // ri
 #define SZ3G_DF_MINB 4     // __launch_bounds__ minimum blocks per SM: 4 x 8 warps (smem allows 4)
 #endif
 
+#ifndef SZ3G_DF_PREF
+#define SZ3G_DF_PREF 1   // the window's next ring word loaded one refill ahead, by the taking lanes only
+#endif
 struct DfLane {
   uint32_t hi, lo;  // left-aligned 64-bit bit window (hi = its upper 32 bits)
   uint32_t avail;   // valid bits in the window
   uint32_t rpos;    // next ring word to read (mod DF_RING), counted from the aligned chunk start
   uint32_t fpos;    // ring words requested so far (16-byte copies of 4 words)
   uint32_t nref;    // words appended to the window
+  uint32_t wn;      // SZ3G_DF_PREF: ring word rpos, loaded ahead
 };
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -1103,7 +1107,7 @@ __device__ __forceinline__ void df_topup(DfLane& d, uint32_t s_ring, const uint3
 // branch-free, a 32-bit shared address, clamped funnel shifts (a shift by 32 gives 0)
 __device__ __forceinline__ void df_refill(DfLane& d, uint32_t s_ring) {
   const bool take = d.avail <= 32u;
-  const uint32_t w = lds32(s_ring + 4u * (d.rpos & (DF_RING - 1)));
+  const uint32_t w = SZ3G_DF_PREF ? d.wn : lds32(s_ring + 4u * (d.rpos & (DF_RING - 1)));
   const uint32_t add_hi = __funnelshift_rc(w, 0u, d.avail);          // w >> avail (0 at avail = 32)
   const uint32_t new_lo = __funnelshift_lc(0u, w, 32u - d.avail);    // w << (32 - avail) (0 at avail = 0)
   d.hi = take ? (d.hi | add_hi) : d.hi;
@@ -1111,6 +1115,10 @@ __device__ __forceinline__ void df_refill(DfLane& d, uint32_t s_ring) {
   d.avail += take ? 32u : 0u;
   d.nref += take ? 1u : 0u;
   d.rpos += take ? 1u : 0u;
+  if (SZ3G_DF_PREF)   // the next word, by the taking lanes only (predicated load, off the decode chain)
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.u32 %0, [%1];\n}"
+                 : "+r"(d.wn)
+                 : "r"(s_ring + 4u * (d.rpos & (DF_RING - 1))), "r"((uint32_t)take));
 }
 
 // shift the window left by L (<= 16) bits
@@ -1178,6 +1186,7 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
   d.nref = 0;
   df_topup<DF_RING / 4>(d, s_ring, payload, a0, lim);   // 16 words
   asm volatile("cp.async.wait_all;\n" ::: "memory");
+  d.wn = lds32(s_ring + 4u * (d.rpos & (DF_RING - 1)));
   df_refill(d, s_ring);                      // prime 64 bits
   df_refill(d, s_ring);
   bool bad = false;
