@@ -541,17 +541,31 @@ def config_leg(sz3g, spec, peaks, steps, warmup, flush_buf, x=None):
     for _ in range(warmup):
         rt.step()
     recs = []
+    timed = None
+    try:   # the whole step as one graph with its timing events as graph nodes (no launch gaps)
+        timed = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(6)]
+        rt.capture_timed(timed)
+        launch = "the whole step replayed from ONE CUDA graph, timing events as graph nodes"
+    except Exception as e:
+        print(f"bench: single-graph capture failed for {spec} ({e}); per-segment graphs", file=sys.stderr)
+        torch.cuda.synchronize()
+        timed = None
+    spans = ((4, 5), (0, 1), (2, 3), (4, 3))   # analyze, quantise, decompress, step (event indices)
     for _ in range(steps):
         flush_l2(flush_buf)
-        r = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        rt.step(r)
-        recs.append(r)
+        if timed is not None:
+            rt.replay_timed()
+            torch.cuda.synchronize()
+            recs.append([timed[i].elapsed_time(timed[j]) for i, j in spans])
+        else:
+            r = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            rt.step(r)
+            recs.append(r)
     torch.cuda.synchronize()
+    if timed is None:
+        recs = [[r[i].elapsed_time(r[j]) for i, j in spans] for r in recs]
     res = rt.result()
-    ana = sum(r[4].elapsed_time(r[5]) for r in recs) / steps
-    qua = sum(r[0].elapsed_time(r[1]) for r in recs) / steps
-    dec = sum(r[2].elapsed_time(r[3]) for r in recs) / steps
-    step = sum(r[4].elapsed_time(r[3]) for r in recs) / steps
+    ana, qua, dec, step = (sum(r[k] for r in recs) / steps for k in range(4))
     b = alg_bytes(N, NB, s, res.n_outliers)
     st = sz3g.error_stats(x, rt.out, res.eb_abs).cpu().tolist()
     if st[2] != 0 or not st[0] <= res.eb_abs:

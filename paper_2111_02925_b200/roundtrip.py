@@ -139,6 +139,33 @@ class RoundTrip:
         self.launches_per_step = sz3g.launch_count() - l0   # library kernels in one replayed step
         return self
 
+    def capture_timed(self, record):
+        """The whole step as ONE CUDA graph whose six timing events (``record``, created with
+        ``external=True``) are nodes of the graph, recorded at the segment boundaries exactly as
+        ``step(record)`` records them.  ``replay_timed()`` then runs the step with no host work and no
+        graph-launch gap between segments (small fields: the per-segment graphs of ``capture()`` put a
+        launch boundary inside every timed segment).  Single process only."""
+        if torch.distributed.is_initialized() and torch.distributed.get_world_size(self.group) > 1:
+            raise RuntimeError("capture_timed is single-process")
+        self.step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            st = torch.cuda.current_stream()
+            record[4].record(st)
+            for name, after in zip(self.SEGMENTS, self._AFTER):
+                if name != "_hist":           # single process: no collective
+                    getattr(self, name)(st)
+                record[after].record(st)
+        torch.cuda.synchronize()
+        self.timed_graph, self.timed_record = g, record
+        return self
+
+    def replay_timed(self):
+        """One step from the ``capture_timed`` graph; its events hold this step's segment times."""
+        with torch.cuda.stream(self.stream):
+            self.timed_graph.replay()
+
     def finish(self):
         """Make the stream wait for the last step's histogram all-reduce (part of the step's output)."""
         if self._hist_pending:
