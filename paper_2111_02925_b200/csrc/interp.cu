@@ -251,6 +251,175 @@ __global__ void __launch_bounds__(256) k_interp_pairs(const T* __restrict__ x, T
 }
 
 // ------------------------------------------------------------------------------------------------
+// Level s = 1, passes (1,1) and (1,2) by rows (SZ3G_IP_ROWS, the default).  Both passes stay inside one
+// plane i, and pass (1,2) inside one row (i, j): a row j odd holds the targets of (1,1) at even k (donors:
+// the even rows j -+ 1, j -+ 3 at the same k, final after pass (1,0)) and of (1,2) at odd k (donors: the
+// row's own even k, just computed), a row j even only those of (1,2).  One warp per row, lane l on the
+// column pair (k0 + 2l, k0 + 2l + 1) of a 64-column segment; the (1,2) donors of a segment reach two
+// even columns into the next segment, so the even columns are computed (or, even rows, loaded) one
+// segment ahead.  Every row leaves whole -- x' and codes as pairs, the even column's value and code
+// rewritten unchanged on even rows -- so no store is a partial sector; odd rows (launch 1) and even rows
+// (launch 2) run apart, so no launch reads a sector another warp of it stores.  The prediction and
+// quantisation are k_interp_pass's, op for op: bit-identical to the per-pass schedule.
+#ifndef SZ3G_IP_ROWS
+#define SZ3G_IP_ROWS 1
+#endif
+constexpr int IR_WARPS = 8;
+
+// O8-O10 of one target (k_interp_pass): code (0 = outlier) and x' (x for an outlier)
+template <typename T>
+__device__ __forceinline__ bool ip_quant(T xv, double p, const Consts& K, uint32_t R, uint16_t& code, T& y) {
+  const double xd = to_d<T>(xv);
+  const double t = __dmul_rn(__dsub_rn(xd, p), K.inv2eb);
+  const double sm = __dadd_rn(t, RINT_MAGIC);
+  const double q = __dsub_rn(sm, RINT_MAGIC);
+  const T yy = from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, q)));
+  const bool ok = fabs(t) < (double)R && fabs(q) < (double)R && fabs(__dsub_rn(to_d<T>(yy), xd)) <= K.eb_abs;
+  code = ok ? (uint16_t)(__double2loint(sm) + (int)R) : (uint16_t)0;
+  y = ok ? yy : xv;
+  return ok;
+}
+
+template <typename T>
+__device__ __forceinline__ void ip_append(bool is_out, uint64_t e, T xv, unsigned long long* ocount, uint64_t* oidx,
+                                          T* oval, const IpArgs& a, int lane) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, is_out);
+  if (bal) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(ocount, (unsigned long long)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (is_out) {
+      const unsigned long long pos = base + __popc(bal & ((1u << lane) - 1u));
+      if (pos < a.cap) {
+        oidx[pos] = a.gofs + e;
+        oval[pos] = xv;
+      }
+    }
+  }
+}
+
+template <typename T, bool DEC, bool ODD>
+__global__ void __launch_bounds__(IR_WARPS * 32) k_interp_rows(const T* __restrict__ x, T* __restrict__ xp,
+                                                               uint16_t* __restrict__ codes,
+                                                               uint64_t* __restrict__ oidx, T* __restrict__ oval,
+                                                               unsigned long long* __restrict__ ocount, IpArgs a) {
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    Consts K;
+    s_ok = ip_consts(a, K);
+    s_k = K;
+  }
+  SZ3G_SYNCTHREADS();
+  if (!s_ok) return;
+  const Consts K = s_k;
+  const uint64_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2];
+  const int lane = threadIdx.x & 31;
+  const uint64_t nj = ODD ? n1 / 2 : (n1 + 1) / 2;   // rows of this parity per plane
+  const uint64_t nrows = n0 * nj;
+  const uint64_t nseg = (n2 + 63) / 64;
+  const bool p12 = n2 > 1;                            // pass (1,2) has targets
+  const bool base_al = (reinterpret_cast<uintptr_t>(xp) % (2 * sizeof(T))) == 0 &&
+                       (reinterpret_cast<uintptr_t>(codes) % 4) == 0;
+  for (uint64_t r = (uint64_t)blockIdx.x * IR_WARPS + (threadIdx.x >> 5); r < nrows;
+       r += (uint64_t)gridDim.x * IR_WARPS) {
+    const uint64_t i = r / nj, j = 2 * (r - i * nj) + (ODD ? 1 : 0);
+    const uint64_t re = (i * n1 + j) * n2;
+    const bool vec = (re & 1) == 0 && base_al;        // pairs 2 sizeof(T)-byte / 4-byte (codes) aligned
+    // pass (1,1) mode of this row (odd rows): cubic / linear / copy along j
+    const int mj = (j >= 3 && j + 3 < n1) ? 2 : (j + 1 < n1 ? 1 : 0);
+    // even column ke of segment sg: its x' (computed by (1,1) on odd rows, final on even rows) and code
+    auto even_col = [&](uint64_t sg, T& xe, uint16_t& ce, bool& out) {
+      const uint64_t ke = 64 * sg + 2 * lane;
+      out = false;
+      xe = T(0);
+      ce = 0;
+      if (ke >= n2) return;
+      const uint64_t e = re + ke;
+      if (!ODD) {
+        xe = xp[e];
+        if (!DEC) ce = codes[e];
+        return;
+      }
+      const double b = to_d<T>(xp[e - n2]);
+      const double c = mj >= 1 ? to_d<T>(xp[e + n2]) : 0.0;
+      const double av = mj == 2 ? to_d<T>(xp[e - 3 * n2]) : 0.0;
+      const double ev = mj == 2 ? to_d<T>(xp[e + 3 * n2]) : 0.0;
+      const double p = ip_predict(av, b, c, ev, mj);
+      if (DEC) {
+        const uint16_t cin = codes[e];
+        xe = cin != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)cin - (int)a.R)))) : xp[e];
+      } else {
+        out = !ip_quant<T>(x[e], p, K, a.R, ce, xe);
+      }
+    };
+    T xe_cur, xe_nxt, xe_prev = T(0);
+    uint16_t ce_cur, ce_nxt;
+    bool out_cur, out_nxt;
+    even_col(0, xe_cur, ce_cur, out_cur);
+    for (uint64_t sg = 0; sg < nseg; sg++) {
+      even_col(sg + 1, xe_nxt, ce_nxt, out_nxt);
+      const uint64_t ke = 64 * sg + 2 * lane, ko = ke + 1;
+      // (1,2) donors of ko: ke - 2, ke, ke + 2, ke + 4 (lanes l - 1, l, l + 1, l + 2 or the next segment)
+      const T dn1 = __shfl_up_sync(0xffffffffu, xe_cur, 1);   // every lane takes part in every shuffle
+      const T dm2 = lane == 0 ? xe_prev : dn1;
+      const T up1 = __shfl_down_sync(0xffffffffu, xe_cur, 1), nx0 = __shfl_sync(0xffffffffu, xe_nxt, 0);
+      const T up2 = __shfl_down_sync(0xffffffffu, xe_cur, 2), nx1 = __shfl_sync(0xffffffffu, xe_nxt, 1);
+      const T dp2 = lane == 31 ? nx0 : up1;
+      const T dp4 = lane == 31 ? nx1 : (lane == 30 ? nx0 : up2);
+      xe_prev = __shfl_sync(0xffffffffu, xe_cur, 31);
+      T xo = T(0);
+      uint16_t co = 0;
+      bool out_o = false;
+      const bool has_o = p12 && ko < n2;
+      if (has_o) {
+        const int mk = (ko >= 3 && ko + 3 < n2) ? 2 : (ko + 1 < n2 ? 1 : 0);
+        const double p = ip_predict(to_d<T>(dm2), to_d<T>(xe_cur), to_d<T>(dp2), to_d<T>(dp4), mk);
+        const uint64_t e = re + ko;
+        if (DEC) {
+          const uint16_t cin = codes[e];
+          xo = cin != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)cin - (int)a.R)))) : xp[e];
+        } else {
+          out_o = !ip_quant<T>(x[e], p, K, a.R, co, xo);
+        }
+      }
+      // the row's pair back, whole
+      if (ke < n2) {
+        const uint64_t e = re + ke;
+        if (has_o && vec) {
+          if (sizeof(T) == 4) {
+            float2 v;
+            v.x = (float)xe_cur;
+            v.y = (float)xo;
+            *reinterpret_cast<float2*>(xp + e) = v;
+          } else {
+            double2 v;
+            v.x = (double)xe_cur;
+            v.y = (double)xo;
+            *reinterpret_cast<double2*>(xp + e) = v;
+          }
+          if (!DEC) *reinterpret_cast<uint32_t*>(codes + e) = (uint32_t)ce_cur | ((uint32_t)co << 16);
+        } else {
+          xp[e] = xe_cur;
+          if (!DEC) codes[e] = ce_cur;
+          if (has_o) {
+            xp[e + 1] = xo;
+            if (!DEC) codes[e + 1] = co;
+          }
+        }
+      }
+      if (!DEC) {
+        if (ODD) ip_append<T>(out_cur, re + ke, ke < n2 ? x[re + ke] : T(0), ocount, oidx, oval, a, lane);
+        ip_append<T>(out_o, re + ko, has_o ? x[re + ko] : T(0), ocount, oidx, oval, a, lane);
+      }
+      xe_cur = xe_nxt;
+      ce_cur = ce_nxt;
+      out_cur = out_nxt;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Level s = 1 fused (its three passes hold 7/8 of the targets): one CTA per tile of 2 planes (i0 even,
 // i0 + 1) x L1_TJ rows x L1_TK columns, in shared memory with a halo of 2 even coordinates along j and k
 // (the -+1, -+3 donors).  Pass (1,0) targets (i odd, j and k even) are computed over the whole halo box
@@ -540,6 +709,34 @@ int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* 
         return SZ3G_ECUDA;
       kern<<<grid, L1_WARPS * 32, L1Smem<T>::total, st>>>(x, xp, codes, oidx, oval, ocount, a);
       nl++;
+      break;
+    }
+    if (s == 1 && SZ3G_IP_ROWS) {   // level 1: pass (1,0) by its kernel, passes (1,1) + (1,2) by rows
+      if (pass_geometry(a, s, 0)) {
+        if (DEC && SZ3G_IP_PAIRS) {
+          const uint64_t np = (a.n[2] + 1) / 2;
+          const uint64_t rows = (a.n[0] / 2) * ((a.n[1] + 1) / 2);
+          const dim3 grid((unsigned)((np + 255) / 256), (unsigned)std::min<uint64_t>(rows, 65535));
+          k_interp_pairs<T, DEC, 0><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        } else {
+          const dim3 grid((unsigned)((a.cnt[2] + 255) / 256), (unsigned)std::min<uint64_t>(a.cnt[1], 65535),
+                          (unsigned)std::min<uint64_t>(a.cnt[0], 65535));
+          k_interp_pass<T, DEC><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        }
+        nl++;
+      }
+      pass_geometry(a, s, 2);   // a.s = 1 (the row kernels read only the extents and the constants)
+      const uint64_t odd_rows = a.n[0] * (a.n[1] / 2), even_rows = a.n[0] * ((a.n[1] + 1) / 2);
+      if (odd_rows) {
+        const unsigned g = (unsigned)std::min<uint64_t>((odd_rows + IR_WARPS - 1) / IR_WARPS, 1u << 20);
+        k_interp_rows<T, DEC, true><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        nl++;
+      }
+      if (a.n[2] > 1) {
+        const unsigned g = (unsigned)std::min<uint64_t>((even_rows + IR_WARPS - 1) / IR_WARPS, 1u << 20);
+        k_interp_rows<T, DEC, false><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        nl++;
+      }
       break;
     }
     if (s == 1 && SZ3G_IP_PAIRS && (DEC || SZ3G_IP_PAIRS > 1)) {   // level 1: pair kernels (full-sector stores)
