@@ -265,6 +265,10 @@ __global__ void __launch_bounds__(256) k_interp_pairs(const T* __restrict__ x, T
 #define SZ3G_IP_ROWS 1
 #endif
 constexpr int IR_WARPS = 8;
+#ifndef SZ3G_IR_MINB
+#define SZ3G_IR_MINB 4   // __launch_bounds__ minimum blocks per SM of the row kernels (c5 A/B, compress /
+                         // decompress ms: 1 -> 37.6 / 25.8, 4 -> 30.6 / 22.4, 6 -> 32.9 / 24.3, 8 -> 41.9 / 24.5)
+#endif
 
 // O8-O10 of one target (k_interp_pass): code (0 = outlier) and x' (x for an outlier)
 template <typename T>
@@ -298,8 +302,8 @@ __device__ __forceinline__ void ip_append(bool is_out, uint64_t e, T xv, unsigne
   }
 }
 
-template <typename T, bool DEC, bool ODD>
-__global__ void __launch_bounds__(IR_WARPS * 32) k_interp_rows(const T* __restrict__ x, T* __restrict__ xp,
+template <typename T, bool DEC, int KIND>
+__global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(const T* __restrict__ x, T* __restrict__ xp,
                                                                uint16_t* __restrict__ codes,
                                                                uint64_t* __restrict__ oidx, T* __restrict__ oval,
                                                                unsigned long long* __restrict__ ocount, IpArgs a) {
@@ -315,56 +319,86 @@ __global__ void __launch_bounds__(IR_WARPS * 32) k_interp_rows(const T* __restri
   const Consts K = s_k;
   const uint64_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2];
   const int lane = threadIdx.x & 31;
-  const uint64_t nj = ODD ? n1 / 2 : (n1 + 1) / 2;   // rows of this parity per plane
-  const uint64_t nrows = n0 * nj;
+  // rows of this launch: KIND 1 (i, j odd); KIND 2 (i odd, j even); KIND 0 (i even, j even)
+  const uint64_t nj = KIND == 1 ? n1 / 2 : (n1 + 1) / 2;
+  const uint64_t ni = KIND == 1 ? n0 : (KIND == 2 ? n0 / 2 : (n0 + 1) / 2);
+  const uint64_t nrows = ni * nj;
   const uint64_t nseg = (n2 + 63) / 64;
   const bool p12 = n2 > 1;                            // pass (1,2) has targets
   const bool base_al = (reinterpret_cast<uintptr_t>(xp) % (2 * sizeof(T))) == 0 &&
                        (reinterpret_cast<uintptr_t>(codes) % 4) == 0;
+  // the loads of one segment (issued one segment before their use): the even column's inputs -- its
+  // (1,1) donors and x (odd rows), or its final x' and code (even rows) -- and the odd column's x (compress)
+  // or code (decompress)
+  struct Ld {
+    T b, c, av, ev, xe, xo;
+    uint16_t ce, co;
+  };
   for (uint64_t r = (uint64_t)blockIdx.x * IR_WARPS + (threadIdx.x >> 5); r < nrows;
        r += (uint64_t)gridDim.x * IR_WARPS) {
-    const uint64_t i = r / nj, j = 2 * (r - i * nj) + (ODD ? 1 : 0);
+    const uint64_t ti = r / nj;
+    const uint64_t i = KIND == 1 ? ti : 2 * ti + (KIND == 2 ? 1 : 0), j = 2 * (r - ti * nj) + (KIND == 1 ? 1 : 0);
     const uint64_t re = (i * n1 + j) * n2;
     const bool vec = (re & 1) == 0 && base_al;        // pairs 2 sizeof(T)-byte / 4-byte (codes) aligned
-    // pass (1,1) mode of this row (odd rows): cubic / linear / copy along j
-    const int mj = (j >= 3 && j + 3 < n1) ? 2 : (j + 1 < n1 ? 1 : 0);
-    // even column ke of segment sg: its x' (computed by (1,1) on odd rows, final on even rows) and code
-    auto even_col = [&](uint64_t sg, T& xe, uint16_t& ce, bool& out) {
+    // the even column's pass: (1,1) along j (KIND 1) or (1,0) along i (KIND 2), cubic / linear / copy
+    constexpr bool COMP = KIND != 0;
+    const uint64_t sd = KIND == 1 ? n2 : n1 * n2, id = KIND == 1 ? j : i, nd = KIND == 1 ? n1 : n0;
+    const int mj = (id >= 3 && id + 3 < nd) ? 2 : (id + 1 < nd ? 1 : 0);
+    auto load = [&](uint64_t sg) {
+      Ld L;
+      L.b = L.c = L.av = L.ev = L.xe = L.xo = T(0);
+      L.ce = L.co = 0;
+      const uint64_t ke = 64 * sg + 2 * lane;
+      if (ke >= n2) return L;
+      const uint64_t e = re + ke;
+      if (COMP) {
+        L.b = xp[e - sd];
+        if (mj >= 1) L.c = xp[e + sd];
+        if (mj == 2) {
+          L.av = xp[e - 3 * sd];
+          L.ev = xp[e + 3 * sd];
+        }
+        if (DEC) L.ce = codes[e];
+        else L.xe = x[e];
+      } else {
+        L.xe = xp[e];
+        if (!DEC) L.ce = codes[e];
+      }
+      if (p12 && ke + 1 < n2) {
+        if (DEC) L.co = codes[e + 1];
+        else L.xo = x[e + 1];
+      }
+      return L;
+    };
+    // the even column's x' and code from its loads (KIND 1 / 2: passes (1,1) / (1,0); KIND 0: as loaded)
+    auto even_col = [&](uint64_t sg, const Ld& L, T& xe, uint16_t& ce, bool& out) {
       const uint64_t ke = 64 * sg + 2 * lane;
       out = false;
-      xe = T(0);
-      ce = 0;
-      if (ke >= n2) return;
-      const uint64_t e = re + ke;
-      if (!ODD) {
-        xe = xp[e];
-        if (!DEC) ce = codes[e];
-        return;
-      }
-      const double b = to_d<T>(xp[e - n2]);
-      const double c = mj >= 1 ? to_d<T>(xp[e + n2]) : 0.0;
-      const double av = mj == 2 ? to_d<T>(xp[e - 3 * n2]) : 0.0;
-      const double ev = mj == 2 ? to_d<T>(xp[e + 3 * n2]) : 0.0;
-      const double p = ip_predict(av, b, c, ev, mj);
+      xe = L.xe;
+      ce = L.ce;
+      if (!COMP || ke >= n2) return;
+      const double p = ip_predict(to_d<T>(L.av), to_d<T>(L.b), to_d<T>(L.c), to_d<T>(L.ev), mj);
       if (DEC) {
-        const uint16_t cin = codes[e];
-        xe = cin != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)cin - (int)a.R)))) : xp[e];
+        xe = L.ce != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)L.ce - (int)a.R)))) : xp[re + ke];
       } else {
-        out = !ip_quant<T>(x[e], p, K, a.R, ce, xe);
+        out = !ip_quant<T>(L.xe, p, K, a.R, ce, xe);
       }
     };
+    Ld l_cur = load(0), l_nxt = load(1);
     T xe_cur, xe_nxt, xe_prev = T(0);
     uint16_t ce_cur, ce_nxt;
     bool out_cur, out_nxt;
-    even_col(0, xe_cur, ce_cur, out_cur);
+    even_col(0, l_cur, xe_cur, ce_cur, out_cur);
     for (uint64_t sg = 0; sg < nseg; sg++) {
-      even_col(sg + 1, xe_nxt, ce_nxt, out_nxt);
+      const Ld l_nn = load(sg + 2);
+      even_col(sg + 1, l_nxt, xe_nxt, ce_nxt, out_nxt);
       const uint64_t ke = 64 * sg + 2 * lane, ko = ke + 1;
-      // (1,2) donors of ko: ke - 2, ke, ke + 2, ke + 4 (lanes l - 1, l, l + 1, l + 2 or the next segment)
-      const T dn1 = __shfl_up_sync(0xffffffffu, xe_cur, 1);   // every lane takes part in every shuffle
-      const T dm2 = lane == 0 ? xe_prev : dn1;
+      // (1,2) donors of ko: ke - 2, ke, ke + 2, ke + 4 (lanes l - 1, l, l + 1, l + 2 or the next segment);
+      // every lane takes part in every shuffle
+      const T dn1 = __shfl_up_sync(0xffffffffu, xe_cur, 1);
       const T up1 = __shfl_down_sync(0xffffffffu, xe_cur, 1), nx0 = __shfl_sync(0xffffffffu, xe_nxt, 0);
       const T up2 = __shfl_down_sync(0xffffffffu, xe_cur, 2), nx1 = __shfl_sync(0xffffffffu, xe_nxt, 1);
+      const T dm2 = lane == 0 ? xe_prev : dn1;
       const T dp2 = lane == 31 ? nx0 : up1;
       const T dp4 = lane == 31 ? nx1 : (lane == 30 ? nx0 : up2);
       xe_prev = __shfl_sync(0xffffffffu, xe_cur, 31);
@@ -375,12 +409,11 @@ __global__ void __launch_bounds__(IR_WARPS * 32) k_interp_rows(const T* __restri
       if (has_o) {
         const int mk = (ko >= 3 && ko + 3 < n2) ? 2 : (ko + 1 < n2 ? 1 : 0);
         const double p = ip_predict(to_d<T>(dm2), to_d<T>(xe_cur), to_d<T>(dp2), to_d<T>(dp4), mk);
-        const uint64_t e = re + ko;
         if (DEC) {
-          const uint16_t cin = codes[e];
-          xo = cin != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)cin - (int)a.R)))) : xp[e];
+          xo = l_cur.co != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)l_cur.co - (int)a.R))))
+                             : xp[re + ko];
         } else {
-          out_o = !ip_quant<T>(x[e], p, K, a.R, co, xo);
+          out_o = !ip_quant<T>(l_cur.xo, p, K, a.R, co, xo);
         }
       }
       // the row's pair back, whole
@@ -409,9 +442,11 @@ __global__ void __launch_bounds__(IR_WARPS * 32) k_interp_rows(const T* __restri
         }
       }
       if (!DEC) {
-        if (ODD) ip_append<T>(out_cur, re + ke, ke < n2 ? x[re + ke] : T(0), ocount, oidx, oval, a, lane);
-        ip_append<T>(out_o, re + ko, has_o ? x[re + ko] : T(0), ocount, oidx, oval, a, lane);
+        if (COMP) ip_append<T>(out_cur, re + ke, l_cur.xe, ocount, oidx, oval, a, lane);
+        ip_append<T>(out_o, re + ko, l_cur.xo, ocount, oidx, oval, a, lane);
       }
+      l_cur = l_nxt;
+      l_nxt = l_nn;
       xe_cur = xe_nxt;
       ce_cur = ce_nxt;
       out_cur = out_nxt;
@@ -711,30 +746,17 @@ int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* 
       nl++;
       break;
     }
-    if (s == 1 && SZ3G_IP_ROWS) {   // level 1: pass (1,0) by its kernel, passes (1,1) + (1,2) by rows
-      if (pass_geometry(a, s, 0)) {
-        if (DEC && SZ3G_IP_PAIRS) {
-          const uint64_t np = (a.n[2] + 1) / 2;
-          const uint64_t rows = (a.n[0] / 2) * ((a.n[1] + 1) / 2);
-          const dim3 grid((unsigned)((np + 255) / 256), (unsigned)std::min<uint64_t>(rows, 65535));
-          k_interp_pairs<T, DEC, 0><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
-        } else {
-          const dim3 grid((unsigned)((a.cnt[2] + 255) / 256), (unsigned)std::min<uint64_t>(a.cnt[1], 65535),
-                          (unsigned)std::min<uint64_t>(a.cnt[0], 65535));
-          k_interp_pass<T, DEC><<<grid, 256, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
-        }
-        nl++;
-      }
+    if (s == 1 && SZ3G_IP_ROWS) {   // level 1 by rows: (1,0) + (1,2), then (1,2), then (1,1) + (1,2)
       pass_geometry(a, s, 2);   // a.s = 1 (the row kernels read only the extents and the constants)
-      const uint64_t odd_rows = a.n[0] * (a.n[1] / 2), even_rows = a.n[0] * ((a.n[1] + 1) / 2);
-      if (odd_rows) {
-        const unsigned g = (unsigned)std::min<uint64_t>((odd_rows + IR_WARPS - 1) / IR_WARPS, 1u << 20);
-        k_interp_rows<T, DEC, true><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
-        nl++;
-      }
-      if (a.n[2] > 1) {
-        const unsigned g = (unsigned)std::min<uint64_t>((even_rows + IR_WARPS - 1) / IR_WARPS, 1u << 20);
-        k_interp_rows<T, DEC, false><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+      const uint64_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2];
+      const uint64_t rows[3] = {((n0 + 1) / 2) * ((n1 + 1) / 2), n0 * (n1 / 2), (n0 / 2) * ((n1 + 1) / 2)};
+      const bool run[3] = {n2 > 1, n1 > 1, n0 > 1};
+      for (int kind : {2, 0, 1}) {
+        if (!rows[kind] || !run[kind]) continue;
+        const unsigned g = (unsigned)std::min<uint64_t>((rows[kind] + IR_WARPS - 1) / IR_WARPS, 1u << 20);
+        if (kind == 2) k_interp_rows<T, DEC, 2><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        else if (kind == 0) k_interp_rows<T, DEC, 0><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
+        else k_interp_rows<T, DEC, 1><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
         nl++;
       }
       break;

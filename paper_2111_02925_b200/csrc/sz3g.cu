@@ -966,7 +966,23 @@ __global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ 
   if ((reinterpret_cast<uintptr_t>(codes) & 15) == 0) {
     const uint4* cv = reinterpret_cast<const uint4*>(codes);
     const uint64_t nv = n / 8;
-    for (uint64_t v = tid; v < nv; v += nth) {
+    uint64_t v = tid;
+    // four 16-byte loads in flight per thread (one per iteration left the SMs short of bytes in flight)
+    for (; v + 3 * nth < nv; v += 4 * nth) {
+      uint4 q[4];
+#pragma unroll
+      for (int r = 0; r < 4; r++) q[r] = __ldcs(cv + v + r * nth);
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const uint32_t w4[4] = {q[r].x, q[r].y, q[r].z, q[r].w};
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          add(w4[u] & 0xffffu);
+          add(w4[u] >> 16);
+        }
+      }
+    }
+    for (; v < nv; v += nth) {
       const uint4 q = __ldcs(cv + v);
       const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
