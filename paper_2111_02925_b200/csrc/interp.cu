@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) k_interp_pairs(const T* __restrict__ x, T
 // (launch 2) run apart, so no launch reads a sector another warp of it stores.  The prediction and
 // quantisation are k_interp_pass's, op for op: bit-identical to the per-pass schedule.
 #ifndef SZ3G_IP_ROWS
-#define SZ3G_IP_ROWS 1
+#define SZ3G_IP_ROWS 2   // 1: level 1 by rows, coarser levels by k_interp_pass; 2: every level by rows
 #endif
 constexpr int IR_WARPS = 8;
 #ifndef SZ3G_IR_MINB
@@ -317,14 +317,16 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
   SZ3G_SYNCTHREADS();
   if (!s_ok) return;
   const Consts K = s_k;
-  const uint64_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2];
+  const uint64_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], S = a.s;
+  // the level's sub-grid (the multiples of s): coordinates ic, jc, kc; extents m0, m1, m2
+  const uint64_t m0 = (n0 - 1) / S + 1, m1 = (n1 - 1) / S + 1, m2 = (n2 - 1) / S + 1;
   const int lane = threadIdx.x & 31;
-  // rows of this launch: KIND 1 (i, j odd); KIND 2 (i odd, j even); KIND 0 (i even, j even)
-  const uint64_t nj = KIND == 1 ? n1 / 2 : (n1 + 1) / 2;
-  const uint64_t ni = KIND == 1 ? n0 : (KIND == 2 ? n0 / 2 : (n0 + 1) / 2);
+  // rows of this launch: KIND 1 (ic, jc odd); KIND 2 (ic odd, jc even); KIND 0 (ic even, jc even)
+  const uint64_t nj = KIND == 1 ? m1 / 2 : (m1 + 1) / 2;
+  const uint64_t ni = KIND == 1 ? m0 : (KIND == 2 ? m0 / 2 : (m0 + 1) / 2);
   const uint64_t nrows = ni * nj;
-  const uint64_t nseg = (n2 + 63) / 64;
-  const bool p12 = n2 > 1;                            // pass (1,2) has targets
+  const uint64_t nseg = (m2 + 63) / 64;
+  const bool p12 = m2 > 1;                            // pass (s,2) has targets
   const bool base_al = (reinterpret_cast<uintptr_t>(xp) % (2 * sizeof(T))) == 0 &&
                        (reinterpret_cast<uintptr_t>(codes) % 4) == 0;
   // the loads of one segment (issued one segment before their use): the even column's inputs -- its
@@ -337,20 +339,21 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
   for (uint64_t r = (uint64_t)blockIdx.x * IR_WARPS + (threadIdx.x >> 5); r < nrows;
        r += (uint64_t)gridDim.x * IR_WARPS) {
     const uint64_t ti = r / nj;
-    const uint64_t i = KIND == 1 ? ti : 2 * ti + (KIND == 2 ? 1 : 0), j = 2 * (r - ti * nj) + (KIND == 1 ? 1 : 0);
-    const uint64_t re = (i * n1 + j) * n2;
-    const bool vec = (re & 1) == 0 && base_al;        // pairs 2 sizeof(T)-byte / 4-byte (codes) aligned
-    // the even column's pass: (1,1) along j (KIND 1) or (1,0) along i (KIND 2), cubic / linear / copy
+    const uint64_t ic = KIND == 1 ? ti : 2 * ti + (KIND == 2 ? 1 : 0), jc = 2 * (r - ti * nj) + (KIND == 1 ? 1 : 0);
+    const uint64_t re = (ic * S * n1 + jc * S) * n2;
+    const bool vec = S == 1 && (re & 1) == 0 && base_al;   // pairs 2 sizeof(T)-byte / 4-byte (codes) aligned
+    // the even column's pass: (s,1) along j (KIND 1) or (s,0) along i (KIND 2), cubic / linear / copy
+    // (the I3 conditions i_d >= 3s, i_d + 3s < n_d, i_d + s < n_d on the sub-grid: c >= 3, c + 3 < m, c + 1 < m)
     constexpr bool COMP = KIND != 0;
-    const uint64_t sd = KIND == 1 ? n2 : n1 * n2, id = KIND == 1 ? j : i, nd = KIND == 1 ? n1 : n0;
+    const uint64_t sd = S * (KIND == 1 ? n2 : n1 * n2), id = KIND == 1 ? jc : ic, nd = KIND == 1 ? m1 : m0;
     const int mj = (id >= 3 && id + 3 < nd) ? 2 : (id + 1 < nd ? 1 : 0);
     auto load = [&](uint64_t sg) {
       Ld L;
       L.b = L.c = L.av = L.ev = L.xe = L.xo = T(0);
       L.ce = L.co = 0;
-      const uint64_t ke = 64 * sg + 2 * lane;
-      if (ke >= n2) return L;
-      const uint64_t e = re + ke;
+      const uint64_t kc = 64 * sg + 2 * lane;
+      if (kc >= m2) return L;
+      const uint64_t e = re + kc * S;
       if (COMP) {
         L.b = xp[e - sd];
         if (mj >= 1) L.c = xp[e + sd];
@@ -364,22 +367,22 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
         L.xe = xp[e];
         if (!DEC) L.ce = codes[e];
       }
-      if (p12 && ke + 1 < n2) {
-        if (DEC) L.co = codes[e + 1];
-        else L.xo = x[e + 1];
+      if (p12 && kc + 1 < m2) {
+        if (DEC) L.co = codes[e + S];
+        else L.xo = x[e + S];
       }
       return L;
     };
     // the even column's x' and code from its loads (KIND 1 / 2: passes (1,1) / (1,0); KIND 0: as loaded)
     auto even_col = [&](uint64_t sg, const Ld& L, T& xe, uint16_t& ce, bool& out) {
-      const uint64_t ke = 64 * sg + 2 * lane;
+      const uint64_t kc = 64 * sg + 2 * lane;
       out = false;
       xe = L.xe;
       ce = L.ce;
-      if (!COMP || ke >= n2) return;
+      if (!COMP || kc >= m2) return;
       const double p = ip_predict(to_d<T>(L.av), to_d<T>(L.b), to_d<T>(L.c), to_d<T>(L.ev), mj);
       if (DEC) {
-        xe = L.ce != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)L.ce - (int)a.R)))) : xp[re + ke];
+        xe = L.ce != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)L.ce - (int)a.R)))) : xp[re + kc * S];
       } else {
         out = !ip_quant<T>(L.xe, p, K, a.R, ce, xe);
       }
@@ -392,7 +395,7 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
     for (uint64_t sg = 0; sg < nseg; sg++) {
       const Ld l_nn = load(sg + 2);
       even_col(sg + 1, l_nxt, xe_nxt, ce_nxt, out_nxt);
-      const uint64_t ke = 64 * sg + 2 * lane, ko = ke + 1;
+      const uint64_t kc = 64 * sg + 2 * lane, ke = kc * S, ko = ke + S;
       // (1,2) donors of ko: ke - 2, ke, ke + 2, ke + 4 (lanes l - 1, l, l + 1, l + 2 or the next segment);
       // every lane takes part in every shuffle
       const T dn1 = __shfl_up_sync(0xffffffffu, xe_cur, 1);
@@ -405,9 +408,9 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
       T xo = T(0);
       uint16_t co = 0;
       bool out_o = false;
-      const bool has_o = p12 && ko < n2;
+      const bool has_o = p12 && kc + 1 < m2;
       if (has_o) {
-        const int mk = (ko >= 3 && ko + 3 < n2) ? 2 : (ko + 1 < n2 ? 1 : 0);
+        const int mk = (kc + 1 >= 3 && kc + 4 < m2) ? 2 : (kc + 2 < m2 ? 1 : 0);
         const double p = ip_predict(to_d<T>(dm2), to_d<T>(xe_cur), to_d<T>(dp2), to_d<T>(dp4), mk);
         if (DEC) {
           xo = l_cur.co != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)l_cur.co - (int)a.R))))
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
         }
       }
       // the row's pair back, whole
-      if (ke < n2) {
+      if (kc < m2) {
         const uint64_t e = re + ke;
         if (has_o && vec) {
           if (sizeof(T) == 4) {
@@ -433,11 +436,13 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
           }
           if (!DEC) *reinterpret_cast<uint32_t*>(codes + e) = (uint32_t)ce_cur | ((uint32_t)co << 16);
         } else {
-          xp[e] = xe_cur;
-          if (!DEC) codes[e] = ce_cur;
+          if (COMP || S == 1) {   // KIND 0 at s > 1: the even column is unchanged and no sector is whole anyway
+            xp[e] = xe_cur;
+            if (!DEC) codes[e] = ce_cur;
+          }
           if (has_o) {
-            xp[e + 1] = xo;
-            if (!DEC) codes[e + 1] = co;
+            xp[e + S] = xo;
+            if (!DEC) codes[e + S] = co;
           }
         }
       }
@@ -746,11 +751,12 @@ int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* 
       nl++;
       break;
     }
-    if (s == 1 && SZ3G_IP_ROWS) {   // level 1 by rows: (1,0) + (1,2), then (1,2), then (1,1) + (1,2)
-      pass_geometry(a, s, 2);   // a.s = 1 (the row kernels read only the extents and the constants)
-      const uint64_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2];
-      const uint64_t rows[3] = {((n0 + 1) / 2) * ((n1 + 1) / 2), n0 * (n1 / 2), (n0 / 2) * ((n1 + 1) / 2)};
-      const bool run[3] = {n2 > 1, n1 > 1, n0 > 1};
+    if (SZ3G_IP_ROWS && (s == 1 || SZ3G_IP_ROWS > 1)) {
+      // level s by rows of its sub-grid: (s,0) + (s,2), then (s,2), then (s,1) + (s,2)
+      pass_geometry(a, s, 2);   // a.s = s (the row kernels read the extents, s and the constants)
+      const uint64_t m0 = (a.n[0] - 1) / s + 1, m1 = (a.n[1] - 1) / s + 1, m2 = (a.n[2] - 1) / s + 1;
+      const uint64_t rows[3] = {((m0 + 1) / 2) * ((m1 + 1) / 2), m0 * (m1 / 2), (m0 / 2) * ((m1 + 1) / 2)};
+      const bool run[3] = {m2 > 1, m1 > 1, m0 > 1};
       for (int kind : {2, 0, 1}) {
         if (!rows[kind] || !run[kind]) continue;
         const unsigned g = (unsigned)std::min<uint64_t>((rows[kind] + IR_WARPS - 1) / IR_WARPS, 1u << 20);
@@ -759,7 +765,8 @@ int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* 
         else k_interp_rows<T, DEC, 1><<<g, IR_WARPS * 32, 0, st>>>(x, xp, codes, oidx, oval, ocount, a);
         nl++;
       }
-      break;
+      if (s == 1) break;
+      continue;
     }
     if (s == 1 && SZ3G_IP_PAIRS && (DEC || SZ3G_IP_PAIRS > 1)) {   // level 1: pair kernels (full-sector stores)
       const uint64_t np = (a.n[2] + 1) / 2;
