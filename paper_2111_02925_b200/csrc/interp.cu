@@ -7,9 +7,11 @@
 // already RECONSTRUCTED, so passes run in plan order, one launch each, while the targets of one pass are
 // independent of one another (their donors are even multiples of s along d) and run fully in parallel:
 //   k_interp_anchor   the anchor (0,0,0) stored as an outlier; eb_abs / status; x'[0] = x[0]
-//   k_interp_pass<T, DEC>  one thread per target of pass (s, d): donors from x' at -3s, -s, +s, +3s along
-//                     d, cubic / linear / copy (I3), then O8-O10 (compress: code, x', outlier append
-//                     warp-aggregated) or the recovery (decompress: x' for code != 0)
+//   k_interp_rows<T, DEC, KIND>  the default: level s by rows of its sub-grid (three launches per level,
+//                     one warp per row; see the comment above the kernel)
+//   k_interp_pass<T, DEC>  (-DSZ3G_IP_ROWS=0) one thread per target of pass (s, d): donors from x' at -3s, -s,
+//                     +s, +3s along d, cubic / linear / copy (I3), then O8-O10 (compress: code, x', outlier
+//                     append warp-aggregated) or the recovery (decompress: x' for code != 0)
 //   k_interp_scatter  decompress: outlier values into x' before the passes
 //   k_interp_final    outlier-capacity status
 // The histogram (O11) is the standalone sz3g_histogram over the finished codes.  Arithmetic is the
@@ -251,16 +253,20 @@ __global__ void __launch_bounds__(256) k_interp_pairs(const T* __restrict__ x, T
 }
 
 // ------------------------------------------------------------------------------------------------
-// Level s = 1, passes (1,1) and (1,2) by rows (SZ3G_IP_ROWS, the default).  Both passes stay inside one
-// plane i, and pass (1,2) inside one row (i, j): a row j odd holds the targets of (1,1) at even k (donors:
-// the even rows j -+ 1, j -+ 3 at the same k, final after pass (1,0)) and of (1,2) at odd k (donors: the
-// row's own even k, just computed), a row j even only those of (1,2).  One warp per row, lane l on the
-// column pair (k0 + 2l, k0 + 2l + 1) of a 64-column segment; the (1,2) donors of a segment reach two
-// even columns into the next segment, so the even columns are computed (or, even rows, loaded) one
-// segment ahead.  Every row leaves whole -- x' and codes as pairs, the even column's value and code
-// rewritten unchanged on even rows -- so no store is a partial sector; odd rows (launch 1) and even rows
-// (launch 2) run apart, so no launch reads a sector another warp of it stores.  The prediction and
-// quantisation are k_interp_pass's, op for op: bit-identical to the per-pass schedule.
+// Level s by rows of its sub-grid (the multiples of s; coordinates ic, jc, kc).  Pass (s,2) stays inside a
+// row (i, j), passes (s,0) and (s,1) touch only even columns: a row with jc odd (KIND 1) holds the (s,1)
+// targets at its even columns (donors: the rows jc -+ 1, -+ 3, final once KIND 2 has run) and the (s,2)
+// targets at its odd columns (donors: the row's own even columns, just computed); a row with ic odd and
+// jc even (KIND 2) the (s,0) targets at its even columns (donors: planes ic -+ 1, -+ 3, coarser levels)
+// and (s,2); a row with ic, jc even (KIND 0) only (s,2).  Launched KIND 2, 0, 1: the plan order (s,0),
+// (s,1), (s,2) up to targets that do not depend on one another.  One warp per row, lane l on the column
+// pair (kc0 + 2l, kc0 + 2l + 1) of a 64-column segment; the (s,2) donors of a segment reach two even
+// columns into the next segment, so the even columns are computed (or loaded) one segment ahead, and
+// every load is issued one segment before its use.  At s = 1 every row leaves whole -- x' and codes as
+// pairs, the even column's value and code rewritten unchanged on KIND 0 rows -- so no store is a
+// partial sector; the three kinds run as separate launches, so no launch reads a sector another warp of
+// it stores.  The prediction and quantisation are k_interp_pass's, op for op: bit-identical to the
+// per-pass schedule.
 #ifndef SZ3G_IP_ROWS
 #define SZ3G_IP_ROWS 2   // 1: level 1 by rows, coarser levels by k_interp_pass; 2: every level by rows
 #endif
