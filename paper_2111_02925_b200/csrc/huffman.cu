@@ -16,12 +16,15 @@
 //                     the chunk (first / last word by atomicOr), the image is copied out coalesced.
 //   k_huff_decode     one thread per chunk: 64-bit bit window, 12-bit LUT in shared memory,
 //                     canonical search for longer codes, 8 codes per 16-byte store.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
 
 #include "../../include/sz3g.h"
 #include "ptx.cuh"
@@ -1050,6 +1053,9 @@ constexpr int DF_WARPS = 8, DF_ROUND = 32, DF_RING = 16, DF_RING_W = 20;   // ri
 #ifndef SZ3G_DF_DIRECT
 #define SZ3G_DF_DIRECT 0   // 1: a round's codes leave with the lane's own 16-byte stores (no staging)
 #endif
+#ifndef SZ3G_DF_TMA
+#define SZ3G_DF_TMA 1      // a round's codes leave by one 2D TMA store per warp (else staged 16-byte stores)
+#endif
 #ifndef SZ3G_DF_MINB
 #define SZ3G_DF_MINB 4     // __launch_bounds__ minimum blocks per SM: 4 x 8 warps (smem allows 4)
 #endif
@@ -1057,6 +1063,10 @@ constexpr int DF_WARPS = 8, DF_ROUND = 32, DF_RING = 16, DF_RING_W = 20;   // ri
 #ifndef SZ3G_DF_PREF
 #define SZ3G_DF_PREF 1   // the window's next ring word loaded one refill ahead, by the taking lanes only
 #endif
+__host__ __device__ constexpr size_t df_smem_core_bytes() {   // LUT, per-length tables, rings
+  return 4ull * ((1 << HF_LUT_BITS) + 3 * HF_MAXL) + 4ull * DF_WARPS * 32 * DF_RING_W;
+}
+
 struct DfLane {
   uint32_t hi, lo;  // left-aligned 64-bit bit window (hi = its upper 32 bits)
   uint32_t avail;   // valid bits in the window
@@ -1148,14 +1158,21 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
                                                                     const uint64_t* __restrict__ offs, uint64_t nch,
                                                                     uint64_t nfull, const DTab* __restrict__ dt,
                                                                     uint32_t max_len, uint16_t* __restrict__ codes,
-                                                                    int32_t* status) {
+                                                                    int32_t* status,
+                                                                    const __grid_constant__ CUtensorMap tm_out,
+                                                                    int tma_out) {
   extern __shared__ __align__(16) uint32_t dsm[];
+  // tma_out: a round's codes leave by one TMA store of a {32 codes, 32 chunks} box per warp, staged in a
+  // 2 KB buffer per warp laid out as the map's 64-byte swizzle (1024-byte aligned: the XOR pattern
+  // follows the address bits)
+  uint4* s_tma = reinterpret_cast<uint4*>(
+      (reinterpret_cast<uintptr_t>(dsm) + df_smem_core_bytes() + 1023) & ~uintptr_t(1023));
   uint32_t* s_lut = dsm;                                  // 4096
   uint32_t* s_first = s_lut + (1 << HF_LUT_BITS);         // 32
   uint32_t* s_base = s_first + HF_MAXL;
   uint32_t* s_ljl = s_base + HF_MAXL;
   uint32_t* s_rings = s_ljl + HF_MAXL;                    // [DF_WARPS * 32][DF_RING_W]
-  uint4* s_out = reinterpret_cast<uint4*>(s_rings + DF_WARPS * 32 * DF_RING_W);   // [DF_WARPS][128] uint4
+  uint4* s_out = s_tma;                                   // [DF_WARPS][128] uint4 (staging, both store paths)
   for (int i = threadIdx.x; i < (1 << HF_LUT_BITS); i += blockDim.x) s_lut[i] = dt->lut[i];
   if (threadIdx.x < HF_MAXL) {
     const uint32_t l = threadIdx.x;
@@ -1220,6 +1237,21 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
       }
       continue;
     }
+    if (tma_out) {
+      uint4* tb = s_tma + wl * 128;   // row r = lane (chunk c0 + r): 64 bytes, 16-byte unit j at j ^ ((r >> 1) & 3)
+      if (lane == 0) sz3g::ptx::bulk_wait_read0();   // the previous round's store has read the buffer
+      SZ3G_SYNCWARP();
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        tb[4 * lane + (j ^ ((lane >> 1) & 3))] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+      sz3g::ptx::fence_proxy_async_smem();
+      SZ3G_SYNCWARP();
+      if (lane == 0) {
+        sz3g::ptx::tma_store_2d(&tm_out, tb, (int)e, (int)c0);
+        sz3g::ptx::bulk_commit();
+      }
+      continue;
+    }
     // stage: lane l's 4 uint4 at slots 4 l + j, swizzled (conflict-free both ways)
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -1236,14 +1268,12 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
     SZ3G_SYNCWARP();
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (tma_out && lane == 0) sz3g::ptx::bulk_wait0();
   const uint64_t consumed = 32ull * d.nref - d.avail;
   if (live && (bad || consumed > nwc * 32)) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
 }
 
-size_t df_smem_bytes() {
-  return 4ull * ((1 << HF_LUT_BITS) + 3 * HF_MAXL) + 4ull * DF_WARPS * 32 * DF_RING_W +
-         (SZ3G_DF_DIRECT ? 0ull : 16ull * 128 * DF_WARPS);
-}
+size_t df_smem_bytes() { return df_smem_core_bytes() + (SZ3G_DF_DIRECT ? 0ull : 16ull * 128 * DF_WARPS + 1024); }
 
 
 std::atomic<uint64_t> g_hf_launches{0};
@@ -1253,6 +1283,31 @@ int hf_check(int nl) {
   if (e != cudaSuccess) return SZ3G_ECUDA;
   g_hf_launches.fetch_add((uint64_t)nl, std::memory_order_relaxed);
   return SZ3G_OK;
+}
+
+// the decoder's output as a 2D map: rows = full chunks (2048 codes, 4096 bytes), box {32 codes, 32 chunks},
+// 64-byte swizzle (the staging layout of k_huff_decode_full), no L2 promotion (stores)
+typedef CUresult (*HfEncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool df_out_map(CUtensorMap* m, uint16_t* codes, uint64_t nfull) {
+  static HfEncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<HfEncodeTiledFn>(p);
+  });
+  if (!fn || nfull == 0 || nfull >= (1ull << 31)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)EW_CHUNK, nfull};
+  const cuuint64_t strides[1] = {(cuuint64_t)EW_CHUNK * 2};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 int sm_count_hf() {
@@ -1383,8 +1438,11 @@ int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, 
         cudaSuccess)
       return hf_check(nl);
     const uint64_t per_cta = 32ull * DF_WARPS;
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    const int tma = SZ3G_DF_TMA && !SZ3G_DF_DIRECT && df_out_map(&tm, codes, nfull) ? 1 : 0;
     k_huff_decode_full<<<(unsigned)((nfull + per_cta - 1) / per_cta), DF_WARPS * 32, smem, st>>>(
-        payload, chunk_offsets, nch, nfull, reinterpret_cast<const DTab*>(dtable), max_len, codes, d_status);
+        payload, chunk_offsets, nch, nfull, reinterpret_cast<const DTab*>(dtable), max_len, codes, d_status, tm, tma);
     nl++;
   }
   if (nch > nfull) {
