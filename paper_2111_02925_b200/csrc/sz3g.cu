@@ -1120,7 +1120,7 @@ EncodeTiledFn encode_fn() {
 // promotion: with 256-B promotion a 384-B (or 192-B) row covers 1.5 promoted blocks and L2 fills the
 // unwritten half from DRAM (ncu: DRAM reads = 1/3 of the bytes written).
 bool make_map(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, const Geo& g, int box_j = BS,
-              bool store = false) {
+              bool store = false, bool no_promo = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[3] = {g.n2, g.n1, g.n0};
@@ -1129,7 +1129,7 @@ bool make_map(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* 
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_NONE,
-                  store ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  (store || no_promo) ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -1473,13 +1473,16 @@ int launch_lr_tma(const Geo& g, const void* x, const KArgs& ka, const CompressOu
 #endif
 constexpr int LDW = SZ3G_LRD_W, LDD = SZ3G_LRD_D;   // LR decompress: self-fed warps x code-tile stages
 
+#ifndef SZ3G_LRD_NOPROMO
+#define SZ3G_LRD_NOPROMO 1   // the SZ3-LR decompressor's code-tile map without L2 256-byte promotion (c5: DRAM reads 12.69 -> 11.20 GB, 6.47 -> 6.39 ms)
+#endif
 template <typename T, int W, int D>
 int launch_lr_dec_tma(const Geo& g, const uint16_t* codes, const int32_t* coef, const uint8_t* flags, void* xo,
                       const KArgs& ka, cudaStream_t st) {
   using L = LrDecSmem<W, D>;
   static_assert(L::total <= 232448, "smem");
   CUtensorMap mc;
-  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g)) return SZ3G_ECUDA;
+  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g, BS, false, SZ3G_LRD_NOPROMO != 0)) return SZ3G_ECUDA;
   auto kern = k_lr_decompress_tma<T, W, D>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
