@@ -486,7 +486,7 @@ __device__ __forceinline__ void coef_warp_tile(const double* __restrict__ bstage
 // NOR0 mode: the quantise warp turns the staged beta of its lanes' blocks into the decoded coefficients
 // and fast-path constants itself (the same block_codes / fast32_consts as the role-0 warp); warp q == 0
 // writes the coefficient codes
-template <typename T, bool HIST, bool FULL, int P>
+template <typename T, bool HIST, bool FULL, int P, bool ROW = false>
 __device__ __forceinline__ void quant_warp_tile_beta(const T* __restrict__ xs, const double* __restrict__ bstage,
                                                      uint16_t* slab, int j0, bool write_codes, const TileCoord tc,
                                                      const Geo& g, const Consts& K, uint32_t R,
@@ -505,7 +505,7 @@ __device__ __forceinline__ void quant_warp_tile_beta(const T* __restrict__ xs, c
   const Fast32 F = fast32_consts(bh, K);
   const bool has_out =
       quantize_rows<T, true, HIST, FULL, P, true>(xs, BS * TK, TK, slab, 0, 0, j0, L, bh, F, K, R, hs, o.hist);
-  rare_path<T, HIST, P>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, has_out, tc, g, o, hs);
+  rare_path<T, HIST, P, ROW>(xs, BS * TK, TK, slab, P * TK, TK, j0, j0, L, has_out, tc, g, o, hs);
 }
 
 // NOR0 with SZ3G_QDERIV1: only the group's first quantise warp turns the staged beta into coefficient codes,
@@ -578,7 +578,7 @@ __device__ __forceinline__ void quant_warp_tile(const T* __restrict__ xs, const 
 #define SZ3G_QWAIT 1   // quantise warps' wait for a full stage: 0 = try_wait + nanosleep(64) polling,
                        // 1 = hardware-suspended try_wait (no polling instructions: less issue, less power)
 #endif
-template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF, int HW, bool NOR0>
+template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF, int HW, bool NOR0, bool ROW = false>
 __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0>::WARPS * 32, 1)
     k_compress_tma(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_c, int codes_tma,
                    KArgs a, CompressOut<T> o) {
@@ -770,9 +770,9 @@ __global__ void __launch_bounds__(CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0
               quant_warp_tile_shared<T, HIST, false, P>(xs, bst, &slots[s], slab, j0, q == 0, grp, 32 * Q, tc, g, K,
                                                         a.R, o, hs);
           } else if (tfull) {
-            quant_warp_tile_beta<T, HIST, true, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+            quant_warp_tile_beta<T, HIST, true, P, ROW>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
           } else {
-            quant_warp_tile_beta<T, HIST, false, P>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
+            quant_warp_tile_beta<T, HIST, false, P, ROW>(xs, bst, slab, j0, q == 0, tc, g, K, a.R, o, hs);
           }
         } else {
           if (tfull) quant_warp_tile<T, HIST, true, P>(xs, &slots[s], slab, j0, tc, g, K, a.R, o, hs);
@@ -1271,7 +1271,12 @@ constexpr int AW32 = SZ3G_AW, AD32 = SZ3G_AD;   // f32 analyze: 12 self-fed warp
 #endif
 constexpr int AW64 = SZ3G_AW64, AD64 = SZ3G_AD64;   // f64 analyze: 7 self-fed warps x 1 stage of 27 KiB (A/B on c4: 71.7 vs 75.8 us for 4 x 2)
 
-template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN, bool NOR0 = false>
+// radius at or below which the two-pass quantiser writes its outlier list row piece by row piece
+// (c5 at R = 16, 38.6% outliers: decompress 31.7 -> 17.3 ms, quantise 21.1 -> 19.3 ms)
+constexpr uint32_t ROW_RADIUS = 1024;
+
+template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN, bool NOR0 = false,
+          bool ROW = false>
 int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes_tma, const KArgs& ka,
                         const CompressOut<T>& co, cudaStream_t st) {
   using L = CompressSmem<T, NG, Q, D, BETA, SELF, HW, NOR0>;
@@ -1281,7 +1286,7 @@ int launch_compress_tma(const Geo& g, const void* x, uint16_t* codes, bool codes
   if (!make_map(&mx, dt, sizeof(T), x, g)) return SZ3G_ECUDA;
   memset(&mc, 0, sizeof(mc));
   if (codes_tma && !make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, codes, g, L::P, true)) codes_tma = false;
-  auto kern = k_compress_tma<T, NG, Q, D, HIST, BETA, SELF, HW, NOR0>;
+  auto kern = k_compress_tma<T, NG, Q, D, HIST, BETA, SELF, HW, NOR0, ROW>;
   cudaError_t e = set_smem(kern, L::total);
   if (e != cudaSuccess) return cuda_fail(e);
   const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)sm_count());
@@ -1333,15 +1338,22 @@ int compress_launch(const Geo& g, const void* x, uint16_t* codes, bool tma, bool
                           : launch_compress_tma<T, 5, 3, 2, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
       }
       if constexpr (BETA) {   // default two-pass shape: 5 groups x 3 quantise warps, no role-0 warp (A/B best)
+        if (ka.R <= ROW_RADIUS)   // small radius: outliers are common, the row-ordered outlier list instance
+          return use_hist ? launch_compress_tma<T, 5, 3, 2, true, true, false, HWIN, true, true>(g, x, codes, codes_tma, ka, co, st)
+                          : launch_compress_tma<T, 5, 3, 2, false, true, false, HWIN, true, true>(g, x, codes, codes_tma, ka, co, st);
         return use_hist ? launch_compress_tma<T, 5, 3, 2, true, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st)
                         : launch_compress_tma<T, 5, 3, 2, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
       }
       return use_hist ? launch_compress_tma<T, CN32, CQ32, CD32, true, BETA>(g, x, codes, codes_tma, ka, co, st)
                       : launch_compress_tma<T, CN32, CQ32, CD32, false, BETA>(g, x, codes, codes_tma, ka, co, st);
     } else {
-      if constexpr (BETA && SZ3G_CNOR64 != 0)
+      if constexpr (BETA && SZ3G_CNOR64 != 0) {
+        if (ka.R <= ROW_RADIUS)
+          return use_hist ? launch_compress_tma<T, CN64, CQ64, CD64, true, true, false, HWIN, true, true>(g, x, codes, codes_tma, ka, co, st)
+                          : launch_compress_tma<T, CN64, CQ64, CD64, false, true, false, HWIN, true, true>(g, x, codes, codes_tma, ka, co, st);
         return use_hist ? launch_compress_tma<T, CN64, CQ64, CD64, true, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st)
                         : launch_compress_tma<T, CN64, CQ64, CD64, false, true, false, HWIN, true>(g, x, codes, codes_tma, ka, co, st);
+      }
       return use_hist ? launch_compress_tma<T, CN64, CQ64, CD64, true, BETA>(g, x, codes, codes_tma, ka, co, st)
                       : launch_compress_tma<T, CN64, CQ64, CD64, false, BETA>(g, x, codes, codes_tma, ka, co, st);
     }

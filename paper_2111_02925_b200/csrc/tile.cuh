@@ -569,13 +569,62 @@ __device__ __forceinline__ bool quantize_rows(const T* __restrict__ xs, uint64_t
 }
 
 // Rare path (warp-uniform entry): outliers of rows [j0, j0+PJ) -> (global index, value) with a
-// warp-aggregated append, and their count into bin 0.  The list is written row piece by row piece: for
+// warp-aggregated append, and their count into bin 0.
+template <typename T, bool HIST, int PJ>
+__device__ __forceinline__ void rare_path_lanes(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+                                          const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
+                                          int cs_j0, const LaneGeom& L, bool has_out, const TileCoord tc,
+                                          const Geo& g, const CompressOut<T>& o, const HistSmem& hs) {
+  const int lane = threadIdx.x & 31;
+  if (!__any_sync(0xffffffffu, has_out)) return;
+  const int j1 = min(j0 + PJ, L.m1);
+  uint32_t nout = 0;
+  if (has_out) {
+    for (int j = j0; j < j1; j++)
+      for (int kk = 0; kk < 3; kk++) {
+        if (!L.kv(kk)) continue;
+        for (int i = 0; i < L.m0; i++) nout += (cs[i * ci + (j - cs_j0) * cj + L.kcol + kk] == 0u) ? 1u : 0u;
+      }
+  }
+  uint32_t incl = nout;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long basepos = 0;
+  if (lane == 31) {
+    basepos = atomicAdd(o.ocount, (unsigned long long)total);
+    if (HIST) atomicAdd(hs.zero, total);
+  }
+  basepos = __shfl_sync(0xffffffffu, basepos, 31);
+  unsigned long long pos = basepos + (incl - nout);
+  if (nout) {
+    const uint64_t gbase =
+        g.gofs + ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)L.kb * BS + 3 * L.h;
+    for (int j = j0; j < j1; j++)
+      for (int kk = 0; kk < 3; kk++) {
+        if (!L.kv(kk)) continue;
+        for (int i = 0; i < L.m0; i++) {
+          if (cs[i * ci + (j - cs_j0) * cj + L.kcol + kk] != 0) continue;
+          if (pos < o.cap) {
+            o.oidx[pos] = gbase + ((uint64_t)i * g.n1 + j) * g.n2 + kk;
+            o.oval[pos] = xs[i * si + j * sj + L.kcol + kk];
+          }
+          pos++;
+        }
+      }
+  }
+}
+
+// Row-ordered rare path (ROW, the kernel instances for small radii, where outliers are common): the list is written row piece by row piece: for
 // every (j, i) the warp's outliers of that 96-column row piece take consecutive slots (ballot per column
 // of the lanes' three), so the list's stores are coalesced and the decompressor's scatter of
 // consecutive entries hits the same few sectors at once (round 1 appended each lane's outliers as one
 // run across six planes: on an outlier-heavy field the scatter wrote every sector many times apart).
 template <typename T, bool HIST, int PJ>
-__device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+__device__ __forceinline__ void rare_path_rows(const T* __restrict__ xs, uint64_t si, uint64_t sj,
                                           const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
                                           int cs_j0, const LaneGeom& L, bool has_out, const TileCoord tc,
                                           const Geo& g, const CompressOut<T>& o, const HistSmem& hs) {
@@ -617,6 +666,19 @@ __device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si,
         }
         pos += __popc(bal);
       }
+}
+
+// Rare path (warp-uniform entry): outliers of rows [j0, j0+PJ) -> (global index, value), their count into
+// bin 0.  ROW selects the row-ordered append; the default keeps each lane's outliers as one run (its
+// code does not disturb the register allocation of the hot quantise loop: the row-ordered one, in the
+// same kernel, cost the c5 quantise kernel 3% through register moves in that loop).
+template <typename T, bool HIST, int PJ, bool ROW = false>
+__device__ __forceinline__ void rare_path(const T* __restrict__ xs, uint64_t si, uint64_t sj,
+                                          const uint16_t* __restrict__ cs, uint64_t ci, uint64_t cj, int j0,
+                                          int cs_j0, const LaneGeom& L, bool has_out, const TileCoord tc,
+                                          const Geo& g, const CompressOut<T>& o, const HistSmem& hs) {
+  if (ROW) rare_path_rows<T, HIST, PJ>(xs, si, sj, cs, ci, cj, j0, cs_j0, L, has_out, tc, g, o, hs);
+  else rare_path_lanes<T, HIST, PJ>(xs, si, sj, cs, ci, cj, j0, cs_j0, L, has_out, tc, g, o, hs);
 }
 
 // One warp compresses a whole tile (plain kernel).  BETA: the block coefficients come from the
