@@ -353,42 +353,52 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
     constexpr bool COMP = KIND != 0;
     const uint64_t sd = S * (KIND == 1 ? n2 : n1 * n2), id = KIND == 1 ? jc : ic, nd = KIND == 1 ? m1 : m0;
     const int mj = (id >= 3 && id + 3 < nd) ? 2 : (id + 1 < nd ? 1 : 0);
-    auto load = [&](uint64_t sg) {
+    // row pointers and 32-bit column offsets (the host keeps n2 < 2^31): the segment loop's address
+    // arithmetic was half of its instructions with 64-bit element indices
+    const uint32_t m2u = (uint32_t)m2, S32 = (uint32_t)S;
+    const T* xr = DEC ? nullptr : x + re;
+    T* pr = xp + re;
+    uint16_t* cr = codes + re;
+    const T* pm1 = COMP ? pr - sd : pr;
+    const T* pp1 = COMP ? pr + sd : pr;
+    const T* pm3 = COMP ? pr - 3 * sd : pr;
+    const T* pp3 = COMP ? pr + 3 * sd : pr;
+    auto load = [&](uint32_t sg) {
       Ld L;
       L.b = L.c = L.av = L.ev = L.xe = L.xo = T(0);
       L.ce = L.co = 0;
-      const uint64_t kc = 64 * sg + 2 * lane;
-      if (kc >= m2) return L;
-      const uint64_t e = re + kc * S;
+      const uint32_t kc = 64u * sg + 2u * lane;
+      if (kc >= m2u) return L;
+      const uint32_t off = kc * S32;
       if (COMP) {
-        L.b = xp[e - sd];
-        if (mj >= 1) L.c = xp[e + sd];
+        L.b = pm1[off];
+        if (mj >= 1) L.c = pp1[off];
         if (mj == 2) {
-          L.av = xp[e - 3 * sd];
-          L.ev = xp[e + 3 * sd];
+          L.av = pm3[off];
+          L.ev = pp3[off];
         }
-        if (DEC) L.ce = codes[e];
-        else L.xe = x[e];
+        if (DEC) L.ce = cr[off];
+        else L.xe = xr[off];
       } else {
-        L.xe = xp[e];
-        if (!DEC) L.ce = codes[e];
+        L.xe = pr[off];
+        if (!DEC) L.ce = cr[off];
       }
-      if (p12 && kc + 1 < m2) {
-        if (DEC) L.co = codes[e + S];
-        else L.xo = x[e + S];
+      if (p12 && kc + 1 < m2u) {
+        if (DEC) L.co = cr[off + S32];
+        else L.xo = xr[off + S32];
       }
       return L;
     };
-    // the even column's x' and code from its loads (KIND 1 / 2: passes (1,1) / (1,0); KIND 0: as loaded)
-    auto even_col = [&](uint64_t sg, const Ld& L, T& xe, uint16_t& ce, bool& out) {
-      const uint64_t kc = 64 * sg + 2 * lane;
+    // the even column's x' and code from its loads (KIND 1 / 2: passes (s,1) / (s,0); KIND 0: as loaded)
+    auto even_col = [&](uint32_t sg, const Ld& L, T& xe, uint16_t& ce, bool& out) {
+      const uint32_t kc = 64u * sg + 2u * lane;
       out = false;
       xe = L.xe;
       ce = L.ce;
-      if (!COMP || kc >= m2) return;
+      if (!COMP || kc >= m2u) return;
       const double p = ip_predict(to_d<T>(L.av), to_d<T>(L.b), to_d<T>(L.c), to_d<T>(L.ev), mj);
       if (DEC) {
-        xe = L.ce != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)L.ce - (int)a.R)))) : xp[re + kc * S];
+        xe = L.ce != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)L.ce - (int)a.R)))) : pr[kc * S32];
       } else {
         out = !ip_quant<T>(L.xe, p, K, a.R, ce, xe);
       }
@@ -398,12 +408,13 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
     uint16_t ce_cur, ce_nxt;
     bool out_cur, out_nxt;
     even_col(0, l_cur, xe_cur, ce_cur, out_cur);
-    for (uint64_t sg = 0; sg < nseg; sg++) {
+    const uint32_t nseg32 = (uint32_t)nseg;
+    for (uint32_t sg = 0; sg < nseg32; sg++) {
       const Ld l_nn = load(sg + 2);
       even_col(sg + 1, l_nxt, xe_nxt, ce_nxt, out_nxt);
-      const uint64_t kc = 64 * sg + 2 * lane, ke = kc * S, ko = ke + S;
-      // (1,2) donors of ko: ke - 2, ke, ke + 2, ke + 4 (lanes l - 1, l, l + 1, l + 2 or the next segment);
-      // every lane takes part in every shuffle
+      const uint32_t kc = 64u * sg + 2u * lane, ke = kc * S32, ko = ke + S32;
+      // (s,2) donors of ko: ke - 2s, ke, ke + 2s, ke + 4s (lanes l - 1, l, l + 1, l + 2 or the next
+      // segment); every lane takes part in every shuffle
       const T dn1 = __shfl_up_sync(0xffffffffu, xe_cur, 1);
       const T up1 = __shfl_down_sync(0xffffffffu, xe_cur, 1), nx0 = __shfl_sync(0xffffffffu, xe_nxt, 0);
       const T up2 = __shfl_down_sync(0xffffffffu, xe_cur, 2), nx1 = __shfl_sync(0xffffffffu, xe_nxt, 1);
@@ -414,41 +425,40 @@ __global__ void __launch_bounds__(IR_WARPS * 32, SZ3G_IR_MINB) k_interp_rows(con
       T xo = T(0);
       uint16_t co = 0;
       bool out_o = false;
-      const bool has_o = p12 && kc + 1 < m2;
+      const bool has_o = p12 && kc + 1 < m2u;
       if (has_o) {
-        const int mk = (kc + 1 >= 3 && kc + 4 < m2) ? 2 : (kc + 2 < m2 ? 1 : 0);
+        const int mk = (kc + 1 >= 3 && kc + 4 < m2u) ? 2 : (kc + 2 < m2u ? 1 : 0);
         const double p = ip_predict(to_d<T>(dm2), to_d<T>(xe_cur), to_d<T>(dp2), to_d<T>(dp4), mk);
         if (DEC) {
           xo = l_cur.co != 0 ? from_d<T>(__dadd_rn(p, __dmul_rn(K.twoeb, (double)((int)l_cur.co - (int)a.R))))
-                             : xp[re + ko];
+                             : pr[ko];
         } else {
           out_o = !ip_quant<T>(l_cur.xo, p, K, a.R, co, xo);
         }
       }
       // the row's pair back, whole
-      if (kc < m2) {
-        const uint64_t e = re + ke;
+      if (kc < m2u) {
         if (has_o && vec) {
           if (sizeof(T) == 4) {
             float2 v;
             v.x = (float)xe_cur;
             v.y = (float)xo;
-            *reinterpret_cast<float2*>(xp + e) = v;
+            *reinterpret_cast<float2*>(pr + ke) = v;
           } else {
             double2 v;
             v.x = (double)xe_cur;
             v.y = (double)xo;
-            *reinterpret_cast<double2*>(xp + e) = v;
+            *reinterpret_cast<double2*>(pr + ke) = v;
           }
-          if (!DEC) *reinterpret_cast<uint32_t*>(codes + e) = (uint32_t)ce_cur | ((uint32_t)co << 16);
+          if (!DEC) *reinterpret_cast<uint32_t*>(cr + ke) = (uint32_t)ce_cur | ((uint32_t)co << 16);
         } else {
           if (COMP || S == 1) {   // KIND 0 at s > 1: the even column is unchanged and no sector is whole anyway
-            xp[e] = xe_cur;
-            if (!DEC) codes[e] = ce_cur;
+            pr[ke] = xe_cur;
+            if (!DEC) cr[ke] = ce_cur;
           }
           if (has_o) {
-            xp[e + S] = xo;
-            if (!DEC) codes[e + S] = co;
+            pr[ko] = xo;
+            if (!DEC) cr[ko] = co;
           }
         }
       }
@@ -757,7 +767,7 @@ int run_passes(IpArgs a, const T* x, T* xp, uint16_t* codes, uint64_t* oidx, T* 
       nl++;
       break;
     }
-    if (SZ3G_IP_ROWS && (s == 1 || SZ3G_IP_ROWS > 1)) {
+    if (SZ3G_IP_ROWS && (s == 1 || SZ3G_IP_ROWS > 1) && a.n[2] < (1ull << 31)) {
       // level s by rows of its sub-grid: (s,0) + (s,2), then (s,2), then (s,1) + (s,2)
       pass_geometry(a, s, 2);   // a.s = s (the row kernels read the extents, s and the constants)
       const uint64_t m0 = (a.n[0] - 1) / s + 1, m1 = (a.n[1] - 1) / s + 1, m2 = (a.n[2] - 1) / s + 1;
