@@ -967,7 +967,11 @@ __global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ 
     const uint4* cv = reinterpret_cast<const uint4*>(codes);
     const uint64_t nv = n / 8;
     uint64_t v = tid;
-    // four 16-byte loads in flight per thread (one per iteration left the SMs short of bytes in flight)
+    // four 16-byte loads in flight per thread (one per iteration left the SMs short of bytes in flight).
+    // In-window codes (the bulk) go to the window by an unconditional red.shared -- the others to a
+    // per-lane sink slot -- and are counted by the branchy path only when some lane holds one
+    const uint32_t win_sh = (uint32_t)__cvta_generic_to_shared(s_win);
+    const uint32_t sink = (uint32_t)__cvta_generic_to_shared(hs.dummy) + 4u * (threadIdx.x & 31);
     for (; v + 3 * nth < nv; v += 4 * nth) {
       uint4 q[4];
 #pragma unroll
@@ -975,10 +979,21 @@ __global__ void __launch_bounds__(512) k_histogram(const uint16_t* __restrict__ 
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         const uint32_t w4[4] = {q[r].x, q[r].y, q[r].z, q[r].w};
+        bool rare = false;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          add(w4[u] & 0xffffu);
-          add(w4[u] >> 16);
+        for (int u = 0; u < 8; u++) {
+          const uint32_t c = (w4[u >> 1] >> (16 * (u & 1))) & 0xffffu;
+          const uint32_t w = c - hs.lo;
+          const bool in = w < hs.nwin && c < nb;
+          rare |= !in;
+          red_smem_add(in ? win_sh + 4u * w : sink, 1u);
+        }
+        if (__any_sync(0xffffffffu, rare)) {
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const uint32_t c = (w4[u >> 1] >> (16 * (u & 1))) & 0xffffu;
+            if (!(c - hs.lo < hs.nwin && c < nb)) add(c);
+          }
         }
       }
     }
