@@ -1049,22 +1049,25 @@ size_t dec_smem_bytes() {
 // window takes one ring word whenever it holds <= 32 bits (predicated).  A round's 32 codes stay in
 // registers and leave through a swizzled shared-memory stage with 16-byte stores (4 lanes per 64-byte
 // chunk row).
-constexpr int DF_WARPS = 8, DF_ROUND = 32, DF_RING = 16, DF_RING_W = 20;   // ring: 16 words, 80-byte row stride
+constexpr int DF_ROUND = 32, DF_RING = 16, DF_RING_W = 20;   // ring: 16 words, 80-byte row stride
 #ifndef SZ3G_DF_DIRECT
 #define SZ3G_DF_DIRECT 0   // 1: a round's codes leave with the lane's own 16-byte stores (no staging)
 #endif
 #ifndef SZ3G_DF_TMA
 #define SZ3G_DF_TMA 1      // a round's codes leave by one 2D TMA store per warp (else staged 16-byte stores)
 #endif
-#ifndef SZ3G_DF_MINB
-#define SZ3G_DF_MINB 4     // __launch_bounds__ minimum blocks per SM: 4 x 8 warps (smem allows 4)
-#endif
-
+// Two shapes (the launch picks one, sz3g_huffman_decode):
+//  * WARPS = 32, one CTA per SM, persistent (a grid of #SMs CTAs; warp wl of CTA b takes the groups of 32
+//    chunks b * 32 + wl, + 32 * gridDim.x, ...): one copy of the tables per SM, built once, and the
+//    smallest shared-memory footprint per warp (161 KB for 32 warps against 4 x 54 KB);
+//  * WARPS = 8, up to 4 CTAs per SM, one group per warp: fields with fewer groups than 32 per SM would
+//    leave SMs idle with the 32-warp CTA.
+constexpr int DF_BIG = 32, DF_SMALL = 8;
 #ifndef SZ3G_DF_PREF
 #define SZ3G_DF_PREF 1   // the window's next ring word loaded one refill ahead, by the taking lanes only
 #endif
-__host__ __device__ constexpr size_t df_smem_core_bytes() {   // LUT, per-length tables, rings
-  return 4ull * ((1 << HF_LUT_BITS) + 3 * HF_MAXL) + 4ull * DF_WARPS * 32 * DF_RING_W;
+__host__ __device__ constexpr size_t df_smem_core_bytes(int warps) {   // LUT, per-length tables, rings
+  return 4ull * ((1 << HF_LUT_BITS) + 3 * HF_MAXL) + 4ull * warps * 32 * DF_RING_W;
 }
 
 struct DfLane {
@@ -1082,11 +1085,29 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   return v;
 }
 
+#ifndef SZ3G_DF_CG
+#define SZ3G_DF_CG 1        // ring copies bypass L1 (cp.async.cg; .ca measured 5.6 against 4.6 ms on c5)
+#endif
+#ifndef SZ3G_DF_CARVE
+#define SZ3G_DF_CARVE -1    // >= 0: cudaFuncAttributePreferredSharedMemoryCarveout of the decoder (percent)
+#endif
+#ifndef SZ3G_DF_IMAD
+#define SZ3G_DF_IMAD 1
+#endif
+// shared address of the 12-bit LUT entry indexed by the window's top bits
+__device__ __forceinline__ uint32_t df_lut_addr(uint32_t hi, uint32_t k_hi, uint32_t k4, uint32_t lut_sh) {
+  if (SZ3G_DF_IMAD) return __umulhi(hi, k_hi) * k4 + lut_sh;   // (hi >> 20) * 4 + base
+  return lut_sh + ((hi >> (32 - HF_LUT_BITS)) << 2);
+}
+
 __device__ __forceinline__ void df_copy16(uint32_t s_dst, const uint32_t* __restrict__ payload, uint64_t p,
                                           uint64_t lim) {
   const uint32_t bytes = p >= lim ? 0u : (lim - p >= 4 ? 16u : (uint32_t)(4 * (lim - p)));
   const uint32_t* src = payload + (p < lim ? p : 0);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s_dst), "l"(src), "r"(bytes) : "memory");
+  if (SZ3G_DF_CG)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s_dst), "l"(src), "r"(bytes) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s_dst), "l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void df_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void df_wait2() {
@@ -1154,7 +1175,8 @@ __device__ __forceinline__ uint32_t df_code(DfLane& d, uint32_t s_lut, const uin
   return sym;
 }
 
-__global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_full(const uint32_t* __restrict__ payload,
+template <int DF_WARPS>
+__global__ void __launch_bounds__(DF_WARPS * 32, DF_WARPS == DF_BIG ? 1 : 4) k_huff_decode_full(const uint32_t* __restrict__ payload,
                                                                     const uint64_t* __restrict__ offs, uint64_t nch,
                                                                     uint64_t nfull, const DTab* __restrict__ dt,
                                                                     uint32_t max_len, uint16_t* __restrict__ codes,
@@ -1166,7 +1188,7 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
   // 2 KB buffer per warp laid out as the map's 64-byte swizzle (1024-byte aligned: the XOR pattern
   // follows the address bits)
   uint4* s_tma = reinterpret_cast<uint4*>(
-      (reinterpret_cast<uintptr_t>(dsm) + df_smem_core_bytes() + 1023) & ~uintptr_t(1023));
+      (reinterpret_cast<uintptr_t>(dsm) + df_smem_core_bytes(DF_WARPS) + 1023) & ~uintptr_t(1023));
   uint32_t* s_lut = dsm;                                  // 4096
   uint32_t* s_first = s_lut + (1 << HF_LUT_BITS);         // 32
   uint32_t* s_base = s_first + HF_MAXL;
@@ -1183,13 +1205,19 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
   }
   SZ3G_SYNCTHREADS();
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const uint64_t c0 = ((uint64_t)blockIdx.x * DF_WARPS + wl) * 32;
-  if (c0 >= nfull) return;
+  // groups of 32 chunks: persistent for the 32-warp shape, one group per warp for the 8-warp one
+  for (uint64_t grp = (uint64_t)blockIdx.x * DF_WARPS + wl; grp * 32 < nfull;
+       grp += DF_WARPS == DF_BIG ? (uint64_t)gridDim.x * DF_WARPS : nfull) {
+  const uint64_t c0 = grp * 32;
   const uint16_t* syms = reinterpret_cast<const uint16_t*>(dt + 1);
   uint4* so = s_out + wl * 128;
   const uint32_t s_ring = (uint32_t)__cvta_generic_to_shared(s_rings + threadIdx.x * DF_RING_W);
   // &s_lut[idx] = lut_sh + 4 idx; the index is the window's top 12 bits: (hi >> 20) << 2
   const uint32_t lut_sh = (uint32_t)__cvta_generic_to_shared(s_lut);
+  // 2^12 and 4 as values the compiler cannot fold (max_len >= 1 for any table that decodes), so that
+  // the address is IMAD.HI + IMAD on the FMA pipe (SZ3G_DF_IMAD) rather than shift / mask / add on the
+  // ALU pipe, which bounds this kernel
+  const uint32_t k_hi = max_len ? (1u << HF_LUT_BITS) : 0u, k4 = max_len ? 4u : 0u;
   const bool live = c0 + lane < nfull;
   const uint64_t c = live ? c0 + lane : nfull - 1;   // a dead lane decodes the last full chunk again, unstored
   const uint64_t lim = offs[nch];
@@ -1214,10 +1242,10 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
     for (int h = 0; h < 16; h++) {
       if ((h % 4 == 0) && (h || e)) df_topup<1>(d, s_ring, payload, a0, lim);
       // two codes (<= 32 bits, the window holds > 32): LUT entry (len << 16) | sym, 0 = longer than the LUT
-      const uint32_t ea = lds32(lut_sh + ((d.hi >> (32 - HF_LUT_BITS)) << 2));
+      const uint32_t ea = lds32(df_lut_addr(d.hi, k_hi, k4, lut_sh));
       const uint32_t la = ea >> 16;
       const uint32_t hi1 = __funnelshift_l(d.lo, d.hi, la);
-      const uint32_t eb = lds32(lut_sh + ((hi1 >> (32 - HF_LUT_BITS)) << 2));
+      const uint32_t eb = lds32(df_lut_addr(hi1, k_hi, k4, lut_sh));
       if (__any_sync(0xffffffffu, ea == 0u || eb == 0u)) {
         const uint32_t a = df_code(d, lut_sh, s_ljl, s_first, s_base, syms, maxl, bad);
         const uint32_t b = df_code(d, lut_sh, s_ljl, s_first, s_base, syms, maxl, bad);
@@ -1271,9 +1299,12 @@ __global__ void __launch_bounds__(DF_WARPS * 32, SZ3G_DF_MINB) k_huff_decode_ful
   if (tma_out && lane == 0) sz3g::ptx::bulk_wait0();
   const uint64_t consumed = 32ull * d.nref - d.avail;
   if (live && (bad || consumed > nwc * 32)) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
+  }
 }
 
-size_t df_smem_bytes() { return df_smem_core_bytes() + (SZ3G_DF_DIRECT ? 0ull : 16ull * 128 * DF_WARPS + 1024); }
+size_t df_smem_bytes(int warps) { return df_smem_core_bytes(warps) + (SZ3G_DF_DIRECT ? 0ull : 16ull * 128 * warps + 1024); }
+
+
 
 
 std::atomic<uint64_t> g_hf_launches{0};
@@ -1315,6 +1346,28 @@ int sm_count_hf() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return sms;
+}
+
+template <int W>
+int df_launch(const uint32_t* payload, const uint64_t* offs, uint64_t nch, uint64_t nfull, const DTab* dt,
+              uint32_t max_len, uint16_t* codes, int32_t* status, cudaStream_t st) {
+  const size_t smem = df_smem_bytes(W);
+  if (cudaFuncSetAttribute(k_huff_decode_full<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return SZ3G_ECUDA;
+  if (SZ3G_DF_CARVE >= 0 &&
+      cudaFuncSetAttribute(k_huff_decode_full<W>, cudaFuncAttributePreferredSharedMemoryCarveout, SZ3G_DF_CARVE) !=
+          cudaSuccess)
+    return SZ3G_ECUDA;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  const int tma = SZ3G_DF_TMA && !SZ3G_DF_DIRECT && df_out_map(&tm, codes, nfull) ? 1 : 0;
+  const uint64_t per_cta = 32ull * W;
+  uint64_t nblk = (nfull + per_cta - 1) / per_cta;
+  if (W == DF_BIG) nblk = std::min<uint64_t>(nblk, (uint64_t)sm_count_hf());
+  k_huff_decode_full<W><<<(unsigned)nblk, W * 32, smem, st>>>(payload, offs, nch, nfull, dt, max_len, codes, status,
+                                                             tm, tma);
+  return SZ3G_OK;
 }
 
 }  // namespace
@@ -1433,16 +1486,12 @@ int sz3g_huffman_decode(const uint32_t* payload, const uint64_t* chunk_offsets, 
   const uint64_t nfull = (chunk == EW_CHUNK && (reinterpret_cast<uintptr_t>(payload) & 15) == 0) ? n / EW_CHUNK : 0;
   int nl = 0;
   if (nfull) {
-    const size_t smem = df_smem_bytes();
-    if (cudaFuncSetAttribute(k_huff_decode_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return hf_check(nl);
-    const uint64_t per_cta = 32ull * DF_WARPS;
-    CUtensorMap tm;
-    memset(&tm, 0, sizeof(tm));
-    const int tma = SZ3G_DF_TMA && !SZ3G_DF_DIRECT && df_out_map(&tm, codes, nfull) ? 1 : 0;
-    k_huff_decode_full<<<(unsigned)((nfull + per_cta - 1) / per_cta), DF_WARPS * 32, smem, st>>>(
-        payload, chunk_offsets, nch, nfull, reinterpret_cast<const DTab*>(dtable), max_len, codes, d_status, tm, tma);
+    // the 32-warp persistent shape once every SM gets at least one group per warp
+    const bool big = (nfull + 31) / 32 >= (uint64_t)sm_count_hf() * DF_BIG;
+    const DTab* dt = reinterpret_cast<const DTab*>(dtable);
+    const int r = big ? df_launch<DF_BIG>(payload, chunk_offsets, nch, nfull, dt, max_len, codes, d_status, st)
+                      : df_launch<DF_SMALL>(payload, chunk_offsets, nch, nfull, dt, max_len, codes, d_status, st);
+    if (r != SZ3G_OK) return hf_check(nl);
     nl++;
   }
   if (nch > nfull) {
