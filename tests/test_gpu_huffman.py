@@ -205,3 +205,46 @@ def test_full_chunk_boundaries(n):
     R = 512
     q = np.clip(np.round(rng.standard_normal(n) * 20) + R, 1, 2 * R - 1).astype(np.uint16)
     round_trip(q, np.bincount(q, minlength=2 * R))
+
+
+def test_persistent_decoder_shape_large_stream():
+    """Past 32 groups of 32 full chunks per SM the decoder runs as one persistent 32-warp CTA per SM
+    (csrc/huffman.cu, k_huff_decode_full<32>); smaller streams take the 8-warp CTAs the other tests
+    cover.  A 312 M-code stream with a heavy tail (codes longer than the 12-bit LUT, slow path taken by
+    many warps), a partial last group and a ragged last chunk: codebook vs the oracle, decode(encode(q))
+    == q on the GPU, and the payload of sampled chunks (every chunk starts on a word boundary, DEFINITION
+    H4) bit-exact vs the oracle's encoding of the same chunk."""
+    s = sz()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 2048 * (sms * 32 * 32 + 1000 + 17) + 123
+    g = torch.Generator(device="cuda")
+    g.manual_seed(2111)
+    R = 32768
+    z = torch.randn(n, generator=g, device="cuda") * 6.0
+    tail = torch.rand(n, generator=g, device="cuda") < 0.01
+    z = torch.where(tail, z * 300.0, z)
+    q = (torch.round(z) + R).clamp_(1, 2 * R - 1).to(torch.int32)
+    hist = torch.bincount(q, minlength=2 * R)
+    q = q.to(torch.uint16)
+    del z, tail
+    hist_np = hist.cpu().numpy()
+    t, lens, cws = gpu_table(hist_np)
+    olens = oracle.huffman_lengths(hist_np.astype(np.int64), 16)
+    ocws = oracle.huffman_canonical(olens)
+    assert np.array_equal(lens, olens) and np.array_equal(cws, ocws)
+    assert (hist_np[olens > 12].sum() / n) > 1e-3, "the stream must exercise the long-code slow path"
+    hs = s.huffman_encode(q, t, 2048).check()
+    dec = s.huffman_decode(hs, t)
+    torch.cuda.synchronize()
+    assert int(hs.status.item()) == 0
+    assert torch.equal(dec.view(torch.int16), q.view(torch.int16)), "decode(encode(q))"
+    offs = hs.offsets.cpu().numpy().view(np.uint64)
+    nch = (n + 2047) // 2048
+    rng = np.random.default_rng(7)
+    sample = sorted(set(rng.integers(0, nch, 48).tolist()) | {0, nch - 2, nch - 1})
+    for c in sample:
+        lo, hi = c * 2048, min(n, (c + 1) * 2048)
+        qc = q[lo:hi].view(torch.int16).cpu().numpy().view(np.uint16)
+        o_offs, o_words = oracle.huffman_encode(qc, olens, ocws, 2048)
+        w = hs.payload[int(offs[c]):int(offs[c + 1])].cpu().numpy().view(np.uint32)
+        assert int(offs[c + 1] - offs[c]) == int(o_offs[-1]) and np.array_equal(w, o_words), f"chunk {c}"
