@@ -1073,10 +1073,9 @@ __host__ __device__ constexpr size_t df_smem_core_bytes(int warps) {   // LUT, p
 struct DfLane {
   uint32_t hi, lo;  // left-aligned 64-bit bit window (hi = its upper 32 bits)
   uint32_t avail;   // valid bits in the window
-  uint32_t rpos;    // next ring word to read (mod DF_RING), counted from the aligned chunk start
-  uint32_t fpos;    // ring words requested so far (16-byte copies of 4 words)
-  uint32_t nref;    // words appended to the window
-  uint32_t wn;      // SZ3G_DF_PREF: ring word rpos, loaded ahead
+  uint32_t rp4;     // 4 x (next ring word to read), counted from the aligned chunk start (ring byte = rp4 mod 64)
+  uint32_t fp4;     // 4 x (ring words requested so far; 16-byte copies of 4 words)
+  uint32_t wn;      // SZ3G_DF_PREF: ring word rp4 / 4, loaded ahead
 };
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -1100,10 +1099,12 @@ __device__ __forceinline__ uint32_t df_lut_addr(uint32_t hi, uint32_t k_hi, uint
   return lut_sh + ((hi >> (32 - HF_LUT_BITS)) << 2);
 }
 
-__device__ __forceinline__ void df_copy16(uint32_t s_dst, const uint32_t* __restrict__ payload, uint64_t p,
-                                          uint64_t lim) {
-  const uint32_t bytes = p >= lim ? 0u : (lim - p >= 4 ? 16u : (uint32_t)(4 * (lim - p)));
-  const uint32_t* src = payload + (p < lim ? p : 0);
+// 16 bytes of the lane's payload from byte fp4 of its aligned start pl (lim4 = payload bytes from pl,
+// clamped to 2^30), zero-filled past the end of the payload; 32-bit arithmetic only
+__device__ __forceinline__ void df_copy16(uint32_t s_dst, const uint8_t* __restrict__ pl, uint32_t fp4,
+                                          uint32_t lim4) {
+  const uint32_t bytes = fp4 >= lim4 ? 0u : min(16u, lim4 - fp4);
+  const uint8_t* src = pl + (fp4 < lim4 ? fp4 : 0u);
   if (SZ3G_DF_CG)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s_dst), "l"(src), "r"(bytes) : "memory");
   else
@@ -1121,13 +1122,12 @@ __device__ __forceinline__ void df_wait2() {
 // min(g + 4, 13) - 4 >= min(g, 9), and g starts at 14 (16 words, 2 of them in the primed window); the
 // words requested before the previous call reach >= g_prev - 4 >= 5 >= 4 words past the read position.
 template <int K>
-__device__ __forceinline__ void df_topup(DfLane& d, uint32_t s_ring, const uint32_t* __restrict__ payload,
-                                         uint64_t a0, uint64_t lim) {
+__device__ __forceinline__ void df_topup(DfLane& d, uint32_t s_ring, const uint8_t* __restrict__ pl, uint32_t lim4) {
 #pragma unroll
   for (int k = 0; k < K; k++) {
-    if (d.fpos + 4 <= d.rpos + DF_RING) {
-      df_copy16(s_ring + 4u * (d.fpos & (DF_RING - 1)), payload, a0 + d.fpos, lim);
-      d.fpos += 4;
+    if (d.fp4 + 16 <= d.rp4 + 4 * DF_RING) {
+      df_copy16(s_ring + (d.fp4 & (4 * DF_RING - 1)), pl, d.fp4, lim4);
+      d.fp4 += 16;
     }
   }
   df_commit();
@@ -1138,18 +1138,17 @@ __device__ __forceinline__ void df_topup(DfLane& d, uint32_t s_ring, const uint3
 // branch-free, a 32-bit shared address, clamped funnel shifts (a shift by 32 gives 0)
 __device__ __forceinline__ void df_refill(DfLane& d, uint32_t s_ring) {
   const bool take = d.avail <= 32u;
-  const uint32_t w = SZ3G_DF_PREF ? d.wn : lds32(s_ring + 4u * (d.rpos & (DF_RING - 1)));
+  const uint32_t w = SZ3G_DF_PREF ? d.wn : lds32(s_ring + (d.rp4 & (4 * DF_RING - 1)));
   const uint32_t add_hi = __funnelshift_rc(w, 0u, d.avail);          // w >> avail (0 at avail = 32)
   const uint32_t new_lo = __funnelshift_lc(0u, w, 32u - d.avail);    // w << (32 - avail) (0 at avail = 0)
   d.hi |= add_hi;   // 0 unless take: the clamped shift by avail >= 33 gives 0
   d.lo = take ? new_lo : d.lo;
   d.avail += take ? 32u : 0u;
-  d.nref += take ? 1u : 0u;
-  d.rpos += take ? 1u : 0u;
+  d.rp4 += take ? 4u : 0u;
   if (SZ3G_DF_PREF)   // the next word, by the taking lanes only (predicated load, off the decode chain)
     asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.u32 %0, [%1];\n}"
                  : "+r"(d.wn)
-                 : "r"(s_ring + 4u * (d.rpos & (DF_RING - 1))), "r"((uint32_t)take));
+                 : "r"(s_ring + (d.rp4 & (4 * DF_RING - 1))), "r"((uint32_t)take));
 }
 
 // shift the window left by L (<= 16) bits
@@ -1245,14 +1244,16 @@ __global__ void __launch_bounds__(DF_WARPS * 32, DF_WARPS == DF_BIG ? 1 : 4) k_h
   const uint64_t w0 = offs[c], nwc = offs[c + 1] - w0;
   DfLane d;
   const uint64_t a0 = w0 & ~3ull;
-  d.rpos = (uint32_t)(w0 & 3u);
-  d.fpos = 0;
+  const uint8_t* pl = reinterpret_cast<const uint8_t*>(payload + a0);
+  const uint32_t lim4 = (uint32_t)(lim - a0 < (1ull << 28) ? lim - a0 : (1ull << 28)) * 4u;
+  const uint32_t rp4_0 = 4u * (uint32_t)(w0 & 3u);
+  d.rp4 = rp4_0;
+  d.fp4 = 0;
   d.hi = d.lo = 0;
   d.avail = 0;
-  d.nref = 0;
-  df_topup<DF_RING / 4>(d, s_ring, payload, a0, lim);   // 16 words
+  df_topup<DF_RING / 4>(d, s_ring, pl, lim4);   // 16 words
   asm volatile("cp.async.wait_all;\n" ::: "memory");
-  d.wn = lds32(s_ring + 4u * (d.rpos & (DF_RING - 1)));
+  d.wn = lds32(s_ring + (d.rp4 & (4 * DF_RING - 1)));
   df_refill(d, s_ring);                      // prime 64 bits
   df_refill(d, s_ring);
   bool bad = false;
@@ -1293,7 +1294,7 @@ __global__ void __launch_bounds__(DF_WARPS * 32, DF_WARPS == DF_BIG ? 1 : 4) k_h
       uint4* tb = s_tma + wl * 128;   // row r = lane (chunk c0 + r): 64 bytes, 16-byte unit j at j ^ ((r >> 1) & 3)
 #pragma unroll 1
       for (uint32_t q = 0; q < 4; q++) {
-        if (q || e) df_topup<1>(d, s_ring, payload, a0, lim);
+        if (q || e) df_topup<1>(d, s_ring, pl, lim4);
         uint32_t o4[4];
 #pragma unroll
         for (int h = 0; h < 4; h++) o4[h] = pair();
@@ -1315,7 +1316,7 @@ __global__ void __launch_bounds__(DF_WARPS * 32, DF_WARPS == DF_BIG ? 1 : 4) k_h
     uint32_t o[16];
 #pragma unroll
     for (int h = 0; h < 16; h++) {
-      if ((h % 4 == 0) && (h || e)) df_topup<1>(d, s_ring, payload, a0, lim);
+      if ((h % 4 == 0) && (h || e)) df_topup<1>(d, s_ring, pl, lim4);
       o[h] = pair();
     }
     if (SZ3G_DF_DIRECT) {
@@ -1358,7 +1359,7 @@ __global__ void __launch_bounds__(DF_WARPS * 32, DF_WARPS == DF_BIG ? 1 : 4) k_h
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   if (tma_out && lane == 0) sz3g::ptx::bulk_wait0();
-  const uint64_t consumed = 32ull * d.nref - d.avail;
+  const uint64_t consumed = 8ull * (d.rp4 - rp4_0) - d.avail;   // 32 bits per word taken
   if (live && (bad || consumed > nwc * 32)) atomicOr(status, (int)SZ3G_STATUS_BAD_HUFFMAN);
   }
 }
