@@ -425,6 +425,30 @@ __device__ __forceinline__ void store_code_slab(const uint16_t* __restrict__ sla
   const int m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
   const int kval = (int)umin64(TK, g.n2 - (uint64_t)tc.c * TK);
   const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+  if ((g.n2 & 3) == 0 && (reinterpret_cast<uintptr_t>(codes) & 7) == 0) {
+    // rows of a multiple of 4 codes (c2's 500): every row piece starts on 8 bytes and kval is a multiple of
+    // 4, so lane l < 24 owns codes [4 l, 4 l + 4) of each of the slab's 6 P rows: 12 8-byte stores, the row
+    // addresses by additions (the generic loop below spent 24 instructions per element on c2)
+    const int k0 = 4 * lane;
+    if (k0 < kval) {
+      const uint64_t s0 = g.n1 * g.n2;
+      uint16_t* row0 = codes + off + (uint64_t)j0 * g.n2 + k0;
+#pragma unroll
+      for (int i = 0; i < BS; i++) {
+        if (i < m0) {
+          uint16_t* dst = row0;
+#pragma unroll
+          for (int jj = 0; jj < P; jj++) {
+            if (j0 + jj < m1)
+              *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(slab + (i * P + jj) * TK + k0);
+            dst += g.n2;
+          }
+        }
+        row0 += s0;
+      }
+    }
+    return;
+  }
   const bool even = (g.n2 & 1) == 0 && (reinterpret_cast<uintptr_t>(codes) & 3) == 0;
   for (int i = 0; i < m0; i++)
     for (int jj = 0; jj < P && j0 + jj < m1; jj++) {
