@@ -848,6 +848,78 @@ __global__ void __launch_bounds__(128) k_decompress_plain(const uint16_t* __rest
   }
 }
 
+// a8 for f32 fields whose rows are a multiple of 4 values but not of 8 (c2's 500: 1000-byte code rows have
+// no TMA map): a warp stages a tile's codes in shared memory with 8-byte loads (36 independent loads per
+// lane in flight), decodes from / into shared memory and writes x' rows with 16-byte stores.  The plain
+// kernel's 2-byte loads and 4-byte stores at a 3-element lane stride were latency bound (c2: 58 us).
+constexpr int DS_WARPS = 16, DS_PJ = 3;   // x' leaves in two halves of 3 rows per plane: 13.8 KB per warp, 16 warps per SM
+constexpr size_t DS_WARP_BYTES = sizeof(uint16_t) * TILE_ELEMS + sizeof(float) * (TILE_ELEMS / BS * DS_PJ);
+__global__ void __launch_bounds__(DS_WARPS * 32, 1) k_decompress_staged(const uint16_t* __restrict__ codes,
+                                                                        const int32_t* __restrict__ coef,
+                                                                        float* __restrict__ xo, KArgs a) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ Consts s_k;
+  __shared__ int s_ok;
+  if (!cta_consts(a, &s_k, &s_ok)) return;
+  const Consts K = s_k;
+  const Geo& g = a.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint16_t* cs = reinterpret_cast<uint16_t*>(dsm + w * DS_WARP_BYTES);
+  float* os = reinterpret_cast<float*>(dsm + w * DS_WARP_BYTES + sizeof(uint16_t) * TILE_ELEMS);
+  const uint64_t warps = (uint64_t)gridDim.x * DS_WARPS, s0 = g.n1 * g.n2;
+  const int k0 = 4 * lane;   // the lane's 4 codes / 4 values of a row (lanes 0..23)
+  for (uint64_t t = blockIdx.x * (uint64_t)DS_WARPS + w; t < g.ntiles; t += warps) {
+    const TileCoord tc = decode_tile(t, g);
+    const uint64_t off = ((uint64_t)tc.a * BS * g.n1 + (uint64_t)tc.b * BS) * g.n2 + (uint64_t)tc.c * TK;
+    const int m0 = (int)umin64(BS, g.n0 - (uint64_t)tc.a * BS);
+    const int m1 = (int)umin64(BS, g.n1 - (uint64_t)tc.b * BS);
+    const int kval = (int)umin64(TK, g.n2 - (uint64_t)tc.c * TK);   // a multiple of 4
+    if (lane < TK / 4) {
+      const bool kin = k0 < kval;
+      uint2 v[BS * BS];
+      const uint16_t* row0 = codes + off + k0;
+#pragma unroll
+      for (int i = 0; i < BS; i++) {
+#pragma unroll
+        for (int j = 0; j < BS; j++) {
+          const bool in = kin && i < m0 && j < m1;
+          v[i * BS + j] = in ? __ldcs(reinterpret_cast<const uint2*>(row0 + (uint64_t)j * g.n2)) : make_uint2(0u, 0u);
+        }
+        row0 += s0;
+      }
+#pragma unroll
+      for (int r = 0; r < BS * BS; r++) *reinterpret_cast<uint2*>(cs + r * TK + k0) = v[r];
+    }
+    SZ3G_SYNCWARP();
+    const bool full = tile_full(tc, g);
+    const LaneGeom L = full ? lane_geom<true>(tc, g) : lane_geom<false>(tc, g);
+    int4 cc = make_int4(0, 0, 0, 0);
+    if (L.m2 > 0) cc = __ldg(reinterpret_cast<const int4*>(coef) + ((uint64_t)tc.a * g.NB1 + tc.b) * g.NB2 + L.kb);
+    double bh[4];
+    decode_coefs(cc, K, bh);
+#pragma unroll 1
+    for (int j0 = 0; j0 < BS; j0 += DS_PJ) {
+      decompress_rows<float, true, true, true, DS_PJ>(cs, 0, 0, os, 0, 0, j0, L, bh, K, a.R);   // invalid codes are 0 -> 0
+      SZ3G_SYNCWARP();
+      if (lane < TK / 4 && k0 < kval) {
+        float* row0 = xo + off + (uint64_t)j0 * g.n2 + k0;
+#pragma unroll
+        for (int i = 0; i < BS; i++) {
+          if (i < m0) {
+#pragma unroll
+            for (int jj = 0; jj < DS_PJ; jj++)
+              if (j0 + jj < m1)
+                __stcs(reinterpret_cast<float4*>(row0 + (uint64_t)jj * g.n2),
+                       *reinterpret_cast<const float4*>(os + (i * DS_PJ + jj) * TK + k0));
+          }
+          row0 += s0;
+        }
+      }
+      SZ3G_SYNCWARP();
+    }
+  }
+}
+
 // Persistent, one CTA per SM, same producer / private-ring structure as k_compress_tma.  A stage
 // holds a tile's codes (TMA, 6x6x96 u16) and its <= 16 blocks' coefficient codes (1D bulk copy,
 // 16 B per block).  A group of G warps shares a stage; each warp decodes rows [j0, j0 + 6/G) into
@@ -1679,8 +1751,19 @@ int sz3g_regression_decompress(const sz3g_grid* grid, const sz3g_params* params,
       rc = launch_decompress_tma<float, DG32, DN32, DD32, DOB32>(g, codes, coef_codes, x_out, ka, st);
       if (rc) return rc;
     } else {
-      const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
-      k_decompress_plain<float><<<blocks, 128, 0, st>>>(codes, coef_codes, (float*)x_out, ka);
+      if (!generic && (g.n2 & 3) == 0 && (reinterpret_cast<uintptr_t>(codes) & 7) == 0 &&
+          (reinterpret_cast<uintptr_t>(x_out) & 15) == 0) {
+        const size_t smem = DS_WARPS * DS_WARP_BYTES;
+        if (cudaFuncSetAttribute(k_decompress_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+          return SZ3G_ECUDA;
+        const unsigned blocks =
+            (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + DS_WARPS - 1) / DS_WARPS, sm_count()));
+        k_decompress_staged<<<blocks, DS_WARPS * 32, smem, st>>>(codes, coef_codes, (float*)x_out, ka);
+      } else {
+        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((g.ntiles + 3) / 4, sm_count() * 8));
+        k_decompress_plain<float><<<blocks, 128, 0, st>>>(codes, coef_codes, (float*)x_out, ka);
+      }
       launched++;
     }
     if (n_outliers) {
