@@ -7,6 +7,7 @@
 //                              written back by TMA store, smem histogram window
 //   k_compress_plain<T>        same arithmetic, predicated coalesced global loads (any shape)
 //   k_decompress_tma<T,W,S>    a8: TMA-loaded code tiles -> x' tiles -> TMA store
+//   k_decompress_staged        a8, f32 rows of a multiple of 4 values without a TMA map: codes / x' through smem
 //   k_decompress_plain<T>      a8 for any shape
 //   k_outlier_scatter<T>       a8: x[idx] = val
 //   k_histogram                a7 standalone (smem window + global atomics)

@@ -89,6 +89,17 @@ def test_fuzz_parity(t, flags):
     check(f, eb, mode, R, flags)
 
 
+# rows of a multiple of 4 but not of 8 values (c2's 500): no TMA map for the codes, so the quantiser takes the
+# 8-byte plain slab store and the f32 decompressor the shared-memory staged kernel (k_decompress_staged)
+@pytest.mark.parametrize("two_pass", [False, True], ids=["fused", "two-pass"])
+@pytest.mark.parametrize("dims", [(13, 17, 100), (7, 50, 292), (6, 6, 4), (1, 1, 500), (25, 8, 196), (12, 7, 12)])
+@pytest.mark.parametrize("R", [32768, 8])
+def test_rows_multiple_of_4_not_8(dims, R, two_pass):
+    rng = np.random.default_rng(abs(hash((dims, R))) % (1 << 31))
+    f = np.cumsum(rng.normal(size=dims), axis=-1).astype(np.float32)
+    check(f, 1e-3, "rel", R, 0, two_pass=two_pass)
+
+
 # ----------------------------------------------------------------------------- two-pass (analyze -> quantize)
 def assert_same_outputs(a: dict, b: dict):
     """Bit-identical compression outputs (outliers compared as sets keyed by index)."""
