@@ -1385,7 +1385,10 @@ constexpr int AW64 = SZ3G_AW64, AD64 = SZ3G_AD64;   // f64 analyze: 7 self-fed w
 
 // radius at or below which the two-pass quantiser writes its outlier list row piece by row piece
 // (c5 at R = 16, 38.6% outliers: decompress 31.7 -> 17.3 ms, quantise 21.1 -> 19.3 ms)
-constexpr uint32_t ROW_RADIUS = 1024;
+#ifndef SZ3G_ROW_RADIUS
+#define SZ3G_ROW_RADIUS 1024
+#endif
+constexpr uint32_t ROW_RADIUS = SZ3G_ROW_RADIUS;
 
 template <typename T, int NG, int Q, int D, bool HIST, bool BETA, bool SELF = false, int HW = HWIN, bool NOR0 = false,
           bool ROW = false>
