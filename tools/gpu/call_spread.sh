@@ -1,5 +1,6 @@
 #!/bin/bash
-# timing experiment: outlier counter spread over 128 addresses (wrong results) vs the single counter
+# timing experiment: outlier counter spread over 128 addresses (wrong results) vs the single counter;
+# lib/ab/SPREAD.so = the tree with tools/experiments/outlier_counter_spread.patch applied, built with -DSZ3G_EXP_SPREAD=1
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 O=gpurun_out/row; mkdir -p $O
 L=paper_2111_02925_b200/lib
