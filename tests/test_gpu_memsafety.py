@@ -52,7 +52,10 @@ def shapes():
     return {"c1": make_field("c1", device="cuda"),
             "c2crop": make_field("c2", device="cuda", shape=(30, 100, 200)),
             "c4crop": make_field("c4", device="cuda", shape=(20, 50, 96)),
-            "odd": torch.from_numpy(rng.normal(size=(7, 13, 97)).astype(np.float32)).cuda()}
+            "odd": torch.from_numpy(rng.normal(size=(7, 13, 97)).astype(np.float32)).cuda(),
+            # rows of a multiple of 4 but not of 8 values: no TMA map for the codes -> the 8-byte plain slab
+            # store and k_decompress_staged
+            "rows4": torch.from_numpy(np.cumsum(rng.normal(size=(14, 20, 100)), axis=-1).astype(np.float32)).cuda()}
 
 
 def run_regression(x, R, flags, fill, guard_input):
