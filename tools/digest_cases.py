@@ -52,6 +52,8 @@ def fields():
         "c4": make_field("c4", device="cuda", shape=(20, 50, 96)),              # f64
         "odd": torch.from_numpy(rng.normal(size=(7, 13, 97)).astype(np.float32)).cuda(),   # no 16-B pitch
         "big": make_field("c5", device="cuda", shape=(96, 512, 1024)),          # many tiles per CTA
+        # rows of a multiple of 4 but not of 8 values: plain 8-byte slab store + k_decompress_staged
+        "rows4": torch.from_numpy(np.cumsum(rng.normal(size=(14, 20, 100)), axis=-1).astype(np.float32)).cuda(),
     }
 
 
