@@ -1,4 +1,5 @@
 #!/bin/bash
+# (needs tools/experiments/huffman_fused_encoder.patch applied: the fused encoder is not in the tree, DESIGN 10)
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 O=gpurun_out/ef; mkdir -p $O
 cat > /tmp/ef_time.py <<'PY'
